@@ -1,0 +1,209 @@
+/*
+ * greengate_b200.h — C ABI of the B200-native gated-inference hot path.
+ *
+ * This is the drop-in boundary.  The reference `greengate`
+ * package is pure Python; its de-facto operator interface for this path is the
+ * `AdmissionController` object (pkg/src/greengate/controller.py:256-362).  The
+ * Python shim in `paper_2601_04250_b200/controller.py` keeps that object's
+ * names, arguments and exceptions and calls the entry points below through
+ * ctypes (INTEGRATION.md shows the binding).  Each entry point names the
+ * reference interface it replaces.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch types;
+ *   - every `*_dev` pointer is CUDA device memory owned by the caller
+ *     (the library never allocates or frees device memory);
+ *   - every compute call is stream-ordered on `stream` (a cudaStream_t passed
+ *     as void*) and returns immediately; device-side per-row errors are
+ *     reported in caller-provided device buffers;
+ *   - the return value is a gg_status for launch/argument errors only.
+ *
+ * Numerics: all controller arithmetic is IEEE fp64, evaluated in the
+ * reference's operation order with no FMA contraction, CPython-3.12
+ * Neumaier summation for `sum()`, and ln(K) computed on the host with libm.
+ */
+#ifndef GREENGATE_B200_H
+#define GREENGATE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GG_ABI_VERSION 1
+/* Largest supported p95 latency window (reference default 100,
+ * controller.py:274 / servesim.py:80). */
+#define GG_P95_WINDOW_MAX 1024
+
+typedef enum {
+  GG_OK = 0,
+  GG_ERR_INVALID_ARGUMENT = 1,     /* ValueError / ConfigError */
+  GG_ERR_INVALID_DISTRIBUTION = 2, /* errors.py:8  InvalidDistribution */
+  GG_ERR_NEGATIVE_MEASUREMENT = 3, /* errors.py:20 NegativeMeasurement */
+  GG_ERR_INVALID_SCHEDULE = 4,     /* errors.py:12 InvalidSchedule */
+  GG_ERR_INVALID_LAMBDA = 5,       /* errors.py:16 InvalidLambda */
+  GG_ERR_CUDA = 6,                 /* launch failure */
+  GG_ERR_UNSUPPORTED = 7
+} gg_status;
+
+/* Direction (controller.py:38-47) */
+enum { GG_DIR_GEQ = 0, GG_DIR_LT = 1 };
+/* UtilityProxy (controller.py:50-52) */
+enum { GG_UTIL_ENTROPY = 0, GG_UTIL_ONE_MINUS_CONFIDENCE = 1 };
+/* RoutePolicy (controller.py:55-58) */
+enum { GG_ROUTE_ALL_DIRECT = 0, GG_ROUTE_ALL_BATCHED = 1, GG_ROUTE_THRESHOLD_ON_QUEUE = 2 };
+/* Per-row decision codes written by gg_admit (AdmissionDecision.admit/path,
+ * controller.py:206-211; ServicePath controller.py:61-64). */
+enum {
+  GG_DECISION_SKIP = 0,        /* admit=False, path=NONE */
+  GG_DECISION_DIRECT = 1,      /* admit=True,  path=DIRECT */
+  GG_DECISION_BATCHED = 2,     /* admit=True,  path=BATCHED */
+  GG_DECISION_INVALID = 255    /* InvalidDistribution: no state change */
+};
+
+/* Immutable controller parameters: CostWeights (controller.py:73-88),
+ * ThresholdSchedule minus t_origin (controller.py:91-111), the rest of
+ * ControllerConfig (controller.py:219-233), EnergyLedger.ewma_lambda
+ * (energy.py:60) and the p95 window length (controller.py:274). */
+typedef struct {
+  double alpha, beta, gamma;
+  double tau0, tau_inf, k;
+  double ewma_lambda;
+  int32_t direction;
+  int32_t utility_proxy;
+  int32_t routing;
+  int32_t queue_threshold;
+  int32_t p95_window;
+  int32_t reserved;
+} gg_params;
+
+/* One NormalizerChannel (controller.py:157-183).  `seen` = 0 stands for the
+ * reference's running_min/running_max being None. */
+typedef struct {
+  double lo, hi;
+  int32_t seen;
+  int32_t reserved;
+} gg_channel;
+
+/* Mutable loop state, resident in device memory (one per controller).
+ * Mirrors AdmissionController fields (controller.py:276-287) plus the
+ * EnergyLedger EWMA (energy.py:55-87).  The latency window is kept twice: in
+ * arrival order (the deque, controller.py:285) and sorted, so the nearest-rank
+ * p95 (telemetry.py:35-46) is an O(1) read. */
+typedef struct {
+  gg_channel n_energy;       /* NormalizerState.energy      */
+  gg_channel n_queue_depth;  /* NormalizerState.queue_depth */
+  gg_channel n_p95_ms;       /* NormalizerState.p95_ms      */
+  double ewma_joules_per_request;
+  double total_joules;
+  double t_origin;           /* ThresholdSchedule.t_origin; reset_clock mutates it */
+  double p95_current;        /* p95 of the window, 0.0 when empty (controller.py:289-293) */
+  int64_t samples_seen;
+  int64_t admitted_total;
+  int64_t skipped_total;
+  int64_t outcomes_total;
+  int32_t queue_depth;       /* last reported depth (gateway.py:50, 191, 230) */
+  int32_t win_count;         /* len(deque) */
+  int32_t win_head;          /* index of the oldest element in win[] */
+  int32_t reserved;
+  double win[GG_P95_WINDOW_MAX];        /* circular, arrival order */
+  double win_sorted[GG_P95_WINDOW_MAX]; /* first win_count entries ascending */
+} gg_state;
+
+/* CongestionSnapshot (servesim.py:113-119). */
+typedef struct {
+  int64_t queue_depth;
+  double p95_latency_ms;
+  double batch_fill;
+} gg_snapshot;
+
+/* Per-launch summary written by gg_admit (device memory). */
+typedef struct {
+  int64_t n_admitted;
+  int64_t n_skipped;
+  int64_t n_invalid;
+  int64_t first_invalid;     /* -1 when every row is valid */
+  double energy;             /* E(x), identical for every valid row of the batch */
+  double congestion;         /* C(x), identical for every valid row of the batch */
+} gg_batch_info;
+
+/* ---- library identity ---------------------------------------------------- */
+const char* gg_version(void);
+int gg_abi_version(void);
+size_t gg_state_bytes(void);
+/* Replaces EnergyLedger(ewma_lambda) + ControllerConfig.build(...) state setup
+ * (controller.py:235-287; energy.py:55-73): validates params, zeroes state,
+ * sets t_origin.  Returns GG_ERR_INVALID_SCHEDULE / GG_ERR_INVALID_LAMBDA like
+ * ThresholdSchedule.__post_init__ (controller.py:100-105) and
+ * EnergyLedger.__post_init__ (energy.py:64-69). */
+int gg_validate_params(const gg_params* params);
+int gg_state_init(gg_state* state_dev, double t_origin, void* stream);
+
+/* ---- K1: fused admission + order-preserving compaction -------------------- */
+/* Replaces AdmissionController.decide (controller.py:309-343) applied to the
+ * rows of `probs_dev` in order against ONE congestion snapshot (the frozen
+ * snapshot of a micro-batch; with n == 1 it is exactly one decide() call).
+ *   probs_dev      [n, row_stride] fp64, first k columns are the scores
+ *   now_dev        [n] fp64 decision time per row (controller.py:327)
+ *   snapshot_dev   NULL -> the default snapshot (queue_depth from state,
+ *                  state p95, batch_fill 0; controller.py:295-300)
+ *   decision_dev   [n] u8 GG_DECISION_* codes
+ *   breakdown_dev  NULL or [n, 3] fp64 (utility, composite, threshold)
+ *   admitted_idx_dev NULL or [n] int32: ascending indices of admitted rows
+ *   info_dev       gg_batch_info (device)
+ *   workspace_dev  >= gg_admit_workspace_bytes(n) bytes, any content
+ * Effects on state (stream-ordered): admitted_total/skipped_total += counts;
+ * the queue/p95 (and energy) normalizer channels observe the snapshot if at
+ * least one row was valid — exactly what sequential decide() calls do. */
+size_t gg_admit_workspace_bytes(int64_t n);
+int gg_admit(const gg_params* params, gg_state* state_dev,
+             const double* probs_dev, int64_t n, int32_t k, int64_t row_stride,
+             const double* now_dev, const gg_snapshot* snapshot_dev,
+             uint8_t* decision_dev, double* breakdown_dev,
+             int32_t* admitted_idx_dev, gg_batch_info* info_dev,
+             void* workspace_dev, size_t workspace_bytes, void* stream);
+
+/* ---- K2: outcome feedback -------------------------------------------------- */
+/* Replaces AdmissionController.record_outcome (controller.py:345-358) for n
+ * served requests in completion order: EWMA (energy.py:24-36, 75-87), latency
+ * window + nearest-rank p95 (controller.py:285, 289-293), channel observes.
+ * A negative value stops the sequence at that index (earlier outcomes stay
+ * applied, like a Python loop that raises) and writes the index to
+ * error_index_dev (else -1).  queue_depth of the last applied outcome becomes
+ * state.queue_depth when `set_queue_depth` != 0 (gateway.py:230). */
+int gg_outcome(const gg_params* params, gg_state* state_dev,
+               const double* latency_ms_dev, const double* joules_dev,
+               const int32_t* queue_depth_dev, int64_t n, int32_t set_queue_depth,
+               int64_t* error_index_dev, void* stream);
+
+/* Replaces AdmissionController.reset_clock (controller.py:360-362). */
+int gg_reset_clock(gg_state* state_dev, double t_origin, void* stream);
+/* Sets the externally reported queue depth (gateway.py:191-192). */
+int gg_set_queue_depth(gg_state* state_dev, int32_t queue_depth, void* stream);
+
+/* ---- K3: logit -> probability epilogue ------------------------------------ */
+/* fp32 logits [n, k] (row stride ld) -> fp64 softmax probabilities that pass
+ * _validate_distribution (controller.py:126-135), first-max argmax
+ * (RequestFeatures.top_class, workload.py:42-43), confidence (max p) and the
+ * controller's utility of the row (entropy_utility controller.py:138-142 or
+ * one_minus_confidence_utility 145-148).  Any output pointer may be NULL. */
+int gg_epilogue(const float* logits_dev, int64_t n, int32_t k, int64_t ld,
+                int32_t utility_proxy, double* probs_dev, int32_t* argmax_dev,
+                double* confidence_dev, double* utility_dev, void* stream);
+
+/* ---- serving-loop helpers (device FIFO of admitted requests) -------------- */
+/* Appends the admitted ids of the last gg_admit (admitted_idx + base id) to a
+ * device ring buffer; the forward pass pops fixed-size batches from it. */
+typedef struct {
+  int64_t head;      /* total popped */
+  int64_t tail;      /* total pushed */
+  int64_t capacity;  /* ring size (power of two) */
+  int64_t reserved;
+} gg_fifo;
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GREENGATE_B200_H */
