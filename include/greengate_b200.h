@@ -153,7 +153,8 @@ int gg_state_init(gg_state* state_dev, double t_origin, void* stream);
  *   breakdown_dev  NULL or [n, 3] fp64 (utility, composite, threshold)
  *   admitted_idx_dev NULL or [n] int32: ascending indices of admitted rows
  *   info_dev       gg_batch_info (device)
- *   workspace_dev  >= gg_admit_workspace_bytes(n) bytes, any content
+ *   workspace_dev  >= gg_admit_workspace_bytes(n) bytes, zero-filled before
+ *                  first use; every launch leaves it zero-filled again
  * Effects on state (stream-ordered): admitted_total/skipped_total += counts;
  * the queue/p95 (and energy) normalizer channels observe the snapshot if at
  * least one row was valid — exactly what sequential decide() calls do. */
@@ -193,15 +194,18 @@ int gg_epilogue(const float* logits_dev, int64_t n, int32_t k, int64_t ld,
                 int32_t utility_proxy, double* probs_dev, int32_t* argmax_dev,
                 double* confidence_dev, double* utility_dev, void* stream);
 
-/* ---- serving-loop helpers (device FIFO of admitted requests) -------------- */
-/* Appends the admitted ids of the last gg_admit (admitted_idx + base id) to a
- * device ring buffer; the forward pass pops fixed-size batches from it. */
-typedef struct {
-  int64_t head;      /* total popped */
-  int64_t tail;      /* total pushed */
-  int64_t capacity;  /* ring size (power of two) */
-  int64_t reserved;
-} gg_fifo;
+/* ---- stateless batch forms of the controller's pure functions ------------- */
+/* entropy_utility / one_minus_confidence_utility (controller.py:138-148) over
+ * n rows: utility_dev[i] (NaN when invalid), valid_dev[i] = 0 when the row
+ * would raise InvalidDistribution (controller.py:126-135). */
+int gg_utility(const double* probs_dev, int64_t n, int32_t k, int64_t row_stride,
+               int32_t utility_proxy, double* utility_dev, uint8_t* valid_dev, void* stream);
+/* threshold_at (controller.py:114-123) for n times against one schedule. */
+int gg_threshold(double tau0, double tau_inf, double k, double t_origin,
+                 const double* t_dev, double* tau_dev, int64_t n, void* stream);
+/* cost (controller.py:214-216) for n (u, e, c) triples, [n, 3] row-major. */
+int gg_cost(double alpha, double beta, double gamma, const double* uec_dev,
+            double* j_dev, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,60 @@
+// gg_common.cuh — shared helpers for the greengate B200 kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/greengate_b200.h"
+
+#define GG_CUDA_OK(expr)                                   \
+  do {                                                     \
+    cudaError_t _e = (expr);                               \
+    if (_e != cudaSuccess) return GG_ERR_CUDA;             \
+  } while (0)
+
+#define GG_LAUNCH_OK()                                     \
+  do {                                                     \
+    cudaError_t _e = cudaGetLastError();                   \
+    if (_e != cudaSuccess) return GG_ERR_CUDA;             \
+  } while (0)
+
+static inline cudaStream_t gg_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Every fp64 operation of the controller goes through these so the rounding is
+// exactly CPython's (one IEEE rounding per binary op, no FMA contraction).
+__device__ __forceinline__ double f64_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double f64_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double f64_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double f64_div(double a, double b) { return __ddiv_rn(a, b); }
+
+// CPython 3.12 builtin sum() over floats: Neumaier compensation
+// (Objects/bltinmodule.c builtin_sum_impl; used by controller.py:132, 141).
+struct NeumaierSum {
+  double s = 0.0, c = 0.0;
+  __device__ __forceinline__ void add(double x) {
+    double t = f64_add(s, x);
+    if (fabs(s) >= fabs(x)) c = f64_add(c, f64_add(f64_sub(s, t), x));
+    else c = f64_add(c, f64_add(f64_sub(x, t), s));
+    s = t;
+  }
+  __device__ __forceinline__ double result() const {
+    return (c != 0.0 && isfinite(c)) ? f64_add(s, c) : s;
+  }
+};
+
+// min(1.0, max(0.0, v)) with Python's first-argument-wins ties.
+__device__ __forceinline__ double clamp01(double v) {
+  v = (v > 0.0) ? v : 0.0;
+  return (v < 1.0) ? v : 1.0;
+}
+
+// NormalizerChannel.observe / normalize (controller.py:164-180).
+__device__ __forceinline__ void ch_observe(gg_channel& c, double raw) {
+  if (!c.seen || raw < c.lo) c.lo = raw;
+  if (!c.seen || raw > c.hi) c.hi = raw;
+  c.seen = 1;
+}
+__device__ __forceinline__ double ch_normalize(gg_channel& c, double raw) {
+  ch_observe(c, raw);
+  if (c.hi <= c.lo) return 0.0;
+  return clamp01(f64_div(f64_sub(raw, c.lo), f64_sub(c.hi, c.lo)));
+}

@@ -1,0 +1,780 @@
+// gg_controller.cu — admission (K1), outcome feedback (K2) and logit epilogue
+// (K3) kernels of the gated-inference hot path, plus their C-ABI entry points
+// (include/greengate_b200.h).
+//
+// Compiled with -fmad=false; every controller operation additionally goes
+// through the __d*_rn intrinsics in gg_common.cuh, so each fp64 binary op
+// rounds exactly like CPython's float op in the reference
+// (pkg/src/greengate/controller.py, energy.py, telemetry.py).
+#include <math.h>
+#include <stdio.h>
+
+#include "gg_common.cuh"
+
+namespace gg {
+
+// ---------------------------------------------------------------------------
+// Workspace layout (zero-filled once; every gg_admit launch leaves it zeroed).
+struct AdmitWorkspace {
+  unsigned long long vblock_counter;  // virtual block ids (forward-progress-safe lookback)
+  unsigned long long done_counter;    // completion ticket; the last block finalizes
+  unsigned long long n_skipped;
+  unsigned long long n_invalid;
+  unsigned long long first_invalid_enc;  // max over (n - row); 0 == none
+  unsigned long long reserved[3];
+  unsigned long long status[1];       // [num_blocks] decoupled look-back words
+};
+constexpr size_t kWsHeader = offsetof(AdmitWorkspace, status);
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPrefix = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Single-thread decoupled look-back (Merrill & Garland): returns the exclusive
+// prefix of admitted rows before virtual block `vb`.
+__device__ unsigned long long lookback(unsigned long long* status, int vb, unsigned long long agg) {
+  if (vb == 0) {
+    st_relaxed(&status[0], kFlagPrefix | agg);
+    return 0ull;
+  }
+  st_relaxed(&status[vb], kFlagAgg | agg);
+  unsigned long long prefix = 0;
+  int p = vb - 1;
+  while (true) {
+    unsigned long long w;
+    do {
+      w = ld_relaxed(&status[p]);
+    } while ((w >> 62) == 0ull);
+    prefix += w & kValMask;
+    if ((w >> 62) == 2ull) break;
+    --p;
+  }
+  st_relaxed(&status[vb], kFlagPrefix | (prefix + agg));
+  return prefix;
+}
+
+struct AdmitArgs {
+  gg_params p;
+  gg_state* state;
+  const double* probs;
+  int64_t n;
+  int32_t k;
+  int64_t stride;
+  const double* now;
+  const gg_snapshot* snap;
+  uint8_t* decision;
+  double* breakdown;
+  int32_t* admitted_idx;
+  gg_batch_info* info;
+  AdmitWorkspace* ws;
+  double ln_k;  // math.log(len(xs)) computed on the host with libm (controller.py:142)
+};
+
+// Batch-constant part of decide() (controller.py:316-325).  Within one frozen
+// snapshot every valid request sees the same E and C: the first valid
+// request's normalize() observes the raw values, later ones re-observe the
+// same values (idempotent), so evaluating normalize on a copy of the channels
+// yields exactly the per-request values.
+struct BatchConst {
+  double e, c, p95, fill, t_origin, ewma;
+  int64_t qd;
+  int64_t samples_seen;
+};
+
+__device__ BatchConst batch_constants(const gg_state* st, const gg_snapshot* snap) {
+  BatchConst b;
+  b.samples_seen = st->samples_seen;
+  b.ewma = st->ewma_joules_per_request;
+  b.t_origin = st->t_origin;
+  if (snap) {
+    b.qd = snap->queue_depth;
+    b.p95 = snap->p95_latency_ms;
+    b.fill = snap->batch_fill;
+  } else {  // default congestion source (controller.py:295-300; gateway.py:58-64)
+    b.qd = st->queue_depth;
+    b.p95 = st->p95_current;
+    b.fill = 0.0;
+  }
+  gg_channel ce = st->n_energy, cq = st->n_queue_depth, cp = st->n_p95_ms;
+  b.e = (b.samples_seen > 0) ? ch_normalize(ce, b.ewma) : 0.0;
+  double qn = ch_normalize(cq, (double)b.qd);
+  double pn = ch_normalize(cp, b.p95);
+  b.c = f64_div(f64_add(f64_add(qn, pn), b.fill), 3.0);
+  return b;
+}
+
+// _validate_distribution + utility proxy, one streaming pass over the row in
+// index order (controller.py:126-148).
+struct RowAcc {
+  bool ok = true;
+  bool first = true;
+  NeumaierSum tot, h;
+  double mx = 0.0;
+  __device__ __forceinline__ void add(double x, bool entropy) {
+    if (!isfinite(x) || x < 0.0) ok = false;
+    tot.add(x);
+    if (entropy) {
+      if (x > 0.0) h.add(f64_mul(x, log(x)));
+    } else {
+      if (first || x > mx) mx = x;
+      first = false;
+    }
+  }
+  __device__ __forceinline__ bool finish(int k, bool entropy, double ln_k, double& u) const {
+    if (!ok || k < 2) return false;
+    if (fabs(f64_sub(tot.result(), 1.0)) > 1e-9) return false;
+    if (entropy) u = clamp01(f64_div(-h.result(), ln_k));
+    else u = f64_sub(1.0, mx);
+    return true;
+  }
+};
+
+// The per-request tail of decide(): J, tau(now), admit, route
+// (controller.py:326-337).
+__device__ __forceinline__ uint8_t decide_row(const AdmitArgs& a, const BatchConst& b, double u,
+                                              double now, double& j, double& tau) {
+  const gg_params& p = a.p;
+  j = f64_add(f64_add(f64_mul(p.alpha, u), f64_mul(p.beta, b.e)), f64_mul(p.gamma, b.c));
+  double el = f64_sub(now, b.t_origin);
+  el = (el > 0.0) ? el : 0.0;
+  tau = f64_add(p.tau_inf, f64_mul(f64_sub(p.tau0, p.tau_inf), exp(f64_mul(-p.k, el))));
+  bool admit = (p.direction == GG_DIR_GEQ) ? (j >= tau) : (j < tau);
+  if (!admit) return GG_DECISION_SKIP;
+  if (p.routing == GG_ROUTE_ALL_BATCHED) return GG_DECISION_BATCHED;
+  if (p.routing == GG_ROUTE_THRESHOLD_ON_QUEUE)
+    return (b.qd > (int64_t)p.queue_threshold) ? GG_DECISION_BATCHED : GG_DECISION_DIRECT;
+  return GG_DECISION_DIRECT;
+}
+
+template <int THREADS, int RPT>
+struct AdmitShared {
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr int GROUPS = RPT * WARPS;
+  static_assert(GROUPS <= 32, "one warp scans the groups");
+  BatchConst bc;
+  unsigned long long block_prefix;
+  int group_cnt[GROUPS];
+  int group_off[GROUPS];
+  int vb;
+  int last;
+};
+
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long t = __shfl_xor_sync(0xffffffffu, v, o);
+    v = t > v ? t : v;
+  }
+  return v;
+}
+
+// Order-preserving compaction of the tile + counters + last-block finalize.
+template <int THREADS, int RPT>
+__device__ void finish_tile(const AdmitArgs& a, AdmitShared<THREADS, RPT>& sm, int64_t tile0,
+                            const uint32_t (&ballots)[RPT], int my_skip, int my_inv,
+                            unsigned long long my_bad_enc) {
+  constexpr int WARPS = THREADS / 32;
+  constexpr int GROUPS = RPT * WARPS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (lane == 0) {
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) sm.group_cnt[j * WARPS + warp] = __popc(ballots[j]);
+  }
+  // counters: warp-reduce then one atomic per warp
+  int ws = warp_sum(my_skip), wi = warp_sum(my_inv);
+  unsigned long long wb = warp_max_u64(my_bad_enc);
+  if (lane == 0) {
+    if (ws) atomicAdd(&a.ws->n_skipped, (unsigned long long)ws);
+    if (wi) atomicAdd(&a.ws->n_invalid, (unsigned long long)wi);
+    if (wb) atomicMax(&a.ws->first_invalid_enc, wb);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int c = lane < GROUPS ? sm.group_cnt[lane] : 0;
+    int v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
+    }
+    int total = __shfl_sync(0xffffffffu, v, 31);
+    if (lane < GROUPS) sm.group_off[lane] = v - c;
+    if (lane == 0) sm.block_prefix = lookback(a.ws->status, sm.vb, (unsigned long long)total);
+  }
+  __syncthreads();
+  if (a.admitted_idx) {
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      if ((ballots[j] >> lane) & 1u) {
+        unsigned long long pos = sm.block_prefix + sm.group_off[j * WARPS + warp] +
+                                 __popc(ballots[j] & ((1u << lane) - 1u));
+        a.admitted_idx[pos] = (int32_t)(tile0 + (int64_t)j * THREADS + tid);
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long t = atomicAdd(&a.ws->done_counter, 1ull);
+    sm.last = (t == (unsigned long long)gridDim.x - 1ull);
+  }
+  __syncthreads();
+  if (!sm.last) return;
+  // ---- last block: every other block has finished reading state and writing
+  // its counters; apply the batch's state effects once (controller.py:316-337).
+  __threadfence();
+  if (tid == 0) {
+    const int nb = gridDim.x;
+    unsigned long long w = ld_relaxed(&a.ws->status[nb - 1]);
+    int64_t n_adm = (int64_t)(w & kValMask);
+    int64_t n_skip = (int64_t)ld_relaxed(&a.ws->n_skipped);
+    int64_t n_inv = (int64_t)ld_relaxed(&a.ws->n_invalid);
+    unsigned long long benc = ld_relaxed(&a.ws->first_invalid_enc);
+    gg_state* st = a.state;
+    const BatchConst& b = sm.bc;
+    const bool any_valid = (a.n - n_inv) > 0;
+    if (any_valid) {
+      if (b.samples_seen > 0) ch_observe(st->n_energy, b.ewma);
+      ch_observe(st->n_queue_depth, (double)b.qd);
+      ch_observe(st->n_p95_ms, b.p95);
+    }
+    st->admitted_total += n_adm;
+    st->skipped_total += n_skip;
+    if (a.info) {
+      a.info->n_admitted = n_adm;
+      a.info->n_skipped = n_skip;
+      a.info->n_invalid = n_inv;
+      a.info->first_invalid = benc ? (int64_t)(a.n - (int64_t)benc) : -1;
+      a.info->energy = any_valid ? b.e : 0.0;
+      a.info->congestion = any_valid ? b.c : 0.0;
+    }
+    a.ws->vblock_counter = 0;
+    a.ws->done_counter = 0;
+    a.ws->n_skipped = 0;
+    a.ws->n_invalid = 0;
+    a.ws->first_invalid_enc = 0;
+  }
+  __syncthreads();
+  for (int i = tid; i < (int)gridDim.x; i += THREADS) a.ws->status[i] = 0ull;
+}
+
+// K1, small K (K <= 16): RPT rows per thread, rows of a warp contiguous, so a
+// warp's loads of a [32 x K] fp64 slab are fully coalesced.
+template <int KC, int THREADS, int RPT>
+__global__ void __launch_bounds__(THREADS) admit_small_kernel(AdmitArgs a) {
+  __shared__ AdmitShared<THREADS, RPT> sm;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    sm.vb = (int)atomicAdd(&a.ws->vblock_counter, 1ull);
+    sm.bc = batch_constants(a.state, a.snap);
+  }
+  __syncthreads();
+  const BatchConst b = sm.bc;
+  const int64_t tile0 = (int64_t)sm.vb * THREADS * RPT;
+  const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
+  const int k = KC > 0 ? KC : a.k;
+  uint32_t ballots[RPT];
+  int my_skip = 0, my_inv = 0;
+  unsigned long long my_bad = 0;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const int64_t r = tile0 + (int64_t)j * THREADS + tid;
+    const bool in = r < a.n;
+    uint8_t code = GG_DECISION_SKIP;
+    if (in) {
+      const double* row = a.probs + r * a.stride;
+      RowAcc acc;
+      if constexpr (KC == 2) {
+        double2 v = *reinterpret_cast<const double2*>(row);
+        acc.add(v.x, entropy);
+        acc.add(v.y, entropy);
+      } else if constexpr (KC == 4) {
+        double2 v0 = *reinterpret_cast<const double2*>(row);
+        double2 v1 = *reinterpret_cast<const double2*>(row + 2);
+        acc.add(v0.x, entropy);
+        acc.add(v0.y, entropy);
+        acc.add(v1.x, entropy);
+        acc.add(v1.y, entropy);
+      } else {
+        for (int c = 0; c < k; ++c) acc.add(row[c], entropy);
+      }
+      double u, jv = 0.0, tau = 0.0;
+      if (acc.finish(k, entropy, a.ln_k, u)) {
+        code = decide_row(a, b, u, a.now[r], jv, tau);
+        if (code == GG_DECISION_SKIP) ++my_skip;
+      } else {
+        code = GG_DECISION_INVALID;
+        ++my_inv;
+        if (!my_bad) my_bad = (unsigned long long)(a.n - r);
+        u = jv = tau = __longlong_as_double(0x7ff8000000000000ll);
+      }
+      a.decision[r] = code;
+      if (a.breakdown) {
+        a.breakdown[3 * r] = u;
+        a.breakdown[3 * r + 1] = jv;
+        a.breakdown[3 * r + 2] = tau;
+      }
+    }
+    ballots[j] = __ballot_sync(0xffffffffu, in && (code == GG_DECISION_DIRECT || code == GG_DECISION_BATCHED));
+  }
+  finish_tile<THREADS, RPT>(a, sm, tile0, ballots, my_skip, my_inv, my_bad);
+}
+
+// K1, large K (ResNet K=1000): one row per thread, the block's [128 x 32]
+// column chunks staged through shared memory with coalesced loads; the row
+// scan stays sequential (CPython sum order) per thread.  Row stride 33
+// doubles keeps the per-thread column reads bank-conflict free.
+constexpr int kLargeThreads = 128;
+constexpr int kChunk = 32;
+
+__global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a) {
+  __shared__ AdmitShared<kLargeThreads, 1> sm;
+  __shared__ double tile[kLargeThreads][kChunk + 1];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    sm.vb = (int)atomicAdd(&a.ws->vblock_counter, 1ull);
+    sm.bc = batch_constants(a.state, a.snap);
+  }
+  __syncthreads();
+  const BatchConst b = sm.bc;
+  const int64_t tile0 = (int64_t)sm.vb * kLargeThreads;
+  const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
+  const int64_t r = tile0 + tid;
+  const bool in = r < a.n;
+  RowAcc acc;
+  for (int c0 = 0; c0 < a.k; c0 += kChunk) {
+    const int cw = min(kChunk, a.k - c0);
+#pragma unroll 4
+    for (int e = tid; e < kLargeThreads * kChunk; e += kLargeThreads) {
+      const int rr = e / kChunk, cc = e % kChunk;
+      const int64_t gr = tile0 + rr;
+      double v = 0.0;
+      if (gr < a.n && cc < cw) v = __ldg(a.probs + gr * a.stride + c0 + cc);
+      tile[rr][cc] = v;
+    }
+    __syncthreads();
+    if (in)
+      for (int cc = 0; cc < cw; ++cc) acc.add(tile[tid][cc], entropy);
+    __syncthreads();
+  }
+  uint8_t code = GG_DECISION_SKIP;
+  int my_skip = 0, my_inv = 0;
+  unsigned long long my_bad = 0;
+  if (in) {
+    double u, jv = 0.0, tau = 0.0;
+    if (acc.finish(a.k, entropy, a.ln_k, u)) {
+      code = decide_row(a, b, u, a.now[r], jv, tau);
+      if (code == GG_DECISION_SKIP) ++my_skip;
+    } else {
+      code = GG_DECISION_INVALID;
+      ++my_inv;
+      if (!my_bad) my_bad = (unsigned long long)(a.n - r);
+      u = jv = tau = __longlong_as_double(0x7ff8000000000000ll);
+    }
+    a.decision[r] = code;
+    if (a.breakdown) {
+      a.breakdown[3 * r] = u;
+      a.breakdown[3 * r + 1] = jv;
+      a.breakdown[3 * r + 2] = tau;
+    }
+  }
+  uint32_t ballots[1] = {__ballot_sync(0xffffffffu, in && (code == GG_DECISION_DIRECT || code == GG_DECISION_BATCHED))};
+  finish_tile<kLargeThreads, 1>(a, sm, tile0, ballots, my_skip, my_inv, my_bad);
+}
+
+// ---------------------------------------------------------------------------
+// K2: record_outcome() x n, sequential in completion order (controller.py:345-358).
+// One warp: scalars are evaluated redundantly by every lane (identical values);
+// the sorted latency window is updated with warp-parallel shifts so the
+// nearest-rank p95 (telemetry.py:35-46) is one shared-memory read.
+
+__device__ __forceinline__ int warp_min_int(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Remove one element equal to `x` from srt[0..cnt).
+__device__ void sorted_remove(double* srt, int cnt, double x) {
+  const int lane = threadIdx.x & 31;
+  int pos = cnt;
+  for (int base = 0; base < cnt; base += 32) {
+    int i = base + lane;
+    unsigned m = __ballot_sync(0xffffffffu, i < cnt && srt[i] == x);
+    if (m) {
+      pos = base + __ffs(m) - 1;
+      break;
+    }
+  }
+  if (pos >= cnt) return;  // not found (NaN); window content is then undefined like sorted()
+  for (int base = pos; base < cnt - 1; base += 32) {  // ascending left shift
+    int i = base + lane;
+    double v = (i + 1 < cnt) ? srt[i + 1] : 0.0;
+    __syncwarp();
+    if (i + 1 < cnt) srt[i] = v;
+    __syncwarp();
+  }
+}
+
+// Insert `x` into srt[0..cnt) keeping it ascending (after all elements < x).
+__device__ void sorted_insert(double* srt, int cnt, double x) {
+  const int lane = threadIdx.x & 31;
+  int less = 0;
+  for (int i = lane; i < cnt; i += 32) less += (srt[i] < x) ? 1 : 0;
+  const int pos = warp_sum(less);
+  for (int top = cnt; top > pos; top -= 32) {  // descending right shift of [pos, cnt)
+    int i = top - 1 - lane;
+    double v = (i >= pos) ? srt[i] : 0.0;
+    __syncwarp();
+    if (i >= pos) srt[i + 1] = v;
+    __syncwarp();
+  }
+  if (lane == 0) srt[pos] = x;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, const double* lat,
+                                                     const double* jou, const int32_t* qd, int64_t n,
+                                                     int set_qd, int64_t* err) {
+  __shared__ double win[GG_P95_WINDOW_MAX];
+  __shared__ double srt[GG_P95_WINDOW_MAX];
+  const int lane = threadIdx.x;
+  const int cap = p.p95_window;
+  int count = st->win_count, head = st->win_head;
+  for (int i = lane; i < cap; i += 32) win[i] = st->win[i];
+  for (int i = lane; i < count; i += 32) srt[i] = st->win_sorted[i];
+  double ewma = st->ewma_joules_per_request, total = st->total_joules, p95 = st->p95_current;
+  int64_t seen = st->samples_seen, outc = st->outcomes_total;
+  gg_channel ce = st->n_energy, cq = st->n_queue_depth, cp = st->n_p95_ms;
+  int last_qd = st->queue_depth;
+  const double lam = p.ewma_lambda, one_minus_lam = f64_sub(1.0, p.ewma_lambda);
+  int64_t bad = -1;
+  __syncwarp();
+  for (int64_t i = 0; i < n; ++i) {
+    const double L = lat[i], J = jou[i];
+    const int32_t Q = qd[i];
+    if (L < 0.0 || J < 0.0 || Q < 0) {  // NegativeMeasurement (controller.py:347-353)
+      bad = i;
+      break;
+    }
+    // EnergyLedger.observe_request -> ewma_update (energy.py:24-36, 75-87)
+    ewma = (seen > 0) ? f64_add(f64_mul(lam, ewma), f64_mul(one_minus_lam, J)) : J;
+    seen += 1;
+    total = f64_add(total, J);
+    // deque(maxlen=p95_window).append(latency)
+    if (count < cap) {
+      if (lane == 0) win[(head + count) % cap] = L;
+      __syncwarp();
+      sorted_insert(srt, count, L);
+      count += 1;
+    } else {
+      const double old = win[head];
+      __syncwarp();
+      if (lane == 0) win[head] = L;
+      head = (head + 1) % cap;
+      sorted_remove(srt, count, old);
+      sorted_insert(srt, count - 1, L);
+    }
+    const int rank = (int)ceil(f64_mul(0.95, (double)count));  // ceil(95.0/100.0 * n)
+    p95 = srt[rank - 1];
+    ch_observe(ce, ewma);
+    ch_observe(cq, (double)Q);
+    ch_observe(cp, p95);
+    outc += 1;
+    if (set_qd) last_qd = Q;
+  }
+  __syncwarp();
+  for (int i = lane; i < cap; i += 32) st->win[i] = win[i];
+  for (int i = lane; i < count; i += 32) st->win_sorted[i] = srt[i];
+  if (lane == 0) {
+    st->ewma_joules_per_request = ewma;
+    st->total_joules = total;
+    st->samples_seen = seen;
+    st->p95_current = p95;
+    st->n_energy = ce;
+    st->n_queue_depth = cq;
+    st->n_p95_ms = cp;
+    st->win_count = count;
+    st->win_head = head;
+    st->outcomes_total = outc;
+    st->queue_depth = last_qd;
+    if (err) *err = bad;
+  }
+}
+
+__global__ void state_scalar_kernel(gg_state* st, int which, double t, int32_t q) {
+  if (threadIdx.x != 0) return;
+  if (which == 0) st->t_origin = t;
+  else st->queue_depth = q;
+}
+
+// ---------------------------------------------------------------------------
+// K3: fp32 logits -> fp64 probabilities, one warp per row.  Probabilities are
+// exp((double)x - max) / sum in fp64, so |sum(p) - 1| is a few ulp and the rows
+// pass _validate_distribution (controller.py:132-134); fp32 rows would not.
+__global__ void __launch_bounds__(256) epilogue_kernel(const float* logits, int64_t n, int32_t k,
+                                                       int64_t ld, int32_t proxy, double ln_k,
+                                                       double* probs, int32_t* argmax,
+                                                       double* conf, double* util) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= n) return;
+  const float* x = logits + row * ld;
+  float m = -INFINITY;
+  for (int j = lane; j < k; j += 32) m = fmaxf(m, x[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const double md = (double)m;
+  double s = 0.0;
+  for (int j = lane; j < k; j += 32) s += exp((double)x[j] - md);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const double inv = 1.0 / s;
+  double best = -1.0;
+  int bi = 0x7fffffff;
+  double* prow = probs ? probs + row * (int64_t)k : nullptr;
+  for (int j = lane; j < k; j += 32) {
+    double pj = exp((double)x[j] - md) * inv;
+    if (prow) prow[j] = pj;
+    if (pj > best) {
+      best = pj;
+      bi = j;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) {
+      best = ob;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    if (argmax) argmax[row] = bi;
+    if (conf) conf[row] = best;
+  }
+  if (util && prow) {
+    __syncwarp();
+    if (lane == 0) {  // the controller's own sequential utility of the written row
+      RowAcc acc;
+      const bool entropy = proxy == GG_UTIL_ENTROPY;
+      for (int j = 0; j < k; ++j) acc.add(prow[j], entropy);
+      double u;
+      util[row] = acc.finish(k, entropy, ln_k, u) ? u : __longlong_as_double(0x7ff8000000000000ll);
+    }
+  }
+}
+
+// Stateless batch forms (gg_utility / gg_threshold / gg_cost).
+__global__ void utility_kernel(const double* probs, int64_t n, int32_t k, int64_t stride,
+                               int32_t proxy, double ln_k, double* util, uint8_t* valid) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const bool entropy = proxy == GG_UTIL_ENTROPY;
+  RowAcc acc;
+  for (int c = 0; c < k; ++c) acc.add(probs[r * stride + c], entropy);
+  double u;
+  const bool ok = acc.finish(k, entropy, ln_k, u);
+  if (util) util[r] = ok ? u : __longlong_as_double(0x7ff8000000000000ll);
+  if (valid) valid[r] = ok ? 1 : 0;
+}
+
+__global__ void threshold_kernel(double tau0, double tau_inf, double k, double t_origin,
+                                 const double* t, double* tau, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double el = f64_sub(t[i], t_origin);
+  el = (el > 0.0) ? el : 0.0;
+  tau[i] = f64_add(tau_inf, f64_mul(f64_sub(tau0, tau_inf), exp(f64_mul(-k, el))));
+}
+
+__global__ void cost_kernel(double alpha, double beta, double gamma, const double* uec, double* j,
+                            int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  j[i] = f64_add(f64_add(f64_mul(alpha, uec[3 * i]), f64_mul(beta, uec[3 * i + 1])),
+                 f64_mul(gamma, uec[3 * i + 2]));
+}
+
+}  // namespace gg
+
+// ===========================================================================
+// C ABI
+using namespace gg;
+
+extern "C" {
+
+const char* gg_version(void) { return "greengate-b200 0.1.0 (sm_100a)"; }
+int gg_abi_version(void) { return GG_ABI_VERSION; }
+size_t gg_state_bytes(void) { return sizeof(gg_state); }
+
+int gg_validate_params(const gg_params* p) {
+  if (!p) return GG_ERR_INVALID_ARGUMENT;
+  // CostWeights.__post_init__ (controller.py:85-88) -> ValueError
+  if (!(isfinite(p->alpha) && isfinite(p->beta) && isfinite(p->gamma))) return GG_ERR_INVALID_ARGUMENT;
+  // ThresholdSchedule.__post_init__ (controller.py:100-105)
+  if (!(isfinite(p->tau0) && isfinite(p->tau_inf) && isfinite(p->k))) return GG_ERR_INVALID_SCHEDULE;
+  if (p->k <= 0.0) return GG_ERR_INVALID_SCHEDULE;
+  // EnergyLedger.__post_init__ (energy.py:64-69)
+  if (!(isfinite(p->ewma_lambda) && p->ewma_lambda > 0.0 && p->ewma_lambda < 1.0)) return GG_ERR_INVALID_LAMBDA;
+  if (p->direction < 0 || p->direction > 1) return GG_ERR_INVALID_ARGUMENT;
+  if (p->utility_proxy < 0 || p->utility_proxy > 1) return GG_ERR_INVALID_ARGUMENT;
+  if (p->routing < 0 || p->routing > 2) return GG_ERR_INVALID_ARGUMENT;
+  if (p->p95_window < 1 || p->p95_window > GG_P95_WINDOW_MAX) return GG_ERR_INVALID_ARGUMENT;
+  return GG_OK;
+}
+
+int gg_state_init(gg_state* state_dev, double t_origin, void* stream) {
+  if (!state_dev) return GG_ERR_INVALID_ARGUMENT;
+  if (!isfinite(t_origin)) return GG_ERR_INVALID_SCHEDULE;
+  cudaStream_t s = gg_stream(stream);
+  GG_CUDA_OK(cudaMemsetAsync(state_dev, 0, sizeof(gg_state), s));
+  state_scalar_kernel<<<1, 32, 0, s>>>(state_dev, 0, t_origin, 0);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_reset_clock(gg_state* state_dev, double t_origin, void* stream) {
+  if (!state_dev) return GG_ERR_INVALID_ARGUMENT;
+  if (!isfinite(t_origin)) return GG_ERR_INVALID_SCHEDULE;
+  state_scalar_kernel<<<1, 32, 0, gg_stream(stream)>>>(state_dev, 0, t_origin, 0);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_set_queue_depth(gg_state* state_dev, int32_t queue_depth, void* stream) {
+  if (!state_dev || queue_depth < 0) return GG_ERR_INVALID_ARGUMENT;
+  state_scalar_kernel<<<1, 32, 0, gg_stream(stream)>>>(state_dev, 1, 0.0, queue_depth);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+static int64_t admit_blocks(int64_t n, int32_t k) {
+  const int64_t rows_per_block = (k <= 16) ? 256 * 4 : kLargeThreads;
+  int64_t nb = (n + rows_per_block - 1) / rows_per_block;
+  return nb < 1 ? 1 : nb;
+}
+
+size_t gg_admit_workspace_bytes(int64_t n) {
+  const int64_t nb = (n + kLargeThreads - 1) / kLargeThreads;  // worst case over kernels
+  return kWsHeader + sizeof(unsigned long long) * (size_t)(nb < 1 ? 1 : nb);
+}
+
+int gg_admit(const gg_params* params, gg_state* state_dev, const double* probs_dev, int64_t n,
+             int32_t k, int64_t row_stride, const double* now_dev, const gg_snapshot* snapshot_dev,
+             uint8_t* decision_dev, double* breakdown_dev, int32_t* admitted_idx_dev,
+             gg_batch_info* info_dev, void* workspace_dev, size_t workspace_bytes, void* stream) {
+  int rc = gg_validate_params(params);
+  if (rc != GG_OK) return rc;
+  if (!state_dev || !decision_dev || !workspace_dev || n < 0 || k < 1 || row_stride < k)
+    return GG_ERR_INVALID_ARGUMENT;
+  if (n > 0 && (!probs_dev || !now_dev)) return GG_ERR_INVALID_ARGUMENT;
+  if (n > (int64_t)0x7fffffff) return GG_ERR_UNSUPPORTED;  // int32 admitted indices
+  if (workspace_bytes < gg_admit_workspace_bytes(n)) return GG_ERR_INVALID_ARGUMENT;
+  AdmitArgs a;
+  a.p = *params;
+  a.state = state_dev;
+  a.probs = probs_dev;
+  a.n = n;
+  a.k = k;
+  a.stride = row_stride;
+  a.now = now_dev;
+  a.snap = snapshot_dev;
+  a.decision = decision_dev;
+  a.breakdown = breakdown_dev;
+  a.admitted_idx = admitted_idx_dev;
+  a.info = info_dev;
+  a.ws = reinterpret_cast<AdmitWorkspace*>(workspace_dev);
+  a.ln_k = log((double)k);  // host libm == CPython math.log (controller.py:142)
+  const int64_t nb = admit_blocks(n, k);
+  cudaStream_t s = gg_stream(stream);
+  const bool aligned16 = ((reinterpret_cast<uintptr_t>(probs_dev) & 15) == 0) && (row_stride % 2 == 0);
+  if (k == 2 && aligned16)
+    admit_small_kernel<2, 256, 4><<<(unsigned)nb, 256, 0, s>>>(a);
+  else if (k == 4 && aligned16)
+    admit_small_kernel<4, 256, 4><<<(unsigned)nb, 256, 0, s>>>(a);
+  else if (k <= 16)
+    admit_small_kernel<0, 256, 4><<<(unsigned)nb, 256, 0, s>>>(a);
+  else
+    admit_large_kernel<<<(unsigned)nb, kLargeThreads, 0, s>>>(a);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_outcome(const gg_params* params, gg_state* state_dev, const double* latency_ms_dev,
+               const double* joules_dev, const int32_t* queue_depth_dev, int64_t n,
+               int32_t set_queue_depth, int64_t* error_index_dev, void* stream) {
+  int rc = gg_validate_params(params);
+  if (rc != GG_OK) return rc;
+  if (!state_dev || n < 0) return GG_ERR_INVALID_ARGUMENT;
+  if (n > 0 && (!latency_ms_dev || !joules_dev || !queue_depth_dev)) return GG_ERR_INVALID_ARGUMENT;
+  outcome_kernel<<<1, 32, 0, gg_stream(stream)>>>(*params, state_dev, latency_ms_dev, joules_dev,
+                                                   queue_depth_dev, n, set_queue_depth,
+                                                   error_index_dev);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_epilogue(const float* logits_dev, int64_t n, int32_t k, int64_t ld, int32_t utility_proxy,
+                double* probs_dev, int32_t* argmax_dev, double* confidence_dev, double* utility_dev,
+                void* stream) {
+  if (!logits_dev || n < 0 || k < 1 || ld < k) return GG_ERR_INVALID_ARGUMENT;
+  if (utility_dev && !probs_dev) return GG_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GG_OK;
+  const int rows_per_block = 8;
+  const int64_t nb = (n + rows_per_block - 1) / rows_per_block;
+  epilogue_kernel<<<(unsigned)nb, 256, 0, gg_stream(stream)>>>(
+      logits_dev, n, k, ld, utility_proxy, log((double)k), probs_dev, argmax_dev, confidence_dev,
+      utility_dev);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_utility(const double* probs_dev, int64_t n, int32_t k, int64_t row_stride,
+               int32_t utility_proxy, double* utility_dev, uint8_t* valid_dev, void* stream) {
+  if (n < 0 || k < 1 || row_stride < k || (n > 0 && !probs_dev)) return GG_ERR_INVALID_ARGUMENT;
+  if (utility_proxy < 0 || utility_proxy > 1) return GG_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GG_OK;
+  utility_kernel<<<(unsigned)((n + 127) / 128), 128, 0, gg_stream(stream)>>>(
+      probs_dev, n, k, row_stride, utility_proxy, log((double)k), utility_dev, valid_dev);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_threshold(double tau0, double tau_inf, double k, double t_origin, const double* t_dev,
+                 double* tau_dev, int64_t n, void* stream) {
+  // threshold_at re-checks the rate (controller.py:120-121)
+  if (!(isfinite(k) && k > 0.0)) return GG_ERR_INVALID_SCHEDULE;
+  if (n < 0 || (n > 0 && (!t_dev || !tau_dev))) return GG_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GG_OK;
+  threshold_kernel<<<(unsigned)((n + 255) / 256), 256, 0, gg_stream(stream)>>>(
+      tau0, tau_inf, k, t_origin, t_dev, tau_dev, n);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_cost(double alpha, double beta, double gamma, const double* uec_dev, double* j_dev,
+            int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && (!uec_dev || !j_dev))) return GG_ERR_INVALID_ARGUMENT;
+  if (n == 0) return GG_OK;
+  cost_kernel<<<(unsigned)((n + 255) / 256), 256, 0, gg_stream(stream)>>>(alpha, beta, gamma,
+                                                                          uec_dev, j_dev, n);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+}  // extern "C"
