@@ -36,6 +36,9 @@ SIGNATURES: dict[str, tuple] = {
     "gg_utility": (C.c_int, [_P, _I64, _I32, _I64, _I32, _P, _P, _P]),
     "gg_threshold": (C.c_int, [_D, _D, _D, _D, _P, _P, _I64, _P]),
     "gg_cost": (C.c_int, [_D, _D, _D, _P, _P, _I64, _P]),
+    # forward pass (include/greengate_b200_forward.h)
+    "gg_gemm_bf16": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I32,
+                               _I32, _P]),
 }
 
 

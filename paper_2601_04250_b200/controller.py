@@ -556,7 +556,7 @@ class AdmissionController:
         n, k = int(scores.shape[0]), int(scores.shape[1])
         if scores.dtype != torch.float64 or now.dtype != torch.float64:
             raise TypeError("scores and now must be float64 CUDA tensors")
-        if scores.stride(1) != 1:
+        if n > 0 and k > 1 and scores.stride(1) != 1:
             raise ValueError("scores rows must be contiguous")
         self._ensure_ws(n)
         if out is None:

@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include "../../include/greengate_b200.h"
+#include "../../include/greengate_b200_forward.h"
 
 #define GG_CUDA_OK(expr)                                   \
   do {                                                     \

@@ -1,0 +1,291 @@
+// gg_gemm.cu — tcgen05/TMEM GEMM with TMA operand loads and fused epilogues.
+//
+//   D[M, N] = act( A[M, K] . B[N, K]^T + bias[N] (+ residual[M, N]) )     bf16 out
+//
+// A and B are bf16, K-contiguous (activations x nn.Linear weight layout), fp32
+// accumulation in tensor memory.  One CTA computes a BM x BN tile:
+//   warp 0      TMA producer (one elected lane), S-stage smem ring, mbarriers
+//   warp 1      TMEM allocator + tcgen05.mma issuer (one elected lane)
+//   warps 2..5  epilogue: tcgen05.ld -> bias/residual/activation -> bf16 stores
+// The CTA is persistent over tiles (grid = #SMs); the accumulator is double
+// buffered in TMEM so the epilogue of tile i overlaps the MMAs of tile i+1.
+#include <cudaTypedefs.h>
+#include <stdio.h>
+
+#include "gg_common.cuh"
+#include "gg_tc.cuh"
+#include "gg_kernels.h"
+
+namespace gg {
+using namespace tc;
+
+enum : int { ACT_NONE = 0, ACT_RELU = 1, ACT_GELU = 2 };
+
+struct GemmEpilogue {
+  __nv_bfloat16* D;
+  int64_t ldd;
+  const float* bias;               // [N] or null
+  const __nv_bfloat16* residual;   // [M, ldr] or null
+  int64_t ldr;
+  int act;
+};
+
+constexpr int kBK = 64;            // 64 bf16 = 128 B = one swizzle row
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+
+template <int BM, int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int A_BYTES = BM * kBK * 2;
+  static constexpr int B_BYTES = BN * kBK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
+};
+
+template <int BM, int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
+                      const __grid_constant__ CUtensorMap map_b, int M, int N, int K,
+                      GemmEpilogue ep) {
+  using L = GemmSmem<BM, BN, STAGES>;
+  static_assert(BM == 128, "cta_group::1 tiles use all 128 TMEM lanes");
+  static_assert(2 * BN <= 512, "two accumulators must fit TMEM");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;     // [2]
+  uint64_t* acc_empty = acc_full + 2;      // [2]
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = K / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], kEpiWarps);
+    }
+    fence_mbar_init();
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+  }
+  if (warp == 1) tmem_alloc(tmem_base_smem, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int tm = tile % tiles_m, tn = tile / tiles_m;  // M-fastest: B tile stays hot in L2
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t round = it / STAGES;
+          mbar_wait(&empty[s], (round & 1) ^ 1);
+          uint8_t* sa = smem + s * L::STAGE_BYTES;
+          uint8_t* sb = sa + L::A_BYTES;
+          mbar_expect_tx(&full[s], L::STAGE_BYTES);
+          tma_load_2d(sa, &map_a, &full[s], kb * kBK, tm * BM);
+          tma_load_2d(sb, &map_b, &full[s], kb * kBK, tn * BN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      int it = 0, t = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+        const int acc = t & 1;
+        const uint32_t use = t >> 1;
+        mbar_wait(&acc_empty[acc], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t round = it / STAGES;
+          mbar_wait(&full[s], round & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
+          const uint32_t sb = sa + L::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            umma_bf16(d_tmem, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sb + kk * 32), idesc,
+                      (kb | kk) != 0);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&acc_full[acc]);
+      }
+    }
+  } else {
+    // ===== epilogue warps =====
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    int t = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      const int acc = t & 1;
+      const uint32_t use = t >> 1;
+      mbar_wait(&acc_full[acc], use & 1);
+      tc_fence_after();
+      const int row = tm * BM + quarter * 32 + lane;
+      const bool row_ok = row < M;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
+        tmem_ld_wait();
+        const int col0 = tn * BN + c;
+        if (!row_ok || col0 >= N) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (ep.bias) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            float4 b = *reinterpret_cast<const float4*>(ep.bias + col0 + i);
+            v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
+          }
+        }
+        if (ep.residual) {
+          const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + (int64_t)row * ep.ldr + col0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u = rp[q];
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float2 f = __bfloat1622float2(h[e]);
+              v[q * 8 + 2 * e] += f.x;
+              v[q * 8 + 2 * e + 1] += f.y;
+            }
+          }
+        }
+        if (ep.act == ACT_RELU) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+        } else if (ep.act == ACT_GELU) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
+        }
+        uint4* dp = reinterpret_cast<uint4*>(ep.D + (int64_t)row * ep.ldd + col0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+          u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+          u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+          u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+          dp[q] = u;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side: tensor-map encoding through the driver entry point (no -lcuda).
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int get_encoder() {
+  if (g_encode) return GG_OK;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn)
+    return GG_ERR_CUDA;
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return GG_OK;
+}
+
+// 2-D bf16 K-major operand [rows, cols] with row pitch ld (elements); box =
+// [64 cols (128 B), box_rows], 128-byte swizzle, OOB -> 0.
+int make_map_2d(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                int box_rows) {
+  if (get_encoder() != GG_OK) return GG_ERR_CUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? GG_OK : GG_ERR_INVALID_ARGUMENT;
+}
+
+static int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_num_sms;
+}
+
+template <int BM, int BN, int STAGES>
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
+                       const GemmEpilogue& ep, cudaStream_t s, int max_ctas) {
+  using L = GemmSmem<BM, BN, STAGES>;
+  auto kern = gemm_bf16_tcgen05<BM, BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL) != cudaSuccess)
+      return GG_ERR_CUDA;
+    attr = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  int grid = tiles < num_sms() ? tiles : num_sms();
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  kern<<<grid, kThreads, L::TOTAL, s>>>(ma, mb, M, N, K, ep);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+}  // namespace gg
+
+using namespace gg;
+
+extern "C" int gg_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
+                            int64_t ldd, int64_t M, int64_t N, int64_t K, const float* bias,
+                            const void* residual, int64_t ldr, int32_t act, int32_t tile_n,
+                            void* stream) {
+  if (!A || !B || !D || M <= 0 || N <= 0 || K <= 0) return GG_ERR_INVALID_ARGUMENT;
+  if (K % 64 || N % 32 || lda % 8 || ldb % 8 || ldd % 8 || (residual && ldr % 8)) return GG_ERR_INVALID_ARGUMENT;
+  if (act < 0 || act > 2) return GG_ERR_INVALID_ARGUMENT;
+  int bn = tile_n > 0 ? tile_n : (N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64));
+  if (bn != 64 && bn != 128 && bn != 256) return GG_ERR_INVALID_ARGUMENT;
+  CUtensorMap ma, mb;
+  int rc = make_map_2d(&ma, A, M, K, lda, 128);
+  if (rc) return rc;
+  rc = make_map_2d(&mb, B, N, K, ldb, bn);
+  if (rc) return rc;
+  GemmEpilogue ep{reinterpret_cast<__nv_bfloat16*>(D), ldd, bias,
+                  reinterpret_cast<const __nv_bfloat16*>(residual), ldr, act};
+  cudaStream_t s = gg_stream(stream);
+  switch (bn) {
+    case 256: return launch_gemm<128, 256, 4>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
+    case 128: return launch_gemm<128, 128, 6>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
+    default: return launch_gemm<128, 64, 8>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
+  }
+}

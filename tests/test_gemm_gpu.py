@@ -1,0 +1,85 @@
+"""tcgen05 GEMM (gg_gemm_bf16) vs a plain PyTorch fp32 reference of the same op."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    from paper_2601_04250_b200 import _native
+    return torch, _native, _native.load()
+
+
+def run_gemm(env, A, B, bias=None, residual=None, act=0, tile_n=0):
+    torch, nat, lib = env
+    M, K = A.shape
+    N = B.shape[0]
+    D = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    rc = lib.gg_gemm_bf16(nat.ptr(A), A.stride(0), nat.ptr(B), B.stride(0), nat.ptr(D), D.stride(0),
+                          M, N, K, nat.ptr(bias), nat.ptr(residual),
+                          residual.stride(0) if residual is not None else 0, act, tile_n,
+                          nat.stream_ptr())
+    nat.check("gg_gemm_bf16", rc)
+    return D
+
+
+def reference(A, B, bias, residual, act):
+    import torch
+    y = A.float() @ B.float().t()
+    if bias is not None:
+        y = y + bias.float()
+    if residual is not None:
+        y = y + residual.float()
+    if act == 1:
+        y = torch.relu(y)
+    elif act == 2:
+        y = torch.nn.functional.gelu(y)
+    return y
+
+
+@pytest.mark.parametrize("M,N,K,tile_n", [
+    (128, 256, 64, 256), (256, 256, 128, 256), (300, 512, 768, 0), (1000, 768, 768, 0),
+    (16384, 2304, 768, 0), (16384, 768, 3072, 0), (4096, 3072, 768, 128), (513, 64, 1024, 64),
+    (128, 32, 768, 64)])
+def test_gemm_shapes(env, M, N, K, tile_n):
+    torch = env[0]
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn((M, K), device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn((N, K), device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    D = run_gemm(env, A, B, tile_n=tile_n)
+    ref = reference(A, B, None, None, 0)
+    torch.cuda.synchronize()
+    err = (D.float() - ref).abs().max().item()
+    # bf16 output rounding of O(1) values plus fp32 accumulation order: 2e-2 (north-star bf16 tolerance)
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("act", [0, 1, 2])
+def test_gemm_fused_epilogue(env, act):
+    torch = env[0]
+    g = torch.Generator(device="cuda").manual_seed(act)
+    M, N, K = 777, 768, 768
+    A = torch.randn((M, K), device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn((N, K), device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn((M, N), device="cuda", generator=g).to(torch.bfloat16)
+    D = run_gemm(env, A, B, bias=bias, residual=res, act=act)
+    ref = reference(A, B, bias, res, act)
+    err = (D.float() - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
+def test_gemm_rejects_bad_shapes(env):
+    torch, nat, lib = env
+    A = torch.zeros((128, 100), dtype=torch.bfloat16, device="cuda")
+    B = torch.zeros((64, 100), dtype=torch.bfloat16, device="cuda")
+    D = torch.zeros((128, 64), dtype=torch.bfloat16, device="cuda")
+    rc = lib.gg_gemm_bf16(nat.ptr(A), 100, nat.ptr(B), 100, nat.ptr(D), 64, 128, 64, 100,
+                          None, None, 0, 0, 0, nat.stream_ptr())
+    assert rc != 0
