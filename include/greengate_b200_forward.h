@@ -30,6 +30,62 @@ int gg_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* D
                  int64_t M, int64_t N, int64_t K, const float* bias, const void* residual,
                  int64_t ldr, int32_t act, int32_t tile_n, void* stream);
 
+/* Output layouts of gg_gemm. */
+enum {
+  GG_OUT_BF16 = 0,       /* D bf16 [M, ldd] */
+  GG_OUT_F32 = 1,        /* D fp32 [M, ldd] (classifier logits for K3) */
+  GG_OUT_QKV_HEADS = 2   /* fused-QKV projection: D = bf16 [3][B][H][S][64] planes:
+                            Q * 1/sqrt(64), K, and V stored transposed [B][H][64][S] */
+};
+typedef struct {
+  const float* bias;     /* [N] fp32 or NULL */
+  const void* residual;  /* bf16 [M, ldr] or NULL, added before the activation */
+  int64_t ldr;
+  int32_t act;           /* GG_ACT_* */
+  int32_t out_mode;      /* GG_OUT_* */
+  int32_t seq_len;       /* GG_OUT_QKV_HEADS: S (multiple of 128) */
+  int32_t heads;         /* GG_OUT_QKV_HEADS: H, N == 3 * H * 64 */
+  int32_t tile_n;        /* 0 = auto, 64 / 128 / 256 */
+  int32_t reserved;
+} gg_gemm_epilogue;
+int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
+            int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* epilogue, void* stream);
+
+/* Multi-head self-attention for head dim 64 on the GG_OUT_QKV_HEADS planes:
+ * ctx[b*S + s, h*64 + d] = softmax(Q K^T + mask) V, one CTA per (b, h), both
+ * products on tcgen05 with the scores and the output in TMEM.  mask: int32
+ * [B, S] (0 = masked key, DistilBERT's masked_fill with finfo.min) or NULL.
+ * Requires S == 128. */
+int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int64_t ldc, int32_t batch,
+                 int32_t heads, int32_t seq_len, void* stream);
+
+/* y = LayerNorm(x) * gamma + beta over rows of width `width` (fp32 statistics),
+ * bf16 in/out; eps as in the model config (DistilBERT 1e-12). */
+int gg_layernorm(const void* x, int64_t ldx, void* y, int64_t ldy, const float* gamma,
+                 const float* beta, int64_t rows, int32_t width, float eps, void* stream);
+
+/* DistilBERT embeddings: y[t] = LayerNorm(word[ids[t]] + pos[t % seq_len]) (bf16 tables). */
+int gg_embed_layernorm(const int32_t* ids, const void* word, const void* pos, void* y,
+                       const float* gamma, const float* beta, int64_t tokens, int32_t seq_len,
+                       int32_t width, float eps, void* stream);
+
+/* ---- ResNet-18 (NHWC bf16) ------------------------------------------------ */
+/* Implicit-GEMM convolution on tcgen05: y[n,ho,wo,co] = relu?(sum_{r,s,c}
+ * x[n, ho*stride-pad+r, wo*stride-pad+s, c] * w[co, (r*S+s)*C + c] + bias[co]
+ * (+ residual[n,ho,wo,co])).  w is BN-folded, [Cout, Kpad] with Kpad a
+ * multiple of 64 >= R*S*C (zero tail); C % 8 == 0, Cout % 64 == 0. */
+int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
+              int32_t Cout, int32_t R, int32_t S, int32_t stride, int32_t pad, int32_t Kpad,
+              const float* bias, const void* residual, int32_t relu, void* y, void* stream);
+/* fp32 NCHW image batch -> bf16 NHWC with channels zero-padded to cpad (% 8). */
+int gg_nchw_to_nhwc(const float* x, int32_t N, int32_t C, int32_t H, int32_t W, int32_t cpad,
+                    void* y, void* stream);
+/* 3x3 / stride 2 / pad 1 max pool (NHWC, C % 8 == 0). */
+int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, void* y,
+                    void* stream);
+/* Global average pool NHWC [N, HW, C] -> [N, C]. */
+int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

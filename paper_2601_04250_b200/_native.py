@@ -39,6 +39,15 @@ SIGNATURES: dict[str, tuple] = {
     # forward pass (include/greengate_b200_forward.h)
     "gg_gemm_bf16": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I32,
                                _I32, _P]),
+    "gg_gemm": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P]),
+    "gg_attention": (C.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, _P]),
+    "gg_layernorm": (C.c_int, [_P, _I64, _P, _I64, _P, _P, _I64, _I32, C.c_float, _P]),
+    "gg_embed_layernorm": (C.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, C.c_float, _P]),
+    "gg_conv2d": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32,
+                            _P, _P, _I32, _P, _P]),
+    "gg_nchw_to_nhwc": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
+    "gg_maxpool3x3s2": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P]),
+    "gg_avgpool": (C.c_int, [_P, _I32, _I32, _I32, _P, _P]),
 }
 
 

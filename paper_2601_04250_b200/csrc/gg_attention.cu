@@ -1,0 +1,186 @@
+// gg_attention.cu — DistilBERT self-attention (S = 128, head dim 64) on tcgen05.
+//
+// One CTA per (batch, head), 4 warps:
+//   TMA  : Q [128 x 64], K [128 x 64] and V^T [64 x 128] (written transposed by
+//          the QKV GEMM epilogue) into 128B-swizzled smem;
+//   MMA 1: S = Q K^T (M=128, N=128, K=64) into TMEM columns [0, 128);
+//   softmax: each thread owns one query row, reads its 128 scores with
+//          tcgen05.ld, applies the key mask, exp(s - max) in fp32, writes the
+//          unnormalized P row (bf16, <= 1) into the swizzled A-operand layout;
+//   MMA 2: O = P V (M=128, N=64, K=128) into TMEM columns [128, 192);
+//   epilogue: O / rowsum -> bf16 ctx[b*S + s, h*64 + d].
+#include <cudaTypedefs.h>
+
+#include "gg_common.cuh"
+#include "gg_kernels.h"
+#include "gg_tc.cuh"
+
+namespace gg {
+using namespace tc;
+
+constexpr int kAttnS = 128;
+constexpr int kAttnD = 64;
+constexpr int kAttnThreads = 128;
+constexpr int kOffQ = 0, kOffK = 16384, kOffV = 32768, kOffP = 49152;
+constexpr int kAttnSmem = 81920 + 64 + 1024;
+
+__global__ void __launch_bounds__(kAttnThreads, 2)
+    attention_tcgen05(const __grid_constant__ CUtensorMap map_q,
+                      const __grid_constant__ CUtensorMap map_k,
+                      const __grid_constant__ CUtensorMap map_vt, const int32_t* mask,
+                      __nv_bfloat16* ctx, int64_t ldc, int heads) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar_load = reinterpret_cast<uint64_t*>(smem + 81920);
+  uint64_t* bar_s = bar_load + 1;
+  uint64_t* bar_o = bar_load + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_load + 3);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bh = blockIdx.x;
+  const int b = bh / heads, h = bh % heads;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_load, 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_o, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(bar_load, 16384 + 16384 + 2 * 8192);  // Q + K + V^T (two 64-key blocks)
+    tma_load_2d(smem + kOffQ, &map_q, bar_load, 0, bh * kAttnS);
+    tma_load_2d(smem + kOffK, &map_k, bar_load, 0, bh * kAttnS);
+    tma_load_2d(smem + kOffV, &map_vt, bar_load, 0, bh * kAttnD);
+    tma_load_2d(smem + kOffV + 8192, &map_vt, bar_load, 64, bh * kAttnD);
+    mbar_wait(bar_load, 0);
+    tc_fence_after();
+    const uint32_t sq = smem_u32(smem + kOffQ), sk = smem_u32(smem + kOffK);
+    constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      umma_bf16(tmem, sdesc_k_sw128(sq + kk * 32), sdesc_k_sw128(sk + kk * 32), idesc_s, kk != 0);
+    umma_commit(bar_s);
+  }
+
+  // ---- softmax: thread = query row ----
+  const int row = warp * 32 + lane;
+  mbar_wait(bar_s, 0);
+  tc_fence_after();
+  float s[kAttnS];
+#pragma unroll
+  for (int c = 0; c < kAttnS; c += 32) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + c, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(r[i]);
+  }
+  if (mask) {
+    const int32_t* mrow = mask + (int64_t)b * kAttnS;
+#pragma unroll
+    for (int j = 0; j < kAttnS; ++j)
+      if (__ldg(mrow + j) == 0) s[j] = -INFINITY;
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < kAttnS; ++j) mx = fmaxf(mx, s[j]);
+  const float mref = (mx == -INFINITY) ? 0.0f : mx;
+  float sum = 0.0f;
+  const float l2e = 1.4426950408889634f;
+#pragma unroll
+  for (int j = 0; j < kAttnS; ++j) {
+    s[j] = exp2f((s[j] - mref) * l2e);
+    sum += s[j];
+  }
+  // P row -> A operand (K-major, SW128): key block kb = j / 64, 16-byte chunk c = (j % 64) / 8
+  uint8_t* prow = smem + kOffP + (row >> 3) * 1024 + (row & 7) * 128;
+#pragma unroll
+  for (int kb = 0; kb < 2; ++kb) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int j = kb * 64 + c * 8;
+      uint4 u;
+      u.x = pack_bf16(s[j + 0], s[j + 1]);
+      u.y = pack_bf16(s[j + 2], s[j + 3]);
+      u.z = pack_bf16(s[j + 4], s[j + 5]);
+      u.w = pack_bf16(s[j + 6], s[j + 7]);
+      *reinterpret_cast<uint4*>(prow + kb * 16384 + ((c ^ (row & 7)) << 4)) = u;
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tc_fence_after();
+    const uint32_t sp = smem_u32(smem + kOffP), sv = smem_u32(smem + kOffV);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(128, 64);
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16(tmem + 128, sdesc_k_sw128(sp + kb * 16384 + kk * 32),
+                  sdesc_k_sw128(sv + kb * 8192 + kk * 32), idesc_o, (kb | kk) != 0);
+    umma_commit(bar_o);
+  }
+  mbar_wait(bar_o, 0);
+  tc_fence_after();
+  const float inv = 1.0f / sum;
+  __nv_bfloat16* out = ctx + ((int64_t)b * kAttnS + row) * ldc + h * kAttnD;
+#pragma unroll
+  for (int c = 0; c < kAttnD; c += 32) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + 128 + c, r);
+    tmem_ld_wait();
+    uint4* dp = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      u.x = pack_bf16(__uint_as_float(r[8 * q + 0]) * inv, __uint_as_float(r[8 * q + 1]) * inv);
+      u.y = pack_bf16(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv);
+      u.z = pack_bf16(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv);
+      u.w = pack_bf16(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv);
+      dp[q] = u;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+}  // namespace gg
+
+using namespace gg;
+
+extern "C" int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int64_t ldc,
+                            int32_t batch, int32_t heads, int32_t seq_len, void* stream) {
+  if (!qkv || !ctx || batch <= 0 || heads <= 0) return GG_ERR_INVALID_ARGUMENT;
+  if (seq_len != kAttnS || ldc % 8 || ldc < (int64_t)heads * kAttnD) return GG_ERR_UNSUPPORTED;
+  const int64_t plane = (int64_t)batch * heads * seq_len * kAttnD;
+  const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(qkv);
+  CUtensorMap mq, mk, mv;
+  const int64_t rows = (int64_t)batch * heads * seq_len;
+  int rc = make_map_2d(&mq, base, rows, kAttnD, kAttnD, 128);
+  if (!rc) rc = make_map_2d(&mk, base + plane, rows, kAttnD, kAttnD, 128);
+  if (!rc) rc = make_map_2d(&mv, base + 2 * plane, (int64_t)batch * heads * kAttnD, seq_len, seq_len, 64);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(attention_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kAttnSmem) != cudaSuccess)
+      return GG_ERR_CUDA;
+    attr = true;
+  }
+  attention_tcgen05<<<batch * heads, kAttnThreads, kAttnSmem, gg_stream(stream)>>>(
+      mq, mk, mv, mask, reinterpret_cast<__nv_bfloat16*>(ctx), ldc, heads);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}

@@ -680,9 +680,9 @@ int gg_admit(const gg_params* params, gg_state* state_dev, const double* probs_d
              gg_batch_info* info_dev, void* workspace_dev, size_t workspace_bytes, void* stream) {
   int rc = gg_validate_params(params);
   if (rc != GG_OK) return rc;
-  if (!state_dev || !decision_dev || !workspace_dev || n < 0 || k < 1 || row_stride < k)
+  if (!state_dev || !workspace_dev || n < 0 || k < 1 || row_stride < k)
     return GG_ERR_INVALID_ARGUMENT;
-  if (n > 0 && (!probs_dev || !now_dev)) return GG_ERR_INVALID_ARGUMENT;
+  if (n > 0 && (!probs_dev || !now_dev || !decision_dev)) return GG_ERR_INVALID_ARGUMENT;
   if (n > (int64_t)0x7fffffff) return GG_ERR_UNSUPPORTED;  // int32 admitted indices
   if (workspace_bytes < gg_admit_workspace_bytes(n)) return GG_ERR_INVALID_ARGUMENT;
   AdmitArgs a;

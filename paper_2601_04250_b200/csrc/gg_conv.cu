@@ -1,0 +1,408 @@
+// gg_conv.cu — ResNet-18 building blocks on sm_100a (NHWC bf16).
+//
+// Implicit-GEMM convolution on tcgen05:
+//   D[m, co] = relu?( sum_k A[m, k] * W[co, k] + bias[co] (+ residual[m, co]) )
+//   m = (n, ho, wo) output pixel, k = (r, s, c) with c fastest, W = BN-folded
+//   weights [Cout, Kpad] (K-major, zero padded to a multiple of 64).
+// The A operand is never materialized: producer warps gather each 128-pixel x
+// 64-k tile straight from the NHWC activation with 16-byte cp.async (zero-fill
+// for padding and K tail) into the 128B-swizzled layout tcgen05 reads; B comes
+// in by TMA; the fp32 accumulator lives in TMEM (double buffered, persistent
+// CTAs); the epilogue fuses folded-BN bias, the residual add and ReLU.
+//
+//   warps 0-3  A gather (cp.async) + warp 0 lane 0 B TMA
+//   warp 4     TMEM allocator + MMA issuer
+//   warps 5-8  epilogue
+#include <cudaTypedefs.h>
+
+#include "gg_common.cuh"
+#include "gg_kernels.h"
+#include "gg_tc.cuh"
+
+namespace gg {
+using namespace tc;
+
+struct ConvShape {
+  int N, H, W, C;      // input NHWC (C multiple of 8)
+  int Ho, Wo, Cout;
+  int R, S, stride, pad;
+  int Kpad;            // multiple of 64, >= R*S*C
+  int M;               // N*Ho*Wo
+};
+
+struct ConvEpi {
+  __nv_bfloat16* y;               // [M, Cout]
+  const float* bias;              // [Cout]
+  const __nv_bfloat16* residual;  // [M, Cout] or null
+  int relu;
+};
+
+constexpr int kConvProdWarps = 4;
+constexpr int kConvThreads = 32 * (kConvProdWarps + 1 + 4);
+constexpr int kLag = 2;  // cp.async groups in flight per producer thread
+
+template <int BN, int STAGES>
+struct ConvSmem {
+  static constexpr int A_BYTES = 128 * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+__device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kConvThreads, 1)
+    conv_bf16_tcgen05(const __nv_bfloat16* __restrict__ x, const __grid_constant__ CUtensorMap map_w,
+                      ConvShape sh, ConvEpi ep) {
+  using L = ConvSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = (sh.M + 127) / 128, tiles_n = sh.Cout / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = sh.Kpad / 64;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 32 * kConvProdWarps + 1);  // 128 gather arrivals + the B TMA arrive
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 4);
+    }
+    fence_mbar_init();
+    tma_prefetch(&map_w);
+  }
+  if (warp == kConvProdWarps) tmem_alloc(tmem_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < kConvProdWarps) {
+    // ===== A gather: thread = tile row (output pixel) =====
+    const int r_local = threadIdx.x;  // 0..127
+    const uint32_t row_off = (r_local >> 3) * 1024 + (r_local & 7) * 128;
+    const int sw = r_local & 7;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      const int m = tm * 128 + r_local;
+      const bool m_ok = m < sh.M;
+      int n = 0, ho = 0, wo = 0;
+      if (m_ok) {
+        n = m / (sh.Ho * sh.Wo);
+        const int rem = m - n * sh.Ho * sh.Wo;
+        ho = rem / sh.Wo;
+        wo = rem - ho * sh.Wo;
+      }
+      const int hi0 = ho * sh.stride - sh.pad, wi0 = wo * sh.stride - sh.pad;
+      const __nv_bfloat16* xn = x + (int64_t)n * sh.H * sh.W * sh.C;
+      for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t round = it / STAGES;
+        mbar_wait(&empty[s], (round & 1) ^ 1);
+        const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES) + row_off;
+        if (threadIdx.x == 0) {
+          mbar_expect_tx(&full[s], L::B_BYTES);
+          tma_load_2d(smem + s * L::STAGE_BYTES + L::A_BYTES, &map_w, &full[s], kb * 64, tn * BN);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = kb * 64 + j * 8;
+          const int tap = k / sh.C, c0 = k - tap * sh.C;
+          const int rr = tap / sh.S, ss = tap - rr * sh.S;
+          const int hi = hi0 + rr, wi = wi0 + ss;
+          const bool ok = m_ok && tap < sh.R * sh.S && hi >= 0 && hi < sh.H && wi >= 0 && wi < sh.W;
+          const __nv_bfloat16* src = ok ? xn + ((int64_t)hi * sh.W + wi) * sh.C + c0 : x;
+          cp_async_16(sa + ((j ^ sw) << 4), src, ok);
+        }
+        cp_async_commit();
+        if (it >= kLag) {
+          cp_async_wait<kLag>();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&full[(it - kLag) % STAGES]);
+        }
+      }
+    }
+    // drain the last kLag stages
+    cp_async_wait<0>();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int d = (it >= kLag ? it - kLag : 0); d < it; ++d) mbar_arrive(&full[d % STAGES]);
+  } else if (warp == kConvProdWarps) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+      int it = 0, t = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+        const int acc = t & 1;
+        const uint32_t use = t >> 1;
+        mbar_wait(&acc_empty[acc], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
+          const uint32_t sb = sa + L::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_bf16(d_tmem, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sb + kk * 32), idesc,
+                      (kb | kk) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&acc_full[acc]);
+      }
+    }
+  } else {
+    // ===== epilogue =====
+    const int quarter = warp & 3;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      const int acc = t & 1;
+      mbar_wait(&acc_full[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const int m = tm * 128 + quarter * 32 + lane;
+      const bool ok = m < sh.M;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
+        tmem_ld_wait();
+        if (!ok) continue;
+        const int col0 = tn * BN + c;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + i));
+          v[i] = __uint_as_float(r[i]) + b.x;
+          v[i + 1] = __uint_as_float(r[i + 1]) + b.y;
+          v[i + 2] = __uint_as_float(r[i + 2]) + b.z;
+          v[i + 3] = __uint_as_float(r[i + 3]) + b.w;
+        }
+        if (ep.residual) {
+          const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + (int64_t)m * sh.Cout + col0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 u = __ldg(rp + q);
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h2[e]);
+              v[q * 8 + 2 * e] += f.x;
+              v[q * 8 + 2 * e + 1] += f.y;
+            }
+          }
+        }
+        if (ep.relu) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+        }
+        uint4* dp = reinterpret_cast<uint4*>(ep.y + (int64_t)m * sh.Cout + col0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+          u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+          u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+          u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+          dp[q] = u;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == kConvProdWarps) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+template <int BN, int STAGES>
+static int launch_conv(const __nv_bfloat16* x, const CUtensorMap& mw, const ConvShape& sh,
+                       const ConvEpi& ep, cudaStream_t s) {
+  using L = ConvSmem<BN, STAGES>;
+  auto kern = conv_bf16_tcgen05<BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL) != cudaSuccess)
+      return GG_ERR_CUDA;
+    attr = true;
+  }
+  const int tiles = ((sh.M + 127) / 128) * (sh.Cout / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, kConvThreads, L::TOTAL, s>>>(x, mw, sh, ep);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+// ---- pooling / layout kernels (HBM-bound) -----------------------------------
+// NCHW fp32 image -> NHWC bf16 with channels zero-padded to cpad.
+__global__ void nchw_to_nhwc_pad(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                 int N, int C, int H, int W, int cpad) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pixel
+  if (p >= (int64_t)N * H * W) return;
+  const int n = p / (H * W);
+  const int hw = p - (int64_t)n * H * W;
+  __align__(16) __nv_bfloat16 v[8];
+  for (int c0 = 0; c0 < cpad; c0 += 8) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int c = c0 + e;
+      v[e] = __float2bfloat16_rn(c < C ? __ldg(in + ((int64_t)n * C + c) * H * W + hw) : 0.0f);
+    }
+    *reinterpret_cast<uint4*>(out + p * cpad + c0) = *reinterpret_cast<uint4*>(v);
+  }
+}
+
+// 3x3 stride-2 pad-1 max pool, NHWC, 8 channels per thread.
+__global__ void maxpool3x3s2(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                             int N, int H, int W, int C, int Ho, int Wo) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int cg = C / 8;
+  if (idx >= (int64_t)N * Ho * Wo * cg) return;
+  const int c0 = (idx % cg) * 8;
+  const int64_t p = idx / cg;
+  const int wo = p % Wo, ho = (p / Wo) % Ho, n = p / ((int64_t)Wo * Ho);
+  float m[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) m[e] = -INFINITY;
+  for (int r = 0; r < 3; ++r) {
+    const int hi = ho * 2 - 1 + r;
+    if (hi < 0 || hi >= H) continue;
+    for (int s = 0; s < 3; ++s) {
+      const int wi = wo * 2 - 1 + s;
+      if (wi < 0 || wi >= W) continue;
+      const uint4 u = __ldg(reinterpret_cast<const uint4*>(in + (((int64_t)n * H + hi) * W + wi) * C + c0));
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h2[e]);
+        m[2 * e] = fmaxf(m[2 * e], f.x);
+        m[2 * e + 1] = fmaxf(m[2 * e + 1], f.y);
+      }
+    }
+  }
+  uint4 u;
+  u.x = pack_bf16(m[0], m[1]);
+  u.y = pack_bf16(m[2], m[3]);
+  u.z = pack_bf16(m[4], m[5]);
+  u.w = pack_bf16(m[6], m[7]);
+  *reinterpret_cast<uint4*>(out + p * C + c0) = u;
+}
+
+// Global average pool NHWC [N, HW, C] -> [N, C] bf16 (fp32 sum), one thread per (n, 8 channels).
+__global__ void avgpool_global(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                               int N, int HW, int C) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cg = C / 8;
+  if (idx >= N * cg) return;
+  const int n = idx / cg, c0 = (idx % cg) * 8;
+  float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int p = 0; p < HW; ++p) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(in + ((int64_t)n * HW + p) * C + c0));
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h2[e]);
+      s[2 * e] += f.x;
+      s[2 * e + 1] += f.y;
+    }
+  }
+  const float inv = 1.0f / HW;
+  uint4 u;
+  u.x = pack_bf16(s[0] * inv, s[1] * inv);
+  u.y = pack_bf16(s[2] * inv, s[3] * inv);
+  u.z = pack_bf16(s[4] * inv, s[5] * inv);
+  u.w = pack_bf16(s[6] * inv, s[7] * inv);
+  *reinterpret_cast<uint4*>(out + (int64_t)n * C + c0) = u;
+}
+
+}  // namespace gg
+
+using namespace gg;
+
+extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
+                         int32_t Cout, int32_t R, int32_t S, int32_t stride, int32_t pad,
+                         int32_t Kpad, const float* bias, const void* residual, int32_t relu,
+                         void* y, void* stream) {
+  if (!x || !w || !y || !bias || N <= 0 || H <= 0 || W <= 0 || R <= 0 || S <= 0 || stride <= 0)
+    return GG_ERR_INVALID_ARGUMENT;
+  if (C % 8 || Kpad % 64 || Kpad < R * S * C || Cout % 64) return GG_ERR_UNSUPPORTED;
+  ConvShape sh;
+  sh.N = N; sh.H = H; sh.W = W; sh.C = C; sh.Cout = Cout;
+  sh.R = R; sh.S = S; sh.stride = stride; sh.pad = pad; sh.Kpad = Kpad;
+  sh.Ho = (H + 2 * pad - R) / stride + 1;
+  sh.Wo = (W + 2 * pad - S) / stride + 1;
+  const int64_t M = (int64_t)N * sh.Ho * sh.Wo;
+  if (M > 0x7fffffff) return GG_ERR_UNSUPPORTED;
+  sh.M = (int)M;
+  ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
+             reinterpret_cast<const __nv_bfloat16*>(residual), relu};
+  const int bn = Cout >= 256 ? 256 : Cout;
+  CUtensorMap mw;
+  int rc = make_map_2d(&mw, w, Cout, Kpad, Kpad, bn);
+  if (rc) return rc;
+  cudaStream_t s = gg_stream(stream);
+  const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  switch (bn) {
+    case 256: return launch_conv<256, 4>(xb, mw, sh, ep, s);
+    case 128: return launch_conv<128, 6>(xb, mw, sh, ep, s);
+    case 64: return launch_conv<64, 8>(xb, mw, sh, ep, s);
+    default: return GG_ERR_UNSUPPORTED;
+  }
+}
+
+extern "C" int gg_nchw_to_nhwc(const float* x, int32_t N, int32_t C, int32_t H, int32_t W,
+                               int32_t cpad, void* y, void* stream) {
+  if (!x || !y || cpad % 8 || cpad < C) return GG_ERR_INVALID_ARGUMENT;
+  const int64_t pixels = (int64_t)N * H * W;
+  nchw_to_nhwc_pad<<<(unsigned)((pixels + 255) / 256), 256, 0, gg_stream(stream)>>>(
+      x, reinterpret_cast<__nv_bfloat16*>(y), N, C, H, W, cpad);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+extern "C" int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, void* y,
+                               void* stream) {
+  if (!x || !y || C % 8) return GG_ERR_INVALID_ARGUMENT;
+  const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
+  const int64_t work = (int64_t)N * Ho * Wo * (C / 8);
+  maxpool3x3s2<<<(unsigned)((work + 255) / 256), 256, 0, gg_stream(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, H, W, C,
+      Ho, Wo);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+extern "C" int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y, void* stream) {
+  if (!x || !y || C % 8) return GG_ERR_INVALID_ARGUMENT;
+  const int work = N * (C / 8);
+  avgpool_global<<<(work + 127) / 128, 128, 0, gg_stream(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, HW, C);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}

@@ -21,13 +21,19 @@ using namespace tc;
 
 enum : int { ACT_NONE = 0, ACT_RELU = 1, ACT_GELU = 2 };
 
+enum : int { OUT_BF16 = 0, OUT_F32 = 1, OUT_QKV_HEADS = 2 };
+
 struct GemmEpilogue {
-  __nv_bfloat16* D;
+  void* D;
   int64_t ldd;
   const float* bias;               // [N] or null
   const __nv_bfloat16* residual;   // [M, ldr] or null
   int64_t ldr;
   int act;
+  int out_mode;                    // OUT_*
+  int seq_len;                     // OUT_QKV_HEADS: tokens per sequence (S)
+  int heads;                       // OUT_QKV_HEADS: H (head dim fixed at 64)
+  int64_t qkv_plane;               // OUT_QKV_HEADS: elements per Q/K/V^T plane (B*H*S*64)
 };
 
 constexpr int kBK = 64;            // 64 bf16 = 128 B = one swizzle row
@@ -179,7 +185,35 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
         }
-        uint4* dp = reinterpret_cast<uint4*>(ep.D + (int64_t)row * ep.ldd + col0);
+        if (ep.out_mode == OUT_F32) {
+          float4* dp = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.D) + (int64_t)row * ep.ldd + col0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) dp[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          continue;
+        }
+        __nv_bfloat16* dst;
+        if (ep.out_mode == OUT_QKV_HEADS) {
+          // [M, 3*H*64] -> Q (pre-scaled by 1/sqrt(64), exact), K as [B,H,S,64]; V^T as [B,H,64,S]
+          const int hd = ep.heads * 64;
+          const int which = col0 / hd, h = (col0 % hd) / 64, d0 = col0 % 64;
+          const int b = row / ep.seq_len, s_ = row % ep.seq_len;
+          __nv_bfloat16* plane = reinterpret_cast<__nv_bfloat16*>(ep.D) + which * ep.qkv_plane;
+          const int64_t bh = (int64_t)b * ep.heads + h;
+          if (which == 2) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              plane[(bh * 64 + d0 + i) * ep.seq_len + s_] = __float2bfloat16_rn(v[i]);
+            continue;
+          }
+          if (which == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= 0.125f;
+          }
+          dst = plane + (bh * ep.seq_len + s_) * 64 + d0;
+        } else {
+          dst = reinterpret_cast<__nv_bfloat16*>(ep.D) + (int64_t)row * ep.ldd + col0;
+        }
+        uint4* dp = reinterpret_cast<uint4*>(dst);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint4 u;
@@ -266,26 +300,40 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
 
 using namespace gg;
 
-extern "C" int gg_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
-                            int64_t ldd, int64_t M, int64_t N, int64_t K, const float* bias,
-                            const void* residual, int64_t ldr, int32_t act, int32_t tile_n,
-                            void* stream) {
-  if (!A || !B || !D || M <= 0 || N <= 0 || K <= 0) return GG_ERR_INVALID_ARGUMENT;
-  if (K % 64 || N % 32 || lda % 8 || ldb % 8 || ldd % 8 || (residual && ldr % 8)) return GG_ERR_INVALID_ARGUMENT;
-  if (act < 0 || act > 2) return GG_ERR_INVALID_ARGUMENT;
-  int bn = tile_n > 0 ? tile_n : (N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64));
+extern "C" int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
+                       int64_t ldd, int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* e,
+                       void* stream) {
+  if (!A || !B || !D || !e || M <= 0 || N <= 0 || K <= 0) return GG_ERR_INVALID_ARGUMENT;
+  if (K % 64 || N % 32 || lda % 8 || ldb % 8 || (e->residual && e->ldr % 8)) return GG_ERR_INVALID_ARGUMENT;
+  if (e->act < 0 || e->act > 2 || e->out_mode < 0 || e->out_mode > 2) return GG_ERR_INVALID_ARGUMENT;
+  if (e->out_mode == OUT_BF16 && ldd % 8) return GG_ERR_INVALID_ARGUMENT;
+  if (e->out_mode == OUT_F32 && ldd % 4) return GG_ERR_INVALID_ARGUMENT;
+  if (e->out_mode == OUT_QKV_HEADS &&
+      (e->seq_len <= 0 || e->heads <= 0 || N != 3 * 64 * (int64_t)e->heads || M % e->seq_len ||
+       e->seq_len % 128))
+    return GG_ERR_INVALID_ARGUMENT;
+  int bn = e->tile_n > 0 ? e->tile_n : (N % 256 == 0 ? 256 : (N % 128 == 0 ? 128 : 64));
   if (bn != 64 && bn != 128 && bn != 256) return GG_ERR_INVALID_ARGUMENT;
   CUtensorMap ma, mb;
   int rc = make_map_2d(&ma, A, M, K, lda, 128);
   if (rc) return rc;
   rc = make_map_2d(&mb, B, N, K, ldb, bn);
   if (rc) return rc;
-  GemmEpilogue ep{reinterpret_cast<__nv_bfloat16*>(D), ldd, bias,
-                  reinterpret_cast<const __nv_bfloat16*>(residual), ldr, act};
+  GemmEpilogue ep{D, ldd, e->bias, reinterpret_cast<const __nv_bfloat16*>(e->residual), e->ldr,
+                  e->act, e->out_mode, e->seq_len, e->heads,
+                  e->out_mode == OUT_QKV_HEADS ? M * 64 * (int64_t)e->heads : 0};
   cudaStream_t s = gg_stream(stream);
   switch (bn) {
     case 256: return launch_gemm<128, 256, 4>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
     case 128: return launch_gemm<128, 128, 6>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
     default: return launch_gemm<128, 64, 8>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
   }
+}
+
+extern "C" int gg_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
+                            int64_t ldd, int64_t M, int64_t N, int64_t K, const float* bias,
+                            const void* residual, int64_t ldr, int32_t act, int32_t tile_n,
+                            void* stream) {
+  gg_gemm_epilogue e{bias, residual, ldr, act, OUT_BF16, 0, 0, tile_n, 0};
+  return gg_gemm(A, lda, B, ldb, D, ldd, M, N, K, &e, stream);
 }

@@ -1,0 +1,162 @@
+"""ResNet-18 (torchvision architecture, 224x224) forward on sm_100a, NHWC bf16.
+
+Every convolution is one implicit-GEMM tcgen05 kernel (gg_conv2d) with the
+eval-mode BatchNorm folded into its weights/bias and the residual add + ReLU
+fused into the epilogue; the 1x1 stride-2 downsample is a conv of the same
+kernel.  Stem/head: gg_nchw_to_nhwc (fp32 NCHW -> bf16 NHWC, channels padded
+to 8), gg_maxpool3x3s2, gg_avgpool, and the fc layer on gg_gemm with fp32
+logits for the K3 epilogue.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _native
+from .distilbert import OUT_F32, gemm
+
+
+def _fold(conv, bn, cpad: int):
+    """BN(conv(x)) == conv'(x) + b' in eval mode; weights -> [Cout, Kpad] (r, s, c) order."""
+    import torch
+
+    w = conv.weight.detach().float()
+    cout, cin, R, S = w.shape
+    scale = bn.weight.detach().float() / torch.sqrt(bn.running_var.detach().float() + bn.eps)
+    bias = bn.bias.detach().float() - bn.running_mean.detach().float() * scale
+    w = w * scale[:, None, None, None]
+    wp = torch.zeros((cout, R, S, cpad), dtype=torch.float32)
+    wp[:, :, :, :cin] = w.permute(0, 2, 3, 1).cpu()
+    k = R * S * cpad
+    kpad = (k + 63) // 64 * 64
+    out = torch.zeros((cout, kpad), dtype=torch.float32)
+    out[:, :k] = wp.reshape(cout, k)
+    return out, bias.cpu(), kpad
+
+
+class _Conv:
+    def __init__(self, conv, bn, cpad, device):
+        import torch
+        w, b, self.kpad = _fold(conv, bn, cpad)
+        self.w = w.to(device=device, dtype=torch.bfloat16).contiguous()
+        self.b = b.to(device=device).contiguous()
+        self.cout = w.shape[0]
+        self.cin = cpad
+        self.r, self.s = conv.kernel_size
+        self.stride = conv.stride[0]
+        self.pad = conv.padding[0]
+
+    def out_hw(self, h, w):
+        return ((h + 2 * self.pad - self.r) // self.stride + 1,
+                (w + 2 * self.pad - self.s) // self.stride + 1)
+
+    def __call__(self, lib, x, n, h, w, y, st, residual=None, relu=True):
+        _native.check("gg_conv2d", lib.gg_conv2d(
+            C.c_void_p(x), n, h, w, self.cin, _native.ptr(self.w), self.cout, self.r, self.s,
+            self.stride, self.pad, self.kpad, _native.ptr(self.b),
+            None if residual is None else C.c_void_p(residual), int(relu), C.c_void_p(y), st))
+        return self.out_hw(h, w)
+
+    def flops(self, n, h, w):
+        ho, wo = self.out_hw(h, w)
+        real_cin = self.cin if self.cin != 8 else 3
+        return 2.0 * n * ho * wo * self.cout * self.r * self.s * real_cin
+
+
+class ResNet18B200:
+    """Packed (BN-folded) weights + NHWC activation buffers for up to max_batch images."""
+
+    def __init__(self, tv_model, max_batch: int = 64, image: int = 224, device="cuda"):
+        torch = _native.require_cuda()
+        self.lib = _native.load()
+        self.device = torch.device(device)
+        self.max_batch, self.image = max_batch, image
+        m = tv_model.eval()
+        self.stem = _Conv(m.conv1, m.bn1, 8, self.device)
+        self.blocks = []
+        cin = 64
+        for layer in (m.layer1, m.layer2, m.layer3, m.layer4):
+            for blk in layer:
+                cout = blk.conv1.out_channels
+                ds = None
+                if blk.downsample is not None:
+                    ds = _Conv(blk.downsample[0], blk.downsample[1], cin, self.device)
+                self.blocks.append((_Conv(blk.conv1, blk.bn1, cin, self.device),
+                                    _Conv(blk.conv2, blk.bn2, cout, self.device), ds))
+                cin = cout
+        self.num_classes = m.fc.out_features
+        npad = (self.num_classes + 31) // 32 * 32
+        wfc = torch.zeros((npad, m.fc.in_features), dtype=torch.float32)
+        wfc[: self.num_classes] = m.fc.weight.detach().float().cpu()
+        bfc = torch.zeros(npad, dtype=torch.float32)
+        bfc[: self.num_classes] = m.fc.bias.detach().float().cpu()
+        self.w_fc = wfc.to(self.device, torch.bfloat16).contiguous()
+        self.b_fc = bfc.to(self.device).contiguous()
+        B, H = max_batch, image
+        z = dict(dtype=torch.bfloat16, device=self.device)
+        self.x8 = torch.empty(B * H * H * 8, **z)
+        big = B * (H // 2) * (H // 2) * 64
+        self.buf = [torch.empty(big, **z) for _ in range(3)]
+        self.pooled = torch.empty((B, 512), **z)
+        self.logits = torch.empty((B, npad), dtype=torch.float32, device=self.device)
+
+    def flops(self, batch: int) -> float:
+        """Algorithmic FLOPs (3.628 GF/img at 224x224)."""
+        n, h = batch, self.image
+        f = self.stem.flops(n, h, h)
+        h = h // 4
+        for c1, c2, ds in self.blocks:
+            f += c1.flops(n, h, h)
+            h2, _ = c1.out_hw(h, h)
+            f += c2.flops(n, h2, h2)
+            if ds is not None:
+                f += ds.flops(n, h, h)
+            h = h2
+        f += 2.0 * n * 512 * self.num_classes
+        return f
+
+    def forward(self, images, batch: int | None = None, stream=None):
+        """images: CUDA fp32 NCHW [B, 3, 224, 224].  Returns fp32 logits [B, 1000] (view)."""
+        lib = self.lib
+        B = int(images.shape[0]) if batch is None else int(batch)
+        assert B <= self.max_batch
+        H = self.image
+        st = _native.stream_ptr(stream)
+        _native.check("gg_nchw_to_nhwc", lib.gg_nchw_to_nhwc(
+            _native.ptr(images), B, 3, H, H, 8, _native.ptr(self.x8), st))
+        a, b, c = (t.data_ptr() for t in self.buf)
+        h, w = self.stem(lib, self.x8.data_ptr(), B, H, H, a, st)           # 112x112x64
+        _native.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(C.c_void_p(a), B, h, w, 64,
+                                                            C.c_void_p(b), st))
+        h, w = (h + 1) // 2, (w + 1) // 2                                      # 56x56x64
+        cur, free = b, [a, c]
+        for conv1, conv2, ds in self.blocks:
+            t1 = free[0]
+            h2, w2 = conv1(lib, cur, B, h, w, t1, st, relu=True)
+            if ds is not None:
+                # identity branch = 1x1/2 conv + BN; the block input is dead afterwards
+                t2 = free[1]
+                ds(lib, cur, B, h, w, t2, st, relu=False)
+                conv2(lib, t1, B, h2, w2, cur, st, residual=t2, relu=True)
+                free = [t1, t2]
+            else:
+                out = free[1]
+                conv2(lib, t1, B, h2, w2, out, st, residual=cur, relu=True)
+                free = [cur, t1]
+                cur = out
+            h, w = h2, w2
+        _native.check("gg_avgpool", lib.gg_avgpool(C.c_void_p(cur), B, h * w, 512,
+                                                   _native.ptr(self.pooled), st))
+        gemm(lib, self.pooled.data_ptr(), 512, self.w_fc, self.logits.data_ptr(),
+             self.logits.stride(0), B, self.w_fc.shape[0], 512, st, bias=self.b_fc,
+             out_mode=OUT_F32, tile_n=64)
+        return self.logits[:B, : self.num_classes]
+
+
+def random_model(seed: int = 0):
+    """Seeded random-init torchvision ResNet-18 (no pretrained weights offline)."""
+    import torch
+    import torchvision
+
+    torch.manual_seed(seed)
+    return torchvision.models.resnet18(weights=None).eval()

@@ -1,0 +1,79 @@
+"""DistilBERT forward (tcgen05 GEMMs + attention + LN) vs transformers eager fp32.
+
+Tolerance: the north star's 2e-2 for the bf16 path, on the logits; the
+attention and LayerNorm kernels are also checked alone against fp32 torch.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    from paper_2601_04250_b200 import _native
+    return torch, _native, _native.load()
+
+
+def test_attention_kernel(env):
+    torch, nat, lib = env
+    B, H, S, D = 3, 12, 128, 64
+    g = torch.Generator(device="cuda").manual_seed(0)
+    q = torch.randn((B, H, S, D), device="cuda", generator=g)
+    k = torch.randn((B, H, S, D), device="cuda", generator=g)
+    v = torch.randn((B, H, S, D), device="cuda", generator=g)
+    mask = torch.ones((B, S), dtype=torch.int32, device="cuda")
+    mask[1, 100:] = 0
+    qkv = torch.empty(3 * B * H * S * D, dtype=torch.bfloat16, device="cuda")
+    plane = B * H * S * D
+    qb, kb, vb = q.to(torch.bfloat16), k.to(torch.bfloat16), v.to(torch.bfloat16)
+    qkv[:plane] = qb.flatten()
+    qkv[plane:2 * plane] = kb.flatten()
+    qkv[2 * plane:] = vb.transpose(2, 3).contiguous().flatten()
+    ctx = torch.empty((B * S, H * D), dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_attention", lib.gg_attention(nat.ptr(qkv), nat.ptr(mask), nat.ptr(ctx), H * D,
+                                               B, H, S, nat.stream_ptr()))
+    s = qb.float() @ kb.float().transpose(2, 3)
+    s = s.masked_fill(mask[:, None, None, :] == 0, float("-inf"))
+    ref = torch.softmax(s, dim=-1) @ vb.float()
+    ref = ref.transpose(1, 2).reshape(B * S, H * D)
+    err = (ctx.float() - ref).abs().max().item()
+    assert err < 2e-2, err
+
+
+def test_layernorm_kernel(env):
+    torch, nat, lib = env
+    x = torch.randn((1000, 768), device="cuda").to(torch.bfloat16)
+    gmm = torch.randn(768, device="cuda")
+    bta = torch.randn(768, device="cuda")
+    y = torch.empty_like(x)
+    nat.check("gg_layernorm", lib.gg_layernorm(nat.ptr(x), 768, nat.ptr(y), 768, nat.ptr(gmm),
+                                               nat.ptr(bta), 1000, 768, C.c_float(1e-12),
+                                               nat.stream_ptr()))
+    ref = torch.nn.functional.layer_norm(x.float(), (768,), gmm, bta, 1e-12)
+    # bf16 output: one rounding of |y| (half an ulp = 2^-9 relative) plus fp32 statistics
+    assert ((y.float() - ref).abs() <= 4e-3 * ref.abs() + 1e-2).all()
+
+
+@pytest.mark.parametrize("batch", [4, 128])
+def test_distilbert_logits_vs_eager(env, batch):
+    torch = env[0]
+    from paper_2601_04250_b200.distilbert import DistilBertB200, random_model
+    model = random_model(0)
+    ids = torch.randint(0, model.config.vocab_size, (batch, 128), generator=torch.Generator().manual_seed(1))
+    mask = torch.ones((batch, 128), dtype=torch.int64)
+    if batch > 2:
+        mask[2, 64:] = 0
+    with torch.no_grad():
+        ref = model.cuda()(input_ids=ids.cuda(), attention_mask=mask.cuda()).logits.float()
+    net = DistilBertB200(model, max_batch=batch)
+    out = net.forward(ids.to(torch.int32).cuda(), mask.to(torch.int32).cuda())
+    torch.cuda.synchronize()
+    err = (out - ref).abs().max().item()
+    print(f"distilbert b={batch}: max |logit err| = {err:.3e}, |ref| max {ref.abs().max().item():.3f}")
+    assert err <= 2e-2, err

@@ -1,0 +1,84 @@
+"""ResNet-18 forward (implicit-GEMM tcgen05 convs) vs torchvision eager fp32.
+
+Tolerance: the north star's bf16 2e-2, applied to the logits relative to their
+scale (random-init ResNet-18 logits are O(1..10); bf16 activations through 20
+convs carry ~1e-2 relative error).  Single convolutions are checked against
+torch's fp32 conv2d on the same bf16 inputs.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    from paper_2601_04250_b200 import _native
+    return torch, _native, _native.load()
+
+
+@pytest.mark.parametrize("n,h,cin,cout,r,stride,pad,res", [
+    (2, 56, 64, 64, 3, 1, 1, True), (2, 56, 64, 128, 3, 2, 1, False), (2, 56, 64, 128, 1, 2, 0, False),
+    (1, 14, 256, 512, 3, 2, 1, False), (1, 7, 512, 512, 3, 1, 1, True), (2, 30, 8, 64, 7, 2, 3, False),
+    (3, 28, 128, 256, 3, 1, 1, True)])
+def test_conv_vs_torch(env, n, h, cin, cout, r, stride, pad, res):
+    torch, nat, lib = env
+    g = torch.Generator(device="cuda").manual_seed(n * h + cin)
+    x = torch.randn((n, cin, h, h), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((cout, cin, r, r), device="cuda", generator=g) / (cin * r * r) ** 0.5).to(torch.bfloat16)
+    b = torch.randn(cout, device="cuda", generator=g)
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=stride, padding=pad)
+    ho = ref.shape[2]
+    resid = torch.randn((n, ho, ho, cout), device="cuda", generator=g).to(torch.bfloat16) if res else None
+    if res:
+        ref = ref + resid.float().permute(0, 3, 1, 2)
+    ref = torch.relu(ref)
+    k = r * r * cin
+    kpad = (k + 63) // 64 * 64
+    wk = torch.zeros((cout, kpad), dtype=torch.bfloat16, device="cuda")
+    wk[:, :k] = w.permute(0, 2, 3, 1).reshape(cout, k)
+    xn = x.permute(0, 2, 3, 1).contiguous()
+    y = torch.empty((n, ho, ho, cout), dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_conv2d", lib.gg_conv2d(nat.ptr(xn), n, h, h, cin, nat.ptr(wk), cout, r, r, stride,
+                                         pad, kpad, nat.ptr(b), nat.ptr(resid), 1, nat.ptr(y),
+                                         nat.stream_ptr()))
+    got = y.float().permute(0, 3, 1, 2)
+    err = (got - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
+def test_pools(env):
+    torch, nat, lib = env
+    x = torch.randn((2, 64, 112, 112), device="cuda").to(torch.bfloat16)
+    xn = x.permute(0, 2, 3, 1).contiguous()
+    y = torch.empty((2, 56, 56, 64), dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(nat.ptr(xn), 2, 112, 112, 64, nat.ptr(y),
+                                                     nat.stream_ptr()))
+    ref = torch.nn.functional.max_pool2d(x.float(), 3, 2, 1)
+    assert torch.equal(y.float().permute(0, 3, 1, 2), ref)
+    z = torch.empty((2, 64), dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_avgpool", lib.gg_avgpool(nat.ptr(y), 2, 56 * 56, 64, nat.ptr(z), nat.stream_ptr()))
+    assert (z.float() - ref.mean(dim=(2, 3))).abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("batch", [2, 64])
+def test_resnet18_logits_vs_eager(env, batch):
+    torch = env[0]
+    from paper_2601_04250_b200.resnet18 import ResNet18B200, random_model
+    model = random_model(0)
+    x = torch.randn((batch, 3, 224, 224), generator=torch.Generator().manual_seed(1))
+    with torch.no_grad():
+        ref = model.cuda()(x.cuda()).float()
+    net = ResNet18B200(model, max_batch=batch)
+    out = net.forward(x.cuda())
+    torch.cuda.synchronize()
+    scale = ref.abs().max().item()
+    err = (out - ref).abs().max().item()
+    print(f"resnet18 b={batch}: max |logit err| = {err:.3e}, logit scale {scale:.3f}, "
+          f"argmax agree {(out.argmax(1) == ref.argmax(1)).float().mean().item():.3f}")
+    assert err <= 2e-2 * max(1.0, scale), err
