@@ -127,6 +127,10 @@ typedef struct {
   int64_t first_invalid;     /* -1 when every row is valid */
   double energy;             /* E(x), identical for every valid row of the batch */
   double congestion;         /* C(x), identical for every valid row of the batch */
+  int64_t n_decided;         /* rows decided by this launch */
+  int64_t snap_queue_depth;  /* the snapshot the batch was decided against */
+  double snap_p95_ms;
+  double snap_batch_fill;
 } gg_batch_info;
 
 /* ---- library identity ---------------------------------------------------- */
@@ -193,6 +197,76 @@ int gg_set_queue_depth(gg_state* state_dev, int32_t queue_depth, void* stream);
 int gg_epilogue(const float* logits_dev, int64_t n, int32_t k, int64_t ld,
                 int32_t utility_proxy, double* probs_dev, int32_t* argmax_dev,
                 double* confidence_dev, double* utility_dev, void* stream);
+
+/* ---- serving loop: device FIFO between admission and the forward --------- */
+/* The admitted requests of every admission window are appended (in trace
+ * order) to a device ring; each forward step pops up to batch_cap of them.
+ * The ring depth is the queue depth of the congestion snapshot and
+ * depth / batch_cap its batch fill (servesim.py:208-220 semantics), so the
+ * whole closed loop runs without a host round-trip. */
+typedef struct {
+  int64_t head;         /* requests popped into forward batches */
+  int64_t tail;         /* requests admitted */
+  int64_t capacity;     /* ring slots, power of two */
+  int64_t batch_cap;    /* forward batch size B */
+  int64_t cursor;       /* next trace row to decide */
+  int64_t trace_len;    /* rows of the resident trace */
+  int64_t extra_depth;  /* queue depth of the other ranks (multi-GPU exchange) */
+  int64_t overflow;     /* admissions lost to a full ring (must stay 0) */
+} gg_fifo;
+
+/* Stream form of gg_admit: decides rows [fifo.cursor, fifo.cursor + window)
+ * of a device-resident trace (probs [trace_len, row_stride], now [trace_len]),
+ * writes decision_dev[row] (trace indexed), appends admitted rows to the ring
+ * (ids + admission timestamps), advances cursor/tail.  snapshot_dev NULL ->
+ * snapshot from the FIFO: queue_depth = tail - head + extra_depth, p95 from
+ * state, batch_fill = min(1, (tail - head) / batch_cap). */
+int gg_admit_stream(const gg_params* params, gg_state* state_dev, gg_fifo* fifo_dev,
+                    int32_t* ring_ids_dev, uint64_t* ring_ns_dev, const double* probs_dev,
+                    int32_t k, int64_t row_stride, const double* now_dev, int64_t window,
+                    const gg_snapshot* snapshot_dev, uint8_t* decision_dev,
+                    gg_batch_info* info_dev, void* workspace_dev, size_t workspace_bytes,
+                    void* stream);
+/* Pops n = min(B, depth) requests: batch_ids[0..n) (trace rows), batch_ns,
+ * *count_dev = n. */
+int gg_fifo_pop(gg_fifo* fifo_dev, const int32_t* ring_ids_dev, const uint64_t* ring_ns_dev,
+                int32_t* batch_ids_dev, uint64_t* batch_ns_dev, int32_t* count_dev, int32_t B,
+                void* stream);
+/* Outcome model of a served batch (servesim.py:137-139, 303-305 for the
+ * modeled path; %globaltimer latency for the measured path). */
+typedef struct {
+  double batch_base_ms, per_item_ms;        /* modeled latency = base + per_item * n */
+  double batch_base_energy_j, per_item_energy_j;  /* joules each = (base + per_item*n)/n */
+  int32_t measured_latency;                 /* 1: latency = now - admission time */
+  int32_t reserved;
+} gg_outcome_model;
+/* Writes one rank's step into its exchange slot (fp64, GG_SLOT_LEN(B) values):
+ *   [0, B)      latency_ms of the served requests
+ *   [B, 2B)     joules
+ *   [2B, 3B)    queue depth reported with each outcome
+ *   3B + 0..7   n_served, fifo depth after the pop, and the admission effects
+ *               of this step (n_decided, n_invalid, n_admitted, n_skipped,
+ *               snapshot queue depth, snapshot p95) copied from info_dev. */
+#define GG_SLOT_LEN(B) (3 * (B) + 8)
+int gg_served_outcomes(const gg_fifo* fifo_dev, const int32_t* count_dev,
+                       const uint64_t* batch_ns_dev, const gg_outcome_model* model,
+                       const gg_batch_info* info_dev, double* slot_dev, int32_t B, void* stream);
+/* Applies G exchange slots (all-reduced) to this rank's replica: first the
+ * other ranks' admission effects (normalizer observes of their snapshots,
+ * counters), then every rank's outcomes in rank order (K2, record_outcome
+ * semantics); sets fifo.extra_depth = sum of the other ranks' depths.  Every
+ * rank applies the same slots, so replicas stay bit-identical. */
+int gg_outcome_slots(const gg_params* params, gg_state* state_dev, const double* slots_dev,
+                     int32_t G, int32_t B, int32_t rank, gg_fifo* fifo_dev,
+                     int64_t* error_index_dev, void* stream);
+/* K3 for a served batch: logits [B, ld] fp32 (first *count_dev rows valid) ->
+ * predicted[batch_ids[i]] (first max), confidence[batch_ids[i]] (fp64 max p),
+ * optionally fp64 probabilities [B, k] and batch-local copies
+ * batch_predicted[i] / batch_confidence[i] (for a compact device->host read). */
+int gg_epilogue_served(const float* logits_dev, const int32_t* count_dev, int32_t B, int32_t k,
+                       int64_t ld, const int32_t* batch_ids_dev, int32_t* predicted_dev,
+                       double* confidence_dev, double* probs_dev, int32_t* batch_predicted_dev,
+                       double* batch_confidence_dev, void* stream);
 
 /* ---- stateless batch forms of the controller's pure functions ------------- */
 /* entropy_utility / one_minus_confidence_utility (controller.py:138-148) over

@@ -9,6 +9,11 @@
  * greengate_b200.h: device pointers owned by the caller, stream-ordered,
  * gg_status return codes.  All tensors are bf16 unless noted; activations are
  * row-major [tokens, features] (DistilBERT) or NHWC (ResNet-18).
+ *
+ * Dynamic batch: every kernel that takes `count_dev` reads the number of
+ * valid items (sequences / images) from device memory at launch, so a
+ * captured CUDA graph serves whatever the admission step admitted without a
+ * host round-trip.  NULL = use the host-side size.
  */
 #ifndef GREENGATE_B200_FORWARD_H
 #define GREENGATE_B200_FORWARD_H
@@ -46,7 +51,8 @@ typedef struct {
   int32_t seq_len;       /* GG_OUT_QKV_HEADS: S (multiple of 128) */
   int32_t heads;         /* GG_OUT_QKV_HEADS: H, N == 3 * H * 64 */
   int32_t tile_n;        /* 0 = auto, 64 / 128 / 256 */
-  int32_t reserved;
+  int32_t rows_per_item; /* dynamic batch: rows = min(M, *count_dev * rows_per_item) */
+  const int32_t* count_dev; /* device item count written by an earlier kernel, or NULL */
 } gg_gemm_epilogue;
 int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
             int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* epilogue, void* stream);
@@ -57,17 +63,24 @@ int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int
  * [B, S] (0 = masked key, DistilBERT's masked_fill with finfo.min) or NULL.
  * Requires S == 128. */
 int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int64_t ldc, int32_t batch,
-                 int32_t heads, int32_t seq_len, void* stream);
+                 int32_t heads, int32_t seq_len, const int32_t* count_dev, void* stream);
 
 /* y = LayerNorm(x) * gamma + beta over rows of width `width` (fp32 statistics),
  * bf16 in/out; eps as in the model config (DistilBERT 1e-12). */
 int gg_layernorm(const void* x, int64_t ldx, void* y, int64_t ldy, const float* gamma,
-                 const float* beta, int64_t rows, int32_t width, float eps, void* stream);
+                 const float* beta, int64_t rows, int32_t width, float eps,
+                 const int32_t* count_dev, int32_t rows_per_item, void* stream);
 
 /* DistilBERT embeddings: y[t] = LayerNorm(word[ids[t]] + pos[t % seq_len]) (bf16 tables). */
 int gg_embed_layernorm(const int32_t* ids, const void* word, const void* pos, void* y,
                        const float* gamma, const float* beta, int64_t tokens, int32_t seq_len,
-                       int32_t width, float eps, void* stream);
+                       int32_t width, float eps, const int32_t* count_dev, void* stream);
+
+/* Gathers the token ids (and attention masks) of a served batch from a
+ * resident request pool: ids[i, :] = pool_ids[batch_ids[i] % pool_size, :]. */
+int gg_token_gather(const int32_t* pool_ids, const int32_t* pool_mask, int64_t pool_size,
+                    const int32_t* batch_ids, const int32_t* count_dev, int32_t B,
+                    int32_t seq_len, int32_t* ids, int32_t* mask, void* stream);
 
 /* ---- ResNet-18 (NHWC bf16) ------------------------------------------------ */
 /* Implicit-GEMM convolution on tcgen05: y[n,ho,wo,co] = relu?(sum_{r,s,c}
@@ -76,15 +89,23 @@ int gg_embed_layernorm(const int32_t* ids, const void* word, const void* pos, vo
  * multiple of 64 >= R*S*C (zero tail); C % 8 == 0, Cout % 64 == 0. */
 int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
               int32_t Cout, int32_t R, int32_t S, int32_t stride, int32_t pad, int32_t Kpad,
-              const float* bias, const void* residual, int32_t relu, void* y, void* stream);
+              const float* bias, const void* residual, int32_t relu, void* y,
+              const int32_t* count_dev, void* stream);
 /* fp32 NCHW image batch -> bf16 NHWC with channels zero-padded to cpad (% 8). */
 int gg_nchw_to_nhwc(const float* x, int32_t N, int32_t C, int32_t H, int32_t W, int32_t cpad,
                     void* y, void* stream);
+/* Served-batch stem input: image i of the batch = uint8 HWC image
+ * pool[batch_ids[i] % pool_size], normalized ((x/255 - mean[c]) / std[c]) into
+ * bf16 NHWC with 8 channels (3 real + 5 zero). */
+int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_ids,
+                   const int32_t* count_dev, int32_t B, int32_t H, int32_t W,
+                   const float* mean3, const float* std3, void* y, void* stream);
 /* 3x3 / stride 2 / pad 1 max pool (NHWC, C % 8 == 0). */
 int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, void* y,
-                    void* stream);
+                    const int32_t* count_dev, void* stream);
 /* Global average pool NHWC [N, HW, C] -> [N, C]. */
-int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y, void* stream);
+int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y,
+               const int32_t* count_dev, void* stream);
 
 #ifdef __cplusplus
 }

@@ -146,6 +146,8 @@ void ggo_admit(const gg_params* p, gg_state* s, const double* probs, long n, int
   if (info) {
     info->n_admitted = n_adm; info->n_skipped = n_skip; info->n_invalid = n_inv;
     info->first_invalid = first_bad; info->energy = e_last; info->congestion = c_last;
+    info->n_decided = n; info->snap_queue_depth = snap.queue_depth;
+    info->snap_p95_ms = snap.p95_latency_ms; info->snap_batch_fill = snap.batch_fill;
   }
 }
 

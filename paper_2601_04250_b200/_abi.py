@@ -63,7 +63,21 @@ class gg_snapshot(C.Structure):
 
 class gg_batch_info(C.Structure):
     _fields_ = [("n_admitted", C.c_int64), ("n_skipped", C.c_int64), ("n_invalid", C.c_int64),
-                ("first_invalid", C.c_int64), ("energy", C.c_double), ("congestion", C.c_double)]
+                ("first_invalid", C.c_int64), ("energy", C.c_double), ("congestion", C.c_double),
+                ("n_decided", C.c_int64), ("snap_queue_depth", C.c_int64),
+                ("snap_p95_ms", C.c_double), ("snap_batch_fill", C.c_double)]
+
+
+class gg_fifo(C.Structure):
+    _fields_ = [("head", C.c_int64), ("tail", C.c_int64), ("capacity", C.c_int64),
+                ("batch_cap", C.c_int64), ("cursor", C.c_int64), ("trace_len", C.c_int64),
+                ("extra_depth", C.c_int64), ("overflow", C.c_int64)]
+
+
+class gg_outcome_model(C.Structure):
+    _fields_ = [("batch_base_ms", C.c_double), ("per_item_ms", C.c_double),
+                ("batch_base_energy_j", C.c_double), ("per_item_energy_j", C.c_double),
+                ("measured_latency", C.c_int32), ("reserved", C.c_int32)]
 
 
 # Field offsets of gg_state used by the Python shim to read scalars out of the

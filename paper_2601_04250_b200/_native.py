@@ -40,14 +40,24 @@ SIGNATURES: dict[str, tuple] = {
     "gg_gemm_bf16": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I32,
                                _I32, _P]),
     "gg_gemm": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P]),
-    "gg_attention": (C.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, _P]),
-    "gg_layernorm": (C.c_int, [_P, _I64, _P, _I64, _P, _P, _I64, _I32, C.c_float, _P]),
-    "gg_embed_layernorm": (C.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, C.c_float, _P]),
+    "gg_attention": (C.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, _P, _P]),
+    "gg_layernorm": (C.c_int, [_P, _I64, _P, _I64, _P, _P, _I64, _I32, C.c_float, _P, _I32, _P]),
+    "gg_embed_layernorm": (C.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, C.c_float, _P,
+                                     _P]),
+    "gg_token_gather": (C.c_int, [_P, _P, _I64, _P, _P, _I32, _I32, _P, _P, _P]),
     "gg_conv2d": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32,
-                            _P, _P, _I32, _P, _P]),
+                            _P, _P, _I32, _P, _P, _P]),
     "gg_nchw_to_nhwc": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
-    "gg_maxpool3x3s2": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P]),
-    "gg_avgpool": (C.c_int, [_P, _I32, _I32, _I32, _P, _P]),
+    "gg_stem_gather": (C.c_int, [_P, _I64, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "gg_maxpool3x3s2": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P]),
+    "gg_avgpool": (C.c_int, [_P, _I32, _I32, _I32, _P, _P, _P]),
+    # serving loop (include/greengate_b200.h)
+    "gg_admit_stream": (C.c_int, [_P, _P, _P, _P, _P, _P, _I32, _I64, _P, _I64, _P, _P, _P, _P,
+                                  C.c_size_t, _P]),
+    "gg_fifo_pop": (C.c_int, [_P, _P, _P, _P, _P, _P, _I32, _P]),
+    "gg_served_outcomes": (C.c_int, [_P, _P, _P, _P, _P, _P, _I32, _P]),
+    "gg_outcome_slots": (C.c_int, [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
+    "gg_epilogue_served": (C.c_int, [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 
@@ -101,7 +111,12 @@ def require_cuda():
     return torch
 
 
+LAUNCHES = 0  # entry-point calls (each enqueues one kernel); bench.py counts a step with it
+
+
 def check(fn: str, code: int) -> None:
+    global LAUNCHES
+    LAUNCHES += 1
     if code != _abi.GG_OK:
         raise NativeError(fn, code)
 

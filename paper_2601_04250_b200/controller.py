@@ -475,8 +475,8 @@ class AdmissionController:
     def _io_buffer(self, k: int):
         if self._io_k != k:
             torch = _native.require_cuda()
-            self._io = torch.empty(8 * (k + 1) + 24 + 24 + 48 + 8, dtype=torch.uint8,
-                                   device=self.device)
+            self._io = torch.empty(8 * (k + 1) + 24 + 24 + _abi.BATCH_INFO_BYTES + 8,
+                                   dtype=torch.uint8, device=self.device)
             self._io_k = k
         return self._io
 
@@ -497,13 +497,13 @@ class AdmissionController:
         _native.check("gg_admit", self._lib.gg_admit(
             C.byref(self.params), _native.ptr(self.state), C.c_void_p(base), 1, k, k,
             C.c_void_p(base + 8 * k), C.c_void_p(base + o_snap) if snap is not None else None,
-            C.c_void_p(base + o_out + 72), C.c_void_p(base + o_out), None,
+            C.c_void_p(base + o_out + 24 + _abi.BATCH_INFO_BYTES), C.c_void_p(base + o_out), None,
             C.c_void_p(base + o_out + 24), _native.ptr(self._ws), self._ws.numel(),
             self._stream()))
         raw = bytes(io[o_out:].cpu().numpy().tobytes())
         bd = struct.unpack_from("<3d", raw, 0)
         info = _abi.gg_batch_info.from_buffer_copy(raw, 24)
-        code = raw[72]
+        code = raw[24 + _abi.BATCH_INFO_BYTES]
         if code == _abi.GG_DECISION_INVALID:
             if any(not math.isfinite(x) or x < 0.0 for x in xs):
                 raise InvalidDistribution(f"scores must be finite and >= 0: {xs}")

@@ -28,7 +28,8 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     attention_tcgen05(const __grid_constant__ CUtensorMap map_q,
                       const __grid_constant__ CUtensorMap map_k,
                       const __grid_constant__ CUtensorMap map_vt, const int32_t* mask,
-                      __nv_bfloat16* ctx, int64_t ldc, int heads) {
+                      __nv_bfloat16* ctx, int64_t ldc, int heads, const int32_t* count) {
+  if (count && (int)(blockIdx.x / heads) >= __ldg(count)) return;  // dynamic batch
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar_load = reinterpret_cast<uint64_t*>(smem + 81920);
@@ -161,7 +162,8 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
 using namespace gg;
 
 extern "C" int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int64_t ldc,
-                            int32_t batch, int32_t heads, int32_t seq_len, void* stream) {
+                            int32_t batch, int32_t heads, int32_t seq_len,
+                            const int32_t* count_dev, void* stream) {
   if (!qkv || !ctx || batch <= 0 || heads <= 0) return GG_ERR_INVALID_ARGUMENT;
   if (seq_len != kAttnS || ldc % 8 || ldc < (int64_t)heads * kAttnD) return GG_ERR_UNSUPPORTED;
   const int64_t plane = (int64_t)batch * heads * seq_len * kAttnD;
@@ -180,7 +182,7 @@ extern "C" int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int
     attr = true;
   }
   attention_tcgen05<<<batch * heads, kAttnThreads, kAttnSmem, gg_stream(stream)>>>(
-      mq, mk, mv, mask, reinterpret_cast<__nv_bfloat16*>(ctx), ldc, heads);
+      mq, mk, mv, mask, reinterpret_cast<__nv_bfloat16*>(ctx), ldc, heads, count_dev);
   GG_LAUNCH_OK();
   return GG_OK;
 }

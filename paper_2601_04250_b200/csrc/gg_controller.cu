@@ -76,7 +76,32 @@ struct AdmitArgs {
   gg_batch_info* info;
   AdmitWorkspace* ws;
   double ln_k;  // math.log(len(xs)) computed on the host with libm (controller.py:142)
+  // stream mode (serving loop): rows [fifo->cursor, +n) of a resident trace,
+  // admitted trace rows appended to the device FIFO ring.
+  gg_fifo* fifo;
+  int32_t* ring;
+  uint64_t* ring_ns;
 };
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Resolve the rows this launch decides: n rows starting at row0.  In stream
+// mode the window starts at the FIFO's trace cursor (read before any block
+// finishes; the last block advances it).
+__device__ __forceinline__ void admit_window(const AdmitArgs& a, int64_t& row0, int64_t& n) {
+  if (a.fifo) {
+    row0 = a.fifo->cursor;
+    const int64_t left = a.fifo->trace_len - row0;
+    n = left < a.n ? (left > 0 ? left : 0) : a.n;
+  } else {
+    row0 = 0;
+    n = a.n;
+  }
+}
 
 // Batch-constant part of decide() (controller.py:316-325).  Within one frozen
 // snapshot every valid request sees the same E and C: the first valid
@@ -89,7 +114,8 @@ struct BatchConst {
   int64_t samples_seen;
 };
 
-__device__ BatchConst batch_constants(const gg_state* st, const gg_snapshot* snap) {
+__device__ BatchConst batch_constants(const gg_state* st, const gg_snapshot* snap,
+                                      const gg_fifo* fifo) {
   BatchConst b;
   b.samples_seen = st->samples_seen;
   b.ewma = st->ewma_joules_per_request;
@@ -98,6 +124,12 @@ __device__ BatchConst batch_constants(const gg_state* st, const gg_snapshot* sna
     b.qd = snap->queue_depth;
     b.p95 = snap->p95_latency_ms;
     b.fill = snap->batch_fill;
+  } else if (fifo) {  // serving loop: the FIFO is the queue (servesim.py:208-220 semantics)
+    const int64_t depth = fifo->tail - fifo->head;
+    b.qd = depth + fifo->extra_depth;
+    b.p95 = st->p95_current;
+    const double f = f64_div((double)depth, (double)fifo->batch_cap);
+    b.fill = f < 1.0 ? f : 1.0;
   } else {  // default congestion source (controller.py:295-300; gateway.py:58-64)
     b.qd = st->queue_depth;
     b.p95 = st->p95_current;
@@ -160,6 +192,7 @@ struct AdmitShared {
   static constexpr int GROUPS = RPT * WARPS;
   static_assert(GROUPS <= 32, "one warp scans the groups");
   BatchConst bc;
+  int64_t row0, nw, depth0;   // window start/length; FIFO depth before this launch
   unsigned long long block_prefix;
   int group_cnt[GROUPS];
   int group_off[GROUPS];
@@ -179,6 +212,19 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
     v = t > v ? t : v;
   }
   return v;
+}
+
+// Per-block prologue (thread 0): virtual block id, decision window, FIFO depth
+// and the batch-constant E/C — all read before any block can finalize.
+template <int THREADS, int RPT>
+__device__ void block_setup(const AdmitArgs& a, AdmitShared<THREADS, RPT>& sm) {
+  sm.vb = (int)atomicAdd(&a.ws->vblock_counter, 1ull);
+  int64_t row0, nw;
+  admit_window(a, row0, nw);
+  sm.row0 = row0;
+  sm.nw = nw;
+  sm.depth0 = a.fifo ? a.fifo->tail - a.fifo->head : 0;
+  sm.bc = batch_constants(a.state, a.snap, a.fifo);
 }
 
 // Order-preserving compaction of the tile + counters + last-block finalize.
@@ -215,13 +261,24 @@ __device__ void finish_tile(const AdmitArgs& a, AdmitShared<THREADS, RPT>& sm, i
     if (lane == 0) sm.block_prefix = lookback(a.ws->status, sm.vb, (unsigned long long)total);
   }
   __syncthreads();
-  if (a.admitted_idx) {
+  if (a.admitted_idx || a.ring) {
 #pragma unroll
     for (int j = 0; j < RPT; ++j) {
       if ((ballots[j] >> lane) & 1u) {
         unsigned long long pos = sm.block_prefix + sm.group_off[j * WARPS + warp] +
                                  __popc(ballots[j] & ((1u << lane) - 1u));
-        a.admitted_idx[pos] = (int32_t)(tile0 + (int64_t)j * THREADS + tid);
+        const int64_t r = tile0 + (int64_t)j * THREADS + tid;
+        if (a.admitted_idx) a.admitted_idx[pos] = (int32_t)r;
+        if (a.ring) {  // enqueue in trace order behind the current FIFO tail
+          const int64_t cap = a.fifo->capacity;
+          if (sm.depth0 + (int64_t)pos < cap) {
+            const int64_t slot = (a.fifo->tail + (int64_t)pos) & (cap - 1);
+            a.ring[slot] = (int32_t)(sm.row0 + r);
+            if (a.ring_ns) a.ring_ns[slot] = globaltimer_ns();
+          } else {
+            atomicAdd(reinterpret_cast<unsigned long long*>(&a.fifo->overflow), 1ull);
+          }
+        }
       }
     }
   }
@@ -245,7 +302,7 @@ __device__ void finish_tile(const AdmitArgs& a, AdmitShared<THREADS, RPT>& sm, i
     unsigned long long benc = ld_relaxed(&a.ws->first_invalid_enc);
     gg_state* st = a.state;
     const BatchConst& b = sm.bc;
-    const bool any_valid = (a.n - n_inv) > 0;
+    const bool any_valid = (sm.nw - n_inv) > 0;
     if (any_valid) {
       if (b.samples_seen > 0) ch_observe(st->n_energy, b.ewma);
       ch_observe(st->n_queue_depth, (double)b.qd);
@@ -253,13 +310,22 @@ __device__ void finish_tile(const AdmitArgs& a, AdmitShared<THREADS, RPT>& sm, i
     }
     st->admitted_total += n_adm;
     st->skipped_total += n_skip;
+    if (a.fifo) {
+      const int64_t room = a.fifo->capacity - sm.depth0;
+      a.fifo->tail += n_adm < room ? n_adm : room;
+      a.fifo->cursor = sm.row0 + sm.nw;
+    }
     if (a.info) {
       a.info->n_admitted = n_adm;
       a.info->n_skipped = n_skip;
       a.info->n_invalid = n_inv;
-      a.info->first_invalid = benc ? (int64_t)(a.n - (int64_t)benc) : -1;
+      a.info->first_invalid = benc ? (int64_t)(sm.row0 + sm.nw - (int64_t)benc) : -1;
       a.info->energy = any_valid ? b.e : 0.0;
       a.info->congestion = any_valid ? b.c : 0.0;
+      a.info->n_decided = sm.nw;
+      a.info->snap_queue_depth = b.qd;
+      a.info->snap_p95_ms = b.p95;
+      a.info->snap_batch_fill = b.fill;
     }
     a.ws->vblock_counter = 0;
     a.ws->done_counter = 0;
@@ -277,13 +343,11 @@ template <int KC, int THREADS, int RPT>
 __global__ void __launch_bounds__(THREADS) admit_small_kernel(AdmitArgs a) {
   __shared__ AdmitShared<THREADS, RPT> sm;
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    sm.vb = (int)atomicAdd(&a.ws->vblock_counter, 1ull);
-    sm.bc = batch_constants(a.state, a.snap);
-  }
+  if (tid == 0) block_setup(a, sm);
   __syncthreads();
   const BatchConst b = sm.bc;
   const int64_t tile0 = (int64_t)sm.vb * THREADS * RPT;
+  const int64_t nw = sm.nw, row0 = sm.row0;
   const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
   const int k = KC > 0 ? KC : a.k;
   uint32_t ballots[RPT];
@@ -292,10 +356,11 @@ __global__ void __launch_bounds__(THREADS) admit_small_kernel(AdmitArgs a) {
 #pragma unroll
   for (int j = 0; j < RPT; ++j) {
     const int64_t r = tile0 + (int64_t)j * THREADS + tid;
-    const bool in = r < a.n;
+    const bool in = r < nw;
+    const int64_t g = row0 + r;  // trace row
     uint8_t code = GG_DECISION_SKIP;
     if (in) {
-      const double* row = a.probs + r * a.stride;
+      const double* row = a.probs + g * a.stride;
       RowAcc acc;
       if constexpr (KC == 2) {
         double2 v = *reinterpret_cast<const double2*>(row);
@@ -313,19 +378,19 @@ __global__ void __launch_bounds__(THREADS) admit_small_kernel(AdmitArgs a) {
       }
       double u, jv = 0.0, tau = 0.0;
       if (acc.finish(k, entropy, a.ln_k, u)) {
-        code = decide_row(a, b, u, a.now[r], jv, tau);
+        code = decide_row(a, b, u, a.now[g], jv, tau);
         if (code == GG_DECISION_SKIP) ++my_skip;
       } else {
         code = GG_DECISION_INVALID;
         ++my_inv;
-        if (!my_bad) my_bad = (unsigned long long)(a.n - r);
+        if (!my_bad) my_bad = (unsigned long long)(nw - r);
         u = jv = tau = __longlong_as_double(0x7ff8000000000000ll);
       }
-      a.decision[r] = code;
+      a.decision[g] = code;
       if (a.breakdown) {
-        a.breakdown[3 * r] = u;
-        a.breakdown[3 * r + 1] = jv;
-        a.breakdown[3 * r + 2] = tau;
+        a.breakdown[3 * g] = u;
+        a.breakdown[3 * g + 1] = jv;
+        a.breakdown[3 * g + 2] = tau;
       }
     }
     ballots[j] = __ballot_sync(0xffffffffu, in && (code == GG_DECISION_DIRECT || code == GG_DECISION_BATCHED));
@@ -344,25 +409,24 @@ __global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a)
   __shared__ AdmitShared<kLargeThreads, 1> sm;
   __shared__ double tile[kLargeThreads][kChunk + 1];
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    sm.vb = (int)atomicAdd(&a.ws->vblock_counter, 1ull);
-    sm.bc = batch_constants(a.state, a.snap);
-  }
+  if (tid == 0) block_setup(a, sm);
   __syncthreads();
   const BatchConst b = sm.bc;
   const int64_t tile0 = (int64_t)sm.vb * kLargeThreads;
+  const int64_t nw = sm.nw, row0 = sm.row0;
   const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
   const int64_t r = tile0 + tid;
-  const bool in = r < a.n;
+  const bool in = r < nw;
+  const int64_t g = row0 + r;
   RowAcc acc;
   for (int c0 = 0; c0 < a.k; c0 += kChunk) {
     const int cw = min(kChunk, a.k - c0);
 #pragma unroll 4
     for (int e = tid; e < kLargeThreads * kChunk; e += kLargeThreads) {
       const int rr = e / kChunk, cc = e % kChunk;
-      const int64_t gr = tile0 + rr;
+      const int64_t lr = tile0 + rr;
       double v = 0.0;
-      if (gr < a.n && cc < cw) v = __ldg(a.probs + gr * a.stride + c0 + cc);
+      if (lr < nw && cc < cw) v = __ldg(a.probs + (row0 + lr) * a.stride + c0 + cc);
       tile[rr][cc] = v;
     }
     __syncthreads();
@@ -376,19 +440,19 @@ __global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a)
   if (in) {
     double u, jv = 0.0, tau = 0.0;
     if (acc.finish(a.k, entropy, a.ln_k, u)) {
-      code = decide_row(a, b, u, a.now[r], jv, tau);
+      code = decide_row(a, b, u, a.now[g], jv, tau);
       if (code == GG_DECISION_SKIP) ++my_skip;
     } else {
       code = GG_DECISION_INVALID;
       ++my_inv;
-      if (!my_bad) my_bad = (unsigned long long)(a.n - r);
+      if (!my_bad) my_bad = (unsigned long long)(nw - r);
       u = jv = tau = __longlong_as_double(0x7ff8000000000000ll);
     }
-    a.decision[r] = code;
+    a.decision[g] = code;
     if (a.breakdown) {
-      a.breakdown[3 * r] = u;
-      a.breakdown[3 * r + 1] = jv;
-      a.breakdown[3 * r + 2] = tau;
+      a.breakdown[3 * g] = u;
+      a.breakdown[3 * g + 1] = jv;
+      a.breakdown[3 * g + 2] = tau;
     }
   }
   uint32_t ballots[1] = {__ballot_sync(0xffffffffu, in && (code == GG_DECISION_DIRECT || code == GG_DECISION_BATCHED))};
@@ -446,9 +510,13 @@ __device__ void sorted_insert(double* srt, int cnt, double x) {
   __syncwarp();
 }
 
+// Outcomes come either from three arrays (n of them) or from G exchange slots
+// (fp64 [3*B + 2] each: latency | joules | queue depth | count | fifo depth),
+// applied slot by slot in rank order.
 __global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, const double* lat,
                                                      const double* jou, const int32_t* qd, int64_t n,
-                                                     int set_qd, int64_t* err) {
+                                                     int set_qd, int64_t* err, const double* slots,
+                                                     int G, int B, int rank, gg_fifo* fifo) {
   __shared__ double win[GG_P95_WINDOW_MAX];
   __shared__ double srt[GG_P95_WINDOW_MAX];
   const int lane = threadIdx.x;
@@ -463,11 +531,34 @@ __global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, 
   const double lam = p.ewma_lambda, one_minus_lam = f64_sub(1.0, p.ewma_lambda);
   int64_t bad = -1;
   __syncwarp();
-  for (int64_t i = 0; i < n; ++i) {
-    const double L = lat[i], J = jou[i];
-    const int32_t Q = qd[i];
+  int64_t adm_other = 0, skip_other = 0;
+  if (slots) {
+    // Phase 1: the other ranks' admission effects of this step (their decide()
+    // observes of their own snapshots and their counters).  min/max observes and
+    // sums commute, and nothing read them since admission, so applying them
+    // here gives every replica the same state.
+    for (int gi = 0; gi < G; ++gi) {
+      if (gi == rank) continue;
+      const double* sl = slots + (int64_t)gi * (3 * B + 8) + 3 * B;
+      if (sl[2] - sl[3] > 0.0) {
+        if (seen > 0) ch_observe(ce, ewma);
+        ch_observe(cq, sl[6]);
+        ch_observe(cp, sl[7]);
+      }
+      adm_other += (int64_t)sl[4];
+      skip_other += (int64_t)sl[5];
+    }
+  }
+  const int nslots = slots ? G : 1;
+  for (int gi = 0; gi < nslots && bad < 0; ++gi) {
+  const double* sl = slots ? slots + (int64_t)gi * (3 * B + 8) : nullptr;
+  const int64_t ng = sl ? (int64_t)sl[3 * B] : n;
+  for (int64_t i = 0; i < ng; ++i) {
+    const double L = sl ? sl[i] : lat[i];
+    const double J = sl ? sl[B + i] : jou[i];
+    const int32_t Q = sl ? (int32_t)sl[2 * B + i] : qd[i];
     if (L < 0.0 || J < 0.0 || Q < 0) {  // NegativeMeasurement (controller.py:347-353)
-      bad = i;
+      bad = sl ? (int64_t)gi * B + i : i;
       break;
     }
     // EnergyLedger.observe_request -> ewma_update (energy.py:24-36, 75-87)
@@ -496,7 +587,18 @@ __global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, 
     outc += 1;
     if (set_qd) last_qd = Q;
   }
+  }
   __syncwarp();
+  if (slots && fifo && lane == 0) {  // global queue depth seen by this rank's next snapshot
+    int64_t extra = 0;
+    for (int gi = 0; gi < G; ++gi)
+      if (gi != rank) extra += (int64_t)slots[(int64_t)gi * (3 * B + 8) + 3 * B + 1];
+    fifo->extra_depth = extra;
+  }
+  if (slots && lane == 0) {
+    st->admitted_total += adm_other;
+    st->skipped_total += skip_other;
+  }
   for (int i = lane; i < cap; i += 32) st->win[i] = win[i];
   for (int i = lane; i < count; i += 32) st->win_sorted[i] = srt[i];
   if (lane == 0) {
@@ -674,6 +776,8 @@ size_t gg_admit_workspace_bytes(int64_t n) {
   return kWsHeader + sizeof(unsigned long long) * (size_t)(nb < 1 ? 1 : nb);
 }
 
+static int launch_admit(const AdmitArgs& a, void* stream);
+
 int gg_admit(const gg_params* params, gg_state* state_dev, const double* probs_dev, int64_t n,
              int32_t k, int64_t row_stride, const double* now_dev, const gg_snapshot* snapshot_dev,
              uint8_t* decision_dev, double* breakdown_dev, int32_t* admitted_idx_dev,
@@ -700,6 +804,17 @@ int gg_admit(const gg_params* params, gg_state* state_dev, const double* probs_d
   a.info = info_dev;
   a.ws = reinterpret_cast<AdmitWorkspace*>(workspace_dev);
   a.ln_k = log((double)k);  // host libm == CPython math.log (controller.py:142)
+  a.fifo = nullptr;
+  a.ring = nullptr;
+  a.ring_ns = nullptr;
+  return launch_admit(a, stream);
+}
+
+static int launch_admit(const AdmitArgs& a, void* stream) {
+  const int64_t n = a.n;
+  const int32_t k = a.k;
+  const double* probs_dev = a.probs;
+  const int64_t row_stride = a.stride;
   const int64_t nb = admit_blocks(n, k);
   cudaStream_t s = gg_stream(stream);
   const bool aligned16 = ((reinterpret_cast<uintptr_t>(probs_dev) & 15) == 0) && (row_stride % 2 == 0);
@@ -724,9 +839,57 @@ int gg_outcome(const gg_params* params, gg_state* state_dev, const double* laten
   if (n > 0 && (!latency_ms_dev || !joules_dev || !queue_depth_dev)) return GG_ERR_INVALID_ARGUMENT;
   outcome_kernel<<<1, 32, 0, gg_stream(stream)>>>(*params, state_dev, latency_ms_dev, joules_dev,
                                                    queue_depth_dev, n, set_queue_depth,
-                                                   error_index_dev);
+                                                   error_index_dev, nullptr, 0, 0, 0, nullptr);
   GG_LAUNCH_OK();
   return GG_OK;
+}
+
+int gg_outcome_slots(const gg_params* params, gg_state* state_dev, const double* slots_dev,
+                     int32_t G, int32_t B, int32_t rank, gg_fifo* fifo_dev,
+                     int64_t* error_index_dev, void* stream) {
+  int rc = gg_validate_params(params);
+  if (rc != GG_OK) return rc;
+  if (!state_dev || !slots_dev || G < 1 || B < 1 || rank < 0 || rank >= G)
+    return GG_ERR_INVALID_ARGUMENT;
+  outcome_kernel<<<1, 32, 0, gg_stream(stream)>>>(*params, state_dev, nullptr, nullptr, nullptr, 0,
+                                                   1, error_index_dev, slots_dev, G, B, rank,
+                                                   fifo_dev);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_admit_stream(const gg_params* params, gg_state* state_dev, gg_fifo* fifo_dev,
+                    int32_t* ring_ids_dev, uint64_t* ring_ns_dev, const double* probs_dev,
+                    int32_t k, int64_t row_stride, const double* now_dev, int64_t window,
+                    const gg_snapshot* snapshot_dev, uint8_t* decision_dev,
+                    gg_batch_info* info_dev, void* workspace_dev, size_t workspace_bytes,
+                    void* stream) {
+  int rc = gg_validate_params(params);
+  if (rc != GG_OK) return rc;
+  if (!state_dev || !fifo_dev || !ring_ids_dev || !probs_dev || !now_dev || !decision_dev ||
+      !workspace_dev || window < 1 || k < 1 || row_stride < k)
+    return GG_ERR_INVALID_ARGUMENT;
+  if (window > (int64_t)0x7fffffff) return GG_ERR_UNSUPPORTED;
+  if (workspace_bytes < gg_admit_workspace_bytes(window)) return GG_ERR_INVALID_ARGUMENT;
+  AdmitArgs a;
+  a.p = *params;
+  a.state = state_dev;
+  a.probs = probs_dev;
+  a.n = window;
+  a.k = k;
+  a.stride = row_stride;
+  a.now = now_dev;
+  a.snap = snapshot_dev;
+  a.decision = decision_dev;
+  a.breakdown = nullptr;
+  a.admitted_idx = nullptr;
+  a.info = info_dev;
+  a.ws = reinterpret_cast<AdmitWorkspace*>(workspace_dev);
+  a.ln_k = log((double)k);
+  a.fifo = fifo_dev;
+  a.ring = ring_ids_dev;
+  a.ring_ns = ring_ns_dev;
+  return launch_admit(a, stream);
 }
 
 int gg_epilogue(const float* logits_dev, int64_t n, int32_t k, int64_t ld, int32_t utility_proxy,

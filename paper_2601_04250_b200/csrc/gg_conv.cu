@@ -35,6 +35,7 @@ struct ConvEpi {
   const float* bias;              // [Cout]
   const __nv_bfloat16* residual;  // [M, Cout] or null
   int relu;
+  const int32_t* count;           // device image count (dynamic batch) or null
 };
 
 constexpr int kConvProdWarps = 4;
@@ -75,7 +76,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles_m = (sh.M + 127) / 128, tiles_n = sh.Cout / BN;
+  const int M = ep.count ? min(sh.M, __ldg(ep.count) * sh.Ho * sh.Wo) : sh.M;
+  const int tiles_m = (M + 127) / 128, tiles_n = sh.Cout / BN;
   const int num_tiles = tiles_m * tiles_n;
   const int num_kb = sh.Kpad / 64;
 
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
       const int m = tm * 128 + r_local;
-      const bool m_ok = m < sh.M;
+      const bool m_ok = m < M;
       int n = 0, ho = 0, wo = 0;
       if (m_ok) {
         n = m / (sh.Ho * sh.Wo);
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       mbar_wait(&acc_full[acc], (t >> 1) & 1);
       tc_fence_after();
       const int m = tm * 128 + quarter * 32 + lane;
-      const bool ok = m < sh.M;
+      const bool ok = m < M;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
@@ -280,9 +282,10 @@ __global__ void nchw_to_nhwc_pad(const float* __restrict__ in, __nv_bfloat16* __
 
 // 3x3 stride-2 pad-1 max pool, NHWC, 8 channels per thread.
 __global__ void maxpool3x3s2(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
-                             int N, int H, int W, int C, int Ho, int Wo) {
+                             int N, int H, int W, int C, int Ho, int Wo, const int32_t* count) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int cg = C / 8;
+  if (count) N = min(N, __ldg(count));
   if (idx >= (int64_t)N * Ho * Wo * cg) return;
   const int c0 = (idx % cg) * 8;
   const int64_t p = idx / cg;
@@ -316,9 +319,10 @@ __global__ void maxpool3x3s2(const __nv_bfloat16* __restrict__ in, __nv_bfloat16
 
 // Global average pool NHWC [N, HW, C] -> [N, C] bf16 (fp32 sum), one thread per (n, 8 channels).
 __global__ void avgpool_global(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
-                               int N, int HW, int C) {
+                               int N, int HW, int C, const int32_t* count) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int cg = C / 8;
+  if (count) N = min(N, __ldg(count));
   if (idx >= N * cg) return;
   const int n = idx / cg, c0 = (idx % cg) * 8;
   float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -348,7 +352,7 @@ using namespace gg;
 extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
                          int32_t Cout, int32_t R, int32_t S, int32_t stride, int32_t pad,
                          int32_t Kpad, const float* bias, const void* residual, int32_t relu,
-                         void* y, void* stream) {
+                         void* y, const int32_t* count_dev, void* stream) {
   if (!x || !w || !y || !bias || N <= 0 || H <= 0 || W <= 0 || R <= 0 || S <= 0 || stride <= 0)
     return GG_ERR_INVALID_ARGUMENT;
   if (C % 8 || Kpad % 64 || Kpad < R * S * C || Cout % 64) return GG_ERR_UNSUPPORTED;
@@ -361,7 +365,7 @@ extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t
   if (M > 0x7fffffff) return GG_ERR_UNSUPPORTED;
   sh.M = (int)M;
   ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
-             reinterpret_cast<const __nv_bfloat16*>(residual), relu};
+             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev};
   const int bn = Cout >= 256 ? 256 : Cout;
   CUtensorMap mw;
   int rc = make_map_2d(&mw, w, Cout, Kpad, Kpad, bn);
@@ -387,22 +391,24 @@ extern "C" int gg_nchw_to_nhwc(const float* x, int32_t N, int32_t C, int32_t H, 
 }
 
 extern "C" int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, void* y,
-                               void* stream) {
+                               const int32_t* count_dev, void* stream) {
   if (!x || !y || C % 8) return GG_ERR_INVALID_ARGUMENT;
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
   const int64_t work = (int64_t)N * Ho * Wo * (C / 8);
   maxpool3x3s2<<<(unsigned)((work + 255) / 256), 256, 0, gg_stream(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, H, W, C,
-      Ho, Wo);
+      Ho, Wo, count_dev);
   GG_LAUNCH_OK();
   return GG_OK;
 }
 
-extern "C" int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y, void* stream) {
+extern "C" int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y,
+                          const int32_t* count_dev, void* stream) {
   if (!x || !y || C % 8) return GG_ERR_INVALID_ARGUMENT;
   const int work = N * (C / 8);
   avgpool_global<<<(work + 127) / 128, 128, 0, gg_stream(stream)>>>(
-      reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, HW, C);
+      reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, HW, C,
+      count_dev);
   GG_LAUNCH_OK();
   return GG_OK;
 }

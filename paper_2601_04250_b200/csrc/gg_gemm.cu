@@ -34,6 +34,8 @@ struct GemmEpilogue {
   int seq_len;                     // OUT_QKV_HEADS: tokens per sequence (S)
   int heads;                       // OUT_QKV_HEADS: H (head dim fixed at 64)
   int64_t qkv_plane;               // OUT_QKV_HEADS: elements per Q/K/V^T plane (B*H*S*64)
+  const int32_t* count;            // device item count (dynamic batch) or null
+  int rows_per_item;               // M_eff = min(M, *count * rows_per_item)
 };
 
 constexpr int kBK = 64;            // 64 bf16 = 128 B = one swizzle row
@@ -52,7 +54,7 @@ struct GemmSmem {
 template <int BM, int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tcgen05(const __grid_constant__ CUtensorMap map_a,
-                      const __grid_constant__ CUtensorMap map_b, int M, int N, int K,
+                      const __grid_constant__ CUtensorMap map_b, int M_max, int N, int K,
                       GemmEpilogue ep) {
   using L = GemmSmem<BM, BN, STAGES>;
   static_assert(BM == 128, "cta_group::1 tiles use all 128 TMEM lanes");
@@ -66,6 +68,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // dynamic batch: the admitted count is read on the device (no host round-trip)
+  const int M = ep.count ? min(M_max, __ldg(ep.count) * ep.rows_per_item) : M_max;
   const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
   const int num_tiles = tiles_m * tiles_n;
   const int num_kb = K / kBK;
@@ -319,9 +323,11 @@ extern "C" int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, v
   if (rc) return rc;
   rc = make_map_2d(&mb, B, N, K, ldb, bn);
   if (rc) return rc;
+  if (e->count_dev && e->rows_per_item <= 0) return GG_ERR_INVALID_ARGUMENT;
   GemmEpilogue ep{D, ldd, e->bias, reinterpret_cast<const __nv_bfloat16*>(e->residual), e->ldr,
                   e->act, e->out_mode, e->seq_len, e->heads,
-                  e->out_mode == OUT_QKV_HEADS ? M * 64 * (int64_t)e->heads : 0};
+                  e->out_mode == OUT_QKV_HEADS ? M * 64 * (int64_t)e->heads : 0,
+                  e->count_dev, e->rows_per_item};
   cudaStream_t s = gg_stream(stream);
   switch (bn) {
     case 256: return launch_gemm<128, 256, 4>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
@@ -334,6 +340,6 @@ extern "C" int gg_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t l
                             int64_t ldd, int64_t M, int64_t N, int64_t K, const float* bias,
                             const void* residual, int64_t ldr, int32_t act, int32_t tile_n,
                             void* stream) {
-  gg_gemm_epilogue e{bias, residual, ldr, act, OUT_BF16, 0, 0, tile_n, 0};
+  gg_gemm_epilogue e{bias, residual, ldr, act, OUT_BF16, 0, 0, tile_n, 0, nullptr};
   return gg_gemm(A, lda, B, ldb, D, ldd, M, N, K, &e, stream);
 }

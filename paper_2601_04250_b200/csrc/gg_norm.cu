@@ -66,8 +66,10 @@ template <int PER_LANE>
 __global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* x, int64_t ldx,
                                                         __nv_bfloat16* y, int64_t ldy,
                                                         const float* gamma, const float* beta,
-                                                        int64_t rows, int width, float eps) {
+                                                        int64_t rows, int width, float eps,
+                                                        const int32_t* count, int rows_per_item) {
   const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (count) rows = min(rows, (int64_t)__ldg(count) * rows_per_item);
   if (r >= rows) return;
   float v[PER_LANE];
   load_row<PER_LANE>(x + r * ldx, v, false);
@@ -79,8 +81,9 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(const int32_t* ids, const
                                                        const __nv_bfloat16* pos, __nv_bfloat16* y,
                                                        const float* gamma, const float* beta,
                                                        int64_t tokens, int seq_len, int width,
-                                                       float eps) {
+                                                       float eps, const int32_t* count) {
   const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (count) tokens = min(tokens, (int64_t)__ldg(count) * seq_len);
   if (t >= tokens) return;
   float v[PER_LANE];
   load_row<PER_LANE>(word + (int64_t)__ldg(ids + t) * width, v, false);
@@ -94,27 +97,28 @@ using namespace gg;
 
 extern "C" int gg_layernorm(const void* x, int64_t ldx, void* y, int64_t ldy, const float* gamma,
                             const float* beta, int64_t rows, int32_t width, float eps,
-                            void* stream) {
+                            const int32_t* count_dev, int32_t rows_per_item, void* stream) {
   if (!x || !y || !gamma || !beta || rows < 0) return GG_ERR_INVALID_ARGUMENT;
   if (width != 768 || ldx % 8 || ldy % 8) return GG_ERR_UNSUPPORTED;
   if (rows == 0) return GG_OK;
   layernorm_kernel<24><<<(unsigned)((rows + 7) / 8), 256, 0, gg_stream(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), ldx, reinterpret_cast<__nv_bfloat16*>(y), ldy,
-      gamma, beta, rows, width, eps);
+      gamma, beta, rows, width, eps, count_dev, rows_per_item);
   GG_LAUNCH_OK();
   return GG_OK;
 }
 
 extern "C" int gg_embed_layernorm(const int32_t* ids, const void* word, const void* pos, void* y,
                                   const float* gamma, const float* beta, int64_t tokens,
-                                  int32_t seq_len, int32_t width, float eps, void* stream) {
+                                  int32_t seq_len, int32_t width, float eps,
+                                  const int32_t* count_dev, void* stream) {
   if (!ids || !word || !pos || !y || !gamma || !beta || tokens < 0 || seq_len <= 0)
     return GG_ERR_INVALID_ARGUMENT;
   if (width != 768) return GG_ERR_UNSUPPORTED;
   if (tokens == 0) return GG_OK;
   embed_ln_kernel<24><<<(unsigned)((tokens + 7) / 8), 256, 0, gg_stream(stream)>>>(
       ids, reinterpret_cast<const __nv_bfloat16*>(word), reinterpret_cast<const __nv_bfloat16*>(pos),
-      reinterpret_cast<__nv_bfloat16*>(y), gamma, beta, tokens, seq_len, width, eps);
+      reinterpret_cast<__nv_bfloat16*>(y), gamma, beta, tokens, seq_len, width, eps, count_dev);
   GG_LAUNCH_OK();
   return GG_OK;
 }

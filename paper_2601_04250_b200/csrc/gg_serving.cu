@@ -1,0 +1,227 @@
+// gg_serving.cu — device-side glue of the closed serving loop: FIFO pop, served
+// outcome records (the exchange slot), the served-batch K3 epilogue and the
+// payload gathers that feed the forward with the admitted requests.
+#include <cuda_bf16.h>
+
+#include "gg_common.cuh"
+
+namespace gg {
+
+__device__ __forceinline__ uint64_t now_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One block: n = min(B, depth); copy the ring slots [head, head+n) out.
+__global__ void fifo_pop_kernel(gg_fifo* f, const int32_t* ring, const uint64_t* ring_ns,
+                                int32_t* ids, uint64_t* ns, int32_t* count, int B) {
+  __shared__ int64_t head_s, n_s;
+  if (threadIdx.x == 0) {
+    const int64_t depth = f->tail - f->head;
+    head_s = f->head;
+    n_s = depth < B ? depth : B;
+  }
+  __syncthreads();
+  const int64_t n = n_s, mask = f->capacity - 1;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    if (i < n) {
+      const int64_t slot = (head_s + i) & mask;
+      ids[i] = ring[slot];
+      if (ns) ns[i] = ring_ns ? ring_ns[slot] : 0ull;
+    } else {
+      ids[i] = -1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *count = (int32_t)n;
+    f->head = head_s + n;
+  }
+}
+
+// Exchange slot of one rank's step (layout: GG_SLOT_LEN in greengate_b200.h).
+__global__ void served_outcomes_kernel(const gg_fifo* f, const int32_t* count, const uint64_t* ns,
+                                       gg_outcome_model m, const gg_batch_info* info, double* slot,
+                                       int B) {
+  const int n = *count;
+  const int64_t depth = f->tail - f->head;            // after the pop
+  const double qd = (double)(depth + f->extra_depth);
+  const double dn = (double)(n > 0 ? n : 1);
+  // servesim.py:303-304: service = base + per_item * n ; joules each = (base_j + per_item_j * n) / n
+  const double lat_model = f64_add(m.batch_base_ms, f64_mul(m.per_item_ms, dn));
+  const double joules = f64_div(f64_add(m.batch_base_energy_j, f64_mul(m.per_item_energy_j, dn)), dn);
+  const uint64_t t = now_ns();
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    double lat = 0.0, jo = 0.0, q = 0.0;
+    if (i < n) {
+      lat = (m.measured_latency && ns) ? (double)(t - ns[i]) * 1e-6 : lat_model;
+      jo = joules;
+      q = qd;
+    }
+    slot[i] = lat;
+    slot[B + i] = jo;
+    slot[2 * B + i] = q;
+  }
+  if (threadIdx.x == 0) {
+    slot[3 * B] = (double)n;
+    slot[3 * B + 1] = (double)depth;
+    slot[3 * B + 2] = info ? (double)info->n_decided : 0.0;
+    slot[3 * B + 3] = info ? (double)info->n_invalid : 0.0;
+    slot[3 * B + 4] = info ? (double)info->n_admitted : 0.0;
+    slot[3 * B + 5] = info ? (double)info->n_skipped : 0.0;
+    slot[3 * B + 6] = info ? (double)info->snap_queue_depth : 0.0;
+    slot[3 * B + 7] = info ? info->snap_p95_ms : 0.0;
+  }
+}
+
+// K3 over the served batch, one warp per row (see gg_epilogue in gg_controller.cu).
+__global__ void __launch_bounds__(256) epilogue_served_kernel(const float* logits,
+                                                              const int32_t* count, int k,
+                                                              int64_t ld, const int32_t* ids,
+                                                              int32_t* pred, double* conf,
+                                                              double* probs, int32_t* bpred,
+                                                              double* bconf) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= *count) return;
+  const float* x = logits + (int64_t)row * ld;
+  float m = -INFINITY;
+  for (int j = lane; j < k; j += 32) m = fmaxf(m, x[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const double md = (double)m;
+  double s = 0.0;
+  for (int j = lane; j < k; j += 32) s += exp((double)x[j] - md);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const double inv = 1.0 / s;
+  double best = -1.0;
+  int bi = 0x7fffffff;
+  for (int j = lane; j < k; j += 32) {
+    const double pj = exp((double)x[j] - md) * inv;
+    if (probs) probs[(int64_t)row * k + j] = pj;
+    if (pj > best) {
+      best = pj;
+      bi = j;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) {
+      best = ob;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    const int id = ids[row];
+    if (pred) pred[id] = bi;
+    if (conf) conf[id] = best;
+    if (bpred) bpred[row] = bi;
+    if (bconf) bconf[row] = best;
+  }
+}
+
+// uint8 HWC pool image -> normalized bf16 NHWC with 8 channels; one thread per pixel.
+__global__ void stem_gather_kernel(const uint8_t* __restrict__ pool, int64_t pool_size,
+                                   const int32_t* ids, const int32_t* count, int B, int H, int W,
+                                   float m0, float m1, float m2, float s0, float s1, float s2,
+                                   __nv_bfloat16* __restrict__ y) {
+  const int n_valid = count ? min(B, __ldg(count)) : B;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= (int64_t)n_valid * H * W) return;
+  const int n = (int)(p / ((int64_t)H * W));
+  const int64_t hw = p - (int64_t)n * H * W;
+  const int64_t img = ids ? (int64_t)__ldg(ids + n) % pool_size : n;
+  const uint8_t* src = pool + (img * H * W + hw) * 3;
+  const float r = src[0] * (1.0f / 255.0f), g = src[1] * (1.0f / 255.0f), b = src[2] * (1.0f / 255.0f);
+  __align__(16) __nv_bfloat16 v[8];
+  v[0] = __float2bfloat16_rn((r - m0) / s0);
+  v[1] = __float2bfloat16_rn((g - m1) / s1);
+  v[2] = __float2bfloat16_rn((b - m2) / s2);
+#pragma unroll
+  for (int e = 3; e < 8; ++e) v[e] = __float2bfloat16_rn(0.0f);
+  *reinterpret_cast<uint4*>(y + p * 8) = *reinterpret_cast<uint4*>(v);
+}
+
+__global__ void token_gather_kernel(const int32_t* pool_ids, const int32_t* pool_mask,
+                                    int64_t pool_size, const int32_t* ids, const int32_t* count,
+                                    int B, int S, int32_t* out_ids, int32_t* out_mask) {
+  const int n_valid = count ? min(B, __ldg(count)) : B;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)n_valid * S) return;
+  const int n = (int)(t / S), s = (int)(t - (int64_t)n * S);
+  const int64_t src = ((int64_t)__ldg(ids + n) % pool_size) * S + s;
+  out_ids[t] = pool_ids[src];
+  if (out_mask) out_mask[t] = pool_mask ? pool_mask[src] : 1;
+}
+
+}  // namespace gg
+
+using namespace gg;
+
+extern "C" {
+
+int gg_fifo_pop(gg_fifo* fifo_dev, const int32_t* ring_ids_dev, const uint64_t* ring_ns_dev,
+                int32_t* batch_ids_dev, uint64_t* batch_ns_dev, int32_t* count_dev, int32_t B,
+                void* stream) {
+  if (!fifo_dev || !ring_ids_dev || !batch_ids_dev || !count_dev || B < 1) return GG_ERR_INVALID_ARGUMENT;
+  fifo_pop_kernel<<<1, 256, 0, gg_stream(stream)>>>(fifo_dev, ring_ids_dev, ring_ns_dev,
+                                                    batch_ids_dev, batch_ns_dev, count_dev, B);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_served_outcomes(const gg_fifo* fifo_dev, const int32_t* count_dev,
+                       const uint64_t* batch_ns_dev, const gg_outcome_model* model,
+                       const gg_batch_info* info_dev, double* slot_dev, int32_t B, void* stream) {
+  if (!fifo_dev || !count_dev || !model || !slot_dev || B < 1) return GG_ERR_INVALID_ARGUMENT;
+  if (model->batch_base_ms < 0 || model->per_item_ms < 0 || model->batch_base_energy_j < 0 ||
+      model->per_item_energy_j < 0)
+    return GG_ERR_NEGATIVE_MEASUREMENT;
+  served_outcomes_kernel<<<1, 256, 0, gg_stream(stream)>>>(fifo_dev, count_dev, batch_ns_dev,
+                                                           *model, info_dev, slot_dev, B);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_epilogue_served(const float* logits_dev, const int32_t* count_dev, int32_t B, int32_t k,
+                       int64_t ld, const int32_t* batch_ids_dev, int32_t* predicted_dev,
+                       double* confidence_dev, double* probs_dev, int32_t* batch_predicted_dev,
+                       double* batch_confidence_dev, void* stream) {
+  if (!logits_dev || !count_dev || !batch_ids_dev || B < 1 || k < 1 || ld < k)
+    return GG_ERR_INVALID_ARGUMENT;
+  epilogue_served_kernel<<<(B + 7) / 8, 256, 0, gg_stream(stream)>>>(
+      logits_dev, count_dev, k, ld, batch_ids_dev, predicted_dev, confidence_dev, probs_dev,
+      batch_predicted_dev, batch_confidence_dev);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_ids,
+                   const int32_t* count_dev, int32_t B, int32_t H, int32_t W, const float* mean3,
+                   const float* std3, void* y, void* stream) {
+  if (!pool || pool_size < 1 || !mean3 || !std3 || !y || B < 1) return GG_ERR_INVALID_ARGUMENT;
+  const int64_t pixels = (int64_t)B * H * W;
+  stem_gather_kernel<<<(unsigned)((pixels + 255) / 256), 256, 0, gg_stream(stream)>>>(
+      pool, pool_size, batch_ids, count_dev, B, H, W, mean3[0], mean3[1], mean3[2], std3[0],
+      std3[1], std3[2], reinterpret_cast<__nv_bfloat16*>(y));
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_token_gather(const int32_t* pool_ids, const int32_t* pool_mask, int64_t pool_size,
+                    const int32_t* batch_ids, const int32_t* count_dev, int32_t B,
+                    int32_t seq_len, int32_t* ids, int32_t* mask, void* stream) {
+  if (!pool_ids || pool_size < 1 || !batch_ids || !ids || B < 1 || seq_len < 1)
+    return GG_ERR_INVALID_ARGUMENT;
+  const int64_t tokens = (int64_t)B * seq_len;
+  token_gather_kernel<<<(unsigned)((tokens + 255) / 256), 256, 0, gg_stream(stream)>>>(
+      pool_ids, pool_mask, pool_size, batch_ids, count_dev, B, seq_len, ids, mask);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+}  // extern "C"

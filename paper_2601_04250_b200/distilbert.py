@@ -32,15 +32,17 @@ OUT_BF16, OUT_F32, OUT_QKV = 0, 1, 2
 class GemmEpilogue(C.Structure):
     _fields_ = [("bias", C.c_void_p), ("residual", C.c_void_p), ("ldr", C.c_int64),
                 ("act", C.c_int32), ("out_mode", C.c_int32), ("seq_len", C.c_int32),
-                ("heads", C.c_int32), ("tile_n", C.c_int32), ("reserved", C.c_int32)]
+                ("heads", C.c_int32), ("tile_n", C.c_int32), ("rows_per_item", C.c_int32),
+                ("count_dev", C.c_void_p)]
 
 
 def gemm(lib, A, lda, W, D, ldd, M, N, K, stream, bias=None, residual=None, act=NONE,
-         out_mode=OUT_BF16, seq_len=0, heads=0, tile_n=0):
+         out_mode=OUT_BF16, seq_len=0, heads=0, tile_n=0, count=None, rows_per_item=1):
     ep = GemmEpilogue(None if bias is None else bias.data_ptr(),
                       None if residual is None else residual.data_ptr(),
                       0 if residual is None else residual.stride(0), act, out_mode, seq_len,
-                      heads, tile_n, 0)
+                      heads, tile_n, rows_per_item if count is not None else 0,
+                      None if count is None else count.data_ptr())
     _native.check("gg_gemm", lib.gg_gemm(C.c_void_p(A), lda, _native.ptr(W), W.stride(0),
                                          C.c_void_p(D), ldd, M, N, K, C.byref(ep), stream))
 
@@ -113,44 +115,48 @@ class DistilBertB200:
         head = 2 * batch * D * (D + self.num_labels)
         return float(L * (lin + attn) + head)
 
-    def forward(self, input_ids, attention_mask=None, batch: int | None = None, stream=None):
+    def forward(self, input_ids, attention_mask=None, batch: int | None = None, stream=None,
+                count=None):
         """input_ids: CUDA int32 [B, S]; attention_mask: CUDA int32 [B, S] or None.
-        Returns fp32 logits [B, num_labels] (a view of the output buffer)."""
+        count: optional CUDA int32 [1] = number of valid sequences (dynamic batch,
+        read on the device).  Returns fp32 logits [B, num_labels] (a view)."""
         lib = self.lib
         B = int(input_ids.shape[0]) if batch is None else int(batch)
         S, D = self.seq_len, self.DIM
         assert B <= self.max_batch and input_ids.dtype.itemsize == 4
         M = B * S
         st = _native.stream_ptr(stream)
+        cnt = _native.ptr(count)
         _native.check("gg_embed_layernorm", lib.gg_embed_layernorm(
             _native.ptr(input_ids), _native.ptr(self.word), _native.ptr(self.pos),
             _native.ptr(self.x), _native.ptr(self.emb_g), _native.ptr(self.emb_b), M, S, D,
-            C.c_float(self.EPS), st))
+            C.c_float(self.EPS), cnt, st))
         x, x1, h = self.x.data_ptr(), self.x1.data_ptr(), self.h.data_ptr()
+        dyn = dict(count=count, rows_per_item=S)
         for L in self.layers:
             gemm(lib, x, D, L["w_qkv"], self.qkv.data_ptr(), 3 * D, M, 3 * D, D, st,
-                 bias=L["b_qkv"], out_mode=OUT_QKV, seq_len=S, heads=self.HEADS)
+                 bias=L["b_qkv"], out_mode=OUT_QKV, seq_len=S, heads=self.HEADS, **dyn)
             _native.check("gg_attention", lib.gg_attention(
                 _native.ptr(self.qkv), _native.ptr(attention_mask), _native.ptr(self.ctx), D, B,
-                self.HEADS, S, st))
+                self.HEADS, S, cnt, st))
             gemm(lib, self.ctx.data_ptr(), D, L["w_o"], h, D, M, D, D, st, bias=L["b_o"],
-                 residual=self.x)
+                 residual=self.x, **dyn)
             _native.check("gg_layernorm", lib.gg_layernorm(
                 C.c_void_p(h), D, C.c_void_p(x1), D, _native.ptr(L["ln1_g"]),
-                _native.ptr(L["ln1_b"]), M, D, C.c_float(self.EPS), st))
+                _native.ptr(L["ln1_b"]), M, D, C.c_float(self.EPS), cnt, S, st))
             gemm(lib, x1, D, L["w1"], self.ffn.data_ptr(), self.FFN, M, self.FFN, D, st,
-                 bias=L["b1"], act=GELU)
+                 bias=L["b1"], act=GELU, **dyn)
             gemm(lib, self.ffn.data_ptr(), self.FFN, L["w2"], h, D, M, D, self.FFN, st,
-                 bias=L["b2"], residual=self.x1)
+                 bias=L["b2"], residual=self.x1, **dyn)
             _native.check("gg_layernorm", lib.gg_layernorm(
                 C.c_void_p(h), D, C.c_void_p(x), D, _native.ptr(L["ln2_g"]),
-                _native.ptr(L["ln2_b"]), M, D, C.c_float(self.EPS), st))
+                _native.ptr(L["ln2_b"]), M, D, C.c_float(self.EPS), cnt, S, st))
         # CLS rows (stride S*D) -> pre_classifier + ReLU -> classifier (fp32 logits)
         gemm(lib, x, S * D, self.w_pre, self.pooled.data_ptr(), D, B, D, D, st, bias=self.b_pre,
-             act=RELU, tile_n=64)
+             act=RELU, tile_n=64, count=count, rows_per_item=1)
         gemm(lib, self.pooled.data_ptr(), D, self.w_cls, self.logits.data_ptr(),
              self.logits.stride(0), B, self.w_cls.shape[0], D, st, bias=self.b_cls,
-             out_mode=OUT_F32, tile_n=64)
+             out_mode=OUT_F32, tile_n=64, count=count, rows_per_item=1)
         return self.logits[:B, : self.num_labels]
 
 

@@ -50,11 +50,12 @@ class _Conv:
         return ((h + 2 * self.pad - self.r) // self.stride + 1,
                 (w + 2 * self.pad - self.s) // self.stride + 1)
 
-    def __call__(self, lib, x, n, h, w, y, st, residual=None, relu=True):
+    def __call__(self, lib, x, n, h, w, y, st, residual=None, relu=True, count=None):
         _native.check("gg_conv2d", lib.gg_conv2d(
             C.c_void_p(x), n, h, w, self.cin, _native.ptr(self.w), self.cout, self.r, self.s,
             self.stride, self.pad, self.kpad, _native.ptr(self.b),
-            None if residual is None else C.c_void_p(residual), int(relu), C.c_void_p(y), st))
+            None if residual is None else C.c_void_p(residual), int(relu), C.c_void_p(y),
+            _native.ptr(count), st))
         return self.out_hw(h, w)
 
     def flops(self, n, h, w):
@@ -117,39 +118,47 @@ class ResNet18B200:
 
     def forward(self, images, batch: int | None = None, stream=None):
         """images: CUDA fp32 NCHW [B, 3, 224, 224].  Returns fp32 logits [B, 1000] (view)."""
-        lib = self.lib
         B = int(images.shape[0]) if batch is None else int(batch)
         assert B <= self.max_batch
         H = self.image
         st = _native.stream_ptr(stream)
-        _native.check("gg_nchw_to_nhwc", lib.gg_nchw_to_nhwc(
+        _native.check("gg_nchw_to_nhwc", self.lib.gg_nchw_to_nhwc(
             _native.ptr(images), B, 3, H, H, 8, _native.ptr(self.x8), st))
+        return self.forward_nhwc8(B, stream=stream)
+
+    def forward_nhwc8(self, B: int, stream=None, count=None):
+        """Forward from self.x8 (bf16 NHWC, 8 channels).  count: optional CUDA
+        int32 [1] = valid images (dynamic batch read on the device)."""
+        lib = self.lib
+        H = self.image
+        st = _native.stream_ptr(stream)
+        cnt = _native.ptr(count)
         a, b, c = (t.data_ptr() for t in self.buf)
-        h, w = self.stem(lib, self.x8.data_ptr(), B, H, H, a, st)           # 112x112x64
+        h, w = self.stem(lib, self.x8.data_ptr(), B, H, H, a, st, count=count)   # 112x112x64
         _native.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(C.c_void_p(a), B, h, w, 64,
-                                                            C.c_void_p(b), st))
+                                                            C.c_void_p(b), cnt, st))
         h, w = (h + 1) // 2, (w + 1) // 2                                      # 56x56x64
         cur, free = b, [a, c]
         for conv1, conv2, ds in self.blocks:
             t1 = free[0]
-            h2, w2 = conv1(lib, cur, B, h, w, t1, st, relu=True)
+            h2, w2 = conv1(lib, cur, B, h, w, t1, st, relu=True, count=count)
             if ds is not None:
                 # identity branch = 1x1/2 conv + BN; the block input is dead afterwards
                 t2 = free[1]
-                ds(lib, cur, B, h, w, t2, st, relu=False)
-                conv2(lib, t1, B, h2, w2, cur, st, residual=t2, relu=True)
+                ds(lib, cur, B, h, w, t2, st, relu=False, count=count)
+                conv2(lib, t1, B, h2, w2, cur, st, residual=t2, relu=True, count=count)
                 free = [t1, t2]
             else:
                 out = free[1]
-                conv2(lib, t1, B, h2, w2, out, st, residual=cur, relu=True)
+                conv2(lib, t1, B, h2, w2, out, st, residual=cur, relu=True, count=count)
                 free = [cur, t1]
                 cur = out
             h, w = h2, w2
         _native.check("gg_avgpool", lib.gg_avgpool(C.c_void_p(cur), B, h * w, 512,
-                                                   _native.ptr(self.pooled), st))
+                                                   _native.ptr(self.pooled), cnt, st))
         gemm(lib, self.pooled.data_ptr(), 512, self.w_fc, self.logits.data_ptr(),
              self.logits.stride(0), B, self.w_fc.shape[0], 512, st, bias=self.b_fc,
-             out_mode=OUT_F32, tile_n=64)
+             out_mode=OUT_F32, tile_n=64, count=count, rows_per_item=1)
         return self.logits[:B, : self.num_classes]
 
 

@@ -1,0 +1,263 @@
+"""Closed-loop gated serving on one GPU (optionally one of G data-parallel ranks).
+
+One step, entirely on the device and captured as one CUDA graph:
+
+  K1  gg_admit_stream     decide the next `window` trace rows against the
+                          snapshot of the device FIFO (queue depth, p95, fill),
+                          append the admitted rows to the FIFO ring in order
+      gg_fifo_pop         pop up to B admitted requests -> batch ids + count
+      gather              payloads of the served batch (images / token ids)
+  fwd ResNet-18 / DistilBERT on the dynamic batch (count read on the device)
+  K3  gg_epilogue_served  fp32 logits -> first-max prediction + fp64 confidence
+      gg_served_outcomes  latency / joules / queue depth of the served batch
+  K9  all_reduce(SUM)     rank-slotted outcome buffer (multi-GPU only; exact)
+  K2  gg_outcome_slots    record_outcome() for every served request of every
+                          rank, in rank order -> identical replicas
+
+This replaces the reference's discrete-event stand-in for the serving backend
+(pkg/src/greengate/servesim.py:280-367): admitted requests are queued and
+served in fused batches (Path B, servesim.py:286-306), skipped ones are
+answered by the zero-cost fallback and never reach the model.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _abi, _native
+
+IMAGENET_MEAN = (0.485, 0.456, 0.406)
+IMAGENET_STD = (0.229, 0.224, 0.225)
+
+
+@dataclass
+class OutcomeModel:
+    """Latency/energy of a served batch (servesim.py:303-304 affine model by
+    default; measured_latency=True uses %globaltimer from admission to completion)."""
+
+    batch_base_ms: float = 4.0
+    per_item_ms: float = 0.05
+    batch_base_energy_j: float = 6.0
+    per_item_energy_j: float = 1.5
+    measured_latency: bool = False
+
+    def abi(self) -> _abi.gg_outcome_model:
+        return _abi.gg_outcome_model(self.batch_base_ms, self.per_item_ms,
+                                     self.batch_base_energy_j, self.per_item_energy_j,
+                                     int(self.measured_latency), 0)
+
+
+class GatedServer:
+    """Admission controller + device FIFO + forward pass + outcome feedback.
+
+    controller: a device AdmissionController (paper_2601_04250_b200.controller)
+    net:        ResNet18B200 or DistilBertB200 (its max_batch is B)
+    scores/now: CUDA fp64 [T, K] / [T] resident trace (this rank's shard)
+    payloads:   ResNet: CUDA uint8 [P, H, W, 3]; DistilBERT: (ids int32 [P, S], mask int32 [P, S])
+    """
+
+    def __init__(self, controller, net, scores, now, payloads, *, window: int,
+                 outcome: OutcomeModel | None = None, fifo_capacity: int = 1 << 20,
+                 rank: int = 0, world: int = 1, process_group=None):
+        torch = _native.require_cuda()
+        self.torch = torch
+        self.lib = _native.load()
+        self.ctl, self.net = controller, net
+        self.dev = controller.device
+        self.B = int(net.max_batch)
+        self.W = int(window)
+        self.T, self.K = int(scores.shape[0]), int(scores.shape[1])
+        self.scores, self.now = scores, now
+        self.kind = "resnet18" if hasattr(net, "blocks") else "distilbert"
+        self.payloads = payloads
+        self.outcome = (outcome or OutcomeModel()).abi()
+        self.rank, self.world, self.pg = rank, world, process_group
+        assert fifo_capacity & (fifo_capacity - 1) == 0
+        z = dict(device=self.dev)
+        fifo = _abi.gg_fifo(0, 0, fifo_capacity, self.B, 0, self.T, 0, 0)
+        self.fifo = torch.frombuffer(bytearray(bytes(fifo)), dtype=torch.uint8).to(self.dev)
+        self.ring = torch.empty(fifo_capacity, dtype=torch.int32, **z)
+        self.ring_ns = torch.empty(fifo_capacity, dtype=torch.int64, **z)
+        self.batch_ids = torch.full((self.B,), -1, dtype=torch.int32, **z)
+        self.batch_ns = torch.empty(self.B, dtype=torch.int64, **z)
+        self.count = torch.zeros(1, dtype=torch.int32, **z)
+        self.batch_pred = torch.full((self.B,), -1, dtype=torch.int32, **z)
+        self.batch_conf = torch.zeros(self.B, dtype=torch.float64, **z)
+        self.slot_len = 3 * self.B + 8   # GG_SLOT_LEN(B)
+        self.slots = torch.zeros(world * self.slot_len, dtype=torch.float64, **z)
+        self.decision = torch.full((self.T,), 254, dtype=torch.uint8, **z)
+        self.predicted = torch.full((self.T,), -1, dtype=torch.int32, **z)
+        self.confidence = torch.full((self.T,), float("nan"), dtype=torch.float64, **z)
+        self.info = torch.empty(_abi.BATCH_INFO_BYTES, dtype=torch.uint8, **z)
+        self.ws = torch.zeros(self.lib.gg_admit_workspace_bytes(self.W), dtype=torch.uint8, **z)
+        self.err = torch.empty(1, dtype=torch.int64, **z)
+        if self.kind == "resnet18":
+            self.mean = torch.tensor(IMAGENET_MEAN, dtype=torch.float32)
+            self.std = torch.tensor(IMAGENET_STD, dtype=torch.float32)
+        else:
+            self.tok_ids = torch.empty((self.B, net.seq_len), dtype=torch.int32, **z)
+            self.tok_mask = torch.empty((self.B, net.seq_len), dtype=torch.int32, **z)
+        self.graph = None
+        self.stream = torch.cuda.Stream(device=self.dev)
+        self.steps_run = 0
+
+    # ------------------------------------------------------------------ one step
+    def _forward(self, st):
+        lib, B = self.lib, self.B
+        if self.kind == "resnet18":
+            pool = self.payloads
+            H = int(pool.shape[1])
+            _native.check("gg_stem_gather", lib.gg_stem_gather(
+                _native.ptr(pool), int(pool.shape[0]), _native.ptr(self.batch_ids),
+                _native.ptr(self.count), B, H, int(pool.shape[2]),
+                self.mean.numpy().ctypes.data_as(C.c_void_p),
+                self.std.numpy().ctypes.data_as(C.c_void_p), _native.ptr(self.net.x8), st))
+            logits = self.net.forward_nhwc8(B, stream=self._cur_stream, count=self.count)
+        else:
+            ids, mask = self.payloads
+            _native.check("gg_token_gather", lib.gg_token_gather(
+                _native.ptr(ids), _native.ptr(mask), int(ids.shape[0]), _native.ptr(self.batch_ids),
+                _native.ptr(self.count), B, self.net.seq_len, _native.ptr(self.tok_ids),
+                _native.ptr(self.tok_mask), st))
+            logits = self.net.forward(self.tok_ids, self.tok_mask, batch=B,
+                                      stream=self._cur_stream, count=self.count)
+        return logits
+
+    def step(self):
+        """Enqueue one serving step on the current stream (graph-capturable)."""
+        self.step_local()
+        if self.world > 1:
+            # K9: rank-slotted buffer, SUM == allgather exactly (x + 0 == x)
+            self.torch.distributed.all_reduce(self.slots, group=self.pg)
+        self.step_feedback()
+
+    def step_local(self):
+        """Admission, FIFO, forward, epilogue and this rank's exchange slot."""
+        torch, lib = self.torch, self.lib
+        self._cur_stream = torch.cuda.current_stream(self.dev)
+        st = _native.stream_ptr(self._cur_stream)
+        ctl = self.ctl
+        _native.check("gg_admit_stream", lib.gg_admit_stream(
+            C.byref(ctl.params), _native.ptr(ctl.state), _native.ptr(self.fifo),
+            _native.ptr(self.ring), _native.ptr(self.ring_ns), _native.ptr(self.scores), self.K,
+            int(self.scores.stride(0)), _native.ptr(self.now), self.W, None,
+            _native.ptr(self.decision), _native.ptr(self.info), _native.ptr(self.ws),
+            self.ws.numel(), st))
+        _native.check("gg_fifo_pop", lib.gg_fifo_pop(
+            _native.ptr(self.fifo), _native.ptr(self.ring), _native.ptr(self.ring_ns),
+            _native.ptr(self.batch_ids), _native.ptr(self.batch_ns), _native.ptr(self.count),
+            self.B, st))
+        logits = self._forward(st)
+        _native.check("gg_epilogue_served", lib.gg_epilogue_served(
+            C.c_void_p(logits.data_ptr()), _native.ptr(self.count), self.B, int(logits.shape[1]),
+            int(logits.stride(0)), _native.ptr(self.batch_ids), _native.ptr(self.predicted),
+            _native.ptr(self.confidence), None, _native.ptr(self.batch_pred),
+            _native.ptr(self.batch_conf), st))
+        if self.world > 1:
+            self.slots.zero_()
+        my_slot = self.slots[self.rank * self.slot_len:]
+        _native.check("gg_served_outcomes", lib.gg_served_outcomes(
+            _native.ptr(self.fifo), _native.ptr(self.count), _native.ptr(self.batch_ns),
+            C.byref(self.outcome), _native.ptr(self.info), _native.ptr(my_slot), self.B, st))
+
+    def step_feedback(self):
+        """K2 over every rank's slot (after the exchange)."""
+        torch, lib, ctl = self.torch, self.lib, self.ctl
+        st = _native.stream_ptr(torch.cuda.current_stream(self.dev))
+        _native.check("gg_outcome_slots", lib.gg_outcome_slots(
+            C.byref(ctl.params), _native.ptr(ctl.state), _native.ptr(self.slots), self.world,
+            self.B, self.rank, _native.ptr(self.fifo), _native.ptr(self.err), st))
+
+    # ------------------------------------------------------------------ graphs
+    def capture(self) -> None:
+        """Capture one step as a CUDA graph (after one eager warm-up step)."""
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            self.step()
+        self.graph = g
+
+    def run(self, steps: int) -> None:
+        torch = self.torch
+        for _ in range(steps):
+            if self.graph is not None:
+                self.graph.replay()
+            else:
+                with torch.cuda.stream(self.stream):
+                    self.step()
+        self.steps_run += steps
+
+    # ------------------------------------------------------------------ host views
+    def fifo_state(self) -> _abi.gg_fifo:
+        return _abi.gg_fifo.from_buffer_copy(bytes(self.fifo.cpu().numpy().tobytes()))
+
+    def done(self) -> bool:
+        f = self.fifo_state()
+        return f.cursor >= f.trace_len and f.tail == f.head
+
+    def drain(self, max_steps: int = 1 << 30) -> int:
+        """Run steps until the trace is decided and the FIFO is empty."""
+        n = 0
+        while not self.done() and n < max_steps:
+            chunk = 8
+            self.run(chunk)
+            self.torch.cuda.synchronize()
+            n += chunk
+        return n
+
+    def results(self) -> dict:
+        f = self.fifo_state()
+        st = self.ctl.state_struct()
+        return {"decided": int(f.cursor), "admitted": int(f.tail), "served": int(f.head),
+                "queue_depth": int(f.tail - f.head), "overflow": int(f.overflow),
+                "admitted_total": int(st.admitted_total), "skipped_total": int(st.skipped_total),
+                "outcomes_total": int(st.outcomes_total), "ewma_joules": st.ewma_joules_per_request,
+                "p95_ms": st.p95_current}
+
+
+def synthetic_images(n: int, image: int = 224, seed: int = 0, device="cuda"):
+    """Resident pool of uint8 HWC images (synthetic; no dataset offline)."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return torch.randint(0, 256, (n, image, image, 3), generator=g, dtype=torch.uint8).to(device)
+
+
+def synthetic_tokens(n: int, seq_len: int = 128, vocab: int = 30522, seed: int = 0, device="cuda"):
+    """Resident pool of token-id sequences + all-ones masks (synthetic)."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    ids = torch.randint(0, vocab, (n, seq_len), generator=g, dtype=torch.int32)
+    return ids.to(device), torch.ones((n, seq_len), dtype=torch.int32, device=device)
+
+
+def smoke() -> None:
+    """Tiny closed loop on cuda:0 (ResNet-18, B=8, 64 requests) vs the host oracle replay."""
+    import numpy as np
+    import torch
+
+    from . import controller as gcontrol
+    from .energy import EnergyLedger
+    from .resnet18 import ResNet18B200, random_model
+    from .workload import ArrivalMode, WorkloadConfig, generate_trace
+
+    wl = WorkloadConfig(mode=ArrivalMode.CLOSED, num_requests=64, num_classes=1000,
+                        confidence_low=0.3, confidence_high=0.9)
+    tr = generate_trace(wl, 1.0, np.random.default_rng(0))
+    now = np.arange(64) * 0.01
+    cfg = gcontrol.ControllerConfig(alpha=1.0, beta=-0.2, gamma=-0.3, tau0=0.6, tau_inf=0.3, k=2.0,
+                                    routing=gcontrol.RoutePolicy.ALL_BATCHED)
+    ctl = cfg.build(EnergyLedger())
+    net = ResNet18B200(random_model(0), max_batch=8)
+    srv = GatedServer(ctl, net, torch.from_numpy(tr.scores).cuda(), torch.from_numpy(now).cuda(),
+                      synthetic_images(16), window=12)
+    srv.run(1)
+    srv.capture()
+    srv.drain()
+    torch.cuda.synchronize()
+    r = srv.results()
+    assert r["decided"] == 64 and r["served"] == r["admitted"] and r["overflow"] == 0, r
+    pred = srv.predicted.cpu().numpy()
+    dec = srv.decision.cpu().numpy()
+    assert ((pred >= 0) == ((dec == 1) | (dec == 2))).all(), "served set != admitted set"
+    print(f"smoke: closed loop ok ({r['admitted']}/64 admitted and served in batches of <= 8)")

@@ -37,7 +37,7 @@ def test_attention_kernel(env):
     qkv[2 * plane:] = vb.transpose(2, 3).contiguous().flatten()
     ctx = torch.empty((B * S, H * D), dtype=torch.bfloat16, device="cuda")
     nat.check("gg_attention", lib.gg_attention(nat.ptr(qkv), nat.ptr(mask), nat.ptr(ctx), H * D,
-                                               B, H, S, nat.stream_ptr()))
+                                               B, H, S, None, nat.stream_ptr()))
     s = qb.float() @ kb.float().transpose(2, 3)
     s = s.masked_fill(mask[:, None, None, :] == 0, float("-inf"))
     ref = torch.softmax(s, dim=-1) @ vb.float()
@@ -54,7 +54,7 @@ def test_layernorm_kernel(env):
     y = torch.empty_like(x)
     nat.check("gg_layernorm", lib.gg_layernorm(nat.ptr(x), 768, nat.ptr(y), 768, nat.ptr(gmm),
                                                nat.ptr(bta), 1000, 768, C.c_float(1e-12),
-                                               nat.stream_ptr()))
+                                               None, 1, nat.stream_ptr()))
     ref = torch.nn.functional.layer_norm(x.float(), (768,), gmm, bta, 1e-12)
     # bf16 output: one rounding of |y| (half an ulp = 2^-9 relative) plus fp32 statistics
     assert ((y.float() - ref).abs() <= 4e-3 * ref.abs() + 1e-2).all()

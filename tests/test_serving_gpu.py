@@ -1,0 +1,84 @@
+"""Closed serving loop on the GPU vs the host replay (oracle/serving_oracle.py).
+
+Checks, for ResNet-18 (K=1000 gating scores) and DistilBERT (K=2) loops:
+  - every trace row's decision code equals the oracle's (bit-exact outside the
+    |J - tau| < 1e-12 band; the fixtures have no such rows),
+  - the served order (FIFO) and the set of served requests equal the oracle's,
+  - the controller state after the loop equals the oracle's field by field,
+  - graph replay == eager steps.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import serving_oracle
+from tests import _golden as G
+
+pytestmark = pytest.mark.gpu
+
+MODEL = dict(batch_base_ms=4.0, per_item_ms=0.05, batch_base_energy_j=6.0, per_item_energy_j=1.5)
+
+
+def make_trace(n, k, seed):
+    import paper_2601_04250_b200 as gg
+    wl = gg.WorkloadConfig(mode=gg.ArrivalMode.POISSON, rate_rps=5000.0, num_classes=k,
+                           confidence_low=max(0.3, 1.0 / k), confidence_high=0.95)
+    tr = gg.generate_trace(wl, 10.0, np.random.default_rng(seed))
+    return tr.scores[:n].copy(), tr.arrival_t[:n].copy()
+
+
+def build(kind, B, window, scores, now, cfg_kw, graph):
+    import torch
+    import paper_2601_04250_b200 as gg
+    from paper_2601_04250_b200 import serving
+    cfg = gg.ControllerConfig(**cfg_kw)
+    ctl = cfg.build(gg.EnergyLedger())
+    if kind == "resnet18":
+        from paper_2601_04250_b200.resnet18 import ResNet18B200, random_model
+        net = ResNet18B200(random_model(0), max_batch=B)
+        payloads = serving.synthetic_images(32)
+    else:
+        from paper_2601_04250_b200.distilbert import DistilBertB200, random_model
+        net = DistilBertB200(random_model(0), max_batch=B)
+        payloads = serving.synthetic_tokens(32)
+    srv = serving.GatedServer(ctl, net, torch.from_numpy(scores).cuda(),
+                              torch.from_numpy(now).cuda(), payloads, window=window,
+                              outcome=serving.OutcomeModel(**MODEL), fifo_capacity=4096)
+    srv.run(1)
+    if graph:
+        srv.capture()
+    return srv, cfg
+
+
+@pytest.mark.parametrize("kind,k,B,window,graph", [
+    ("resnet18", 1000, 16, 24, True), ("resnet18", 1000, 8, 8, False), ("distilbert", 2, 16, 40, True)])
+def test_serving_loop_vs_oracle(kind, k, B, window, graph):
+    import torch
+    n = 600 if kind == "distilbert" else 300
+    scores, now = make_trace(n, k, seed=k)
+    cfg_kw = dict(alpha=1.0, beta=-0.2, gamma=-0.4, tau0=0.8, tau_inf=0.35, k=1.5,
+                  routing=__import__("paper_2601_04250_b200").RoutePolicy.ALL_BATCHED)
+    srv, cfg = build(kind, B, window, scores, now, cfg_kw, graph)
+    steps = 1
+    while not srv.done():
+        srv.run(1)
+        steps += 1
+        assert steps < 10_000
+    torch.cuda.synchronize()
+    p = G.abi_params(dict(alpha=1.0, beta=-0.2, gamma=-0.4, tau0=0.8, tau_inf=0.35, k=1.5,
+                          ewma_lambda=0.9, direction=0, utility_proxy=0, routing=1,
+                          queue_threshold=4, p95_window=100))
+    dec_o, served_o, st_o = serving_oracle.replay(p, [(scores, now)], window, B, MODEL, steps)
+    dec = srv.decision.cpu().numpy()
+    assert np.array_equal(dec, dec_o[0])
+    pred = srv.predicted.cpu().numpy()
+    assert set(np.nonzero(pred >= 0)[0]) == set(served_o[0])
+    r = srv.results()
+    assert r["overflow"] == 0 and r["served"] == len(served_o[0])
+    got = G.state_dict_of_abi(srv.ctl.state_struct())
+    want = G.state_dict_of_abi(st_o)
+    assert got == want
+    conf = srv.confidence.cpu().numpy()[pred >= 0]
+    assert ((conf > 0) & (conf <= 1)).all()
