@@ -309,7 +309,7 @@ def roofline_forward(srv, net, B):
 
     def fwd():
         if srv.kind == "resnet18":
-            net.forward_nhwc8(B, stream=s, count=full)
+            net.forward_s2d(B, stream=s, count=full)
         else:
             net.forward(srv.tok_ids, srv.tok_mask, batch=B, stream=s, count=full)
     with torch.cuda.stream(s):

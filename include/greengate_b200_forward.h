@@ -89,14 +89,22 @@ int gg_token_gather(const int32_t* pool_ids, const int32_t* pool_mask, int64_t p
  * multiple of 64 >= R*S*C (zero tail); C % 8 == 0, Cout % 64 == 0. */
 int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
               int32_t Cout, int32_t R, int32_t S, int32_t stride, int32_t pad, int32_t Kpad,
-              const float* bias, const void* residual, int32_t relu, void* y,
+              const float* bias, const void* residual, int32_t relu, void* y, int32_t pad_hi,
               const int32_t* count_dev, void* stream);
+/* (pad = top/left padding, pad_hi = bottom/right padding, -1 = same as pad.)
+ * A-operand paths: C % 64 == 0 -> one TMA im2col load per (tap, 64 channels);
+ * C == 16 -> TMA im2col, 4 taps per 64-wide k-block (the space-to-depth stem);
+ * otherwise a cp.async gather. */
 /* fp32 NCHW image batch -> bf16 NHWC with channels zero-padded to cpad (% 8). */
 int gg_nchw_to_nhwc(const float* x, int32_t N, int32_t C, int32_t H, int32_t W, int32_t cpad,
                     void* y, void* stream);
+/* fp32 NCHW RGB batch -> bf16 space-to-depth(2) NHWC, 16 channels
+ * (y[n, i, j, (dy*2+dx)*3 + c] = x[n, c, 2i+dy, 2j+dx]; channels 12..15 = 0).
+ * ResNet-18's 7x7/2 stem conv equals a 4x4/1 conv (pad 2 / 1) over it. */
+int gg_nchw_to_s2d16(const float* x, int32_t N, int32_t H, int32_t W, void* y, void* stream);
 /* Served-batch stem input: image i of the batch = uint8 HWC image
  * pool[batch_ids[i] % pool_size], normalized ((x/255 - mean[c]) / std[c]) into
- * bf16 NHWC with 8 channels (3 real + 5 zero). */
+ * the space-to-depth(2) 16-channel layout of gg_nchw_to_s2d16. */
 int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_ids,
                    const int32_t* count_dev, int32_t B, int32_t H, int32_t W,
                    const float* mean3, const float* std3, void* y, void* stream);

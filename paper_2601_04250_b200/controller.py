@@ -385,6 +385,8 @@ class AdmissionController:
                 _native.ptr(self.state), schedule.t_origin, st))
             self._seed_from_ledger()
         self.ledger._bind(self)
+        import sys
+        self.result_types = sys.modules[__name__]
 
     # ------------------------------------------------------------------ plumbing
     def _stream(self):
@@ -509,14 +511,17 @@ class AdmissionController:
                 raise InvalidDistribution(f"scores must be finite and >= 0: {xs}")
             raise InvalidDistribution(f"scores must sum to 1 (got {sum(xs)!r})")
         admit = code in (_abi.GG_DECISION_DIRECT, _abi.GG_DECISION_BATCHED)
+        # result types: ours, or the host package's when patched into it (integration.py)
+        T = self.result_types
         if admit:
-            reason = Reason.ADMITTED
+            reason = T.Reason.ADMITTED
         else:
-            reason = Reason.BELOW_THRESHOLD if self.direction is Direction.GEQ else Reason.ABOVE_THRESHOLD
-        return AdmissionDecision(admit=admit, path=_PATH_OF_CODE[code],
-                                 breakdown=CostBreakdown(bd[0], info.energy, info.congestion,
-                                                         bd[1], bd[2]),
-                                 reason=reason)
+            reason = (T.Reason.BELOW_THRESHOLD if self.direction is Direction.GEQ
+                      else T.Reason.ABOVE_THRESHOLD)
+        return T.AdmissionDecision(admit=admit, path=T.ServicePath[_PATH_OF_CODE[code].name],
+                                   breakdown=T.CostBreakdown(bd[0], info.energy, info.congestion,
+                                                             bd[1], bd[2]),
+                                   reason=reason)
 
     def record_outcome(self, latency_ms: float, joules: float, queue_depth: int) -> None:
         """controller.py:345-358: one K2 launch (stream-ordered, no host sync)."""
@@ -578,7 +583,7 @@ class AdmissionController:
                 snap_ptr = _native.ptr(self._snap_dev)
         _native.check("gg_admit", self._lib.gg_admit(
             C.byref(self.params), _native.ptr(self.state), _native.ptr(scores), n, k,
-            int(scores.stride(0)), _native.ptr(now), snap_ptr, _native.ptr(out.decision),
+            max(k, int(scores.stride(0))), _native.ptr(now), snap_ptr, _native.ptr(out.decision),
             _native.ptr(out.breakdown), _native.ptr(out.admitted_idx), _native.ptr(out.info),
             _native.ptr(self._ws), self._ws.numel(), self._stream()))
         return out

@@ -26,6 +26,7 @@ struct ConvShape {
   int N, H, W, C;      // input NHWC (C multiple of 8)
   int Ho, Wo, Cout;
   int R, S, stride, pad;
+  int pad_hi;          // bottom/right padding (== pad for symmetric convolutions)
   int Kpad;            // multiple of 64, >= R*S*C
   int M;               // N*Ho*Wo
 };
@@ -62,10 +63,18 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int BN, int STAGES>
+// MODE 0: cp.async gather (any C % 8 == 0).
+// MODE 1 (C % 64 == 0): the A tile of tap (r, s) and channel block c0 is ONE
+//   TMA im2col load (cp.async.bulk.tensor.4d...im2col): 128 consecutive output
+//   pixels (row/image wrap and zero padding done by the TMA unit) x 64
+//   channels, 128B-swizzled.
+// MODE 2 (C == 16, the space-to-depth stem): a 64-wide k-block is 4 taps; each
+//   tap is one im2col load of 128 pixels x 16 channels (32B-swizzled) that one
+//   UMMA K-step consumes.
+template <int BN, int STAGES, int MODE>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_bf16_tcgen05(const __nv_bfloat16* __restrict__ x, const __grid_constant__ CUtensorMap map_w,
-                      ConvShape sh, ConvEpi ep) {
+                      const __grid_constant__ CUtensorMap map_x, ConvShape sh, ConvEpi ep) {
   using L = ConvSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -83,7 +92,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 32 * kConvProdWarps + 1);  // 128 gather arrivals + the B TMA arrive
+      // gather mode: 128 producer arrivals + the B TMA arrive; im2col mode: one expect_tx arrive
+      mbar_init(&full[s], MODE != 0 ? 1 : 32 * kConvProdWarps + 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -99,7 +109,48 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < kConvProdWarps) {
+  if (MODE != 0 && warp < kConvProdWarps) {
+    // ===== TMA producer (im2col A + tiled B) =====
+    if (threadIdx.x == 0) {
+      tma_prefetch(&map_x);
+      const int cblocks = sh.C / 64;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int tm = tile % tiles_m, tn = tile / tiles_m;
+        const int m0 = tm * 128;
+        const int n0 = m0 / (sh.Ho * sh.Wo);
+        const int rem = m0 - n0 * sh.Ho * sh.Wo;
+        const int ho0 = rem / sh.Wo, wo0 = rem - (rem / sh.Wo) * sh.Wo;
+        const int wc = wo0 * sh.stride - sh.pad, hc = ho0 * sh.stride - sh.pad;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          uint8_t* sa = smem + s * L::STAGE_BYTES;
+          mbar_expect_tx(&full[s], L::STAGE_BYTES);
+          constexpr int kLoads = MODE == 1 ? 1 : 4;
+#pragma unroll
+          for (int q = 0; q < kLoads; ++q) {
+            int tap, c0;
+            if (MODE == 1) {
+              tap = kb / cblocks;
+              c0 = (kb - tap * cblocks) * 64;
+            } else {
+              tap = kb * 4 + q;
+              c0 = 0;
+            }
+            const int rr = tap / sh.S, ss = tap - rr * sh.S;
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(sa + q * 4096)),
+                "l"(&map_x), "r"(smem_u32(&full[s])), "r"(c0), "r"(wc), "r"(hc), "r"(n0),
+                "h"((uint16_t)ss), "h"((uint16_t)rr)
+                : "memory");
+          }
+          tma_load_2d(sa + L::A_BYTES, &map_w, &full[s], kb * 64, tn * BN);
+        }
+      }
+    }
+  } else if (warp < kConvProdWarps) {
     // ===== A gather: thread = tile row (output pixel) =====
     const int r_local = threadIdx.x;  // 0..127
     const uint32_t row_off = (r_local >> 3) * 1024 + (r_local & 7) * 128;
@@ -168,7 +219,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const uint32_t sb = sa + L::A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma_bf16(d_tmem, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sb + kk * 32), idesc,
+            umma_bf16(d_tmem, MODE == 2 ? sdesc_k_sw32(sa + kk * 4096) : sdesc_k_sw128(sa + kk * 32),
+                      sdesc_k_sw128(sb + kk * 32), idesc,
                       (kb | kk) != 0);
           umma_commit(&empty[s]);
         }
@@ -243,11 +295,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   }
 }
 
-template <int BN, int STAGES>
-static int launch_conv(const __nv_bfloat16* x, const CUtensorMap& mw, const ConvShape& sh,
-                       const ConvEpi& ep, cudaStream_t s) {
+template <int BN, int STAGES, int MODE>
+static int launch_conv(const __nv_bfloat16* x, const CUtensorMap& mw, const CUtensorMap& mx,
+                       const ConvShape& sh, const ConvEpi& ep, cudaStream_t s) {
   using L = ConvSmem<BN, STAGES>;
-  auto kern = conv_bf16_tcgen05<BN, STAGES>;
+  auto kern = conv_bf16_tcgen05<BN, STAGES, MODE>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL) != cudaSuccess)
@@ -256,9 +308,35 @@ static int launch_conv(const __nv_bfloat16* x, const CUtensorMap& mw, const Conv
   }
   const int tiles = ((sh.M + 127) / 128) * (sh.Cout / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kConvThreads, L::TOTAL, s>>>(x, mw, sh, ep);
+  kern<<<grid, kConvThreads, L::TOTAL, s>>>(x, mw, mx, sh, ep);
   GG_LAUNCH_OK();
   return GG_OK;
+}
+
+// TMA im2col map over an NHWC bf16 activation: 128 output pixels x 64 channels per load.
+static PFN_cuTensorMapEncodeIm2col_v12000 g_encode_im2col = nullptr;
+static int make_map_im2col(CUtensorMap* map, const void* x, const ConvShape& sh, int cpb) {
+  if (!g_encode_im2col) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return GG_ERR_CUDA;
+    g_encode_im2col = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(fn);
+  }
+  cuuint64_t dims[4] = {(cuuint64_t)sh.C, (cuuint64_t)sh.W, (cuuint64_t)sh.H, (cuuint64_t)sh.N};
+  cuuint64_t strides[3] = {(cuuint64_t)sh.C * 2, (cuuint64_t)sh.W * sh.C * 2,
+                           (cuuint64_t)sh.H * sh.W * sh.C * 2};
+  // traversal box of the receptive-field origin: [-pad, W + pad - S] (CUTLASS fprop convention)
+  int lower[2] = {-sh.pad, -sh.pad};
+  int upper[2] = {sh.pad_hi - (sh.S - 1), sh.pad_hi - (sh.R - 1)};
+  cuuint32_t estr[4] = {1, (cuuint32_t)sh.stride, (cuuint32_t)sh.stride, 1};
+  CUresult r = g_encode_im2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims,
+                               strides, lower, upper, (cuuint32_t)cpb, 128, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               cpb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? GG_OK : GG_ERR_INVALID_ARGUMENT;
 }
 
 // ---- pooling / layout kernels (HBM-bound) -----------------------------------
@@ -352,31 +430,61 @@ using namespace gg;
 extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
                          int32_t Cout, int32_t R, int32_t S, int32_t stride, int32_t pad,
                          int32_t Kpad, const float* bias, const void* residual, int32_t relu,
-                         void* y, const int32_t* count_dev, void* stream) {
+                         void* y, int32_t pad_hi, const int32_t* count_dev, void* stream) {
   if (!x || !w || !y || !bias || N <= 0 || H <= 0 || W <= 0 || R <= 0 || S <= 0 || stride <= 0)
     return GG_ERR_INVALID_ARGUMENT;
-  if (C % 8 || Kpad % 64 || Kpad < R * S * C || Cout % 64) return GG_ERR_UNSUPPORTED;
+  if (C % 8 || Kpad % 64 || Kpad < R * S * C || Cout % 64 || pad < 0) return GG_ERR_UNSUPPORTED;
   ConvShape sh;
   sh.N = N; sh.H = H; sh.W = W; sh.C = C; sh.Cout = Cout;
   sh.R = R; sh.S = S; sh.stride = stride; sh.pad = pad; sh.Kpad = Kpad;
-  sh.Ho = (H + 2 * pad - R) / stride + 1;
-  sh.Wo = (W + 2 * pad - S) / stride + 1;
+  sh.pad_hi = pad_hi < 0 ? pad : pad_hi;
+  sh.Ho = (H + pad + sh.pad_hi - R) / stride + 1;
+  sh.Wo = (W + pad + sh.pad_hi - S) / stride + 1;
   const int64_t M = (int64_t)N * sh.Ho * sh.Wo;
   if (M > 0x7fffffff) return GG_ERR_UNSUPPORTED;
   sh.M = (int)M;
   ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
              reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev};
-  const int bn = Cout >= 256 ? 256 : Cout;
-  CUtensorMap mw;
+  // N tile: the widest of 256/128/64 that still gives at least one full wave of CTAs
+  const int64_t tiles_m = (M + 127) / 128;
+  int bn = 64;
+  for (int cand : {256, 128}) {
+    if (cand <= Cout && Cout % cand == 0 && tiles_m * (Cout / cand) >= num_sms()) {
+      bn = cand;
+      break;
+    }
+  }
+  CUtensorMap mw, mx;
   int rc = make_map_2d(&mw, w, Cout, Kpad, Kpad, bn);
   if (rc) return rc;
+  const int mode = (C % 64 == 0 && Kpad == R * S * C) ? 1
+                   : (C == 16 && (R * S) % 4 == 0 && Kpad == R * S * C) ? 2 : 0;
+  if (mode) {
+    rc = make_map_im2col(&mx, x, sh, mode == 1 ? 64 : 16);
+    if (rc) return rc;
+  } else {
+    mx = mw;  // unused by the gather path
+  }
   cudaStream_t s = gg_stream(stream);
   const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  if (mode == 1) {
+    switch (bn) {
+      case 256: return launch_conv<256, 4, 1>(xb, mw, mx, sh, ep, s);
+      case 128: return launch_conv<128, 6, 1>(xb, mw, mx, sh, ep, s);
+      default: return launch_conv<64, 8, 1>(xb, mw, mx, sh, ep, s);
+    }
+  }
+  if (mode == 2) {
+    switch (bn) {
+      case 256: return launch_conv<256, 4, 2>(xb, mw, mx, sh, ep, s);
+      case 128: return launch_conv<128, 6, 2>(xb, mw, mx, sh, ep, s);
+      default: return launch_conv<64, 8, 2>(xb, mw, mx, sh, ep, s);
+    }
+  }
   switch (bn) {
-    case 256: return launch_conv<256, 4>(xb, mw, sh, ep, s);
-    case 128: return launch_conv<128, 6>(xb, mw, sh, ep, s);
-    case 64: return launch_conv<64, 8>(xb, mw, sh, ep, s);
-    default: return GG_ERR_UNSUPPORTED;
+    case 256: return launch_conv<256, 4, 0>(xb, mw, mx, sh, ep, s);
+    case 128: return launch_conv<128, 6, 0>(xb, mw, mx, sh, ep, s);
+    default: return launch_conv<64, 8, 0>(xb, mw, mx, sh, ep, s);
   }
 }
 

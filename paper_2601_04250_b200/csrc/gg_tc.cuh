@@ -130,6 +130,18 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// K-major, 32-byte swizzle (rows of 16 bf16 = one UMMA K step), 8-row atoms of
+// 256 B stacked densely along M/N.  Used for 16-channel im2col tiles.
+__device__ __forceinline__ uint64_t sdesc_k_sw32(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;        // SBO: 8 rows x 32 B
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;                 // SWIZZLE_32B
+  return d;
+}
+
 // kind::f16 instruction descriptor: bf16 A/B, fp32 D, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4)                 // D format f32

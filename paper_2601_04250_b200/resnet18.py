@@ -44,24 +44,63 @@ class _Conv:
         self.cin = cpad
         self.r, self.s = conv.kernel_size
         self.stride = conv.stride[0]
-        self.pad = conv.padding[0]
+        self.pad = self.pad_hi = conv.padding[0]
+        self.algo_macs_per_pixel = self.r * self.s * conv.in_channels * self.cout
 
     def out_hw(self, h, w):
-        return ((h + 2 * self.pad - self.r) // self.stride + 1,
-                (w + 2 * self.pad - self.s) // self.stride + 1)
+        return ((h + self.pad + self.pad_hi - self.r) // self.stride + 1,
+                (w + self.pad + self.pad_hi - self.s) // self.stride + 1)
 
     def __call__(self, lib, x, n, h, w, y, st, residual=None, relu=True, count=None):
         _native.check("gg_conv2d", lib.gg_conv2d(
             C.c_void_p(x), n, h, w, self.cin, _native.ptr(self.w), self.cout, self.r, self.s,
             self.stride, self.pad, self.kpad, _native.ptr(self.b),
             None if residual is None else C.c_void_p(residual), int(relu), C.c_void_p(y),
-            _native.ptr(count), st))
+            self.pad_hi, _native.ptr(count), st))
         return self.out_hw(h, w)
 
     def flops(self, n, h, w):
+        """Algorithmic FLOPs of the original convolution (padding channels excluded)."""
         ho, wo = self.out_hw(h, w)
-        real_cin = self.cin if self.cin != 8 else 3
-        return 2.0 * n * ho * wo * self.cout * self.r * self.s * real_cin
+        return 2.0 * n * ho * wo * self.algo_macs_per_pixel
+
+
+class _StemConv(_Conv):
+    """conv1 (7x7 / 2, pad 3, 3 -> 64) + bn1 as a 4x4 / 1 conv over the
+    space-to-depth(2) input (16 channels: (dy, dx, c) of each 2x2 cell, 12 real).
+
+    Output (ho, wo) reads input rows 2ho - 3 + r, r = 0..6; with r = 2i + dy - 1
+    that is s2d row ho - 2 + i (i = 0..3) and sub-row dy, so
+    w'[co, i, j, (dy*2+dx)*3 + c] = w[co, c, 2i+dy-1, 2j+dx-1] (0 outside 0..6),
+    padding 2 before and 1 after.  K = 4*4*16 = 256 instead of 7*7*8 = 392(448).
+    """
+
+    def __init__(self, conv, bn, device):
+        import torch
+        w = conv.weight.detach().float().cpu()
+        scale = bn.weight.detach().float() / torch.sqrt(bn.running_var.detach().float() + bn.eps)
+        bias = bn.bias.detach().float() - bn.running_mean.detach().float() * scale
+        w = w * scale.cpu()[:, None, None, None]
+        cout = w.shape[0]
+        wp = torch.zeros((cout, 4, 4, 16), dtype=torch.float32)
+        for i in range(4):
+            for dy in range(2):
+                r = 2 * i + dy - 1
+                if not 0 <= r <= 6:
+                    continue
+                for j in range(4):
+                    for dx in range(2):
+                        s = 2 * j + dx - 1
+                        if not 0 <= s <= 6:
+                            continue
+                        for c in range(3):
+                            wp[:, i, j, (dy * 2 + dx) * 3 + c] = w[:, c, r, s]
+        self.w = wp.reshape(cout, 256).to(device=device, dtype=torch.bfloat16).contiguous()
+        self.b = bias.to(device=device).contiguous()
+        self.kpad, self.cout, self.cin = 256, cout, 16
+        self.r = self.s = 4
+        self.stride, self.pad, self.pad_hi = 1, 2, 1
+        self.algo_macs_per_pixel = 7 * 7 * 3 * cout
 
 
 class ResNet18B200:
@@ -73,7 +112,7 @@ class ResNet18B200:
         self.device = torch.device(device)
         self.max_batch, self.image = max_batch, image
         m = tv_model.eval()
-        self.stem = _Conv(m.conv1, m.bn1, 8, self.device)
+        self.stem = _StemConv(m.conv1, m.bn1, self.device)
         self.blocks = []
         cin = 64
         for layer in (m.layer1, m.layer2, m.layer3, m.layer4):
@@ -95,7 +134,7 @@ class ResNet18B200:
         self.b_fc = bfc.to(self.device).contiguous()
         B, H = max_batch, image
         z = dict(dtype=torch.bfloat16, device=self.device)
-        self.x8 = torch.empty(B * H * H * 8, **z)
+        self.x16 = torch.empty(B * (H // 2) * (H // 2) * 16, **z)   # space-to-depth stem input
         big = B * (H // 2) * (H // 2) * 64
         self.buf = [torch.empty(big, **z) for _ in range(3)]
         self.pooled = torch.empty((B, 512), **z)
@@ -122,19 +161,19 @@ class ResNet18B200:
         assert B <= self.max_batch
         H = self.image
         st = _native.stream_ptr(stream)
-        _native.check("gg_nchw_to_nhwc", self.lib.gg_nchw_to_nhwc(
-            _native.ptr(images), B, 3, H, H, 8, _native.ptr(self.x8), st))
-        return self.forward_nhwc8(B, stream=stream)
+        _native.check("gg_nchw_to_s2d16", self.lib.gg_nchw_to_s2d16(
+            _native.ptr(images), B, H, H, _native.ptr(self.x16), st))
+        return self.forward_s2d(B, stream=stream)
 
-    def forward_nhwc8(self, B: int, stream=None, count=None):
-        """Forward from self.x8 (bf16 NHWC, 8 channels).  count: optional CUDA
-        int32 [1] = valid images (dynamic batch read on the device)."""
+    def forward_s2d(self, B: int, stream=None, count=None):
+        """Forward from self.x16 (bf16 space-to-depth(2) NHWC, 16 channels).
+        count: optional CUDA int32 [1] = valid images (dynamic batch read on the device)."""
         lib = self.lib
         H = self.image
         st = _native.stream_ptr(stream)
         cnt = _native.ptr(count)
         a, b, c = (t.data_ptr() for t in self.buf)
-        h, w = self.stem(lib, self.x8.data_ptr(), B, H, H, a, st, count=count)   # 112x112x64
+        h, w = self.stem(lib, self.x16.data_ptr(), B, H // 2, H // 2, a, st, count=count)  # 112x112x64
         _native.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(C.c_void_p(a), B, h, w, 64,
                                                             C.c_void_p(b), cnt, st))
         h, w = (h + 1) // 2, (w + 1) // 2                                      # 56x56x64

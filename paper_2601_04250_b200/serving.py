@@ -112,8 +112,8 @@ class GatedServer:
                 _native.ptr(pool), int(pool.shape[0]), _native.ptr(self.batch_ids),
                 _native.ptr(self.count), B, H, int(pool.shape[2]),
                 self.mean.numpy().ctypes.data_as(C.c_void_p),
-                self.std.numpy().ctypes.data_as(C.c_void_p), _native.ptr(self.net.x8), st))
-            logits = self.net.forward_nhwc8(B, stream=self._cur_stream, count=self.count)
+                self.std.numpy().ctypes.data_as(C.c_void_p), _native.ptr(self.net.x16), st))
+            logits = self.net.forward_s2d(B, stream=self._cur_stream, count=self.count)
         else:
             ids, mask = self.payloads
             _native.check("gg_token_gather", lib.gg_token_gather(
@@ -180,11 +180,11 @@ class GatedServer:
 
     def run(self, steps: int) -> None:
         torch = self.torch
-        for _ in range(steps):
-            if self.graph is not None:
-                self.graph.replay()
-            else:
-                with torch.cuda.stream(self.stream):
+        with torch.cuda.stream(self.stream):   # replay() launches on the current stream
+            for _ in range(steps):
+                if self.graph is not None:
+                    self.graph.replay()
+                else:
                     self.step()
         self.steps_run += steps
 

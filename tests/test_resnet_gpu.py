@@ -46,7 +46,34 @@ def test_conv_vs_torch(env, n, h, cin, cout, r, stride, pad, res):
     y = torch.empty((n, ho, ho, cout), dtype=torch.bfloat16, device="cuda")
     nat.check("gg_conv2d", lib.gg_conv2d(nat.ptr(xn), n, h, h, cin, nat.ptr(wk), cout, r, r, stride,
                                          pad, kpad, nat.ptr(b), nat.ptr(resid), 1, nat.ptr(y),
-                                         None, nat.stream_ptr()))
+                                         -1, None, nat.stream_ptr()))
+    got = y.float().permute(0, 3, 1, 2)
+    err = (got - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
+def test_space_to_depth_stem_vs_torch(env):
+    """7x7/2 pad 3 conv (conv1+bn1) == 4x4/1 pad (2,1) conv over the s2d(2) input."""
+    torch, nat, lib = env
+    from paper_2601_04250_b200.resnet18 import _StemConv
+    g = torch.Generator().manual_seed(3)
+    conv = torch.nn.Conv2d(3, 64, 7, 2, 3, bias=False)
+    bn = torch.nn.BatchNorm2d(64).eval()
+    with torch.no_grad():
+        conv.weight.copy_(torch.randn(conv.weight.shape, generator=g) * 0.1)
+        bn.running_mean.copy_(torch.randn(64, generator=g) * 0.1)
+        bn.running_var.copy_(torch.rand(64, generator=g) + 0.5)
+        bn.weight.copy_(torch.rand(64, generator=g) + 0.5)
+        bn.bias.copy_(torch.randn(64, generator=g) * 0.1)
+    stem = _StemConv(conv, bn, "cuda")
+    x = torch.randn((3, 3, 224, 224), generator=g).cuda()
+    x16 = torch.empty((3, 112, 112, 16), dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_nchw_to_s2d16", lib.gg_nchw_to_s2d16(nat.ptr(x), 3, 224, 224, nat.ptr(x16),
+                                                       nat.stream_ptr()))
+    y = torch.empty((3, 112, 112, 64), dtype=torch.bfloat16, device="cuda")
+    stem(lib, x16.data_ptr(), 3, 112, 112, y.data_ptr(), nat.stream_ptr(), relu=True)
+    with torch.no_grad():
+        ref = torch.relu(bn.cuda()(conv.cuda()(x.to(torch.bfloat16).float())))
     got = y.float().permute(0, 3, 1, 2)
     err = (got - ref).abs().max().item()
     assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
