@@ -398,48 +398,107 @@ __global__ void __launch_bounds__(THREADS) admit_small_kernel(AdmitArgs a) {
   finish_tile<THREADS, RPT>(a, sm, tile0, ballots, my_skip, my_inv, my_bad);
 }
 
-// K1, large K (ResNet K=1000): one row per thread, the block's [128 x 32]
-// column chunks staged through shared memory with coalesced loads; the row
-// scan stays sequential (CPython sum order) per thread.  Row stride 33
-// doubles keeps the per-thread column reads bank-conflict free.
-constexpr int kLargeThreads = 128;
+// K1, large K (ResNet K=1000).  The CPython sums are sequential per row, but
+// the K logs are independent, so a block owns 32 rows and splits the work:
+//   warps 2..7  stream [32 x 32] column chunks in with coalesced loads and
+//               compute p*log(p) for every element (FP64-throughput bound,
+//               spread over many SMs instead of one thread per row);
+//   warp 0      lane r: Neumaier entropy sum of row r over the precomputed terms
+//   warp 1      lane r: validation (finite, >= 0), Neumaier total, max
+// double-buffered through shared memory with named barriers, so the two
+// sequential chains overlap the log computation of the next chunk.
+constexpr int kLargeThreads = 256;
+constexpr int kLargeRows = 32;
 constexpr int kChunk = 32;
+constexpr int kProdThreads = kLargeThreads - 64;
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 __global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a) {
   __shared__ AdmitShared<kLargeThreads, 1> sm;
-  __shared__ double tile[kLargeThreads][kChunk + 1];
-  const int tid = threadIdx.x;
+  __shared__ double raw[2][kLargeRows][kChunk + 1];
+  __shared__ double term[2][kLargeRows][kChunk + 1];
+  __shared__ double tot_s[kLargeRows], max_s[kLargeRows];
+  __shared__ int ok_s[kLargeRows];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) block_setup(a, sm);
   __syncthreads();
   const BatchConst b = sm.bc;
-  const int64_t tile0 = (int64_t)sm.vb * kLargeThreads;
+  const int64_t tile0 = (int64_t)sm.vb * kLargeRows;
   const int64_t nw = sm.nw, row0 = sm.row0;
   const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
-  const int64_t r = tile0 + tid;
-  const bool in = r < nw;
-  const int64_t g = row0 + r;
-  RowAcc acc;
-  for (int c0 = 0; c0 < a.k; c0 += kChunk) {
-    const int cw = min(kChunk, a.k - c0);
-#pragma unroll 4
-    for (int e = tid; e < kLargeThreads * kChunk; e += kLargeThreads) {
-      const int rr = e / kChunk, cc = e % kChunk;
-      const int64_t lr = tile0 + rr;
-      double v = 0.0;
-      if (lr < nw && cc < cw) v = __ldg(a.probs + (row0 + lr) * a.stride + c0 + cc);
-      tile[rr][cc] = v;
+  const int nchunks = (a.k + kChunk - 1) / kChunk;
+  // named barriers: 1,2 = buffer full; 3,4 = buffer free
+  if (warp >= 2) {
+    const int pt = tid - 64;
+    for (int c = 0; c < nchunks; ++c) {
+      const int buf = c & 1, c0 = c * kChunk, cw = min(kChunk, a.k - c0);
+      if (c >= 2) named_sync(3 + buf, kLargeThreads);
+      for (int e = pt; e < kLargeRows * kChunk; e += kProdThreads) {
+        const int rr = e / kChunk, cc = e % kChunk;
+        const int64_t lr = tile0 + rr;
+        double v = 0.0, t = 0.0;
+        if (lr < nw && cc < cw) {
+          v = __ldg(a.probs + (row0 + lr) * a.stride + c0 + cc);
+          if (entropy && v > 0.0) t = f64_mul(v, log(v));
+        }
+        raw[buf][rr][cc] = v;
+        term[buf][rr][cc] = t;
+      }
+      named_arrive(1 + buf, kLargeThreads);
     }
-    __syncthreads();
-    if (in)
-      for (int cc = 0; cc < cw; ++cc) acc.add(tile[tid][cc], entropy);
-    __syncthreads();
+  } else {
+    NeumaierSum s;   // warp 0: entropy terms; warp 1: the validation total
+    bool ok = true, first = true;
+    double mx = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int buf = c & 1, cw = min(kChunk, a.k - c * kChunk);
+      named_sync(1 + buf, kLargeThreads);
+      if (warp == 0) {
+        if (entropy)
+          for (int cc = 0; cc < cw; ++cc)
+            if (raw[buf][lane][cc] > 0.0) s.add(term[buf][lane][cc]);
+      } else {
+        for (int cc = 0; cc < cw; ++cc) {
+          const double x = raw[buf][lane][cc];
+          if (!isfinite(x) || x < 0.0) ok = false;
+          s.add(x);
+          if (first || x > mx) mx = x;
+          first = false;
+        }
+      }
+      if (c + 2 < nchunks) named_arrive(3 + buf, kLargeThreads);
+    }
+    if (warp == 1) {
+      tot_s[lane] = s.result();
+      ok_s[lane] = ok;
+      max_s[lane] = mx;
+    }
+    named_sync(5, 64);
+    if (warp == 0) {
+      // fold the two chains into the RowAcc::finish logic (controller.py:126-148)
+      const bool valid = ok_s[lane] && a.k >= 2 && !(fabs(f64_sub(tot_s[lane], 1.0)) > 1e-9);
+      double u = 0.0;
+      if (valid) u = entropy ? clamp01(f64_div(-s.result(), a.ln_k)) : f64_sub(1.0, max_s[lane]);
+      tot_s[lane] = u;
+      ok_s[lane] = valid;
+    }
   }
+  __syncthreads();
+  const int64_t r = tile0 + tid;           // rows live on warp 0's lanes
+  const bool in = warp == 0 && r < nw;
+  const int64_t g = row0 + r;
   uint8_t code = GG_DECISION_SKIP;
   int my_skip = 0, my_inv = 0;
   unsigned long long my_bad = 0;
   if (in) {
-    double u, jv = 0.0, tau = 0.0;
-    if (acc.finish(a.k, entropy, a.ln_k, u)) {
+    double u = tot_s[lane], jv = 0.0, tau = 0.0;
+    if (ok_s[lane]) {
       code = decide_row(a, b, u, a.now[g], jv, tau);
       if (code == GG_DECISION_SKIP) ++my_skip;
     } else {
@@ -462,68 +521,91 @@ __global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a)
 // ---------------------------------------------------------------------------
 // K2: record_outcome() x n, sequential in completion order (controller.py:345-358).
 // One warp: scalars are evaluated redundantly by every lane (identical values);
-// the sorted latency window is updated with warp-parallel shifts so the
-// nearest-rank p95 (telemetry.py:35-46) is one shared-memory read.
+// the sorted latency window lives in registers (position i = slot j * 32 +
+// lane) and is updated with warp shuffles, so an append/evict plus the
+// nearest-rank p95 (telemetry.py:35-46) is a few dozen instructions.
 
-__device__ __forceinline__ int warp_min_int(int v) {
+template <int S>  // slots per lane: window capacity 32 * S
+struct RegSorted {
+  double v[S];
+  __device__ __forceinline__ void load(const double* src, int count) {
+    const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// Remove one element equal to `x` from srt[0..cnt).
-__device__ void sorted_remove(double* srt, int cnt, double x) {
-  const int lane = threadIdx.x & 31;
-  int pos = cnt;
-  for (int base = 0; base < cnt; base += 32) {
-    int i = base + lane;
-    unsigned m = __ballot_sync(0xffffffffu, i < cnt && srt[i] == x);
-    if (m) {
-      pos = base + __ffs(m) - 1;
-      break;
+    for (int j = 0; j < S; ++j) {
+      const int i = j * 32 + lane;
+      v[j] = i < count ? src[i] : INFINITY;
     }
   }
-  if (pos >= cnt) return;  // not found (NaN); window content is then undefined like sorted()
-  for (int base = pos; base < cnt - 1; base += 32) {  // ascending left shift
-    int i = base + lane;
-    double v = (i + 1 < cnt) ? srt[i + 1] : 0.0;
-    __syncwarp();
-    if (i + 1 < cnt) srt[i] = v;
-    __syncwarp();
+  __device__ __forceinline__ void store(double* dst, int count) const {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (j * 32 + lane < count) dst[j * 32 + lane] = v[j];
   }
-}
-
-// Insert `x` into srt[0..cnt) keeping it ascending (after all elements < x).
-__device__ void sorted_insert(double* srt, int cnt, double x) {
-  const int lane = threadIdx.x & 31;
-  int less = 0;
-  for (int i = lane; i < cnt; i += 32) less += (srt[i] < x) ? 1 : 0;
-  const int pos = warp_sum(less);
-  for (int top = cnt; top > pos; top -= 32) {  // descending right shift of [pos, cnt)
-    int i = top - 1 - lane;
-    double v = (i >= pos) ? srt[i] : 0.0;
-    __syncwarp();
-    if (i >= pos) srt[i + 1] = v;
-    __syncwarp();
+  __device__ __forceinline__ int count_less(double x) const {
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) c += __popc(__ballot_sync(0xffffffffu, v[j] < x));
+    return c;
   }
-  if (lane == 0) srt[pos] = x;
-  __syncwarp();
-}
+  __device__ __forceinline__ int find(double x, int count) const {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const unsigned m = __ballot_sync(0xffffffffu, j * 32 + lane < count && v[j] == x);
+      if (m) return j * 32 + __ffs(m) - 1;
+    }
+    return -1;
+  }
+  __device__ __forceinline__ double at(int i) const {
+    double r = 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+      if (j == (i >> 5)) r = v[j];
+    return __shfl_sync(0xffffffffu, r, i & 31);
+  }
+  // positions >= pos move up by one, x lands at pos (positions descending so
+  // lane 0 still sees the old last element of the previous slot)
+  __device__ __forceinline__ void insert_at(int pos, double x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = S - 1; j >= 0; --j) {
+      const double up = __shfl_up_sync(0xffffffffu, v[j], 1);
+      const double carry = j > 0 ? __shfl_sync(0xffffffffu, v[j > 0 ? j - 1 : 0], 31) : 0.0;
+      const int i = j * 32 + lane;
+      const double nv = lane == 0 ? carry : up;
+      if (i > pos) v[j] = nv;
+      else if (i == pos) v[j] = x;
+    }
+  }
+  // positions > pos move down by one; the freed last position becomes +inf
+  __device__ __forceinline__ void remove_at(int pos) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const double down = __shfl_down_sync(0xffffffffu, v[j], 1);
+      const double carry = j + 1 < S ? __shfl_sync(0xffffffffu, v[j + 1 < S ? j + 1 : j], 0) : INFINITY;
+      const int i = j * 32 + lane;
+      if (i >= pos) v[j] = lane == 31 ? carry : down;
+    }
+  }
+};
 
 // Outcomes come either from three arrays (n of them) or from G exchange slots
-// (fp64 [3*B + 2] each: latency | joules | queue depth | count | fifo depth),
-// applied slot by slot in rank order.
+// (fp64 GG_SLOT_LEN(B) each, see greengate_b200.h), applied slot by slot in
+// rank order.
+template <int S>
 __global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, const double* lat,
                                                      const double* jou, const int32_t* qd, int64_t n,
                                                      int set_qd, int64_t* err, const double* slots,
                                                      int G, int B, int rank, gg_fifo* fifo) {
   __shared__ double win[GG_P95_WINDOW_MAX];
-  __shared__ double srt[GG_P95_WINDOW_MAX];
   const int lane = threadIdx.x;
   const int cap = p.p95_window;
   int count = st->win_count, head = st->win_head;
   for (int i = lane; i < cap; i += 32) win[i] = st->win[i];
-  for (int i = lane; i < count; i += 32) srt[i] = st->win_sorted[i];
+  RegSorted<S> srt;
+  srt.load(st->win_sorted, count);
   double ewma = st->ewma_joules_per_request, total = st->total_joules, p95 = st->p95_current;
   int64_t seen = st->samples_seen, outc = st->outcomes_total;
   gg_channel ce = st->n_energy, cq = st->n_queue_depth, cp = st->n_p95_ms;
@@ -569,18 +651,19 @@ __global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, 
     if (count < cap) {
       if (lane == 0) win[(head + count) % cap] = L;
       __syncwarp();
-      sorted_insert(srt, count, L);
+      srt.insert_at(srt.count_less(L), L);
       count += 1;
     } else {
       const double old = win[head];
       __syncwarp();
       if (lane == 0) win[head] = L;
       head = (head + 1) % cap;
-      sorted_remove(srt, count, old);
-      sorted_insert(srt, count - 1, L);
+      const int at = srt.find(old, count);
+      if (at >= 0) srt.remove_at(at);  // (not found only for NaN latencies)
+      srt.insert_at(srt.count_less(L), L);
     }
     const int rank = (int)ceil(f64_mul(0.95, (double)count));  // ceil(95.0/100.0 * n)
-    p95 = srt[rank - 1];
+    p95 = srt.at(rank - 1);
     ch_observe(ce, ewma);
     ch_observe(cq, (double)Q);
     ch_observe(cp, p95);
@@ -600,7 +683,7 @@ __global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, 
     st->skipped_total += skip_other;
   }
   for (int i = lane; i < cap; i += 32) st->win[i] = win[i];
-  for (int i = lane; i < count; i += 32) st->win_sorted[i] = srt[i];
+  srt.store(st->win_sorted, count);
   if (lane == 0) {
     st->ewma_joules_per_request = ewma;
     st->total_joules = total;
@@ -766,17 +849,37 @@ int gg_set_queue_depth(gg_state* state_dev, int32_t queue_depth, void* stream) {
 }
 
 static int64_t admit_blocks(int64_t n, int32_t k) {
-  const int64_t rows_per_block = (k <= 16) ? 256 * 4 : kLargeThreads;
+  const int64_t rows_per_block = (k <= 16) ? 256 * 4 : kLargeRows;
   int64_t nb = (n + rows_per_block - 1) / rows_per_block;
   return nb < 1 ? 1 : nb;
 }
 
 size_t gg_admit_workspace_bytes(int64_t n) {
-  const int64_t nb = (n + kLargeThreads - 1) / kLargeThreads;  // worst case over kernels
+  const int64_t nb = (n + kLargeRows - 1) / kLargeRows;  // worst case over kernels
   return kWsHeader + sizeof(unsigned long long) * (size_t)(nb < 1 ? 1 : nb);
 }
 
 static int launch_admit(const AdmitArgs& a, void* stream);
+
+// K2 instantiation by window capacity (register slots per lane = ceil(W / 32)).
+static int launch_outcome(const gg_params& p, gg_state* st, const double* lat, const double* jou,
+                          const int32_t* qd, int64_t n, int set_qd, int64_t* err,
+                          const double* slots, int G, int B, int rank, gg_fifo* fifo,
+                          void* stream) {
+  cudaStream_t s = gg_stream(stream);
+  const int w = p.p95_window;
+#define GG_OUTCOME(SLOTS) \
+  outcome_kernel<SLOTS><<<1, 32, 0, s>>>(p, st, lat, jou, qd, n, set_qd, err, slots, G, B, rank, fifo)
+  if (w <= 32) GG_OUTCOME(1);
+  else if (w <= 64) GG_OUTCOME(2);
+  else if (w <= 128) GG_OUTCOME(4);
+  else if (w <= 256) GG_OUTCOME(8);
+  else if (w <= 512) GG_OUTCOME(16);
+  else GG_OUTCOME(32);
+#undef GG_OUTCOME
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
 
 int gg_admit(const gg_params* params, gg_state* state_dev, const double* probs_dev, int64_t n,
              int32_t k, int64_t row_stride, const double* now_dev, const gg_snapshot* snapshot_dev,
@@ -837,11 +940,8 @@ int gg_outcome(const gg_params* params, gg_state* state_dev, const double* laten
   if (rc != GG_OK) return rc;
   if (!state_dev || n < 0) return GG_ERR_INVALID_ARGUMENT;
   if (n > 0 && (!latency_ms_dev || !joules_dev || !queue_depth_dev)) return GG_ERR_INVALID_ARGUMENT;
-  outcome_kernel<<<1, 32, 0, gg_stream(stream)>>>(*params, state_dev, latency_ms_dev, joules_dev,
-                                                   queue_depth_dev, n, set_queue_depth,
-                                                   error_index_dev, nullptr, 0, 0, 0, nullptr);
-  GG_LAUNCH_OK();
-  return GG_OK;
+  return launch_outcome(*params, state_dev, latency_ms_dev, joules_dev, queue_depth_dev, n,
+                        set_queue_depth, error_index_dev, nullptr, 0, 0, 0, nullptr, stream);
 }
 
 int gg_outcome_slots(const gg_params* params, gg_state* state_dev, const double* slots_dev,
@@ -851,11 +951,8 @@ int gg_outcome_slots(const gg_params* params, gg_state* state_dev, const double*
   if (rc != GG_OK) return rc;
   if (!state_dev || !slots_dev || G < 1 || B < 1 || rank < 0 || rank >= G)
     return GG_ERR_INVALID_ARGUMENT;
-  outcome_kernel<<<1, 32, 0, gg_stream(stream)>>>(*params, state_dev, nullptr, nullptr, nullptr, 0,
-                                                   1, error_index_dev, slots_dev, G, B, rank,
-                                                   fifo_dev);
-  GG_LAUNCH_OK();
-  return GG_OK;
+  return launch_outcome(*params, state_dev, nullptr, nullptr, nullptr, 0, 1, error_index_dev,
+                        slots_dev, G, B, rank, fifo_dev, stream);
 }
 
 int gg_admit_stream(const gg_params* params, gg_state* state_dev, gg_fifo* fifo_dev,

@@ -445,13 +445,24 @@ extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t
   sh.M = (int)M;
   ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
              reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev};
-  // N tile: the widest of 256/128/64 that still gives at least one full wave of CTAs
+  // N tile: minimize the larger of (tensor time of the busiest SM) and (operand
+  // bytes streamed from L2: every tile re-reads its A rows and its B columns per
+  // k-block).  Measured on B200: ~8 TB/s of TMA operand traffic, MMA 128xBN x K16
+  // in BN/2 cycles.  Small-M late layers prefer wide tiles, layer1 (Cout 64) 64.
   const int64_t tiles_m = (M + 127) / 128;
+  const int64_t nkb = Kpad / 64;
   int bn = 64;
-  for (int cand : {256, 128}) {
-    if (cand <= Cout && Cout % cand == 0 && tiles_m * (Cout / cand) >= num_sms()) {
+  double best = 1e30;
+  for (int cand : {64, 128, 256}) {
+    if (cand > Cout || Cout % cand) continue;
+    const int64_t tiles = tiles_m * (Cout / cand);
+    const int64_t waves = (tiles + num_sms() - 1) / num_sms();
+    const double t_mma = (double)waves * nkb * 2 * cand / 1.9e9;
+    const double t_l2 = (double)tiles * nkb * (16384.0 + cand * 128.0) / 8.0e12;
+    const double t = t_mma > t_l2 ? t_mma : t_l2;
+    if (t < best * 0.97) {
+      best = t;
       bn = cand;
-      break;
     }
   }
   CUtensorMap mw, mx;

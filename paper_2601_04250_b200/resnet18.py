@@ -143,7 +143,7 @@ class ResNet18B200:
     def flops(self, batch: int) -> float:
         """Algorithmic FLOPs (3.628 GF/img at 224x224)."""
         n, h = batch, self.image
-        f = self.stem.flops(n, h, h)
+        f = self.stem.flops(n, h // 2, h // 2)   # the stem runs on the s2d(2) input
         h = h // 4
         for c1, c2, ds in self.blocks:
             f += c1.flops(n, h, h)
