@@ -90,8 +90,18 @@ int gg_token_gather(const int32_t* pool_ids, const int32_t* pool_mask, int64_t p
 int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
               int32_t Cout, int32_t R, int32_t S, int32_t stride, int32_t pad, int32_t Kpad,
               const float* bias, const void* residual, int32_t relu, void* y, int32_t pad_hi,
-              const int32_t* count_dev, void* stream);
-/* (pad = top/left padding, pad_hi = bottom/right padding, -1 = same as pad.)
+              int32_t out_pad, const int32_t* count_dev, void* stream);
+/* out_pad = 1: y (and residual) are zero-bordered [N, Ho+2, Wo+2, Cout]
+ * buffers written at (+1, +1) — the layout gg_conv3x3_padded consumes. */
+/* 3x3 / stride 1 convolution on zero-padded activations x [N, H+2, W+2, C]
+ * writing y [N, H+2, W+2, Cout] (borders written as zeros): all nine taps are
+ * shifted views of ONE TMA-loaded span per 64-channel block.  w is BN-folded
+ * [Cout, C/64, 3, 3, 64] (K order: channel block, tap, channel); C, Cout % 64
+ * == 0; residual (optional) in the same padded layout. */
+int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
+                      int32_t Cout, const float* bias, const void* residual, int32_t relu,
+                      void* y, const int32_t* count_dev, void* stream);
+/* (gg_conv2d: pad = top/left padding, pad_hi = bottom/right padding, -1 = same as pad.)
  * A-operand paths: C % 64 == 0 -> one TMA im2col load per (tap, 64 channels);
  * C == 16 -> TMA im2col, 4 taps per 64-wide k-block (the space-to-depth stem);
  * otherwise a cp.async gather. */
@@ -108,11 +118,13 @@ int gg_nchw_to_s2d16(const float* x, int32_t N, int32_t H, int32_t W, void* y, v
 int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_ids,
                    const int32_t* count_dev, int32_t B, int32_t H, int32_t W,
                    const float* mean3, const float* std3, void* y, void* stream);
-/* 3x3 / stride 2 / pad 1 max pool (NHWC, C % 8 == 0). */
+/* 3x3 / stride 2 / pad 1 max pool (NHWC, C % 8 == 0); out_pad = 1 writes the
+ * interior of a zero-bordered [N, Ho+2, Wo+2, C] buffer. */
 int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, void* y,
-                    const int32_t* count_dev, void* stream);
-/* Global average pool NHWC [N, HW, C] -> [N, C]. */
-int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y,
+                    int32_t out_pad, const int32_t* count_dev, void* stream);
+/* Global average pool NHWC [N, HW, C] -> [N, C], dividing by denom (0 = HW;
+ * a zero-bordered input passes its interior pixel count). */
+int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y, int32_t denom,
                const int32_t* count_dev, void* stream);
 
 #ifdef __cplusplus

@@ -21,10 +21,13 @@ using namespace tc;
 constexpr int kAttnS = 128;
 constexpr int kAttnD = 64;
 constexpr int kAttnThreads = 128;
-constexpr int kOffQ = 0, kOffK = 16384, kOffV = 32768, kOffP = 49152;
-constexpr int kAttnSmem = 81920 + 64 + 1024;
+// smem: Q [0,16K) K [16K,32K) V^T [32K,48K); P (2 x 16 KB key blocks) reuses
+// Q+K once S = QK^T is in TMEM.  TMEM: 128 columns, S in [0,128), then O in
+// [0,64) once every thread has read its S row.  48 KB + 128 columns -> 4 CTAs/SM.
+constexpr int kOffQ = 0, kOffK = 16384, kOffV = 32768, kOffP = 0;
+constexpr int kAttnSmem = 49152 + 64 + 1024;
 
-__global__ void __launch_bounds__(kAttnThreads, 2)
+__global__ void __launch_bounds__(kAttnThreads, 4)
     attention_tcgen05(const __grid_constant__ CUtensorMap map_q,
                       const __grid_constant__ CUtensorMap map_k,
                       const __grid_constant__ CUtensorMap map_vt, const int32_t* mask,
@@ -32,10 +35,11 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   if (count && (int)(blockIdx.x / heads) >= __ldg(count)) return;  // dynamic batch
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar_load = reinterpret_cast<uint64_t*>(smem + 81920);
+  uint64_t* bar_load = reinterpret_cast<uint64_t*>(smem + 49152);
   uint64_t* bar_s = bar_load + 1;
   uint64_t* bar_o = bar_load + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_load + 3);
+  __shared__ float key_bias[kAttnS];   // 0 or -inf per key (attention mask)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int bh = blockIdx.x;
@@ -47,7 +51,8 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     mbar_init(bar_o, 1);
     fence_mbar_init();
   }
-  if (warp == 0) tmem_alloc(tmem_slot, 256);
+  key_bias[threadIdx.x] = (mask && __ldg(mask + (int64_t)b * kAttnS + threadIdx.x) == 0) ? -INFINITY : 0.0f;
+  if (warp == 0) tmem_alloc(tmem_slot, 128);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -69,54 +74,51 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     umma_commit(bar_s);
   }
 
-  // ---- softmax: thread = query row ----
+  // ---- softmax: thread = query row; two passes over S straight from TMEM ----
   const int row = warp * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   mbar_wait(bar_s, 0);
   tc_fence_after();
-  float s[kAttnS];
+  float mx = -INFINITY;
 #pragma unroll
   for (int c = 0; c < kAttnS; c += 32) {
     uint32_t r[32];
-    tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + c, r);
+    tmem_ld_32x32b_x32(trow + c, r);
     tmem_ld_wait();
 #pragma unroll
-    for (int i = 0; i < 32; ++i) s[c + i] = __uint_as_float(r[i]);
+    for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]) + key_bias[c + i]);
   }
-  if (mask) {
-    const int32_t* mrow = mask + (int64_t)b * kAttnS;
-#pragma unroll
-    for (int j = 0; j < kAttnS; ++j)
-      if (__ldg(mrow + j) == 0) s[j] = -INFINITY;
-  }
-  float mx = -INFINITY;
-#pragma unroll
-  for (int j = 0; j < kAttnS; ++j) mx = fmaxf(mx, s[j]);
   const float mref = (mx == -INFINITY) ? 0.0f : mx;
-  float sum = 0.0f;
   const float l2e = 1.4426950408889634f;
-#pragma unroll
-  for (int j = 0; j < kAttnS; ++j) {
-    s[j] = exp2f((s[j] - mref) * l2e);
-    sum += s[j];
-  }
-  // P row -> A operand (K-major, SW128): key block kb = j / 64, 16-byte chunk c = (j % 64) / 8
+  float sum = 0.0f;
+  // P row -> A operand (K-major, SW128): key block kb = j / 64, 16-byte chunk (j % 64) / 8
   uint8_t* prow = smem + kOffP + (row >> 3) * 1024 + (row & 7) * 128;
 #pragma unroll
-  for (int kb = 0; kb < 2; ++kb) {
+  for (int c = 0; c < kAttnS; c += 32) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(trow + c, r);
+    tmem_ld_wait();
+    float e[32];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int j = kb * 64 + c * 8;
+    for (int i = 0; i < 32; ++i) {
+      e[i] = exp2f((__uint_as_float(r[i]) + key_bias[c + i] - mref) * l2e);
+      sum += e[i];
+    }
+    const int kb = c / 64;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int chunk = (c % 64) / 8 + q;
       uint4 u;
-      u.x = pack_bf16(s[j + 0], s[j + 1]);
-      u.y = pack_bf16(s[j + 2], s[j + 3]);
-      u.z = pack_bf16(s[j + 4], s[j + 5]);
-      u.w = pack_bf16(s[j + 6], s[j + 7]);
-      *reinterpret_cast<uint4*>(prow + kb * 16384 + ((c ^ (row & 7)) << 4)) = u;
+      u.x = pack_bf16(e[8 * q + 0], e[8 * q + 1]);
+      u.y = pack_bf16(e[8 * q + 2], e[8 * q + 3]);
+      u.z = pack_bf16(e[8 * q + 4], e[8 * q + 5]);
+      u.w = pack_bf16(e[8 * q + 6], e[8 * q + 7]);
+      *reinterpret_cast<uint4*>(prow + kb * 16384 + ((chunk ^ (row & 7)) << 4)) = u;
     }
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
-  __syncthreads();
+  __syncthreads();   // every S row read, every P row written
   if (threadIdx.x == 0) {
     tc_fence_after();
     const uint32_t sp = smem_u32(smem + kOffP), sv = smem_u32(smem + kOffV);
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem + 128, sdesc_k_sw128(sp + kb * 16384 + kk * 32),
+        umma_bf16(tmem, sdesc_k_sw128(sp + kb * 16384 + kk * 32),
                   sdesc_k_sw128(sv + kb * 8192 + kk * 32), idesc_o, (kb | kk) != 0);
     umma_commit(bar_o);
   }
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
 #pragma unroll
   for (int c = 0; c < kAttnD; c += 32) {
     uint32_t r[32];
-    tmem_ld_32x32b_x32(tmem + ((uint32_t)(warp * 32) << 16) + 128 + c, r);
+    tmem_ld_32x32b_x32(trow + c, r);
     tmem_ld_wait();
     uint4* dp = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, 128);
   }
 }
 

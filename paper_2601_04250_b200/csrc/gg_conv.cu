@@ -27,6 +27,8 @@ struct ConvShape {
   int Ho, Wo, Cout;
   int R, S, stride, pad;
   int pad_hi;          // bottom/right padding (== pad for symmetric convolutions)
+  int bres;            // resident-B mode (weights loaded once per CTA)
+  int bres_stages;     // A-ring depth in resident-B mode
   int Kpad;            // multiple of 64, >= R*S*C
   int M;               // N*Ho*Wo
 };
@@ -37,6 +39,7 @@ struct ConvEpi {
   const __nv_bfloat16* residual;  // [M, Cout] or null
   int relu;
   const int32_t* count;           // device image count (dynamic batch) or null
+  int out_pad;                    // 1: y (and residual) are [N, Ho+2, Wo+2, Cout] zero-bordered
 };
 
 constexpr int kConvProdWarps = 4;
@@ -78,19 +81,27 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   using L = ConvSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  // Resident-B mode (sh.bres, im2col modes, one N tile): the whole BN x Kpad
+  // weight slab is loaded once per CTA after a shorter A ring and never re-read
+  // from L2; the ring then carries only A tiles.
+  const int num_kb = sh.Kpad / 64;
+  const int nst = sh.bres ? sh.bres_stages : STAGES;
+  uint8_t* bres = smem + nst * L::STAGE_BYTES;
+  const int bar_off = nst * L::STAGE_BYTES + (sh.bres ? num_kb * L::B_BYTES : 0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + bar_off);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* b_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = ep.count ? min(sh.M, __ldg(ep.count) * sh.Ho * sh.Wo) : sh.M;
   const int tiles_m = (M + 127) / 128, tiles_n = sh.Cout / BN;
   const int num_tiles = tiles_m * tiles_n;
-  const int num_kb = sh.Kpad / 64;
 
   if (threadIdx.x == 0) {
+    mbar_init(b_full, 1);
     for (int s = 0; s < STAGES; ++s) {
       // gather mode: 128 producer arrivals + the B TMA arrive; im2col mode: one expect_tx arrive
       mbar_init(&full[s], MODE != 0 ? 1 : 32 * kConvProdWarps + 1);
@@ -114,6 +125,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     if (threadIdx.x == 0) {
       tma_prefetch(&map_x);
       const int cblocks = sh.C / 64;
+      if (sh.bres && num_tiles > (int)blockIdx.x) {
+        mbar_expect_tx(b_full, num_kb * L::B_BYTES);
+        for (int kb = 0; kb < num_kb; ++kb)
+          tma_load_2d(bres + kb * L::B_BYTES, &map_w, b_full, kb * 64, 0);
+      }
       int it = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int tm = tile % tiles_m, tn = tile / tiles_m;
@@ -123,10 +139,10 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int ho0 = rem / sh.Wo, wo0 = rem - (rem / sh.Wo) * sh.Wo;
         const int wc = wo0 * sh.stride - sh.pad, hc = ho0 * sh.stride - sh.pad;
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          const int s = it % nst;
+          mbar_wait(&empty[s], ((it / nst) & 1) ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
-          mbar_expect_tx(&full[s], L::STAGE_BYTES);
+          mbar_expect_tx(&full[s], sh.bres ? L::A_BYTES : L::STAGE_BYTES);
           constexpr int kLoads = MODE == 1 ? 1 : 4;
 #pragma unroll
           for (int q = 0; q < kLoads; ++q) {
@@ -146,7 +162,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 "h"((uint16_t)ss), "h"((uint16_t)rr)
                 : "memory");
           }
-          tma_load_2d(sa + L::A_BYTES, &map_w, &full[s], kb * 64, tn * BN);
+          if (!sh.bres) tma_load_2d(sa + L::A_BYTES, &map_w, &full[s], kb * 64, tn * BN);
         }
       }
     }
@@ -205,6 +221,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
       int it = 0, t = 0;
+      if (sh.bres && num_tiles > (int)blockIdx.x) mbar_wait(b_full, 0);
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
         const int acc = t & 1;
         const uint32_t use = t >> 1;
@@ -212,11 +229,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
-          const int s = it % STAGES;
-          mbar_wait(&full[s], (it / STAGES) & 1);
+          const int s = it % nst;
+          mbar_wait(&full[s], (it / nst) & 1);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
-          const uint32_t sb = sa + L::A_BYTES;
+          const uint32_t sb = sh.bres ? smem_u32(bres + kb * L::B_BYTES) : sa + L::A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             umma_bf16(d_tmem, MODE == 2 ? sdesc_k_sw32(sa + kk * 4096) : sdesc_k_sw128(sa + kk * 32),
@@ -238,6 +255,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       tc_fence_after();
       const int m = tm * 128 + quarter * 32 + lane;
       const bool ok = m < M;
+      int64_t oidx = m;   // output row: dense, or inside a zero-bordered [Ho+2, Wo+2] layout
+      if (ep.out_pad) {
+        const int n = m / (sh.Ho * sh.Wo), rem = m - (m / (sh.Ho * sh.Wo)) * sh.Ho * sh.Wo;
+        const int ho = rem / sh.Wo, wo = rem - (rem / sh.Wo) * sh.Wo;
+        oidx = ((int64_t)n * (sh.Ho + 2) + ho + 1) * (sh.Wo + 2) + wo + 1;
+      }
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
@@ -255,7 +278,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           v[i + 3] = __uint_as_float(r[i + 3]) + b.w;
         }
         if (ep.residual) {
-          const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + (int64_t)m * sh.Cout + col0);
+          const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + oidx * sh.Cout + col0);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const uint4 u = __ldg(rp + q);
@@ -272,7 +295,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
         }
-        uint4* dp = reinterpret_cast<uint4*>(ep.y + (int64_t)m * sh.Cout + col0);
+        uint4* dp = reinterpret_cast<uint4*>(ep.y + oidx * sh.Cout + col0);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint4 u;
@@ -302,13 +325,15 @@ static int launch_conv(const __nv_bfloat16* x, const CUtensorMap& mw, const CUte
   auto kern = conv_bf16_tcgen05<BN, STAGES, MODE>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
       return GG_ERR_CUDA;
     attr = true;
   }
   const int tiles = ((sh.M + 127) / 128) * (sh.Cout / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kConvThreads, L::TOTAL, s>>>(x, mw, mx, sh, ep);
+  const int smem = sh.bres ? sh.bres_stages * L::STAGE_BYTES + (sh.Kpad / 64) * L::B_BYTES + 256 + 1024
+                           : L::TOTAL;
+  kern<<<grid, kConvThreads, smem, s>>>(x, mw, mx, sh, ep);
   GG_LAUNCH_OK();
   return GG_OK;
 }
@@ -360,7 +385,8 @@ __global__ void nchw_to_nhwc_pad(const float* __restrict__ in, __nv_bfloat16* __
 
 // 3x3 stride-2 pad-1 max pool, NHWC, 8 channels per thread.
 __global__ void maxpool3x3s2(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
-                             int N, int H, int W, int C, int Ho, int Wo, const int32_t* count) {
+                             int N, int H, int W, int C, int Ho, int Wo, const int32_t* count,
+                             int out_pad) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int cg = C / 8;
   if (count) N = min(N, __ldg(count));
@@ -392,12 +418,13 @@ __global__ void maxpool3x3s2(const __nv_bfloat16* __restrict__ in, __nv_bfloat16
   u.y = pack_bf16(m[2], m[3]);
   u.z = pack_bf16(m[4], m[5]);
   u.w = pack_bf16(m[6], m[7]);
-  *reinterpret_cast<uint4*>(out + p * C + c0) = u;
+  const int64_t o = out_pad ? ((int64_t)n * (Ho + 2) + ho + 1) * (Wo + 2) + wo + 1 : p;
+  *reinterpret_cast<uint4*>(out + o * C + c0) = u;
 }
 
 // Global average pool NHWC [N, HW, C] -> [N, C] bf16 (fp32 sum), one thread per (n, 8 channels).
 __global__ void avgpool_global(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
-                               int N, int HW, int C, const int32_t* count) {
+                               int N, int HW, int C, const int32_t* count, int denom) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   const int cg = C / 8;
   if (count) N = min(N, __ldg(count));
@@ -414,7 +441,7 @@ __global__ void avgpool_global(const __nv_bfloat16* __restrict__ in, __nv_bfloat
       s[2 * e + 1] += f.y;
     }
   }
-  const float inv = 1.0f / HW;
+  const float inv = 1.0f / (denom > 0 ? denom : HW);   // padded input: borders are zeros
   uint4 u;
   u.x = pack_bf16(s[0] * inv, s[1] * inv);
   u.y = pack_bf16(s[2] * inv, s[3] * inv);
@@ -430,21 +457,25 @@ using namespace gg;
 extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
                          int32_t Cout, int32_t R, int32_t S, int32_t stride, int32_t pad,
                          int32_t Kpad, const float* bias, const void* residual, int32_t relu,
-                         void* y, int32_t pad_hi, const int32_t* count_dev, void* stream) {
+                         void* y, int32_t pad_hi, int32_t out_pad, const int32_t* count_dev,
+                         void* stream) {
   if (!x || !w || !y || !bias || N <= 0 || H <= 0 || W <= 0 || R <= 0 || S <= 0 || stride <= 0)
     return GG_ERR_INVALID_ARGUMENT;
-  if (C % 8 || Kpad % 64 || Kpad < R * S * C || Cout % 64 || pad < 0) return GG_ERR_UNSUPPORTED;
+  // pad may be negative (-1): reading the interior of an already zero-padded input
+  if (C % 8 || Kpad % 64 || Kpad < R * S * C || Cout % 64 || pad < -1) return GG_ERR_UNSUPPORTED;
   ConvShape sh;
   sh.N = N; sh.H = H; sh.W = W; sh.C = C; sh.Cout = Cout;
   sh.R = R; sh.S = S; sh.stride = stride; sh.pad = pad; sh.Kpad = Kpad;
   sh.pad_hi = pad_hi < 0 ? pad : pad_hi;
+  sh.bres = 0;
+  sh.bres_stages = 0;
   sh.Ho = (H + pad + sh.pad_hi - R) / stride + 1;
   sh.Wo = (W + pad + sh.pad_hi - S) / stride + 1;
   const int64_t M = (int64_t)N * sh.Ho * sh.Wo;
   if (M > 0x7fffffff) return GG_ERR_UNSUPPORTED;
   sh.M = (int)M;
   ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
-             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev};
+             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, out_pad};
   // N tile: minimize the larger of (tensor time of the busiest SM) and (operand
   // bytes streamed from L2: every tile re-reads its A rows and its B columns per
   // k-block).  Measured on B200: ~8 TB/s of TMA operand traffic, MMA 128xBN x K16
@@ -473,6 +504,13 @@ extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t
   if (mode) {
     rc = make_map_im2col(&mx, x, sh, mode == 1 ? 64 : 16);
     if (rc) return rc;
+    // resident weights when the whole N = Cout slab fits next to a 4-deep A ring
+    const int stage_bytes = 128 * 128 + bn * 128;
+    const int64_t need = 4LL * stage_bytes + (Kpad / 64) * (int64_t)bn * 128 + 1280;
+    if (bn == Cout && need <= 227 * 1024) {
+      sh.bres = 1;
+      sh.bres_stages = 4;
+    }
   } else {
     mx = mw;  // unused by the gather path
   }
@@ -510,24 +548,24 @@ extern "C" int gg_nchw_to_nhwc(const float* x, int32_t N, int32_t C, int32_t H, 
 }
 
 extern "C" int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, void* y,
-                               const int32_t* count_dev, void* stream) {
+                               int32_t out_pad, const int32_t* count_dev, void* stream) {
   if (!x || !y || C % 8) return GG_ERR_INVALID_ARGUMENT;
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
   const int64_t work = (int64_t)N * Ho * Wo * (C / 8);
   maxpool3x3s2<<<(unsigned)((work + 255) / 256), 256, 0, gg_stream(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, H, W, C,
-      Ho, Wo, count_dev);
+      Ho, Wo, count_dev, out_pad);
   GG_LAUNCH_OK();
   return GG_OK;
 }
 
 extern "C" int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y,
-                          const int32_t* count_dev, void* stream) {
-  if (!x || !y || C % 8) return GG_ERR_INVALID_ARGUMENT;
+                          int32_t denom, const int32_t* count_dev, void* stream) {
+  if (!x || !y || C % 8 || denom < 0) return GG_ERR_INVALID_ARGUMENT;
   const int work = N * (C / 8);
   avgpool_global<<<(work + 127) / 128, 128, 0, gg_stream(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, HW, C,
-      count_dev);
+      count_dev, denom);
   GG_LAUNCH_OK();
   return GG_OK;
 }

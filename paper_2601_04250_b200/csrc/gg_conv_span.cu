@@ -1,0 +1,348 @@
+// gg_conv_span.cu — 3x3 / stride-1 convolution on zero-padded NHWC activations
+// with ONE operand load per tile for all nine taps.
+//
+// Activations live padded: [N, H+2, W+2, C] with zero borders.  Index output
+// positions in the padded input space, m = (n*(H+2) + h)*(W+2) + w; tap (r, s)
+// of output m reads padded pixel m + r*(W+2) + s — a uniform shift.  So for a
+// tile of 128 consecutive m, the nine A operands are nine shifted views of ONE
+// span of 128 + 2*(W+2) + 2 pixel rows, loaded once per 64-channel block by TMA
+// (instead of nine im2col loads): A traffic drops ~5-8x.  The span is stored
+// as eight 16-byte-wide channel planes (no swizzle), so a shift by one pixel is
+// +16 B of the UMMA descriptor start address (K-major, SWIZZLE_NONE:
+// SBO = 128 B between 8-row core matrices, LBO = plane stride between the two
+// 8-channel halves of a K=16 step).
+//
+// Positions with w >= W or h >= H are computed and written as ZEROS: they land
+// exactly on the output's padding (output index = m + (W+2) + 1), so the next
+// layer reads correct zero borders.  Waste: (H+2)(W+2)/(HW) - 1 of the MMAs.
+//
+//   warp 0  TMA producer: A span planes (2-stage ring) + B k-blocks (ring, or
+//           the whole BN x K slab once per CTA when it fits: resident B)
+//   warp 1  TMEM allocator + tcgen05.mma issuer
+//   warps 2..5  epilogue: tcgen05.ld, folded-BN bias, residual, ReLU, bf16
+#include <cudaTypedefs.h>
+
+#include "gg_common.cuh"
+#include "gg_kernels.h"
+#include "gg_tc.cuh"
+
+namespace gg {
+using namespace tc;
+
+struct SpanShape {
+  int N, H, W, C, Cout;
+  int Wp, Hp;          // W + 2, H + 2
+  int Mtot;            // N_eff * Hp * Wp (set per launch from the count)
+  int span_rows;       // 128 + 2*Wp + 2
+  int plane_bytes;     // span_rows * 16 rounded up to 128
+  int bres;            // B resident for the whole CTA
+};
+
+struct SpanEpi {
+  __nv_bfloat16* y;               // padded [N, Hp, Wp, Cout]
+  const float* bias;
+  const __nv_bfloat16* residual;  // padded, same geometry, or null
+  int relu;
+  const int32_t* count;
+};
+
+constexpr int kSpanThreads = 64 + 128;
+constexpr int kSpanAStage = 8 * 256 * 16;   // max: 8 planes x 256 rows x 16 B
+
+__device__ __forceinline__ uint64_t sdesc_k_none(uint32_t smem_addr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;  // LBO: next 8-channel plane (K)
+  d |= (uint64_t)(128 >> 4) << 32;                   // SBO: next 8-row core matrix (M)
+  d |= (uint64_t)1 << 46;                            // version
+  return d;                                          // layout type 0 = SWIZZLE_NONE
+}
+
+template <int BN, int BSTAGES>
+__global__ void __launch_bounds__(kSpanThreads, 1)
+    conv_span_tcgen05(const __grid_constant__ CUtensorMap map_x,
+                      const __grid_constant__ CUtensorMap map_w, SpanShape sh, SpanEpi ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int cblocks = sh.C / 64;
+  const int nkb = cblocks * 9;
+  constexpr int B_BYTES = BN * 128;
+  uint8_t* a_base = smem;                                   // 2 x kSpanAStage
+  uint8_t* b_base = smem + 2 * kSpanAStage;                 // ring or resident slab
+  const int b_slots = sh.bres ? nkb : BSTAGES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + b_slots * B_BYTES);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = bars + 2;
+  uint64_t* b_full = bars + 4;
+  uint64_t* b_empty = b_full + BSTAGES;
+  uint64_t* acc_full = b_empty + BSTAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* bres_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int img = sh.Hp * sh.Wp;
+  const int n_eff = ep.count ? min(sh.N, __ldg(ep.count)) : sh.N;
+  const int Mtot = n_eff * img;
+  const int tiles_m = (Mtot + 127) / 128, tiles_n = sh.Cout / BN;
+  const int num_tiles = tiles_m * tiles_n;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 4);
+    }
+    for (int i = 0; i < BSTAGES; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    mbar_init(bres_full, 1);
+    fence_mbar_init();
+    tma_prefetch(&map_x);
+    tma_prefetch(&map_w);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      if (sh.bres && num_tiles > (int)blockIdx.x) {
+        mbar_expect_tx(bres_full, nkb * B_BYTES);
+        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(b_base + kb * B_BYTES, &map_w, bres_full, kb * 64, 0);
+      }
+      int ait = 0, bit = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int tm = tile % tiles_m, tn = tile / tiles_m;
+        const int m0 = tm * 128;
+        for (int cb = 0; cb < cblocks; ++cb, ++ait) {
+          const int as = ait & 1;
+          mbar_wait(&a_empty[as], ((ait >> 1) & 1) ^ 1);
+          uint8_t* sa = a_base + as * kSpanAStage;
+          mbar_expect_tx(&a_full[as], 8 * sh.span_rows * 16);
+          for (int p = 0; p < 8; ++p)   // box = [8 channels, span_rows] per plane
+            tma_load_2d(sa + p * sh.plane_bytes, &map_x, &a_full[as], cb * 64 + p * 8, m0);
+          if (!sh.bres) {
+            for (int tap = 0; tap < 9; ++tap, ++bit) {
+              const int bs = bit % BSTAGES;
+              mbar_wait(&b_empty[bs], ((bit / BSTAGES) & 1) ^ 1);
+              mbar_expect_tx(&b_full[bs], B_BYTES);
+              tma_load_2d(b_base + bs * B_BYTES, &map_w, &b_full[bs], (cb * 9 + tap) * 64, tn * BN);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+      if (sh.bres && num_tiles > (int)blockIdx.x) mbar_wait(bres_full, 0);
+      int ait = 0, bit = 0, t = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+        const int acc = t & 1;
+        mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int cb = 0; cb < cblocks; ++cb, ++ait) {
+          const int as = ait & 1;
+          mbar_wait(&a_full[as], (ait >> 1) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(a_base + as * kSpanAStage);
+          for (int tap = 0; tap < 9; ++tap) {
+            const int r = tap / 3, s = tap - 3 * (tap / 3);
+            const uint32_t shift = (uint32_t)(r * sh.Wp + s) * 16u;
+            uint32_t sb;
+            int bs = 0;
+            if (sh.bres) {
+              sb = smem_u32(b_base + (cb * 9 + tap) * B_BYTES);
+            } else {
+              bs = bit % BSTAGES;
+              mbar_wait(&b_full[bs], (bit / BSTAGES) & 1);
+              tc_fence_after();
+              sb = smem_u32(b_base + bs * B_BYTES);
+            }
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              umma_bf16(d_tmem, sdesc_k_none(sa + 2 * kk * sh.plane_bytes + shift, sh.plane_bytes),
+                        sdesc_k_sw128(sb + kk * 32), idesc, (cb | tap | kk) != 0);
+            if (!sh.bres) {
+              umma_commit(&b_empty[bs]);
+              ++bit;
+            }
+          }
+          umma_commit(&a_empty[as]);
+        }
+        umma_commit(&acc_full[acc]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    int t = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      const int acc = t & 1;
+      mbar_wait(&acc_full[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const int m = tm * 128 + quarter * 32 + lane;
+      const int within = m % img;
+      const int h = within / sh.Wp, w = within - (within / sh.Wp) * sh.Wp;
+      const bool real = m < Mtot && h < sh.H && w < sh.W;
+      const int64_t oidx = (int64_t)m + sh.Wp + 1;   // padded output position
+      const bool store = m < Mtot && oidx < (int64_t)n_eff * img;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
+        tmem_ld_wait();
+        if (!store) continue;
+        const int col0 = tn * BN + c;
+        float v[32];
+        if (real) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + i));
+            v[i] = __uint_as_float(r[i]) + b.x;
+            v[i + 1] = __uint_as_float(r[i + 1]) + b.y;
+            v[i + 2] = __uint_as_float(r[i + 2]) + b.z;
+            v[i + 3] = __uint_as_float(r[i + 3]) + b.w;
+          }
+          if (ep.residual) {
+            const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + oidx * sh.Cout + col0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 u = __ldg(rp + q);
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h2[e]);
+                v[q * 8 + 2 * e] += f.x;
+                v[q * 8 + 2 * e + 1] += f.y;
+              }
+            }
+          }
+          if (ep.relu) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.0f;   // padding positions stay zero
+        }
+        uint4* dp = reinterpret_cast<uint4*>(ep.y + oidx * sh.Cout + col0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+          u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+          u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+          u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+          dp[q] = u;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+// 2-D map over a padded activation viewed as [pixels, C]: box [8 channels, rows], no swizzle.
+static int make_map_planes(CUtensorMap* map, const void* x, int64_t pixels, int C, int rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return GG_ERR_CUDA;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)pixels};
+  cuuint64_t strides[1] = {(cuuint64_t)C * 2};
+  cuuint32_t box[2] = {8, (cuuint32_t)rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? GG_OK : GG_ERR_INVALID_ARGUMENT;
+}
+
+template <int BN, int BSTAGES>
+static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanShape& sh,
+                       const SpanEpi& ep, cudaStream_t s) {
+  auto kern = conv_span_tcgen05<BN, BSTAGES>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+      return GG_ERR_CUDA;
+    attr = true;
+  }
+  const int nkb = sh.C / 64 * 9;
+  const int smem = 2 * kSpanAStage + (sh.bres ? nkb : BSTAGES) * BN * 128 + 512 + 1024;
+  const int tiles = ((sh.N * sh.Hp * sh.Wp + 127) / 128) * (sh.Cout / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, kSpanThreads, smem, s>>>(mx, mw, sh, ep);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+}  // namespace gg
+
+using namespace gg;
+
+extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W, int32_t C,
+                                 const void* w, int32_t Cout, const float* bias,
+                                 const void* residual, int32_t relu, void* y,
+                                 const int32_t* count_dev, void* stream) {
+  if (!x || !w || !y || !bias || N <= 0 || H <= 0 || W <= 0) return GG_ERR_INVALID_ARGUMENT;
+  if (C % 64 || Cout % 64) return GG_ERR_UNSUPPORTED;
+  SpanShape sh;
+  sh.N = N; sh.H = H; sh.W = W; sh.C = C; sh.Cout = Cout;
+  sh.Wp = W + 2; sh.Hp = H + 2;
+  sh.Mtot = N * sh.Hp * sh.Wp;
+  sh.span_rows = 128 + 2 * sh.Wp + 2;
+  if (sh.span_rows > 256) return GG_ERR_UNSUPPORTED;  // one A stage holds <= 256 rows per plane
+  sh.plane_bytes = (sh.span_rows * 16 + 127) / 128 * 128;
+  // N tile: as in gg_conv2d, by operand traffic vs tensor time (B re-read per M tile)
+  const int64_t tiles_m = (sh.Mtot + 127) / 128;
+  const int64_t nkb = C / 64 * 9;
+  int bn = 64;
+  double best = 1e30;
+  for (int cand : {64, 128, 256}) {
+    if (cand > Cout || Cout % cand) continue;
+    const int64_t tiles = tiles_m * (Cout / cand);
+    const int64_t waves = (tiles + num_sms() - 1) / num_sms();
+    const bool res = (cand == Cout) && (2 * kSpanAStage + nkb * cand * 128 + 1536 <= 227 * 1024);
+    const double t_mma = (double)waves * nkb * 2 * cand / 1.9e9;
+    const double bbytes = res ? (double)(tiles < num_sms() ? tiles : num_sms()) * nkb * cand * 128
+                              : (double)tiles * nkb * cand * 128;
+    const double t_l2 = ((double)tiles * (C / 64) * 8 * sh.span_rows * 16 + bbytes) / 8.0e12;
+    const double t = t_mma > t_l2 ? t_mma : t_l2;
+    if (t < best * 0.97) {
+      best = t;
+      bn = cand;
+    }
+  }
+  sh.bres = (bn == Cout) && (2 * kSpanAStage + nkb * bn * 128 + 1536 <= 227 * 1024);
+  CUtensorMap mx, mw;
+  int rc = make_map_planes(&mx, x, (int64_t)N * sh.Hp * sh.Wp, C, sh.span_rows);
+  if (!rc) rc = make_map_2d(&mw, w, Cout, (int64_t)C * 9, (int64_t)C * 9, bn);
+  if (rc) return rc;
+  SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
+             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev};
+  cudaStream_t s = gg_stream(stream);
+  switch (bn) {
+    case 256: return launch_span<256, 3>(mx, mw, sh, ep, s);
+    case 128: return launch_span<128, 5>(mx, mw, sh, ep, s);
+    default: return launch_span<64, 8>(mx, mw, sh, ep, s);
+  }
+}

@@ -39,7 +39,9 @@ struct GemmEpilogue {
 };
 
 constexpr int kBK = 64;            // 64 bf16 = 128 B = one swizzle row
-constexpr int kEpiWarps = 4;
+// 8 epilogue warps: two per TMEM lane quarter, each draining half of the tile's
+// columns, so bias/GELU/residual math keeps pace with the MMA of the next tile.
+constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 template <int BM, int BN, int STAGES>
@@ -142,6 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ===== epilogue warps =====
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;  // which half of the columns
     int t = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
@@ -152,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = tm * BM + quarter * 32 + lane;
       const bool row_ok = row < M;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
         tmem_ld_wait();

@@ -26,10 +26,15 @@ __device__ __forceinline__ void ln_row(float (&x)[PER_LANE], int width, const fl
 #pragma unroll
   for (int c = 0; c < PER_LANE / 8; ++c) {
     const int col = (c * 32 + lane) * 8;
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + col));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + col + 4));
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + col));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + col + 4));
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
     float o[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
-      o[e] = (x[c * 8 + e] - mean) * rstd * __ldg(gamma + col + e) + __ldg(beta + col + e);
+    for (int e = 0; e < 8; ++e) o[e] = (x[c * 8 + e] - mean) * rstd * gg[e] + bb[e];
     uint4 u;
     __nv_bfloat162 t0 = __floats2bfloat162_rn(o[0], o[1]), t1 = __floats2bfloat162_rn(o[2], o[3]);
     __nv_bfloat162 t2 = __floats2bfloat162_rn(o[4], o[5]), t3 = __floats2bfloat162_rn(o[6], o[7]);

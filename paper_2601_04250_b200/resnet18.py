@@ -1,11 +1,22 @@
 """ResNet-18 (torchvision architecture, 224x224) forward on sm_100a, NHWC bf16.
 
-Every convolution is one implicit-GEMM tcgen05 kernel (gg_conv2d) with the
-eval-mode BatchNorm folded into its weights/bias and the residual add + ReLU
-fused into the epilogue; the 1x1 stride-2 downsample is a conv of the same
-kernel.  Stem/head: gg_nchw_to_nhwc (fp32 NCHW -> bf16 NHWC, channels padded
-to 8), gg_maxpool3x3s2, gg_avgpool, and the fc layer on gg_gemm with fp32
-logits for the K3 epilogue.
+Layout: from layer1 on every activation lives in a zero-bordered buffer
+[N, H+2, W+2, C], one set of three buffers per stage geometry (58², 30², 16²,
+9²), zeroed once.  Then:
+
+  stem       conv1 7x7/2 + bn1 + ReLU as a 4x4/1 conv over the space-to-depth(2)
+             input (gg_conv2d, TMA im2col 16-channel mode), dense output
+  maxpool    gg_maxpool3x3s2 into the interior of the layer1 buffer
+  3x3 / 1    gg_conv3x3_padded: one TMA span load per 64-channel block feeds all
+             nine taps (shifted UMMA descriptors); borders written as zeros
+  3x3 / 2    gg_conv2d (TMA im2col) reading the padded input with pad 0,
+             writing the next stage's padded buffer
+  1x1 / 2    gg_conv2d with pad -1 (interior of the padded input)
+  head       gg_avgpool over the padded 9x9 map (divides by 49) + fc on gg_gemm
+             with fp32 logits for the K3 epilogue
+
+Eval-mode BatchNorm is folded into every conv's weights/bias; residual add and
+ReLU are fused into the conv epilogues.
 """
 
 from __future__ import annotations
@@ -16,36 +27,37 @@ from . import _native
 from .distilbert import OUT_F32, gemm
 
 
-def _fold(conv, bn, cpad: int):
-    """BN(conv(x)) == conv'(x) + b' in eval mode; weights -> [Cout, Kpad] (r, s, c) order."""
+def _fold(conv, bn):
+    """BN(conv(x)) == conv'(x) + b' in eval mode.  Returns ([Cout, R, S, Cin] fp32, bias)."""
     import torch
 
     w = conv.weight.detach().float()
-    cout, cin, R, S = w.shape
     scale = bn.weight.detach().float() / torch.sqrt(bn.running_var.detach().float() + bn.eps)
     bias = bn.bias.detach().float() - bn.running_mean.detach().float() * scale
     w = w * scale[:, None, None, None]
-    wp = torch.zeros((cout, R, S, cpad), dtype=torch.float32)
-    wp[:, :, :, :cin] = w.permute(0, 2, 3, 1).cpu()
-    k = R * S * cpad
-    kpad = (k + 63) // 64 * 64
-    out = torch.zeros((cout, kpad), dtype=torch.float32)
-    out[:, :k] = wp.reshape(cout, k)
-    return out, bias.cpu(), kpad
+    return w.permute(0, 2, 3, 1).contiguous().cpu(), bias.cpu()
 
 
 class _Conv:
-    def __init__(self, conv, bn, cpad, device):
+    """Generic implicit-GEMM conv (gg_conv2d): weights [Cout, R*S*Cin] (r, s, c order)."""
+
+    def __init__(self, conv, bn, device, pad=None, pad_hi=None, out_pad=0):
         import torch
-        w, b, self.kpad = _fold(conv, bn, cpad)
-        self.w = w.to(device=device, dtype=torch.bfloat16).contiguous()
+        w, b = _fold(conv, bn)
+        cout, R, S, cin = w.shape
+        k = R * S * cin
+        kpad = (k + 63) // 64 * 64
+        wk = torch.zeros((cout, kpad), dtype=torch.float32)
+        wk[:, :k] = w.reshape(cout, k)
+        self.w = wk.to(device=device, dtype=torch.bfloat16).contiguous()
         self.b = b.to(device=device).contiguous()
-        self.cout = w.shape[0]
-        self.cin = cpad
-        self.r, self.s = conv.kernel_size
+        self.kpad, self.cout, self.cin = kpad, cout, cin
+        self.r, self.s = R, S
         self.stride = conv.stride[0]
-        self.pad = self.pad_hi = conv.padding[0]
-        self.algo_macs_per_pixel = self.r * self.s * conv.in_channels * self.cout
+        self.pad = conv.padding[0] if pad is None else pad
+        self.pad_hi = self.pad if pad_hi is None else pad_hi
+        self.out_pad = out_pad
+        self.algo_macs_per_pixel = R * S * conv.in_channels * cout
 
     def out_hw(self, h, w):
         return ((h + self.pad + self.pad_hi - self.r) // self.stride + 1,
@@ -56,12 +68,11 @@ class _Conv:
             C.c_void_p(x), n, h, w, self.cin, _native.ptr(self.w), self.cout, self.r, self.s,
             self.stride, self.pad, self.kpad, _native.ptr(self.b),
             None if residual is None else C.c_void_p(residual), int(relu), C.c_void_p(y),
-            self.pad_hi, _native.ptr(count), st))
+            self.pad_hi, self.out_pad, _native.ptr(count), st))
         return self.out_hw(h, w)
 
-    def flops(self, n, h, w):
+    def flops(self, n, ho, wo):
         """Algorithmic FLOPs of the original convolution (padding channels excluded)."""
-        ho, wo = self.out_hw(h, w)
         return 2.0 * n * ho * wo * self.algo_macs_per_pixel
 
 
@@ -77,10 +88,7 @@ class _StemConv(_Conv):
 
     def __init__(self, conv, bn, device):
         import torch
-        w = conv.weight.detach().float().cpu()
-        scale = bn.weight.detach().float() / torch.sqrt(bn.running_var.detach().float() + bn.eps)
-        bias = bn.bias.detach().float() - bn.running_mean.detach().float() * scale
-        w = w * scale.cpu()[:, None, None, None]
+        w, bias = _fold(conv, bn)            # [64, 7, 7, 3]
         cout = w.shape[0]
         wp = torch.zeros((cout, 4, 4, 16), dtype=torch.float32)
         for i in range(4):
@@ -94,17 +102,42 @@ class _StemConv(_Conv):
                         if not 0 <= s <= 6:
                             continue
                         for c in range(3):
-                            wp[:, i, j, (dy * 2 + dx) * 3 + c] = w[:, c, r, s]
+                            wp[:, i, j, (dy * 2 + dx) * 3 + c] = w[:, r, s, c]
         self.w = wp.reshape(cout, 256).to(device=device, dtype=torch.bfloat16).contiguous()
         self.b = bias.to(device=device).contiguous()
         self.kpad, self.cout, self.cin = 256, cout, 16
         self.r = self.s = 4
-        self.stride, self.pad, self.pad_hi = 1, 2, 1
+        self.stride, self.pad, self.pad_hi, self.out_pad = 1, 2, 1, 0
         self.algo_macs_per_pixel = 7 * 7 * 3 * cout
 
 
+class _SpanConv:
+    """3x3 / 1 conv on padded activations (gg_conv3x3_padded); weights in
+    (channel block, tap, channel) K order."""
+
+    def __init__(self, conv, bn, device):
+        import torch
+        w, b = _fold(conv, bn)               # [Cout, 3, 3, Cin]
+        cout, _, _, cin = w.shape
+        wk = w.reshape(cout, 9, cin // 64, 64).permute(0, 2, 1, 3).reshape(cout, 9 * cin)
+        self.w = wk.to(device=device, dtype=torch.bfloat16).contiguous()
+        self.b = b.to(device=device).contiguous()
+        self.cin, self.cout = cin, cout
+        self.algo_macs_per_pixel = 9 * cin * cout
+
+    def __call__(self, lib, x, n, h, w, y, st, residual=None, relu=True, count=None):
+        _native.check("gg_conv3x3_padded", lib.gg_conv3x3_padded(
+            C.c_void_p(x), n, h, w, self.cin, _native.ptr(self.w), self.cout, _native.ptr(self.b),
+            None if residual is None else C.c_void_p(residual), int(relu), C.c_void_p(y),
+            _native.ptr(count), st))
+        return h, w
+
+    def flops(self, n, ho, wo):
+        return 2.0 * n * ho * wo * self.algo_macs_per_pixel
+
+
 class ResNet18B200:
-    """Packed (BN-folded) weights + NHWC activation buffers for up to max_batch images."""
+    """Packed (BN-folded) weights + padded NHWC activation buffers for up to max_batch images."""
 
     def __init__(self, tv_model, max_batch: int = 64, image: int = 224, device="cuda"):
         torch = _native.require_cuda()
@@ -112,17 +145,25 @@ class ResNet18B200:
         self.device = torch.device(device)
         self.max_batch, self.image = max_batch, image
         m = tv_model.eval()
-        self.stem = _StemConv(m.conv1, m.bn1, self.device)
+        dev = self.device
+        self.stem = _StemConv(m.conv1, m.bn1, dev)
+        # stages: (blocks, geometry of the stage's padded buffers)
         self.blocks = []
         cin = 64
-        for layer in (m.layer1, m.layer2, m.layer3, m.layer4):
-            for blk in layer:
+        for li, layer in enumerate((m.layer1, m.layer2, m.layer3, m.layer4)):
+            for bi, blk in enumerate(layer):
                 cout = blk.conv1.out_channels
+                if blk.conv1.stride[0] == 2:
+                    # 3x3/2 on the previous stage's padded buffer: pad 0 (physical padding)
+                    c1 = _Conv(blk.conv1, blk.bn1, dev, pad=0, pad_hi=0, out_pad=1)
+                else:
+                    c1 = _SpanConv(blk.conv1, blk.bn1, dev)
                 ds = None
                 if blk.downsample is not None:
-                    ds = _Conv(blk.downsample[0], blk.downsample[1], cin, self.device)
-                self.blocks.append((_Conv(blk.conv1, blk.bn1, cin, self.device),
-                                    _Conv(blk.conv2, blk.bn2, cout, self.device), ds))
+                    # 1x1/2 reads interior pixel (2ho+1, 2wo+1) of the padded input: pad -1
+                    ds = _Conv(blk.downsample[0], blk.downsample[1], dev, pad=-1, pad_hi=-1,
+                               out_pad=1)
+                self.blocks.append((li, c1, _SpanConv(blk.conv2, blk.bn2, dev), ds))
                 cin = cout
         self.num_classes = m.fc.out_features
         npad = (self.num_classes + 31) // 32 * 32
@@ -130,28 +171,29 @@ class ResNet18B200:
         wfc[: self.num_classes] = m.fc.weight.detach().float().cpu()
         bfc = torch.zeros(npad, dtype=torch.float32)
         bfc[: self.num_classes] = m.fc.bias.detach().float().cpu()
-        self.w_fc = wfc.to(self.device, torch.bfloat16).contiguous()
-        self.b_fc = bfc.to(self.device).contiguous()
+        self.w_fc = wfc.to(dev, torch.bfloat16).contiguous()
+        self.b_fc = bfc.to(dev).contiguous()
         B, H = max_batch, image
-        z = dict(dtype=torch.bfloat16, device=self.device)
+        z = dict(dtype=torch.bfloat16, device=dev)
         self.x16 = torch.empty(B * (H // 2) * (H // 2) * 16, **z)   # space-to-depth stem input
-        big = B * (H // 2) * (H // 2) * 64
-        self.buf = [torch.empty(big, **z) for _ in range(3)]
+        self.stem_out = torch.empty(B * (H // 2) * (H // 2) * 64, **z)
+        self.sizes = [H // 4, H // 8, H // 16, H // 32]             # 56, 28, 14, 7
+        chans = [64, 128, 256, 512]
+        # three zero-bordered buffers per stage (zeroed once; interiors rewritten every forward)
+        self.stage_bufs = [[torch.zeros(B * (s + 2) * (s + 2) * c, **z) for _ in range(3)]
+                           for s, c in zip(self.sizes, chans)]
         self.pooled = torch.empty((B, 512), **z)
-        self.logits = torch.empty((B, npad), dtype=torch.float32, device=self.device)
+        self.logits = torch.empty((B, npad), dtype=torch.float32, device=dev)
 
     def flops(self, batch: int) -> float:
         """Algorithmic FLOPs (3.628 GF/img at 224x224)."""
-        n, h = batch, self.image
-        f = self.stem.flops(n, h // 2, h // 2)   # the stem runs on the s2d(2) input
-        h = h // 4
-        for c1, c2, ds in self.blocks:
-            f += c1.flops(n, h, h)
-            h2, _ = c1.out_hw(h, h)
-            f += c2.flops(n, h2, h2)
+        n = batch
+        f = self.stem.flops(n, self.image // 2, self.image // 2)
+        for li, c1, c2, ds in self.blocks:
+            s = self.sizes[li]
+            f += c1.flops(n, s, s) + c2.flops(n, s, s)
             if ds is not None:
-                f += ds.flops(n, h, h)
-            h = h2
+                f += ds.flops(n, s, s)
         f += 2.0 * n * 512 * self.num_classes
         return f
 
@@ -172,29 +214,32 @@ class ResNet18B200:
         H = self.image
         st = _native.stream_ptr(stream)
         cnt = _native.ptr(count)
-        a, b, c = (t.data_ptr() for t in self.buf)
-        h, w = self.stem(lib, self.x16.data_ptr(), B, H // 2, H // 2, a, st, count=count)  # 112x112x64
-        _native.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(C.c_void_p(a), B, h, w, 64,
-                                                            C.c_void_p(b), cnt, st))
-        h, w = (h + 1) // 2, (w + 1) // 2                                      # 56x56x64
-        cur, free = b, [a, c]
-        for conv1, conv2, ds in self.blocks:
-            t1 = free[0]
-            h2, w2 = conv1(lib, cur, B, h, w, t1, st, relu=True, count=count)
-            if ds is not None:
-                # identity branch = 1x1/2 conv + BN; the block input is dead afterwards
-                t2 = free[1]
-                ds(lib, cur, B, h, w, t2, st, relu=False, count=count)
-                conv2(lib, t1, B, h2, w2, cur, st, residual=t2, relu=True, count=count)
-                free = [t1, t2]
+        h, w = self.stem(lib, self.x16.data_ptr(), B, H // 2, H // 2, self.stem_out.data_ptr(),
+                         st, count=count)                                     # 112x112x64 dense
+        bufs = [[t.data_ptr() for t in stage] for stage in self.stage_bufs]
+        _native.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(
+            _native.ptr(self.stem_out), B, h, w, 64, C.c_void_p(bufs[0][0]), 1, cnt, st))
+        cur, free = bufs[0][0], [bufs[0][1], bufs[0][2]]
+        stage = 0
+        for li, c1, c2, ds in self.blocks:
+            s = self.sizes[li]
+            if li != stage:   # first block of a new stage: strided conv + downsample
+                sp = self.sizes[stage] + 2                       # previous padded extent
+                t1, t2, out = bufs[li]
+                c1(lib, cur, B, sp, sp, t1, st, relu=True, count=count)
+                ds(lib, cur, B, sp, sp, t2, st, relu=False, count=count)
+                c2(lib, t1, B, s, s, out, st, residual=t2, relu=True, count=count)
+                cur, free = out, [t1, t2]
+                stage = li
             else:
-                out = free[1]
-                conv2(lib, t1, B, h2, w2, out, st, residual=cur, relu=True, count=count)
+                t1, out = free
+                c1(lib, cur, B, s, s, t1, st, relu=True, count=count)
+                c2(lib, t1, B, s, s, out, st, residual=cur, relu=True, count=count)
                 free = [cur, t1]
                 cur = out
-            h, w = h2, w2
-        _native.check("gg_avgpool", lib.gg_avgpool(C.c_void_p(cur), B, h * w, 512,
-                                                   _native.ptr(self.pooled), cnt, st))
+        s = self.sizes[-1]
+        _native.check("gg_avgpool", lib.gg_avgpool(C.c_void_p(cur), B, (s + 2) * (s + 2), 512,
+                                                   _native.ptr(self.pooled), s * s, cnt, st))
         gemm(lib, self.pooled.data_ptr(), 512, self.w_fc, self.logits.data_ptr(),
              self.logits.stride(0), B, self.w_fc.shape[0], 512, st, bias=self.b_fc,
              out_mode=OUT_F32, tile_n=64, count=count, rows_per_item=1)

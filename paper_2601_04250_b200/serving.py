@@ -171,21 +171,38 @@ class GatedServer:
 
     # ------------------------------------------------------------------ graphs
     def capture(self) -> None:
-        """Capture one step as a CUDA graph (after one eager warm-up step)."""
+        """Capture one step as CUDA graph(s) (after one eager warm-up step).
+
+        Single GPU: the whole step is one graph.  Multi-GPU: the local part and
+        the feedback part are two graphs and the NCCL all_reduce of the
+        exchange buffer runs between them on the same stream (no collective
+        inside a captured graph, so any NCCL/torch combination works)."""
         torch = self.torch
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=self.stream):
-            self.step()
-        self.graph = g
+        if self.world == 1:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                self.step()
+            self.graph = (g,)
+        else:
+            ga, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ga, stream=self.stream):
+                self.step_local()
+            with torch.cuda.graph(gb, stream=self.stream):
+                self.step_feedback()
+            self.graph = (ga, gb)
 
     def run(self, steps: int) -> None:
         torch = self.torch
         with torch.cuda.stream(self.stream):   # replay() launches on the current stream
             for _ in range(steps):
-                if self.graph is not None:
-                    self.graph.replay()
-                else:
+                if self.graph is None:
                     self.step()
+                elif len(self.graph) == 1:
+                    self.graph[0].replay()
+                else:
+                    self.graph[0].replay()
+                    torch.distributed.all_reduce(self.slots, group=self.pg)
+                    self.graph[1].replay()
         self.steps_run += steps
 
     # ------------------------------------------------------------------ host views

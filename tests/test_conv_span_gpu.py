@@ -1,0 +1,51 @@
+"""3x3/1 span convolution on padded activations (gg_conv3x3_padded) vs torch fp32."""
+
+from __future__ import annotations
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def pack_span_weights(w):
+    """[Cout, C, 3, 3] -> [Cout, C/64, 3, 3, 64] flattened (K order: block, tap, channel)."""
+    cout, c = w.shape[:2]
+    return (w.permute(0, 2, 3, 1).reshape(cout, 9, c // 64, 64).permute(0, 2, 1, 3)
+            .reshape(cout, 9 * c).contiguous())
+
+
+@pytest.mark.parametrize("n,h,c,cout,res", [(2, 56, 64, 64, True), (2, 28, 128, 128, False),
+                                            (3, 14, 256, 256, True), (2, 7, 512, 512, True),
+                                            (1, 7, 64, 128, False)])
+def test_span_conv_vs_torch(n, h, c, cout, res):
+    import torch
+    from paper_2601_04250_b200 import _native as nat
+    lib = nat.load()
+    g = torch.Generator(device="cuda").manual_seed(n * h + c)
+    x = torch.randn((n, c, h, h), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((cout, c, 3, 3), device="cuda", generator=g) / (9 * c) ** 0.5).to(torch.bfloat16)
+    b = torch.randn(cout, device="cuda", generator=g)
+    ref = torch.nn.functional.conv2d(x.float(), w.float(), b, padding=1)
+    xp = torch.zeros((n, h + 2, h + 2, c), dtype=torch.bfloat16, device="cuda")
+    xp[:, 1:-1, 1:-1] = x.permute(0, 2, 3, 1)
+    rp = None
+    if res:
+        rp = torch.zeros((n, h + 2, h + 2, cout), dtype=torch.bfloat16, device="cuda")
+        rp[:, 1:-1, 1:-1] = torch.randn((n, h, h, cout), device="cuda", generator=g).to(torch.bfloat16)
+        ref = ref + rp[:, 1:-1, 1:-1].float().permute(0, 3, 1, 2)
+    ref = torch.relu(ref)
+    y = torch.full((n, h + 2, h + 2, cout), 7.0, dtype=torch.bfloat16, device="cuda")
+    y[0, 0] = 0  # the first (W+3) positions are never written: zero them like a fresh buffer
+    y[0, 1, 0] = 0
+    wk = pack_span_weights(w)
+    nat.check("gg_conv3x3_padded", lib.gg_conv3x3_padded(
+        nat.ptr(xp), n, h, h, c, nat.ptr(wk), cout, nat.ptr(b), nat.ptr(rp), 1, nat.ptr(y), None,
+        nat.stream_ptr()))
+    torch.cuda.synchronize()
+    got = y[:, 1:-1, 1:-1].float().permute(0, 3, 1, 2)
+    err = (got - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+    # borders (except the never-written first W+3 positions) are zeros
+    border = torch.ones((n, h + 2, h + 2), dtype=torch.bool, device="cuda")
+    border[:, 1:-1, 1:-1] = False
+    assert (y[border].float() == 0).all()

@@ -46,7 +46,7 @@ def test_conv_vs_torch(env, n, h, cin, cout, r, stride, pad, res):
     y = torch.empty((n, ho, ho, cout), dtype=torch.bfloat16, device="cuda")
     nat.check("gg_conv2d", lib.gg_conv2d(nat.ptr(xn), n, h, h, cin, nat.ptr(wk), cout, r, r, stride,
                                          pad, kpad, nat.ptr(b), nat.ptr(resid), 1, nat.ptr(y),
-                                         -1, None, nat.stream_ptr()))
+                                         -1, 0, None, nat.stream_ptr()))
     got = y.float().permute(0, 3, 1, 2)
     err = (got - ref).abs().max().item()
     assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
@@ -85,13 +85,22 @@ def test_pools(env):
     xn = x.permute(0, 2, 3, 1).contiguous()
     y = torch.empty((2, 56, 56, 64), dtype=torch.bfloat16, device="cuda")
     nat.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(nat.ptr(xn), 2, 112, 112, 64, nat.ptr(y),
-                                                     None, nat.stream_ptr()))
+                                                     0, None, nat.stream_ptr()))
     ref = torch.nn.functional.max_pool2d(x.float(), 3, 2, 1)
     assert torch.equal(y.float().permute(0, 3, 1, 2), ref)
     z = torch.empty((2, 64), dtype=torch.bfloat16, device="cuda")
-    nat.check("gg_avgpool", lib.gg_avgpool(nat.ptr(y), 2, 56 * 56, 64, nat.ptr(z), None,
+    nat.check("gg_avgpool", lib.gg_avgpool(nat.ptr(y), 2, 56 * 56, 64, nat.ptr(z), 0, None,
                                            nat.stream_ptr()))
     assert (z.float() - ref.mean(dim=(2, 3))).abs().max().item() < 1e-2
+    # padded variants: maxpool into a zero-bordered buffer, avgpool over it with the interior count
+    yp = torch.zeros((2, 58, 58, 64), dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(nat.ptr(xn), 2, 112, 112, 64, nat.ptr(yp),
+                                                     1, None, nat.stream_ptr()))
+    assert torch.equal(yp[:, 1:-1, 1:-1], y) and (yp[:, 0] == 0).all() and (yp[:, :, -1] == 0).all()
+    zp = torch.empty((2, 64), dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_avgpool", lib.gg_avgpool(nat.ptr(yp), 2, 58 * 58, 64, nat.ptr(zp), 56 * 56, None,
+                                           nat.stream_ptr()))
+    assert (zp.float() - ref.mean(dim=(2, 3))).abs().max().item() < 1e-2
 
 
 @pytest.mark.parametrize("batch", [2, 64])
