@@ -208,6 +208,7 @@ def run_ours(args, wl, rank, world, local_rank, pg):
 
     # ---- roofline of the forward (full batch, CUDA events on the launch stream)
     ro = roofline_forward(srv, net, B)
+    k1 = admission_kernel_roofline(dev) if rank == 0 else None
 
     tot = torch.tensor([ms, float(served), float(decided), float(admitted), e2e["ms"],
                         float(e2e["served"])], dtype=torch.float64, device=dev)
@@ -222,14 +223,18 @@ def run_ours(args, wl, rank, world, local_rank, pg):
     e2e_served_all = tot[5].item()
     res = srv.results()
     return dict(ms=ms_max, served=served_all, decided=decided_all, admitted=admitted_all,
-                e2e_ms=e2e_ms_max, e2e_served=e2e_served_all, e2e=e2e, roofline=ro, clocks=clk,
+                e2e_ms=e2e_ms_max, e2e_served=e2e_served_all, e2e=e2e, roofline=ro, clocks=clk, k1=k1,
                 launches_per_step=launches_per_step, overflow=res["overflow"],
                 queue_depth=res["queue_depth"])
 
 
 def run_e2e(srv, scores_np, now_np, payloads, wl, steps, warmup):
-    """Public-API loop with host buffers: per step H2D of the window rows and their
-    payloads (pinned), graph replay, D2H of the served batch's outputs + decisions."""
+    """Public-API loop with host buffers, pipelined like a serving front end: the
+    window of step i+1 (scores, arrival times, payload images: pinned host ->
+    device on a copy stream) uploads while step i computes; every step's served
+    predictions/confidences and the window's decisions come back device -> host
+    and the host waits for them one step behind.  All copies are inside the
+    timed region (CUDA events)."""
     import torch
     W, T = srv.W, srv.T
     f = srv.fifo_state()
@@ -238,66 +243,117 @@ def run_e2e(srv, scores_np, now_np, payloads, wl, steps, warmup):
     if srv.kind == "resnet18":
         host_pay = torch.randint(0, 256, tuple(payloads.shape[1:]), dtype=torch.uint8)
         host_pay = host_pay.unsqueeze(0).repeat(W, 1, 1, 1).pin_memory()
+        dev_pay = payloads
+        pay_row = host_pay[0].numel()
     else:
         host_pay = payloads[0][:W].cpu().pin_memory()
+        dev_pay = payloads[0]
+        pay_row = host_pay[0].numel() * 4
     host_scores = torch.from_numpy(scores_np).pin_memory()
     host_now = torch.from_numpy(now_np).pin_memory()
-    out_count = torch.empty(1, dtype=torch.int32).pin_memory()
-    out_pred = torch.empty(srv.B, dtype=torch.int32).pin_memory()
-    out_conf = torch.empty(srv.B, dtype=torch.float64).pin_memory()
-    out_dec = torch.empty(W, dtype=torch.uint8).pin_memory()
-    h2d = d2h = 0
+    outs = [dict(count=torch.empty(1, dtype=torch.int32).pin_memory(),
+                 pred=torch.empty(srv.B, dtype=torch.int32).pin_memory(),
+                 conf=torch.empty(srv.B, dtype=torch.float64).pin_memory(),
+                 dec=torch.empty(W, dtype=torch.uint8).pin_memory()) for _ in range(2)]
     s = srv.stream
+    cs = torch.cuda.Stream(device=srv.dev)
+    ev_in = [torch.cuda.Event(), torch.cuda.Event()]
+    ev_out = [torch.cuda.Event(), torch.cuda.Event()]
+    stats = {"h2d": 0, "d2h": 0}
 
-    def one(c):
-        nonlocal h2d, d2h
+    def upload(c, slot):
         c1 = min(T, c + W)
         n = c1 - c
-        with torch.cuda.stream(s):
+        with torch.cuda.stream(cs):
             srv.scores[c:c1].copy_(host_scores[c:c1], non_blocking=True)
             srv.now[c:c1].copy_(host_now[c:c1], non_blocking=True)
-            # payloads of the window into their pool slots (row % P)
-            lo, hi = c % P, c % P + n
-            if srv.kind == "resnet18":
-                if hi <= P:
-                    payloads[lo:hi].copy_(host_pay[:n], non_blocking=True)
-                else:
-                    payloads[lo:].copy_(host_pay[:P - lo], non_blocking=True)
-                    payloads[: hi - P].copy_(host_pay[P - lo:n], non_blocking=True)
-                pay_bytes = n * host_pay[0].numel()
+            lo, hi = c % P, c % P + n        # payloads go to their pool slots (row % P)
+            if hi <= P:
+                dev_pay[lo:hi].copy_(host_pay[:n], non_blocking=True)
             else:
-                ids = payloads[0]
-                if hi <= P:
-                    ids[lo:hi].copy_(host_pay[:n], non_blocking=True)
-                else:
-                    ids[lo:].copy_(host_pay[:P - lo], non_blocking=True)
-                    ids[: hi - P].copy_(host_pay[P - lo:n], non_blocking=True)
-                pay_bytes = n * host_pay[0].numel() * 4
-            h2d += n * (srv.K + 1) * 8 + pay_bytes
-        srv.run(1)
-        with torch.cuda.stream(s):
-            out_count.copy_(srv.count, non_blocking=True)
-            out_pred.copy_(srv.batch_pred, non_blocking=True)
-            out_conf.copy_(srv.batch_conf, non_blocking=True)
-            out_dec[:n].copy_(srv.decision[c:c1], non_blocking=True)
-            d2h += 4 + srv.B * 12 + n
-        s.synchronize()
+                dev_pay[lo:].copy_(host_pay[:P - lo], non_blocking=True)
+                dev_pay[: hi - P].copy_(host_pay[P - lo:n], non_blocking=True)
+            ev_in[slot].record(cs)
+        stats["h2d"] += n * (srv.K + 1) * 8 + n * pay_row
         return c1
 
-    for _ in range(warmup):
-        cursor = one(cursor)
+    def run(nsteps, c):
+        nxt = upload(c, 0)
+        for i in range(nsteps):
+            slot = i & 1
+            s.wait_event(ev_in[slot])
+            srv.run(1)
+            o = outs[slot]
+            n = nxt - c
+            with torch.cuda.stream(s):
+                o["count"].copy_(srv.count, non_blocking=True)
+                o["pred"].copy_(srv.batch_pred, non_blocking=True)
+                o["conf"].copy_(srv.batch_conf, non_blocking=True)
+                o["dec"][:n].copy_(srv.decision[c:nxt], non_blocking=True)
+                ev_out[slot].record(s)
+            stats["d2h"] += 4 + srv.B * 12 + n
+            c = nxt
+            if i + 1 < nsteps:
+                nxt = upload(c, slot ^ 1)
+            if i >= 1:
+                ev_out[slot ^ 1].synchronize()   # host consumes step i-1's results
+        ev_out[(nsteps - 1) & 1].synchronize()
+        return c
+
+    cursor = run(warmup, cursor)
     f0 = srv.fifo_state()
-    h2d = d2h = 0
+    stats["h2d"] = stats["d2h"] = 0
     torch.cuda.synchronize()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st.record(s)
-    for _ in range(steps):
-        cursor = one(cursor)
+    cs.wait_stream(s)
+    cursor = run(steps, cursor)
     en.record(s)
     torch.cuda.synchronize()
     f1 = srv.fifo_state()
     return {"ms": st.elapsed_time(en), "served": int(f1.head - f0.head),
-            "h2d_bytes_per_step": h2d // max(1, steps), "d2h_bytes_per_step": d2h // max(1, steps)}
+            "h2d_bytes_per_step": stats["h2d"] // max(1, steps),
+            "d2h_bytes_per_step": stats["d2h"] // max(1, steps)}
+
+
+def admission_kernel_roofline(dev, n_rows: int = 1 << 26, k: int = 2, reps: int = 10):
+    """K1 alone at scale (the north star's HBM evidence): decide_batch over n_rows
+    device-resident K=2 fp64 score rows with one frozen snapshot, writing the
+    decision codes and the dense admitted-index list.  Algorithmic bytes per
+    launch = n*(8k + 8 + 1) + 4*n_admitted; inputs (1.6 GB) exceed L2."""
+    import torch
+    import paper_2601_04250_b200 as gg
+    g = torch.Generator(device=dev).manual_seed(7)
+    c = torch.rand(n_rows, generator=g, device=dev, dtype=torch.float64) * 0.5 + 0.5
+    scores = torch.stack([c, 1.0 - c], dim=1).contiguous()
+    now = torch.linspace(0.0, 10.0, n_rows, device=dev, dtype=torch.float64)
+    del c
+    ctl = gg.ControllerConfig(alpha=1.0, beta=-0.1, gamma=-0.3, tau0=0.9, tau_inf=0.4, k=0.5,
+                              routing=gg.RoutePolicy.THRESHOLD_ON_QUEUE).build(gg.EnergyLedger(),
+                                                                               device=dev)
+    snap = gg.CongestionSnapshot(3, 7.5, 0.25)
+    out = ctl.decide_batch(scores, now, snap, breakdown=False)
+    torch.cuda.synchronize()
+    n_adm = out.n_admitted
+    s = torch.cuda.current_stream(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(reps):
+        ctl.decide_batch(scores, now, snap, breakdown=False, out=out)
+    b.record(s)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    nbytes = n_rows * (8 * k + 8 + 1) + 4 * n_adm
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    pk = peaks()
+    res = {"kernel": "admit_small_kernel<2> (K1: validate + entropy + J/tau + ballot compaction)",
+           "rows": n_rows, "k": k, "ms_per_launch": round(ms, 4),
+           "decisions_per_s": round(n_rows / (ms * 1e-3), 1), "bound": "hbm",
+           "achieved": round(gbs, 1), "peak": pk["hbm"], "unit": "GB/s",
+           "frac": round(gbs / pk["hbm"], 4), "bytes_per_launch": nbytes, "admitted": n_adm}
+    del scores, now, out
+    torch.cuda.empty_cache()
+    return res
 
 
 def roofline_forward(srv, net, B):
@@ -467,7 +523,7 @@ def main():
             "admission_rate": round(r["admitted"] / max(1, r["decided"]), 4),
             "mean_forward_batch": round(r["served"] / (args.steps * world), 2),
             "queue_depth_end": r["queue_depth"], "fifo_overflow": r["overflow"],
-            "roofline": r["roofline"], "cpu_baseline": cpu,
+            "roofline": r["roofline"], "admission_roofline": r["k1"], "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 2) if e2e_value else None, "unit": "inferences/s",
                     "h2d_bytes_per_step": r["e2e"]["h2d_bytes_per_step"],
                     "d2h_bytes_per_step": r["e2e"]["d2h_bytes_per_step"]},

@@ -631,14 +631,30 @@ __global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, 
       skip_other += (int64_t)sl[5];
     }
   }
+  // Inputs are staged through shared memory in chunks (coalesced, all lanes) so
+  // the sequential loop never waits on a global-memory round trip.
+  constexpr int kStage = 256;
+  __shared__ double st_l[kStage], st_j[kStage];
+  __shared__ int32_t st_q[kStage];
   const int nslots = slots ? G : 1;
   for (int gi = 0; gi < nslots && bad < 0; ++gi) {
   const double* sl = slots ? slots + (int64_t)gi * (3 * B + 8) : nullptr;
   const int64_t ng = sl ? (int64_t)sl[3 * B] : n;
-  for (int64_t i = 0; i < ng; ++i) {
-    const double L = sl ? sl[i] : lat[i];
-    const double J = sl ? sl[B + i] : jou[i];
-    const int32_t Q = sl ? (int32_t)sl[2 * B + i] : qd[i];
+  for (int64_t i0 = 0; i0 < ng && bad < 0; i0 += kStage) {
+  const int cn = (int)min((int64_t)kStage, ng - i0);
+  __syncwarp();
+  for (int e = lane; e < cn; e += 32) {
+    const int64_t i = i0 + e;
+    st_l[e] = sl ? sl[i] : lat[i];
+    st_j[e] = sl ? sl[B + i] : jou[i];
+    st_q[e] = sl ? (int32_t)sl[2 * B + i] : qd[i];
+  }
+  __syncwarp();
+  for (int e = 0; e < cn; ++e) {
+    const int64_t i = i0 + e;
+    const double L = st_l[e];
+    const double J = st_j[e];
+    const int32_t Q = st_q[e];
     if (L < 0.0 || J < 0.0 || Q < 0) {  // NegativeMeasurement (controller.py:347-353)
       bad = sl ? (int64_t)gi * B + i : i;
       break;
@@ -669,6 +685,7 @@ __global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, 
     ch_observe(cp, p95);
     outc += 1;
     if (set_qd) last_qd = Q;
+  }
   }
   }
   __syncwarp();
