@@ -32,9 +32,12 @@ __device__ __forceinline__ double f64_div(double a, double b) { return __ddiv_rn
 struct NeumaierSum {
   double s = 0.0, c = 0.0;
   __device__ __forceinline__ void add(double x) {
-    double t = f64_add(s, x);
-    if (fabs(s) >= fabs(x)) c = f64_add(c, f64_add(f64_sub(s, t), x));
-    else c = f64_add(c, f64_add(f64_sub(x, t), s));
+    // both compensation candidates are computed and one is selected (no
+    // divergence, and only `s` is on the loop-carried critical path)
+    const double t = f64_add(s, x);
+    const double big_s = f64_add(f64_sub(s, t), x);
+    const double big_x = f64_add(f64_sub(x, t), s);
+    c = f64_add(c, fabs(s) >= fabs(x) ? big_s : big_x);
     s = t;
   }
   __device__ __forceinline__ double result() const {

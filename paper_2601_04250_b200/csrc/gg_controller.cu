@@ -169,6 +169,37 @@ struct RowAcc {
   }
 };
 
+// ---- fast filter (no breakdown requested) ---------------------------------
+// The decision only needs the SIGN of J - tau.  Utilities from fp32 logs
+// (summed in fp64) and tau from an fp32 exp are within a proven bound of the
+// exact fp64 values (|du| <= 1e-5, |dtau| <= 1e-4 |tau0 - tau_inf|); when
+// |J_fast - tau_fast| exceeds the induced margin the decision is provably the
+// exact one, otherwise the row is recomputed exactly (CPython-order fp64).
+// Validation (the sum check) is always exact.
+__device__ __forceinline__ double entropy_term_fast(double p) {
+  const float pf = (float)p;
+  return (pf > 0.0f) ? (double)(pf * __logf(pf)) : 0.0;   // p < FLT_MIN: |p ln p| < 1e-36
+}
+
+// Returns the decision code, or -1 when J is too close to tau to decide fast.
+__device__ __forceinline__ int decide_fast(const AdmitArgs& a, const BatchConst& b, double u_f,
+                                           double du, double now) {
+  const gg_params& p = a.p;
+  const double j = p.alpha * u_f + p.beta * b.e + p.gamma * b.c;
+  double el = now - b.t_origin;
+  el = (el > 0.0) ? el : 0.0;
+  const double e = (double)__expf((float)(-p.k * el));
+  const double tau = p.tau_inf + (p.tau0 - p.tau_inf) * e;
+  const double margin = fabs(p.alpha) * du + fabs(p.tau0 - p.tau_inf) * 1e-4 + 1e-12;
+  if (fabs(j - tau) <= margin) return -1;
+  const bool admit = (p.direction == GG_DIR_GEQ) ? (j > tau) : (j < tau);
+  if (!admit) return GG_DECISION_SKIP;
+  if (p.routing == GG_ROUTE_ALL_BATCHED) return GG_DECISION_BATCHED;
+  if (p.routing == GG_ROUTE_THRESHOLD_ON_QUEUE)
+    return (b.qd > (int64_t)p.queue_threshold) ? GG_DECISION_BATCHED : GG_DECISION_DIRECT;
+  return GG_DECISION_DIRECT;
+}
+
 // The per-request tail of decide(): J, tau(now), admit, route
 // (controller.py:326-337).
 __device__ __forceinline__ uint8_t decide_row(const AdmitArgs& a, const BatchConst& b, double u,
@@ -361,24 +392,50 @@ __global__ void __launch_bounds__(THREADS) admit_small_kernel(AdmitArgs a) {
     uint8_t code = GG_DECISION_SKIP;
     if (in) {
       const double* row = a.probs + g * a.stride;
-      RowAcc acc;
+      double xv[KC > 0 ? KC : 16];
       if constexpr (KC == 2) {
-        double2 v = *reinterpret_cast<const double2*>(row);
-        acc.add(v.x, entropy);
-        acc.add(v.y, entropy);
+        const double2 v = *reinterpret_cast<const double2*>(row);
+        xv[0] = v.x; xv[1] = v.y;
       } else if constexpr (KC == 4) {
-        double2 v0 = *reinterpret_cast<const double2*>(row);
-        double2 v1 = *reinterpret_cast<const double2*>(row + 2);
-        acc.add(v0.x, entropy);
-        acc.add(v0.y, entropy);
-        acc.add(v1.x, entropy);
-        acc.add(v1.y, entropy);
+        const double2 v0 = *reinterpret_cast<const double2*>(row);
+        const double2 v1 = *reinterpret_cast<const double2*>(row + 2);
+        xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
       } else {
-        for (int c = 0; c < k; ++c) acc.add(row[c], entropy);
+        for (int c = 0; c < k; ++c) xv[c] = row[c];
       }
       double u, jv = 0.0, tau = 0.0;
-      if (acc.finish(k, entropy, a.ln_k, u)) {
-        code = decide_row(a, b, u, a.now[g], jv, tau);
+      bool valid;
+      const double now_g = a.now[g];
+      int fast = -1;
+      if (!a.breakdown) {
+        // exact validation (cheap), approximate utility, then the margin test
+        bool ok = true, first = true;
+        NeumaierSum tot;
+        double hf = 0.0, mx = 0.0;
+#pragma unroll
+        for (int c = 0; c < (KC > 0 ? KC : 16); ++c) {
+          if (KC == 0 && c >= k) break;
+          const double x = xv[c];
+          if (!isfinite(x) || x < 0.0) ok = false;
+          tot.add(x);
+          if (entropy) hf += entropy_term_fast(x);
+          if (first || x > mx) mx = x;
+          first = false;
+        }
+        valid = ok && k >= 2 && !(fabs(f64_sub(tot.result(), 1.0)) > 1e-9);
+        if (valid) {
+          const double u_f = entropy ? clamp01(-hf / a.ln_k) : f64_sub(1.0, mx);
+          fast = decide_fast(a, b, u_f, entropy ? 1e-5 : 0.0, now_g);
+          if (fast >= 0) code = (uint8_t)fast;
+        }
+      }
+      if (a.breakdown || (valid && fast < 0)) {
+        RowAcc acc;   // exact CPython-order evaluation (controller.py:126-148)
+        for (int c = 0; c < k; ++c) acc.add(xv[c], entropy);
+        valid = acc.finish(k, entropy, a.ln_k, u);
+        if (valid) code = decide_row(a, b, u, now_g, jv, tau);
+      }
+      if (valid) {
         if (code == GG_DECISION_SKIP) ++my_skip;
       } else {
         code = GG_DECISION_INVALID;
@@ -459,12 +516,18 @@ __global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a)
     for (int c = 0; c < nchunks; ++c) {
       const int buf = c & 1, cw = min(kChunk, a.k - c * kChunk);
       named_sync(1 + buf, kLargeThreads);
+      // unrolled with a guard so the shared-memory loads issue ahead of the
+      // loop-carried Neumaier chain
       if (warp == 0) {
-        if (entropy)
-          for (int cc = 0; cc < cw; ++cc)
-            if (raw[buf][lane][cc] > 0.0) s.add(term[buf][lane][cc]);
+        if (entropy) {
+#pragma unroll 8
+          for (int cc = 0; cc < kChunk; ++cc)
+            if (cc < cw && raw[buf][lane][cc] > 0.0) s.add(term[buf][lane][cc]);
+        }
       } else {
-        for (int cc = 0; cc < cw; ++cc) {
+#pragma unroll 8
+        for (int cc = 0; cc < kChunk; ++cc) {
+          if (cc >= cw) break;
           const double x = raw[buf][lane][cc];
           if (!isfinite(x) || x < 0.0) ok = false;
           s.add(x);
@@ -514,6 +577,81 @@ __global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a)
       a.breakdown[3 * g + 2] = tau;
     }
   }
+  uint32_t ballots[1] = {__ballot_sync(0xffffffffu, in && (code == GG_DECISION_DIRECT || code == GG_DECISION_BATCHED))};
+  finish_tile<kLargeThreads, 1>(a, sm, tile0, ballots, my_skip, my_inv, my_bad);
+}
+
+// K1, large K, fast filter (no breakdown requested; the serving loop): one warp
+// per row, coalesced loads, fp64 sum of the probabilities and of fp32-log
+// entropy terms, warp reductions — no sequential chain.  A row is recomputed
+// exactly (sequential CPython order, one lane) only when its sum lies within
+// 1e-13 of the 1e-9 validation bound or J lies within the margin of tau.
+__global__ void __launch_bounds__(kLargeThreads) admit_large_fast_kernel(AdmitArgs a) {
+  __shared__ AdmitShared<kLargeThreads, 1> sm;
+  __shared__ uint8_t codes[kLargeRows];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) block_setup(a, sm);
+  __syncthreads();
+  const BatchConst b = sm.bc;
+  const int64_t tile0 = (int64_t)sm.vb * kLargeRows;
+  const int64_t nw = sm.nw, row0 = sm.row0;
+  const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
+  for (int lr = warp; lr < kLargeRows; lr += kLargeThreads / 32) {
+    const int64_t r = tile0 + lr;
+    if (r >= nw) {
+      if (lane == 0) codes[lr] = GG_DECISION_SKIP;
+      continue;
+    }
+    const int64_t g = row0 + r;
+    const double* row = a.probs + g * a.stride;
+    double sum = 0.0, hf = 0.0, mx = -INFINITY;
+    bool ok = true;
+    for (int c = lane; c < a.k; c += 32) {
+      const double x = __ldg(row + c);
+      if (!isfinite(x) || x < 0.0) ok = false;
+      sum += x;
+      if (entropy) hf += entropy_term_fast(x);
+      mx = fmax(mx, x);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      hf += __shfl_xor_sync(0xffffffffu, hf, o);
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (lane == 0) {
+      // pairwise-ish fp64 sum of <= K nonnegative terms: |error| < K * 2^-52 * sum
+      const double dev = fabs(sum - 1.0), bound = (double)a.k * 2.3e-16 * (sum + 1.0);
+      int code;
+      bool exact = false, valid = ok && a.k >= 2;
+      if (valid && dev > 1e-9 + bound) valid = false;
+      else if (valid && dev > 1e-9 - bound) exact = true;   // too close to the bound
+      if (valid && !exact) {
+        const double u_f = entropy ? clamp01(-hf / a.ln_k) : f64_sub(1.0, mx);
+        code = decide_fast(a, b, u_f, entropy ? 1e-5 : 0.0, a.now[g]);
+        if (code < 0) exact = true;
+      } else {
+        code = GG_DECISION_INVALID;
+      }
+      if (exact) {   // rare: the reference's own sequential evaluation
+        RowAcc acc;
+        for (int c = 0; c < a.k; ++c) acc.add(row[c], entropy);
+        double u, jv, tau;
+        code = acc.finish(a.k, entropy, a.ln_k, u) ? decide_row(a, b, u, a.now[g], jv, tau)
+                                                   : GG_DECISION_INVALID;
+      }
+      codes[lr] = (uint8_t)code;
+      a.decision[g] = (uint8_t)code;
+    }
+  }
+  __syncthreads();
+  const int64_t r = tile0 + tid;           // rows live on warp 0's lanes for the compaction
+  const bool in = warp == 0 && r < nw;
+  const uint8_t code = in ? codes[tid] : (uint8_t)GG_DECISION_SKIP;
+  int my_skip = (in && code == GG_DECISION_SKIP) ? 1 : 0;
+  int my_inv = (in && code == GG_DECISION_INVALID) ? 1 : 0;
+  unsigned long long my_bad = my_inv ? (unsigned long long)(nw - r) : 0ull;
   uint32_t ballots[1] = {__ballot_sync(0xffffffffu, in && (code == GG_DECISION_DIRECT || code == GG_DECISION_BATCHED))};
   finish_tile<kLargeThreads, 1>(a, sm, tile0, ballots, my_skip, my_inv, my_bad);
 }
@@ -944,6 +1082,8 @@ static int launch_admit(const AdmitArgs& a, void* stream) {
     admit_small_kernel<4, 256, 4><<<(unsigned)nb, 256, 0, s>>>(a);
   else if (k <= 16)
     admit_small_kernel<0, 256, 4><<<(unsigned)nb, 256, 0, s>>>(a);
+  else if (a.breakdown == nullptr && !getenv("GG_ADMIT_EXACT_ONLY"))
+    admit_large_fast_kernel<<<(unsigned)nb, kLargeThreads, 0, s>>>(a);
   else
     admit_large_kernel<<<(unsigned)nb, kLargeThreads, 0, s>>>(a);
   GG_LAUNCH_OK();

@@ -36,6 +36,7 @@ struct SpanShape {
   int span_rows;       // 128 + 2*Wp + 2
   int plane_bytes;     // span_rows * 16 rounded up to 128
   int bres;            // B resident for the whole CTA
+  int sw128;           // A span as 128B-swizzled 64-channel rows (else 16-B channel planes)
 };
 
 struct SpanEpi {
@@ -124,8 +125,12 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
           mbar_wait(&a_empty[as], ((ait >> 1) & 1) ^ 1);
           uint8_t* sa = a_base + as * kSpanAStage;
           mbar_expect_tx(&a_full[as], 8 * sh.span_rows * 16);
-          for (int p = 0; p < 8; ++p)   // box = [8 channels, span_rows] per plane
-            tma_load_2d(sa + p * sh.plane_bytes, &map_x, &a_full[as], cb * 64 + p * 8, m0);
+          if (sh.sw128) {   // one box [64 channels, span_rows], 128B-swizzled rows
+            tma_load_2d(sa, &map_x, &a_full[as], cb * 64, m0);
+          } else {
+            for (int p = 0; p < 8; ++p)   // box = [8 channels, span_rows] per plane
+              tma_load_2d(sa + p * sh.plane_bytes, &map_x, &a_full[as], cb * 64 + p * 8, m0);
+          }
           if (!sh.bres) {
             for (int tap = 0; tap < 9; ++tap, ++bit) {
               const int bs = bit % BSTAGES;
@@ -167,7 +172,9 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
             }
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              umma_bf16(d_tmem, sdesc_k_none(sa + 2 * kk * sh.plane_bytes + shift, sh.plane_bytes),
+              umma_bf16(d_tmem,
+                        sh.sw128 ? sdesc_k_sw128(sa + shift * 8 + kk * 32)   // row shift: base offset
+                                 : sdesc_k_none(sa + 2 * kk * sh.plane_bytes + shift, sh.plane_bytes),
                         sdesc_k_sw128(sb + kk * 32), idesc, (cb | tap | kk) != 0);
             if (!sh.bres) {
               umma_commit(&b_empty[bs]);
@@ -334,7 +341,10 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
   }
   sh.bres = (bn == Cout) && (2 * kSpanAStage + nkb * bn * 128 + 1536 <= 227 * 1024);
   CUtensorMap mx, mw;
-  int rc = make_map_planes(&mx, x, (int64_t)N * sh.Hp * sh.Wp, C, sh.span_rows);
+  const char* lay = getenv("GG_SPAN_LAYOUT");
+  sh.sw128 = !(lay && lay[0] == 'p');   // default: 128B-swizzled rows; "planes" = 16-B planes
+  int rc = sh.sw128 ? make_map_2d(&mx, x, (int64_t)N * sh.Hp * sh.Wp, C, C, sh.span_rows)
+                    : make_map_planes(&mx, x, (int64_t)N * sh.Hp * sh.Wp, C, sh.span_rows);
   if (!rc) rc = make_map_2d(&mw, w, Cout, (int64_t)C * 9, (int64_t)C * 9, bn);
   if (rc) return rc;
   SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,

@@ -236,7 +236,8 @@ def test_replay_batch_api(gg, torch, name):
 
 @pytest.mark.parametrize("n,k", [(0, 2), (1, 2), (1023, 2), (1025, 4), (4_194_304, 2),
                                  (100_003, 4), (3000, 7), (2048, 1000), (129, 37)])
-def test_admit_vs_c_oracle_large(gg, torch, n, k):
+@pytest.mark.parametrize("breakdown", [True, False])
+def test_admit_vs_c_oracle_large(gg, torch, n, k, breakdown):
     """Order-preserving compaction and counters at scale vs the C oracle."""
     rng = np.random.default_rng(n + k)
     if k == 2:
@@ -261,8 +262,9 @@ def test_admit_vs_c_oracle_large(gg, torch, n, k):
     ctl.record_outcomes(torch.tensor([3.0, 5.0, 4.0], dtype=torch.float64, device="cuda"),
                         torch.tensor([1.0, 2.0, 1.5], dtype=torch.float64, device="cuda"),
                         torch.tensor([1, 5, 2], dtype=torch.int32, device="cuda"))
+    # with a breakdown: the exact path; without: the fast filter + exact refinement
     out = ctl.decide_batch(torch.from_numpy(rows).cuda(), torch.from_numpy(now).cuda(),
-                           gg.CongestionSnapshot(*snap))
+                           gg.CongestionSnapshot(*snap), breakdown=breakdown)
     dec = out.decision.cpu().numpy()
     band = np.abs(bd_o[:, 1] - bd_o[:, 2]) < EPS_BAND
     assert np.array_equal(dec[~band], dec_o[~band])
@@ -271,9 +273,36 @@ def test_admit_vs_c_oracle_large(gg, torch, n, k):
     assert summ["first_invalid"] == info_o.first_invalid
     assert summ["n_admitted"] == info_o.n_admitted
     assert np.array_equal(out.admitted_idx[: summ["n_admitted"]].cpu().numpy(), idx_o)
-    assert_close_ulp(out.breakdown.cpu().numpy(), bd_o, f"admit n={n} k={k}")
+    if breakdown:
+        assert_close_ulp(out.breakdown.cpu().numpy(), bd_o, f"admit n={n} k={k}")
     st = G.state_dict_of_abi(ctl.state_struct())
     assert st == G.state_dict_of_abi(orc.state)
+
+
+@pytest.mark.parametrize("k", [2, 4, 1000])
+def test_fast_filter_near_threshold(gg, torch, k):
+    """Rows engineered to sit within the fast-path margin of tau take the exact
+    path; decisions must still equal the oracle's bit-for-bit."""
+    rng = np.random.default_rng(k)
+    n = 4096
+    base = rng.integers(1, 60, size=(n, k))
+    rows = G.rows_from_base(base)
+    p = dict(alpha=1.0, beta=0.0, gamma=0.0, tau0=0.5, tau_inf=0.5, k=1.0, ewma_lambda=0.9,
+             direction=0, utility_proxy=0, routing=0, queue_threshold=4, p95_window=100)
+    orc0 = c_oracle.COracle(G.abi_params(p))
+    _d, bd0, _i, _f = orc0.admit(rows, np.zeros(n))
+    tau = float(np.median(bd0[:, 0]))          # threshold inside the utility distribution
+    p.update(tau0=tau, tau_inf=tau)
+    orc = c_oracle.COracle(G.abi_params(p))
+    dec_o, bd_o, idx_o, info_o = orc.admit(rows, np.zeros(n))
+    assert (np.abs(bd_o[:, 1] - tau) < 1e-5).sum() > 0 or k == 1000
+    ctl = gg.ControllerConfig(tau0=tau, tau_inf=tau, k=1.0).build(gg.EnergyLedger())
+    out = ctl.decide_batch(torch.from_numpy(rows).cuda(), torch.zeros(n, dtype=torch.float64,
+                                                                      device="cuda"),
+                           breakdown=False)
+    band = np.abs(bd_o[:, 1] - bd_o[:, 2]) < EPS_BAND
+    assert np.array_equal(out.decision.cpu().numpy()[~band], dec_o[~band])
+    assert np.array_equal(out.admitted_idx[: out.n_admitted].cpu().numpy(), idx_o)
 
 
 def test_epilogue_vs_oracle(gg, torch):
