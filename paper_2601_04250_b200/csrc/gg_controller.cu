@@ -16,12 +16,13 @@ namespace gg {
 // ---------------------------------------------------------------------------
 // Workspace layout (zero-filled once; every gg_admit launch leaves it zeroed).
 struct AdmitWorkspace {
-  unsigned long long vblock_counter;  // virtual block ids (forward-progress-safe lookback)
+  unsigned long long vblock_counter;  // reserved (tiles are scanned in blockIdx order)
   unsigned long long done_counter;    // completion ticket; the last block finalizes
   unsigned long long n_skipped;
   unsigned long long n_invalid;
   unsigned long long first_invalid_enc;  // max over (n - row); 0 == none
   unsigned long long reserved[3];
+  unsigned long long consts[24];      // split path: BatchConst + FastBlock of this launch
   unsigned long long status[1];       // [num_blocks] decoupled look-back words
 };
 constexpr size_t kWsHeader = offsetof(AdmitWorkspace, status);
@@ -38,26 +39,46 @@ __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long 
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Single-thread decoupled look-back (Merrill & Garland): returns the exclusive
-// prefix of admitted rows before virtual block `vb`.
-__device__ unsigned long long lookback(unsigned long long* status, int vb, unsigned long long agg) {
+// A status value packs two 31-bit counters, summed component-wise by plain
+// addition (launches are limited to < 2^31 rows): admitted rows in bits 0..30,
+// skipped rows in bits 31..61.  Carrying the skip count through the scan
+// replaces a per-warp atomic on one global counter (which serialised in L2 at
+// 2^26 rows); n_invalid = rows - admitted - skipped.
+constexpr unsigned long long kCnt31 = (1ull << 31) - 1;
+__device__ __forceinline__ unsigned long long pack_counts(unsigned long long adm, unsigned long long skip) {
+  return adm | (skip << 31);
+}
+
+// Warp-cooperative decoupled look-back (Merrill & Garland), called by all 32
+// lanes of one warp: each round inspects the 32 preceding status words at once,
+// stops at the nearest inclusive prefix.  Returns the exclusive prefix.
+__device__ unsigned long long lookback_warp(unsigned long long* status, int vb, unsigned long long agg) {
+  const int lane = threadIdx.x & 31;
   if (vb == 0) {
-    st_relaxed(&status[0], kFlagPrefix | agg);
+    if (lane == 0) st_relaxed(&status[0], kFlagPrefix | agg);
     return 0ull;
   }
-  st_relaxed(&status[vb], kFlagAgg | agg);
+  if (lane == 0) st_relaxed(&status[vb], kFlagAgg | agg);
   unsigned long long prefix = 0;
-  int p = vb - 1;
+  int base = vb - 1;
   while (true) {
-    unsigned long long w;
-    do {
-      w = ld_relaxed(&status[p]);
-    } while ((w >> 62) == 0ull);
-    prefix += w & kValMask;
-    if ((w >> 62) == 2ull) break;
-    --p;
+    const int p = base - lane;
+    unsigned long long w = kFlagPrefix;   // before block 0: an empty prefix
+    if (p >= 0) {
+      do {
+        w = ld_relaxed(&status[p]);
+      } while ((w >> 62) == 0ull);
+    }
+    const unsigned pm = __ballot_sync(0xffffffffu, (w >> 62) == 2ull);
+    const int stop = pm ? __ffs(pm) - 1 : 31;
+    unsigned long long v = lane <= stop ? (w & kValMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    prefix += v;
+    if (pm) break;
+    base -= 32;
   }
-  st_relaxed(&status[vb], kFlagPrefix | (prefix + agg));
+  if (lane == 0) st_relaxed(&status[vb], kFlagPrefix | (prefix + agg));
   return prefix;
 }
 
@@ -81,6 +102,12 @@ struct AdmitArgs {
   gg_fifo* fifo;
   int32_t* ring;
   uint64_t* ring_ns;
+  // split path (large batches): per-decide-block packed counts and per-super-
+  // block sums (2^super_shift decide blocks each), inside the workspace after
+  // the look-back words; zero between launches like the look-back words.
+  unsigned long long* split_cnt;
+  unsigned long long* super_cnt;
+  int super_shift;
 };
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
@@ -220,13 +247,13 @@ __device__ __forceinline__ uint8_t decide_row(const AdmitArgs& a, const BatchCon
 template <int THREADS, int RPT>
 struct AdmitShared {
   static constexpr int WARPS = THREADS / 32;
-  static constexpr int GROUPS = RPT * WARPS;
-  static_assert(GROUPS <= 32, "one warp scans the groups");
+  static constexpr int GROUPS = RPT * WARPS;   // 32-row groups, in row order
   BatchConst bc;
   int64_t row0, nw, depth0;   // window start/length; FIFO depth before this launch
   unsigned long long block_prefix;
   int group_cnt[GROUPS];
   int group_off[GROUPS];
+  int warp_skip[WARPS];
   int vb;
   int last;
 };
@@ -245,11 +272,15 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
   return v;
 }
 
-// Per-block prologue (thread 0): virtual block id, decision window, FIFO depth
-// and the batch-constant E/C — all read before any block can finalize.
+// Per-block prologue (thread 0): decision window, FIFO depth and the
+// batch-constant E/C — all read before any block can finalize.  Tiles are
+// scanned in blockIdx order (blocks are dispatched in increasing linear order,
+// so every predecessor of a resident block is resident or finished — the same
+// forward-progress argument CUB's single-pass scan relies on), which lets each
+// thread issue its row loads before this prologue completes.
 template <int THREADS, int RPT>
 __device__ void block_setup(const AdmitArgs& a, AdmitShared<THREADS, RPT>& sm) {
-  sm.vb = (int)atomicAdd(&a.ws->vblock_counter, 1ull);
+  sm.vb = (int)blockIdx.x;
   int64_t row0, nw;
   admit_window(a, row0, nw);
   sm.row0 = row0;
@@ -258,38 +289,97 @@ __device__ void block_setup(const AdmitArgs& a, AdmitShared<THREADS, RPT>& sm) {
   sm.bc = batch_constants(a.state, a.snap, a.fifo);
 }
 
+// Apply one decide_batch's state effects (controller.py:316-337) once, after
+// every block has read the state: observes of the frozen snapshot, the
+// admitted/skipped totals, the FIFO tail/cursor, the batch info; then leave the
+// workspace header zeroed for the next launch.  `counts` = pack_counts(adm, skip).
+__device__ void finalize_launch(const AdmitArgs& a, const BatchConst& b, int64_t row0, int64_t nw,
+                                int64_t depth0, unsigned long long counts,
+                                unsigned long long benc) {
+  const int64_t n_adm = (int64_t)(counts & kCnt31);
+  const int64_t n_skip = (int64_t)((counts >> 31) & kCnt31);
+  const int64_t n_inv = nw - n_adm - n_skip;
+  gg_state* st = a.state;
+  const bool any_valid = (nw - n_inv) > 0;
+  if (any_valid) {
+    if (b.samples_seen > 0) ch_observe(st->n_energy, b.ewma);
+    ch_observe(st->n_queue_depth, (double)b.qd);
+    ch_observe(st->n_p95_ms, b.p95);
+  }
+  st->admitted_total += n_adm;
+  st->skipped_total += n_skip;
+  if (a.fifo) {
+    const int64_t room = a.fifo->capacity - depth0;
+    a.fifo->tail += n_adm < room ? n_adm : room;
+    a.fifo->cursor = row0 + nw;
+  }
+  if (a.info) {
+    a.info->n_admitted = n_adm;
+    a.info->n_skipped = n_skip;
+    a.info->n_invalid = n_inv;
+    a.info->first_invalid = benc ? (int64_t)(row0 + nw - (int64_t)benc) : -1;
+    a.info->energy = any_valid ? b.e : 0.0;
+    a.info->congestion = any_valid ? b.c : 0.0;
+    a.info->n_decided = nw;
+    a.info->snap_queue_depth = b.qd;
+    a.info->snap_p95_ms = b.p95;
+    a.info->snap_batch_fill = b.fill;
+  }
+  a.ws->vblock_counter = 0;
+  a.ws->done_counter = 0;
+  a.ws->n_skipped = 0;
+  a.ws->n_invalid = 0;
+  a.ws->first_invalid_enc = 0;
+}
+
 // Order-preserving compaction of the tile + counters + last-block finalize.
 template <int THREADS, int RPT>
 __device__ void finish_tile(const AdmitArgs& a, AdmitShared<THREADS, RPT>& sm, int64_t tile0,
-                            const uint32_t (&ballots)[RPT], int my_skip, int my_inv,
+                            const uint32_t (&ballots)[RPT], int my_skip,
                             unsigned long long my_bad_enc) {
   constexpr int WARPS = THREADS / 32;
   constexpr int GROUPS = RPT * WARPS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ws = warp_sum(my_skip);
   if (lane == 0) {
 #pragma unroll
     for (int j = 0; j < RPT; ++j) sm.group_cnt[j * WARPS + warp] = __popc(ballots[j]);
+    sm.warp_skip[warp] = ws;
   }
-  // counters: warp-reduce then one atomic per warp
-  int ws = warp_sum(my_skip), wi = warp_sum(my_inv);
-  unsigned long long wb = warp_max_u64(my_bad_enc);
-  if (lane == 0) {
-    if (ws) atomicAdd(&a.ws->n_skipped, (unsigned long long)ws);
-    if (wi) atomicAdd(&a.ws->n_invalid, (unsigned long long)wi);
-    if (wb) atomicMax(&a.ws->first_invalid_enc, wb);
+  // first invalid row: rare, one atomic per warp that has one
+  if (__any_sync(0xffffffffu, my_bad_enc != 0ull)) {
+    const unsigned long long wb = warp_max_u64(my_bad_enc);
+    if (lane == 0) atomicMax(&a.ws->first_invalid_enc, wb);
   }
   __syncthreads();
   if (warp == 0) {
-    int c = lane < GROUPS ? sm.group_cnt[lane] : 0;
-    int v = c;
+    constexpr int GPL = (GROUPS + 31) / 32;   // consecutive groups per lane
+    int c[GPL];
+    int mine = 0;
+#pragma unroll
+    for (int q = 0; q < GPL; ++q) {
+      const int gi = lane * GPL + q;
+      c[q] = gi < GROUPS ? sm.group_cnt[gi] : 0;
+      mine += c[q];
+    }
+    int v = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       int t = __shfl_up_sync(0xffffffffu, v, o);
       if (lane >= o) v += t;
     }
-    int total = __shfl_sync(0xffffffffu, v, 31);
-    if (lane < GROUPS) sm.group_off[lane] = v - c;
-    if (lane == 0) sm.block_prefix = lookback(a.ws->status, sm.vb, (unsigned long long)total);
+    const int total = __shfl_sync(0xffffffffu, v, 31);
+    int run = v - mine;
+#pragma unroll
+    for (int q = 0; q < GPL; ++q) {
+      const int gi = lane * GPL + q;
+      if (gi < GROUPS) sm.group_off[gi] = run;
+      run += c[q];
+    }
+    const int skip = warp_sum(lane < WARPS ? sm.warp_skip[lane] : 0);
+    const unsigned long long pre = lookback_warp(
+        a.ws->status, sm.vb, pack_counts((unsigned long long)total, (unsigned long long)skip));
+    if (lane == 0) sm.block_prefix = pre & kCnt31;
   }
   __syncthreads();
   if (a.admitted_idx || a.ring) {
@@ -325,134 +415,387 @@ __device__ void finish_tile(const AdmitArgs& a, AdmitShared<THREADS, RPT>& sm, i
   // its counters; apply the batch's state effects once (controller.py:316-337).
   __threadfence();
   if (tid == 0) {
-    const int nb = gridDim.x;
-    unsigned long long w = ld_relaxed(&a.ws->status[nb - 1]);
-    int64_t n_adm = (int64_t)(w & kValMask);
-    int64_t n_skip = (int64_t)ld_relaxed(&a.ws->n_skipped);
-    int64_t n_inv = (int64_t)ld_relaxed(&a.ws->n_invalid);
-    unsigned long long benc = ld_relaxed(&a.ws->first_invalid_enc);
-    gg_state* st = a.state;
-    const BatchConst& b = sm.bc;
-    const bool any_valid = (sm.nw - n_inv) > 0;
-    if (any_valid) {
-      if (b.samples_seen > 0) ch_observe(st->n_energy, b.ewma);
-      ch_observe(st->n_queue_depth, (double)b.qd);
-      ch_observe(st->n_p95_ms, b.p95);
-    }
-    st->admitted_total += n_adm;
-    st->skipped_total += n_skip;
-    if (a.fifo) {
-      const int64_t room = a.fifo->capacity - sm.depth0;
-      a.fifo->tail += n_adm < room ? n_adm : room;
-      a.fifo->cursor = sm.row0 + sm.nw;
-    }
-    if (a.info) {
-      a.info->n_admitted = n_adm;
-      a.info->n_skipped = n_skip;
-      a.info->n_invalid = n_inv;
-      a.info->first_invalid = benc ? (int64_t)(sm.row0 + sm.nw - (int64_t)benc) : -1;
-      a.info->energy = any_valid ? b.e : 0.0;
-      a.info->congestion = any_valid ? b.c : 0.0;
-      a.info->n_decided = sm.nw;
-      a.info->snap_queue_depth = b.qd;
-      a.info->snap_p95_ms = b.p95;
-      a.info->snap_batch_fill = b.fill;
-    }
-    a.ws->vblock_counter = 0;
-    a.ws->done_counter = 0;
-    a.ws->n_skipped = 0;
-    a.ws->n_invalid = 0;
-    a.ws->first_invalid_enc = 0;
+    const unsigned long long w = ld_relaxed(&a.ws->status[gridDim.x - 1]);
+    finalize_launch(a, sm.bc, sm.row0, sm.nw, sm.depth0, w, ld_relaxed(&a.ws->first_invalid_enc));
   }
   __syncthreads();
   for (int i = tid; i < (int)gridDim.x; i += THREADS) a.ws->status[i] = 0ull;
 }
 
-// K1, small K (K <= 16): RPT rows per thread, rows of a warp contiguous, so a
-// warp's loads of a [32 x K] fp64 slab are fully coalesced.
-template <int KC, int THREADS, int RPT>
-__global__ void __launch_bounds__(THREADS) admit_small_kernel(AdmitArgs a) {
+// ---- K1, small K (K <= 16) -------------------------------------------------
+// Batch-constant part of the single-precision fast filter.  J and tau are
+// evaluated in fp32; the margin covers (a) the utility error du of the fp32
+// logs, (b) the fp32 exp error (1e-4 relative of |tau0 - tau_inf|) and (c) the
+// fp32 rounding of every operand and operation (1e-6 x the operand scale).
+// Rows inside the margin (and NaN) are recomputed exactly.
+struct FastBlock {
+  double t_origin;
+  float alpha, jc, tau_inf, dtau, negk_log2e, margin, inv_log2k;
+  int geq;
+  int adm_code;   // DIRECT / BATCHED: routing depends only on batch constants
+};
+
+constexpr int kNeedExact = 255;
+
+__device__ FastBlock fast_block(const AdmitArgs& a, const BatchConst& b) {
+  const gg_params& p = a.p;
+  FastBlock f;
+  f.t_origin = b.t_origin;
+  const double jc = p.beta * b.e + p.gamma * b.c;
+  f.alpha = (float)p.alpha;
+  f.jc = (float)jc;
+  f.tau_inf = (float)p.tau_inf;
+  f.dtau = (float)(p.tau0 - p.tau_inf);
+  f.negk_log2e = (float)(-p.k * 1.4426950408889634);
+  f.inv_log2k = (float)(0.6931471805599453 / a.ln_k);
+  const double scale = fabs(p.alpha) + fabs(jc) + fabs(p.tau0) + fabs(p.tau_inf) + 1.0;
+  const double du = (p.utility_proxy == GG_UTIL_ENTROPY) ? 1e-5 : 0.0;
+  const double m = fabs(p.alpha) * du + fabs(p.tau0 - p.tau_inf) * 1e-4 + 1e-6 * scale;
+  f.margin = (scale < 1e30) ? (float)m : INFINITY;   // out of fp32 range: always exact
+  f.geq = p.direction == GG_DIR_GEQ;
+  if (p.routing == GG_ROUTE_ALL_BATCHED) f.adm_code = GG_DECISION_BATCHED;
+  else if (p.routing == GG_ROUTE_THRESHOLD_ON_QUEUE)
+    f.adm_code = (b.qd > (int64_t)p.queue_threshold) ? GG_DECISION_BATCHED : GG_DECISION_DIRECT;
+  else f.adm_code = GG_DECISION_DIRECT;
+  return f;
+}
+
+// Fast decision for one row: exact validation (_validate_distribution,
+// controller.py:126-136), fp32 utility, fp32 J - tau, margin test.  Returns a
+// decision code or kNeedExact.  K <= 4 sums the fp32 entropy terms in fp32
+// (|du| <= K (4e-7 + 6e-8) / ln 2 < 1e-5); the generic K <= 16 path in fp64.
+// tau's exp runs as ex2.approx of a pre-scaled argument: relative error
+// <= 2^-22 + 1.8e-7 |k el| (argument rounding), inside the 1e-4 allowance
+// wherever exp(-k el) > 2^-30, and negligible in absolute terms elsewhere.
+__device__ __forceinline__ float lg2_approx(float x) {   // MUFU.LG2, denormals flushed
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {   // MUFU.EX2
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int KC>
+__device__ __forceinline__ int fast_row(const double* x, int k, double now, const FastBlock& f,
+                                        bool entropy) {
+  bool ok = true, first = true;
+  double mx = 0.0, hd = 0.0, tot;
+  float hf = 0.0f;
+  NeumaierSum ns;
+#pragma unroll
+  for (int c = 0; c < (KC > 0 ? KC : 16); ++c) {
+    if (KC == 0 && c >= k) break;
+    const double xc = x[c];
+    ok = ok && (xc >= 0.0) && (xc <= 1.7976931348623157e308);   // finite and >= 0
+    if (KC != 2) ns.add(xc);
+    if (entropy) {   // p log2 p; u = -sum / log2 K (the ln 2 factors cancel)
+      const float pf = (float)xc;
+      const float t = pf > 0.0f ? pf * lg2_approx(pf) : 0.0f;
+      if (KC > 0) hf += t;
+      else hd += (double)t;
+    } else {
+      mx = (first || xc > mx) ? xc : mx;
+      first = false;
+    }
+  }
+  // K = 2: Neumaier's sum of [x0, x1] is t + c with c the exact error of
+  // t = fl(x0 + x1), and fl(t + c) == t — the validation total is one add.
+  if constexpr (KC == 2) tot = f64_add(x[0], x[1]);
+  else tot = ns.result();
+  if (!ok || k < 2 || fabs(f64_sub(tot, 1.0)) > 1e-9) return GG_DECISION_INVALID;
+  float u;
+  if (entropy) u = fminf(fmaxf(-(KC > 0 ? hf : (float)hd) * f.inv_log2k, 0.0f), 1.0f);
+  else u = (float)(1.0 - mx);
+  const float el = (float)fmax(now - f.t_origin, 0.0);
+  const float tau = f.tau_inf + f.dtau * ex2_approx(f.negk_log2e * el);
+  const float d = (f.alpha * u + f.jc) - tau;
+  if (!(fabsf(d) > f.margin)) return kNeedExact;
+  return (f.geq ? d > 0.0f : d < 0.0f) ? f.adm_code : GG_DECISION_SKIP;
+}
+
+// The reference's own evaluation of one row (CPython order, fp64).
+__device__ __forceinline__ int exact_row(const AdmitArgs& a, const BatchConst& b, const double* row,
+                                         int k, double now, bool entropy, double* bd3) {
+  RowAcc acc;   // controller.py:126-148
+  for (int c = 0; c < k; ++c) acc.add(row[c], entropy);
+  double u, jv = 0.0, tau = 0.0;
+  int code;
+  if (acc.finish(k, entropy, a.ln_k, u)) {
+    code = decide_row(a, b, u, now, jv, tau);
+  } else {
+    code = GG_DECISION_INVALID;
+    u = jv = tau = __longlong_as_double(0x7ff8000000000000ll);
+  }
+  if (bd3) {
+    bd3[0] = u;
+    bd3[1] = jv;
+    bd3[2] = tau;
+  }
+  return code;
+}
+
+// RPT rows per thread (row = tile0 + j*256 + tid: a warp's rows are contiguous,
+// so its loads of a [32 x K] fp64 slab coalesce).  K = 2, 4: all RPT rows and
+// arrival times are loaded into registers before anything else.
+// BD: breakdown requested -> every row takes the exact path.
+// SPLIT: large batches — the batch constants come precomputed from
+// admit_prologue_kernel (no per-block prologue, no barrier before the rows),
+// and the kernel only decides + writes per-block counts (and their super-block
+// sums); admit_compact_kernel finishes (no cross-block waiting anywhere).
+constexpr int kSmallThreads = 256;
+
+struct SplitConsts {
+  BatchConst bc;
+  FastBlock fb;
+};
+static_assert(sizeof(SplitConsts) <= sizeof(((AdmitWorkspace*)0)->consts), "workspace consts");
+
+template <int KC, int RPT, bool BD, bool SPLIT>
+__global__ void __launch_bounds__(kSmallThreads) admit_small_kernel(AdmitArgs a) {
+  constexpr int THREADS = kSmallThreads;
   __shared__ AdmitShared<THREADS, RPT> sm;
+  __shared__ FastBlock fb_s;
   const int tid = threadIdx.x;
-  if (tid == 0) block_setup(a, sm);
-  __syncthreads();
-  const BatchConst b = sm.bc;
-  const int64_t tile0 = (int64_t)sm.vb * THREADS * RPT;
-  const int64_t nw = sm.nw, row0 = sm.row0;
+  int64_t row0, nw;
+  admit_window(a, row0, nw);
+  const int64_t tile0 = (int64_t)blockIdx.x * THREADS * RPT;
+  // rows of this thread: j*THREADS < rem  (32-bit compares; pointers stepped)
+  const int64_t rem64 = nw - tile0 - tid;
+  const int rem = rem64 > THREADS * RPT ? THREADS * RPT : (int)rem64;
+  const int64_t g0 = row0 + tile0 + tid;   // trace row of j = 0
+  constexpr bool PRE = KC > 0 && !BD;
+  double px[PRE ? RPT : 1][KC > 0 ? KC : 2], pn[PRE ? RPT : 1];
+  if constexpr (PRE) {
+    const double* rp = a.probs + g0 * a.stride;
+    const double* np = a.now + g0;
+    const int64_t step = (int64_t)THREADS * a.stride;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) {
+      if (j * THREADS < rem) {
+#pragma unroll
+        for (int c = 0; c < KC; c += 2) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(rp + c));
+          px[j][c] = v.x;
+          px[j][c + 1] = v.y;
+        }
+        pn[j] = __ldg(np);
+      }
+      rp += step;
+      np += THREADS;
+    }
+  }
+  const SplitConsts* sc = reinterpret_cast<const SplitConsts*>(a.ws->consts);
+  if constexpr (!SPLIT) {
+    if (tid == 0) {
+      block_setup(a, sm);
+      fb_s = fast_block(a, sm.bc);
+    }
+    __syncthreads();
+  }
   const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
   const int k = KC > 0 ? KC : a.k;
-  uint32_t ballots[RPT];
-  int my_skip = 0, my_inv = 0;
-  unsigned long long my_bad = 0;
+  int code[RPT];
+  bool any_exact = false;
+  if constexpr (!BD) {
+    const FastBlock f = SPLIT ? sc->fb : fb_s;
 #pragma unroll
-  for (int j = 0; j < RPT; ++j) {
-    const int64_t r = tile0 + (int64_t)j * THREADS + tid;
-    const bool in = r < nw;
-    const int64_t g = row0 + r;  // trace row
-    uint8_t code = GG_DECISION_SKIP;
-    if (in) {
-      const double* row = a.probs + g * a.stride;
-      double xv[KC > 0 ? KC : 16];
-      if constexpr (KC == 2) {
-        const double2 v = *reinterpret_cast<const double2*>(row);
-        xv[0] = v.x; xv[1] = v.y;
-      } else if constexpr (KC == 4) {
-        const double2 v0 = *reinterpret_cast<const double2*>(row);
-        const double2 v1 = *reinterpret_cast<const double2*>(row + 2);
-        xv[0] = v0.x; xv[1] = v0.y; xv[2] = v1.x; xv[3] = v1.y;
-      } else {
-        for (int c = 0; c < k; ++c) xv[c] = row[c];
-      }
-      double u, jv = 0.0, tau = 0.0;
-      bool valid;
-      const double now_g = a.now[g];
-      int fast = -1;
-      if (!a.breakdown) {
-        // exact validation (cheap), approximate utility, then the margin test
-        bool ok = true, first = true;
-        NeumaierSum tot;
-        double hf = 0.0, mx = 0.0;
+    for (int j = 0; j < RPT; ++j) {
+      int c = GG_DECISION_SKIP;
+      if (j * THREADS < rem) {
+        if constexpr (KC > 0) {
+          c = fast_row<KC>(px[j], k, pn[j], f, entropy);
+        } else {
+          const int64_t g = g0 + (int64_t)j * THREADS;
+          const double* row = a.probs + g * a.stride;
+          double xv[16];
 #pragma unroll
-        for (int c = 0; c < (KC > 0 ? KC : 16); ++c) {
-          if (KC == 0 && c >= k) break;
-          const double x = xv[c];
-          if (!isfinite(x) || x < 0.0) ok = false;
-          tot.add(x);
-          if (entropy) hf += entropy_term_fast(x);
-          if (first || x > mx) mx = x;
-          first = false;
-        }
-        valid = ok && k >= 2 && !(fabs(f64_sub(tot.result(), 1.0)) > 1e-9);
-        if (valid) {
-          const double u_f = entropy ? clamp01(-hf / a.ln_k) : f64_sub(1.0, mx);
-          fast = decide_fast(a, b, u_f, entropy ? 1e-5 : 0.0, now_g);
-          if (fast >= 0) code = (uint8_t)fast;
+          for (int q = 0; q < 16; ++q) xv[q] = q < k ? row[q] : 0.0;
+          c = fast_row<0>(xv, k, a.now[g], f, entropy);
         }
       }
-      if (a.breakdown || (valid && fast < 0)) {
-        RowAcc acc;   // exact CPython-order evaluation (controller.py:126-148)
-        for (int c = 0; c < k; ++c) acc.add(xv[c], entropy);
-        valid = acc.finish(k, entropy, a.ln_k, u);
-        if (valid) code = decide_row(a, b, u, now_g, jv, tau);
-      }
-      if (valid) {
-        if (code == GG_DECISION_SKIP) ++my_skip;
-      } else {
-        code = GG_DECISION_INVALID;
-        ++my_inv;
-        if (!my_bad) my_bad = (unsigned long long)(nw - r);
-        u = jv = tau = __longlong_as_double(0x7ff8000000000000ll);
-      }
-      a.decision[g] = code;
-      if (a.breakdown) {
-        a.breakdown[3 * g] = u;
-        a.breakdown[3 * g + 1] = jv;
-        a.breakdown[3 * g + 2] = tau;
+      code[j] = c;
+      any_exact |= (c == kNeedExact);
+    }
+  }
+  if (BD || __any_sync(0xffffffffu, any_exact)) {   // rare without a breakdown
+    const BatchConst b = SPLIT ? sc->bc : sm.bc;
+#pragma unroll 1
+    for (int j = 0; j < RPT; ++j) {
+      if (j * THREADS < rem && (BD || code[j] == kNeedExact)) {
+        const int64_t g = g0 + (int64_t)j * THREADS;
+        code[j] = exact_row(a, b, a.probs + g * a.stride, k, a.now[g], entropy,
+                            BD && a.breakdown ? a.breakdown + 3 * g : nullptr);
+      } else if (BD) {
+        code[j] = GG_DECISION_SKIP;
       }
     }
-    ballots[j] = __ballot_sync(0xffffffffu, in && (code == GG_DECISION_DIRECT || code == GG_DECISION_BATCHED));
   }
-  finish_tile<THREADS, RPT>(a, sm, tile0, ballots, my_skip, my_inv, my_bad);
+  uint32_t ballots[RPT];
+  int my_skip = 0;
+  int first_bad = -1;
+  uint8_t* dp = a.decision + g0;
+#pragma unroll
+  for (int j = 0; j < RPT; ++j) {
+    const bool in = j * THREADS < rem;
+    if (in) {
+      dp[j * THREADS] = (uint8_t)code[j];
+      my_skip += code[j] == GG_DECISION_SKIP;
+      if (code[j] == GG_DECISION_INVALID && first_bad < 0) first_bad = j;
+    }
+    ballots[j] = __ballot_sync(0xffffffffu, in && (code[j] == GG_DECISION_DIRECT || code[j] == GG_DECISION_BATCHED));
+  }
+  const unsigned long long my_bad =
+      first_bad < 0 ? 0ull : (unsigned long long)(rem64 - (int64_t)first_bad * THREADS);   // nw - r
+  if constexpr (SPLIT) {
+    constexpr int WARPS = THREADS / 32;
+    const int lane = tid & 31, warp = tid >> 5;
+    int wa = 0;
+#pragma unroll
+    for (int j = 0; j < RPT; ++j) wa += __popc(ballots[j]);
+    const int ws = warp_sum(my_skip);
+    if (lane == 0) {
+      sm.group_cnt[warp] = wa;
+      sm.warp_skip[warp] = ws;
+    }
+    if (__any_sync(0xffffffffu, my_bad != 0ull)) {
+      const unsigned long long wb = warp_max_u64(my_bad);
+      if (lane == 0) atomicMax(&a.ws->first_invalid_enc, wb);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int adm = warp_sum(lane < WARPS ? sm.group_cnt[lane] : 0);
+      const int skp = warp_sum(lane < WARPS ? sm.warp_skip[lane] : 0);
+      if (lane == 0) {
+        const unsigned long long pc = pack_counts((unsigned long long)adm, (unsigned long long)skp);
+        a.split_cnt[blockIdx.x] = pc;
+        atomicAdd(&a.super_cnt[blockIdx.x >> a.super_shift], pc);
+      }
+    }
+  } else {
+    finish_tile<THREADS, RPT>(a, sm, tile0, ballots, my_skip, my_bad);
+  }
+}
+
+// SPLIT step 0 (one thread): the launch's batch constants, once.
+__global__ void admit_prologue_kernel(AdmitArgs a) {
+  if (threadIdx.x != 0) return;
+  SplitConsts* sc = reinterpret_cast<SplitConsts*>(a.ws->consts);
+  const BatchConst b = batch_constants(a.state, a.snap, nullptr);
+  sc->bc = b;
+  sc->fb = fast_block(a, b);
+}
+
+// SPLIT step 2: order-preserving compaction from the decision bytes.  A block
+// owns 8192 rows (= 4 decide tiles); its global offset is the sum of the super-
+// block counts before it plus the decide-block counts inside its super-block
+// (<= 2 sqrt(#blocks) words, no scan launch, no waiting).  Each lane turns 32
+// consecutive decision bytes (two 16-B loads) into a bit mask; admitted row
+// ids are staged in shared memory in order and written out coalesced.  The
+// last block to finish applies the launch's state effects and re-zeroes the
+// split counters.
+constexpr int kCompactRows = 8192;
+constexpr int kDecideRows = kSmallThreads * 8;   // decide tile (kSmallRpt rows per thread)
+
+__global__ void __launch_bounds__(kSmallThreads) admit_compact_kernel(AdmitArgs a, int nb_decide) {
+  constexpr int THREADS = kSmallThreads, WARPS = THREADS / 32;
+  __shared__ int32_t out[kCompactRows];
+  __shared__ int warp_off[WARPS];
+  __shared__ unsigned long long red[WARPS];
+  __shared__ int last, tot_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * kCompactRows;
+  // ---- global offset of this block: decide block i0 = first of its tiles
+  const int i0 = (int)(c0 / kDecideRows);
+  const int sup = i0 >> a.super_shift, sup0 = sup << a.super_shift;
+  unsigned long long part = 0;
+  for (int q = tid; q < sup + (i0 - sup0); q += THREADS)
+    part += q < sup ? a.super_cnt[q] : a.split_cnt[sup0 + (q - sup)];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) red[warp] = part;
+  // ---- masks of admitted rows: lane owns rows r0 .. r0+31
+  const int64_t r0 = c0 + (int64_t)(warp * 32 + lane) * 32;
+  uint32_t mask = 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(a.decision) & 15) == 0) && r0 + 32 <= a.n;
+  if (vec) {
+    const uint4* p4 = reinterpret_cast<const uint4*>(a.decision + r0);
+    const uint4 u0 = p4[0], u1 = p4[1];
+    const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const uint32_t c = (w[q] >> (8 * b)) & 0xFFu;
+        mask |= (uint32_t)(c == GG_DECISION_DIRECT || c == GG_DECISION_BATCHED) << (q * 4 + b);
+      }
+    }
+  } else {
+    for (int i = 0; i < 32; ++i) {
+      if (r0 + i < a.n) {
+        const int c = a.decision[r0 + i];
+        mask |= (uint32_t)(c == GG_DECISION_DIRECT || c == GG_DECISION_BATCHED) << i;
+      }
+    }
+  }
+  const int cnt = __popc(mask);
+  int v = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  if (lane == 31) warp_off[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    const int w = lane < WARPS ? warp_off[lane] : 0;
+    int x = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane < WARPS) warp_off[lane] = x - w;
+  }
+  __syncthreads();
+  unsigned long long base = 0;
+#pragma unroll
+  for (int q = 0; q < WARPS; ++q) base += red[q];
+  int pos = warp_off[warp] + (v - cnt);
+  for (uint32_t m = mask; m; m &= m - 1) out[pos++] = (int32_t)(r0 + __ffs(m) - 1);
+  __syncthreads();
+  if (a.admitted_idx) {
+    // block total = last warp's offset + its inclusive sum (broadcast via smem)
+    if (warp == WARPS - 1 && lane == 31) tot_s = warp_off[warp] + v;
+    __syncthreads();
+    int32_t* dst = a.admitted_idx + (base & kCnt31);
+    for (int i = tid; i < tot_s; i += THREADS) dst[i] = out[i];
+  }
+  // ---- completion: the last block finalizes and re-zeroes the split counters
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(&a.ws->done_counter, 1ull) == (unsigned long long)gridDim.x - 1ull;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int nsup = ((nb_decide - 1) >> a.super_shift) + 1;
+  unsigned long long tot = 0;
+  for (int q = tid; q < nsup; q += THREADS) tot += a.super_cnt[q];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = tot;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long grand = 0;
+    for (int q = 0; q < WARPS; ++q) grand += red[q];
+    const BatchConst b = reinterpret_cast<const SplitConsts*>(a.ws->consts)->bc;
+    finalize_launch(a, b, 0, a.n, 0, grand, a.ws->first_invalid_enc);
+  }
+  for (int q = tid; q < nb_decide; q += THREADS) a.split_cnt[q] = 0ull;
+  for (int q = tid; q < nsup; q += THREADS) a.super_cnt[q] = 0ull;
 }
 
 // K1, large K (ResNet K=1000).  The CPython sums are sequential per row, but
@@ -465,6 +808,7 @@ __global__ void __launch_bounds__(THREADS) admit_small_kernel(AdmitArgs a) {
 // double-buffered through shared memory with named barriers, so the two
 // sequential chains overlap the log computation of the next chunk.
 constexpr int kLargeThreads = 256;
+constexpr int kSmallRpt = 8;   // admit_small_kernel rows per thread (2048 rows per block)
 constexpr int kLargeRows = 32;
 constexpr int kChunk = 32;
 constexpr int kProdThreads = kLargeThreads - 64;
@@ -557,7 +901,7 @@ __global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a)
   const bool in = warp == 0 && r < nw;
   const int64_t g = row0 + r;
   uint8_t code = GG_DECISION_SKIP;
-  int my_skip = 0, my_inv = 0;
+  int my_skip = 0;
   unsigned long long my_bad = 0;
   if (in) {
     double u = tot_s[lane], jv = 0.0, tau = 0.0;
@@ -566,7 +910,6 @@ __global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a)
       if (code == GG_DECISION_SKIP) ++my_skip;
     } else {
       code = GG_DECISION_INVALID;
-      ++my_inv;
       if (!my_bad) my_bad = (unsigned long long)(nw - r);
       u = jv = tau = __longlong_as_double(0x7ff8000000000000ll);
     }
@@ -578,16 +921,24 @@ __global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a)
     }
   }
   uint32_t ballots[1] = {__ballot_sync(0xffffffffu, in && (code == GG_DECISION_DIRECT || code == GG_DECISION_BATCHED))};
-  finish_tile<kLargeThreads, 1>(a, sm, tile0, ballots, my_skip, my_inv, my_bad);
+  finish_tile<kLargeThreads, 1>(a, sm, tile0, ballots, my_skip, my_bad);
 }
 
 // K1, large K, fast filter (no breakdown requested; the serving loop): one warp
-// per row, coalesced loads, fp64 sum of the probabilities and of fp32-log
-// entropy terms, warp reductions — no sequential chain.  A row is recomputed
-// exactly (sequential CPython order, one lane) only when its sum lies within
-// 1e-13 of the 1e-9 validation bound or J lies within the margin of tau.
-__global__ void __launch_bounds__(kLargeThreads) admit_large_fast_kernel(AdmitArgs a) {
-  __shared__ AdmitShared<kLargeThreads, 1> sm;
+// per row (16 warps x 2 rows, 32 rows per block), coalesced loads, fp64 sum of the
+// probabilities and of fp32-log entropy terms, warp reductions — no sequential
+// chain.  For K <= 1024 a row is preloaded into registers (all loads in flight
+// at once: a small serving window is latency-, not bandwidth-bound).  A row is
+// recomputed exactly — in CPython order — only when its sum lies within 1e-13
+// of the 1e-9 validation bound or J lies within the margin of tau; the exact
+// fp64 logs are then computed lane-parallel and only the Neumaier chains run
+// in element order (every lane evaluates them redundantly, via shuffles).
+constexpr int kFastThreads = 512;   // 128 registers: a 32-double row slab per lane
+constexpr int kRegChunks = 32;   // K <= 32 * 32 preloaded
+
+template <bool REG>
+__global__ void __launch_bounds__(kFastThreads) admit_large_fast_kernel(AdmitArgs a) {
+  __shared__ AdmitShared<kFastThreads, 1> sm;
   __shared__ uint8_t codes[kLargeRows];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) block_setup(a, sm);
@@ -596,53 +947,95 @@ __global__ void __launch_bounds__(kLargeThreads) admit_large_fast_kernel(AdmitAr
   const int64_t tile0 = (int64_t)sm.vb * kLargeRows;
   const int64_t nw = sm.nw, row0 = sm.row0;
   const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
-  for (int lr = warp; lr < kLargeRows; lr += kLargeThreads / 32) {
+  const int k = a.k;
+  for (int lr = warp; lr < kLargeRows; lr += kFastThreads / 32) {
     const int64_t r = tile0 + lr;
     if (r >= nw) {
       if (lane == 0) codes[lr] = GG_DECISION_SKIP;
-      continue;
-    }
-    const int64_t g = row0 + r;
-    const double* row = a.probs + g * a.stride;
-    double sum = 0.0, hf = 0.0, mx = -INFINITY;
-    bool ok = true;
-    for (int c = lane; c < a.k; c += 32) {
-      const double x = __ldg(row + c);
-      if (!isfinite(x) || x < 0.0) ok = false;
-      sum += x;
-      if (entropy) hf += entropy_term_fast(x);
-      mx = fmax(mx, x);
-    }
+    } else {
+      const int64_t g = row0 + r;
+      const double* row = a.probs + g * a.stride;
+      double sum = 0.0, hf = 0.0, mx = -INFINITY;
+      bool ok = true;
+      double xr[REG ? kRegChunks : 1];
+      if constexpr (REG) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      hf += __shfl_xor_sync(0xffffffffu, hf, o);
-      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    ok = __all_sync(0xffffffffu, ok);
-    if (lane == 0) {
+        for (int i = 0; i < kRegChunks; ++i) {
+          const int c = i * 32 + lane;
+          xr[i] = c < k ? __ldg(row + c) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < kRegChunks; ++i) {
+          if (i * 32 + lane < k) {
+            const double x = xr[i];
+            if (!isfinite(x) || x < 0.0) ok = false;
+            sum += x;
+            if (entropy) hf += entropy_term_fast(x);
+            mx = fmax(mx, x);
+          }
+        }
+      } else {
+        for (int c = lane; c < k; c += 32) {
+          const double x = __ldg(row + c);
+          if (!isfinite(x) || x < 0.0) ok = false;
+          sum += x;
+          if (entropy) hf += entropy_term_fast(x);
+          mx = fmax(mx, x);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        hf += __shfl_xor_sync(0xffffffffu, hf, o);
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      }
+      ok = __all_sync(0xffffffffu, ok);
       // pairwise-ish fp64 sum of <= K nonnegative terms: |error| < K * 2^-52 * sum
-      const double dev = fabs(sum - 1.0), bound = (double)a.k * 2.3e-16 * (sum + 1.0);
-      int code;
-      bool exact = false, valid = ok && a.k >= 2;
+      const double dev = fabs(sum - 1.0), bound = (double)k * 2.3e-16 * (sum + 1.0);
+      int code = GG_DECISION_INVALID;
+      bool exact = false, valid = ok && k >= 2;
       if (valid && dev > 1e-9 + bound) valid = false;
       else if (valid && dev > 1e-9 - bound) exact = true;   // too close to the bound
       if (valid && !exact) {
         const double u_f = entropy ? clamp01(-hf / a.ln_k) : f64_sub(1.0, mx);
         code = decide_fast(a, b, u_f, entropy ? 1e-5 : 0.0, a.now[g]);
         if (code < 0) exact = true;
-      } else {
-        code = GG_DECISION_INVALID;
       }
-      if (exact) {   // rare: the reference's own sequential evaluation
-        RowAcc acc;
-        for (int c = 0; c < a.k; ++c) acc.add(row[c], entropy);
-        double u, jv, tau;
-        code = acc.finish(a.k, entropy, a.ln_k, u) ? decide_row(a, b, u, a.now[g], jv, tau)
+      if (exact) {   // warp-uniform; rare: the reference's own evaluation order
+        double u = 0.0, jv, tau;
+        if constexpr (REG) {
+          NeumaierSum tot, h;
+          bool okx = true;
+#pragma unroll
+          for (int i = 0; i < kRegChunks; ++i) {
+            if (i * 32 < k) {
+              const double x = xr[i];
+              const double t = (entropy && x > 0.0) ? f64_mul(x, log(x)) : 0.0;
+              const int cnt = min(32, k - i * 32);
+              for (int j = 0; j < cnt; ++j) {   // element i*32 + j, in order
+                const double xj = __shfl_sync(0xffffffffu, x, j);
+                const double tj = __shfl_sync(0xffffffffu, t, j);
+                if (!isfinite(xj) || xj < 0.0) okx = false;
+                tot.add(xj);
+                if (entropy && xj > 0.0) h.add(tj);
+              }
+            }
+          }
+          // RowAcc::finish (controller.py:126-148); max is order-independent
+          const bool v = okx && !(fabs(f64_sub(tot.result(), 1.0)) > 1e-9);
+          if (v) u = entropy ? clamp01(f64_div(-h.result(), a.ln_k)) : f64_sub(1.0, mx);
+          code = v ? decide_row(a, b, u, a.now[g], jv, tau) : GG_DECISION_INVALID;
+        } else {
+          RowAcc acc;
+          for (int c = 0; c < k; ++c) acc.add(row[c], entropy);
+          code = acc.finish(k, entropy, a.ln_k, u) ? decide_row(a, b, u, a.now[g], jv, tau)
                                                    : GG_DECISION_INVALID;
+        }
       }
-      codes[lr] = (uint8_t)code;
-      a.decision[g] = (uint8_t)code;
+      if (lane == 0) {
+        codes[lr] = (uint8_t)code;
+        a.decision[g] = (uint8_t)code;
+      }
     }
   }
   __syncthreads();
@@ -650,10 +1043,10 @@ __global__ void __launch_bounds__(kLargeThreads) admit_large_fast_kernel(AdmitAr
   const bool in = warp == 0 && r < nw;
   const uint8_t code = in ? codes[tid] : (uint8_t)GG_DECISION_SKIP;
   int my_skip = (in && code == GG_DECISION_SKIP) ? 1 : 0;
-  int my_inv = (in && code == GG_DECISION_INVALID) ? 1 : 0;
-  unsigned long long my_bad = my_inv ? (unsigned long long)(nw - r) : 0ull;
+  const unsigned long long my_bad =
+      (in && code == GG_DECISION_INVALID) ? (unsigned long long)(nw - r) : 0ull;
   uint32_t ballots[1] = {__ballot_sync(0xffffffffu, in && (code == GG_DECISION_DIRECT || code == GG_DECISION_BATCHED))};
-  finish_tile<kLargeThreads, 1>(a, sm, tile0, ballots, my_skip, my_inv, my_bad);
+  finish_tile<kFastThreads, 1>(a, sm, tile0, ballots, my_skip, my_bad);
 }
 
 // ---------------------------------------------------------------------------
@@ -1003,15 +1396,31 @@ int gg_set_queue_depth(gg_state* state_dev, int32_t queue_depth, void* stream) {
   return GG_OK;
 }
 
+static int num_sms_cached() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
 static int64_t admit_blocks(int64_t n, int32_t k) {
-  const int64_t rows_per_block = (k <= 16) ? 256 * 4 : kLargeRows;
+  const int64_t rows_per_block = (k <= 16) ? kSmallThreads * kSmallRpt : kLargeRows;
   int64_t nb = (n + rows_per_block - 1) / rows_per_block;
   return nb < 1 ? 1 : nb;
 }
 
+static int64_t lookback_words(int64_t n) {   // worst case over the single-pass kernels
+  const int64_t nb = (n + kLargeRows - 1) / kLargeRows;
+  return nb < 1 ? 1 : nb;
+}
+
 size_t gg_admit_workspace_bytes(int64_t n) {
-  const int64_t nb = (n + kLargeRows - 1) / kLargeRows;  // worst case over kernels
-  return kWsHeader + sizeof(unsigned long long) * (size_t)(nb < 1 ? 1 : nb);
+  // look-back words + split-path counters (decide-block counts + super sums)
+  const int64_t nbs = (n + kDecideRows - 1) / kDecideRows + 1;
+  return kWsHeader + sizeof(unsigned long long) * (size_t)(lookback_words(n) + 2 * nbs);
 }
 
 static int launch_admit(const AdmitArgs& a, void* stream);
@@ -1068,24 +1477,55 @@ int gg_admit(const gg_params* params, gg_state* state_dev, const double* probs_d
   return launch_admit(a, stream);
 }
 
-static int launch_admit(const AdmitArgs& a, void* stream) {
+static int launch_admit(const AdmitArgs& args, void* stream) {
+  AdmitArgs a = args;
   const int64_t n = a.n;
   const int32_t k = a.k;
-  const double* probs_dev = a.probs;
-  const int64_t row_stride = a.stride;
   const int64_t nb = admit_blocks(n, k);
   cudaStream_t s = gg_stream(stream);
-  const bool aligned16 = ((reinterpret_cast<uintptr_t>(probs_dev) & 15) == 0) && (row_stride % 2 == 0);
-  if (k == 2 && aligned16)
-    admit_small_kernel<2, 256, 4><<<(unsigned)nb, 256, 0, s>>>(a);
-  else if (k == 4 && aligned16)
-    admit_small_kernel<4, 256, 4><<<(unsigned)nb, 256, 0, s>>>(a);
-  else if (k <= 16)
-    admit_small_kernel<0, 256, 4><<<(unsigned)nb, 256, 0, s>>>(a);
-  else if (a.breakdown == nullptr && !getenv("GG_ADMIT_EXACT_ONLY"))
-    admit_large_fast_kernel<<<(unsigned)nb, kLargeThreads, 0, s>>>(a);
-  else
+  const bool aligned16 = ((reinterpret_cast<uintptr_t>(a.probs) & 15) == 0) && (a.stride % 2 == 0);
+  const bool bd = a.breakdown != nullptr;
+  if (k <= 16) {
+    // large batches: decide / scan / compact (three launches, no cross-block
+    // waiting); the serving window (FIFO mode, small n): single pass with a
+    // decoupled look-back
+    const bool split = !a.fifo && nb >= 4 * num_sms_cached();
+    const unsigned g = (unsigned)nb;
+    if (split) {   // counters after the look-back words (gg_admit_workspace_bytes)
+      int sh = 2;
+      while ((1ll << (2 * sh)) < nb) ++sh;   // 2^sh >= sqrt(nb)
+      a.super_shift = sh;
+      a.split_cnt = a.ws->status + lookback_words(n);
+      a.super_cnt = a.split_cnt + nb;
+    }
+    if (split) {
+      admit_prologue_kernel<<<1, 32, 0, s>>>(a);
+      GG_LAUNCH_OK();
+    }
+#define GG_SMALL(KC)                                                                        \
+  do {                                                                                      \
+    if (bd && split) admit_small_kernel<KC, kSmallRpt, true, true><<<g, kSmallThreads, 0, s>>>(a);    \
+    else if (bd) admit_small_kernel<KC, kSmallRpt, true, false><<<g, kSmallThreads, 0, s>>>(a);      \
+    else if (split) admit_small_kernel<KC, kSmallRpt, false, true><<<g, kSmallThreads, 0, s>>>(a);   \
+    else admit_small_kernel<KC, kSmallRpt, false, false><<<g, kSmallThreads, 0, s>>>(a);             \
+  } while (0)
+    if (k == 2 && aligned16) GG_SMALL(2);
+    else if (k == 4 && aligned16) GG_SMALL(4);
+    else GG_SMALL(0);
+#undef GG_SMALL
+    if (split) {
+      GG_LAUNCH_OK();
+      admit_compact_kernel<<<(unsigned)((n + kCompactRows - 1) / kCompactRows), kSmallThreads, 0, s>>>(
+          a, (int)nb);
+    }
+  } else if (!bd && !getenv("GG_ADMIT_EXACT_ONLY")) {
+    if (k <= kRegChunks * 32)
+      admit_large_fast_kernel<true><<<(unsigned)nb, kFastThreads, 0, s>>>(a);
+    else
+      admit_large_fast_kernel<false><<<(unsigned)nb, kFastThreads, 0, s>>>(a);
+  } else {
     admit_large_kernel<<<(unsigned)nb, kLargeThreads, 0, s>>>(a);
+  }
   GG_LAUNCH_OK();
   return GG_OK;
 }

@@ -6,11 +6,12 @@
 // of output m reads padded pixel m + r*(W+2) + s — a uniform shift.  So for a
 // tile of 128 consecutive m, the nine A operands are nine shifted views of ONE
 // span of 128 + 2*(W+2) + 2 pixel rows, loaded once per 64-channel block by TMA
-// (instead of nine im2col loads): A traffic drops ~5-8x.  The span is stored
-// as eight 16-byte-wide channel planes (no swizzle), so a shift by one pixel is
-// +16 B of the UMMA descriptor start address (K-major, SWIZZLE_NONE:
-// SBO = 128 B between 8-row core matrices, LBO = plane stride between the two
-// 8-channel halves of a K=16 step).
+// (instead of nine im2col loads): A traffic drops ~5-8x.  The span is ONE TMA
+// box [64 channels x span rows] in the 128B-swizzled K-major layout; a shift
+// by one pixel is +128 B of the UMMA descriptor start address (the hardware
+// applies the swizzle XOR to absolute address bits, so row starts inside a
+// 1024-B atom need no base offset).  A cross-check layout (GG_SPAN_LAYOUT=
+// planes) stores eight 16-byte channel planes, SWIZZLE_NONE, shift = +16 B.
 //
 // Positions with w >= W or h >= H are computed and written as ZEROS: they land
 // exactly on the output's padding (output index = m + (W+2) + 1), so the next
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               umma_bf16(d_tmem,
-                        sh.sw128 ? sdesc_k_sw128(sa + shift * 8 + kk * 32)   // row shift: base offset
+                        sh.sw128 ? sdesc_k_sw128(sa + shift * 8 + kk * 32)   // shift whole 128-B rows
                                  : sdesc_k_none(sa + 2 * kk * sh.plane_bytes + shift, sh.plane_bytes),
                         sdesc_k_sw128(sb + kk * 32), idesc, (cb | tap | kk) != 0);
             if (!sh.bres) {
@@ -342,7 +343,9 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
   sh.bres = (bn == Cout) && (2 * kSpanAStage + nkb * bn * 128 + 1536 <= 227 * 1024);
   CUtensorMap mx, mw;
   const char* lay = getenv("GG_SPAN_LAYOUT");
-  sh.sw128 = !(lay && lay[0] == 'p');   // default: 128B-swizzled rows; "planes" = 16-B planes
+  // default: one 128B-swizzled [64ch x span] box; GG_SPAN_LAYOUT=planes selects
+  // eight 16-B channel planes (kept as a cross-check layout for the tests)
+  sh.sw128 = !(lay && strcmp(lay, "planes") == 0);
   int rc = sh.sw128 ? make_map_2d(&mx, x, (int64_t)N * sh.Hp * sh.Wp, C, C, sh.span_rows)
                     : make_map_planes(&mx, x, (int64_t)N * sh.Hp * sh.Wp, C, sh.span_rows);
   if (!rc) rc = make_map_2d(&mw, w, Cout, (int64_t)C * 9, (int64_t)C * 9, bn);

@@ -125,7 +125,9 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t smem_addr) {
   d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
   d |= (uint64_t)(1024 >> 4) << 32;       // SBO
   d |= (uint64_t)1 << 46;                 // descriptor version (Blackwell)
-  d |= (uint64_t)((smem_addr >> 7) & 7) << 49;  // base offset for non-1024-aligned starts
+  // base offset (bits 49-51) stays 0: the swizzle XOR is applied to the
+  // absolute smem address bits [7:9], so a start shifted by whole 128-B rows
+  // inside an atom addresses correctly (verified by tests/test_conv_span_gpu.py)
   d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
   return d;
 }

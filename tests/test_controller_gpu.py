@@ -235,7 +235,8 @@ def test_replay_batch_api(gg, torch, name):
 
 
 @pytest.mark.parametrize("n,k", [(0, 2), (1, 2), (1023, 2), (1025, 4), (4_194_304, 2),
-                                 (100_003, 4), (3000, 7), (2048, 1000), (129, 37)])
+                                 (100_003, 4), (3000, 7), (2048, 1000), (129, 37),
+                                 (1_500_007, 4), (1_300_001, 5)])   # the last two: split path
 @pytest.mark.parametrize("breakdown", [True, False])
 def test_admit_vs_c_oracle_large(gg, torch, n, k, breakdown):
     """Order-preserving compaction and counters at scale vs the C oracle."""
@@ -279,12 +280,11 @@ def test_admit_vs_c_oracle_large(gg, torch, n, k, breakdown):
     assert st == G.state_dict_of_abi(orc.state)
 
 
-@pytest.mark.parametrize("k", [2, 4, 1000])
-def test_fast_filter_near_threshold(gg, torch, k):
+@pytest.mark.parametrize("n,k", [(4096, 2), (4096, 4), (4096, 1000), (1_250_000, 2)])
+def test_fast_filter_near_threshold(gg, torch, n, k):
     """Rows engineered to sit within the fast-path margin of tau take the exact
     path; decisions must still equal the oracle's bit-for-bit."""
     rng = np.random.default_rng(k)
-    n = 4096
     base = rng.integers(1, 60, size=(n, k))
     rows = G.rows_from_base(base)
     p = dict(alpha=1.0, beta=0.0, gamma=0.0, tau0=0.5, tau_inf=0.5, k=1.0, ewma_lambda=0.9,
@@ -295,7 +295,8 @@ def test_fast_filter_near_threshold(gg, torch, k):
     p.update(tau0=tau, tau_inf=tau)
     orc = c_oracle.COracle(G.abi_params(p))
     dec_o, bd_o, idx_o, info_o = orc.admit(rows, np.zeros(n))
-    assert (np.abs(bd_o[:, 1] - tau) < 1e-5).sum() > 0 or k == 1000
+    # tau is the median utility, so some rows sit inside the fast filter's margin
+    assert np.min(np.abs(bd_o[:, 0] - tau)) < 1e-3
     ctl = gg.ControllerConfig(tau0=tau, tau_inf=tau, k=1.0).build(gg.EnergyLedger())
     out = ctl.decide_batch(torch.from_numpy(rows).cuda(), torch.zeros(n, dtype=torch.float64,
                                                                       device="cuda"),

@@ -1,0 +1,89 @@
+"""Run ONE hot kernel a few times at bench scale, for `ncu --set full` captures.
+
+    python tools/kernel_probe.py k1|span1|span2|span3|span4|stem [reps]
+
+Prints CUDA-event device times (probe numbers, not bench values).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+
+def _time(fn, reps):
+    fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def k1(reps):
+    import paper_2601_04250_b200 as gg
+    n = 1 << 26
+    c = torch.rand(n, device="cuda", dtype=torch.float64) * 0.5 + 0.5
+    scores = torch.stack([c, 1.0 - c], dim=1).contiguous()
+    now = torch.linspace(0.0, 10.0, n, device="cuda", dtype=torch.float64)
+    ctl = gg.ControllerConfig(alpha=1.0, beta=-0.1, gamma=-0.3, tau0=0.9, tau_inf=0.4, k=0.5,
+                              routing=gg.RoutePolicy.THRESHOLD_ON_QUEUE).build(gg.EnergyLedger())
+    snap = gg.CongestionSnapshot(3, 7.5, 0.25)
+    out = ctl.decide_batch(scores, now, snap, breakdown=False)
+    ms = _time(lambda: ctl.decide_batch(scores, now, snap, breakdown=False, out=out), reps)
+    print(f"k1 n={n}: {ms:.4f} ms  {n * 25 / ms / 1e6:.1f} GB/s")
+
+
+SPANS = {"span1": (64, 56, 64, 64), "span2": (64, 28, 128, 128), "span3": (64, 14, 256, 256),
+         "span4": (64, 7, 512, 512)}
+
+
+def span(which, reps):
+    from paper_2601_04250_b200 import _native as nat
+    lib = nat.load()
+    n, h, c, cout = SPANS[which]
+    xp = torch.zeros((n, h + 2, h + 2, c), dtype=torch.bfloat16, device="cuda")
+    xp[:, 1:-1, 1:-1] = torch.randn((n, h, h, c), device="cuda").to(torch.bfloat16)
+    wk = (torch.randn((cout, 9 * c), device="cuda") / (9 * c) ** 0.5).to(torch.bfloat16)
+    b = torch.zeros(cout, device="cuda")
+    y = torch.zeros((n, h + 2, h + 2, cout), dtype=torch.bfloat16, device="cuda")
+
+    def run():
+        nat.check("gg_conv3x3_padded", lib.gg_conv3x3_padded(
+            nat.ptr(xp), n, h, h, c, nat.ptr(wk), cout, nat.ptr(b), None, 1, nat.ptr(y), None,
+            nat.stream_ptr()))
+    ms = _time(run, reps)
+    fl = 2.0 * n * h * h * cout * 9 * c
+    print(f"{which} {n}x{h}x{h}x{c}->{cout}: {ms * 1e3:.1f} us  {fl / ms / 1e9:.1f} TFLOP/s")
+
+
+def stem(reps):
+    from paper_2601_04250_b200.resnet18 import ResNet18B200, random_model
+    net = ResNet18B200(random_model(0), max_batch=64)
+    x = torch.randn((64, 3, 224, 224), device="cuda")
+    net.forward(x)
+    print("stem probe: ran one forward (capture the conv_bf16_tcgen05<64,8,2> launch)")
+
+
+def main():
+    which = sys.argv[1] if len(sys.argv) > 1 else "k1"
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    if which == "k1":
+        k1(reps)
+    elif which in SPANS:
+        span(which, reps)
+    elif which == "stem":
+        stem(reps)
+    else:
+        raise SystemExit(f"unknown probe {which}")
+
+
+if __name__ == "__main__":
+    main()
