@@ -110,14 +110,23 @@ int gg_nchw_to_nhwc(const float* x, int32_t N, int32_t C, int32_t H, int32_t W, 
                     void* y, void* stream);
 /* fp32 NCHW RGB batch -> bf16 space-to-depth(2) NHWC, 16 channels
  * (y[n, i, j, (dy*2+dx)*3 + c] = x[n, c, 2i+dy, 2j+dx]; channels 12..15 = 0).
- * ResNet-18's 7x7/2 stem conv equals a 4x4/1 conv (pad 2 / 1) over it. */
-int gg_nchw_to_s2d16(const float* x, int32_t N, int32_t H, int32_t W, void* y, void* stream);
+ * ResNet-18's 7x7/2 stem conv equals a 4x4/1 conv (pad 2 / 1) over it.
+ * padded = 1: write the interior of a zero-bordered [N, H/2+3, W/2+3, 16]
+ * buffer at (+2, +2) — the input layout of gg_stem_s2d_span. */
+int gg_nchw_to_s2d16(const float* x, int32_t N, int32_t H, int32_t W, int32_t padded, void* y,
+                     void* stream);
+/* ResNet-18 stem (conv1 + bn1 + relu) as a span convolution: 4x4 / 1 over the
+ * padded space-to-depth input x [N, Hs+3, Ws+3, 16] (Hs = H/2), w BN-folded
+ * [64, 4, 4, 16] (gg_nchw_to_s2d16 cell order), y dense [N, Hs, Ws, 64]. */
+int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws, const void* w, int32_t Cout,
+                     const float* bias, int32_t relu, void* y, const int32_t* count_dev,
+                     void* stream);
 /* Served-batch stem input: image i of the batch = uint8 HWC image
  * pool[batch_ids[i] % pool_size], normalized ((x/255 - mean[c]) / std[c]) into
  * the space-to-depth(2) 16-channel layout of gg_nchw_to_s2d16. */
 int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_ids,
                    const int32_t* count_dev, int32_t B, int32_t H, int32_t W,
-                   const float* mean3, const float* std3, void* y, void* stream);
+                   const float* mean3, const float* std3, int32_t padded, void* y, void* stream);
 /* 3x3 / stride 2 / pad 1 max pool (NHWC, C % 8 == 0); out_pad = 1 writes the
  * interior of a zero-bordered [N, Ho+2, Wo+2, C] buffer. */
 int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, void* y,

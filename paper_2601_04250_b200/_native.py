@@ -50,8 +50,9 @@ SIGNATURES: dict[str, tuple] = {
     "gg_conv3x3_padded": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _I32, _P, _P,
                                     _P]),
     "gg_nchw_to_nhwc": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
-    "gg_nchw_to_s2d16": (C.c_int, [_P, _I32, _I32, _I32, _P, _P]),
-    "gg_stem_gather": (C.c_int, [_P, _I64, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
+    "gg_nchw_to_s2d16": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P]),
+    "gg_stem_s2d_span": (C.c_int, [_P, _I32, _I32, _I32, _P, _I32, _P, _I32, _P, _P, _P]),
+    "gg_stem_gather": (C.c_int, [_P, _I64, _P, _P, _I32, _I32, _I32, _P, _P, _I32, _P, _P]),
     "gg_maxpool3x3s2": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P]),
     "gg_avgpool": (C.c_int, [_P, _I32, _I32, _I32, _P, _I32, _P, _P]),
     # serving loop (include/greengate_b200.h)

@@ -1,27 +1,41 @@
-// gg_conv_span.cu — 3x3 / stride-1 convolution on zero-padded NHWC activations
-// with ONE operand load per tile for all nine taps.
+// gg_conv_span.cu — stride-1 convolutions on zero-padded NHWC activations with
+// ONE operand load per tile for all taps ("span" convolution).
 //
-// Activations live padded: [N, H+2, W+2, C] with zero borders.  Index output
-// positions in the padded input space, m = (n*(H+2) + h)*(W+2) + w; tap (r, s)
-// of output m reads padded pixel m + r*(W+2) + s — a uniform shift.  So for a
-// tile of 128 consecutive m, the nine A operands are nine shifted views of ONE
-// span of 128 + 2*(W+2) + 2 pixel rows, loaded once per 64-channel block by TMA
-// (instead of nine im2col loads): A traffic drops ~5-8x.  The span is ONE TMA
-// box [64 channels x span rows] in the 128B-swizzled K-major layout; a shift
-// by one pixel is +128 B of the UMMA descriptor start address (the hardware
-// applies the swizzle XOR to absolute address bits, so row starts inside a
-// 1024-B atom need no base offset).  A cross-check layout (GG_SPAN_LAYOUT=
-// planes) stores eight 16-byte channel planes, SWIZZLE_NONE, shift = +16 B.
+// Activations live padded: [N, Hp, Wp, C] with zero borders.  Index output
+// positions in the padded input space, m = (n*Hp + h)*Wp + w; tap (r, s) of
+// output m reads padded pixel m + r*Wp + s — a uniform shift.  So for a tile
+// of 128 consecutive m, the RT x RT A operands are shifted views of ONE span of
+// 128 + (RT-1)*(Wp+1) pixel rows, loaded once per channel block by TMA
+// (instead of RT*RT im2col loads).  The span sits in shared memory in the
+// K-major swizzled layout (CH = 64 channels: 128-B rows, SWIZZLE_128B; CH = 16:
+// 32-B rows, SWIZZLE_32B); a shift by one pixel is +row bytes on the UMMA
+// descriptor start address — the hardware applies the swizzle XOR to absolute
+// address bits, so row starts inside a swizzle atom need no base offset
+// (verified by tests/test_conv_span_gpu.py).
 //
-// Positions with w >= W or h >= H are computed and written as ZEROS: they land
-// exactly on the output's padding (output index = m + (W+2) + 1), so the next
-// layer reads correct zero borders.  Waste: (H+2)(W+2)/(HW) - 1 of the MMAs.
+// Two instantiations serve ResNet-18:
+//   * 3x3 / 1, pad 1, C % 64 == 0 (layers 1-4): output written padded in the
+//     same geometry at m + Wp + 1; positions with h >= H or w >= W are written
+//     as ZEROS — they land exactly on the output's padding, so the next layer
+//     reads correct zero borders.
+//   * the stem: 7x7 / 2 on the image = 4x4 / 1 over its space-to-depth(2)
+//     (16 channels), input padded 2 before / 1 after; output dense (positions
+//     outside the real 112 x 112 grid are skipped).
 //
-//   warp 0  TMA producer: A span planes (2-stage ring) + B k-blocks (ring, or
-//           the whole BN x K slab once per CTA when it fits: resident B)
-//   warp 1  TMEM allocator + tcgen05.mma issuer
-//   warps 2..5  epilogue: tcgen05.ld, folded-BN bias, residual, ReLU, bf16
+// Roles (persistent CTAs, one per SM):
+//   warp 0      TMA producer: A spans (ring of as many stages as fit) and B
+//               (the whole BN x K weight slab once per CTA when it fits, else
+//               a ring of one tap slab per stage)
+//   warp 1      TMEM allocator + tcgen05.mma issuer.  The issue loop is lean —
+//               descriptors are base + offsets, all taps unrolled — because at
+//               N = 64 the tensor pipe takes a new MMA every 32-48 cycles
+//               (tools/mma_bench.cu: a naive loop issues one per ~90 cycles)
+//   warps 2..9  epilogue: tcgen05.ld, folded-BN bias, residual, ReLU, bf16;
+//               two column halves x four TMEM lane quarters
 #include <cudaTypedefs.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "gg_common.cuh"
 #include "gg_kernels.h"
@@ -30,54 +44,57 @@
 namespace gg {
 using namespace tc;
 
+constexpr int kSpanMaxStages = 8;
+constexpr int kSpanEpiWarps = 8;
+constexpr int kSpanThreads = 64 + 32 * kSpanEpiWarps;
+constexpr int kSpanSmemMax = 227 * 1024;
+
 struct SpanShape {
   int N, H, W, C, Cout;
-  int Wp, Hp;          // W + 2, H + 2
-  int Mtot;            // N_eff * Hp * Wp (set per launch from the count)
-  int span_rows;       // 128 + 2*Wp + 2
-  int plane_bytes;     // span_rows * 16 rounded up to 128
-  int bres;            // B resident for the whole CTA
-  int sw128;           // A span as 128B-swizzled 64-channel rows (else 16-B channel planes)
+  int Hp, Wp;          // padded input extents
+  int Ho, Wo;          // real output extents (dense mode: output row pitch)
+  int span_rows;       // 128 + (RT-1)*(Wp+1)
+  int box_rows, boxes; // the span as `boxes` TMA boxes of box_rows (<= 256) rows
+  int a_stage_bytes;   // boxes * box_rows * row bytes, rounded up to 1 KB
+  int a_stages;
+  int b_stages;        // ring depth (ignored when bres)
+  int bres;            // whole weight slab resident
 };
 
 struct SpanEpi {
-  __nv_bfloat16* y;               // padded [N, Hp, Wp, Cout]
+  __nv_bfloat16* y;
   const float* bias;
-  const __nv_bfloat16* residual;  // padded, same geometry, or null
+  const __nv_bfloat16* residual;  // padded, same geometry as y (padded mode), or null
   int relu;
   const int32_t* count;
 };
 
-constexpr int kSpanThreads = 64 + 128;
-constexpr int kSpanAStage = 8 * 256 * 16;   // max: 8 planes x 256 rows x 16 B
-
-__device__ __forceinline__ uint64_t sdesc_k_none(uint32_t smem_addr, uint32_t lbo_bytes) {
-  uint64_t d = 0;
-  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;  // LBO: next 8-channel plane (K)
-  d |= (uint64_t)(128 >> 4) << 32;                   // SBO: next 8-row core matrix (M)
-  d |= (uint64_t)1 << 46;                            // version
-  return d;                                          // layout type 0 = SWIZZLE_NONE
+__device__ __forceinline__ uint64_t sdesc_sw(uint32_t addr, int row_bytes) {
+  return row_bytes == 128 ? sdesc_k_sw128(addr) : sdesc_k_sw32(addr);
 }
 
-template <int BN, int BSTAGES>
+template <int BN, int CH, int RT, bool DENSE>
 __global__ void __launch_bounds__(kSpanThreads, 1)
     conv_span_tcgen05(const __grid_constant__ CUtensorMap map_x,
                       const __grid_constant__ CUtensorMap map_w, SpanShape sh, SpanEpi ep) {
+  constexpr int RB = CH * 2;                 // bytes per pixel row (one swizzle row)
+  constexpr int KSTEPS = CH / 16;            // MMAs per tap
+  constexpr int TAPS = RT * RT;
+  constexpr int B_BYTES = BN * RB;           // one tap slab of B
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int cblocks = sh.C / 64;
-  const int nkb = cblocks * 9;
-  constexpr int B_BYTES = BN * 128;
-  uint8_t* a_base = smem;                                   // 2 x kSpanAStage
-  uint8_t* b_base = smem + 2 * kSpanAStage;                 // ring or resident slab
-  const int b_slots = sh.bres ? nkb : BSTAGES;
+  const int cblocks = sh.C / CH;
+  const int nkb = cblocks * TAPS;
+  const int AST = sh.a_stages, BST = sh.b_stages;
+  uint8_t* a_base = smem;
+  uint8_t* b_base = smem + AST * sh.a_stage_bytes;
+  const int b_slots = sh.bres ? nkb : BST;
   uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + b_slots * B_BYTES);
   uint64_t* a_full = bars;
-  uint64_t* a_empty = bars + 2;
-  uint64_t* b_full = bars + 4;
-  uint64_t* b_empty = b_full + BSTAGES;
-  uint64_t* acc_full = b_empty + BSTAGES;
+  uint64_t* a_empty = a_full + kSpanMaxStages;
+  uint64_t* b_full = a_empty + kSpanMaxStages;
+  uint64_t* b_empty = b_full + kSpanMaxStages;
+  uint64_t* acc_full = b_empty + kSpanMaxStages;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* bres_full = acc_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
@@ -90,15 +107,15 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   const int num_tiles = tiles_m * tiles_n;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSpanMaxStages; ++i) {
       mbar_init(&a_full[i], 1);
       mbar_init(&a_empty[i], 1);
-      mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], 4);
-    }
-    for (int i = 0; i < BSTAGES; ++i) {
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kSpanEpiWarps);
     }
     mbar_init(bres_full, 1);
     fence_mbar_init();
@@ -115,29 +132,25 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     if (lane == 0) {
       if (sh.bres && num_tiles > (int)blockIdx.x) {
         mbar_expect_tx(bres_full, nkb * B_BYTES);
-        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(b_base + kb * B_BYTES, &map_w, bres_full, kb * 64, 0);
+        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(b_base + kb * B_BYTES, &map_w, bres_full, kb * CH, 0);
       }
       int ait = 0, bit = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int tm = tile % tiles_m, tn = tile / tiles_m;
         const int m0 = tm * 128;
         for (int cb = 0; cb < cblocks; ++cb, ++ait) {
-          const int as = ait & 1;
-          mbar_wait(&a_empty[as], ((ait >> 1) & 1) ^ 1);
-          uint8_t* sa = a_base + as * kSpanAStage;
-          mbar_expect_tx(&a_full[as], 8 * sh.span_rows * 16);
-          if (sh.sw128) {   // one box [64 channels, span_rows], 128B-swizzled rows
-            tma_load_2d(sa, &map_x, &a_full[as], cb * 64, m0);
-          } else {
-            for (int p = 0; p < 8; ++p)   // box = [8 channels, span_rows] per plane
-              tma_load_2d(sa + p * sh.plane_bytes, &map_x, &a_full[as], cb * 64 + p * 8, m0);
-          }
+          const int as = ait % AST;
+          mbar_wait(&a_empty[as], ((ait / AST) & 1) ^ 1);
+          uint8_t* sa = a_base + as * sh.a_stage_bytes;
+          mbar_expect_tx(&a_full[as], sh.boxes * sh.box_rows * RB);
+          for (int bx = 0; bx < sh.boxes; ++bx)   // boxes of <= 256 rows (TMA limit)
+            tma_load_2d(sa + bx * sh.box_rows * RB, &map_x, &a_full[as], cb * CH, m0 + bx * sh.box_rows);
           if (!sh.bres) {
-            for (int tap = 0; tap < 9; ++tap, ++bit) {
-              const int bs = bit % BSTAGES;
-              mbar_wait(&b_empty[bs], ((bit / BSTAGES) & 1) ^ 1);
+            for (int tap = 0; tap < TAPS; ++tap, ++bit) {
+              const int bs = bit % BST;
+              mbar_wait(&b_empty[bs], ((bit / BST) & 1) ^ 1);
               mbar_expect_tx(&b_full[bs], B_BYTES);
-              tma_load_2d(b_base + bs * B_BYTES, &map_w, &b_full[bs], (cb * 9 + tap) * 64, tn * BN);
+              tma_load_2d(b_base + bs * B_BYTES, &map_w, &b_full[bs], (cb * TAPS + tap) * CH, tn * BN);
             }
           }
         }
@@ -146,7 +159,12 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+      uint64_t tap_off[TAPS];   // row shift of tap (r, s) in 16-B descriptor units
+#pragma unroll
+      for (int tap = 0; tap < TAPS; ++tap)
+        tap_off[tap] = (uint64_t)(((tap / RT) * sh.Wp + tap % RT) * (RB / 16));
       if (sh.bres && num_tiles > (int)blockIdx.x) mbar_wait(bres_full, 0);
+      const uint64_t bres_desc = sdesc_sw(smem_u32(b_base), RB);
       int ait = 0, bit = 0, t = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
         const int acc = t & 1;
@@ -154,32 +172,34 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int cb = 0; cb < cblocks; ++cb, ++ait) {
-          const int as = ait & 1;
-          mbar_wait(&a_full[as], (ait >> 1) & 1);
+          const int as = ait % AST;
+          mbar_wait(&a_full[as], (ait / AST) & 1);
           tc_fence_after();
-          const uint32_t sa = smem_u32(a_base + as * kSpanAStage);
-          for (int tap = 0; tap < 9; ++tap) {
-            const int r = tap / 3, s = tap - 3 * (tap / 3);
-            const uint32_t shift = (uint32_t)(r * sh.Wp + s) * 16u;
-            uint32_t sb;
-            int bs = 0;
-            if (sh.bres) {
-              sb = smem_u32(b_base + (cb * 9 + tap) * B_BYTES);
-            } else {
-              bs = bit % BSTAGES;
-              mbar_wait(&b_full[bs], (bit / BSTAGES) & 1);
-              tc_fence_after();
-              sb = smem_u32(b_base + bs * B_BYTES);
-            }
+          const uint64_t ad = sdesc_sw(smem_u32(a_base + as * sh.a_stage_bytes), RB);
+          if (sh.bres) {
+            const uint64_t bd = bres_desc + (uint64_t)(cb * TAPS * (B_BYTES >> 4));
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              umma_bf16(d_tmem,
-                        sh.sw128 ? sdesc_k_sw128(sa + shift * 8 + kk * 32)   // shift whole 128-B rows
-                                 : sdesc_k_none(sa + 2 * kk * sh.plane_bytes + shift, sh.plane_bytes),
-                        sdesc_k_sw128(sb + kk * 32), idesc, (cb | tap | kk) != 0);
-            if (!sh.bres) {
+            for (int tap = 0; tap < TAPS; ++tap) {
+              const uint64_t ao = ad + tap_off[tap];
+              const uint64_t bo = bd + (uint64_t)(tap * (B_BYTES >> 4));
+#pragma unroll
+              for (int kk = 0; kk < KSTEPS; ++kk)
+                umma_bf16(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
+                          (cb | tap | kk) != 0);
+            }
+          } else {
+#pragma unroll
+            for (int tap = 0; tap < TAPS; ++tap, ++bit) {
+              const int bs = bit % BST;
+              mbar_wait(&b_full[bs], (bit / BST) & 1);
+              tc_fence_after();
+              const uint64_t ao = ad + tap_off[tap];
+              const uint64_t bo = bres_desc + (uint64_t)(bs * (B_BYTES >> 4));
+#pragma unroll
+              for (int kk = 0; kk < KSTEPS; ++kk)
+                umma_bf16(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
+                          (cb | tap | kk) != 0);
               umma_commit(&b_empty[bs]);
-              ++bit;
             }
           }
           umma_commit(&a_empty[as]);
@@ -188,26 +208,45 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       }
     }
   } else {
+    // epilogue: warp w handles TMEM lane quarter (w % 4) and column half (w - 2) / 4
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    constexpr int HALF = BN / 2;
     int t = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
       const int acc = t & 1;
+      const int m = tm * 128 + quarter * 32 + lane;
+      const int nimg = m / img;
+      const int within = m - nimg * img;
+      const int h = within / sh.Wp, w = within - (within / sh.Wp) * sh.Wp;
+      const bool real = m < Mtot && h < sh.Ho && w < sh.Wo;
+      int64_t oidx;
+      bool store;
+      if constexpr (DENSE) {
+        oidx = ((int64_t)nimg * sh.Ho + h) * sh.Wo + w;
+        store = real;
+      } else {
+        oidx = (int64_t)m + sh.Wp + 1;   // padded output position
+        store = m < Mtot && oidx < (int64_t)n_eff * img;
+      }
       mbar_wait(&acc_full[acc], (t >> 1) & 1);
       tc_fence_after();
-      const int m = tm * 128 + quarter * 32 + lane;
-      const int within = m % img;
-      const int h = within / sh.Wp, w = within - (within / sh.Wp) * sh.Wp;
-      const bool real = m < Mtot && h < sh.H && w < sh.W;
-      const int64_t oidx = (int64_t)m + sh.Wp + 1;   // padded output position
-      const bool store = m < Mtot && oidx < (int64_t)n_eff * img;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = half * HALF; c < (half + 1) * HALF; c += 32) {
+        const int col0 = tn * BN + c;
+        // residual loads first: their latency overlaps the TMEM read
+        uint4 res[4];
+        const bool use_res = !DENSE && ep.residual != nullptr && store && real;
+        if (use_res) {
+          const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + oidx * sh.Cout + col0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) res[q] = __ldg(rp + q);
+        }
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
         tmem_ld_wait();
         if (!store) continue;
-        const int col0 = tn * BN + c;
         float v[32];
         if (real) {
 #pragma unroll
@@ -218,12 +257,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
             v[i + 2] = __uint_as_float(r[i + 2]) + b.z;
             v[i + 3] = __uint_as_float(r[i + 3]) + b.w;
           }
-          if (ep.residual) {
-            const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + oidx * sh.Cout + col0);
+          if (use_res) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const uint4 u = __ldg(rp + q);
-              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&res[q]);
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 f = __bfloat1622float2(h2[e]);
@@ -263,8 +300,9 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   }
 }
 
-// 2-D map over a padded activation viewed as [pixels, C]: box [8 channels, rows], no swizzle.
-static int make_map_planes(CUtensorMap* map, const void* x, int64_t pixels, int C, int rows) {
+// 2-D map over a [rows, cols] bf16 matrix, box [ch, box_rows], swizzle by row bytes.
+static int make_map_span(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int ch,
+                         int box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     cudaDriverEntryPointQueryResult q;
@@ -274,33 +312,66 @@ static int make_map_planes(CUtensorMap* map, const void* x, int64_t pixels, int 
       return GG_ERR_CUDA;
     enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  cuuint64_t dims[2] = {(cuuint64_t)C, (cuuint64_t)pixels};
-  cuuint64_t strides[1] = {(cuuint64_t)C * 2};
-  cuuint32_t box[2] = {8, (cuuint32_t)rows};
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)ch, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   ch == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? GG_OK : GG_ERR_INVALID_ARGUMENT;
 }
 
-template <int BN, int BSTAGES>
+static int span_smem_bytes(const SpanShape& sh, int bn, int rb, int taps) {
+  const int nkb = sh.C / (rb / 2) * taps;
+  return sh.a_stages * sh.a_stage_bytes + (sh.bres ? nkb : sh.b_stages) * bn * rb + 1024 + 1024;
+}
+
+template <int BN, int CH, int RT, bool DENSE>
 static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanShape& sh,
                        const SpanEpi& ep, cudaStream_t s) {
-  auto kern = conv_span_tcgen05<BN, BSTAGES>;
+  auto kern = conv_span_tcgen05<BN, CH, RT, DENSE>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpanSmemMax) != cudaSuccess)
       return GG_ERR_CUDA;
     attr = true;
   }
-  const int nkb = sh.C / 64 * 9;
-  const int smem = 2 * kSpanAStage + (sh.bres ? nkb : BSTAGES) * BN * 128 + 512 + 1024;
+  const int smem = span_smem_bytes(sh, BN, CH * 2, RT * RT);
   const int tiles = ((sh.N * sh.Hp * sh.Wp + 127) / 128) * (sh.Cout / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   kern<<<grid, kSpanThreads, smem, s>>>(mx, mw, sh, ep);
   GG_LAUNCH_OK();
   return GG_OK;
+}
+
+// Fill the stage plan: B resident (only with a single N tile) if it fits beside
+// >= 3 A stages, else a B ring; A stages = as many as fit (<= kSpanMaxStages).
+static bool plan_span(SpanShape& sh, int bn, int rb, int taps) {
+  // several boxes: multiples of 8 rows so each box starts on a swizzle atom
+  sh.boxes = (sh.span_rows + 255) / 256;
+  sh.box_rows = sh.boxes == 1 ? sh.span_rows : ((sh.span_rows + sh.boxes - 1) / sh.boxes + 7) / 8 * 8;
+  sh.a_stage_bytes = (sh.boxes * sh.box_rows * rb + 1023) / 1024 * 1024;
+  const int nkb = sh.C / (rb / 2) * taps;
+  const int avail = kSpanSmemMax - 2048;
+  const int b_all = nkb * bn * rb;
+  if (bn == sh.Cout && b_all + 3 * sh.a_stage_bytes <= avail) {   // one N tile: slab fixed
+    sh.bres = 1;
+    sh.b_stages = 1;
+    sh.a_stages = (avail - b_all) / sh.a_stage_bytes;
+  } else {
+    sh.bres = 0;
+    sh.b_stages = 4;
+    sh.a_stages = (avail - sh.b_stages * bn * rb) / sh.a_stage_bytes;
+    if (sh.a_stages > 4) {   // spend the rest on B depth
+      const int bmax = (avail - 4 * sh.a_stage_bytes) / (bn * rb);
+      sh.b_stages = bmax < kSpanMaxStages ? bmax : kSpanMaxStages;
+      sh.a_stages = (avail - sh.b_stages * bn * rb) / sh.a_stage_bytes;
+    }
+  }
+  if (sh.a_stages > kSpanMaxStages) sh.a_stages = kSpanMaxStages;
+  return sh.a_stages >= 2 && sh.b_stages >= 1;
 }
 
 }  // namespace gg
@@ -315,47 +386,65 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
   if (C % 64 || Cout % 64) return GG_ERR_UNSUPPORTED;
   SpanShape sh;
   sh.N = N; sh.H = H; sh.W = W; sh.C = C; sh.Cout = Cout;
-  sh.Wp = W + 2; sh.Hp = H + 2;
-  sh.Mtot = N * sh.Hp * sh.Wp;
+  sh.Hp = H + 2; sh.Wp = W + 2;
+  sh.Ho = H; sh.Wo = W;
   sh.span_rows = 128 + 2 * sh.Wp + 2;
-  if (sh.span_rows > 256) return GG_ERR_UNSUPPORTED;  // one A stage holds <= 256 rows per plane
-  sh.plane_bytes = (sh.span_rows * 16 + 127) / 128 * 128;
-  // N tile: as in gg_conv2d, by operand traffic vs tensor time (B re-read per M tile)
-  const int64_t tiles_m = (sh.Mtot + 127) / 128;
+  if (sh.span_rows > 1024) return GG_ERR_UNSUPPORTED;
+  const int64_t Mtot = (int64_t)N * sh.Hp * sh.Wp;
+  // N tile by modelled time: tensor time per wave vs L2 operand traffic
+  const int64_t tiles_m = (Mtot + 127) / 128;
   const int64_t nkb = C / 64 * 9;
   int bn = 64;
   double best = 1e30;
   for (int cand : {64, 128, 256}) {
     if (cand > Cout || Cout % cand) continue;
+    SpanShape t = sh;
+    if (!plan_span(t, cand, 128, 9)) continue;
     const int64_t tiles = tiles_m * (Cout / cand);
     const int64_t waves = (tiles + num_sms() - 1) / num_sms();
-    const bool res = (cand == Cout) && (2 * kSpanAStage + nkb * cand * 128 + 1536 <= 227 * 1024);
-    const double t_mma = (double)waves * nkb * 2 * cand / 1.9e9;
-    const double bbytes = res ? (double)(tiles < num_sms() ? tiles : num_sms()) * nkb * cand * 128
-                              : (double)tiles * nkb * cand * 128;
-    const double t_l2 = ((double)tiles * (C / 64) * 8 * sh.span_rows * 16 + bbytes) / 8.0e12;
-    const double t = t_mma > t_l2 ? t_mma : t_l2;
-    if (t < best * 0.97) {
-      best = t;
+    const double cyc_mma = (cand == 64 ? 48.0 : cand / 2.0) * 4;   // per tap (tools/mma_bench.cu)
+    const double t_mma = (double)waves * nkb * cyc_mma / 1.9e9;
+    const double bbytes = t.bres ? (double)(tiles < num_sms() ? tiles : num_sms()) * nkb * cand * 128
+                                 : (double)tiles * nkb * cand * 128;
+    const double t_l2 = ((double)tiles * (C / 64) * sh.span_rows * 128 + bbytes) / 8.0e12;
+    const double tt = t_mma > t_l2 ? t_mma : t_l2;
+    if (tt < best * 0.97) {
+      best = tt;
       bn = cand;
     }
   }
-  sh.bres = (bn == Cout) && (2 * kSpanAStage + nkb * bn * 128 + 1536 <= 227 * 1024);
+  if (!plan_span(sh, bn, 128, 9)) return GG_ERR_UNSUPPORTED;
   CUtensorMap mx, mw;
-  const char* lay = getenv("GG_SPAN_LAYOUT");
-  // default: one 128B-swizzled [64ch x span] box; GG_SPAN_LAYOUT=planes selects
-  // eight 16-B channel planes (kept as a cross-check layout for the tests)
-  sh.sw128 = !(lay && strcmp(lay, "planes") == 0);
-  int rc = sh.sw128 ? make_map_2d(&mx, x, (int64_t)N * sh.Hp * sh.Wp, C, C, sh.span_rows)
-                    : make_map_planes(&mx, x, (int64_t)N * sh.Hp * sh.Wp, C, sh.span_rows);
-  if (!rc) rc = make_map_2d(&mw, w, Cout, (int64_t)C * 9, (int64_t)C * 9, bn);
+  int rc = make_map_span(&mx, x, Mtot, C, 64, sh.box_rows);
+  if (!rc) rc = make_map_span(&mw, w, Cout, (int64_t)C * 9, 64, bn);
   if (rc) return rc;
   SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
              reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev};
   cudaStream_t s = gg_stream(stream);
   switch (bn) {
-    case 256: return launch_span<256, 3>(mx, mw, sh, ep, s);
-    case 128: return launch_span<128, 5>(mx, mw, sh, ep, s);
-    default: return launch_span<64, 8>(mx, mw, sh, ep, s);
+    case 256: return launch_span<256, 64, 3, false>(mx, mw, sh, ep, s);
+    case 128: return launch_span<128, 64, 3, false>(mx, mw, sh, ep, s);
+    default: return launch_span<64, 64, 3, false>(mx, mw, sh, ep, s);
   }
+}
+
+extern "C" int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws, const void* w,
+                                int32_t Cout, const float* bias, int32_t relu, void* y,
+                                const int32_t* count_dev, void* stream) {
+  if (!x || !w || !y || !bias || N <= 0 || Hs <= 0 || Ws <= 0) return GG_ERR_INVALID_ARGUMENT;
+  if (Cout != 64) return GG_ERR_UNSUPPORTED;
+  SpanShape sh;
+  sh.N = N; sh.H = Hs; sh.W = Ws; sh.C = 16; sh.Cout = Cout;
+  sh.Hp = Hs + 3; sh.Wp = Ws + 3;   // space-to-depth input padded 2 before, 1 after
+  sh.Ho = Hs; sh.Wo = Ws;
+  sh.span_rows = 128 + 3 * sh.Wp + 3;
+  if (sh.span_rows > 1024) return GG_ERR_UNSUPPORTED;
+  if (!plan_span(sh, 64, 32, 16)) return GG_ERR_UNSUPPORTED;
+  const int64_t Mtot = (int64_t)N * sh.Hp * sh.Wp;
+  CUtensorMap mx, mw;
+  int rc = make_map_span(&mx, x, Mtot, 16, 16, sh.box_rows);
+  if (!rc) rc = make_map_span(&mw, w, Cout, 256, 16, 64);
+  if (rc) return rc;
+  SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, relu, count_dev};
+  return launch_span<64, 16, 4, true>(mx, mw, sh, ep, gg_stream(stream));
 }

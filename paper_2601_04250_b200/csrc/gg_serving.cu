@@ -128,10 +128,18 @@ __global__ void __launch_bounds__(256) epilogue_served_kernel(const float* logit
 // channels: y[n, y, x, (dy*2 + dx)*3 + c] = norm(img[2y+dy, 2x+dx, c]), channels
 // 12..15 zero.  The ResNet stem (7x7/2 conv) then runs as a 4x4/1 conv over it.
 // One thread per output (s2d) pixel: 4 x 3 bytes in, 32 bytes out.
+// Destination cell of s2d pixel (yy, xx): dense [N, Ho, Wo, 16], or the
+// interior of the zero-bordered [N, Ho+3, Wo+3, 16] buffer (2 before, 1 after)
+// that gg_stem_s2d_span reads.
+__device__ __forceinline__ int64_t s2d_index(int n, int yy, int xx, int Ho, int Wo, int padded) {
+  if (!padded) return ((int64_t)n * Ho + yy) * Wo + xx;
+  return ((int64_t)n * (Ho + 3) + yy + 2) * (Wo + 3) + xx + 2;
+}
+
 __global__ void stem_gather_kernel(const uint8_t* __restrict__ pool, int64_t pool_size,
                                    const int32_t* ids, const int32_t* count, int B, int H, int W,
                                    float m0, float m1, float m2, float s0, float s1, float s2,
-                                   __nv_bfloat16* __restrict__ y) {
+                                   int padded, __nv_bfloat16* __restrict__ y) {
   const int n_valid = count ? min(B, __ldg(count)) : B;
   const int Ho = H / 2, Wo = W / 2;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -141,6 +149,7 @@ __global__ void stem_gather_kernel(const uint8_t* __restrict__ pool, int64_t poo
   const int yy = rem / Wo, xx = rem - yy * Wo;
   const int64_t img = ids ? (int64_t)__ldg(ids + n) % pool_size : n;
   const float mean[3] = {m0, m1, m2}, sd[3] = {s0, s1, s2};
+  const int64_t q = s2d_index(n, yy, xx, Ho, Wo, padded);
   __align__(16) __nv_bfloat16 v[16];
 #pragma unroll
   for (int dy = 0; dy < 2; ++dy) {
@@ -153,13 +162,13 @@ __global__ void stem_gather_kernel(const uint8_t* __restrict__ pool, int64_t poo
   }
 #pragma unroll
   for (int e = 12; e < 16; ++e) v[e] = __float2bfloat16_rn(0.0f);
-  uint4* dst = reinterpret_cast<uint4*>(y + p * 16);
+  uint4* dst = reinterpret_cast<uint4*>(y + q * 16);
   dst[0] = reinterpret_cast<uint4*>(v)[0];
   dst[1] = reinterpret_cast<uint4*>(v)[1];
 }
 
 // fp32 NCHW (already normalized) -> the same space-to-depth(2) 16-channel layout.
-__global__ void nchw_to_s2d16_kernel(const float* __restrict__ x, int N, int H, int W,
+__global__ void nchw_to_s2d16_kernel(const float* __restrict__ x, int N, int H, int W, int padded,
                                      __nv_bfloat16* __restrict__ y) {
   const int Ho = H / 2, Wo = W / 2;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -167,6 +176,7 @@ __global__ void nchw_to_s2d16_kernel(const float* __restrict__ x, int N, int H, 
   const int n = (int)(p / ((int64_t)Ho * Wo));
   const int rem = (int)(p - (int64_t)n * Ho * Wo);
   const int yy = rem / Wo, xx = rem - yy * Wo;
+  const int64_t q = s2d_index(n, yy, xx, Ho, Wo, padded);
   __align__(16) __nv_bfloat16 v[16];
 #pragma unroll
   for (int dy = 0; dy < 2; ++dy)
@@ -178,7 +188,7 @@ __global__ void nchw_to_s2d16_kernel(const float* __restrict__ x, int N, int H, 
             __float2bfloat16_rn(__ldg(x + (((int64_t)n * 3 + c) * H + 2 * yy + dy) * W + 2 * xx + dx));
 #pragma unroll
   for (int e = 12; e < 16; ++e) v[e] = __float2bfloat16_rn(0.0f);
-  uint4* dst = reinterpret_cast<uint4*>(y + p * 16);
+  uint4* dst = reinterpret_cast<uint4*>(y + q * 16);
   dst[0] = reinterpret_cast<uint4*>(v)[0];
   dst[1] = reinterpret_cast<uint4*>(v)[1];
 }
@@ -239,22 +249,23 @@ int gg_epilogue_served(const float* logits_dev, const int32_t* count_dev, int32_
 
 int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_ids,
                    const int32_t* count_dev, int32_t B, int32_t H, int32_t W, const float* mean3,
-                   const float* std3, void* y, void* stream) {
+                   const float* std3, int32_t padded, void* y, void* stream) {
   if (!pool || pool_size < 1 || !mean3 || !std3 || !y || B < 1 || H % 2 || W % 2)
     return GG_ERR_INVALID_ARGUMENT;
   const int64_t pixels = (int64_t)B * (H / 2) * (W / 2);
   stem_gather_kernel<<<(unsigned)((pixels + 255) / 256), 256, 0, gg_stream(stream)>>>(
       pool, pool_size, batch_ids, count_dev, B, H, W, mean3[0], mean3[1], mean3[2], std3[0],
-      std3[1], std3[2], reinterpret_cast<__nv_bfloat16*>(y));
+      std3[1], std3[2], padded, reinterpret_cast<__nv_bfloat16*>(y));
   GG_LAUNCH_OK();
   return GG_OK;
 }
 
-int gg_nchw_to_s2d16(const float* x, int32_t N, int32_t H, int32_t W, void* y, void* stream) {
+int gg_nchw_to_s2d16(const float* x, int32_t N, int32_t H, int32_t W, int32_t padded, void* y,
+                     void* stream) {
   if (!x || !y || N < 1 || H % 2 || W % 2) return GG_ERR_INVALID_ARGUMENT;
   const int64_t pixels = (int64_t)N * (H / 2) * (W / 2);
   nchw_to_s2d16_kernel<<<(unsigned)((pixels + 255) / 256), 256, 0, gg_stream(stream)>>>(
-      x, N, H, W, reinterpret_cast<__nv_bfloat16*>(y));
+      x, N, H, W, padded, reinterpret_cast<__nv_bfloat16*>(y));
   GG_LAUNCH_OK();
   return GG_OK;
 }

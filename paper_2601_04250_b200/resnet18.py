@@ -110,6 +110,20 @@ class _StemConv(_Conv):
         self.stride, self.pad, self.pad_hi, self.out_pad = 1, 2, 1, 0
         self.algo_macs_per_pixel = 7 * 7 * 3 * cout
 
+    def __call__(self, lib, x, n, h, w, y, st, residual=None, relu=True, count=None):
+        """x: zero-bordered space-to-depth input [n, h+3, w+3, 16] (gg_nchw_to_s2d16 /
+        gg_stem_gather with padded=1); y: dense [n, h, w, 64]."""
+        assert residual is None
+        _native.check("gg_stem_s2d_span", lib.gg_stem_s2d_span(
+            C.c_void_p(x), n, h, w, _native.ptr(self.w), self.cout, _native.ptr(self.b), int(relu),
+            C.c_void_p(y), _native.ptr(count), st))
+        return h, w
+
+    def im2col(self, lib, x, n, h, w, y, st, relu=True, count=None):
+        """Cross-check path: the same conv through gg_conv2d's 16-channel im2col
+        mode on the dense [n, h, w, 16] space-to-depth input."""
+        return _Conv.__call__(self, lib, x, n, h, w, y, st, relu=relu, count=count)
+
 
 class _SpanConv:
     """3x3 / 1 conv on padded activations (gg_conv3x3_padded); weights in
@@ -175,7 +189,8 @@ class ResNet18B200:
         self.b_fc = bfc.to(dev).contiguous()
         B, H = max_batch, image
         z = dict(dtype=torch.bfloat16, device=dev)
-        self.x16 = torch.empty(B * (H // 2) * (H // 2) * 16, **z)   # space-to-depth stem input
+        # zero-bordered space-to-depth stem input [B, H/2+3, H/2+3, 16] (interior rewritten)
+        self.x16 = torch.zeros(B * (H // 2 + 3) * (H // 2 + 3) * 16, **z)
         self.stem_out = torch.empty(B * (H // 2) * (H // 2) * 64, **z)
         self.sizes = [H // 4, H // 8, H // 16, H // 32]             # 56, 28, 14, 7
         chans = [64, 128, 256, 512]
@@ -204,7 +219,7 @@ class ResNet18B200:
         H = self.image
         st = _native.stream_ptr(stream)
         _native.check("gg_nchw_to_s2d16", self.lib.gg_nchw_to_s2d16(
-            _native.ptr(images), B, H, H, _native.ptr(self.x16), st))
+            _native.ptr(images), B, H, H, 1, _native.ptr(self.x16), st))
         return self.forward_s2d(B, stream=stream)
 
     def forward_s2d(self, B: int, stream=None, count=None):

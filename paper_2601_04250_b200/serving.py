@@ -112,7 +112,7 @@ class GatedServer:
                 _native.ptr(pool), int(pool.shape[0]), _native.ptr(self.batch_ids),
                 _native.ptr(self.count), B, H, int(pool.shape[2]),
                 self.mean.numpy().ctypes.data_as(C.c_void_p),
-                self.std.numpy().ctypes.data_as(C.c_void_p), _native.ptr(self.net.x16), st))
+                self.std.numpy().ctypes.data_as(C.c_void_p), 1, _native.ptr(self.net.x16), st))
             logits = self.net.forward_s2d(B, stream=self._cur_stream, count=self.count)
         else:
             ids, mask = self.payloads

@@ -14,14 +14,13 @@ def pack_span_weights(w):
             .reshape(cout, 9 * c).contiguous())
 
 
-@pytest.mark.parametrize("layout", ["sw128", "planes"])
 @pytest.mark.parametrize("n,h,c,cout,res", [(2, 56, 64, 64, True), (2, 28, 128, 128, False),
                                             (3, 14, 256, 256, True), (2, 7, 512, 512, True),
-                                            (1, 7, 64, 128, False)])
-def test_span_conv_vs_torch(n, h, c, cout, res, layout, monkeypatch):
+                                            (1, 7, 64, 128, False), (64, 56, 64, 64, True),
+                                            (64, 28, 128, 128, True), (64, 7, 512, 512, True)])
+def test_span_conv_vs_torch(n, h, c, cout, res):
     import torch
     from paper_2601_04250_b200 import _native as nat
-    monkeypatch.setenv("GG_SPAN_LAYOUT", layout)
     lib = nat.load()
     g = torch.Generator(device="cuda").manual_seed(n * h + c)
     x = torch.randn((n, c, h, h), device="cuda", generator=g).to(torch.bfloat16)

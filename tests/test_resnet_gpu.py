@@ -67,16 +67,25 @@ def test_space_to_depth_stem_vs_torch(env):
         bn.bias.copy_(torch.randn(64, generator=g) * 0.1)
     stem = _StemConv(conv, bn, "cuda")
     x = torch.randn((3, 3, 224, 224), generator=g).cuda()
-    x16 = torch.empty((3, 112, 112, 16), dtype=torch.bfloat16, device="cuda")
-    nat.check("gg_nchw_to_s2d16", lib.gg_nchw_to_s2d16(nat.ptr(x), 3, 224, 224, nat.ptr(x16),
-                                                       nat.stream_ptr()))
-    y = torch.empty((3, 112, 112, 64), dtype=torch.bfloat16, device="cuda")
-    stem(lib, x16.data_ptr(), 3, 112, 112, y.data_ptr(), nat.stream_ptr(), relu=True)
     with torch.no_grad():
         ref = torch.relu(bn.cuda()(conv.cuda()(x.to(torch.bfloat16).float())))
+    # span path: zero-bordered s2d input
+    x16p = torch.zeros((3, 115, 115, 16), dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_nchw_to_s2d16", lib.gg_nchw_to_s2d16(nat.ptr(x), 3, 224, 224, 1, nat.ptr(x16p),
+                                                       nat.stream_ptr()))
+    y = torch.empty((3, 112, 112, 64), dtype=torch.bfloat16, device="cuda")
+    stem(lib, x16p.data_ptr(), 3, 112, 112, y.data_ptr(), nat.stream_ptr(), relu=True)
     got = y.float().permute(0, 3, 1, 2)
     err = (got - ref).abs().max().item()
     assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+    # im2col cross-check path: dense s2d input
+    x16 = torch.empty((3, 112, 112, 16), dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_nchw_to_s2d16", lib.gg_nchw_to_s2d16(nat.ptr(x), 3, 224, 224, 0, nat.ptr(x16),
+                                                       nat.stream_ptr()))
+    y2 = torch.empty_like(y)
+    stem.im2col(lib, x16.data_ptr(), 3, 112, 112, y2.data_ptr(), nat.stream_ptr(), relu=True)
+    err2 = (y2.float().permute(0, 3, 1, 2) - ref).abs().max().item()
+    assert err2 <= 2e-2 * max(1.0, ref.abs().max().item()), err2
 
 
 def test_pools(env):
