@@ -262,7 +262,8 @@ int gg_outcome_slots(const gg_params* params, gg_state* state_dev, const double*
 /* K3 for a served batch: logits [B, ld] fp32 (first *count_dev rows valid) ->
  * predicted[batch_ids[i]] (first max), confidence[batch_ids[i]] (fp64 max p),
  * optionally fp64 probabilities [B, k] and batch-local copies
- * batch_predicted[i] / batch_confidence[i] (for a compact device->host read). */
+ * batch_predicted[i] / batch_confidence[i] (for a compact device->host read).
+ * k <= 1024 (GG_ERR_UNSUPPORTED otherwise). */
 int gg_epilogue_served(const float* logits_dev, const int32_t* count_dev, int32_t B, int32_t k,
                        int64_t ld, const int32_t* batch_ids_dev, int32_t* predicted_dev,
                        double* confidence_dev, double* probs_dev, int32_t* batch_predicted_dev,

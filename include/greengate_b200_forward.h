@@ -132,7 +132,7 @@ int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_
 int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, void* y,
                     int32_t out_pad, const int32_t* count_dev, void* stream);
 /* Global average pool NHWC [N, HW, C] -> [N, C], dividing by denom (0 = HW;
- * a zero-bordered input passes its interior pixel count). */
+ * a zero-bordered input passes its interior pixel count); C % 64 == 0. */
 int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y, int32_t denom,
                const int32_t* count_dev, void* stream);
 

@@ -933,118 +933,139 @@ __global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a)
 // of the 1e-9 validation bound or J lies within the margin of tau; the exact
 // fp64 logs are then computed lane-parallel and only the Neumaier chains run
 // in element order (every lane evaluates them redundantly, via shuffles).
-constexpr int kFastThreads = 512;   // 128 registers: a 32-double row slab per lane
-constexpr int kRegChunks = 32;   // K <= 32 * 32 preloaded
+// Exact (CPython-order) evaluation of one large-K row by a whole warp: the fp64
+// logs are computed lane-parallel, 32 elements at a time, and the Neumaier
+// chains consume them in element order via shuffles (every lane evaluates the
+// chains redundantly).  Compact loop, kept out of line: it is the cold path.
+__device__ __noinline__ int exact_row_warp(const AdmitArgs& a, const BatchConst& b,
+                                           const double* row, int k, double now, bool entropy,
+                                           double mx) {
+  const int lane = threadIdx.x & 31;
+  NeumaierSum tot, h;
+  bool okx = true;
+#pragma unroll 1
+  for (int c0 = 0; c0 < k; c0 += 32) {
+    const int c = c0 + lane;
+    const double x = c < k ? row[c] : 0.0;
+    const double t = (entropy && x > 0.0) ? f64_mul(x, log(x)) : 0.0;
+    const int cnt = min(32, k - c0);
+#pragma unroll 1
+    for (int j = 0; j < cnt; ++j) {   // element c0 + j, in order
+      const double xj = __shfl_sync(0xffffffffu, x, j);
+      const double tj = __shfl_sync(0xffffffffu, t, j);
+      if (!isfinite(xj) || xj < 0.0) okx = false;
+      tot.add(xj);
+      if (entropy && xj > 0.0) h.add(tj);
+    }
+  }
+  // RowAcc::finish (controller.py:126-148); max is order-independent
+  const bool v = okx && k >= 2 && !(fabs(f64_sub(tot.result(), 1.0)) > 1e-9);
+  if (!v) return GG_DECISION_INVALID;
+  const double u = entropy ? clamp01(f64_div(-h.result(), a.ln_k)) : f64_sub(1.0, mx);
+  double jv, tau;
+  return decide_row(a, b, u, now, jv, tau);
+}
+
+constexpr int kFastRows = 8;                 // rows per block: one warp per row
+constexpr int kFastThreads = 32 * kFastRows;
+constexpr int kRegChunks = 32;               // K <= 32 * 32: the row is loaded in one go
+
+// Finite and >= 0 (including -0.0), from the bits: one 64-bit compare.
+__device__ __forceinline__ bool finite_nonneg(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return u < 0x7FF0000000000000ull || u == 0x8000000000000000ull;
+}
 
 template <bool REG>
 __global__ void __launch_bounds__(kFastThreads) admit_large_fast_kernel(AdmitArgs a) {
   __shared__ AdmitShared<kFastThreads, 1> sm;
-  __shared__ uint8_t codes[kLargeRows];
+  __shared__ FastBlock fb_s;
+  __shared__ uint8_t codes[kFastRows];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) block_setup(a, sm);
-  __syncthreads();
-  const BatchConst b = sm.bc;
-  const int64_t tile0 = (int64_t)sm.vb * kLargeRows;
-  const int64_t nw = sm.nw, row0 = sm.row0;
-  const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
+  int64_t row0, nw;
+  admit_window(a, row0, nw);
+  const int64_t tile0 = (int64_t)blockIdx.x * kFastRows;
+  const int64_t r = tile0 + warp;                // this warp's row
+  const bool have = r < nw;
   const int k = a.k;
-  for (int lr = warp; lr < kLargeRows; lr += kFastThreads / 32) {
-    const int64_t r = tile0 + lr;
-    if (r >= nw) {
-      if (lane == 0) codes[lr] = GG_DECISION_SKIP;
-    } else {
-      const int64_t g = row0 + r;
-      const double* row = a.probs + g * a.stride;
-      double sum = 0.0, hf = 0.0, mx = -INFINITY;
-      bool ok = true;
-      double xr[REG ? kRegChunks : 1];
-      if constexpr (REG) {
+  const double* row = a.probs + (row0 + (have ? r : 0)) * a.stride;
+  double xr[REG ? kRegChunks : 1];
+  if constexpr (REG) {   // all loads in flight before the prologue
 #pragma unroll
-        for (int i = 0; i < kRegChunks; ++i) {
-          const int c = i * 32 + lane;
-          xr[i] = c < k ? __ldg(row + c) : 0.0;
-        }
-#pragma unroll
-        for (int i = 0; i < kRegChunks; ++i) {
-          if (i * 32 + lane < k) {
-            const double x = xr[i];
-            if (!isfinite(x) || x < 0.0) ok = false;
-            sum += x;
-            if (entropy) hf += entropy_term_fast(x);
-            mx = fmax(mx, x);
-          }
-        }
+    for (int i = 0; i < kRegChunks; ++i) {
+      const int c = i * 32 + lane;
+      xr[i] = (have && c < k) ? __ldg(row + c) : 0.0;
+    }
+  }
+  if (tid == 0) {
+    block_setup(a, sm);
+    fb_s = fast_block(a, sm.bc);
+  }
+  __syncthreads();
+  const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
+  if (have) {
+    const int64_t g = row0 + r;
+    double sum = 0.0, mx = -INFINITY;
+    float hf = 0.0f;   // per-lane fp32 partial of sum p log2 p (<= 32 terms)
+    bool ok = true;
+    auto take = [&](double x) {
+      ok &= finite_nonneg(x);
+      sum += x;
+      if (entropy) {
+        const float pf = (float)x;
+        hf += pf > 0.0f ? pf * lg2_approx(pf) : 0.0f;
       } else {
-        for (int c = lane; c < k; c += 32) {
-          const double x = __ldg(row + c);
-          if (!isfinite(x) || x < 0.0) ok = false;
-          sum += x;
-          if (entropy) hf += entropy_term_fast(x);
-          mx = fmax(mx, x);
-        }
+        mx = fmax(mx, x);
       }
+    };
+    if constexpr (REG) {
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        hf += __shfl_xor_sync(0xffffffffu, hf, o);
-        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      }
-      ok = __all_sync(0xffffffffu, ok);
-      // pairwise-ish fp64 sum of <= K nonnegative terms: |error| < K * 2^-52 * sum
-      const double dev = fabs(sum - 1.0), bound = (double)k * 2.3e-16 * (sum + 1.0);
-      int code = GG_DECISION_INVALID;
-      bool exact = false, valid = ok && k >= 2;
-      if (valid && dev > 1e-9 + bound) valid = false;
-      else if (valid && dev > 1e-9 - bound) exact = true;   // too close to the bound
-      if (valid && !exact) {
-        const double u_f = entropy ? clamp01(-hf / a.ln_k) : f64_sub(1.0, mx);
-        code = decide_fast(a, b, u_f, entropy ? 1e-5 : 0.0, a.now[g]);
-        if (code < 0) exact = true;
-      }
-      if (exact) {   // warp-uniform; rare: the reference's own evaluation order
-        double u = 0.0, jv, tau;
-        if constexpr (REG) {
-          NeumaierSum tot, h;
-          bool okx = true;
+      for (int i = 0; i < kRegChunks; ++i)
+        if (i * 32 + lane < k) take(xr[i]);
+    } else {
+      for (int c = lane; c < k; c += 32) take(__ldg(row + c));
+    }
+    double hd = (double)hf;
 #pragma unroll
-          for (int i = 0; i < kRegChunks; ++i) {
-            if (i * 32 < k) {
-              const double x = xr[i];
-              const double t = (entropy && x > 0.0) ? f64_mul(x, log(x)) : 0.0;
-              const int cnt = min(32, k - i * 32);
-              for (int j = 0; j < cnt; ++j) {   // element i*32 + j, in order
-                const double xj = __shfl_sync(0xffffffffu, x, j);
-                const double tj = __shfl_sync(0xffffffffu, t, j);
-                if (!isfinite(xj) || xj < 0.0) okx = false;
-                tot.add(xj);
-                if (entropy && xj > 0.0) h.add(tj);
-              }
-            }
-          }
-          // RowAcc::finish (controller.py:126-148); max is order-independent
-          const bool v = okx && !(fabs(f64_sub(tot.result(), 1.0)) > 1e-9);
-          if (v) u = entropy ? clamp01(f64_div(-h.result(), a.ln_k)) : f64_sub(1.0, mx);
-          code = v ? decide_row(a, b, u, a.now[g], jv, tau) : GG_DECISION_INVALID;
-        } else {
-          RowAcc acc;
-          for (int c = 0; c < k; ++c) acc.add(row[c], entropy);
-          code = acc.finish(k, entropy, a.ln_k, u) ? decide_row(a, b, u, a.now[g], jv, tau)
-                                                   : GG_DECISION_INVALID;
-        }
-      }
-      if (lane == 0) {
-        codes[lr] = (uint8_t)code;
-        a.decision[g] = (uint8_t)code;
-      }
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      hd += __shfl_xor_sync(0xffffffffu, hd, o);
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    // fp64 sum of <= K nonnegative terms: |error| < K * 2^-52 * sum
+    const double dev = fabs(sum - 1.0), bound = (double)k * 2.3e-16 * (sum + 1.0);
+    int code = GG_DECISION_INVALID;
+    bool exact = false, valid = ok && k >= 2;
+    if (valid && dev > 1e-9 + bound) valid = false;
+    else if (valid && dev > 1e-9 - bound) exact = true;   // too close to the bound
+    if (valid && !exact) {
+      // fp32 decision as in fast_row; the lane partials add |du| <= 32 * 2^-24 * H2 / log2 K
+      // + the lg2.approx error, inside the 1e-5 allowance
+      const FastBlock f = fb_s;
+      const float u = entropy ? fminf(fmaxf(-(float)hd * f.inv_log2k, 0.0f), 1.0f)
+                              : (float)(1.0 - mx);
+      const float el = (float)fmax(a.now[g] - f.t_origin, 0.0);
+      const float tau = f.tau_inf + f.dtau * ex2_approx(f.negk_log2e * el);
+      const float d = (f.alpha * u + f.jc) - tau;
+      if (!(fabsf(d) > f.margin)) exact = true;
+      else code = (f.geq ? d > 0.0f : d < 0.0f) ? f.adm_code : GG_DECISION_SKIP;
+    }
+    if (exact)   // warp-uniform; rare: the reference's own evaluation order
+      code = exact_row_warp(a, sm.bc, row, k, a.now[g], entropy, mx);
+    if (lane == 0) {
+      codes[warp] = (uint8_t)code;
+      a.decision[g] = (uint8_t)code;
     }
   }
   __syncthreads();
-  const int64_t r = tile0 + tid;           // rows live on warp 0's lanes for the compaction
-  const bool in = warp == 0 && r < nw;
-  const uint8_t code = in ? codes[tid] : (uint8_t)GG_DECISION_SKIP;
-  int my_skip = (in && code == GG_DECISION_SKIP) ? 1 : 0;
+  // compaction: the block's rows on warp 0's lanes 0..kFastRows-1
+  const int64_t rr = tile0 + tid;
+  const bool in = warp == 0 && lane < kFastRows && rr < nw;
+  const uint8_t code = in ? codes[lane] : (uint8_t)GG_DECISION_SKIP;
+  const int my_skip = (in && code == GG_DECISION_SKIP) ? 1 : 0;
   const unsigned long long my_bad =
-      (in && code == GG_DECISION_INVALID) ? (unsigned long long)(nw - r) : 0ull;
+      (in && code == GG_DECISION_INVALID) ? (unsigned long long)(nw - rr) : 0ull;
   uint32_t ballots[1] = {__ballot_sync(0xffffffffu, in && (code == GG_DECISION_DIRECT || code == GG_DECISION_BATCHED))};
   finish_tile<kFastThreads, 1>(a, sm, tile0, ballots, my_skip, my_bad);
 }
@@ -1126,10 +1147,9 @@ struct RegSorted {
 // (fp64 GG_SLOT_LEN(B) each, see greengate_b200.h), applied slot by slot in
 // rank order.
 template <int S>
-__global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, const double* lat,
-                                                     const double* jou, const int32_t* qd, int64_t n,
-                                                     int set_qd, int64_t* err, const double* slots,
-                                                     int G, int B, int rank, gg_fifo* fifo) {
+__device__ __noinline__ void outcome_seq(const gg_params& p, gg_state* st, const double* lat, const double* jou,
+                            const int32_t* qd, int64_t n, int set_qd, int64_t* err,
+                            const double* slots, int G, int B, int rank, gg_fifo* fifo) {
   __shared__ double win[GG_P95_WINDOW_MAX];
   const int lane = threadIdx.x;
   const int cap = p.p95_window;
@@ -1242,6 +1262,279 @@ __global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, 
     st->n_p95_ms = cp;
     st->win_count = count;
     st->win_head = head;
+    st->outcomes_total = outc;
+    st->queue_depth = last_qd;
+    if (err) *err = bad;
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, const double* lat,
+                                                     const double* jou, const int32_t* qd, int64_t n,
+                                                     int set_qd, int64_t* err, const double* slots,
+                                                     int G, int B, int rank, gg_fifo* fifo) {
+  outcome_seq<S>(p, st, lat, jou, qd, n, set_qd, err, slots, G, B, rank, fifo);
+}
+
+// ---------------------------------------------------------------------------
+// K2, parallel form (same results): the EWMA / totals / channel observes are a
+// cheap sequential chain (one thread, CPython order), but the p95 after each
+// outcome — the expensive part of the sequential kernel — depends only on the
+// latency sequence: outcome i's window is the last min(W, h + i + 1) latencies
+// of (history ++ batch), so one warp per outcome selects its nearest-rank
+// element (telemetry.py:35-46) independently: the (count - k + 1)-th largest,
+// extracted by repeated warp max (ties counted with multiplicity).  The ring
+// buffer and the sorted window are rebuilt at the end (positions as the
+// deque's appends would leave them).  NaN latencies (whose sorted() order the
+// sequential kernel models) fall back to outcome_seq.
+constexpr int kOutThreads = 512;
+constexpr int kOutChunk = 512;
+constexpr int kOutMaxSlots = 64;
+
+template <int S>
+__global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
+    gg_params p, gg_state* st, const double* lat, const double* jou, const int32_t* qd, int64_t n,
+    int set_qd, int64_t* err, const double* slots, int G, int B, int rank, gg_fifo* fifo) {
+  __shared__ double seq[GG_P95_WINDOW_MAX + kOutChunk];   // window history ++ chunk latencies
+  __shared__ double sj[kOutChunk];
+  __shared__ int32_t sq[kOutChunk];
+  __shared__ double sp[kOutChunk];
+  __shared__ int64_t slot_off[kOutMaxSlots + 1];
+  __shared__ int s_flag, s_first;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cap = p.p95_window;
+  const int count0 = st->win_count, head0 = st->win_head;
+  // total outcome count and the slot prefix (slots mode)
+  if (tid == 0) {
+    s_flag = 0;
+    int64_t off = 0;
+    if (slots) {
+      #pragma unroll 1
+      for (int gi = 0; gi < G; ++gi) {
+        slot_off[gi] = off;
+        off += (int64_t)slots[(int64_t)gi * (3 * B + 8) + 3 * B];
+      }
+      slot_off[G] = off;
+    }
+  }
+  #pragma unroll 1
+  for (int j = tid; j < count0; j += kOutThreads) seq[j] = st->win[(head0 + j) % cap];
+  __syncthreads();
+  const int64_t n_tot = slots ? slot_off[G] : n;
+  // NaN latencies anywhere -> the sequential kernel's semantics
+  bool nan_here = false;
+  #pragma unroll 1
+  for (int j = tid; j < count0; j += kOutThreads) nan_here |= isnan(seq[j]);
+  #pragma unroll 1
+  for (int64_t e = tid; e < n_tot; e += kOutThreads) {
+    double L;
+    if (slots) {
+      int gi = 0;
+      while (e >= slot_off[gi + 1]) ++gi;
+      L = slots[(int64_t)gi * (3 * B + 8) + (e - slot_off[gi])];
+    } else {
+      L = lat[e];
+    }
+    nan_here |= isnan(L);
+  }
+  if (__syncthreads_or(nan_here)) {
+    if (warp == 0) outcome_seq<S>(p, st, lat, jou, qd, n, set_qd, err, slots, G, B, rank, fifo);
+    return;
+  }
+  // thread 0's sequential state (CPython order)
+  double ewma = st->ewma_joules_per_request, total = st->total_joules, p95 = st->p95_current;
+  int64_t seen = st->samples_seen, outc = st->outcomes_total;
+  gg_channel ce = st->n_energy, cq = st->n_queue_depth, cp = st->n_p95_ms;
+  int last_qd = st->queue_depth;
+  const double lam = p.ewma_lambda, one_minus_lam = f64_sub(1.0, p.ewma_lambda);
+  int64_t adm_other = 0, skip_other = 0;
+  if (slots && tid == 0) {   // other ranks' admission effects first (see outcome_seq)
+    #pragma unroll 1
+    for (int gi = 0; gi < G; ++gi) {
+      if (gi == rank) continue;
+      const double* sl = slots + (int64_t)gi * (3 * B + 8) + 3 * B;
+      if (sl[2] - sl[3] > 0.0) {
+        if (seen > 0) ch_observe(ce, ewma);
+        ch_observe(cq, sl[6]);
+        ch_observe(cp, sl[7]);
+      }
+      adm_other += (int64_t)sl[4];
+      skip_other += (int64_t)sl[5];
+    }
+  }
+  int h = count0;            // history length held in seq[0, h)
+  int64_t bad = -1, m_total = 0;
+  #pragma unroll 1
+  for (int64_t e0 = 0; e0 < n_tot && bad < 0; e0 += kOutChunk) {
+    const int cn = (int)min((int64_t)kOutChunk, n_tot - e0);
+    if (tid == 0) s_first = cn;
+    __syncthreads();
+    #pragma unroll 1
+    for (int c = tid; c < cn; c += kOutThreads) {
+      const int64_t e = e0 + c;
+      double L, J;
+      int32_t Q;
+      if (slots) {
+        int gi = 0;
+        while (e >= slot_off[gi + 1]) ++gi;
+        const double* sl = slots + (int64_t)gi * (3 * B + 8);
+        const int64_t i = e - slot_off[gi];
+        L = sl[i];
+        J = sl[B + i];
+        Q = (int32_t)sl[2 * B + i];
+      } else {
+        L = lat[e];
+        J = jou[e];
+        Q = qd[e];
+      }
+      seq[h + c] = L;
+      sj[c] = J;
+      sq[c] = Q;
+      if (L < 0.0 || J < 0.0 || Q < 0) atomicMin(&s_first, c);   // NegativeMeasurement
+    }
+    __syncthreads();
+    const int nc = s_first;
+    if (nc < cn) {
+      const int64_t e = e0 + nc;
+      if (slots) {
+        int gi = 0;
+        while (e >= slot_off[gi + 1]) ++gi;
+        bad = (int64_t)gi * B + (e - slot_off[gi]);
+      } else {
+        bad = e;
+      }
+    }
+    // p95 after each outcome: one warp per outcome
+    #pragma unroll 1
+    for (int c = warp; c < nc; c += kOutThreads / 32) {
+      const int cnt = min(cap, h + c + 1);
+      const int start = h + c + 1 - cnt;
+      double v[S];
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        const int j = q * 32 + lane;
+        v[q] = j < cnt ? seq[start + j] : -INFINITY;
+      }
+      const int k = (int)ceil(f64_mul(0.95, (double)cnt));   // ceil(95.0/100.0 * n)
+      const int r = cnt - k + 1;                             // k-th smallest = r-th largest
+      double got = 0.0;
+      #pragma unroll 1
+      for (int it = 0; it < r; ++it) {
+        double bv = v[0];
+        int bq = 0;
+#pragma unroll
+        for (int q = 1; q < S; ++q)
+          if (v[q] > bv) {
+            bv = v[q];
+            bq = q;
+          }
+        int bl = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+          const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+          if (ov > bv || (ov == bv && (oq * 32 + ol) < (bq * 32 + bl))) {
+            bv = ov;
+            bl = ol;
+            bq = oq;
+          }
+        }
+        got = bv;
+        if (lane == bl) {
+#pragma unroll
+          for (int q = 0; q < S; ++q)
+            if (q == bq) v[q] = -INFINITY;
+        }
+      }
+      if (lane == 0) sp[c] = got;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      #pragma unroll 1
+      for (int c = 0; c < nc; ++c) {
+        const double J = sj[c];
+        const int32_t Q = sq[c];
+        // EnergyLedger.observe_request -> ewma_update (energy.py:24-36, 75-87)
+        ewma = (seen > 0) ? f64_add(f64_mul(lam, ewma), f64_mul(one_minus_lam, J)) : J;
+        seen += 1;
+        total = f64_add(total, J);
+        p95 = sp[c];
+        ch_observe(ce, ewma);
+        ch_observe(cq, (double)Q);
+        ch_observe(cp, p95);
+        outc += 1;
+        if (set_qd) last_qd = Q;
+      }
+    }
+    // keep the last min(cap, h + nc) latencies as the next history
+    const int hn = min(cap, h + nc), src = h + nc - hn;
+    double tmp[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = tid + q * kOutThreads;
+      tmp[q] = j < hn ? seq[src + j] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = tid + q * kOutThreads;
+      if (j < hn) seq[j] = tmp[q];
+    }
+    h = hn;
+    m_total += nc;
+    __syncthreads();
+  }
+  // ring buffer: window element j sits at (head_f + j) % cap
+  const int head_f = (count0 + m_total <= cap) ? head0 : (int)((head0 + (count0 + m_total - cap)) % cap);
+  #pragma unroll 1
+  for (int j = tid; j < h; j += kOutThreads) st->win[(head_f + j) % cap] = seq[j];
+  // sorted window: bitonic sort of seq[0, h) padded with +inf to 1024 (in place)
+  #pragma unroll 1
+  for (int j = h + tid; j < GG_P95_WINDOW_MAX; j += kOutThreads) seq[j] = INFINITY;
+  __syncthreads();
+  #pragma unroll 1
+  for (int size = 2; size <= GG_P95_WINDOW_MAX; size <<= 1) {
+    #pragma unroll 1
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      #pragma unroll 1
+      for (int i = tid; i < GG_P95_WINDOW_MAX; i += kOutThreads) {
+        const int jx = i ^ stride;
+        if (jx > i) {
+          const bool up = (i & size) == 0;
+          const double a = seq[i], b = seq[jx];
+          if ((a > b) == up) {
+            seq[i] = b;
+            seq[jx] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  #pragma unroll 1
+  for (int j = tid; j < h; j += kOutThreads) st->win_sorted[j] = seq[j];
+  if (tid == 0) {
+    if (slots && fifo) {   // global queue depth seen by this rank's next snapshot
+      int64_t extra = 0;
+      #pragma unroll 1
+      for (int gi = 0; gi < G; ++gi)
+        if (gi != rank) extra += (int64_t)slots[(int64_t)gi * (3 * B + 8) + 3 * B + 1];
+      fifo->extra_depth = extra;
+    }
+    if (slots) {
+      st->admitted_total += adm_other;
+      st->skipped_total += skip_other;
+    }
+    st->ewma_joules_per_request = ewma;
+    st->total_joules = total;
+    st->samples_seen = seen;
+    st->p95_current = p95;
+    st->n_energy = ce;
+    st->n_queue_depth = cq;
+    st->n_p95_ms = cp;
+    st->win_count = h;
+    st->win_head = head_f;
     st->outcomes_total = outc;
     st->queue_depth = last_qd;
     if (err) *err = bad;
@@ -1413,7 +1706,7 @@ static int64_t admit_blocks(int64_t n, int32_t k) {
 }
 
 static int64_t lookback_words(int64_t n) {   // worst case over the single-pass kernels
-  const int64_t nb = (n + kLargeRows - 1) / kLargeRows;
+  const int64_t nb = (n + kFastRows - 1) / kFastRows;
   return nb < 1 ? 1 : nb;
 }
 
@@ -1432,8 +1725,16 @@ static int launch_outcome(const gg_params& p, gg_state* st, const double* lat, c
                           void* stream) {
   cudaStream_t s = gg_stream(stream);
   const int w = p.p95_window;
-#define GG_OUTCOME(SLOTS) \
-  outcome_kernel<SLOTS><<<1, 32, 0, s>>>(p, st, lat, jou, qd, n, set_qd, err, slots, G, B, rank, fifo)
+  const bool par = !getenv("GG_OUTCOME_SEQ") && (!slots || G <= kOutMaxSlots);
+#define GG_OUTCOME(SLOTS)                                                                        \
+  do {                                                                                           \
+    if (par)                                                                                     \
+      outcome_par_kernel<SLOTS><<<1, kOutThreads, 0, s>>>(p, st, lat, jou, qd, n, set_qd, err, slots, \
+                                                          G, B, rank, fifo);                     \
+    else                                                                                         \
+      outcome_kernel<SLOTS><<<1, 32, 0, s>>>(p, st, lat, jou, qd, n, set_qd, err, slots, G, B,   \
+                                             rank, fifo);                                        \
+  } while (0)
   if (w <= 32) GG_OUTCOME(1);
   else if (w <= 64) GG_OUTCOME(2);
   else if (w <= 128) GG_OUTCOME(4);
@@ -1519,10 +1820,11 @@ static int launch_admit(const AdmitArgs& args, void* stream) {
           a, (int)nb);
     }
   } else if (!bd && !getenv("GG_ADMIT_EXACT_ONLY")) {
+    const unsigned g = (unsigned)((n + kFastRows - 1) / kFastRows > 0 ? (n + kFastRows - 1) / kFastRows : 1);
     if (k <= kRegChunks * 32)
-      admit_large_fast_kernel<true><<<(unsigned)nb, kFastThreads, 0, s>>>(a);
+      admit_large_fast_kernel<true><<<g, kFastThreads, 0, s>>>(a);
     else
-      admit_large_fast_kernel<false><<<(unsigned)nb, kFastThreads, 0, s>>>(a);
+      admit_large_fast_kernel<false><<<g, kFastThreads, 0, s>>>(a);
   } else {
     admit_large_kernel<<<(unsigned)nb, kLargeThreads, 0, s>>>(a);
   }

@@ -422,17 +422,22 @@ __global__ void maxpool3x3s2(const __nv_bfloat16* __restrict__ in, __nv_bfloat16
   *reinterpret_cast<uint4*>(out + o * C + c0) = u;
 }
 
-// Global average pool NHWC [N, HW, C] -> [N, C] bf16 (fp32 sum), one thread per (n, 8 channels).
-__global__ void avgpool_global(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
-                               int N, int HW, int C, const int32_t* count, int denom) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  const int cg = C / 8;
+// Global average pool NHWC [N, HW, C] -> [N, C] bf16 (fp32 sum).  Block =
+// (image, 64 channels): warp w owns channels 8w..8w+7 (one 16-byte load per
+// pixel), its lanes stride over the pixels, then a warp reduction.
+__global__ void __launch_bounds__(256) avgpool_global(const __nv_bfloat16* __restrict__ in,
+                                                      __nv_bfloat16* __restrict__ out, int N,
+                                                      int HW, int C, const int32_t* count,
+                                                      int denom) {
   if (count) N = min(N, __ldg(count));
-  if (idx >= N * cg) return;
-  const int n = idx / cg, c0 = (idx % cg) * 8;
+  const int n = blockIdx.y;
+  if (n >= N) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * 64 + warp * 8;
   float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int p = 0; p < HW; ++p) {
-    const uint4 u = __ldg(reinterpret_cast<const uint4*>(in + ((int64_t)n * HW + p) * C + c0));
+  const __nv_bfloat16* base = in + (int64_t)n * HW * C + c0;
+  for (int p = lane; p < HW; p += 32) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)p * C));
     const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -441,13 +446,19 @@ __global__ void avgpool_global(const __nv_bfloat16* __restrict__ in, __nv_bfloat
       s[2 * e + 1] += f.y;
     }
   }
-  const float inv = 1.0f / (denom > 0 ? denom : HW);   // padded input: borders are zeros
-  uint4 u;
-  u.x = pack_bf16(s[0] * inv, s[1] * inv);
-  u.y = pack_bf16(s[2] * inv, s[3] * inv);
-  u.z = pack_bf16(s[4] * inv, s[5] * inv);
-  u.w = pack_bf16(s[6] * inv, s[7] * inv);
-  *reinterpret_cast<uint4*>(out + (int64_t)n * C + c0) = u;
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s[e] += __shfl_xor_sync(0xffffffffu, s[e], o);
+  if (lane == 0) {
+    const float inv = 1.0f / (denom > 0 ? denom : HW);   // padded input: borders are zeros
+    uint4 u;
+    u.x = pack_bf16(s[0] * inv, s[1] * inv);
+    u.y = pack_bf16(s[2] * inv, s[3] * inv);
+    u.z = pack_bf16(s[4] * inv, s[5] * inv);
+    u.w = pack_bf16(s[6] * inv, s[7] * inv);
+    *reinterpret_cast<uint4*>(out + (int64_t)n * C + c0) = u;
+  }
 }
 
 }  // namespace gg
@@ -561,9 +572,9 @@ extern "C" int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, i
 
 extern "C" int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y,
                           int32_t denom, const int32_t* count_dev, void* stream) {
-  if (!x || !y || C % 8 || denom < 0) return GG_ERR_INVALID_ARGUMENT;
-  const int work = N * (C / 8);
-  avgpool_global<<<(work + 127) / 128, 128, 0, gg_stream(stream)>>>(
+  if (!x || !y || C % 8 || denom < 0 || N < 1) return GG_ERR_INVALID_ARGUMENT;
+  if (C % 64 || N > 65535) return GG_ERR_UNSUPPORTED;
+  avgpool_global<<<dim3((unsigned)(C / 64), (unsigned)N), 256, 0, gg_stream(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, HW, C,
       count_dev, denom);
   GG_LAUNCH_OK();

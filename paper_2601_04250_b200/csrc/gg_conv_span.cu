@@ -67,13 +67,20 @@ struct SpanEpi {
   const __nv_bfloat16* residual;  // padded, same geometry as y (padded mode), or null
   int relu;
   const int32_t* count;
+  unsigned long long* prof;   // debug (GG_SPAN_PROF): per-CTA globaltimer start / end
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint64_t sdesc_sw(uint32_t addr, int row_bytes) {
   return row_bytes == 128 ? sdesc_k_sw128(addr) : sdesc_k_sw32(addr);
 }
 
-template <int BN, int CH, int RT, bool DENSE>
+template <int BN, int CH, int RT, bool DENSE, int MT>
 __global__ void __launch_bounds__(kSpanThreads, 1)
     conv_span_tcgen05(const __grid_constant__ CUtensorMap map_x,
                       const __grid_constant__ CUtensorMap map_w, SpanShape sh, SpanEpi ep) {
@@ -81,6 +88,8 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   constexpr int KSTEPS = CH / 16;            // MMAs per tap
   constexpr int TAPS = RT * RT;
   constexpr int B_BYTES = BN * RB;           // one tap slab of B
+  constexpr int BM = 128 * MT;               // MT M=128 sub-tiles share every B slab
+  constexpr int ACC_COLS = MT * BN;          // TMEM columns per accumulator buffer
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int cblocks = sh.C / CH;
@@ -100,10 +109,14 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (ep.prof && threadIdx.x == 0) {
+    ep.prof[2 * blockIdx.x] = gtimer();
+    ep.prof[2048 + 2 * blockIdx.x] = clock64();
+  }
   const int img = sh.Hp * sh.Wp;
   const int n_eff = ep.count ? min(sh.N, __ldg(ep.count)) : sh.N;
   const int Mtot = n_eff * img;
-  const int tiles_m = (Mtot + 127) / 128, tiles_n = sh.Cout / BN;
+  const int tiles_m = (Mtot + BM - 1) / BM, tiles_n = sh.Cout / BN;
   const int num_tiles = tiles_m * tiles_n;
 
   if (threadIdx.x == 0) {
@@ -122,7 +135,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     tma_prefetch(&map_x);
     tma_prefetch(&map_w);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 1) tmem_alloc(tmem_slot, 2 * ACC_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -137,10 +150,12 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       int ait = 0, bit = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int tm = tile % tiles_m, tn = tile / tiles_m;
-        const int m0 = tm * 128;
+        const int m0 = tm * BM;
         for (int cb = 0; cb < cblocks; ++cb, ++ait) {
           const int as = ait % AST;
           mbar_wait(&a_empty[as], ((ait / AST) & 1) ^ 1);
+          if (ep.prof && blockIdx.x == 0 && cb == 0 && ait / cblocks < 16)
+            ep.prof[4096 + (ait / cblocks) * 8 + 0] = clock64();
           uint8_t* sa = a_base + as * sh.a_stage_bytes;
           mbar_expect_tx(&a_full[as], sh.boxes * sh.box_rows * RB);
           for (int bx = 0; bx < sh.boxes; ++bx)   // boxes of <= 256 rows (TMA limit)
@@ -170,10 +185,11 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
         const int acc = t & 1;
         mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * ACC_COLS;
         for (int cb = 0; cb < cblocks; ++cb, ++ait) {
           const int as = ait % AST;
           mbar_wait(&a_full[as], (ait / AST) & 1);
+          if (ep.prof && blockIdx.x == 0 && cb == 0 && t < 16) ep.prof[4096 + t * 8 + 1] = clock64();
           tc_fence_after();
           const uint64_t ad = sdesc_sw(smem_u32(a_base + as * sh.a_stage_bytes), RB);
           if (sh.bres) {
@@ -184,8 +200,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
               const uint64_t bo = bd + (uint64_t)(tap * (B_BYTES >> 4));
 #pragma unroll
               for (int kk = 0; kk < KSTEPS; ++kk)
-                umma_bf16(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
-                          (cb | tap | kk) != 0);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+                  umma_bf16(d_tmem + mt * BN, ao + (uint64_t)(mt * 128 * RB / 16 + kk * 2),
+                            bo + (uint64_t)(kk * 2), idesc, (cb | tap | kk) != 0);
             }
           } else {
 #pragma unroll
@@ -197,14 +215,17 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
               const uint64_t bo = bres_desc + (uint64_t)(bs * (B_BYTES >> 4));
 #pragma unroll
               for (int kk = 0; kk < KSTEPS; ++kk)
-                umma_bf16(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
-                          (cb | tap | kk) != 0);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+                  umma_bf16(d_tmem + mt * BN, ao + (uint64_t)(mt * 128 * RB / 16 + kk * 2),
+                            bo + (uint64_t)(kk * 2), idesc, (cb | tap | kk) != 0);
               umma_commit(&b_empty[bs]);
             }
           }
           umma_commit(&a_empty[as]);
         }
         umma_commit(&acc_full[acc]);
+        if (ep.prof && blockIdx.x == 0 && t < 16) ep.prof[4096 + t * 8 + 2] = clock64();
       }
     }
   } else {
@@ -216,87 +237,97 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
       const int acc = t & 1;
-      const int m = tm * 128 + quarter * 32 + lane;
-      const int nimg = m / img;
-      const int within = m - nimg * img;
-      const int h = within / sh.Wp, w = within - (within / sh.Wp) * sh.Wp;
-      const bool real = m < Mtot && h < sh.Ho && w < sh.Wo;
-      int64_t oidx;
-      bool store;
-      if constexpr (DENSE) {
-        oidx = ((int64_t)nimg * sh.Ho + h) * sh.Wo + w;
-        store = real;
-      } else {
-        oidx = (int64_t)m + sh.Wp + 1;   // padded output position
-        store = m < Mtot && oidx < (int64_t)n_eff * img;
-      }
       mbar_wait(&acc_full[acc], (t >> 1) & 1);
+      if (ep.prof && blockIdx.x == 0 && warp == 2 && lane == 0 && t < 16) ep.prof[4096 + t * 8 + 3] = clock64();
       tc_fence_after();
 #pragma unroll 1
-      for (int c = half * HALF; c < (half + 1) * HALF; c += 32) {
-        const int col0 = tn * BN + c;
-        // residual loads first: their latency overlaps the TMEM read
-        uint4 res[4];
-        const bool use_res = !DENSE && ep.residual != nullptr && store && real;
-        if (use_res) {
-          const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + oidx * sh.Cout + col0);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) res[q] = __ldg(rp + q);
+      for (int mt = 0; mt < MT; ++mt) {
+        const int m = tm * BM + mt * 128 + quarter * 32 + lane;
+        const int nimg = m / img;
+        const int within = m - nimg * img;
+        const int h = within / sh.Wp, w = within - (within / sh.Wp) * sh.Wp;
+        const bool real = m < Mtot && h < sh.Ho && w < sh.Wo;
+        int64_t oidx;
+        bool store;
+        if constexpr (DENSE) {
+          oidx = ((int64_t)nimg * sh.Ho + h) * sh.Wo + w;
+          store = real;
+        } else {
+          oidx = (int64_t)m + sh.Wp + 1;   // padded output position
+          store = m < Mtot && oidx < (int64_t)n_eff * img;
         }
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
-        tmem_ld_wait();
-        if (!store) continue;
-        float v[32];
-        if (real) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + i));
-            v[i] = __uint_as_float(r[i]) + b.x;
-            v[i + 1] = __uint_as_float(r[i + 1]) + b.y;
-            v[i + 2] = __uint_as_float(r[i + 2]) + b.z;
-            v[i + 3] = __uint_as_float(r[i + 3]) + b.w;
-          }
+        const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ACC_COLS + mt * BN;
+#pragma unroll 1
+        for (int c = half * HALF; c < (half + 1) * HALF; c += 32) {
+          const int col0 = tn * BN + c;
+          // residual loads first: their latency overlaps the TMEM read
+          uint4 res[4];
+          const bool use_res = !DENSE && ep.residual != nullptr && store && real;
           if (use_res) {
+            const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + oidx * sh.Cout + col0);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&res[q]);
+            for (int q = 0; q < 4; ++q) res[q] = __ldg(rp + q);
+          }
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tcol + c, r);
+          tmem_ld_wait();
+          if (!store) continue;
+          float v[32];
+          if (real) {
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h2[e]);
-                v[q * 8 + 2 * e] += f.x;
-                v[q * 8 + 2 * e + 1] += f.y;
+            for (int i = 0; i < 32; i += 4) {
+              const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + i));
+              v[i] = __uint_as_float(r[i]) + b.x;
+              v[i + 1] = __uint_as_float(r[i + 1]) + b.y;
+              v[i + 2] = __uint_as_float(r[i + 2]) + b.z;
+              v[i + 3] = __uint_as_float(r[i + 3]) + b.w;
+            }
+            if (use_res) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&res[q]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = __bfloat1622float2(h2[e]);
+                  v[q * 8 + 2 * e] += f.x;
+                  v[q * 8 + 2 * e + 1] += f.y;
+                }
               }
             }
+            if (ep.relu) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.0f;   // padding positions stay zero
           }
-          if (ep.relu) {
+          uint4* dp = reinterpret_cast<uint4*>(ep.y + oidx * sh.Cout + col0);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+            u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+            u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+            u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+            dp[q] = u;
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0.0f;   // padding positions stay zero
-        }
-        uint4* dp = reinterpret_cast<uint4*>(ep.y + oidx * sh.Cout + col0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 u;
-          u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-          u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-          u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-          u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
-          dp[q] = u;
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      if (ep.prof && blockIdx.x == 0 && warp == 2 && lane == 0 && t < 16) ep.prof[4096 + t * 8 + 4] = clock64();
     }
   }
   __syncthreads();
+  if (ep.prof && threadIdx.x == 0) {
+    ep.prof[2 * blockIdx.x + 1] = gtimer();
+    ep.prof[2048 + 2 * blockIdx.x + 1] = clock64();
+  }
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * BN);
+    tmem_dealloc(tmem_base, 2 * ACC_COLS);
   }
 }
 
@@ -328,10 +359,10 @@ static int span_smem_bytes(const SpanShape& sh, int bn, int rb, int taps) {
   return sh.a_stages * sh.a_stage_bytes + (sh.bres ? nkb : sh.b_stages) * bn * rb + 1024 + 1024;
 }
 
-template <int BN, int CH, int RT, bool DENSE>
+template <int BN, int CH, int RT, bool DENSE, int MT>
 static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanShape& sh,
                        const SpanEpi& ep, cudaStream_t s) {
-  auto kern = conv_span_tcgen05<BN, CH, RT, DENSE>;
+  auto kern = conv_span_tcgen05<BN, CH, RT, DENSE, MT>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpanSmemMax) != cudaSuccess)
@@ -339,10 +370,52 @@ static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanS
     attr = true;
   }
   const int smem = span_smem_bytes(sh, BN, CH * 2, RT * RT);
-  const int tiles = ((sh.N * sh.Hp * sh.Wp + 127) / 128) * (sh.Cout / BN);
+  const int tiles = ((sh.N * sh.Hp * sh.Wp + 128 * MT - 1) / (128 * MT)) * (sh.Cout / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, kSpanThreads, smem, s>>>(mx, mw, sh, ep);
+  SpanEpi e2 = ep;
+  static unsigned long long* prof = nullptr;
+  const bool do_prof = getenv("GG_SPAN_PROF") != nullptr;
+  if (do_prof) {
+    if (!prof) cudaMalloc(&prof, 8 * 1024 * sizeof(unsigned long long));
+    e2.prof = prof;
+    cudaMemsetAsync(prof + 4096, 0, 4096 * sizeof(unsigned long long), s);
+  }
+  static int prof_calls = 0;
+  const int prof_at = do_prof ? atoi(getenv("GG_SPAN_PROF")) : 0;
+  const bool report = do_prof && ++prof_calls >= (prof_at > 0 ? prof_at : 1);
+  kern<<<grid, kSpanThreads, smem, s>>>(mx, mw, sh, e2);
   GG_LAUNCH_OK();
+  if (report) {
+    prof_calls = 0;
+    static unsigned long long h[8 * 1024];
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, prof, 8 * 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    const unsigned long long c0 = h[2048];
+    fprintf(stderr, "CTA0 timeline (cycles from CTA start): tile: tma_issue a_full mma_issued epi_got epi_done\n");
+    for (int t = 0; t < 16; ++t) {
+      const unsigned long long* e = h + 4096 + t * 8;
+      if (!e[1]) break;
+      fprintf(stderr, "  %2d: %7lld %7lld %7lld %7lld %7lld\n", t, (long long)(e[0] - c0),
+              (long long)(e[1] - c0), (long long)(e[2] - c0), (long long)(e[3] - c0), (long long)(e[4] - c0));
+    }
+    double csum = 0;
+    for (int i = 0; i < grid; ++i) csum += (double)(h[2048 + 2 * i + 1] - h[2048 + 2 * i]);
+    fprintf(stderr, "span mean CTA clock64 cycles %.0f\n", csum / grid);
+    unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+    double dsum = 0;
+    for (int i = 0; i < grid; ++i) {
+      s0 = h[2 * i] < s0 ? h[2 * i] : s0;
+      s1 = h[2 * i] > s1 ? h[2 * i] : s1;
+      e0 = h[2 * i + 1] < e0 ? h[2 * i + 1] : e0;
+      e1 = h[2 * i + 1] > e1 ? h[2 * i + 1] : e1;
+      dsum += (double)(h[2 * i + 1] - h[2 * i]);
+    }
+    fprintf(stderr, "span BN=%d CH=%d RT=%d MT=%d C=%d Cout=%d H=%d: grid %d tiles %d stages A%d B%d%s | "
+            "start spread %.2f us, end spread %.2f us, mean CTA %.2f us, total %.2f us\n",
+            BN, CH, RT, MT, sh.C, sh.Cout, sh.H, grid, tiles, sh.a_stages, sh.b_stages,
+            sh.bres ? " (B resident)" : "", (s1 - s0) * 1e-3, (e1 - e0) * 1e-3, dsum / grid * 1e-3,
+            (e1 - s0) * 1e-3);
+  }
   return GG_OK;
 }
 
@@ -388,43 +461,60 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
   sh.N = N; sh.H = H; sh.W = W; sh.C = C; sh.Cout = Cout;
   sh.Hp = H + 2; sh.Wp = W + 2;
   sh.Ho = H; sh.Wo = W;
-  sh.span_rows = 128 + 2 * sh.Wp + 2;
-  if (sh.span_rows > 1024) return GG_ERR_UNSUPPORTED;
   const int64_t Mtot = (int64_t)N * sh.Hp * sh.Wp;
-  // N tile by modelled time: tensor time per wave vs L2 operand traffic
-  const int64_t tiles_m = (Mtot + 127) / 128;
-  const int64_t nkb = C / 64 * 9;
-  int bn = 64;
+  // Tile shape (BN x 128*MT) by a per-SM time model: MMA cycles per tile
+  // (tools/mma_bench.cu: 48 / 64 / 128 cycles per K=16 step at N = 64/128/256)
+  // vs the SM's operand ingress (~40 B/cycle: B slabs unless resident + A
+  // spans), tiles per CTA, plus the last tile's epilogue and the resident-B
+  // prologue, which nothing overlaps.
+  const int cblocks = C / 64;
+  struct Cand { int bn, mt; };
+  const Cand cands[] = {{64, 1}, {128, 1}, {256, 1}, {64, 2}, {128, 2}};
+  int best_bn = 64, best_mt = 1;
   double best = 1e30;
-  for (int cand : {64, 128, 256}) {
-    if (cand > Cout || Cout % cand) continue;
+  for (const Cand& cd : cands) {
+    if (cd.bn > Cout || Cout % cd.bn) continue;
     SpanShape t = sh;
-    if (!plan_span(t, cand, 128, 9)) continue;
-    const int64_t tiles = tiles_m * (Cout / cand);
-    const int64_t waves = (tiles + num_sms() - 1) / num_sms();
-    const double cyc_mma = (cand == 64 ? 48.0 : cand / 2.0) * 4;   // per tap (tools/mma_bench.cu)
-    const double t_mma = (double)waves * nkb * cyc_mma / 1.9e9;
-    const double bbytes = t.bres ? (double)(tiles < num_sms() ? tiles : num_sms()) * nkb * cand * 128
-                                 : (double)tiles * nkb * cand * 128;
-    const double t_l2 = ((double)tiles * (C / 64) * sh.span_rows * 128 + bbytes) / 8.0e12;
-    const double tt = t_mma > t_l2 ? t_mma : t_l2;
+    t.span_rows = 128 * cd.mt + 2 * sh.Wp + 2;
+    if (t.span_rows > 1024 || !plan_span(t, cd.bn, 128, 9)) continue;
+    const int64_t tiles = (Mtot + 128 * cd.mt - 1) / (128 * cd.mt) * (Cout / cd.bn);
+    const int64_t per_cta = (tiles + num_sms() - 1) / num_sms();
+    const double cyc_k = cd.bn == 64 ? 48.0 : cd.bn / 2.0;
+    const double mma = (double)cblocks * 9 * 4 * cd.mt * cyc_k;
+    const double ingress = ((double)cblocks * t.boxes * t.box_rows * 128 +
+                            (t.bres ? 0.0 : (double)cblocks * 9 * cd.bn * 128)) / 40.0;
+    const double tile = mma > ingress ? mma : ingress;
+    const double epi = cd.mt * (cd.bn / 64.0) * 700.0;
+    const double pro = t.bres ? (double)cblocks * 9 * cd.bn * 128 / 40.0 : 0.0;
+    const double tt = per_cta * tile + epi + pro;
     if (tt < best * 0.97) {
       best = tt;
-      bn = cand;
+      best_bn = cd.bn;
+      best_mt = cd.mt;
     }
   }
-  if (!plan_span(sh, bn, 128, 9)) return GG_ERR_UNSUPPORTED;
+  if (getenv("GG_SPAN_TILE")) {   // debug override "BN,MT"
+    int a = 0, b = 0;
+    if (sscanf(getenv("GG_SPAN_TILE"), "%d,%d", &a, &b) == 2 && a > 0 && Cout % a == 0 && (b == 1 || b == 2)) {
+      best_bn = a;
+      best_mt = b;
+    }
+  }
+  sh.span_rows = 128 * best_mt + 2 * sh.Wp + 2;
+  if (sh.span_rows > 1024 || !plan_span(sh, best_bn, 128, 9)) return GG_ERR_UNSUPPORTED;
   CUtensorMap mx, mw;
   int rc = make_map_span(&mx, x, Mtot, C, 64, sh.box_rows);
-  if (!rc) rc = make_map_span(&mw, w, Cout, (int64_t)C * 9, 64, bn);
+  if (!rc) rc = make_map_span(&mw, w, Cout, (int64_t)C * 9, 64, best_bn);
   if (rc) return rc;
   SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
-             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev};
+             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr};
   cudaStream_t s = gg_stream(stream);
-  switch (bn) {
-    case 256: return launch_span<256, 64, 3, false>(mx, mw, sh, ep, s);
-    case 128: return launch_span<128, 64, 3, false>(mx, mw, sh, ep, s);
-    default: return launch_span<64, 64, 3, false>(mx, mw, sh, ep, s);
+  switch (best_bn * 4 + best_mt) {
+    case 256 * 4 + 1: return launch_span<256, 64, 3, false, 1>(mx, mw, sh, ep, s);
+    case 128 * 4 + 1: return launch_span<128, 64, 3, false, 1>(mx, mw, sh, ep, s);
+    case 128 * 4 + 2: return launch_span<128, 64, 3, false, 2>(mx, mw, sh, ep, s);
+    case 64 * 4 + 2: return launch_span<64, 64, 3, false, 2>(mx, mw, sh, ep, s);
+    default: return launch_span<64, 64, 3, false, 1>(mx, mw, sh, ep, s);
   }
 }
 
@@ -445,6 +535,6 @@ extern "C" int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws
   int rc = make_map_span(&mx, x, Mtot, 16, 16, sh.box_rows);
   if (!rc) rc = make_map_span(&mw, w, Cout, 256, 16, 64);
   if (rc) return rc;
-  SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, relu, count_dev};
-  return launch_span<64, 16, 4, true>(mx, mw, sh, ep, gg_stream(stream));
+  SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, relu, count_dev, nullptr};
+  return launch_span<64, 16, 4, true, 1>(mx, mw, sh, ep, gg_stream(stream));
 }

@@ -75,47 +75,87 @@ __global__ void served_outcomes_kernel(const gg_fifo* f, const int32_t* count, c
   }
 }
 
-// K3 over the served batch, one warp per row (see gg_epilogue in gg_controller.cu).
-__global__ void __launch_bounds__(256) epilogue_served_kernel(const float* logits,
-                                                              const int32_t* count, int k,
-                                                              int64_t ld, const int32_t* ids,
-                                                              int32_t* pred, double* conf,
-                                                              double* probs, int32_t* bpred,
-                                                              double* bconf) {
-  const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+// K3 over the served batch (see gg_epilogue in gg_controller.cu): one 128-thread
+// block per row; each thread keeps its <= 8 logits in registers, so every
+// element costs one fp64 exp (max, sum of exp(x - max), then p = e / sum with
+// the argmax taken over p, lowest index on ties, as before).
+constexpr int kEpiThreads = 128;
+constexpr int kEpiPer = 8;   // K <= 1024 in registers
+
+__device__ __forceinline__ void epi_best(double& best, int& bi, double ob, int oi) {
+  if (ob > best || (ob == best && oi < bi)) {
+    best = ob;
+    bi = oi;
+  }
+}
+
+__global__ void __launch_bounds__(kEpiThreads) epilogue_served_kernel(const float* logits,
+                                                                     const int32_t* count, int k,
+                                                                     int64_t ld, const int32_t* ids,
+                                                                     int32_t* pred, double* conf,
+                                                                     double* probs, int32_t* bpred,
+                                                                     double* bconf) {
+  __shared__ float red_m[kEpiThreads / 32];
+  __shared__ double red_s[kEpiThreads / 32];
+  __shared__ double red_b[kEpiThreads / 32];
+  __shared__ int red_i[kEpiThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row = blockIdx.x;
   if (row >= *count) return;
   const float* x = logits + (int64_t)row * ld;
+  float xv[kEpiPer];
   float m = -INFINITY;
-  for (int j = lane; j < k; j += 32) m = fmaxf(m, x[j]);
+#pragma unroll
+  for (int i = 0; i < kEpiPer; ++i) {
+    const int j = tid + i * kEpiThreads;
+    xv[i] = j < k ? __ldg(x + j) : -INFINITY;
+    m = fmaxf(m, xv[i]);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) red_m[warp] = m;
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < kEpiThreads / 32; ++w) m = fmaxf(m, red_m[w]);
   const double md = (double)m;
+  double ev[kEpiPer];
   double s = 0.0;
-  for (int j = lane; j < k; j += 32) s += exp((double)x[j] - md);
+#pragma unroll
+  for (int i = 0; i < kEpiPer; ++i) {
+    const int j = tid + i * kEpiThreads;
+    ev[i] = j < k ? exp((double)xv[i] - md) : 0.0;
+    s += ev[i];
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) red_s[warp] = s;
+  __syncthreads();
+  s = 0.0;
+#pragma unroll
+  for (int w = 0; w < kEpiThreads / 32; ++w) s += red_s[w];
   const double inv = 1.0 / s;
   double best = -1.0;
   int bi = 0x7fffffff;
-  for (int j = lane; j < k; j += 32) {
-    const double pj = exp((double)x[j] - md) * inv;
-    if (probs) probs[(int64_t)row * k + j] = pj;
-    if (pj > best) {
-      best = pj;
-      bi = j;
+#pragma unroll
+  for (int i = 0; i < kEpiPer; ++i) {
+    const int j = tid + i * kEpiThreads;
+    if (j < k) {
+      const double pj = ev[i] * inv;
+      if (probs) probs[(int64_t)row * k + j] = pj;
+      epi_best(best, bi, pj, j);
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ob > best || (ob == best && oi < bi)) {
-      best = ob;
-      bi = oi;
-    }
-  }
+  for (int o = 16; o > 0; o >>= 1)
+    epi_best(best, bi, __shfl_xor_sync(0xffffffffu, best, o), __shfl_xor_sync(0xffffffffu, bi, o));
   if (lane == 0) {
+    red_b[warp] = best;
+    red_i[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int w = 1; w < kEpiThreads / 32; ++w) epi_best(best, bi, red_b[w], red_i[w]);
     const int id = ids[row];
     if (pred) pred[id] = bi;
     if (conf) conf[id] = best;
@@ -136,35 +176,50 @@ __device__ __forceinline__ int64_t s2d_index(int n, int yy, int xx, int Ho, int 
   return ((int64_t)n * (Ho + 3) + yy + 2) * (Wo + 3) + xx + 2;
 }
 
-__global__ void stem_gather_kernel(const uint8_t* __restrict__ pool, int64_t pool_size,
-                                   const int32_t* ids, const int32_t* count, int B, int H, int W,
-                                   float m0, float m1, float m2, float s0, float s1, float s2,
-                                   int padded, __nv_bfloat16* __restrict__ y) {
+// One block per (image, s2d row): the two source image rows (2 x W x 3 bytes)
+// are staged in shared memory with 16-byte loads when aligned, then each thread
+// builds s2d pixels from shared memory and writes 32 contiguous bytes
+// (consecutive threads -> consecutive pixels: coalesced).
+constexpr int kGatherThreads = 128;
+
+__global__ void __launch_bounds__(kGatherThreads) stem_gather_kernel(
+    const uint8_t* __restrict__ pool, int64_t pool_size, const int32_t* ids, const int32_t* count,
+    int B, int H, int W, float m0, float m1, float m2, float s0, float s1, float s2, int padded,
+    __nv_bfloat16* __restrict__ y) {
+  extern __shared__ __align__(16) uint8_t rows[];   // [2][W * 3]
   const int n_valid = count ? min(B, __ldg(count)) : B;
+  const int n = blockIdx.y, yy = blockIdx.x;
+  if (n >= n_valid) return;
   const int Ho = H / 2, Wo = W / 2;
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= (int64_t)n_valid * Ho * Wo) return;
-  const int n = (int)(p / ((int64_t)Ho * Wo));
-  const int rem = (int)(p - (int64_t)n * Ho * Wo);
-  const int yy = rem / Wo, xx = rem - yy * Wo;
   const int64_t img = ids ? (int64_t)__ldg(ids + n) % pool_size : n;
-  const float mean[3] = {m0, m1, m2}, sd[3] = {s0, s1, s2};
-  const int64_t q = s2d_index(n, yy, xx, Ho, Wo, padded);
-  __align__(16) __nv_bfloat16 v[16];
-#pragma unroll
-  for (int dy = 0; dy < 2; ++dy) {
-    const uint8_t* row = pool + ((img * H + 2 * yy + dy) * W + 2 * xx) * 3;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {  // (dx, c) pairs of this input row
-      const int c = i % 3, dx = i / 3;
-      v[(dy * 2 + dx) * 3 + c] = __float2bfloat16_rn((row[i] * (1.0f / 255.0f) - mean[c]) / sd[c]);
-    }
+  const int rb = W * 3;
+  const uint8_t* src = pool + (img * H + 2 * yy) * (int64_t)rb;   // two consecutive rows
+  if (((reinterpret_cast<uintptr_t>(src) | (uintptr_t)rb) & 15) == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    for (int i = threadIdx.x; i < 2 * rb / 16; i += kGatherThreads)
+      reinterpret_cast<uint4*>(rows)[i] = __ldg(s4 + i);
+  } else {
+    for (int i = threadIdx.x; i < 2 * rb; i += kGatherThreads) rows[i] = __ldg(src + i);
   }
+  __syncthreads();
+  const float mean[3] = {m0, m1, m2}, sd[3] = {s0, s1, s2};
+  for (int xx = threadIdx.x; xx < Wo; xx += kGatherThreads) {
+    __align__(16) __nv_bfloat16 v[16];
 #pragma unroll
-  for (int e = 12; e < 16; ++e) v[e] = __float2bfloat16_rn(0.0f);
-  uint4* dst = reinterpret_cast<uint4*>(y + q * 16);
-  dst[0] = reinterpret_cast<uint4*>(v)[0];
-  dst[1] = reinterpret_cast<uint4*>(v)[1];
+    for (int dy = 0; dy < 2; ++dy) {
+      const uint8_t* row = rows + dy * rb + 2 * xx * 3;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {  // (dx, c) pairs of this input row
+        const int c = i % 3, dx = i / 3;
+        v[(dy * 2 + dx) * 3 + c] = __float2bfloat16_rn((row[i] * (1.0f / 255.0f) - mean[c]) / sd[c]);
+      }
+    }
+#pragma unroll
+    for (int e = 12; e < 16; ++e) v[e] = __float2bfloat16_rn(0.0f);
+    uint4* dst = reinterpret_cast<uint4*>(y + s2d_index(n, yy, xx, Ho, Wo, padded) * 16);
+    dst[0] = reinterpret_cast<uint4*>(v)[0];
+    dst[1] = reinterpret_cast<uint4*>(v)[1];
+  }
 }
 
 // fp32 NCHW (already normalized) -> the same space-to-depth(2) 16-channel layout.
@@ -240,7 +295,8 @@ int gg_epilogue_served(const float* logits_dev, const int32_t* count_dev, int32_
                        double* batch_confidence_dev, void* stream) {
   if (!logits_dev || !count_dev || !batch_ids_dev || B < 1 || k < 1 || ld < k)
     return GG_ERR_INVALID_ARGUMENT;
-  epilogue_served_kernel<<<(B + 7) / 8, 256, 0, gg_stream(stream)>>>(
+  if (k > kEpiThreads * kEpiPer) return GG_ERR_UNSUPPORTED;
+  epilogue_served_kernel<<<B, kEpiThreads, 0, gg_stream(stream)>>>(
       logits_dev, count_dev, k, ld, batch_ids_dev, predicted_dev, confidence_dev, probs_dev,
       batch_predicted_dev, batch_confidence_dev);
   GG_LAUNCH_OK();
@@ -252,8 +308,9 @@ int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_
                    const float* std3, int32_t padded, void* y, void* stream) {
   if (!pool || pool_size < 1 || !mean3 || !std3 || !y || B < 1 || H % 2 || W % 2)
     return GG_ERR_INVALID_ARGUMENT;
-  const int64_t pixels = (int64_t)B * (H / 2) * (W / 2);
-  stem_gather_kernel<<<(unsigned)((pixels + 255) / 256), 256, 0, gg_stream(stream)>>>(
+  if (2 * W * 3 > 48 * 1024 || B > 65535) return GG_ERR_UNSUPPORTED;
+  stem_gather_kernel<<<dim3((unsigned)(H / 2), (unsigned)B), kGatherThreads, 2 * W * 3,
+                       gg_stream(stream)>>>(
       pool, pool_size, batch_ids, count_dev, B, H, W, mean3[0], mean3[1], mean3[2], std3[0],
       std3[1], std3[2], padded, reinterpret_cast<__nv_bfloat16*>(y));
   GG_LAUNCH_OK();

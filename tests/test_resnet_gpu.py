@@ -128,3 +128,33 @@ def test_resnet18_logits_vs_eager(env, batch):
     print(f"resnet18 b={batch}: max |logit err| = {err:.3e}, logit scale {scale:.3f}, "
           f"argmax agree {(out.argmax(1) == ref.argmax(1)).float().mean().item():.3f}")
     assert err <= 2e-2 * max(1.0, scale), err
+
+
+@pytest.mark.parametrize("padded", [0, 1])
+def test_stem_gather(env, padded):
+    """uint8 HWC pool -> normalized space-to-depth(2) 16-channel input, through
+    batch ids (modulo the pool) and a device count (rows past it untouched)."""
+    torch, nat, lib = env
+    g = torch.Generator().manual_seed(5)
+    pool = torch.randint(0, 256, (5, 224, 224, 3), dtype=torch.uint8, generator=g).cuda()
+    ids = torch.tensor([3, 7, 0, 12], dtype=torch.int32, device="cuda")
+    count = torch.tensor([3], dtype=torch.int32, device="cuda")
+    mean = torch.tensor([0.485, 0.456, 0.406], dtype=torch.float32)
+    std = torch.tensor([0.229, 0.224, 0.225], dtype=torch.float32)
+    shape = (4, 115, 115, 16) if padded else (4, 112, 112, 16)
+    y = torch.full(shape, 9.0, dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_stem_gather", lib.gg_stem_gather(
+        nat.ptr(pool), 5, nat.ptr(ids), nat.ptr(count), 4, 224, 224,
+        mean.numpy().ctypes.data_as(C.c_void_p), std.numpy().ctypes.data_as(C.c_void_p), padded,
+        nat.ptr(y), nat.stream_ptr()))
+    torch.cuda.synchronize()
+    # same fp32 arithmetic as the kernel: x * fl32(1/255), then (. - mean) / std
+    imgs = pool[(ids[:3] % 5).long()].float() * torch.tensor(1.0 / 255.0, dtype=torch.float32).cuda()
+    norm = (imgs - mean.cuda()) / std.cuda()
+    s2d = norm.reshape(3, 112, 2, 112, 2, 3).permute(0, 1, 3, 2, 4, 5).reshape(3, 112, 112, 12)
+    got = y[:3, 2:-1, 2:-1] if padded else y[:3]
+    assert torch.equal(got[..., :12].float(), s2d.to(torch.bfloat16).float())
+    assert (got[..., 12:].float() == 0).all()
+    assert (y[3].float() == 9.0).all()                            # beyond the count
+    if padded:
+        assert (y[:3, :2].float() == 9.0).all()                   # borders not written
