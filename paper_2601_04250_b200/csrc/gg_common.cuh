@@ -20,6 +20,11 @@
 
 static inline cudaStream_t gg_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Programmatic dependent launch (see launch_pdl in gg_kernels.h): wait for the
+// stream predecessor's completion + memory flush / let the successor's CTAs start.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // Every fp64 operation of the controller goes through these so the rounding is
 // exactly CPython's (one IEEE rounding per binary op, no FMA contraction).
 __device__ __forceinline__ double f64_add(double a, double b) { return __dadd_rn(a, b); }

@@ -10,6 +10,7 @@
 #include <stdio.h>
 
 #include "gg_common.cuh"
+#include "gg_kernels.h"
 
 namespace gg {
 
@@ -555,6 +556,8 @@ static_assert(sizeof(SplitConsts) <= sizeof(((AdmitWorkspace*)0)->consts), "work
 
 template <int KC, int RPT, bool BD, bool SPLIT>
 __global__ void __launch_bounds__(kSmallThreads) admit_small_kernel(AdmitArgs a) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   constexpr int THREADS = kSmallThreads;
   __shared__ AdmitShared<THREADS, RPT> sm;
   __shared__ FastBlock fb_s;
@@ -681,6 +684,8 @@ __global__ void __launch_bounds__(kSmallThreads) admit_small_kernel(AdmitArgs a)
 
 // SPLIT step 0 (one thread): the launch's batch constants, once.
 __global__ void admit_prologue_kernel(AdmitArgs a) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   if (threadIdx.x != 0) return;
   SplitConsts* sc = reinterpret_cast<SplitConsts*>(a.ws->consts);
   const BatchConst b = batch_constants(a.state, a.snap, nullptr);
@@ -700,6 +705,8 @@ constexpr int kCompactRows = 8192;
 constexpr int kDecideRows = kSmallThreads * 8;   // decide tile (kSmallRpt rows per thread)
 
 __global__ void __launch_bounds__(kSmallThreads) admit_compact_kernel(AdmitArgs a, int nb_decide) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   constexpr int THREADS = kSmallThreads, WARPS = THREADS / 32;
   __shared__ int32_t out[kCompactRows];
   __shared__ int warp_off[WARPS];
@@ -821,6 +828,8 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
 }
 
 __global__ void __launch_bounds__(kLargeThreads) admit_large_kernel(AdmitArgs a) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   __shared__ AdmitShared<kLargeThreads, 1> sm;
   __shared__ double raw[2][kLargeRows][kChunk + 1];
   __shared__ double term[2][kLargeRows][kChunk + 1];
@@ -978,6 +987,8 @@ __device__ __forceinline__ bool finite_nonneg(double x) {
 
 template <bool REG>
 __global__ void __launch_bounds__(kFastThreads) admit_large_fast_kernel(AdmitArgs a) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   __shared__ AdmitShared<kFastThreads, 1> sm;
   __shared__ FastBlock fb_s;
   __shared__ uint8_t codes[kFastRows];
@@ -1273,6 +1284,8 @@ __global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, 
                                                      const double* jou, const int32_t* qd, int64_t n,
                                                      int set_qd, int64_t* err, const double* slots,
                                                      int G, int B, int rank, gg_fifo* fifo) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   outcome_seq<S>(p, st, lat, jou, qd, n, set_qd, err, slots, G, B, rank, fifo);
 }
 
@@ -1295,6 +1308,8 @@ template <int S>
 __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
     gg_params p, gg_state* st, const double* lat, const double* jou, const int32_t* qd, int64_t n,
     int set_qd, int64_t* err, const double* slots, int G, int B, int rank, gg_fifo* fifo) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   __shared__ double seq[GG_P95_WINDOW_MAX + kOutChunk];   // window history ++ chunk latencies
   __shared__ double sj[kOutChunk];
   __shared__ int32_t sq[kOutChunk];
@@ -1729,10 +1744,10 @@ static int launch_outcome(const gg_params& p, gg_state* st, const double* lat, c
 #define GG_OUTCOME(SLOTS)                                                                        \
   do {                                                                                           \
     if (par)                                                                                     \
-      outcome_par_kernel<SLOTS><<<1, kOutThreads, 0, s>>>(p, st, lat, jou, qd, n, set_qd, err, slots, \
+      GG_PDL_LAUNCH((outcome_par_kernel<SLOTS>), 1, kOutThreads, 0, s, p, st, lat, jou, qd, n, set_qd, err, slots, \
                                                           G, B, rank, fifo);                     \
     else                                                                                         \
-      outcome_kernel<SLOTS><<<1, 32, 0, s>>>(p, st, lat, jou, qd, n, set_qd, err, slots, G, B,   \
+      GG_PDL_LAUNCH((outcome_kernel<SLOTS>), 1, 32, 0, s, p, st, lat, jou, qd, n, set_qd, err, slots, G, B,   \
                                              rank, fifo);                                        \
   } while (0)
   if (w <= 32) GG_OUTCOME(1);
@@ -1800,15 +1815,15 @@ static int launch_admit(const AdmitArgs& args, void* stream) {
       a.super_cnt = a.split_cnt + nb;
     }
     if (split) {
-      admit_prologue_kernel<<<1, 32, 0, s>>>(a);
+      GG_PDL_LAUNCH((admit_prologue_kernel), 1, 32, 0, s, a);
       GG_LAUNCH_OK();
     }
 #define GG_SMALL(KC)                                                                        \
   do {                                                                                      \
-    if (bd && split) admit_small_kernel<KC, kSmallRpt, true, true><<<g, kSmallThreads, 0, s>>>(a);    \
-    else if (bd) admit_small_kernel<KC, kSmallRpt, true, false><<<g, kSmallThreads, 0, s>>>(a);      \
-    else if (split) admit_small_kernel<KC, kSmallRpt, false, true><<<g, kSmallThreads, 0, s>>>(a);   \
-    else admit_small_kernel<KC, kSmallRpt, false, false><<<g, kSmallThreads, 0, s>>>(a);             \
+    if (bd && split) GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, true, true>), g, kSmallThreads, 0, s, a);    \
+    else if (bd) GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, true, false>), g, kSmallThreads, 0, s, a);      \
+    else if (split) GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, false, true>), g, kSmallThreads, 0, s, a);   \
+    else GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, false, false>), g, kSmallThreads, 0, s, a);             \
   } while (0)
     if (k == 2 && aligned16) GG_SMALL(2);
     else if (k == 4 && aligned16) GG_SMALL(4);
@@ -1816,17 +1831,17 @@ static int launch_admit(const AdmitArgs& args, void* stream) {
 #undef GG_SMALL
     if (split) {
       GG_LAUNCH_OK();
-      admit_compact_kernel<<<(unsigned)((n + kCompactRows - 1) / kCompactRows), kSmallThreads, 0, s>>>(
+      GG_PDL_LAUNCH((admit_compact_kernel), (unsigned)((n + kCompactRows - 1) / kCompactRows), kSmallThreads, 0, s, 
           a, (int)nb);
     }
   } else if (!bd && !getenv("GG_ADMIT_EXACT_ONLY")) {
     const unsigned g = (unsigned)((n + kFastRows - 1) / kFastRows > 0 ? (n + kFastRows - 1) / kFastRows : 1);
     if (k <= kRegChunks * 32)
-      admit_large_fast_kernel<true><<<g, kFastThreads, 0, s>>>(a);
+      GG_PDL_LAUNCH((admit_large_fast_kernel<true>), g, kFastThreads, 0, s, a);
     else
-      admit_large_fast_kernel<false><<<g, kFastThreads, 0, s>>>(a);
+      GG_PDL_LAUNCH((admit_large_fast_kernel<false>), g, kFastThreads, 0, s, a);
   } else {
-    admit_large_kernel<<<(unsigned)nb, kLargeThreads, 0, s>>>(a);
+    GG_PDL_LAUNCH((admit_large_kernel), (unsigned)nb, kLargeThreads, 0, s, a);
   }
   GG_LAUNCH_OK();
   return GG_OK;

@@ -96,9 +96,9 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int M = ep.count ? min(sh.M, __ldg(ep.count) * sh.Ho * sh.Wo) : sh.M;
-  const int tiles_m = (M + 127) / 128, tiles_n = sh.Cout / BN;
-  const int num_tiles = tiles_m * tiles_n;
+  griddep_launch();   // the successor may begin its prologue as SMs free up
+  const int tiles_n = sh.Cout / BN;
+  const bool b_loaded = MODE != 0 && sh.bres && (sh.M + 127) / 128 * tiles_n > (int)blockIdx.x;
 
   if (threadIdx.x == 0) {
     mbar_init(b_full, 1);
@@ -115,21 +115,24 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     tma_prefetch(&map_w);
   }
   if (warp == kConvProdWarps) tmem_alloc(tmem_slot, 2 * BN);
+  if (b_loaded && threadIdx.x == 0) {   // weights: independent of the predecessor
+    mbar_expect_tx(b_full, num_kb * L::B_BYTES);
+    for (int kb = 0; kb < num_kb; ++kb) tma_load_2d(bres + kb * L::B_BYTES, &map_w, b_full, kb * 64, 0);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();   // activations, residual, count and output follow the predecessor
+  const int M = ep.count ? min(sh.M, __ldg(ep.count) * sh.Ho * sh.Wo) : sh.M;
+  const int tiles_m = (M + 127) / 128;
+  const int num_tiles = tiles_m * tiles_n;
 
   if (MODE != 0 && warp < kConvProdWarps) {
     // ===== TMA producer (im2col A + tiled B) =====
     if (threadIdx.x == 0) {
       tma_prefetch(&map_x);
       const int cblocks = sh.C / 64;
-      if (sh.bres && num_tiles > (int)blockIdx.x) {
-        mbar_expect_tx(b_full, num_kb * L::B_BYTES);
-        for (int kb = 0; kb < num_kb; ++kb)
-          tma_load_2d(bres + kb * L::B_BYTES, &map_w, b_full, kb * 64, 0);
-      }
       int it = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int tm = tile % tiles_m, tn = tile / tiles_m;
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
       int it = 0, t = 0;
-      if (sh.bres && num_tiles > (int)blockIdx.x) mbar_wait(b_full, 0);
+      if (b_loaded) mbar_wait(b_full, 0);   // also when the count leaves no tile: drain
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
         const int acc = t & 1;
         const uint32_t use = t >> 1;
@@ -333,8 +336,8 @@ static int launch_conv(const __nv_bfloat16* x, const CUtensorMap& mw, const CUte
   const int grid = tiles < num_sms() ? tiles : num_sms();
   const int smem = sh.bres ? sh.bres_stages * L::STAGE_BYTES + (sh.Kpad / 64) * L::B_BYTES + 256 + 1024
                            : L::TOTAL;
-  kern<<<grid, kConvThreads, smem, s>>>(x, mw, mx, sh, ep);
-  GG_LAUNCH_OK();
+  if (launch_pdl(kern, dim3(grid), dim3(kConvThreads), smem, s, x, mw, mx, sh, ep) != cudaSuccess)
+    return GG_ERR_CUDA;
   return GG_OK;
 }
 
@@ -387,6 +390,8 @@ __global__ void nchw_to_nhwc_pad(const float* __restrict__ in, __nv_bfloat16* __
 __global__ void maxpool3x3s2(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
                              int N, int H, int W, int C, int Ho, int Wo, const int32_t* count,
                              int out_pad) {
+  griddep_wait();
+  griddep_launch();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int cg = C / 8;
   if (count) N = min(N, __ldg(count));
@@ -429,6 +434,8 @@ __global__ void __launch_bounds__(256) avgpool_global(const __nv_bfloat16* __res
                                                       __nv_bfloat16* __restrict__ out, int N,
                                                       int HW, int C, const int32_t* count,
                                                       int denom) {
+  griddep_wait();
+  griddep_launch();
   if (count) N = min(N, __ldg(count));
   const int n = blockIdx.y;
   if (n >= N) return;
@@ -563,9 +570,10 @@ extern "C" int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, i
   if (!x || !y || C % 8) return GG_ERR_INVALID_ARGUMENT;
   const int Ho = (H + 2 - 3) / 2 + 1, Wo = (W + 2 - 3) / 2 + 1;
   const int64_t work = (int64_t)N * Ho * Wo * (C / 8);
-  maxpool3x3s2<<<(unsigned)((work + 255) / 256), 256, 0, gg_stream(stream)>>>(
+  if (launch_pdl(maxpool3x3s2, dim3((unsigned)((work + 255) / 256)), dim3(256), 0, gg_stream(stream),
       reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, H, W, C,
-      Ho, Wo, count_dev, out_pad);
+      Ho, Wo, count_dev, out_pad) != cudaSuccess)
+    return GG_ERR_CUDA;
   GG_LAUNCH_OK();
   return GG_OK;
 }
@@ -574,9 +582,10 @@ extern "C" int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void*
                           int32_t denom, const int32_t* count_dev, void* stream) {
   if (!x || !y || C % 8 || denom < 0 || N < 1) return GG_ERR_INVALID_ARGUMENT;
   if (C % 64 || N > 65535) return GG_ERR_UNSUPPORTED;
-  avgpool_global<<<dim3((unsigned)(C / 64), (unsigned)N), 256, 0, gg_stream(stream)>>>(
+  if (launch_pdl(avgpool_global, dim3((unsigned)(C / 64), (unsigned)N), dim3(256), 0, gg_stream(stream),
       reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, HW, C,
-      count_dev, denom);
+      count_dev, denom) != cudaSuccess)
+    return GG_ERR_CUDA;
   GG_LAUNCH_OK();
   return GG_OK;
 }

@@ -113,11 +113,9 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     ep.prof[2 * blockIdx.x] = gtimer();
     ep.prof[2048 + 2 * blockIdx.x] = clock64();
   }
+  griddep_launch();   // the successor may begin its prologue as SMs free up
   const int img = sh.Hp * sh.Wp;
-  const int n_eff = ep.count ? min(sh.N, __ldg(ep.count)) : sh.N;
-  const int Mtot = n_eff * img;
-  const int tiles_m = (Mtot + BM - 1) / BM, tiles_n = sh.Cout / BN;
-  const int num_tiles = tiles_m * tiles_n;
+  const int tiles_n = sh.Cout / BN;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSpanMaxStages; ++i) {
@@ -136,17 +134,27 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     tma_prefetch(&map_w);
   }
   if (warp == 1) tmem_alloc(tmem_slot, 2 * ACC_COLS);
+  // the weight slab does not depend on the predecessor: start it before the wait
+  if (warp == 0 && lane == 0 && sh.bres) {
+    const int tiles_max = (sh.N * img + BM - 1) / BM * tiles_n;
+    if (tiles_max > (int)blockIdx.x) {
+      mbar_expect_tx(bres_full, nkb * B_BYTES);
+      for (int kb = 0; kb < nkb; ++kb) tma_load_2d(b_base + kb * B_BYTES, &map_w, bres_full, kb * CH, 0);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();   // activations, residual, count and output all follow the predecessor
+  const int n_eff = ep.count ? min(sh.N, __ldg(ep.count)) : sh.N;
+  const int Mtot = n_eff * img;
+  const int tiles_m = (Mtot + BM - 1) / BM;
+  const int num_tiles = tiles_m * tiles_n;
+  const bool b_loaded = sh.bres && (sh.N * img + BM - 1) / BM * tiles_n > (int)blockIdx.x;
 
   if (warp == 0) {
     if (lane == 0) {
-      if (sh.bres && num_tiles > (int)blockIdx.x) {
-        mbar_expect_tx(bres_full, nkb * B_BYTES);
-        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(b_base + kb * B_BYTES, &map_w, bres_full, kb * CH, 0);
-      }
       int ait = 0, bit = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int tm = tile % tiles_m, tn = tile / tiles_m;
@@ -178,7 +186,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
       for (int tap = 0; tap < TAPS; ++tap)
         tap_off[tap] = (uint64_t)(((tap / RT) * sh.Wp + tap % RT) * (RB / 16));
-      if (sh.bres && num_tiles > (int)blockIdx.x) mbar_wait(bres_full, 0);
+      if (b_loaded) mbar_wait(bres_full, 0);   // also when the count leaves no tile: drain the TMA
       const uint64_t bres_desc = sdesc_sw(smem_u32(b_base), RB);
       int ait = 0, bit = 0, t = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
@@ -383,8 +391,8 @@ static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanS
   static int prof_calls = 0;
   const int prof_at = do_prof ? atoi(getenv("GG_SPAN_PROF")) : 0;
   const bool report = do_prof && ++prof_calls >= (prof_at > 0 ? prof_at : 1);
-  kern<<<grid, kSpanThreads, smem, s>>>(mx, mw, sh, e2);
-  GG_LAUNCH_OK();
+  if (launch_pdl(kern, dim3(grid), dim3(kSpanThreads), smem, s, mx, mw, sh, e2) != cudaSuccess)
+    return GG_ERR_CUDA;
   if (report) {
     prof_calls = 0;
     static unsigned long long h[8 * 1024];

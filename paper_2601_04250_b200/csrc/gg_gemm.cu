@@ -70,10 +70,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // dynamic batch: the admitted count is read on the device (no host round-trip)
-  const int M = ep.count ? min(M_max, __ldg(ep.count) * ep.rows_per_item) : M_max;
-  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
-  const int num_tiles = tiles_m * tiles_n;
+  griddep_launch();   // the successor may begin its prologue as SMs free up
   const int num_kb = K / kBK;
 
   if (threadIdx.x == 0) {
@@ -94,6 +91,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
+  griddep_wait();   // operands, count and output follow the stream predecessor
+  // dynamic batch: the admitted count is read on the device (no host round-trip)
+  const int M = ep.count ? min(M_max, __ldg(ep.count) * ep.rows_per_item) : M_max;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
 
   if (warp == 0) {
     // ===== TMA producer =====
@@ -298,7 +300,8 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  kern<<<grid, kThreads, L::TOTAL, s>>>(ma, mb, M, N, K, ep);
+  if (launch_pdl(kern, dim3(grid), dim3(kThreads), (size_t)L::TOTAL, s, ma, mb, M, N, K, ep) != cudaSuccess)
+    return GG_ERR_CUDA;
   GG_LAUNCH_OK();
   return GG_OK;
 }

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 
 #include "gg_common.cuh"
+#include "gg_kernels.h"
 
 namespace gg {
 
@@ -16,6 +17,8 @@ __device__ __forceinline__ uint64_t now_ns() {
 // One block: n = min(B, depth); copy the ring slots [head, head+n) out.
 __global__ void fifo_pop_kernel(gg_fifo* f, const int32_t* ring, const uint64_t* ring_ns,
                                 int32_t* ids, uint64_t* ns, int32_t* count, int B) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   __shared__ int64_t head_s, n_s;
   if (threadIdx.x == 0) {
     const int64_t depth = f->tail - f->head;
@@ -44,6 +47,8 @@ __global__ void fifo_pop_kernel(gg_fifo* f, const int32_t* ring, const uint64_t*
 __global__ void served_outcomes_kernel(const gg_fifo* f, const int32_t* count, const uint64_t* ns,
                                        gg_outcome_model m, const gg_batch_info* info, double* slot,
                                        int B) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   const int n = *count;
   const int64_t depth = f->tail - f->head;            // after the pop
   const double qd = (double)(depth + f->extra_depth);
@@ -95,6 +100,8 @@ __global__ void __launch_bounds__(kEpiThreads) epilogue_served_kernel(const floa
                                                                      int32_t* pred, double* conf,
                                                                      double* probs, int32_t* bpred,
                                                                      double* bconf) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   __shared__ float red_m[kEpiThreads / 32];
   __shared__ double red_s[kEpiThreads / 32];
   __shared__ double red_b[kEpiThreads / 32];
@@ -186,6 +193,8 @@ __global__ void __launch_bounds__(kGatherThreads) stem_gather_kernel(
     const uint8_t* __restrict__ pool, int64_t pool_size, const int32_t* ids, const int32_t* count,
     int B, int H, int W, float m0, float m1, float m2, float s0, float s1, float s2, int padded,
     __nv_bfloat16* __restrict__ y) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   extern __shared__ __align__(16) uint8_t rows[];   // [2][W * 3]
   const int n_valid = count ? min(B, __ldg(count)) : B;
   const int n = blockIdx.y, yy = blockIdx.x;
@@ -251,6 +260,8 @@ __global__ void nchw_to_s2d16_kernel(const float* __restrict__ x, int N, int H, 
 __global__ void token_gather_kernel(const int32_t* pool_ids, const int32_t* pool_mask,
                                     int64_t pool_size, const int32_t* ids, const int32_t* count,
                                     int B, int S, int32_t* out_ids, int32_t* out_mask) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   const int n_valid = count ? min(B, __ldg(count)) : B;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)n_valid * S) return;
@@ -270,7 +281,7 @@ int gg_fifo_pop(gg_fifo* fifo_dev, const int32_t* ring_ids_dev, const uint64_t* 
                 int32_t* batch_ids_dev, uint64_t* batch_ns_dev, int32_t* count_dev, int32_t B,
                 void* stream) {
   if (!fifo_dev || !ring_ids_dev || !batch_ids_dev || !count_dev || B < 1) return GG_ERR_INVALID_ARGUMENT;
-  fifo_pop_kernel<<<1, 256, 0, gg_stream(stream)>>>(fifo_dev, ring_ids_dev, ring_ns_dev,
+  GG_PDL_LAUNCH((fifo_pop_kernel), 1, 256, 0, gg_stream(stream), fifo_dev, ring_ids_dev, ring_ns_dev,
                                                     batch_ids_dev, batch_ns_dev, count_dev, B);
   GG_LAUNCH_OK();
   return GG_OK;
@@ -283,7 +294,7 @@ int gg_served_outcomes(const gg_fifo* fifo_dev, const int32_t* count_dev,
   if (model->batch_base_ms < 0 || model->per_item_ms < 0 || model->batch_base_energy_j < 0 ||
       model->per_item_energy_j < 0)
     return GG_ERR_NEGATIVE_MEASUREMENT;
-  served_outcomes_kernel<<<1, 256, 0, gg_stream(stream)>>>(fifo_dev, count_dev, batch_ns_dev,
+  GG_PDL_LAUNCH((served_outcomes_kernel), 1, 256, 0, gg_stream(stream), fifo_dev, count_dev, batch_ns_dev,
                                                            *model, info_dev, slot_dev, B);
   GG_LAUNCH_OK();
   return GG_OK;
@@ -296,7 +307,7 @@ int gg_epilogue_served(const float* logits_dev, const int32_t* count_dev, int32_
   if (!logits_dev || !count_dev || !batch_ids_dev || B < 1 || k < 1 || ld < k)
     return GG_ERR_INVALID_ARGUMENT;
   if (k > kEpiThreads * kEpiPer) return GG_ERR_UNSUPPORTED;
-  epilogue_served_kernel<<<B, kEpiThreads, 0, gg_stream(stream)>>>(
+  GG_PDL_LAUNCH((epilogue_served_kernel), B, kEpiThreads, 0, gg_stream(stream), 
       logits_dev, count_dev, k, ld, batch_ids_dev, predicted_dev, confidence_dev, probs_dev,
       batch_predicted_dev, batch_confidence_dev);
   GG_LAUNCH_OK();
@@ -309,8 +320,7 @@ int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_
   if (!pool || pool_size < 1 || !mean3 || !std3 || !y || B < 1 || H % 2 || W % 2)
     return GG_ERR_INVALID_ARGUMENT;
   if (2 * W * 3 > 48 * 1024 || B > 65535) return GG_ERR_UNSUPPORTED;
-  stem_gather_kernel<<<dim3((unsigned)(H / 2), (unsigned)B), kGatherThreads, 2 * W * 3,
-                       gg_stream(stream)>>>(
+  GG_PDL_LAUNCH((stem_gather_kernel), dim3((unsigned)(H / 2), (unsigned)B), kGatherThreads, 2 * W * 3, gg_stream(stream), 
       pool, pool_size, batch_ids, count_dev, B, H, W, mean3[0], mean3[1], mean3[2], std3[0],
       std3[1], std3[2], padded, reinterpret_cast<__nv_bfloat16*>(y));
   GG_LAUNCH_OK();
@@ -333,7 +343,7 @@ int gg_token_gather(const int32_t* pool_ids, const int32_t* pool_mask, int64_t p
   if (!pool_ids || pool_size < 1 || !batch_ids || !ids || B < 1 || seq_len < 1)
     return GG_ERR_INVALID_ARGUMENT;
   const int64_t tokens = (int64_t)B * seq_len;
-  token_gather_kernel<<<(unsigned)((tokens + 255) / 256), 256, 0, gg_stream(stream)>>>(
+  GG_PDL_LAUNCH((token_gather_kernel), (unsigned)((tokens + 255) / 256), 256, 0, gg_stream(stream), 
       pool_ids, pool_mask, pool_size, batch_ids, count_dev, B, seq_len, ids, mask);
   GG_LAUNCH_OK();
   return GG_OK;
