@@ -112,7 +112,10 @@ int gg_nchw_to_nhwc(const float* x, int32_t N, int32_t C, int32_t H, int32_t W, 
  * (y[n, i, j, (dy*2+dx)*3 + c] = x[n, c, 2i+dy, 2j+dx]; channels 12..15 = 0).
  * ResNet-18's 7x7/2 stem conv equals a 4x4/1 conv (pad 2 / 1) over it.
  * padded = 1: write the interior of a zero-bordered [N, H/2+3, W/2+3, 16]
- * buffer at (+2, +2) — the input layout of gg_stem_s2d_span. */
+ * buffer at (+2, +2) — the input layout of gg_stem_s2d_span — PRE-SWIZZLED:
+ * cell q (linear index in the padded buffer) has its two 16-byte halves
+ * (channels 0-7 / 8-15) swapped when bit 2 of q is set, so that a linear copy
+ * into shared memory is the tensor core's SWIZZLE_32B operand layout. */
 int gg_nchw_to_s2d16(const float* x, int32_t N, int32_t H, int32_t W, int32_t padded, void* y,
                      void* stream);
 /* ResNet-18 stem (conv1 + bn1 + relu) as a span convolution: 4x4 / 1 over the

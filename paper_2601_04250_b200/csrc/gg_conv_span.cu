@@ -68,6 +68,8 @@ struct SpanEpi {
   int relu;
   const int32_t* count;
   unsigned long long* prof;   // debug (GG_SPAN_PROF): per-CTA globaltimer start / end
+  const __nv_bfloat16* x16;   // CH == 16: the pre-swizzled input (bulk-copied)
+  int nostore;                // debug (GG_SPAN_NOSTORE): skip the output stores
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -165,9 +167,19 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
           if (ep.prof && blockIdx.x == 0 && cb == 0 && ait / cblocks < 16)
             ep.prof[4096 + (ait / cblocks) * 8 + 0] = clock64();
           uint8_t* sa = a_base + as * sh.a_stage_bytes;
-          mbar_expect_tx(&a_full[as], sh.boxes * sh.box_rows * RB);
-          for (int bx = 0; bx < sh.boxes; ++bx)   // boxes of <= 256 rows (TMA limit)
-            tma_load_2d(sa + bx * sh.box_rows * RB, &map_x, &a_full[as], cb * CH, m0 + bx * sh.box_rows);
+          if constexpr (CH == 16) {
+            // the 16-channel input is stored pre-swizzled (gg_stem_gather / gg_nchw_to_s2d16,
+            // padded): one linear bulk copy of the span reproduces the SW32 image
+            // (rows past the buffer end only feed discarded outputs)
+            const int64_t rows_left = (int64_t)sh.N * img - m0;
+            const int rows = rows_left < sh.span_rows ? (int)rows_left : sh.span_rows;
+            mbar_expect_tx(&a_full[as], rows * RB);
+            bulk_load(sa, ep.x16 + (int64_t)m0 * CH, rows * RB, &a_full[as]);
+          } else {
+            mbar_expect_tx(&a_full[as], sh.boxes * sh.box_rows * RB);
+            for (int bx = 0; bx < sh.boxes; ++bx)   // boxes of <= 256 rows (TMA limit)
+              tma_load_2d(sa + bx * sh.box_rows * RB, &map_x, &a_full[as], cb * CH, m0 + bx * sh.box_rows);
+          }
           if (!sh.bres) {
             for (int tap = 0; tap < TAPS; ++tap, ++bit) {
               const int bs = bit % BST;
@@ -310,6 +322,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = 0.0f;   // padding positions stay zero
           }
+          if (ep.nostore) continue;
           uint4* dp = reinterpret_cast<uint4*>(ep.y + oidx * sh.Cout + col0);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -381,6 +394,7 @@ static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanS
   const int tiles = ((sh.N * sh.Hp * sh.Wp + 128 * MT - 1) / (128 * MT)) * (sh.Cout / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   SpanEpi e2 = ep;
+  e2.nostore = getenv("GG_SPAN_NOSTORE") != nullptr;
   static unsigned long long* prof = nullptr;
   const bool do_prof = getenv("GG_SPAN_PROF") != nullptr;
   if (do_prof) {
@@ -515,7 +529,7 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
   if (!rc) rc = make_map_span(&mw, w, Cout, (int64_t)C * 9, 64, best_bn);
   if (rc) return rc;
   SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
-             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr};
+             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0};
   cudaStream_t s = gg_stream(stream);
   switch (best_bn * 4 + best_mt) {
     case 256 * 4 + 1: return launch_span<256, 64, 3, false, 1>(mx, mw, sh, ep, s);
@@ -543,6 +557,8 @@ extern "C" int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws
   int rc = make_map_span(&mx, x, Mtot, 16, 16, sh.box_rows);
   if (!rc) rc = make_map_span(&mw, w, Cout, 256, 16, 64);
   if (rc) return rc;
-  SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, relu, count_dev, nullptr};
+  SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, relu, count_dev, nullptr,
+             reinterpret_cast<const __nv_bfloat16*>(x), 0};
+  if (reinterpret_cast<uintptr_t>(x) & 15) return GG_ERR_INVALID_ARGUMENT;
   return launch_span<64, 16, 4, true, 1>(mx, mw, sh, ep, gg_stream(stream));
 }

@@ -183,6 +183,18 @@ __device__ __forceinline__ int64_t s2d_index(int n, int yy, int xx, int Ho, int 
   return ((int64_t)n * (Ho + 3) + yy + 2) * (Wo + 3) + xx + 2;
 }
 
+// Store one 32-byte s2d cell.  The padded layout is pre-swizzled for the span
+// stem's SWIZZLE_32B operand: cell q keeps its two 16-byte halves swapped when
+// bit 2 of q is set (smem address bit 7 of row q within a 256-B atom), so a
+// linear bulk copy of any 8-row-aligned span lands as the swizzled tile.
+__device__ __forceinline__ void store_s2d_cell(__nv_bfloat16* y, int64_t q, const uint4& lo,
+                                               const uint4& hi, int padded) {
+  uint4* dst = reinterpret_cast<uint4*>(y + q * 16);
+  const bool swap = padded && ((q >> 2) & 1);
+  dst[0] = swap ? hi : lo;
+  dst[1] = swap ? lo : hi;
+}
+
 // One block per (image, s2d row): the two source image rows (2 x W x 3 bytes)
 // are staged in shared memory with 16-byte loads when aligned, then each thread
 // builds s2d pixels from shared memory and writes 32 contiguous bytes
@@ -225,9 +237,8 @@ __global__ void __launch_bounds__(kGatherThreads) stem_gather_kernel(
     }
 #pragma unroll
     for (int e = 12; e < 16; ++e) v[e] = __float2bfloat16_rn(0.0f);
-    uint4* dst = reinterpret_cast<uint4*>(y + s2d_index(n, yy, xx, Ho, Wo, padded) * 16);
-    dst[0] = reinterpret_cast<uint4*>(v)[0];
-    dst[1] = reinterpret_cast<uint4*>(v)[1];
+    store_s2d_cell(y, s2d_index(n, yy, xx, Ho, Wo, padded), reinterpret_cast<uint4*>(v)[0],
+                   reinterpret_cast<uint4*>(v)[1], padded);
   }
 }
 
@@ -252,9 +263,7 @@ __global__ void nchw_to_s2d16_kernel(const float* __restrict__ x, int N, int H, 
             __float2bfloat16_rn(__ldg(x + (((int64_t)n * 3 + c) * H + 2 * yy + dy) * W + 2 * xx + dx));
 #pragma unroll
   for (int e = 12; e < 16; ++e) v[e] = __float2bfloat16_rn(0.0f);
-  uint4* dst = reinterpret_cast<uint4*>(y + q * 16);
-  dst[0] = reinterpret_cast<uint4*>(v)[0];
-  dst[1] = reinterpret_cast<uint4*>(v)[1];
+  store_s2d_cell(y, q, reinterpret_cast<uint4*>(v)[0], reinterpret_cast<uint4*>(v)[1], padded);
 }
 
 __global__ void token_gather_kernel(const int32_t* pool_ids, const int32_t* pool_mask,

@@ -152,6 +152,10 @@ def test_stem_gather(env, padded):
     imgs = pool[(ids[:3] % 5).long()].float() * torch.tensor(1.0 / 255.0, dtype=torch.float32).cuda()
     norm = (imgs - mean.cuda()) / std.cuda()
     s2d = norm.reshape(3, 112, 2, 112, 2, 3).permute(0, 1, 3, 2, 4, 5).reshape(3, 112, 112, 12)
+    if padded:   # undo the SW32 pre-swizzle: cells with bit 2 of the linear index set are swapped
+        q = torch.arange(115 * 115 * 4, device="cuda").reshape(4, 115, 115)
+        sw = ((q >> 2) & 1).bool()
+        y = torch.where(sw[..., None], torch.cat([y[..., 8:], y[..., :8]], dim=-1), y)
     got = y[:3, 2:-1, 2:-1] if padded else y[:3]
     assert torch.equal(got[..., :12].float(), s2d.to(torch.bfloat16).float())
     assert (got[..., 12:].float() == 0).all()
