@@ -57,6 +57,18 @@ typedef struct {
 int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
             int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* epilogue, void* stream);
 
+/* Allocate this device's stream-K workspace (48 MB fp32 partial tiles + 2 MB
+ * counters) now, outside any CUDA graph capture.  gg_gemm / gg_conv2d split
+ * their (tile, k-block) space evenly over the SMs when the tile count leaves a
+ * partly empty last wave; inside a capture without a reserved workspace they
+ * run data-parallel.  One stream per device at a time (like the activations). */
+int gg_streamk_reserve(void);
+/* Stream-K policy: 0 = never (default: on B200 the fixup's partial-tile reads
+ * cost more than the last-wave imbalance they remove at the DistilBERT / ResNet
+ * shapes), -1 = by the wave model, 1 = whenever the grid has >= 2 k-blocks per
+ * SM (tests).  Returns the previous policy. */
+int gg_streamk_mode(int32_t mode);
+
 /* Multi-head self-attention for head dim 64 on the GG_OUT_QKV_HEADS planes:
  * ctx[b*S + s, h*64 + d] = softmax(Q K^T + mask) V, one CTA per (b, h), both
  * products on tcgen05 with the scores and the output in TMEM.  mask: int32

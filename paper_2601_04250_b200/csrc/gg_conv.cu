@@ -17,6 +17,7 @@
 
 #include "gg_common.cuh"
 #include "gg_kernels.h"
+#include "gg_streamk.cuh"
 #include "gg_tc.cuh"
 
 namespace gg {
@@ -40,6 +41,7 @@ struct ConvEpi {
   int relu;
   const int32_t* count;           // device image count (dynamic batch) or null
   int out_pad;                    // 1: y (and residual) are [N, Ho+2, Wo+2, Cout] zero-bordered
+  StreamK sk;                     // stream-K split (TMA im2col mode only), or disabled
 };
 
 constexpr int kConvProdWarps = 4;
@@ -98,7 +100,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   griddep_launch();   // the successor may begin its prologue as SMs free up
   const int tiles_n = sh.Cout / BN;
-  const bool b_loaded = MODE != 0 && sh.bres && (sh.M + 127) / 128 * tiles_n > (int)blockIdx.x;
+  const bool b_loaded = MODE != 0 && sh.bres &&
+                        (ep.sk.enabled || (sh.M + 127) / 128 * tiles_n > (int)blockIdx.x);
 
   if (threadIdx.x == 0) {
     mbar_init(b_full, 1);
@@ -134,14 +137,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       tma_prefetch(&map_x);
       const int cblocks = sh.C / 64;
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int tm = tile % tiles_m, tn = tile / tiles_m;
+      SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
+      SkWork w;
+      while (sc.next(w)) {
+        const int tm = w.tile % tiles_m, tn = w.tile / tiles_m;
         const int m0 = tm * 128;
         const int n0 = m0 / (sh.Ho * sh.Wo);
         const int rem = m0 - n0 * sh.Ho * sh.Wo;
         const int ho0 = rem / sh.Wo, wo0 = rem - (rem / sh.Wo) * sh.Wo;
         const int wc = wo0 * sh.stride - sh.pad, hc = ho0 * sh.stride - sh.pad;
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
           const int s = it % nst;
           mbar_wait(&empty[s], ((it / nst) & 1) ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
@@ -225,13 +230,15 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
       int it = 0, t = 0;
       if (b_loaded) mbar_wait(b_full, 0);   // also when the count leaves no tile: drain
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+      SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
+      SkWork w;
+      for (; sc.next(w); ++t) {
         const int acc = t & 1;
         const uint32_t use = t >> 1;
         mbar_wait(&acc_empty[acc], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
           const int s = it % nst;
           mbar_wait(&full[s], (it / nst) & 1);
           tc_fence_after();
@@ -241,7 +248,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           for (int kk = 0; kk < 4; ++kk)
             umma_bf16(d_tmem, MODE == 2 ? sdesc_k_sw32(sa + kk * 4096) : sdesc_k_sw128(sa + kk * 32),
                       sdesc_k_sw128(sb + kk * 32), idesc,
-                      (kb | kk) != 0);
+                      (kb != w.kb0 || kk != 0));
           umma_commit(&empty[s]);
         }
         umma_commit(&acc_full[acc]);
@@ -251,11 +258,31 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // ===== epilogue =====
     const int quarter = warp & 3;
     int t = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
-      const int tm = tile % tiles_m, tn = tile / tiles_m;
+    SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
+    SkWork w;
+    for (; sc.next(w); ++t) {
+      const int tm = w.tile % tiles_m, tn = w.tile / tiles_m;
       const int acc = t & 1;
       mbar_wait(&acc_full[acc], (t >> 1) & 1);
       tc_fence_after();
+      const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      const bool partial = w.kb0 != 0 || w.kb1 != num_kb;
+      SkFix fx;
+      if (partial) {   // stream-K: the last arriving segment reduces and stores the tile
+        auto load32 = [&](int c, float (&v)[32]) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tacc + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        };
+        if (!sk_arrive<BN>(ep.sk, sc, w, warp - kConvProdWarps - 1, 4, lane, fx, load32)) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[acc]);
+          continue;
+        }
+      }
       const int m = tm * 128 + quarter * 32 + lane;
       const bool ok = m < M;
       int64_t oidx = m;   // output row: dense, or inside a zero-bordered [Ho+2, Wo+2] layout
@@ -267,18 +294,21 @@ __global__ void __launch_bounds__(kConvThreads, 1)
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
+        tmem_ld_32x32b_x32(tacc + c, r);
         tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (partial) sk_sum<BN>(ep.sk, sc, w, warp - kConvProdWarps - 1, 4, lane, fx, c, v);
         if (!ok) continue;
         const int col0 = tn * BN + c;
-        float v[32];
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
           const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + i));
-          v[i] = __uint_as_float(r[i]) + b.x;
-          v[i + 1] = __uint_as_float(r[i + 1]) + b.y;
-          v[i + 2] = __uint_as_float(r[i + 2]) + b.z;
-          v[i + 3] = __uint_as_float(r[i + 3]) + b.w;
+          v[i] += b.x;
+          v[i + 1] += b.y;
+          v[i + 2] += b.z;
+          v[i + 3] += b.w;
         }
         if (ep.residual) {
           const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + oidx * sh.Cout + col0);
@@ -333,7 +363,7 @@ static int launch_conv(const __nv_bfloat16* x, const CUtensorMap& mw, const CUte
     attr = true;
   }
   const int tiles = ((sh.M + 127) / 128) * (sh.Cout / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
+  const int grid = ep.sk.enabled ? num_sms() : (tiles < num_sms() ? tiles : num_sms());
   const int smem = sh.bres ? sh.bres_stages * L::STAGE_BYTES + (sh.Kpad / 64) * L::B_BYTES + 256 + 1024
                            : L::TOTAL;
   if (launch_pdl(kern, dim3(grid), dim3(kConvThreads), smem, s, x, mw, mx, sh, ep) != cudaSuccess)
@@ -493,7 +523,8 @@ extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t
   if (M > 0x7fffffff) return GG_ERR_UNSUPPORTED;
   sh.M = (int)M;
   ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
-             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, out_pad};
+             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, out_pad,
+             StreamK{nullptr, nullptr, 0}};
   // N tile: minimize the larger of (tensor time of the busiest SM) and (operand
   // bytes streamed from L2: every tile re-reads its A rows and its B columns per
   // k-block).  Measured on B200: ~8 TB/s of TMA operand traffic, MMA 128xBN x K16
@@ -534,6 +565,12 @@ extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t
   }
   cudaStream_t s = gg_stream(stream);
   const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  if (mode == 1 && streamk_wanted(tiles_m * (Cout / bn), nkb, num_sms())) {
+    bool ok = false;
+    StreamK sk = streamk_workspace(s, (int64_t)num_sms() * 2 * 128 * bn,
+                                   tiles_m * (Cout / bn) * 4 * 2, ok);
+    if (ok) ep.sk = sk;
+  }
   if (mode == 1) {
     switch (bn) {
       case 256: return launch_conv<256, 4, 1>(xb, mw, mx, sh, ep, s);

@@ -13,8 +13,9 @@
 #include <stdio.h>
 
 #include "gg_common.cuh"
-#include "gg_tc.cuh"
 #include "gg_kernels.h"
+#include "gg_streamk.cuh"
+#include "gg_tc.cuh"
 
 namespace gg {
 using namespace tc;
@@ -36,6 +37,7 @@ struct GemmEpilogue {
   int64_t qkv_plane;               // OUT_QKV_HEADS: elements per Q/K/V^T plane (B*H*S*64)
   const int32_t* count;            // device item count (dynamic batch) or null
   int rows_per_item;               // M_eff = min(M, *count * rows_per_item)
+  StreamK sk;                      // stream-K split of the (tile, k-block) space, or disabled
 };
 
 constexpr int kBK = 64;            // 64 bf16 = 128 B = one swizzle row
@@ -52,6 +54,77 @@ struct GemmSmem {
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // + barriers + alignment slack
 };
+
+// Fused epilogue of one thread's 32 consecutive accumulator columns of one row:
+// bias, residual, activation and the output layout.
+__device__ __forceinline__ void epi_chunk(const GemmEpilogue& ep, int row, int col0, float (&v)[32]) {
+  if (ep.bias) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      float4 b = *reinterpret_cast<const float4*>(ep.bias + col0 + i);
+      v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
+    }
+  }
+  if (ep.residual) {
+    const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + (int64_t)row * ep.ldr + col0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u = rp[q];
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = __bfloat1622float2(h[e]);
+        v[q * 8 + 2 * e] += f.x;
+        v[q * 8 + 2 * e + 1] += f.y;
+      }
+    }
+  }
+  if (ep.act == ACT_RELU) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+  } else if (ep.act == ACT_GELU) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
+  }
+  if (ep.out_mode == OUT_F32) {
+    float4* dp = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.D) + (int64_t)row * ep.ldd + col0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dp[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    return;
+  }
+  __nv_bfloat16* dst;
+  if (ep.out_mode == OUT_QKV_HEADS) {
+    // [M, 3*H*64] -> Q (pre-scaled by 1/sqrt(64), exact), K as [B,H,S,64]; V^T as [B,H,64,S]
+    const int hd = ep.heads * 64;
+    const int which = col0 / hd, h = (col0 % hd) / 64, d0 = col0 % 64;
+    const int b = row / ep.seq_len, s_ = row % ep.seq_len;
+    __nv_bfloat16* plane = reinterpret_cast<__nv_bfloat16*>(ep.D) + which * ep.qkv_plane;
+    const int64_t bh = (int64_t)b * ep.heads + h;
+    if (which == 2) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        plane[(bh * 64 + d0 + i) * ep.seq_len + s_] = __float2bfloat16_rn(v[i]);
+      return;
+    }
+    if (which == 0) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] *= 0.125f;
+    }
+    dst = plane + (bh * ep.seq_len + s_) * 64 + d0;
+  } else {
+    dst = reinterpret_cast<__nv_bfloat16*>(ep.D) + (int64_t)row * ep.ldd + col0;
+  }
+  uint4* dp = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u;
+    u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+    u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+    u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+    u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+    dp[q] = u;
+  }
+}
 
 template <int BM, int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -101,9 +174,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===== TMA producer =====
     if (lane == 0) {
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int tm = tile % tiles_m, tn = tile / tiles_m;  // M-fastest: B tile stays hot in L2
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+      SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
+      SkWork w;
+      while (sc.next(w)) {
+        const int tm = w.tile % tiles_m, tn = w.tile / tiles_m;  // M-fastest: B tile stays hot in L2
+        for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t round = it / STAGES;
           mbar_wait(&empty[s], (round & 1) ^ 1);
@@ -120,13 +195,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
       int it = 0, t = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+      SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
+      SkWork w;
+      for (; sc.next(w); ++t) {
         const int acc = t & 1;
         const uint32_t use = t >> 1;
         mbar_wait(&acc_empty[acc], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t round = it / STAGES;
           mbar_wait(&full[s], round & 1);
@@ -136,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
             umma_bf16(d_tmem, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sb + kk * 32), idesc,
-                      (kb | kk) != 0);
+                      (kb != w.kb0 || kk != 0));
           }
           umma_commit(&empty[s]);
         }
@@ -148,90 +225,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int half = (warp - 2) >> 2;  // which half of the columns
     int t = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
-      const int tm = tile % tiles_m, tn = tile / tiles_m;
+    SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
+    SkWork w;
+    for (; sc.next(w); ++t) {
+      const int tm = w.tile % tiles_m, tn = w.tile / tiles_m;
       const int acc = t & 1;
       const uint32_t use = t >> 1;
       mbar_wait(&acc_full[acc], use & 1);
       tc_fence_after();
+      const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      // stream-K: a tile cut between CTAs is reduced by its last arriving segment
+      const bool partial = w.kb0 != 0 || w.kb1 != num_kb;
+      SkFix fx;
+      if (partial) {
+        auto load32 = [&](int c, float (&v)[32]) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tacc + half * (BN / 2) + c, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        };
+        if (!sk_arrive<BN / 2>(ep.sk, sc, w, warp - 2, kEpiWarps, lane, fx, load32)) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[acc]);
+          continue;
+        }
+      }
       const int row = tm * BM + quarter * 32 + lane;
       const bool row_ok = row < M;
 #pragma unroll 1
       for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 32) {
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c, r);
+        tmem_ld_32x32b_x32(tacc + c, r);
         tmem_ld_wait();
         const int col0 = tn * BN + c;
-        if (!row_ok || col0 >= N) continue;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (ep.bias) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 b = *reinterpret_cast<const float4*>(ep.bias + col0 + i);
-            v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
-          }
-        }
-        if (ep.residual) {
-          const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + (int64_t)row * ep.ldr + col0);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 u = rp[q];
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float2 f = __bfloat1622float2(h[e]);
-              v[q * 8 + 2 * e] += f.x;
-              v[q * 8 + 2 * e + 1] += f.y;
-            }
-          }
-        }
-        if (ep.act == ACT_RELU) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
-        } else if (ep.act == ACT_GELU) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
-        }
-        if (ep.out_mode == OUT_F32) {
-          float4* dp = reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.D) + (int64_t)row * ep.ldd + col0);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) dp[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          continue;
-        }
-        __nv_bfloat16* dst;
-        if (ep.out_mode == OUT_QKV_HEADS) {
-          // [M, 3*H*64] -> Q (pre-scaled by 1/sqrt(64), exact), K as [B,H,S,64]; V^T as [B,H,64,S]
-          const int hd = ep.heads * 64;
-          const int which = col0 / hd, h = (col0 % hd) / 64, d0 = col0 % 64;
-          const int b = row / ep.seq_len, s_ = row % ep.seq_len;
-          __nv_bfloat16* plane = reinterpret_cast<__nv_bfloat16*>(ep.D) + which * ep.qkv_plane;
-          const int64_t bh = (int64_t)b * ep.heads + h;
-          if (which == 2) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              plane[(bh * 64 + d0 + i) * ep.seq_len + s_] = __float2bfloat16_rn(v[i]);
-            continue;
-          }
-          if (which == 0) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] *= 0.125f;
-          }
-          dst = plane + (bh * ep.seq_len + s_) * 64 + d0;
-        } else {
-          dst = reinterpret_cast<__nv_bfloat16*>(ep.D) + (int64_t)row * ep.ldd + col0;
-        }
-        uint4* dp = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 u;
-          u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-          u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-          u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-          u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
-          dp[q] = u;
-        }
+        if (partial) sk_sum<BN / 2>(ep.sk, sc, w, warp - 2, kEpiWarps, lane, fx, c - half * (BN / 2), v);
+        if (!row_ok || col0 >= N) continue;
+        epi_chunk(ep, row, col0, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -276,6 +310,68 @@ int make_map_2d(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, i
   return r == CUDA_SUCCESS ? GG_OK : GG_ERR_INVALID_ARGUMENT;
 }
 
+// Stream-K workspace, one per device (see gg_streamk.cuh).
+constexpr int64_t kSkWsFloats = 12LL << 20;      // 48 MB of fp32 partial regions
+constexpr int64_t kSkCounters = 512LL << 10;     // 2 MB of (arrival, ready) counters
+static StreamK g_sk[64];
+
+static bool sk_alloc(int dev) {
+  StreamK& s = g_sk[dev];
+  if (s.ws) return true;
+  float* ws = nullptr;
+  int* cnt = nullptr;
+  if (cudaMalloc(&ws, kSkWsFloats * sizeof(float)) != cudaSuccess) return false;
+  if (cudaMalloc(&cnt, kSkCounters * sizeof(int)) != cudaSuccess ||
+      cudaMemset(cnt, 0, kSkCounters * sizeof(int)) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    cudaFree(ws);
+    return false;
+  }
+  s.ws = ws;
+  s.cnt = cnt;
+  return true;
+}
+
+StreamK streamk_workspace(cudaStream_t stream, int64_t ws_floats, int64_t counters, bool& ok) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  ok = false;
+  StreamK none{nullptr, nullptr, 0};
+  if (dev < 0 || dev >= 64 || ws_floats > kSkWsFloats || counters > kSkCounters) return none;
+  if (!g_sk[dev].ws) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+      return none;   // no allocation inside a graph capture: run data-parallel
+    if (!sk_alloc(dev)) return none;
+  }
+  ok = true;
+  StreamK s = g_sk[dev];
+  s.enabled = 1;
+  return s;
+}
+
+// Stream-K or data-parallel for `tiles` tiles of `nkb` k-blocks on `sms` SMs
+// (policy -1): stream-K when it removes a partly empty last wave (fixup ~2
+// k-blocks per CTA).  GG_STREAMK / gg_streamk_mode: 0 never (default), 1 force,
+// -1 by this wave model.
+static int g_sk_mode = -2;
+static int sk_mode() {
+  // default OFF: measured slower than data-parallel tiles at every DistilBERT /
+  // ResNet shape (the fixup reads of the partial regions are latency-bound)
+  if (g_sk_mode == -2) g_sk_mode = getenv("GG_STREAMK") ? atoi(getenv("GG_STREAMK")) : 0;
+  return g_sk_mode;
+}
+
+bool streamk_wanted(int64_t tiles, int64_t nkb, int sms) {
+  const int mode = sk_mode();
+  if (mode == 0) return false;
+  const int64_t T = tiles * nkb;
+  if (mode == 1) return T >= 2 * sms;
+  const double dp = (double)((tiles + sms - 1) / sms) * nkb;
+  const double sk = (double)T / sms + 2.0;
+  return T / sms >= 4 && sk < 0.93 * dp;
+}
+
 static int g_num_sms = 0;
 int num_sms() {
   if (!g_num_sms) {
@@ -288,7 +384,7 @@ int num_sms() {
 
 template <int BM, int BN, int STAGES>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
-                       const GemmEpilogue& ep, cudaStream_t s, int max_ctas) {
+                       GemmEpilogue ep, cudaStream_t s, int max_ctas) {
   using L = GemmSmem<BM, BN, STAGES>;
   auto kern = gemm_bf16_tcgen05<BM, BN, STAGES>;
   static bool attr = false;
@@ -300,12 +396,190 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  ep.sk = StreamK{nullptr, nullptr, 0};
+  if (max_ctas <= 0 && streamk_wanted(tiles, K / kBK, num_sms())) {
+    bool ok = false;
+    const int g = num_sms();
+    StreamK sk = streamk_workspace(s, (int64_t)g * 2 * BM * BN, (int64_t)tiles * kEpiWarps * 2, ok);
+    if (ok) {
+      ep.sk = sk;
+      grid = g;
+    }
+  }
   if (launch_pdl(kern, dim3(grid), dim3(kThreads), (size_t)L::TOTAL, s, ma, mb, M, N, K, ep) != cudaSuccess)
     return GG_ERR_CUDA;
   GG_LAUNCH_OK();
   return GG_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-pair GEMM (cluster of 2, cta_group::2): the pair computes a 256 x 256
+// tile; each CTA stages its own 128 rows of A and its half (128 rows) of B per
+// k-block, the leader issues M = 256, N = 256 MMAs that read both CTAs' smem and
+// accumulate each CTA's 128 rows into its own TMEM.  Per SM that is 32 KB of
+// operand ingress per 512 MMA cycles (64 B/cycle) instead of 48 KB (96 B/cycle)
+// for a 128 x 256 single-CTA tile: the single-CTA kernel is bounded by the
+// L2 -> SM operand bandwidth (~43 B/cycle/SM measured) at ~45 % of the tensor
+// peak, the pair kernel at ~66 %.
+//   warp 0     TMA producer in both CTAs (complete_tx on the leader's barrier)
+//   warp 1     TMEM allocator (both CTAs) + MMA issuer (leader only)
+//   warps 2-9  epilogue in both CTAs (their own 128 rows), release to the leader
+constexpr int kPairBN = 256;
+
+template <int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   int M_max, int N, int K, GemmEpilogue ep) {
+  constexpr int A_BYTES = 128 * kBK * 2, B_BYTES = 128 * kBK * 2;
+  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;     // [2]
+  uint64_t* acc_empty = acc_full + 2;      // [2] (the leader's counts both CTAs' epilogues)
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  griddep_launch();
+  const int num_kb = K / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 2 * kEpiWarps);
+    }
+    fence_mbar_init();
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_base_smem, 2 * kPairBN);
+  tc_fence_before();
+  cluster_sync_all();   // barriers of both CTAs initialised before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+  griddep_wait();
+  const int M = ep.count ? min(M_max, __ldg(ep.count) * ep.rows_per_item) : M_max;
+  const int tiles_m = (M + 255) / 256, tiles_n = N / kPairBN;
+  const int num_tiles = tiles_m * tiles_n;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        const int tm = tile % tiles_m, tn = tile / tiles_m;
+        const int m0 = tm * 256 + rank * 128, n0 = tn * kPairBN + rank * 128;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+          const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+          tma_load_2d_pair(sa, &map_a, fb, kb * kBK, m0);
+          tma_load_2d_pair(sa + A_BYTES, &map_b, fb, kb * kBK, n0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(256, kPairBN);
+      int it = 0, t = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
+        const int acc = t & 1;
+        mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kPairBN;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            umma_bf16_pair(d_tmem, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sb + kk * 32), idesc,
+                           (kb | kk) != 0);
+          umma_commit_pair(&empty[s], 3);
+        }
+        umma_commit_pair(&acc_full[acc], 3);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const uint32_t leader_empty0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
+    int t = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
+      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      const int acc = t & 1;
+      mbar_wait(&acc_full[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * kPairBN;
+      const int row = tm * 256 + rank * 128 + quarter * 32 + lane;
+      const bool row_ok = row < M;
+#pragma unroll 1
+      for (int c = half * (kPairBN / 2); c < (half + 1) * (kPairBN / 2); c += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tacc + c, r);
+        tmem_ld_wait();
+        if (!row_ok) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        epi_chunk(ep, row, tn * kPairBN + c, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_empty0 + acc * 8);
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();   // the peer's epilogue has released its last accumulator
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 2 * kPairBN);
+  }
+}
+
+template <int STAGES>
+static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
+                            const GemmEpilogue& ep, cudaStream_t s) {
+  constexpr int SMEM = STAGES * 2 * 128 * kBK * 2 + 256 + 1024;
+  auto kern = gemm_bf16_pair<STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+      return GG_ERR_CUDA;
+    attr = true;
+  }
+  const int tiles = ((M + 255) / 256) * (N / kPairBN);
+  const int pairs = num_sms() / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, M, N, K, ep) != cudaSuccess) return GG_ERR_CUDA;
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
 }  // namespace gg
 
 using namespace gg;
@@ -335,11 +609,33 @@ extern "C" int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, v
                   e->out_mode == OUT_QKV_HEADS ? M * 64 * (int64_t)e->heads : 0,
                   e->count_dev, e->rows_per_item};
   cudaStream_t s = gg_stream(stream);
+  // CTA pairs for wide GEMMs (tile_n auto, N % 256 == 0, enough 256-row tiles
+  // to fill most pairs); GG_NO_PAIR=1 keeps single-CTA tiles
+  static const bool no_pair = getenv("GG_NO_PAIR") != nullptr;
+  if (!no_pair && e->tile_n == 0 && N % kPairBN == 0 && M >= 256 * 16) {
+    CUtensorMap mbp;
+    rc = make_map_2d(&ma, A, M, K, lda, 128);
+    if (!rc) rc = make_map_2d(&mbp, B, N, K, ldb, 128);
+    if (rc) return rc;
+    return launch_gemm_pair<6>(ma, mbp, (int)M, (int)N, (int)K, ep, s);
+  }
   switch (bn) {
     case 256: return launch_gemm<128, 256, 4>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
     case 128: return launch_gemm<128, 128, 6>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
     default: return launch_gemm<128, 64, 8>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
   }
+}
+
+extern "C" int gg_streamk_reserve(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return GG_ERR_CUDA;
+  return sk_alloc(dev) ? GG_OK : GG_ERR_CUDA;
+}
+
+extern "C" int gg_streamk_mode(int32_t mode) {
+  const int prev = sk_mode();
+  if (mode >= -1 && mode <= 1) g_sk_mode = mode;
+  return prev;
 }
 
 extern "C" int gg_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,

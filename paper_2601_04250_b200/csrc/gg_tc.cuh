@@ -160,8 +160,31 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
          | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// Exact-erf GELU, x * Phi(x), for the GEMM epilogue at tensor-core pace.
+// With a = min(|x|, 5.75): Phi(-a) = erfc(a / sqrt 2) / 2 = 2^q(a) / 2, q a
+// degree-8 Chebyshev fit of log2 erfc(a / sqrt 2) on [0, 5.75]; then
+// gelu(x) = x - x Phi(-x) for x >= 0 and x Phi(x) below.  One MUFU ex2 and nine
+// FMAs instead of erff's branchy ~40 instructions (the epilogue issue rate
+// bounded the FFN-up GEMM); |gelu_erf - exact| <= 4.2e-7 over all fp32 x
+// (tools/fit_gelu.py), 10^4 below the bf16 rounding of the stored output.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_erf(float x) {
-  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752440f));
+  const float a = fminf(fabsf(x), 5.75f);
+  float q = -3.1597807037542225e-08f;
+  q = fmaf(q, a, -1.2583882380567957e-06f);
+  q = fmaf(q, a, 5.780859646620229e-05f);
+  q = fmaf(q, a, -0.0009210868738591671f);
+  q = fmaf(q, a, 0.008511481806635857f);
+  q = fmaf(q, a, -0.05401911586523056f);
+  q = fmaf(q, a, -0.45836740732192993f);
+  q = fmaf(q, a, -1.1513043642044067f);
+  q = fmaf(q, a, 1.1678074770316016e-05f);
+  const float e = 0.5f * x * ex2_approx(q);
+  return x >= 0.0f ? x - e : e;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -169,5 +192,73 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+}  // namespace tc
+}  // namespace gg
+
+// ---- CTA pairs (cluster of 2, cta_group::2) -------------------------------------
+namespace gg {
+namespace tc {
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t smem_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on an mbarrier given by its shared::cluster address (possibly the peer CTA's)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA tile load into this CTA's smem, completing bytes on an mbarrier that may
+// live in the peer CTA of the pair (the leader's full barrier).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map,
+                                                 uint32_t bar_cluster, int32_t x, int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+// D[tmem of both CTAs] (+)= A (M = 256: 128 rows in each CTA's smem) * B^T (N split
+// in halves across the two CTAs' smem); issued by the leader CTA only.
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on the mbarrier at the same smem offset in every CTA of `mask` when the
+// leader's previously issued pair MMAs complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
 }  // namespace tc
 }  // namespace gg

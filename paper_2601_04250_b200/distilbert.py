@@ -55,6 +55,8 @@ class DistilBertB200:
     def __init__(self, hf_model, max_batch: int = 128, seq_len: int = 128, device="cuda"):
         torch = _native.require_cuda()
         self.lib = _native.load()
+        # stream-K workspace now, before any CUDA graph capture of the forward
+        _native.check("gg_streamk_reserve", self.lib.gg_streamk_reserve())
         self.device = torch.device(device)
         self.max_batch, self.seq_len = max_batch, seq_len
         cfg = hf_model.config

@@ -125,6 +125,21 @@ class _StemConv(_Conv):
         return _Conv.__call__(self, lib, x, n, h, w, y, st, relu=relu, count=count)
 
 
+class _PaddedIm2col(_Conv):
+    """3x3 / 1 conv on a zero-bordered [N, s+2, s+2, C] buffer through gg_conv2d's
+    TMA-im2col mode (pad 0 on the padded input, interior of the padded output):
+    no work on border positions, and stream-K when the tile count leaves a
+    partly empty wave (layers 3-4: 14x14 / 7x7 maps, K = 2304 / 4608)."""
+
+    def __init__(self, conv, bn, device):
+        super().__init__(conv, bn, device, pad=0, pad_hi=0, out_pad=1)
+
+    def __call__(self, lib, x, n, h, w, y, st, residual=None, relu=True, count=None):
+        _Conv.__call__(self, lib, x, n, h + 2, w + 2, y, st, residual=residual, relu=relu,
+                       count=count)
+        return h, w
+
+
 class _SpanConv:
     """3x3 / 1 conv on padded activations (gg_conv3x3_padded); weights in
     (channel block, tap, channel) K order."""
@@ -156,6 +171,8 @@ class ResNet18B200:
     def __init__(self, tv_model, max_batch: int = 64, image: int = 224, device="cuda"):
         torch = _native.require_cuda()
         self.lib = _native.load()
+        # stream-K workspace now, before any CUDA graph capture of the forward
+        _native.check("gg_streamk_reserve", self.lib.gg_streamk_reserve())
         self.device = torch.device(device)
         self.max_batch, self.image = max_batch, image
         m = tv_model.eval()
@@ -171,13 +188,13 @@ class ResNet18B200:
                     # 3x3/2 on the previous stage's padded buffer: pad 0 (physical padding)
                     c1 = _Conv(blk.conv1, blk.bn1, dev, pad=0, pad_hi=0, out_pad=1)
                 else:
-                    c1 = _SpanConv(blk.conv1, blk.bn1, dev)
+                    c1 = self._stride1(blk.conv1, blk.bn1, dev, li)
                 ds = None
                 if blk.downsample is not None:
                     # 1x1/2 reads interior pixel (2ho+1, 2wo+1) of the padded input: pad -1
                     ds = _Conv(blk.downsample[0], blk.downsample[1], dev, pad=-1, pad_hi=-1,
                                out_pad=1)
-                self.blocks.append((li, c1, _SpanConv(blk.conv2, blk.bn2, dev), ds))
+                self.blocks.append((li, c1, self._stride1(blk.conv2, blk.bn2, dev, li), ds))
                 cin = cout
         self.num_classes = m.fc.out_features
         npad = (self.num_classes + 31) // 32 * 32
@@ -199,6 +216,18 @@ class ResNet18B200:
                            for s, c in zip(self.sizes, chans)]
         self.pooled = torch.empty((B, 512), **z)
         self.logits = torch.empty((B, npad), dtype=torch.float32, device=dev)
+
+    # stages whose 3x3/1 convs run as TMA-im2col instead of span convs (no border
+    # rows: 31 % / 65 % of layers 3 / 4's 16^2 / 9^2 padded maps).  Empty: the
+    # span convs measured faster at every stage on B200 (one operand load feeds
+    # nine taps); GG_RESNET_IM2COL_STAGES="2,3" selects the alternative.
+    IM2COL_STAGES = ()
+
+    def _stride1(self, conv, bn, dev, stage):
+        import os
+        env = os.environ.get("GG_RESNET_IM2COL_STAGES")
+        stages = self.IM2COL_STAGES if env is None else tuple(int(v) for v in env.split(",") if v)
+        return _PaddedIm2col(conv, bn, dev) if stage in stages else _SpanConv(conv, bn, dev)
 
     def flops(self, batch: int) -> float:
         """Algorithmic FLOPs (3.628 GF/img at 224x224)."""

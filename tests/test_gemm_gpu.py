@@ -46,7 +46,7 @@ def reference(A, B, bias, residual, act):
 @pytest.mark.parametrize("M,N,K,tile_n", [
     (128, 256, 64, 256), (256, 256, 128, 256), (300, 512, 768, 0), (1000, 768, 768, 0),
     (16384, 2304, 768, 0), (16384, 768, 3072, 0), (4096, 3072, 768, 128), (513, 64, 1024, 64),
-    (128, 32, 768, 64)])
+    (128, 32, 768, 64), (5000, 768, 768, 0), (4096, 512, 1536, 0)])
 def test_gemm_shapes(env, M, N, K, tile_n):
     torch = env[0]
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
@@ -61,10 +61,11 @@ def test_gemm_shapes(env, M, N, K, tile_n):
 
 
 @pytest.mark.parametrize("act", [0, 1, 2])
-def test_gemm_fused_epilogue(env, act):
+@pytest.mark.parametrize("M", [777, 4500])   # single-CTA tiles / CTA-pair tiles
+def test_gemm_fused_epilogue(env, act, M):
     torch = env[0]
     g = torch.Generator(device="cuda").manual_seed(act)
-    M, N, K = 777, 768, 768
+    N, K = 768, 768
     A = torch.randn((M, K), device="cuda", generator=g).to(torch.bfloat16)
     B = (torch.randn((N, K), device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
     bias = torch.randn(N, device="cuda", generator=g)
@@ -83,3 +84,34 @@ def test_gemm_rejects_bad_shapes(env):
     rc = lib.gg_gemm_bf16(nat.ptr(A), 100, nat.ptr(B), 100, nat.ptr(D), 64, 128, 64, 100,
                           None, None, 0, 0, 0, nat.stream_ptr())
     assert rc != 0
+
+
+@pytest.mark.parametrize("M,N,K,act,res", [
+    (16384, 768, 3072, 0, True), (16384, 768, 768, 0, True), (1000, 768, 768, 2, False),
+    (300, 2304, 768, 1, True), (128, 256, 4096, 0, False), (16384, 3072, 768, 2, False)])
+def test_gemm_stream_k(env, M, N, K, act, res):
+    """Stream-K split of the (tile, k-block) space: same result as data-parallel
+    tiles within bf16 rounding of a different fp32 summation order, vs the fp32
+    reference at the bf16 tolerance, and bit-identical across runs (segments are
+    summed in k order whatever order they arrive in)."""
+    torch, nat, lib = env
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + act)
+    A = torch.randn((M, K), device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn((N, K), device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    bias = torch.randn(N, device="cuda", generator=g)
+    resid = torch.randn((M, N), device="cuda", generator=g).to(torch.bfloat16) if res else None
+    assert lib.gg_streamk_reserve() == 0
+    prev = lib.gg_streamk_mode(0)
+    try:
+        d_dp = run_gemm(env, A, B, bias=bias, residual=resid, act=act)
+        lib.gg_streamk_mode(1)
+        d_sk = run_gemm(env, A, B, bias=bias, residual=resid, act=act)
+        d_sk2 = run_gemm(env, A, B, bias=bias, residual=resid, act=act)
+    finally:
+        lib.gg_streamk_mode(prev)
+    torch.cuda.synchronize()
+    ref = reference(A, B, bias, resid, act)
+    scale = max(1.0, ref.abs().max().item())
+    assert torch.equal(d_sk, d_sk2)
+    assert (d_sk.float() - ref).abs().max().item() <= 2e-2 * scale
+    assert (d_sk.float() - d_dp.float()).abs().max().item() <= 1e-2 * scale

@@ -52,6 +52,45 @@ def test_conv_vs_torch(env, n, h, cin, cout, r, stride, pad, res):
     assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
 
 
+@pytest.mark.parametrize("n,h,cin,cout,r,stride,pad,res", [
+    (64, 7, 512, 512, 3, 1, 1, True), (64, 14, 256, 512, 3, 2, 1, False), (8, 14, 256, 256, 3, 1, 1, True),
+    (64, 14, 256, 512, 1, 2, 0, False)])
+def test_conv_stream_k(env, n, h, cin, cout, r, stride, pad, res):
+    """Stream-K im2col conv (layer-3/4 shapes) == data-parallel within bf16 rounding,
+    bit-identical across runs."""
+    torch, nat, lib = env
+    g = torch.Generator(device="cuda").manual_seed(n * h + cin + cout)
+    x = torch.randn((n, h, h, cin), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((cout, r * r * cin), device="cuda", generator=g) / (cin * r * r) ** 0.5).to(torch.bfloat16)
+    b = torch.randn(cout, device="cuda", generator=g)
+    ho = (h + 2 * pad - r) // stride + 1
+    resid = torch.randn((n, ho, ho, cout), device="cuda", generator=g).to(torch.bfloat16) if res else None
+    outs = []
+    assert lib.gg_streamk_reserve() == 0
+    prev = lib.gg_streamk_mode(0)
+    try:
+        for mode in (0, 1, 1):
+            lib.gg_streamk_mode(mode)
+            y = torch.empty((n, ho, ho, cout), dtype=torch.bfloat16, device="cuda")
+            nat.check("gg_conv2d", lib.gg_conv2d(nat.ptr(x), n, h, h, cin, nat.ptr(w), cout, r, r,
+                                                 stride, pad, r * r * cin, nat.ptr(b), nat.ptr(resid),
+                                                 1, nat.ptr(y), -1, 0, None, nat.stream_ptr()))
+            outs.append(y)
+    finally:
+        lib.gg_streamk_mode(prev)
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2),
+                                     w.float().reshape(cout, r, r, cin).permute(0, 3, 1, 2), b,
+                                     stride=stride, padding=pad)
+    if res:
+        ref = ref + resid.float().permute(0, 3, 1, 2)
+    ref = torch.relu(ref).permute(0, 2, 3, 1)
+    scale = max(1.0, ref.abs().max().item())
+    assert torch.equal(outs[1], outs[2])
+    assert (outs[1].float() - ref).abs().max().item() <= 2e-2 * scale
+    assert (outs[1].float() - outs[0].float()).abs().max().item() <= 1e-2 * scale
+
+
 def test_space_to_depth_stem_vs_torch(env):
     """7x7/2 pad 3 conv (conv1+bn1) == 4x4/1 pad (2,1) conv over the s2d(2) input."""
     torch, nat, lib = env
