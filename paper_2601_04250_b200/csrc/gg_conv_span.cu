@@ -44,7 +44,7 @@
 namespace gg {
 using namespace tc;
 
-constexpr int kSpanMaxStages = 8;
+constexpr int kSpanMaxStages = 16;
 constexpr int kSpanEpiWarps = 8;
 constexpr int kSpanThreads = 64 + 32 * kSpanEpiWarps;
 constexpr int kSpanSmemMax = 227 * 1024;
@@ -92,6 +92,9 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   constexpr int B_BYTES = BN * RB;           // one tap slab of B
   constexpr int BM = 128 * MT;               // MT M=128 sub-tiles share every B slab
   constexpr int ACC_COLS = MT * BN;          // TMEM columns per accumulator buffer
+  // accumulator buffers in TMEM: 4 when they fit (N = 64 tiles are short — 9
+  // taps x 4 MMAs — so two buffers let one slow epilogue stall the tensor pipe)
+  constexpr int NACC = 512 / ACC_COLS >= 4 ? 4 : 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int cblocks = sh.C / CH;
@@ -106,8 +109,8 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   uint64_t* b_full = a_empty + kSpanMaxStages;
   uint64_t* b_empty = b_full + kSpanMaxStages;
   uint64_t* acc_full = b_empty + kSpanMaxStages;
-  uint64_t* acc_empty = acc_full + 2;
-  uint64_t* bres_full = acc_empty + 2;
+  uint64_t* acc_empty = acc_full + NACC;
+  uint64_t* bres_full = acc_empty + NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -126,7 +129,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NACC; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], kSpanEpiWarps);
     }
@@ -135,7 +138,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     tma_prefetch(&map_x);
     tma_prefetch(&map_w);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 2 * ACC_COLS);
+  if (warp == 1) tmem_alloc(tmem_slot, NACC * ACC_COLS);
   // the weight slab does not depend on the predecessor: start it before the wait
   if (warp == 0 && lane == 0 && sh.bres) {
     const int tiles_max = (sh.N * img + BM - 1) / BM * tiles_n;
@@ -198,17 +201,29 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
       for (int tap = 0; tap < TAPS; ++tap)
         tap_off[tap] = (uint64_t)(((tap / RT) * sh.Wp + tap % RT) * (RB / 16));
+      long long wt[3] = {0, 0, 0};   // GG_SPAN_PROF: cycles waiting on acc_empty / A / B
+      const long long t_mma0 = clock64();
+#define SPAN_WAIT(bar, par, slot)                              \
+  do {                                                         \
+    if (ep.prof) {                                             \
+      const long long t_ = clock64();                          \
+      mbar_wait(bar, par);                                     \
+      wt[slot] += clock64() - t_;                              \
+    } else {                                                   \
+      mbar_wait(bar, par);                                     \
+    }                                                          \
+  } while (0)
       if (b_loaded) mbar_wait(bres_full, 0);   // also when the count leaves no tile: drain the TMA
       const uint64_t bres_desc = sdesc_sw(smem_u32(b_base), RB);
       int ait = 0, bit = 0, t = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
-        const int acc = t & 1;
-        mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);
+        const int acc = t % NACC;
+        SPAN_WAIT(&acc_empty[acc], ((t / NACC) & 1) ^ 1, 0);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * ACC_COLS;
         for (int cb = 0; cb < cblocks; ++cb, ++ait) {
           const int as = ait % AST;
-          mbar_wait(&a_full[as], (ait / AST) & 1);
+          SPAN_WAIT(&a_full[as], (ait / AST) & 1, 1);
           if (ep.prof && blockIdx.x == 0 && cb == 0 && t < 16) ep.prof[4096 + t * 8 + 1] = clock64();
           tc_fence_after();
           const uint64_t ad = sdesc_sw(smem_u32(a_base + as * sh.a_stage_bytes), RB);
@@ -229,7 +244,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
             for (int tap = 0; tap < TAPS; ++tap, ++bit) {
               const int bs = bit % BST;
-              mbar_wait(&b_full[bs], (bit / BST) & 1);
+              SPAN_WAIT(&b_full[bs], (bit / BST) & 1, 2);
               tc_fence_after();
               const uint64_t ao = ad + tap_off[tap];
               const uint64_t bo = bres_desc + (uint64_t)(bs * (B_BYTES >> 4));
@@ -247,6 +262,13 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
         umma_commit(&acc_full[acc]);
         if (ep.prof && blockIdx.x == 0 && t < 16) ep.prof[4096 + t * 8 + 2] = clock64();
       }
+#undef SPAN_WAIT
+      if (ep.prof) {
+        ep.prof[6144 + blockIdx.x * 4 + 0] = wt[0];
+        ep.prof[6144 + blockIdx.x * 4 + 1] = wt[1];
+        ep.prof[6144 + blockIdx.x * 4 + 2] = wt[2];
+        ep.prof[6144 + blockIdx.x * 4 + 3] = clock64() - t_mma0;
+      }
     }
   } else {
     // epilogue: warp w handles TMEM lane quarter (w % 4) and column half (w - 2) / 4
@@ -256,8 +278,8 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     int t = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
-      const int acc = t & 1;
-      mbar_wait(&acc_full[acc], (t >> 1) & 1);
+      const int acc = t % NACC;
+      mbar_wait(&acc_full[acc], (t / NACC) & 1);
       if (ep.prof && blockIdx.x == 0 && warp == 2 && lane == 0 && t < 16) ep.prof[4096 + t * 8 + 3] = clock64();
       tc_fence_after();
 #pragma unroll 1
@@ -348,7 +370,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   }
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * ACC_COLS);
+    tmem_dealloc(tmem_base, NACC * ACC_COLS);
   }
 }
 
@@ -423,6 +445,15 @@ static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanS
     double csum = 0;
     for (int i = 0; i < grid; ++i) csum += (double)(h[2048 + 2 * i + 1] - h[2048 + 2 * i]);
     fprintf(stderr, "span mean CTA clock64 cycles %.0f\n", csum / grid);
+    double w0 = 0, w1 = 0, w2 = 0, wt = 0;
+    for (int i = 0; i < grid; ++i) {
+      w0 += (double)h[6144 + 4 * i];
+      w1 += (double)h[6144 + 4 * i + 1];
+      w2 += (double)h[6144 + 4 * i + 2];
+      wt += (double)h[6144 + 4 * i + 3];
+    }
+    fprintf(stderr, "MMA issuer (mean over CTAs): %.0f cycles, waiting acc_empty %.0f%%, A %.0f%%, B %.0f%%\n",
+            wt / grid, 100 * w0 / wt, 100 * w1 / wt, 100 * w2 / wt);
     unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
     double dsum = 0;
     for (int i = 0; i < grid; ++i) {
@@ -441,9 +472,287 @@ static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanS
   return GG_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-pair span convolution (cluster of 2, cta_group::2) for the 3x3/1 convs of
+// layers 2-4.  Why: a cta_group::1 128 x N x 16 MMA reads (4 KB + N * 32 B) of
+// shared memory per N/2 cycles — at N = 128 that is the SM's whole 128 B/cycle
+// of smem bandwidth, so the TMA writes of the operand ring push the tensor pipe
+// to ~80 cycles per 64-cycle MMA (measured with GG_SPAN_PROF: the issuer waits
+// on loads only ~15 % of the time).  A pair MMA (M = 256 over two SMs, each CTA
+// holding its own 128 rows of A and half of the N columns of B) reads 64 B/cycle
+// per SM at N = 256 (96 at N = 128), and each SM streams only half of the
+// weight slabs.
+// Tile of the pair: output rows [tm*256, tm*256+256) of the padded space (CTA
+// rank r owns 128 of them, with its own A span) x BN output channels.
+template <int BN>
+__global__ void __launch_bounds__(kSpanThreads, 1)
+    conv_span_pair(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+                   SpanShape sh, SpanEpi ep) {
+  constexpr int RB = 128;                    // 64 channels per pixel row
+  constexpr int TAPS = 9;
+  constexpr int BH = BN / 2;                 // B rows per CTA (its half of the N tile)
+  constexpr int B_BYTES = BH * RB;           // one tap slab of this CTA's B half
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int cblocks = sh.C / 64;
+  const int nkb = cblocks * TAPS;
+  const int AST = sh.a_stages, BST = sh.b_stages;
+  uint8_t* a_base = smem;
+  uint8_t* b_base = smem + AST * sh.a_stage_bytes;
+  const int b_slots = sh.bres ? nkb : BST;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + b_slots * B_BYTES);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + kSpanMaxStages;
+  uint64_t* b_full = a_empty + kSpanMaxStages;
+  uint64_t* b_empty = b_full + kSpanMaxStages;
+  uint64_t* acc_full = b_empty + kSpanMaxStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* bres_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  griddep_launch();
+  const int img = sh.Hp * sh.Wp;
+  const int tiles_n = sh.Cout / BN;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSpanMaxStages; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 2 * kSpanEpiWarps);
+    }
+    mbar_init(bres_full, 1);
+    fence_mbar_init();
+    tma_prefetch(&map_x);
+    tma_prefetch(&map_w);
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_slot, 2 * BN);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  // resident weights (this CTA's half of the single N tile): independent of the predecessor
+  const int tiles_max = (sh.N * img + 255) / 256 * tiles_n;
+  const bool b_loaded = sh.bres && tiles_max > pair;
+  if (warp == 0 && lane == 0 && b_loaded) {
+    const uint32_t fb = mapa_shared(smem_u32(bres_full), 0);
+    if (rank == 0) mbar_expect_tx(bres_full, 2 * nkb * B_BYTES);
+    for (int kb = 0; kb < nkb; ++kb)
+      tma_load_2d_pair(b_base + kb * B_BYTES, &map_w, fb, kb * 64, rank * BH);
+  }
+  griddep_wait();
+  const int n_eff = ep.count ? min(sh.N, __ldg(ep.count)) : sh.N;
+  const int Mtot = n_eff * img;
+  const int tiles_m = (Mtot + 255) / 256;
+  const int num_tiles = tiles_m * tiles_n;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int ait = 0, bit = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        const int tm = tile % tiles_m, tn = tile / tiles_m;
+        const int m0 = tm * 256 + rank * 128;
+        for (int cb = 0; cb < cblocks; ++cb, ++ait) {
+          const int as = ait % AST;
+          mbar_wait(&a_empty[as], ((ait / AST) & 1) ^ 1);
+          uint8_t* sa = a_base + as * sh.a_stage_bytes;
+          const uint32_t fa = mapa_shared(smem_u32(&a_full[as]), 0);
+          if (rank == 0) mbar_expect_tx(&a_full[as], 2 * sh.boxes * sh.box_rows * RB);
+          for (int bx = 0; bx < sh.boxes; ++bx)
+            tma_load_2d_pair(sa + bx * sh.box_rows * RB, &map_x, fa, cb * 64, m0 + bx * sh.box_rows);
+          if (!sh.bres) {
+            for (int tap = 0; tap < TAPS; ++tap, ++bit) {
+              const int bs = bit % BST;
+              mbar_wait(&b_empty[bs], ((bit / BST) & 1) ^ 1);
+              const uint32_t fb = mapa_shared(smem_u32(&b_full[bs]), 0);
+              if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * B_BYTES);
+              tma_load_2d_pair(b_base + bs * B_BYTES, &map_w, fb, (cb * TAPS + tap) * 64,
+                               tn * BN + rank * BH);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(256, BN);
+      uint64_t tap_off[TAPS];
+#pragma unroll
+      for (int tap = 0; tap < TAPS; ++tap) tap_off[tap] = (uint64_t)(((tap / 3) * sh.Wp + tap % 3) * (RB / 16));
+      if (b_loaded) mbar_wait(bres_full, 0);
+      const uint64_t bres_desc = sdesc_k_sw128(smem_u32(b_base));
+      int ait = 0, bit = 0, t = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
+        const int acc = t & 1;
+        mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int cb = 0; cb < cblocks; ++cb, ++ait) {
+          const int as = ait % AST;
+          mbar_wait(&a_full[as], (ait / AST) & 1);
+          tc_fence_after();
+          const uint64_t ad = sdesc_k_sw128(smem_u32(a_base + as * sh.a_stage_bytes));
+          if (sh.bres) {
+            const uint64_t bd = bres_desc + (uint64_t)(cb * TAPS * (B_BYTES >> 4));
+#pragma unroll
+            for (int tap = 0; tap < TAPS; ++tap) {
+              const uint64_t ao = ad + tap_off[tap];
+              const uint64_t bo = bd + (uint64_t)(tap * (B_BYTES >> 4));
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
+                               (cb | tap | kk) != 0);
+            }
+          } else {
+#pragma unroll
+            for (int tap = 0; tap < TAPS; ++tap, ++bit) {
+              const int bs = bit % BST;
+              mbar_wait(&b_full[bs], (bit / BST) & 1);
+              tc_fence_after();
+              const uint64_t ao = ad + tap_off[tap];
+              const uint64_t bo = bres_desc + (uint64_t)(bs * (B_BYTES >> 4));
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
+                               (cb | tap | kk) != 0);
+              umma_commit_pair(&b_empty[bs], 3);
+            }
+          }
+          umma_commit_pair(&a_empty[as], 3);
+        }
+        umma_commit_pair(&acc_full[acc], 3);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    constexpr int HALF = BN / 2;
+    const uint32_t leader_empty0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
+    int t = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
+      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      const int acc = t & 1;
+      mbar_wait(&acc_full[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const int m = tm * 256 + rank * 128 + quarter * 32 + lane;
+      const int nimg = m / img;
+      const int within = m - nimg * img;
+      const int h = within / sh.Wp, w = within - (within / sh.Wp) * sh.Wp;
+      const bool real = m < Mtot && h < sh.Ho && w < sh.Wo;
+      const int64_t oidx = (int64_t)m + sh.Wp + 1;   // padded output position
+      const bool store = m < Mtot && oidx < (int64_t)n_eff * img;
+      const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c = half * HALF; c < (half + 1) * HALF; c += 32) {
+        const int col0 = tn * BN + c;
+        uint4 res[4];
+        const bool use_res = ep.residual != nullptr && store && real;
+        if (use_res) {
+          const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + oidx * sh.Cout + col0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) res[q] = __ldg(rp + q);
+        }
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tcol + c, r);
+        tmem_ld_wait();
+        if (!store) continue;
+        float v[32];
+        if (real) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + i));
+            v[i] = __uint_as_float(r[i]) + b.x;
+            v[i + 1] = __uint_as_float(r[i + 1]) + b.y;
+            v[i + 2] = __uint_as_float(r[i + 2]) + b.z;
+            v[i + 3] = __uint_as_float(r[i + 3]) + b.w;
+          }
+          if (use_res) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&res[q]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h2[e]);
+                v[q * 8 + 2 * e] += f.x;
+                v[q * 8 + 2 * e + 1] += f.y;
+              }
+            }
+          }
+          if (ep.relu) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.0f;   // padding positions stay zero
+        }
+        uint4* dp = reinterpret_cast<uint4*>(ep.y + oidx * sh.Cout + col0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+          u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+          u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+          u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+          dp[q] = u;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_empty0 + acc * 8);
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 2 * BN);
+  }
+}
+
+template <int BN>
+static int launch_span_pair(const CUtensorMap& mx, const CUtensorMap& mw, const SpanShape& sh,
+                            const SpanEpi& ep, cudaStream_t s) {
+  auto kern = conv_span_pair<BN>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpanSmemMax) != cudaSuccess)
+      return GG_ERR_CUDA;
+    attr = true;
+  }
+  const int smem = span_smem_bytes(sh, BN / 2, 128, 9);
+  const int tiles = ((sh.N * sh.Hp * sh.Wp + 255) / 256) * (sh.Cout / BN);
+  const int pairs = num_sms() / 2;
+  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kSpanThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  if (cudaLaunchKernelEx(&cfg, kern, mx, mw, sh, ep) != cudaSuccess) return GG_ERR_CUDA;
+  return GG_OK;
+}
+
 // Fill the stage plan: B resident (only with a single N tile) if it fits beside
 // >= 3 A stages, else a B ring; A stages = as many as fit (<= kSpanMaxStages).
-static bool plan_span(SpanShape& sh, int bn, int rb, int taps) {
+static bool plan_span(SpanShape& sh, int bn, int rb, int taps, bool single_ntile) {
   // several boxes: multiples of 8 rows so each box starts on a swizzle atom
   sh.boxes = (sh.span_rows + 255) / 256;
   sh.box_rows = sh.boxes == 1 ? sh.span_rows : ((sh.span_rows + sh.boxes - 1) / sh.boxes + 7) / 8 * 8;
@@ -451,18 +760,24 @@ static bool plan_span(SpanShape& sh, int bn, int rb, int taps) {
   const int nkb = sh.C / (rb / 2) * taps;
   const int avail = kSpanSmemMax - 2048;
   const int b_all = nkb * bn * rb;
-  if (bn == sh.Cout && b_all + 3 * sh.a_stage_bytes <= avail) {   // one N tile: slab fixed
+  if (single_ntile && b_all + 3 * sh.a_stage_bytes <= avail) {   // one N tile: slab fixed
     sh.bres = 1;
     sh.b_stages = 1;
     sh.a_stages = (avail - b_all) / sh.a_stage_bytes;
   } else {
+    // B ring: one tap slab (BN x 64 ch) is consumed every 4 * MT MMAs (~512
+    // cycles) while an A span lasts all nine taps of a channel block, so the
+    // smem goes to B depth (bytes in flight against L2 latency under load):
+    // A double-buffered, B as deep as the rest allows.
+    static const int a_env = getenv("GG_SPAN_ASTAGES") ? atoi(getenv("GG_SPAN_ASTAGES")) : 0;
+    const int a_want = a_env > 1 ? a_env : 2;
     sh.bres = 0;
-    sh.b_stages = 4;
-    sh.a_stages = (avail - sh.b_stages * bn * rb) / sh.a_stage_bytes;
-    if (sh.a_stages > 4) {   // spend the rest on B depth
-      const int bmax = (avail - 4 * sh.a_stage_bytes) / (bn * rb);
-      sh.b_stages = bmax < kSpanMaxStages ? bmax : kSpanMaxStages;
-      sh.a_stages = (avail - sh.b_stages * bn * rb) / sh.a_stage_bytes;
+    sh.a_stages = a_want;
+    const int bmax = (avail - a_want * sh.a_stage_bytes) / (bn * rb);
+    sh.b_stages = bmax < kSpanMaxStages ? bmax : kSpanMaxStages;
+    if (sh.b_stages < 2) {
+      sh.b_stages = 2;
+      sh.a_stages = (avail - 2 * bn * rb) / sh.a_stage_bytes;
     }
   }
   if (sh.a_stages > kSpanMaxStages) sh.a_stages = kSpanMaxStages;
@@ -489,6 +804,24 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
   // vs the SM's operand ingress (~40 B/cycle: B slabs unless resident + A
   // spans), tiles per CTA, plus the last tile's epilogue and the resident-B
   // prologue, which nothing overlaps.
+  // CTA pairs (cta_group::2, M = 256 over two SMs) for Cout >= 128: half the
+  // smem operand reads per MMA and half the weight stream per SM (see
+  // conv_span_pair).  GG_SPAN_PAIR=0 keeps single-CTA tiles.
+  static const bool no_pair = getenv("GG_SPAN_PAIR") && atoi(getenv("GG_SPAN_PAIR")) == 0;
+  if (!no_pair && Cout % 128 == 0 && C >= 128 && !getenv("GG_SPAN_TILE")) {
+    const int bn = Cout % 256 == 0 ? 256 : 128;
+    sh.span_rows = 128 + 2 * sh.Wp + 2;
+    if (sh.span_rows <= 1024 && plan_span(sh, bn / 2, 128, 9, bn == Cout)) {
+      CUtensorMap mx, mw;
+      int rc = make_map_span(&mx, x, Mtot, C, 64, sh.box_rows);
+      if (!rc) rc = make_map_span(&mw, w, Cout, (int64_t)C * 9, 64, bn / 2);
+      if (rc) return rc;
+      SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
+                 reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0};
+      cudaStream_t s = gg_stream(stream);
+      return bn == 256 ? launch_span_pair<256>(mx, mw, sh, ep, s) : launch_span_pair<128>(mx, mw, sh, ep, s);
+    }
+  }
   const int cblocks = C / 64;
   struct Cand { int bn, mt; };
   const Cand cands[] = {{64, 1}, {128, 1}, {256, 1}, {64, 2}, {128, 2}};
@@ -498,7 +831,7 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
     if (cd.bn > Cout || Cout % cd.bn) continue;
     SpanShape t = sh;
     t.span_rows = 128 * cd.mt + 2 * sh.Wp + 2;
-    if (t.span_rows > 1024 || !plan_span(t, cd.bn, 128, 9)) continue;
+    if (t.span_rows > 1024 || !plan_span(t, cd.bn, 128, 9, cd.bn == Cout)) continue;
     const int64_t tiles = (Mtot + 128 * cd.mt - 1) / (128 * cd.mt) * (Cout / cd.bn);
     const int64_t per_cta = (tiles + num_sms() - 1) / num_sms();
     const double cyc_k = cd.bn == 64 ? 48.0 : cd.bn / 2.0;
@@ -523,7 +856,7 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
     }
   }
   sh.span_rows = 128 * best_mt + 2 * sh.Wp + 2;
-  if (sh.span_rows > 1024 || !plan_span(sh, best_bn, 128, 9)) return GG_ERR_UNSUPPORTED;
+  if (sh.span_rows > 1024 || !plan_span(sh, best_bn, 128, 9, best_bn == Cout)) return GG_ERR_UNSUPPORTED;
   CUtensorMap mx, mw;
   int rc = make_map_span(&mx, x, Mtot, C, 64, sh.box_rows);
   if (!rc) rc = make_map_span(&mw, w, Cout, (int64_t)C * 9, 64, best_bn);
@@ -551,7 +884,7 @@ extern "C" int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws
   sh.Ho = Hs; sh.Wo = Ws;
   sh.span_rows = 128 + 3 * sh.Wp + 3;
   if (sh.span_rows > 1024) return GG_ERR_UNSUPPORTED;
-  if (!plan_span(sh, 64, 32, 16)) return GG_ERR_UNSUPPORTED;
+  if (!plan_span(sh, 64, 32, 16, true)) return GG_ERR_UNSUPPORTED;
   const int64_t Mtot = (int64_t)N * sh.Hp * sh.Wp;
   CUtensorMap mx, mw;
   int rc = make_map_span(&mx, x, Mtot, 16, 16, sh.box_rows);

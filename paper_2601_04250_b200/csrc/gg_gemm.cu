@@ -38,6 +38,7 @@ struct GemmEpilogue {
   const int32_t* count;            // device item count (dynamic batch) or null
   int rows_per_item;               // M_eff = min(M, *count * rows_per_item)
   StreamK sk;                      // stream-K split of the (tile, k-block) space, or disabled
+  int raster_n;                    // 1: N-fastest tile order (A larger than ~L2/2), else M-fastest
 };
 
 constexpr int kBK = 64;            // 64 bf16 = 128 B = one swizzle row
@@ -57,11 +58,14 @@ struct GemmSmem {
 
 // Fused epilogue of one thread's 32 consecutive accumulator columns of one row:
 // bias, residual, activation and the output layout.
-__device__ __forceinline__ void epi_chunk(const GemmEpilogue& ep, int row, int col0, float (&v)[32]) {
+__device__ __forceinline__ void epi_chunk(const GemmEpilogue& ep, int row, int col0, float (&v)[32],
+                                          const uint4* res_pre = nullptr,
+                                          const float* bias_smem = nullptr) {
   if (ep.bias) {
+    const float* bsrc = bias_smem ? bias_smem : ep.bias;
 #pragma unroll
     for (int i = 0; i < 32; i += 4) {
-      float4 b = *reinterpret_cast<const float4*>(ep.bias + col0 + i);
+      float4 b = *reinterpret_cast<const float4*>(bsrc + col0 + i);
       v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
     }
   }
@@ -69,7 +73,7 @@ __device__ __forceinline__ void epi_chunk(const GemmEpilogue& ep, int row, int c
     const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + (int64_t)row * ep.ldr + col0);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      uint4 u = rp[q];
+      uint4 u = res_pre ? res_pre[q] : rp[q];
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -177,7 +181,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
       SkWork w;
       while (sc.next(w)) {
-        const int tm = w.tile % tiles_m, tn = w.tile / tiles_m;  // M-fastest: B tile stays hot in L2
+        // raster: M-fastest keeps the weight tile hot across consecutive CTAs; when
+        // A outgrows the L2 (FFN-down: 100 MB) N-fastest makes the CTAs working at
+        // once share A row blocks (read from HBM once, reused across the N tiles)
+        const int tm = ep.raster_n ? w.tile / tiles_n : w.tile % tiles_m;
+        const int tn = ep.raster_n ? w.tile % tiles_n : w.tile / tiles_m;
         for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t round = it / STAGES;
@@ -228,7 +236,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
     SkWork w;
     for (; sc.next(w); ++t) {
-      const int tm = w.tile % tiles_m, tn = w.tile / tiles_m;
+      const int tm = ep.raster_n ? w.tile / tiles_n : w.tile % tiles_m;
+      const int tn = ep.raster_n ? w.tile % tiles_n : w.tile / tiles_m;
       const int acc = t & 1;
       const uint32_t use = t >> 1;
       mbar_wait(&acc_full[acc], use & 1);
@@ -426,6 +435,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
 //   warp 1     TMEM allocator (both CTAs) + MMA issuer (leader only)
 //   warps 2-9  epilogue in both CTAs (their own 128 rows), release to the leader
 constexpr int kPairBN = 256;
+constexpr int kPairMaxN = 4096;   // bias staged in smem
 
 template <int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -440,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = empty + STAGES;     // [2]
   uint64_t* acc_empty = acc_full + 2;      // [2] (the leader's counts both CTAs' epilogues)
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* bias_s = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);   // [N] (N <= kPairMaxN)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -454,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 2 * kEpiWarps);
+      mbar_init(&acc_empty[a], 2);   // one elected arrive per CTA of the pair
     }
     fence_mbar_init();
     tma_prefetch(&map_a);
@@ -474,7 +485,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int it = 0;
       for (int tile = pair; tile < num_tiles; tile += npairs) {
-        const int tm = tile % tiles_m, tn = tile / tiles_m;
+        const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;   // raster: see above
+        const int tn = ep.raster_n ? tile % tiles_n : tile / tiles_m;
         const int m0 = tm * 256 + rank * 128, n0 = tn * kPairBN + rank * 128;
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % STAGES;
@@ -515,29 +527,55 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     const uint32_t leader_empty0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
+    // the bias vector once per CTA in smem (broadcast LDS instead of per-chunk LDG)
+    if (ep.bias)
+      for (int i = threadIdx.x - 64; i < N; i += 32 * kEpiWarps) bias_s[i] = __ldg(ep.bias + i);
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
     int t = 0;
     for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
-      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;
+      const int tn = ep.raster_n ? tile % tiles_n : tile / tiles_m;
       const int acc = t & 1;
       mbar_wait(&acc_full[acc], (t >> 1) & 1);
       tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * kPairBN;
       const int row = tm * 256 + rank * 128 + quarter * 32 + lane;
       const bool row_ok = row < M;
+      // residual rows are prefetched one chunk ahead so their latency overlaps
+      // the TMEM read and the math of the previous chunk
+      const bool pre = ep.residual != nullptr && row_ok;
+      const __nv_bfloat16* rrow = ep.residual + (int64_t)row * ep.ldr + tn * kPairBN;
+      uint4 res[4];
+      if (pre) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) res[q] = __ldg(reinterpret_cast<const uint4*>(rrow + half * (kPairBN / 2)) + q);
+      }
 #pragma unroll 1
       for (int c = half * (kPairBN / 2); c < (half + 1) * (kPairBN / 2); c += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(tacc + c, r);
+        uint4 cur[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cur[q] = res[q];
+        if (pre && c + 32 < (half + 1) * (kPairBN / 2)) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) res[q] = __ldg(reinterpret_cast<const uint4*>(rrow + c + 32) + q);
+        }
         tmem_ld_wait();
         if (!row_ok) continue;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        epi_chunk(ep, row, tn * kPairBN + c, v);
+        epi_chunk(ep, row, tn * kPairBN + c, v, pre ? cur : nullptr, bias_s);
       }
+      // release the accumulator: all epilogue warps of this CTA, then one arrive
+      // on the leader's barrier (local for the leader, remote for the peer)
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(leader_empty0 + acc * 8);
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      if (threadIdx.x == 64) {
+        if (rank == 0) mbar_arrive(&acc_empty[acc]);
+        else mbar_arrive_cluster(leader_empty0 + acc * 8);
+      }
     }
   }
   __syncthreads();
@@ -551,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int STAGES>
 static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
                             const GemmEpilogue& ep, cudaStream_t s) {
-  constexpr int SMEM = STAGES * 2 * 128 * kBK * 2 + 256 + 1024;
+  constexpr int SMEM = STAGES * 2 * 128 * kBK * 2 + 256 + kPairMaxN * 4 + 1024;
   auto kern = gemm_bf16_pair<STAGES>;
   static bool attr = false;
   if (!attr) {
@@ -607,12 +645,13 @@ extern "C" int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, v
   GemmEpilogue ep{D, ldd, e->bias, reinterpret_cast<const __nv_bfloat16*>(e->residual), e->ldr,
                   e->act, e->out_mode, e->seq_len, e->heads,
                   e->out_mode == OUT_QKV_HEADS ? M * 64 * (int64_t)e->heads : 0,
-                  e->count_dev, e->rows_per_item};
+                  e->count_dev, e->rows_per_item, StreamK{nullptr, nullptr, 0},
+                  M * K * 2 > (48LL << 20) ? 1 : 0};
   cudaStream_t s = gg_stream(stream);
   // CTA pairs for wide GEMMs (tile_n auto, N % 256 == 0, enough 256-row tiles
   // to fill most pairs); GG_NO_PAIR=1 keeps single-CTA tiles
   static const bool no_pair = getenv("GG_NO_PAIR") != nullptr;
-  if (!no_pair && e->tile_n == 0 && N % kPairBN == 0 && M >= 256 * 16) {
+  if (!no_pair && e->tile_n == 0 && N % kPairBN == 0 && N <= kPairMaxN && M >= 256 * 16) {
     CUtensorMap mbp;
     rc = make_map_2d(&ma, A, M, K, lda, 128);
     if (!rc) rc = make_map_2d(&mbp, B, N, K, ldb, 128);

@@ -151,6 +151,20 @@ def test_pools(env):
     assert (zp.float() - ref.mean(dim=(2, 3))).abs().max().item() < 1e-2
 
 
+@pytest.mark.parametrize("n,c,h,w", [(3, 64, 29, 31), (1, 128, 9, 10), (2, 8, 7, 5)])
+def test_maxpool_ragged_shapes(env, n, c, h, w):
+    """Blocked max pool (4 x 2 outputs per thread) at sizes that leave partial blocks: exact."""
+    torch, nat, lib = env
+    x = torch.randn((n, c, h, w), device="cuda").to(torch.bfloat16)
+    xn = x.permute(0, 2, 3, 1).contiguous()
+    ref = torch.nn.functional.max_pool2d(x.float(), 3, 2, 1)
+    ho, wo = ref.shape[2], ref.shape[3]
+    y = torch.full((n, ho, wo, c), 7.0, dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(nat.ptr(xn), n, h, w, c, nat.ptr(y), 0, None,
+                                                     nat.stream_ptr()))
+    assert torch.equal(y.float().permute(0, 3, 1, 2), ref)
+
+
 @pytest.mark.parametrize("batch", [2, 64])
 def test_resnet18_logits_vs_eager(env, batch):
     torch = env[0]

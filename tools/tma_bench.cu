@@ -40,6 +40,35 @@ __global__ void __launch_bounds__(32, 1) tma_stream(const __grid_constant__ CUte
   }
 }
 
+// Same stream with 1-D bulk copies (cp.async.bulk) of contiguous row ranges.
+__global__ void __launch_bounds__(32, 1) bulk_stream(const uint8_t* src, int box_rows, int stages,
+                                                     int iters, int total_rows, long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[16];
+  const int stage_bytes = box_rows * 128;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nblk = total_rows / box_rows;
+    long long t0 = clock64();
+    for (int i = 0; i < iters + stages; ++i) {
+      const int s = i % stages;
+      if (i >= stages) mbar_wait(&full[s], ((i - stages) / stages) & 1);
+      if (i < iters) {
+        mbar_expect_tx(&full[s], stage_bytes);
+        const int blk = (blockIdx.x * 7919 + i * 131) % nblk;
+        bulk_load(smem + s * stage_bytes, src + (size_t)blk * stage_bytes, stage_bytes, &full[s]);
+      }
+    }
+    long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 enc;
 
 int main() {
@@ -85,6 +114,25 @@ int main() {
         avg /= sms;
         const double bpc = (double)iters * box_rows * 128 / avg;
         printf("src %5lld MB  box %3d rows x 128 B  stages %d: %6.1f B/cycle/SM  (%.2f TB/s @1.9GHz)\n",
+               mb, box_rows, stages, bpc, bpc * 148 * 1.9e9 / 1e12);
+      }
+    }
+    cudaFuncSetAttribute(bulk_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    for (int box_rows : {64, 128, 256}) {
+      for (int stages : {2, 4, 6}) {
+        if (stages * box_rows * 128 > 200 * 1024) continue;
+        const int iters = 400;
+        const int smem = stages * box_rows * 128 + 1024;
+        for (int rep = 0; rep < 2; ++rep)
+          bulk_stream<<<sms, 32, smem>>>((const uint8_t*)src, box_rows, stages, iters, (int)rows, d_out);
+        if (cudaDeviceSynchronize() != cudaSuccess) { printf("bulk launch failed\n"); return 1; }
+        long long h[148];
+        cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+        double avg = 0;
+        for (int i = 0; i < sms; ++i) avg += h[i];
+        avg /= sms;
+        const double bpc = (double)iters * box_rows * 128 / avg;
+        printf("BULK src %5lld MB  %3d rows x 128 B  stages %d: %6.1f B/cycle/SM  (%.2f TB/s @1.9GHz)\n",
                mb, box_rows, stages, bpc, bpc * 148 * 1.9e9 / 1e12);
       }
     }
