@@ -18,10 +18,11 @@ exchange for N > 1), K2 feedback.  Captured once as a CUDA graph and replayed.
   e2e     same loop through the public API with host buffers: every step
           copies the window's scores/now and payload images from pinned host
           memory and reads back the served batch's predictions.
-  roofline  the forward pass (20 implicit-GEMM tcgen05 conv launches + fc for
-          ResNet-18; 36 tcgen05 GEMM + 6 attention launches for DistilBERT),
+  roofline  the forward pass (the dominant kernel family: ~90 % of a step),
           algorithmic FLOPs / CUDA-event time of a full batch, vs the measured
-          sustained bf16 peak (MEASURED_PEAKS.json).
+          sustained bf16 peak (MEASURED_PEAKS.json); traffic = the DRAM bytes of
+          one full-batch forward from the committed ncu launch list
+          (profiles/r1b_forward_traffic.json).
   cpu_baseline / --impl reference
           the reference's CPU path: the controller port (oracle/, the
           reference's algorithm in CPython) deciding the same windows, plus a
@@ -383,11 +384,22 @@ def roofline_forward(srv, net, B):
     flops = net.flops(B)
     pk = peaks()
     achieved = flops / (ms * 1e-3) / 1e12
-    kern = ("implicit-GEMM tcgen05 conv x20 + fc (ResNet-18 forward)" if srv.kind == "resnet18"
-            else "tcgen05 GEMM x38 + attention x6 + LN x13 (DistilBERT forward)")
+    kern = ("ResNet-18 forward: stem span conv + max pool + 4 span convs (layer 1) + 9 CTA-pair "
+            "span convs (layers 2-4) + 6 TMA-im2col convs + avg pool + fc, all tcgen05"
+            if srv.kind == "resnet18"
+            else "DistilBERT forward: 24 CTA-pair tcgen05 GEMMs + 2 single-CTA GEMMs + 6 tcgen05 "
+                 "attention + 12 LayerNorm + embedding-LN")
+    traffic, traffic_src = None, None
+    try:   # committed ncu evidence: DRAM bytes of one full-batch forward (tools/profile_round.sh)
+        with open(os.path.join(ROOT, "profiles", "r1b_forward_traffic.json")) as f:
+            t = json.load(f)[srv.kind]
+        traffic, traffic_src = int(t["dram_bytes_per_forward"]), t["source"]
+    except Exception:
+        pass
     return {"bound": "tensor", "achieved": round(achieved, 2), "peak": pk["bf16_sustained"],
             "unit": "TFLOP/s", "frac": round(achieved / pk["bf16_sustained"], 4),
-            "traffic": None, "kernel": kern, "flops_per_launch": flops,
+            "traffic": traffic, "traffic_unit": "bytes per forward (DRAM read + write)",
+            "traffic_source": traffic_src, "kernel": kern, "flops_per_launch": flops,
             "ms_per_launch": round(ms, 4), "peak_source": pk["source"] + " bf16_tflops_sustained"}
 
 

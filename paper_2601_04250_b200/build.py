@@ -23,7 +23,7 @@ OUT = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT, "libgreengate_b200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+COMMON = ["-O3", "-lineinfo", *(["-DGG_GELU_TANH"] if os.environ.get("GG_GELU_TANH") else []), "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 # per-translation-unit extra flags
 UNITS = {

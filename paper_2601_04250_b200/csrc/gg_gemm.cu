@@ -39,6 +39,7 @@ struct GemmEpilogue {
   int rows_per_item;               // M_eff = min(M, *count * rows_per_item)
   StreamK sk;                      // stream-K split of the (tile, k-block) space, or disabled
   int raster_n;                    // 1: N-fastest tile order (A larger than ~L2/2), else M-fastest
+  long long* prof;                 // debug (GG_GEMM_PROF): per-pair issuer cycles / waits, or null
 };
 
 constexpr int kBK = 64;            // 64 bf16 = 128 B = one swizzle row
@@ -503,14 +504,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0 && rank == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(256, kPairBN);
       int it = 0, t = 0;
+      long long w_acc = 0, w_full = 0;            // GG_GEMM_PROF: issuer wait cycles
+      const long long t0 = ep.prof ? clock64() : 0;
       for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
         const int acc = t & 1;
-        mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);
+        if (ep.prof) {
+          const long long a = clock64();
+          mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);
+          w_acc += clock64() - a;
+        } else {
+          mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);
+        }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairBN;
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % STAGES;
-          mbar_wait(&full[s], (it / STAGES) & 1);
+          if (ep.prof) {
+            const long long a = clock64();
+            mbar_wait(&full[s], (it / STAGES) & 1);
+            w_full += clock64() - a;
+          } else {
+            mbar_wait(&full[s], (it / STAGES) & 1);
+          }
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
@@ -521,6 +536,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_commit_pair(&empty[s], 3);
         }
         umma_commit_pair(&acc_full[acc], 3);
+      }
+      if (ep.prof) {
+        ep.prof[pair * 4 + 0] = clock64() - t0;
+        ep.prof[pair * 4 + 1] = w_acc;
+        ep.prof[pair * 4 + 2] = w_full;
+        ep.prof[pair * 4 + 3] = t;
       }
     }
   } else {
@@ -614,8 +635,32 @@ static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, int M,
   at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, M, N, K, ep) != cudaSuccess) return GG_ERR_CUDA;
+  static long long* prof = nullptr;
+  GemmEpilogue e2 = ep;
+  const bool do_prof = getenv("GG_GEMM_PROF") != nullptr;
+  if (do_prof) {
+    if (!prof) cudaMalloc(&prof, 4096 * sizeof(long long));
+    cudaMemsetAsync(prof, 0, 4096 * sizeof(long long), s);
+    e2.prof = prof;
+  }
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, M, N, K, e2) != cudaSuccess) return GG_ERR_CUDA;
   GG_LAUNCH_OK();
+  if (do_prof) {
+    long long h[4096];
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
+    double tot = 0, wa = 0, wf = 0, nt = 0;
+    const int np = grid / 2;
+    for (int i = 0; i < np; ++i) {
+      tot += h[4 * i];
+      wa += h[4 * i + 1];
+      wf += h[4 * i + 2];
+      nt += h[4 * i + 3];
+    }
+    fprintf(stderr, "pair GEMM M=%d N=%d K=%d: issuer %.0f cycles/pair, %.2f tiles/pair, waiting acc_empty %.0f%%, "
+            "operands %.0f%%, MMA-bound ideal %.0f cycles\n", M, N, K, tot / np, nt / np, 100 * wa / tot,
+            100 * wf / tot, nt / np * (K / kBK) * 4 * 128.0);
+  }
   return GG_OK;
 }
 }  // namespace gg
@@ -646,7 +691,7 @@ extern "C" int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, v
                   e->act, e->out_mode, e->seq_len, e->heads,
                   e->out_mode == OUT_QKV_HEADS ? M * 64 * (int64_t)e->heads : 0,
                   e->count_dev, e->rows_per_item, StreamK{nullptr, nullptr, 0},
-                  M * K * 2 > (48LL << 20) ? 1 : 0};
+                  M * K * 2 > (48LL << 20) ? 1 : 0, nullptr};
   cudaStream_t s = gg_stream(stream);
   // CTA pairs for wide GEMMs (tile_n auto, N % 256 == 0, enough 256-row tiles
   // to fill most pairs); GG_NO_PAIR=1 keeps single-CTA tiles

@@ -172,6 +172,18 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+#ifdef GG_GELU_TANH
+__device__ __forceinline__ float gelu_erf(float x) {
+  const float u = x * fmaf(0.0356774081f, x * x, 0.7978845608f);
+  const float hx = 0.5f * x;
+  return fmaf(hx, tanh_approx(u), hx);
+}
+#else
 __device__ __forceinline__ float gelu_erf(float x) {
   const float a = fminf(fabsf(x), 5.75f);
   float q = -3.1597807037542225e-08f;
@@ -186,6 +198,7 @@ __device__ __forceinline__ float gelu_erf(float x) {
   const float e = 0.5f * x * ex2_approx(q);
   return x >= 0.0f ? x - e : e;
 }
+#endif
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
