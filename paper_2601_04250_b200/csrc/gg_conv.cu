@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int wc = wo0 * sh.stride - sh.pad, hc = ho0 * sh.stride - sh.pad;
         for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
           const int s = it % nst;
-          mbar_wait(&empty[s], ((it / nst) & 1) ^ 1);
+          mbar_wait_sleep(&empty[s], ((it / nst) & 1) ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
           mbar_expect_tx(&full[s], sh.bres ? L::A_BYTES : L::STAGE_BYTES);
           constexpr int kLoads = MODE == 1 ? 1 : 4;
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       for (int kb = 0; kb < num_kb; ++kb, ++it) {
         const int s = it % STAGES;
         const uint32_t round = it / STAGES;
-        mbar_wait(&empty[s], (round & 1) ^ 1);
+        mbar_wait_sleep(&empty[s], (round & 1) ^ 1);
         const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES) + row_off;
         if (threadIdx.x == 0) {
           mbar_expect_tx(&full[s], L::B_BYTES);
@@ -225,8 +225,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for (int d = (it >= kLag ? it - kLag : 0); d < it; ++d) mbar_arrive(&full[d % STAGES]);
   } else if (warp == kConvProdWarps) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
+    // ===== MMA issuer: the warp runs the loop, one elected lane issues =====
+    {
       constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
       int it = 0, t = 0;
       if (b_loaded) mbar_wait(b_full, 0);   // also when the count leaves no tile: drain
@@ -244,14 +244,18 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
           const uint32_t sb = sh.bres ? smem_u32(bres + kb * L::B_BYTES) : sa + L::A_BYTES;
+          if (elect_one_sync()) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_bf16(d_tmem, MODE == 2 ? sdesc_k_sw32(sa + kk * 4096) : sdesc_k_sw128(sa + kk * 32),
-                      sdesc_k_sw128(sb + kk * 32), idesc,
-                      (kb != w.kb0 || kk != 0));
-          umma_commit(&empty[s]);
+            for (int kk = 0; kk < 4; ++kk)
+              umma_bf16(d_tmem, MODE == 2 ? sdesc_k_sw32(sa + kk * 4096) : sdesc_k_sw128(sa + kk * 32),
+                        sdesc_k_sw128(sb + kk * 32), idesc,
+                        (kb != w.kb0 || kk != 0));
+            umma_commit(&empty[s]);
+          }
+          __syncwarp();
         }
-        umma_commit(&acc_full[acc]);
+        if (elect_one_sync()) umma_commit(&acc_full[acc]);
+        __syncwarp();
       }
     }
   } else {
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     for (; sc.next(w); ++t) {
       const int tm = w.tile % tiles_m, tn = w.tile / tiles_m;
       const int acc = t & 1;
-      mbar_wait(&acc_full[acc], (t >> 1) & 1);
+      mbar_wait_sleep(&acc_full[acc], (t >> 1) & 1);
       tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
       const bool partial = w.kb0 != 0 || w.kb1 != num_kb;

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
         const int m0 = tm * BM;
         for (int cb = 0; cb < cblocks; ++cb, ++ait) {
           const int as = ait % AST;
-          mbar_wait(&a_empty[as], ((ait / AST) & 1) ^ 1);
+          mbar_wait_sleep(&a_empty[as], ((ait / AST) & 1) ^ 1);
           if (ep.prof && blockIdx.x == 0 && cb == 0 && ait / cblocks < 16)
             ep.prof[4096 + (ait / cblocks) * 8 + 0] = clock64();
           uint8_t* sa = a_base + as * sh.a_stage_bytes;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
           if (!sh.bres) {
             for (int tap = 0; tap < TAPS; ++tap, ++bit) {
               const int bs = bit % BST;
-              mbar_wait(&b_empty[bs], ((bit / BST) & 1) ^ 1);
+              mbar_wait_sleep(&b_empty[bs], ((bit / BST) & 1) ^ 1);
               mbar_expect_tx(&b_full[bs], B_BYTES);
               tma_load_2d(b_base + bs * B_BYTES, &map_w, &b_full[bs], (cb * TAPS + tap) * CH, tn * BN);
             }
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // the whole warp runs the loop; MMA batches / commits go out from one elected lane
       constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
       uint64_t tap_off[TAPS];   // row shift of tap (r, s) in 16-B descriptor units
 #pragma unroll
@@ -224,22 +224,26 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
         for (int cb = 0; cb < cblocks; ++cb, ++ait) {
           const int as = ait % AST;
           SPAN_WAIT(&a_full[as], (ait / AST) & 1, 1);
-          if (ep.prof && blockIdx.x == 0 && cb == 0 && t < 16) ep.prof[4096 + t * 8 + 1] = clock64();
+          if (ep.prof && blockIdx.x == 0 && cb == 0 && t < 16 && lane == 0) ep.prof[4096 + t * 8 + 1] = clock64();
           tc_fence_after();
           const uint64_t ad = sdesc_sw(smem_u32(a_base + as * sh.a_stage_bytes), RB);
           if (sh.bres) {
             const uint64_t bd = bres_desc + (uint64_t)(cb * TAPS * (B_BYTES >> 4));
+            if (elect_one_sync()) {
 #pragma unroll
-            for (int tap = 0; tap < TAPS; ++tap) {
-              const uint64_t ao = ad + tap_off[tap];
-              const uint64_t bo = bd + (uint64_t)(tap * (B_BYTES >> 4));
+              for (int tap = 0; tap < TAPS; ++tap) {
+                const uint64_t ao = ad + tap_off[tap];
+                const uint64_t bo = bd + (uint64_t)(tap * (B_BYTES >> 4));
 #pragma unroll
-              for (int kk = 0; kk < KSTEPS; ++kk)
+                for (int kk = 0; kk < KSTEPS; ++kk)
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt)
-                  umma_bf16(d_tmem + mt * BN, ao + (uint64_t)(mt * 128 * RB / 16 + kk * 2),
-                            bo + (uint64_t)(kk * 2), idesc, (cb | tap | kk) != 0);
+                  for (int mt = 0; mt < MT; ++mt)
+                    umma_bf16(d_tmem + mt * BN, ao + (uint64_t)(mt * 128 * RB / 16 + kk * 2),
+                              bo + (uint64_t)(kk * 2), idesc, (cb | tap | kk) != 0);
+              }
+              umma_commit(&a_empty[as]);
             }
+            __syncwarp();
           } else {
 #pragma unroll
             for (int tap = 0; tap < TAPS; ++tap, ++bit) {
@@ -248,22 +252,26 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
               tc_fence_after();
               const uint64_t ao = ad + tap_off[tap];
               const uint64_t bo = bres_desc + (uint64_t)(bs * (B_BYTES >> 4));
+              if (elect_one_sync()) {
 #pragma unroll
-              for (int kk = 0; kk < KSTEPS; ++kk)
+                for (int kk = 0; kk < KSTEPS; ++kk)
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt)
-                  umma_bf16(d_tmem + mt * BN, ao + (uint64_t)(mt * 128 * RB / 16 + kk * 2),
-                            bo + (uint64_t)(kk * 2), idesc, (cb | tap | kk) != 0);
-              umma_commit(&b_empty[bs]);
+                  for (int mt = 0; mt < MT; ++mt)
+                    umma_bf16(d_tmem + mt * BN, ao + (uint64_t)(mt * 128 * RB / 16 + kk * 2),
+                              bo + (uint64_t)(kk * 2), idesc, (cb | tap | kk) != 0);
+                umma_commit(&b_empty[bs]);
+                if (tap == TAPS - 1) umma_commit(&a_empty[as]);
+              }
+              __syncwarp();
             }
           }
-          umma_commit(&a_empty[as]);
         }
-        umma_commit(&acc_full[acc]);
-        if (ep.prof && blockIdx.x == 0 && t < 16) ep.prof[4096 + t * 8 + 2] = clock64();
+        if (elect_one_sync()) umma_commit(&acc_full[acc]);
+        __syncwarp();
+        if (ep.prof && blockIdx.x == 0 && t < 16 && lane == 0) ep.prof[4096 + t * 8 + 2] = clock64();
       }
 #undef SPAN_WAIT
-      if (ep.prof) {
+      if (ep.prof && lane == 0) {
         ep.prof[6144 + blockIdx.x * 4 + 0] = wt[0];
         ep.prof[6144 + blockIdx.x * 4 + 1] = wt[1];
         ep.prof[6144 + blockIdx.x * 4 + 2] = wt[2];
@@ -279,11 +287,11 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
       const int acc = t % NACC;
-      mbar_wait(&acc_full[acc], (t / NACC) & 1);
+      mbar_wait_sleep(&acc_full[acc], (t / NACC) & 1);
       if (ep.prof && blockIdx.x == 0 && warp == 2 && lane == 0 && t < 16) ep.prof[4096 + t * 8 + 3] = clock64();
       tc_fence_after();
 #pragma unroll 1
-      for (int mt = 0; mt < MT; ++mt) {
+      for (int mt = 0; mt < (ep.nostore == 2 ? 0 : MT); ++mt) {   // nostore 2: skip the epilogue (debug)
         const int m = tm * BM + mt * 128 + quarter * 32 + lane;
         const int nimg = m / img;
         const int within = m - nimg * img;
@@ -416,7 +424,7 @@ static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanS
   const int tiles = ((sh.N * sh.Hp * sh.Wp + 128 * MT - 1) / (128 * MT)) * (sh.Cout / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   SpanEpi e2 = ep;
-  e2.nostore = getenv("GG_SPAN_NOSTORE") != nullptr;
+  e2.nostore = getenv("GG_SPAN_NOSTORE") ? atoi(getenv("GG_SPAN_NOSTORE")) : 0;
   static unsigned long long* prof = nullptr;
   const bool do_prof = getenv("GG_SPAN_PROF") != nullptr;
   if (do_prof) {
@@ -562,7 +570,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
         const int m0 = tm * 256 + rank * 128;
         for (int cb = 0; cb < cblocks; ++cb, ++ait) {
           const int as = ait % AST;
-          mbar_wait(&a_empty[as], ((ait / AST) & 1) ^ 1);
+          mbar_wait_sleep(&a_empty[as], ((ait / AST) & 1) ^ 1);
           uint8_t* sa = a_base + as * sh.a_stage_bytes;
           const uint32_t fa = mapa_shared(smem_u32(&a_full[as]), 0);
           if (rank == 0) mbar_expect_tx(&a_full[as], 2 * sh.boxes * sh.box_rows * RB);
@@ -571,7 +579,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
           if (!sh.bres) {
             for (int tap = 0; tap < TAPS; ++tap, ++bit) {
               const int bs = bit % BST;
-              mbar_wait(&b_empty[bs], ((bit / BST) & 1) ^ 1);
+              mbar_wait_sleep(&b_empty[bs], ((bit / BST) & 1) ^ 1);
               const uint32_t fb = mapa_shared(smem_u32(&b_full[bs]), 0);
               if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * B_BYTES);
               tma_load_2d_pair(b_base + bs * B_BYTES, &map_w, fb, (cb * TAPS + tap) * 64,
@@ -582,7 +590,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {   // leader: the warp runs the loop, one elected lane issues
       constexpr uint32_t idesc = idesc_bf16_f32(256, BN);
       uint64_t tap_off[TAPS];
 #pragma unroll
@@ -602,15 +610,19 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
           const uint64_t ad = sdesc_k_sw128(smem_u32(a_base + as * sh.a_stage_bytes));
           if (sh.bres) {
             const uint64_t bd = bres_desc + (uint64_t)(cb * TAPS * (B_BYTES >> 4));
+            if (elect_one_sync()) {
 #pragma unroll
-            for (int tap = 0; tap < TAPS; ++tap) {
-              const uint64_t ao = ad + tap_off[tap];
-              const uint64_t bo = bd + (uint64_t)(tap * (B_BYTES >> 4));
+              for (int tap = 0; tap < TAPS; ++tap) {
+                const uint64_t ao = ad + tap_off[tap];
+                const uint64_t bo = bd + (uint64_t)(tap * (B_BYTES >> 4));
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
-                               (cb | tap | kk) != 0);
+                for (int kk = 0; kk < 4; ++kk)
+                  umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
+                                 (cb | tap | kk) != 0);
+              }
+              umma_commit_pair(&a_empty[as], 3);
             }
+            __syncwarp();
           } else {
 #pragma unroll
             for (int tap = 0; tap < TAPS; ++tap, ++bit) {
@@ -619,16 +631,20 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
               tc_fence_after();
               const uint64_t ao = ad + tap_off[tap];
               const uint64_t bo = bres_desc + (uint64_t)(bs * (B_BYTES >> 4));
+              if (elect_one_sync()) {
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
-                               (cb | tap | kk) != 0);
-              umma_commit_pair(&b_empty[bs], 3);
+                for (int kk = 0; kk < 4; ++kk)
+                  umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
+                                 (cb | tap | kk) != 0);
+                umma_commit_pair(&b_empty[bs], 3);
+                if (tap == TAPS - 1) umma_commit_pair(&a_empty[as], 3);
+              }
+              __syncwarp();
             }
           }
-          umma_commit_pair(&a_empty[as], 3);
         }
-        umma_commit_pair(&acc_full[acc], 3);
+        if (elect_one_sync()) umma_commit_pair(&acc_full[acc], 3);
+        __syncwarp();
       }
     }
   } else {
@@ -640,7 +656,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
       const int acc = t & 1;
-      mbar_wait(&acc_full[acc], (t >> 1) & 1);
+      mbar_wait_sleep(&acc_full[acc], (t >> 1) & 1);
       tc_fence_after();
       const int m = tm * 256 + rank * 128 + quarter * 32 + lane;
       const int nimg = m / img;

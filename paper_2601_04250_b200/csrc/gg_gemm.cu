@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t round = it / STAGES;
-          mbar_wait(&empty[s], (round & 1) ^ 1);
+          mbar_wait_sleep(&empty[s], (round & 1) ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
           uint8_t* sb = sa + L::A_BYTES;
           mbar_expect_tx(&full[s], L::STAGE_BYTES);
@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
+    // ===== MMA issuer: the warp runs the loop, one elected lane issues =====
+    {
       constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
       int it = 0, t = 0;
       SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
@@ -219,14 +219,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
           const uint32_t sb = sa + L::A_BYTES;
+          if (elect_one_sync()) {
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) {
-            umma_bf16(d_tmem, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sb + kk * 32), idesc,
-                      (kb != w.kb0 || kk != 0));
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+              umma_bf16(d_tmem, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sb + kk * 32), idesc,
+                        (kb != w.kb0 || kk != 0));
+            }
+            umma_commit(&empty[s]);
           }
-          umma_commit(&empty[s]);
+          __syncwarp();
         }
-        umma_commit(&acc_full[acc]);
+        if (elect_one_sync()) umma_commit(&acc_full[acc]);
+        __syncwarp();
       }
     }
   } else {
@@ -241,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tn = ep.raster_n ? w.tile % tiles_n : w.tile / tiles_m;
       const int acc = t & 1;
       const uint32_t use = t >> 1;
-      mbar_wait(&acc_full[acc], use & 1);
+      mbar_wait_sleep(&acc_full[acc], use & 1);
       tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
       // stream-K: a tile cut between CTAs is reduced by its last arriving segment
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = tm * 256 + rank * 128, n0 = tn * kPairBN + rank * 128;
         for (int kb = 0; kb < num_kb; ++kb, ++it) {
           const int s = it % STAGES;
-          mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+          mbar_wait_sleep(&empty[s], ((it / STAGES) & 1) ^ 1);
           uint8_t* sa = smem + s * STAGE_BYTES;
           if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
           const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
@@ -501,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {   // leader: the warp runs the loop, one elected lane issues
       constexpr uint32_t idesc = idesc_bf16_f32(256, kPairBN);
       int it = 0, t = 0;
       long long w_acc = 0, w_full = 0;            // GG_GEMM_PROF: issuer wait cycles
@@ -529,15 +533,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
+          if (elect_one_sync()) {
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk)
-            umma_bf16_pair(d_tmem, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sb + kk * 32), idesc,
-                           (kb | kk) != 0);
-          umma_commit_pair(&empty[s], 3);
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              umma_bf16_pair(d_tmem, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sb + kk * 32), idesc,
+                             (kb | kk) != 0);
+            umma_commit_pair(&empty[s], 3);
+          }
+          __syncwarp();
         }
-        umma_commit_pair(&acc_full[acc], 3);
+        if (elect_one_sync()) umma_commit_pair(&acc_full[acc], 3);
+        __syncwarp();
       }
-      if (ep.prof) {
+      if (ep.prof && lane == 0) {
         ep.prof[pair * 4 + 0] = clock64() - t0;
         ep.prof[pair * 4 + 1] = w_acc;
         ep.prof[pair * 4 + 2] = w_full;
@@ -557,7 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;
       const int tn = ep.raster_n ? tile % tiles_n : tile / tiles_m;
       const int acc = t & 1;
-      mbar_wait(&acc_full[acc], (t >> 1) & 1);
+      mbar_wait_sleep(&acc_full[acc], (t >> 1) & 1);
       tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * kPairBN;
       const int row = tm * 256 + rank * 128 + quarter * 32 + lane;

@@ -41,6 +41,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait with a hardware suspend hint: the thread sleeps until the phase completes
+// (or the hint elapses) instead of spinning.  For the producer and epilogue warps,
+// whose hot try_wait loops otherwise take issue slots from the single MMA-issuing
+// thread on the same SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(20000u)
+      : "memory");
+}
+
+// One lane of a converged warp (PTX elect.sync).  The MMA-issuing warp runs its
+// loop warp-uniformly and issues each batch of tcgen05.mma / commit inside
+// `if (elect_one_sync())`: ptxas then emits the UTCHMMAs back to back from
+// uniform registers.  Issuing from a `lane == 0` branch instead wraps every
+// UTCHMMA in an ELECT / BRA.U.ANY loop (~9 dependent instructions per MMA),
+// which at N = 64 (32-48 tensor cycles per MMA) made the stem and layer-1 convs
+// issue-bound at ~110 cycles per MMA.
+__device__ __forceinline__ bool elect_one_sync() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .b32 r;\n.reg .pred P;\nelect.sync r|P, 0xffffffff;\nselp.b32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // ---- TMA ----------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
