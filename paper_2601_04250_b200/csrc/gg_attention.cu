@@ -32,7 +32,6 @@ __global__ void __launch_bounds__(kAttnThreads, 4)
                       const __grid_constant__ CUtensorMap map_k,
                       const __grid_constant__ CUtensorMap map_vt, const int32_t* mask,
                       __nv_bfloat16* ctx, int64_t ldc, int heads, const int32_t* count) {
-  if (count && (int)(blockIdx.x / heads) >= __ldg(count)) return;  // dynamic batch
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar_load = reinterpret_cast<uint64_t*>(smem + 49152);
@@ -45,12 +44,18 @@ __global__ void __launch_bounds__(kAttnThreads, 4)
   const int bh = blockIdx.x;
   const int b = bh / heads, h = bh % heads;
 
+  griddep_launch();   // programmatic dependent launch: the successor's prologue may start
   if (threadIdx.x == 0) {
     mbar_init(bar_load, 1);
     mbar_init(bar_s, 1);
     mbar_init(bar_o, 1);
     fence_mbar_init();
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_vt);
   }
+  griddep_wait();     // Q/K/V, the mask and the count follow the predecessor
+  if (count && (int)(blockIdx.x / heads) >= __ldg(count)) return;  // dynamic batch (CTA-uniform)
   key_bias[threadIdx.x] = (mask && __ldg(mask + (int64_t)b * kAttnS + threadIdx.x) == 0) ? -INFINITY : 0.0f;
   if (warp == 0) tmem_alloc(tmem_slot, 128);
   tc_fence_before();
@@ -183,8 +188,9 @@ extern "C" int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int
       return GG_ERR_CUDA;
     attr = true;
   }
-  attention_tcgen05<<<batch * heads, kAttnThreads, kAttnSmem, gg_stream(stream)>>>(
-      mq, mk, mv, mask, reinterpret_cast<__nv_bfloat16*>(ctx), ldc, heads, count_dev);
+  if (launch_pdl(attention_tcgen05, dim3(batch * heads), dim3(kAttnThreads), kAttnSmem, gg_stream(stream),
+                 mq, mk, mv, mask, reinterpret_cast<__nv_bfloat16*>(ctx), ldc, heads, count_dev) != cudaSuccess)
+    return GG_ERR_CUDA;
   GG_LAUNCH_OK();
   return GG_OK;
 }

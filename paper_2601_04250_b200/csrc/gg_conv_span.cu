@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 
 // 2-D map over a [rows, cols] bf16 matrix, box [ch, box_rows], swizzle by row bytes.
 static int make_map_span(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int ch,
-                         int box_rows) {
+                         int box_rows, bool preswizzled = false) {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (!enc) {
     cudaDriverEntryPointQueryResult q;
@@ -400,7 +400,9 @@ static int make_map_span(CUtensorMap* map, const void* ptr, int64_t rows, int64_
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   ch == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+                   preswizzled ? CU_TENSOR_MAP_SWIZZLE_NONE
+                   : ch == 64  ? CU_TENSOR_MAP_SWIZZLE_128B
+                               : CU_TENSOR_MAP_SWIZZLE_32B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? GG_OK : GG_ERR_INVALID_ARGUMENT;
 }
@@ -493,17 +495,19 @@ static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanS
 // weight slabs.
 // Tile of the pair: output rows [tm*256, tm*256+256) of the padded space (CTA
 // rank r owns 128 of them, with its own A span) x BN output channels.
-template <int BN>
+template <int BN, int CH, int RT, bool DENSE>
 __global__ void __launch_bounds__(kSpanThreads, 1)
     conv_span_pair(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
                    SpanShape sh, SpanEpi ep) {
-  constexpr int RB = 128;                    // 64 channels per pixel row
-  constexpr int TAPS = 9;
+  constexpr int RB = CH * 2;                 // bytes per pixel row
+  constexpr int KSTEPS = CH / 16;            // MMAs per tap
+  constexpr int TAPS = RT * RT;
   constexpr int BH = BN / 2;                 // B rows per CTA (its half of the N tile)
   constexpr int B_BYTES = BH * RB;           // one tap slab of this CTA's B half
+  constexpr int NACC = 512 / BN >= 4 ? 4 : 2;   // TMEM accumulator buffers
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int cblocks = sh.C / 64;
+  const int cblocks = sh.C / CH;
   const int nkb = cblocks * TAPS;
   const int AST = sh.a_stages, BST = sh.b_stages;
   uint8_t* a_base = smem;
@@ -515,8 +519,8 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   uint64_t* b_full = a_empty + kSpanMaxStages;
   uint64_t* b_empty = b_full + kSpanMaxStages;
   uint64_t* acc_full = b_empty + kSpanMaxStages;
-  uint64_t* acc_empty = acc_full + 2;
-  uint64_t* bres_full = acc_empty + 2;
+  uint64_t* acc_empty = acc_full + NACC;
+  uint64_t* bres_full = acc_empty + NACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -533,7 +537,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NACC; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 2 * kSpanEpiWarps);
     }
@@ -542,7 +546,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     tma_prefetch(&map_x);
     tma_prefetch(&map_w);
   }
-  if (warp == 1) tmem_alloc_pair(tmem_slot, 2 * BN);
+  if (warp == 1) tmem_alloc_pair(tmem_slot, NACC * BN);
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -554,7 +558,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     const uint32_t fb = mapa_shared(smem_u32(bres_full), 0);
     if (rank == 0) mbar_expect_tx(bres_full, 2 * nkb * B_BYTES);
     for (int kb = 0; kb < nkb; ++kb)
-      tma_load_2d_pair(b_base + kb * B_BYTES, &map_w, fb, kb * 64, rank * BH);
+      tma_load_2d_pair(b_base + kb * B_BYTES, &map_w, fb, kb * CH, rank * BH);
   }
   griddep_wait();
   const int n_eff = ep.count ? min(sh.N, __ldg(ep.count)) : sh.N;
@@ -575,14 +579,14 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
           const uint32_t fa = mapa_shared(smem_u32(&a_full[as]), 0);
           if (rank == 0) mbar_expect_tx(&a_full[as], 2 * sh.boxes * sh.box_rows * RB);
           for (int bx = 0; bx < sh.boxes; ++bx)
-            tma_load_2d_pair(sa + bx * sh.box_rows * RB, &map_x, fa, cb * 64, m0 + bx * sh.box_rows);
+            tma_load_2d_pair(sa + bx * sh.box_rows * RB, &map_x, fa, cb * CH, m0 + bx * sh.box_rows);
           if (!sh.bres) {
             for (int tap = 0; tap < TAPS; ++tap, ++bit) {
               const int bs = bit % BST;
               mbar_wait_sleep(&b_empty[bs], ((bit / BST) & 1) ^ 1);
               const uint32_t fb = mapa_shared(smem_u32(&b_full[bs]), 0);
               if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * B_BYTES);
-              tma_load_2d_pair(b_base + bs * B_BYTES, &map_w, fb, (cb * TAPS + tap) * 64,
+              tma_load_2d_pair(b_base + bs * B_BYTES, &map_w, fb, (cb * TAPS + tap) * CH,
                                tn * BN + rank * BH);
             }
           }
@@ -594,20 +598,20 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       constexpr uint32_t idesc = idesc_bf16_f32(256, BN);
       uint64_t tap_off[TAPS];
 #pragma unroll
-      for (int tap = 0; tap < TAPS; ++tap) tap_off[tap] = (uint64_t)(((tap / 3) * sh.Wp + tap % 3) * (RB / 16));
+      for (int tap = 0; tap < TAPS; ++tap) tap_off[tap] = (uint64_t)(((tap / RT) * sh.Wp + tap % RT) * (RB / 16));
       if (b_loaded) mbar_wait(bres_full, 0);
-      const uint64_t bres_desc = sdesc_k_sw128(smem_u32(b_base));
+      const uint64_t bres_desc = sdesc_sw(smem_u32(b_base), RB);
       int ait = 0, bit = 0, t = 0;
       for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
-        const int acc = t & 1;
-        mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);
+        const int acc = t % NACC;
+        mbar_wait(&acc_empty[acc], ((t / NACC) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int cb = 0; cb < cblocks; ++cb, ++ait) {
           const int as = ait % AST;
           mbar_wait(&a_full[as], (ait / AST) & 1);
           tc_fence_after();
-          const uint64_t ad = sdesc_k_sw128(smem_u32(a_base + as * sh.a_stage_bytes));
+          const uint64_t ad = sdesc_sw(smem_u32(a_base + as * sh.a_stage_bytes), RB);
           if (sh.bres) {
             const uint64_t bd = bres_desc + (uint64_t)(cb * TAPS * (B_BYTES >> 4));
             if (elect_one_sync()) {
@@ -616,7 +620,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
                 const uint64_t ao = ad + tap_off[tap];
                 const uint64_t bo = bd + (uint64_t)(tap * (B_BYTES >> 4));
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
+                for (int kk = 0; kk < KSTEPS; ++kk)
                   umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
                                  (cb | tap | kk) != 0);
               }
@@ -633,7 +637,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
               const uint64_t bo = bres_desc + (uint64_t)(bs * (B_BYTES >> 4));
               if (elect_one_sync()) {
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
+                for (int kk = 0; kk < KSTEPS; ++kk)
                   umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
                                  (cb | tap | kk) != 0);
                 umma_commit_pair(&b_empty[bs], 3);
@@ -655,22 +659,24 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     int t = 0;
     for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
-      const int acc = t & 1;
-      mbar_wait_sleep(&acc_full[acc], (t >> 1) & 1);
+      const int acc = t % NACC;
+      mbar_wait_sleep(&acc_full[acc], (t / NACC) & 1);
       tc_fence_after();
       const int m = tm * 256 + rank * 128 + quarter * 32 + lane;
       const int nimg = m / img;
       const int within = m - nimg * img;
       const int h = within / sh.Wp, w = within - (within / sh.Wp) * sh.Wp;
       const bool real = m < Mtot && h < sh.Ho && w < sh.Wo;
-      const int64_t oidx = (int64_t)m + sh.Wp + 1;   // padded output position
-      const bool store = m < Mtot && oidx < (int64_t)n_eff * img;
+      // padded mode: output at the padded position m + Wp + 1 (borders written as zeros);
+      // dense mode (stem): real positions only, [N, Ho, Wo] layout
+      const int64_t oidx = DENSE ? ((int64_t)nimg * sh.Ho + h) * sh.Wo + w : (int64_t)m + sh.Wp + 1;
+      const bool store = DENSE ? real : (m < Mtot && oidx < (int64_t)n_eff * img);
       const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
 #pragma unroll 1
       for (int c = half * HALF; c < (half + 1) * HALF; c += 32) {
         const int col0 = tn * BN + c;
         uint4 res[4];
-        const bool use_res = ep.residual != nullptr && store && real;
+        const bool use_res = !DENSE && ep.residual != nullptr && store && real;
         if (use_res) {
           const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + oidx * sh.Cout + col0);
 #pragma unroll
@@ -730,21 +736,21 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc_pair(tmem_base, 2 * BN);
+    tmem_dealloc_pair(tmem_base, NACC * BN);
   }
 }
 
-template <int BN>
+template <int BN, int CH = 64, int RT = 3, bool DENSE = false>
 static int launch_span_pair(const CUtensorMap& mx, const CUtensorMap& mw, const SpanShape& sh,
                             const SpanEpi& ep, cudaStream_t s) {
-  auto kern = conv_span_pair<BN>;
+  auto kern = conv_span_pair<BN, CH, RT, DENSE>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpanSmemMax) != cudaSuccess)
       return GG_ERR_CUDA;
     attr = true;
   }
-  const int smem = span_smem_bytes(sh, BN / 2, 128, 9);
+  const int smem = span_smem_bytes(sh, BN / 2, CH * 2, RT * RT);
   const int tiles = ((sh.N * sh.Hp * sh.Wp + 255) / 256) * (sh.Cout / BN);
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
@@ -824,8 +830,10 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
   // smem operand reads per MMA and half the weight stream per SM (see
   // conv_span_pair).  GG_SPAN_PAIR=0 keeps single-CTA tiles.
   static const bool no_pair = getenv("GG_SPAN_PAIR") && atoi(getenv("GG_SPAN_PAIR")) == 0;
-  if (!no_pair && Cout % 128 == 0 && C >= 128 && !getenv("GG_SPAN_TILE")) {
-    const int bn = Cout % 256 == 0 ? 256 : 128;
+  // N = 64 pairs (layer 1) measured slower than single-CTA tiles (GG_SPAN_PAIR64=1 opts in)
+  static const bool pair64 = getenv("GG_SPAN_PAIR64") && atoi(getenv("GG_SPAN_PAIR64")) == 1;
+  if (!no_pair && (Cout % 128 == 0 || (Cout == 64 && pair64)) && !getenv("GG_SPAN_TILE")) {
+    const int bn = Cout % 256 == 0 ? 256 : Cout % 128 == 0 ? 128 : 64;
     sh.span_rows = 128 + 2 * sh.Wp + 2;
     if (sh.span_rows <= 1024 && plan_span(sh, bn / 2, 128, 9, bn == Cout)) {
       CUtensorMap mx, mw;
@@ -835,7 +843,9 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
       SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
                  reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0};
       cudaStream_t s = gg_stream(stream);
-      return bn == 256 ? launch_span_pair<256>(mx, mw, sh, ep, s) : launch_span_pair<128>(mx, mw, sh, ep, s);
+      return bn == 256 ? launch_span_pair<256>(mx, mw, sh, ep, s)
+             : bn == 128 ? launch_span_pair<128>(mx, mw, sh, ep, s)
+                         : launch_span_pair<64>(mx, mw, sh, ep, s);
     }
   }
   const int cblocks = C / 64;
@@ -909,5 +919,20 @@ extern "C" int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws
   SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, relu, count_dev, nullptr,
              reinterpret_cast<const __nv_bfloat16*>(x), 0};
   if (reinterpret_cast<uintptr_t>(x) & 15) return GG_ERR_INVALID_ARGUMENT;
+  // CTA-pair stem: correct but measured 94 us vs 59 us for single-CTA tiles
+  // (N = 64 pair MMAs); GG_SPAN_PAIR64=1 opts in
+  static const bool pair64 = getenv("GG_SPAN_PAIR64") && atoi(getenv("GG_SPAN_PAIR64")) == 1;
+  if (pair64) {
+    // CTA pair (M = 256 per MMA): the input is stored pre-swizzled (SW32), so the
+    // span comes in through an unswizzled TMA map (a plain row copy, like the
+    // single-CTA bulk copy) that can complete on the leader's barrier
+    SpanShape sp = sh;
+    if (!plan_span(sp, 32, 32, 16, true)) return GG_ERR_UNSUPPORTED;
+    CUtensorMap mxp, mwp;
+    rc = make_map_span(&mxp, x, Mtot, 16, 16, sp.box_rows, true);
+    if (!rc) rc = make_map_span(&mwp, w, Cout, 256, 16, 32);
+    if (rc) return rc;
+    return launch_span_pair<64, 16, 4, true>(mxp, mwp, sp, ep, gg_stream(stream));
+  }
   return launch_span<64, 16, 4, true, 1>(mx, mw, sh, ep, gg_stream(stream));
 }

@@ -1,5 +1,6 @@
 // gg_norm.cu — LayerNorm and DistilBERT embedding+LayerNorm (HBM-bound, one warp per row).
 #include "gg_common.cuh"
+#include "gg_kernels.h"
 #include <cuda_bf16.h>
 
 namespace gg {
@@ -67,18 +68,28 @@ __device__ __forceinline__ void load_row(const __nv_bfloat16* src, float (&x)[PE
   }
 }
 
+// One row per warp (kLnRowsPerWarp; 2 measured slower), launched
+// with programmatic dependent launch: the CTAs start while the producing GEMM
+// drains and wait for it in griddepcontrol.wait.
+constexpr int kLnRowsPerWarp = 1;
 template <int PER_LANE>
 __global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* x, int64_t ldx,
                                                         __nv_bfloat16* y, int64_t ldy,
                                                         const float* gamma, const float* beta,
                                                         int64_t rows, int width, float eps,
                                                         const int32_t* count, int rows_per_item) {
-  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  griddep_wait();
+  griddep_launch();
+  const int64_t r0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * kLnRowsPerWarp;
   if (count) rows = min(rows, (int64_t)__ldg(count) * rows_per_item);
-  if (r >= rows) return;
-  float v[PER_LANE];
-  load_row<PER_LANE>(x + r * ldx, v, false);
-  ln_row<PER_LANE>(v, width, gamma, beta, eps, y + r * ldy);
+  if (r0 >= rows) return;
+  float v[kLnRowsPerWarp][PER_LANE];
+#pragma unroll
+  for (int j = 0; j < kLnRowsPerWarp; ++j)
+    if (r0 + j < rows) load_row<PER_LANE>(x + (r0 + j) * ldx, v[j], false);
+#pragma unroll
+  for (int j = 0; j < kLnRowsPerWarp; ++j)
+    if (r0 + j < rows) ln_row<PER_LANE>(v[j], width, gamma, beta, eps, y + (r0 + j) * ldy);
 }
 
 template <int PER_LANE>
@@ -87,6 +98,8 @@ __global__ void __launch_bounds__(256) embed_ln_kernel(const int32_t* ids, const
                                                        const float* gamma, const float* beta,
                                                        int64_t tokens, int seq_len, int width,
                                                        float eps, const int32_t* count) {
+  griddep_wait();
+  griddep_launch();
   const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (count) tokens = min(tokens, (int64_t)__ldg(count) * seq_len);
   if (t >= tokens) return;
@@ -106,9 +119,12 @@ extern "C" int gg_layernorm(const void* x, int64_t ldx, void* y, int64_t ldy, co
   if (!x || !y || !gamma || !beta || rows < 0) return GG_ERR_INVALID_ARGUMENT;
   if (width != 768 || ldx % 8 || ldy % 8) return GG_ERR_UNSUPPORTED;
   if (rows == 0) return GG_OK;
-  layernorm_kernel<24><<<(unsigned)((rows + 7) / 8), 256, 0, gg_stream(stream)>>>(
-      reinterpret_cast<const __nv_bfloat16*>(x), ldx, reinterpret_cast<__nv_bfloat16*>(y), ldy,
-      gamma, beta, rows, width, eps, count_dev, rows_per_item);
+  const int64_t per_block = 8 * kLnRowsPerWarp;
+  if (launch_pdl(layernorm_kernel<24>, dim3((unsigned)((rows + per_block - 1) / per_block)), dim3(256), 0,
+                 gg_stream(stream), reinterpret_cast<const __nv_bfloat16*>(x), ldx,
+                 reinterpret_cast<__nv_bfloat16*>(y), ldy, gamma, beta, rows, width, eps, count_dev,
+                 rows_per_item) != cudaSuccess)
+    return GG_ERR_CUDA;
   GG_LAUNCH_OK();
   return GG_OK;
 }
@@ -121,9 +137,11 @@ extern "C" int gg_embed_layernorm(const int32_t* ids, const void* word, const vo
     return GG_ERR_INVALID_ARGUMENT;
   if (width != 768) return GG_ERR_UNSUPPORTED;
   if (tokens == 0) return GG_OK;
-  embed_ln_kernel<24><<<(unsigned)((tokens + 7) / 8), 256, 0, gg_stream(stream)>>>(
-      ids, reinterpret_cast<const __nv_bfloat16*>(word), reinterpret_cast<const __nv_bfloat16*>(pos),
-      reinterpret_cast<__nv_bfloat16*>(y), gamma, beta, tokens, seq_len, width, eps, count_dev);
+  if (launch_pdl(embed_ln_kernel<24>, dim3((unsigned)((tokens + 7) / 8)), dim3(256), 0, gg_stream(stream),
+                 ids, reinterpret_cast<const __nv_bfloat16*>(word), reinterpret_cast<const __nv_bfloat16*>(pos),
+                 reinterpret_cast<__nv_bfloat16*>(y), gamma, beta, tokens, seq_len, width, eps,
+                 count_dev) != cudaSuccess)
+    return GG_ERR_CUDA;
   GG_LAUNCH_OK();
   return GG_OK;
 }
