@@ -40,6 +40,7 @@ struct GemmEpilogue {
   StreamK sk;                      // stream-K split of the (tile, k-block) space, or disabled
   int raster_n;                    // 1: N-fastest tile order (A larger than ~L2/2), else M-fastest
   long long* prof;                 // debug (GG_GEMM_PROF): per-pair issuer cycles / waits, or null
+  int tma_out;                     // pair kernel: outputs (and residual) through smem + TMA
 };
 
 constexpr int kBK = 64;            // 64 bf16 = 128 B = one swizzle row
@@ -386,6 +387,20 @@ bool streamk_wanted(int64_t tiles, int64_t nkb, int sms) {
   return T / sms >= 4 && sk < 0.93 * dp;
 }
 
+// [rows, cols] bf16 with row pitch ld (elements); box 32 x 32, 64-byte swizzle:
+// the pair GEMM's epilogue staging boxes (TMA store of outputs, TMA load of residuals).
+static int make_map_box32(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld) {
+  if (get_encoder() != GG_OK) return GG_ERR_CUDA;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? GG_OK : GG_ERR_INVALID_ARGUMENT;
+}
+
 static int g_num_sms = 0;
 int num_sms() {
   if (!g_num_sms) {
@@ -445,6 +460,7 @@ constexpr int kPairMaxN = 4096;   // bias staged in smem
 template <int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_res,
                    int M_max, int N, int K, GemmEpilogue ep) {
   constexpr int A_BYTES = 128 * kBK * 2, B_BYTES = 128 * kBK * 2;
   constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -454,8 +470,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;     // [2]
   uint64_t* acc_empty = acc_full + 2;      // [2] (the leader's counts both CTAs' epilogues)
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  float* bias_s = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);   // [N] (N <= kPairMaxN)
+  uint64_t* res_full = acc_empty + 2;      // [8 warps][2 buffers]: residual boxes landed
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(res_full + 2 * kEpiWarps);
+  float* bias_s = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 512);   // [N] (N <= kPairMaxN)
+  // per epilogue warp: two 2 KB staging buffers = the SWIZZLE_64B image of a
+  // 32 x 32 bf16 box (output for the TMA store, residual from a TMA load)
+  uint8_t* stg_base = smem + ((STAGES * STAGE_BYTES + 512 + kPairMaxN * 4 + 1023) & ~1023);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -472,9 +492,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 2);   // one elected arrive per CTA of the pair
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&res_full[i], 1);
     fence_mbar_init();
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
+    if (ep.tma_out) {
+      tma_prefetch(&map_out);
+      if (ep.residual) tma_prefetch(&map_res);
+    }
   }
   if (warp == 1) tmem_alloc_pair(tmem_base_smem, 2 * kPairBN);
   tc_fence_before();
@@ -561,6 +586,136 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = threadIdx.x - 64; i < N; i += 32 * kEpiWarps) bias_s[i] = __ldg(ep.bias + i);
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
     int t = 0;
+    if (ep.tma_out) {
+      // Coalesced epilogue: a thread owns one accumulator row, so direct global
+      // stores / residual loads touch 32 rows (32 L1 wavefronts) per instruction.
+      // Instead each warp stages its 32 x 32 chunk in smem (SW64 image, conflict-
+      // free for row-per-lane 16-B accesses) and moves it with one TMA store; the
+      // residual box arrives by TMA one chunk ahead.
+      uint8_t* stg = stg_base + (warp - 2) * 4096;
+      uint64_t* rb = res_full + (warp - 2) * 2;
+      uint32_t rph0 = 0, rph1 = 0;
+      const bool has_res = ep.residual != nullptr;
+      const int sw = (lane >> 1) & 3;
+      for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
+        const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;
+        const int tn = ep.raster_n ? tile % tiles_n : tile / tiles_m;
+        const int acc = t & 1;
+        const int row0 = tm * 256 + rank * 128 + quarter * 32;   // this warp's 32 rows
+        const int colw = tn * kPairBN + half * (kPairBN / 2);   // this warp's 128 columns
+        const bool rows_ok = row0 < M;
+        if (has_res && rows_ok && lane == 0) {   // residual of chunk 0
+          bulk_wait_read<0>();
+          mbar_expect_tx(&rb[0], 2048);
+          tma_load_2d(stg, &map_res, &rb[0], colw, row0);
+        }
+        mbar_wait_sleep(&acc_full[acc], (t >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * kPairBN + half * (kPairBN / 2);
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          const int b = c & 1;
+          uint8_t* buf = stg + b * 2048;
+          if (rows_ok && lane == 0) {
+            if (has_res) {
+              if (c + 1 < 4) {   // next chunk's residual into the other buffer once its store has read it
+                bulk_wait_read<0>();
+                mbar_expect_tx(&rb[b ^ 1], 2048);
+                tma_load_2d(stg + (b ^ 1) * 2048, &map_res, &rb[b ^ 1], colw + 32 * (c + 1), row0);
+              }
+            } else {
+              bulk_wait_read<1>();   // the store of chunk c - 2 (same buffer) has read it
+            }
+          }
+          __syncwarp();
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tacc + 32 * c, r);
+          tmem_ld_wait();
+          if (!rows_ok) continue;
+          const int col0 = colw + 32 * c;
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if (ep.bias) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + i);
+              v[i] += bb.x; v[i + 1] += bb.y; v[i + 2] += bb.z; v[i + 3] += bb.w;
+            }
+          }
+          uint4* myrow = reinterpret_cast<uint4*>(buf + lane * 64);
+          if (has_res) {
+            if (b == 0) { mbar_wait(&rb[0], rph0); rph0 ^= 1; }
+            else { mbar_wait(&rb[1], rph1); rph1 ^= 1; }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 u = myrow[q ^ sw];
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h2[e]);
+                v[q * 8 + 2 * e] += f.x;
+                v[q * 8 + 2 * e + 1] += f.y;
+              }
+            }
+          }
+          if (ep.act == ACT_RELU) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+          } else if (ep.act == ACT_GELU) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
+          }
+          int gx = col0, gy = row0;
+          if (ep.out_mode == OUT_QKV_HEADS) {
+            // Q (x 1/sqrt(64)) and K boxes into their [B, H, S, 64] planes (the V^T plane
+            // keeps the lane-coalesced transposed path below)
+            const int hd = ep.heads * 64;
+            const int which = col0 / hd, hh = (col0 % hd) / 64;
+            if (which == 2) {
+              const int bq = row0 / ep.seq_len;
+              __nv_bfloat16* plane = reinterpret_cast<__nv_bfloat16*>(ep.D) + 2 * ep.qkv_plane;
+              const int64_t bh = (int64_t)bq * ep.heads + hh;
+              const int s_ = row0 % ep.seq_len + lane, d0 = col0 % 64;
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                plane[(bh * 64 + d0 + i) * ep.seq_len + s_] = __float2bfloat16_rn(v[i]);
+              continue;
+            }
+            if (which == 0) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] *= 0.125f;
+            }
+            gx = col0 % 64;
+            gy = (int)((int64_t)which * (ep.qkv_plane / 64) +
+                       ((int64_t)(row0 / ep.seq_len) * ep.heads + hh) * ep.seq_len + row0 % ep.seq_len);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+            u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+            u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+            u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+            myrow[q ^ sw] = u;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_out, buf, gx, gy);
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (threadIdx.x == 64) {
+          if (rank == 0) mbar_arrive(&acc_empty[acc]);
+          else mbar_arrive_cluster(leader_empty0 + acc * 8);
+        }
+      }
+      if (lane == 0) bulk_wait<0>();
+    }
+    if (!ep.tma_out)
     for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
       const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;
       const int tn = ep.raster_n ? tile % tiles_n : tile / tiles_m;
@@ -616,9 +771,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int STAGES>
-static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
-                            const GemmEpilogue& ep, cudaStream_t s) {
-  constexpr int SMEM = STAGES * 2 * 128 * kBK * 2 + 256 + kPairMaxN * 4 + 1024;
+static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                            const CUtensorMap& mr, int M, int N, int K, const GemmEpilogue& ep,
+                            cudaStream_t s) {
+  constexpr int SMEM = STAGES * 2 * 128 * kBK * 2 + 512 + kPairMaxN * 4 + 1024 + kEpiWarps * 4096 + 1024;
   auto kern = gemm_bf16_pair<STAGES>;
   static bool attr = false;
   if (!attr) {
@@ -651,7 +807,7 @@ static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, int M,
     cudaMemsetAsync(prof, 0, 4096 * sizeof(long long), s);
     e2.prof = prof;
   }
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, M, N, K, e2) != cudaSuccess) return GG_ERR_CUDA;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mo, mr, M, N, K, e2) != cudaSuccess) return GG_ERR_CUDA;
   GG_LAUNCH_OK();
   if (do_prof) {
     long long h[4096];
@@ -699,17 +855,31 @@ extern "C" int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, v
                   e->act, e->out_mode, e->seq_len, e->heads,
                   e->out_mode == OUT_QKV_HEADS ? M * 64 * (int64_t)e->heads : 0,
                   e->count_dev, e->rows_per_item, StreamK{nullptr, nullptr, 0},
-                  M * K * 2 > (48LL << 20) ? 1 : 0, nullptr};
+                  M * K * 2 > (48LL << 20) ? 1 : 0, nullptr, 0};
   cudaStream_t s = gg_stream(stream);
   // CTA pairs for wide GEMMs (tile_n auto, N % 256 == 0, enough 256-row tiles
   // to fill most pairs); GG_NO_PAIR=1 keeps single-CTA tiles
   static const bool no_pair = getenv("GG_NO_PAIR") != nullptr;
   if (!no_pair && e->tile_n == 0 && N % kPairBN == 0 && N <= kPairMaxN && M >= 256 * 16) {
-    CUtensorMap mbp;
+    CUtensorMap mbp, mo, mr;
     rc = make_map_2d(&ma, A, M, K, lda, 128);
     if (!rc) rc = make_map_2d(&mbp, B, N, K, ldb, 128);
     if (rc) return rc;
-    return launch_gemm_pair<6>(ma, mbp, (int)M, (int)N, (int)K, ep, s);
+    // outputs / residuals through smem + TMA (bf16 outputs; dynamic row counts in
+    // multiples of 32 so a 32-row box is all valid or all beyond the batch)
+    static const bool no_tma_out = getenv("GG_NO_TMA_EPI") != nullptr;
+    const bool tma_ok = !no_tma_out && (e->out_mode == OUT_BF16 || e->out_mode == OUT_QKV_HEADS) &&
+                        (!e->count_dev || e->rows_per_item % 32 == 0);
+    mo = ma;
+    mr = ma;
+    if (tma_ok) {
+      if (e->out_mode == OUT_BF16) rc = make_map_box32(&mo, D, M, N, ldd);
+      else rc = make_map_box32(&mo, D, 3 * M * (int64_t)e->heads, 64, 64);
+      if (!rc && e->residual) rc = make_map_box32(&mr, e->residual, M, N, e->ldr);
+      if (rc) return rc;
+      ep.tma_out = 1;
+    }
+    return launch_gemm_pair<5>(ma, mbp, mo, mr, (int)M, (int)N, (int)K, ep, s);
   }
   switch (bn) {
     case 256: return launch_gemm<128, 256, 4>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
