@@ -48,6 +48,7 @@ constexpr int kSpanMaxStages = 16;
 constexpr int kSpanEpiWarps = 8;
 constexpr int kSpanThreads = 64 + 32 * kSpanEpiWarps;
 constexpr int kSpanSmemMax = 227 * 1024;
+constexpr int kSpanStgBytes = 8 * 4096 + 2048;   // pair TMA epilogue staging (+ alignment)
 
 struct SpanShape {
   int N, H, W, C, Cout;
@@ -70,6 +71,7 @@ struct SpanEpi {
   unsigned long long* prof;   // debug (GG_SPAN_PROF): per-CTA globaltimer start / end
   const __nv_bfloat16* x16;   // CH == 16: the pre-swizzled input (bulk-copied)
   int nostore;                // debug (GG_SPAN_NOSTORE): skip the output stores
+  int tma_out;                // pair kernel, padded mode: outputs / residuals via smem + TMA
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -407,6 +409,28 @@ static int make_map_span(CUtensorMap* map, const void* ptr, int64_t rows, int64_
   return r == CUDA_SUCCESS ? GG_OK : GG_ERR_INVALID_ARGUMENT;
 }
 
+// [rows, cols] bf16 (row pitch = cols), box 32 x 32, 64-byte swizzle: the pair
+// conv's TMA epilogue boxes (outputs and residuals in the padded geometry).
+static int make_map_box32(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return GG_ERR_CUDA;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? GG_OK : GG_ERR_INVALID_ARGUMENT;
+}
+
 static int span_smem_bytes(const SpanShape& sh, int bn, int rb, int taps) {
   const int nkb = sh.C / (rb / 2) * taps;
   return sh.a_stages * sh.a_stage_bytes + (sh.bres ? nkb : sh.b_stages) * bn * rb + 1024 + 1024;
@@ -498,6 +522,7 @@ static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanS
 template <int BN, int CH, int RT, bool DENSE>
 __global__ void __launch_bounds__(kSpanThreads, 1)
     conv_span_pair(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+                   const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_res,
                    SpanShape sh, SpanEpi ep) {
   constexpr int RB = CH * 2;                 // bytes per pixel row
   constexpr int KSTEPS = CH / 16;            // MMAs per tap
@@ -521,7 +546,11 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   uint64_t* acc_full = b_empty + kSpanMaxStages;
   uint64_t* acc_empty = acc_full + NACC;
   uint64_t* bres_full = acc_empty + NACC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
+  uint64_t* res_full = bres_full + 1;      // [8 warps][2]: residual boxes landed (TMA epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 2 * kSpanEpiWarps);
+  // TMA epilogue staging: per epilogue warp two 2 KB SW64 images of 32 x 32 bf16 boxes
+  uint8_t* stg_base = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(bars) + 1024 + 1023) & ~uintptr_t(1023));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -542,9 +571,14 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       mbar_init(&acc_empty[i], 2 * kSpanEpiWarps);
     }
     mbar_init(bres_full, 1);
+    for (int i = 0; i < 2 * kSpanEpiWarps; ++i) mbar_init(&res_full[i], 1);
     fence_mbar_init();
     tma_prefetch(&map_x);
     tma_prefetch(&map_w);
+    if (ep.tma_out) {
+      tma_prefetch(&map_out);
+      if (ep.residual) tma_prefetch(&map_res);
+    }
   }
   if (warp == 1) tmem_alloc_pair(tmem_slot, NACC * BN);
   tc_fence_before();
@@ -657,6 +691,116 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     constexpr int HALF = BN / 2;
     const uint32_t leader_empty0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
     int t = 0;
+    if (!DENSE && ep.tma_out) {
+      // Coalesced epilogue (as in gemm_bf16_pair): the warp's 32 consecutive rows m
+      // map to 32 consecutive padded output rows m + Wp + 1, so each 32 x 32 chunk
+      // is one TMA box; rows that are padding (or past the batch) are written as 0.
+      uint8_t* stg = stg_base + (warp - 2) * 4096;
+      uint64_t* rb = res_full + (warp - 2) * 2;
+      uint32_t rph0 = 0, rph1 = 0;
+      const bool has_res = ep.residual != nullptr;
+      const int sw = (lane >> 1) & 3;
+      constexpr int NCH = HALF / 32;   // chunks per warp
+      for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
+        const int tm = tile % tiles_m, tn = tile / tiles_m;
+        const int acc = t % NACC;
+        const int mw = tm * 256 + rank * 128 + quarter * 32;   // the warp's first row
+        const int orow0 = mw + sh.Wp + 1;
+        const int colw = tn * BN + half * HALF;
+        const bool any = mw < Mtot;
+        if (has_res && any && lane == 0) {
+          bulk_wait_read<0>();
+          mbar_expect_tx(&rb[0], 2048);
+          tma_load_2d(stg, &map_res, &rb[0], colw, orow0);
+        }
+        mbar_wait_sleep(&acc_full[acc], (t / NACC) & 1);
+        tc_fence_after();
+        const int m = mw + lane;
+        const int nimg = m / img;
+        const int within = m - nimg * img;
+        const int h = within / sh.Wp, w = within - (within / sh.Wp) * sh.Wp;
+        const bool real = m < Mtot && h < sh.Ho && w < sh.Wo;
+        const uint32_t tcol = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * HALF;
+#pragma unroll 1
+        for (int c = 0; c < NCH; ++c) {
+          const int bsel = c & 1;
+          uint8_t* buf = stg + bsel * 2048;
+          if (any && lane == 0) {
+            if (has_res) {
+              if (c + 1 < NCH) {
+                bulk_wait_read<0>();
+                mbar_expect_tx(&rb[bsel ^ 1], 2048);
+                tma_load_2d(stg + (bsel ^ 1) * 2048, &map_res, &rb[bsel ^ 1], colw + 32 * (c + 1), orow0);
+              }
+            } else {
+              bulk_wait_read<1>();
+            }
+          }
+          __syncwarp();
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tcol + 32 * c, r);
+          tmem_ld_wait();
+          if (!any) continue;
+          const int col0 = colw + 32 * c;
+          uint4* myrow = reinterpret_cast<uint4*>(buf + lane * 64);
+          float v[32];
+          if (has_res) {
+            if (bsel == 0) { mbar_wait(&rb[0], rph0); rph0 ^= 1; }
+            else { mbar_wait(&rb[1], rph1); rph1 ^= 1; }
+          }
+          if (real) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 bb = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + i));
+              v[i] = __uint_as_float(r[i]) + bb.x;
+              v[i + 1] = __uint_as_float(r[i + 1]) + bb.y;
+              v[i + 2] = __uint_as_float(r[i + 2]) + bb.z;
+              v[i + 3] = __uint_as_float(r[i + 3]) + bb.w;
+            }
+            if (has_res) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint4 u = myrow[q ^ sw];
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = __bfloat1622float2(h2[e]);
+                  v[q * 8 + 2 * e] += f.x;
+                  v[q * 8 + 2 * e + 1] += f.y;
+                }
+              }
+            }
+            if (ep.relu) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.0f;   // padding positions / past the batch
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+            u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+            u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+            u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+            myrow[q ^ sw] = u;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_out, buf, col0, orow0);
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_empty0 + acc * 8);
+      }
+      if (lane == 0) bulk_wait<0>();
+    }
+    if (DENSE || !ep.tma_out)
     for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
       const int acc = t % NACC;
@@ -742,7 +886,8 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 
 template <int BN, int CH = 64, int RT = 3, bool DENSE = false>
 static int launch_span_pair(const CUtensorMap& mx, const CUtensorMap& mw, const SpanShape& sh,
-                            const SpanEpi& ep, cudaStream_t s) {
+                            const SpanEpi& ep, cudaStream_t s, const CUtensorMap* mo = nullptr,
+                            const CUtensorMap* mr = nullptr) {
   auto kern = conv_span_pair<BN, CH, RT, DENSE>;
   static bool attr = false;
   if (!attr) {
@@ -750,7 +895,7 @@ static int launch_span_pair(const CUtensorMap& mx, const CUtensorMap& mw, const 
       return GG_ERR_CUDA;
     attr = true;
   }
-  const int smem = span_smem_bytes(sh, BN / 2, CH * 2, RT * RT);
+  const int smem = span_smem_bytes(sh, BN / 2, CH * 2, RT * RT) + (ep.tma_out ? kSpanStgBytes : 0);
   const int tiles = ((sh.N * sh.Hp * sh.Wp + 255) / 256) * (sh.Cout / BN);
   const int pairs = num_sms() / 2;
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
@@ -768,19 +913,20 @@ static int launch_span_pair(const CUtensorMap& mx, const CUtensorMap& mw, const 
   at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  if (cudaLaunchKernelEx(&cfg, kern, mx, mw, sh, ep) != cudaSuccess) return GG_ERR_CUDA;
+  if (cudaLaunchKernelEx(&cfg, kern, mx, mw, mo ? *mo : mx, mr ? *mr : mx, sh, ep) != cudaSuccess)
+    return GG_ERR_CUDA;
   return GG_OK;
 }
 
 // Fill the stage plan: B resident (only with a single N tile) if it fits beside
 // >= 3 A stages, else a B ring; A stages = as many as fit (<= kSpanMaxStages).
-static bool plan_span(SpanShape& sh, int bn, int rb, int taps, bool single_ntile) {
+static bool plan_span(SpanShape& sh, int bn, int rb, int taps, bool single_ntile, int reserve = 0) {
   // several boxes: multiples of 8 rows so each box starts on a swizzle atom
   sh.boxes = (sh.span_rows + 255) / 256;
   sh.box_rows = sh.boxes == 1 ? sh.span_rows : ((sh.span_rows + sh.boxes - 1) / sh.boxes + 7) / 8 * 8;
   sh.a_stage_bytes = (sh.boxes * sh.box_rows * rb + 1023) / 1024 * 1024;
   const int nkb = sh.C / (rb / 2) * taps;
-  const int avail = kSpanSmemMax - 2048;
+  const int avail = kSpanSmemMax - 2048 - reserve;
   const int b_all = nkb * bn * rb;
   if (single_ntile && b_all + 3 * sh.a_stage_bytes <= avail) {   // one N tile: slab fixed
     sh.bres = 1;
@@ -835,17 +981,25 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
   if (!no_pair && (Cout % 128 == 0 || (Cout == 64 && pair64)) && !getenv("GG_SPAN_TILE")) {
     const int bn = Cout % 256 == 0 ? 256 : Cout % 128 == 0 ? 128 : 64;
     sh.span_rows = 128 + 2 * sh.Wp + 2;
-    if (sh.span_rows <= 1024 && plan_span(sh, bn / 2, 128, 9, bn == Cout)) {
-      CUtensorMap mx, mw;
+    // coalesced TMA-box epilogue (GG_NO_TMA_EPI=1 keeps row-per-thread stores)
+    static const bool no_tma_epi = getenv("GG_NO_TMA_EPI") != nullptr;
+    const bool tma_epi = !no_tma_epi;
+    if (sh.span_rows <= 1024 && plan_span(sh, bn / 2, 128, 9, bn == Cout, tma_epi ? kSpanStgBytes : 0)) {
+      CUtensorMap mx, mw, mo, mr;
       int rc = make_map_span(&mx, x, Mtot, C, 64, sh.box_rows);
       if (!rc) rc = make_map_span(&mw, w, Cout, (int64_t)C * 9, 64, bn / 2);
+      if (!rc && tma_epi) rc = make_map_box32(&mo, y, Mtot, Cout);
+      if (!rc && tma_epi && residual) rc = make_map_box32(&mr, residual, Mtot, Cout);
       if (rc) return rc;
       SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
-                 reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0};
+                 reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0,
+                 tma_epi ? 1 : 0};
       cudaStream_t s = gg_stream(stream);
-      return bn == 256 ? launch_span_pair<256>(mx, mw, sh, ep, s)
-             : bn == 128 ? launch_span_pair<128>(mx, mw, sh, ep, s)
-                         : launch_span_pair<64>(mx, mw, sh, ep, s);
+      const CUtensorMap* po = tma_epi ? &mo : nullptr;
+      const CUtensorMap* pr = tma_epi && residual ? &mr : nullptr;
+      return bn == 256 ? launch_span_pair<256>(mx, mw, sh, ep, s, po, pr)
+             : bn == 128 ? launch_span_pair<128>(mx, mw, sh, ep, s, po, pr)
+                         : launch_span_pair<64>(mx, mw, sh, ep, s, po, pr);
     }
   }
   const int cblocks = C / 64;
@@ -888,7 +1042,7 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
   if (!rc) rc = make_map_span(&mw, w, Cout, (int64_t)C * 9, 64, best_bn);
   if (rc) return rc;
   SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
-             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0};
+             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0, 0};
   cudaStream_t s = gg_stream(stream);
   switch (best_bn * 4 + best_mt) {
     case 256 * 4 + 1: return launch_span<256, 64, 3, false, 1>(mx, mw, sh, ep, s);
@@ -917,7 +1071,7 @@ extern "C" int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws
   if (!rc) rc = make_map_span(&mw, w, Cout, 256, 16, 64);
   if (rc) return rc;
   SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, relu, count_dev, nullptr,
-             reinterpret_cast<const __nv_bfloat16*>(x), 0};
+             reinterpret_cast<const __nv_bfloat16*>(x), 0, 0};
   if (reinterpret_cast<uintptr_t>(x) & 15) return GG_ERR_INVALID_ARGUMENT;
   // CTA-pair stem: correct but measured 94 us vs 59 us for single-CTA tiles
   // (N = 64 pair MMAs); GG_SPAN_PAIR64=1 opts in
