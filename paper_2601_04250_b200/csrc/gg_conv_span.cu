@@ -87,7 +87,8 @@ __device__ __forceinline__ uint64_t sdesc_sw(uint32_t addr, int row_bytes) {
 template <int BN, int CH, int RT, bool DENSE, int MT>
 __global__ void __launch_bounds__(kSpanThreads, 1)
     conv_span_tcgen05(const __grid_constant__ CUtensorMap map_x,
-                      const __grid_constant__ CUtensorMap map_w, SpanShape sh, SpanEpi ep) {
+                      const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_out,
+                      const __grid_constant__ CUtensorMap map_res, SpanShape sh, SpanEpi ep) {
   constexpr int RB = CH * 2;                 // bytes per pixel row (one swizzle row)
   constexpr int KSTEPS = CH / 16;            // MMAs per tap
   constexpr int TAPS = RT * RT;
@@ -113,7 +114,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   uint64_t* acc_full = b_empty + kSpanMaxStages;
   uint64_t* acc_empty = acc_full + NACC;
   uint64_t* bres_full = acc_empty + NACC;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
+  uint64_t* res_full = bres_full + 1;      // [8 warps][2]: residual boxes landed (TMA epilogue)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 2 * kSpanEpiWarps);
+  uint8_t* stg_base = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(bars) + 1024 + 1023) & ~uintptr_t(1023));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (ep.prof && threadIdx.x == 0) {
@@ -136,9 +140,14 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       mbar_init(&acc_empty[i], kSpanEpiWarps);
     }
     mbar_init(bres_full, 1);
+    for (int i = 0; i < 2 * kSpanEpiWarps; ++i) mbar_init(&res_full[i], 1);
     fence_mbar_init();
     tma_prefetch(&map_x);
     tma_prefetch(&map_w);
+    if (ep.tma_out) {
+      tma_prefetch(&map_out);
+      if (ep.residual) tma_prefetch(&map_res);
+    }
   }
   if (warp == 1) tmem_alloc(tmem_slot, NACC * ACC_COLS);
   // the weight slab does not depend on the predecessor: start it before the wait
@@ -286,6 +295,113 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     const int half = (warp - 2) >> 2;
     constexpr int HALF = BN / 2;
     int t = 0;
+    if (!DENSE && ep.tma_out) {
+      // Coalesced epilogue (see conv_span_pair): 32 consecutive rows of a warp are 32
+      // consecutive padded output rows -> one TMA box per 32 x 32 chunk, through a
+      // per-warp SW64 staging buffer; the residual box comes in by TMA first.
+      uint8_t* stg = stg_base + (warp - 2) * 4096;
+      uint64_t* rb = res_full + (warp - 2) * 2;
+      uint32_t rph[2] = {0, 0};
+      const bool has_res = ep.residual != nullptr;
+      const int sw = (lane >> 1) & 3;
+      constexpr int NCH = HALF / 32;
+      int gc = 0;   // running chunk counter: staging buffer gc & 1
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+        const int tm = tile % tiles_m, tn = tile / tiles_m;
+        const int acc = t % NACC;
+        const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ACC_COLS;
+#pragma unroll 1
+        for (int mt = 0; mt < MT; ++mt) {
+          const int mw = tm * BM + mt * 128 + quarter * 32;
+          const int orow0 = mw + sh.Wp + 1;
+          const int colw = tn * BN + half * HALF;
+          const bool any = mw < Mtot;
+          const int m = mw + lane;
+          const int nimg = m / img;
+          const int within = m - nimg * img;
+          const int h = within / sh.Wp, w = within - (within / sh.Wp) * sh.Wp;
+          const bool real = m < Mtot && h < sh.Ho && w < sh.Wo;
+#pragma unroll 1
+          for (int c = 0; c < NCH; ++c, ++gc) {
+            const int bsel = gc & 1;
+            uint8_t* buf = stg + bsel * 2048;
+            if (any && lane == 0) {
+              bulk_wait_read<0>();   // earlier stores have read the staging buffers
+              if (has_res) {
+                mbar_expect_tx(&rb[bsel], 2048);
+                tma_load_2d(buf, &map_res, &rb[bsel], colw + 32 * c, orow0);
+              }
+            }
+            __syncwarp();
+            if (mt == 0 && c == 0) {
+              mbar_wait_sleep(&acc_full[acc], (t / NACC) & 1);
+              tc_fence_after();
+            }
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tbase + mt * BN + half * HALF + 32 * c, r);
+            tmem_ld_wait();
+            if (!any) continue;
+            const int col0 = colw + 32 * c;
+            uint4* myrow = reinterpret_cast<uint4*>(buf + lane * 64);
+            float v[32];
+            if (has_res) {
+              mbar_wait(&rb[bsel], rph[bsel]);
+              rph[bsel] ^= 1;
+            }
+            if (real) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4) {
+                const float4 bb = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + i));
+                v[i] = __uint_as_float(r[i]) + bb.x;
+                v[i + 1] = __uint_as_float(r[i + 1]) + bb.y;
+                v[i + 2] = __uint_as_float(r[i + 2]) + bb.z;
+                v[i + 3] = __uint_as_float(r[i + 3]) + bb.w;
+              }
+              if (has_res) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const uint4 u = myrow[q ^ sw];
+                  const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(h2[e]);
+                    v[q * 8 + 2 * e] += f.x;
+                    v[q * 8 + 2 * e + 1] += f.y;
+                  }
+                }
+              }
+              if (ep.relu) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 u;
+              u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+              u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+              u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+              u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+              myrow[q ^ sw] = u;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&map_out, buf, col0, orow0);
+              bulk_commit();
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      }
+      if (lane == 0) bulk_wait<0>();
+    }
+    if (DENSE || !ep.tma_out)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
       const int acc = t % NACC;
@@ -438,7 +554,8 @@ static int span_smem_bytes(const SpanShape& sh, int bn, int rb, int taps) {
 
 template <int BN, int CH, int RT, bool DENSE, int MT>
 static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanShape& sh,
-                       const SpanEpi& ep, cudaStream_t s) {
+                       const SpanEpi& ep, cudaStream_t s, const CUtensorMap* mo = nullptr,
+                       const CUtensorMap* mr = nullptr) {
   auto kern = conv_span_tcgen05<BN, CH, RT, DENSE, MT>;
   static bool attr = false;
   if (!attr) {
@@ -446,7 +563,7 @@ static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanS
       return GG_ERR_CUDA;
     attr = true;
   }
-  const int smem = span_smem_bytes(sh, BN, CH * 2, RT * RT);
+  const int smem = span_smem_bytes(sh, BN, CH * 2, RT * RT) + (ep.tma_out ? kSpanStgBytes : 0);
   const int tiles = ((sh.N * sh.Hp * sh.Wp + 128 * MT - 1) / (128 * MT)) * (sh.Cout / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   SpanEpi e2 = ep;
@@ -461,7 +578,8 @@ static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanS
   static int prof_calls = 0;
   const int prof_at = do_prof ? atoi(getenv("GG_SPAN_PROF")) : 0;
   const bool report = do_prof && ++prof_calls >= (prof_at > 0 ? prof_at : 1);
-  if (launch_pdl(kern, dim3(grid), dim3(kSpanThreads), smem, s, mx, mw, sh, e2) != cudaSuccess)
+  if (launch_pdl(kern, dim3(grid), dim3(kSpanThreads), smem, s, mx, mw, mo ? *mo : mx, mr ? *mr : mx, sh,
+                 e2) != cudaSuccess)
     return GG_ERR_CUDA;
   if (report) {
     prof_calls = 0;
@@ -1036,20 +1154,28 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
     }
   }
   sh.span_rows = 128 * best_mt + 2 * sh.Wp + 2;
-  if (sh.span_rows > 1024 || !plan_span(sh, best_bn, 128, 9, best_bn == Cout)) return GG_ERR_UNSUPPORTED;
-  CUtensorMap mx, mw;
+  static const bool no_tma_epi1 = getenv("GG_NO_TMA_EPI") != nullptr;
+  const bool tma1 = !no_tma_epi1;
+  if (sh.span_rows > 1024 || !plan_span(sh, best_bn, 128, 9, best_bn == Cout, tma1 ? kSpanStgBytes : 0))
+    return GG_ERR_UNSUPPORTED;
+  CUtensorMap mx, mw, mo, mr;
   int rc = make_map_span(&mx, x, Mtot, C, 64, sh.box_rows);
   if (!rc) rc = make_map_span(&mw, w, Cout, (int64_t)C * 9, 64, best_bn);
+  if (!rc && tma1) rc = make_map_box32(&mo, y, Mtot, Cout);
+  if (!rc && tma1 && residual) rc = make_map_box32(&mr, residual, Mtot, Cout);
   if (rc) return rc;
   SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
-             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0, 0};
+             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0,
+             tma1 ? 1 : 0};
   cudaStream_t s = gg_stream(stream);
+  const CUtensorMap* po = tma1 ? &mo : nullptr;
+  const CUtensorMap* pr = tma1 && residual ? &mr : nullptr;
   switch (best_bn * 4 + best_mt) {
-    case 256 * 4 + 1: return launch_span<256, 64, 3, false, 1>(mx, mw, sh, ep, s);
-    case 128 * 4 + 1: return launch_span<128, 64, 3, false, 1>(mx, mw, sh, ep, s);
-    case 128 * 4 + 2: return launch_span<128, 64, 3, false, 2>(mx, mw, sh, ep, s);
-    case 64 * 4 + 2: return launch_span<64, 64, 3, false, 2>(mx, mw, sh, ep, s);
-    default: return launch_span<64, 64, 3, false, 1>(mx, mw, sh, ep, s);
+    case 256 * 4 + 1: return launch_span<256, 64, 3, false, 1>(mx, mw, sh, ep, s, po, pr);
+    case 128 * 4 + 1: return launch_span<128, 64, 3, false, 1>(mx, mw, sh, ep, s, po, pr);
+    case 128 * 4 + 2: return launch_span<128, 64, 3, false, 2>(mx, mw, sh, ep, s, po, pr);
+    case 64 * 4 + 2: return launch_span<64, 64, 3, false, 2>(mx, mw, sh, ep, s, po, pr);
+    default: return launch_span<64, 64, 3, false, 1>(mx, mw, sh, ep, s, po, pr);
   }
 }
 
