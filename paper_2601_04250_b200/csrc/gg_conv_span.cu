@@ -439,6 +439,32 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
           uint32_t r[32];
           tmem_ld_32x32b_x32(tcol + c, r);
           tmem_ld_wait();
+          if (DENSE && !ep.nostore) {
+            // stem (dense output rows): coalesced stores through the warp's smem tile
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + i));
+              v[i] = __uint_as_float(r[i]) + b.x;
+              v[i + 1] = __uint_as_float(r[i + 1]) + b.y;
+              v[i + 2] = __uint_as_float(r[i + 2]) + b.z;
+              v[i + 3] = __uint_as_float(r[i + 3]) + b.w;
+            }
+            if (ep.relu) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+            }
+            uint4 outr[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              outr[q].x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+              outr[q].y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+              outr[q].z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+              outr[q].w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+            }
+            warp_rows_store(stg_base + (warp - 2) * 4096, ep.y, oidx * sh.Cout + col0, store, lane, outr);
+            continue;
+          }
           if (!store) continue;
           float v[32];
           if (real) {
@@ -563,7 +589,7 @@ static int launch_span(const CUtensorMap& mx, const CUtensorMap& mw, const SpanS
       return GG_ERR_CUDA;
     attr = true;
   }
-  const int smem = span_smem_bytes(sh, BN, CH * 2, RT * RT) + (ep.tma_out ? kSpanStgBytes : 0);
+  const int smem = span_smem_bytes(sh, BN, CH * 2, RT * RT) + ((ep.tma_out || DENSE) ? kSpanStgBytes : 0);
   const int tiles = ((sh.N * sh.Hp * sh.Wp + 128 * MT - 1) / (128 * MT)) * (sh.Cout / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
   SpanEpi e2 = ep;
@@ -1190,7 +1216,7 @@ extern "C" int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws
   sh.Ho = Hs; sh.Wo = Ws;
   sh.span_rows = 128 + 3 * sh.Wp + 3;
   if (sh.span_rows > 1024) return GG_ERR_UNSUPPORTED;
-  if (!plan_span(sh, 64, 32, 16, true)) return GG_ERR_UNSUPPORTED;
+  if (!plan_span(sh, 64, 32, 16, true, kSpanStgBytes)) return GG_ERR_UNSUPPORTED;
   const int64_t Mtot = (int64_t)N * sh.Hp * sh.Wp;
   CUtensorMap mx, mw;
   int rc = make_map_span(&mx, x, Mtot, 16, 16, sh.box_rows);

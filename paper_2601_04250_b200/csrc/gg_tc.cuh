@@ -330,3 +330,49 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 }  // namespace tc
 }  // namespace gg
+
+// ---- coalesced row-chunk epilogue through a per-warp smem tile ------------------
+// A TMEM accumulator load gives lane r the 32 columns of row r, so direct global
+// accesses touch 32 rows (32 L1 wavefronts) per instruction.  These helpers move a
+// warp's 32 rows x 32 bf16 columns (64 B per row) through a 2 KB smem tile laid out
+// with the 64-byte swizzle (16-B chunk q of row r at q ^ ((r >> 1) & 3): conflict-
+// free both for row-per-lane and for 4-lanes-per-row access), so each global
+// instruction covers 8 rows x 64 contiguous bytes.  `off` is this lane's element
+// offset of (its row, first column); rows with ok == false are skipped.
+namespace gg {
+namespace tc {
+__device__ __forceinline__ void warp_rows_load(uint8_t* buf, const __nv_bfloat16* base, int64_t off, bool ok,
+                                               int lane, uint4 (&row)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int rr = j * 8 + (lane >> 2), piece = lane & 3;
+    const int64_t o = __shfl_sync(0xffffffffu, off, rr);
+    const bool k = __shfl_sync(0xffffffffu, ok, rr);
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (k) u = __ldg(reinterpret_cast<const uint4*>(base + o) + piece);
+    *reinterpret_cast<uint4*>(buf + rr * 64 + ((piece ^ ((rr >> 1) & 3)) << 4)) = u;
+  }
+  __syncwarp();
+  const int sw = (lane >> 1) & 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) row[q] = *reinterpret_cast<const uint4*>(buf + lane * 64 + ((q ^ sw) << 4));
+  __syncwarp();
+}
+__device__ __forceinline__ void warp_rows_store(uint8_t* buf, __nv_bfloat16* base, int64_t off, bool ok, int lane,
+                                                const uint4 (&row)[4]) {
+  const int sw = (lane >> 1) & 3;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ sw) << 4)) = row[q];
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int rr = j * 8 + (lane >> 2), piece = lane & 3;
+    const int64_t o = __shfl_sync(0xffffffffu, off, rr);
+    const bool k = __shfl_sync(0xffffffffu, ok, rr);
+    const uint4 u = *reinterpret_cast<const uint4*>(buf + rr * 64 + ((piece ^ ((rr >> 1) & 3)) << 4));
+    if (k) reinterpret_cast<uint4*>(base + o)[piece] = u;
+  }
+  __syncwarp();
+}
+}  // namespace tc
+}  // namespace gg
