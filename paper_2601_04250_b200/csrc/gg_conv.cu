@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(256) maxpool3x3s2_blocked(const __nv_bfloat16*
 #pragma unroll
       for (int e = 0; e < 4; ++e) m[i][j][e] = ninf;
   const __nv_bfloat16* img = in + (int64_t)n * H * W * C + c0;
+  const uint64_t pol = l2_policy_evict_first();   // single-use input (kept in L2 by the stem)
 #pragma unroll
   for (int r = 0; r < 2 * kPoolRows + 1; ++r) {
     const int hi = 2 * ho0 - 1 + r;
@@ -502,7 +503,7 @@ __global__ void __launch_bounds__(256) maxpool3x3s2_blocked(const __nv_bfloat16*
     for (int q = 0; q < 2 * kPoolCols + 1; ++q) {
       const int wi = 2 * wo0 - 1 + q;
       if (wi < 0 || wi >= W) continue;
-      const uint4 u = __ldg(reinterpret_cast<const uint4*>(img + ((int64_t)hi * W + wi) * C));
+      const uint4 u = ld_global_nc_v4_hint(img + ((int64_t)hi * W + wi) * C, pol);
       const __nv_bfloat162* v = reinterpret_cast<const __nv_bfloat162*>(&u);
       // input row r feeds output rows i with 2i <= r <= 2i + 2; column q feeds j with 2j <= q <= 2j + 2
 #pragma unroll

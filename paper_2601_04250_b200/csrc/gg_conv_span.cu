@@ -462,7 +462,9 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
               outr[q].z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
               outr[q].w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
             }
-            warp_rows_store(stg_base + (warp - 2) * 4096, ep.y, oidx * sh.Cout + col0, store, lane, outr);
+            // the stem output (103 MB at batch 64) is read once by the max pool right
+            // after: keep it in L2 (evict_last); the pool reads it evict_first
+            warp_rows_store<true>(stg_base + (warp - 2) * 4096, ep.y, oidx * sh.Cout + col0, store, lane, outr);
             continue;
           }
           if (!store) continue;

@@ -358,6 +358,32 @@ __device__ __forceinline__ void warp_rows_load(uint8_t* buf, const __nv_bfloat16
   for (int q = 0; q < 4; ++q) row[q] = *reinterpret_cast<const uint4*>(buf + lane * 64 + ((q ^ sw) << 4));
   __syncwarp();
 }
+// L2 eviction-priority policies (createpolicy): keep a producer's output for the
+// very next kernel, stream a consumer's single-use reads
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_global_v4_hint(void* ptr, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(ptr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_global_nc_v4_hint(const void* ptr, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(ptr), "l"(pol));
+  return v;
+}
+
+template <bool KEEP_L2 = false>
 __device__ __forceinline__ void warp_rows_store(uint8_t* buf, __nv_bfloat16* base, int64_t off, bool ok, int lane,
                                                 const uint4 (&row)[4]) {
   const int sw = (lane >> 1) & 3;
@@ -370,7 +396,10 @@ __device__ __forceinline__ void warp_rows_store(uint8_t* buf, __nv_bfloat16* bas
     const int64_t o = __shfl_sync(0xffffffffu, off, rr);
     const bool k = __shfl_sync(0xffffffffu, ok, rr);
     const uint4 u = *reinterpret_cast<const uint4*>(buf + rr * 64 + ((piece ^ ((rr >> 1) & 3)) << 4));
-    if (k) reinterpret_cast<uint4*>(base + o)[piece] = u;
+    if (k) {
+      if constexpr (KEEP_L2) st_global_v4_hint(reinterpret_cast<uint4*>(base + o) + piece, u, l2_policy_evict_last());
+      else reinterpret_cast<uint4*>(base + o)[piece] = u;
+    }
   }
   __syncwarp();
 }
