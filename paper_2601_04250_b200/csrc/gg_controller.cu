@@ -1314,6 +1314,7 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
   __shared__ double sj[kOutChunk];
   __shared__ int32_t sq[kOutChunk];
   __shared__ double sp[kOutChunk];
+  __shared__ double sew[kOutChunk];   // EWMA after each outcome (energy channel observes)
   __shared__ int64_t slot_off[kOutMaxSlots + 1];
   __shared__ int s_flag, s_first;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1351,6 +1352,14 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
       L = lat[e];
     }
     nan_here |= isnan(L);
+    // a NaN joule makes the EWMA NaN, whose min/max observes are order-dependent in a
+    // way the parallel ordered reduction below does not model: sequential kernel
+    nan_here |= isnan(slots ? 0.0 : jou[e]);
+    if (slots) {
+      int gi = 0;
+      while (e >= slot_off[gi + 1]) ++gi;
+      nan_here |= isnan(slots[(int64_t)gi * (3 * B + 8) + B + (e - slot_off[gi])]);
+    }
   }
   if (__syncthreads_or(nan_here)) {
     if (warp == 0) outcome_seq<S>(p, st, lat, jou, qd, n, set_qd, err, slots, G, B, rank, fifo);
@@ -1466,20 +1475,74 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
     }
     __syncthreads();
     if (tid == 0) {
+      // the order-dependent chains, one thread in CPython order: the EWMA recurrence
+      // (energy.py:24-36, 75-87) and the running total
       #pragma unroll 1
       for (int c = 0; c < nc; ++c) {
         const double J = sj[c];
-        const int32_t Q = sq[c];
-        // EnergyLedger.observe_request -> ewma_update (energy.py:24-36, 75-87)
         ewma = (seen > 0) ? f64_add(f64_mul(lam, ewma), f64_mul(one_minus_lam, J)) : J;
         seen += 1;
         total = f64_add(total, J);
-        p95 = sp[c];
-        ch_observe(ce, ewma);
-        ch_observe(cq, (double)Q);
-        ch_observe(cp, p95);
-        outc += 1;
-        if (set_qd) last_qd = Q;
+        sew[c] = ewma;
+      }
+      outc += nc;
+      if (nc > 0) {
+        p95 = sp[nc - 1];
+        if (set_qd) last_qd = sq[nc - 1];
+      }
+    }
+    __syncthreads();
+    // NormalizerChannel.observe (controller.py:164-168) over each outcome's energy /
+    // queue-depth / p95 value: a fold with "replace only if strictly smaller /
+    // larger", associative without NaNs (guaranteed above) and order-preserving on
+    // ties, so warp 0 folds contiguous segments per lane and combines them in lane
+    // order; lane 0 (thread 0) folds the running channels in first.
+    if (warp == 0 && nc > 0) {
+      const int seg = (nc + 31) / 32;
+      const int c0 = min(nc, lane * seg), c1 = min(nc, c0 + seg);
+      double lo[3], hi[3];
+      bool has = c0 < c1;
+      if (has) {
+        lo[0] = hi[0] = sew[c0];
+        lo[1] = hi[1] = (double)sq[c0];
+        lo[2] = hi[2] = sp[c0];
+        #pragma unroll 1
+        for (int c = c0 + 1; c < c1; ++c) {
+          const double x0 = sew[c], x1 = (double)sq[c], x2 = sp[c];
+          if (x0 < lo[0]) lo[0] = x0;
+          if (x0 > hi[0]) hi[0] = x0;
+          if (x1 < lo[1]) lo[1] = x1;
+          if (x1 > hi[1]) hi[1] = x1;
+          if (x2 < lo[2]) lo[2] = x2;
+          if (x2 > hi[2]) hi[2] = x2;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) lo[k] = hi[k] = 0.0;
+      }
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {   // combine (this, lane + o) as (left, right)
+        const bool rhas = __shfl_down_sync(0xffffffffu, (int)has, o) != 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double rlo = __shfl_down_sync(0xffffffffu, lo[k], o);
+          const double rhi = __shfl_down_sync(0xffffffffu, hi[k], o);
+          if ((lane & (2 * o - 1)) == 0 && lane + o < 32 && rhas) {
+            if (!has || rlo < lo[k]) lo[k] = rlo;
+            if (!has || rhi > hi[k]) hi[k] = rhi;
+          }
+        }
+        if ((lane & (2 * o - 1)) == 0 && lane + o < 32) has = has || rhas;
+      }
+      if (lane == 0 && has) {
+        gg_channel* ch[3] = {&ce, &cq, &cp};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          gg_channel& c = *ch[k];
+          if (!c.seen || lo[k] < c.lo) c.lo = lo[k];
+          if (!c.seen || hi[k] > c.hi) c.hi = hi[k];
+          c.seen = 1;
+        }
       }
     }
     // keep the last min(cap, h + nc) latencies as the next history
@@ -1504,16 +1567,19 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
   const int head_f = (count0 + m_total <= cap) ? head0 : (int)((head0 + (count0 + m_total - cap)) % cap);
   #pragma unroll 1
   for (int j = tid; j < h; j += kOutThreads) st->win[(head_f + j) % cap] = seq[j];
-  // sorted window: bitonic sort of seq[0, h) padded with +inf to 1024 (in place)
+  // sorted window: bitonic sort of seq[0, h) padded with +inf to the next power of
+  // two (in place)
+  int P2 = 1;
+  while (P2 < h) P2 <<= 1;
   #pragma unroll 1
-  for (int j = h + tid; j < GG_P95_WINDOW_MAX; j += kOutThreads) seq[j] = INFINITY;
+  for (int j = h + tid; j < P2; j += kOutThreads) seq[j] = INFINITY;
   __syncthreads();
   #pragma unroll 1
-  for (int size = 2; size <= GG_P95_WINDOW_MAX; size <<= 1) {
+  for (int size = 2; size <= P2; size <<= 1) {
     #pragma unroll 1
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       #pragma unroll 1
-      for (int i = tid; i < GG_P95_WINDOW_MAX; i += kOutThreads) {
+      for (int i = tid; i < P2; i += kOutThreads) {
         const int jx = i ^ stride;
         if (jx > i) {
           const bool up = (i & size) == 0;
