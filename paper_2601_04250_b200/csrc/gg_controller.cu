@@ -1315,6 +1315,7 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
   __shared__ int32_t sq[kOutChunk];
   __shared__ double sp[kOutChunk];
   __shared__ double sew[kOutChunk];   // EWMA after each outcome (energy channel observes)
+  __shared__ int16_t spos[GG_P95_WINDOW_MAX];   // arrival position: stable sort key
   __shared__ int64_t slot_off[kOutMaxSlots + 1];
   __shared__ int s_flag, s_first;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1448,7 +1449,7 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
         int bq = 0;
 #pragma unroll
         for (int q = 1; q < S; ++q)
-          if (v[q] > bv) {
+          if (v[q] >= bv) {   // ties: the later position (q * 32 + lane grows with q)
             bv = v[q];
             bq = q;
           }
@@ -1458,7 +1459,10 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
           const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
           const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
           const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
-          if (ov > bv || (ov == bv && (oq * 32 + ol) < (bq * 32 + bl))) {
+          // ties: the later arrival first — CPython's sorted() is stable, so counting
+          // down from the top of the ascending window, equal values (e.g. -0.0 and
+          // +0.0) come latest-arrival first
+          if (ov > bv || (ov == bv && (oq * 32 + ol) > (bq * 32 + bl))) {
             bv = ov;
             bl = ol;
             bq = oq;
@@ -1573,6 +1577,8 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
   while (P2 < h) P2 <<= 1;
   #pragma unroll 1
   for (int j = h + tid; j < P2; j += kOutThreads) seq[j] = INFINITY;
+  #pragma unroll 1
+  for (int j = tid; j < P2; j += kOutThreads) spos[j] = (int16_t)j;
   __syncthreads();
   #pragma unroll 1
   for (int size = 2; size <= P2; size <<= 1) {
@@ -1582,11 +1588,17 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
       for (int i = tid; i < P2; i += kOutThreads) {
         const int jx = i ^ stride;
         if (jx > i) {
+          // keys (value, arrival position): the result is CPython's stable sorted()
+          // (equal values such as -0.0 / +0.0 keep their arrival order)
           const bool up = (i & size) == 0;
           const double a = seq[i], b = seq[jx];
-          if ((a > b) == up) {
+          const int16_t pa = spos[i], pb = spos[jx];
+          const bool a_gt_b = a > b || (a == b && pa > pb);
+          if (a_gt_b == up) {
             seq[i] = b;
             seq[jx] = a;
+            spos[i] = pb;
+            spos[jx] = pa;
           }
         }
       }

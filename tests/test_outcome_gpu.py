@@ -42,3 +42,63 @@ def test_outcome_windows(window):
         assert cnt == o.win_count and s.win_head == o.win_head
         assert list(s.win)[:window] == list(o.win)[:window]
         assert list(s.win_sorted)[:cnt] == sorted(list(o.win)[:cnt])
+
+
+@pytest.mark.parametrize("case", ["signed_zeros", "nan_joules", "inf_joules"])
+def test_outcome_special_values(case):
+    """Edge values of the parallel K2 against the CPython restatement
+    (oracle/controller_oracle.py, stable sorted() like the reference): -0.0 / +0.0
+    ties (the nearest-rank element and the sorted window follow the stable order;
+    the normalizer folds keep the first occurrence), a NaN joule (sequential
+    fallback: the NaN EWMA poisons the energy channel in CPython's order) and
+    +inf joules.  Compared bit for bit, signed zeros included."""
+    import math
+    import struct
+
+    import torch
+    import paper_2601_04250_b200 as gg
+    from oracle import controller_oracle as co
+
+    def bits(x):
+        return None if x is None else struct.pack("<d", x)
+
+    def chan(lo, hi, seen):
+        return (bits(lo), bits(hi)) if seen else None
+
+    rng = np.random.default_rng(7)
+    orc = co.OracleController(co.OracleParams(tau0=0.5, tau_inf=0.5, k=1.0, ewma_lambda=0.9))
+    ctl = gg.ControllerConfig(tau0=0.5, tau_inf=0.5, k=1.0).build(gg.EnergyLedger(), p95_window=100)
+    for chunk in range(3):
+        n = 90
+        lat = rng.choice([0.0, -0.0, 1.5, 2.5], size=n)
+        jo = rng.choice([0.0, -0.0, 1.0], size=n)
+        if case == "nan_joules" and chunk == 1:
+            jo[17] = np.nan
+        if case == "inf_joules" and chunk == 1:
+            jo[5] = np.inf
+        qd = rng.integers(0, 3, size=n).astype(np.int32)
+        for a, b, c in zip(lat.tolist(), jo.tolist(), qd.tolist()):
+            orc.record_outcome(a, b, c)
+        ctl.record_outcomes(torch.from_numpy(lat).cuda(), torch.from_numpy(jo).cuda(),
+                            torch.from_numpy(qd).cuda())
+        s = ctl.state_struct()
+        want = orc.state_tuple()
+        assert bits(s.p95_current) == bits(want["p95_current"]), (case, chunk)
+        assert bits(s.ewma_joules_per_request) == bits(orc.ewma) or (
+            math.isnan(s.ewma_joules_per_request) and math.isnan(orc.ewma)), (case, chunk)
+        assert bits(s.total_joules) == bits(orc.total_joules) or math.isnan(orc.total_joules)
+        for got, o in ((s.n_energy, orc.energy), (s.n_queue_depth, orc.queue), (s.n_p95_ms, orc.p95)):
+            g = chan(got.lo, got.hi, got.seen)
+            w = chan(o.lo, o.hi, o.lo is not None)
+            if w is not None and any(math.isnan(v) for v in (o.lo, o.hi)):
+                assert all(math.isnan(a) == math.isnan(b) for a, b in
+                           ((got.lo, o.lo), (got.hi, o.hi))), (case, chunk)
+            else:
+                assert g == w, (case, chunk)
+        cnt = s.win_count
+        if case == "nan_joules":
+            # the sequential fallback keeps its sorted window by value only (the order
+            # of -0.0 / +0.0 inside it is internal; p95 and channels are checked above)
+            assert list(s.win_sorted)[:cnt] == sorted(orc.latencies)
+        else:
+            assert [bits(x) for x in list(s.win_sorted)[:cnt]] == [bits(x) for x in sorted(orc.latencies)]
