@@ -39,6 +39,7 @@
 
 #include "gg_common.cuh"
 #include "gg_kernels.h"
+#include "gg_streamk.cuh"
 #include "gg_tc.cuh"
 
 namespace gg {
@@ -72,6 +73,7 @@ struct SpanEpi {
   const __nv_bfloat16* x16;   // CH == 16: the pre-swizzled input (bulk-copied)
   int nostore;                // debug (GG_SPAN_NOSTORE): skip the output stores
   int tma_out;                // pair kernel, padded mode: outputs / residuals via smem + TMA
+  StreamK sk;                 // pair kernel: stream-K over (pair tile, channel block), or disabled
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -749,10 +751,13 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       int ait = 0, bit = 0;
-      for (int tile = pair; tile < num_tiles; tile += npairs) {
+      SkSched sc(ep.sk.enabled, num_tiles, cblocks, pair, npairs);
+      SkWork wk;
+      while (sc.next(wk)) {
+        const int tile = wk.tile;
         const int tm = tile % tiles_m, tn = tile / tiles_m;
         const int m0 = tm * 256 + rank * 128;
-        for (int cb = 0; cb < cblocks; ++cb, ++ait) {
+        for (int cb = wk.kb0; cb < wk.kb1; ++cb, ++ait) {
           const int as = ait % AST;
           mbar_wait_sleep(&a_empty[as], ((ait / AST) & 1) ^ 1);
           uint8_t* sa = a_base + as * sh.a_stage_bytes;
@@ -782,12 +787,14 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       if (b_loaded) mbar_wait(bres_full, 0);
       const uint64_t bres_desc = sdesc_sw(smem_u32(b_base), RB);
       int ait = 0, bit = 0, t = 0;
-      for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
+      SkSched sc(ep.sk.enabled, num_tiles, cblocks, pair, npairs);
+      SkWork wk;
+      for (; sc.next(wk); ++t) {
         const int acc = t % NACC;
         mbar_wait(&acc_empty[acc], ((t / NACC) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int cb = 0; cb < cblocks; ++cb, ++ait) {
+        for (int cb = wk.kb0; cb < wk.kb1; ++cb, ++ait) {
           const int as = ait % AST;
           mbar_wait(&a_full[as], (ait / AST) & 1);
           tc_fence_after();
@@ -802,7 +809,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
                 for (int kk = 0; kk < KSTEPS; ++kk)
                   umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
-                                 (cb | tap | kk) != 0);
+                                 (cb != wk.kb0 || tap != 0 || kk != 0));
               }
               umma_commit_pair(&a_empty[as], 3);
             }
@@ -819,7 +826,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
                 for (int kk = 0; kk < KSTEPS; ++kk)
                   umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
-                                 (cb | tap | kk) != 0);
+                                 (cb != wk.kb0 || tap != 0 || kk != 0));
                 umma_commit_pair(&b_empty[bs], 3);
                 if (tap == TAPS - 1) umma_commit_pair(&a_empty[as], 3);
               }
@@ -847,9 +854,56 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       const bool has_res = ep.residual != nullptr;
       const int sw = (lane >> 1) & 3;
       constexpr int NCH = HALF / 32;   // chunks per warp
-      for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
+      SkSched sc(ep.sk.enabled, num_tiles, cblocks, pair, npairs);
+      SkWork wk;
+      for (; sc.next(wk); ++t) {
+        const int tile = wk.tile;
         const int tm = tile % tiles_m, tn = tile / tiles_m;
         const int acc = t % NACC;
+        // stream-K: a tile cut between pairs is reduced by its last arriving segment;
+        // each (rank, epilogue warp) region of 32 rows x HALF columns has its own
+        // arrival / ready counters and fp32 partial slots (column-major: coalesced)
+        const bool partial = wk.kb0 != 0 || wk.kb1 != cblocks;
+        const int region = (int)rank * kSpanEpiWarps + (warp - 2);
+        constexpr int kRegions = 2 * kSpanEpiWarps;
+        int c_first = 0, c_last = 0;
+        if (partial) {
+          c_first = sc.cta_of((int64_t)tile * cblocks);
+          c_last = sc.cta_of((int64_t)tile * cblocks + cblocks - 1);
+          const int nseg = c_last - c_first + 1;
+          int* cnt = ep.sk.cnt + ((int64_t)tile * kRegions + region) * 2;
+          mbar_wait_sleep(&acc_full[acc], (t / NACC) & 1);
+          tc_fence_after();
+          int arrive = 0;
+          if (lane == 0) arrive = atomicAdd(cnt, 1);
+          arrive = __shfl_sync(0xffffffffu, arrive, 0);
+          if (arrive < nseg - 1) {   // write this segment's partial and leave
+            const int slot = (tile == (int)(sc.start_of(pair) / cblocks)) ? 0 : 1;
+            float* dst = ep.sk.ws + (((int64_t)pair * 2 + slot) * kRegions + region) * (32 * HALF);
+            const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * HALF;
+#pragma unroll 1
+            for (int c = 0; c < NCH; ++c) {
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(tb + 32 * c, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) __stcg(dst + (32 * c + i) * 32 + lane, __uint_as_float(r[i]));
+            }
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(cnt + 1, 1);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(leader_empty0 + acc * 8);
+            continue;
+          }
+          while (ld_acquire(cnt + 1) < nseg - 1) __nanosleep(64);
+          __syncwarp();
+          if (lane == 0) {   // reset for the next launch (stream-ordered)
+            cnt[0] = 0;
+            cnt[1] = 0;
+          }
+        }
         const int mw = tm * 256 + rank * 128 + quarter * 32;   // the warp's first row
         const int orow0 = mw + sh.Wp + 1;
         const int colw = tn * BN + half * HALF;
@@ -859,8 +913,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
           mbar_expect_tx(&rb[0], 2048);
           tma_load_2d(stg, &map_res, &rb[0], colw, orow0);
         }
-        mbar_wait_sleep(&acc_full[acc], (t / NACC) & 1);
-        tc_fence_after();
+        if (!partial) {
+          mbar_wait_sleep(&acc_full[acc], (t / NACC) & 1);
+          tc_fence_after();
+        }
         const int m = mw + lane;
         const int nimg = m / img;
         const int within = m - nimg * img;
@@ -886,6 +942,28 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
           uint32_t r[32];
           tmem_ld_32x32b_x32(tcol + 32 * c, r);
           tmem_ld_wait();
+          if (partial) {   // k-ordered sum of the tile's segments (deterministic)
+            float accv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) accv[i] = 0.0f;
+#pragma unroll 1
+            for (int seg = c_first; seg <= c_last; ++seg) {
+              if (seg == pair) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) accv[i] += __uint_as_float(r[i]);
+              } else {
+                const int slot = (tile == (int)(sc.start_of(seg) / cblocks)) ? 0 : 1;
+                const float* src = ep.sk.ws + (((int64_t)seg * 2 + slot) * kRegions + region) * (32 * HALF);
+                float pv[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) pv[i] = __ldcg(src + (32 * c + i) * 32 + lane);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) accv[i] += pv[i];
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(accv[i]);
+          }
           if (!any) continue;
           const int col0 = colw + 32 * c;
           uint4* myrow = reinterpret_cast<uint4*>(buf + lane * 64);
@@ -1044,7 +1122,7 @@ static int launch_span_pair(const CUtensorMap& mx, const CUtensorMap& mw, const 
   const int smem = span_smem_bytes(sh, BN / 2, CH * 2, RT * RT) + (ep.tma_out ? kSpanStgBytes : 0);
   const int tiles = ((sh.N * sh.Hp * sh.Wp + 255) / 256) * (sh.Cout / BN);
   const int pairs = num_sms() / 2;
-  const int grid = 2 * (tiles < pairs ? tiles : pairs);
+  const int grid = ep.sk.enabled ? 2 * pairs : 2 * (tiles < pairs ? tiles : pairs);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kSpanThreads);
@@ -1139,8 +1217,25 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
       if (rc) return rc;
       SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
                  reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0,
-                 tma_epi ? 1 : 0};
+                 tma_epi ? 1 : 0, StreamK{nullptr, nullptr, 0}};
       cudaStream_t s = gg_stream(stream);
+      // stream-K over (pair tile, channel block) for pair tiles that leave the last
+      // wave mostly empty (layer 4: 42 tiles on 74 pairs).  Opt-in (GG_SPAN_SK=1):
+      // correct and deterministic (test_span_pair_stream_k) but measured slower at
+      // every ResNet-18 stage (e.g. layer 4: 39 vs 30 us per conv) — the partial
+      // regions' global round trip and the per-item pipeline drains cost more than
+      // the idle SMs of the data-parallel schedule.
+      {
+        const int64_t tiles = (Mtot + 255) / 256 * (Cout / bn);
+        const int P = num_sms() / 2;
+        const char* env = getenv("GG_SPAN_SK");
+        const bool want = env && atoi(env) == 1;
+        if (tma_epi && want && tiles * (C / 64) >= 2 * P) {
+          bool ok = false;
+          StreamK sk = streamk_workspace(s, (int64_t)P * 2 * 16 * 32 * (bn / 2), tiles * 16 * 2, ok);
+          if (ok) ep.sk = sk;
+        }
+      }
       const CUtensorMap* po = tma_epi ? &mo : nullptr;
       const CUtensorMap* pr = tma_epi && residual ? &mr : nullptr;
       return bn == 256 ? launch_span_pair<256>(mx, mw, sh, ep, s, po, pr)
@@ -1194,7 +1289,7 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
   if (rc) return rc;
   SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
              reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0,
-             tma1 ? 1 : 0};
+             tma1 ? 1 : 0, StreamK{nullptr, nullptr, 0}};
   cudaStream_t s = gg_stream(stream);
   const CUtensorMap* po = tma1 ? &mo : nullptr;
   const CUtensorMap* pr = tma1 && residual ? &mr : nullptr;
@@ -1225,7 +1320,7 @@ extern "C" int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws
   if (!rc) rc = make_map_span(&mw, w, Cout, 256, 16, 64);
   if (rc) return rc;
   SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, relu, count_dev, nullptr,
-             reinterpret_cast<const __nv_bfloat16*>(x), 0, 0};
+             reinterpret_cast<const __nv_bfloat16*>(x), 0, 0, StreamK{nullptr, nullptr, 0}};
   if (reinterpret_cast<uintptr_t>(x) & 15) return GG_ERR_INVALID_ARGUMENT;
   // CTA-pair stem: correct but measured 94 us vs 59 us for single-CTA tiles
   // (N = 64 pair MMAs); GG_SPAN_PAIR64=1 opts in
