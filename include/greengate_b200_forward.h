@@ -110,6 +110,15 @@ int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const v
  * shifted views of ONE TMA-loaded span per 64-channel block.  w is BN-folded
  * [Cout, C/64, 3, 3, 64] (K order: channel block, tap, channel); C, Cout % 64
  * == 0; residual (optional) in the same padded layout. */
+/* First block of a ResNet stage: conv1 3x3 / stride 2 (+ folded BN, ReLU) on the
+ * previous stage's zero-bordered [N, H, W, C] buffer fused with the 1x1 / stride-2
+ * downsample (+ folded BN, no ReLU) of the same input — the downsample reads the
+ * 3x3's centre-tap tiles.  w: [Cout, 9*C] (r, s, c order), w_ds: [Cout, C]; y and
+ * y_ds zero-bordered [N, Ho+2, Wo+2, Cout].  C % 64 == 0, Cout % 128 == 0. */
+int gg_conv2d_ds(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
+                 int32_t Cout, const float* bias, void* y, const void* w_ds, const float* bias_ds,
+                 void* y_ds, const int32_t* count_dev, void* stream);
+
 int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
                       int32_t Cout, const float* bias, const void* residual, int32_t relu,
                       void* y, const int32_t* count_dev, void* stream);

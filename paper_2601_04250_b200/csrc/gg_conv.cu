@@ -42,17 +42,20 @@ struct ConvEpi {
   const int32_t* count;           // device image count (dynamic batch) or null
   int out_pad;                    // 1: y (and residual) are [N, Ho+2, Wo+2, Cout] zero-bordered
   StreamK sk;                     // stream-K split (TMA im2col mode only), or disabled
+  __nv_bfloat16* y_ds;            // DS: the fused 1x1 / stride-2 downsample output (no ReLU)
+  const float* bias_ds;           // DS: its folded-BN bias
 };
 
 constexpr int kConvProdWarps = 4;
 constexpr int kConvThreads = 32 * (kConvProdWarps + 1 + 4);
 constexpr int kLag = 2;  // cp.async groups in flight per producer thread
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool DS = false>
 struct ConvSmem {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  // DS: a second weight slab per stage (the downsample's, used at the centre tap)
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES * (DS ? 2 : 1);
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
@@ -76,11 +79,18 @@ __device__ __forceinline__ void cp_async_wait() {
 // MODE 2 (C == 16, the space-to-depth stem): a 64-wide k-block is 4 taps; each
 //   tap is one im2col load of 128 pixels x 16 channels (32B-swizzled) that one
 //   UMMA K-step consumes.
-template <int BN, int STAGES, int MODE>
+// DS (MODE 1, 3x3 / stride 2 on a padded input): the block's 1x1 / stride-2
+//   downsample reads exactly the centre tap's A tiles, so it rides along — a
+//   second weight slab per centre-tap stage and a second TMEM accumulator — instead
+//   of a separate kernel re-loading the input.
+template <int BN, int STAGES, int MODE, bool DS = false>
 __global__ void __launch_bounds__(kConvThreads, 1)
     conv_bf16_tcgen05(const __nv_bfloat16* __restrict__ x, const __grid_constant__ CUtensorMap map_w,
-                      const __grid_constant__ CUtensorMap map_x, ConvShape sh, ConvEpi ep) {
-  using L = ConvSmem<BN, STAGES>;
+                      const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_wds,
+                      ConvShape sh, ConvEpi ep) {
+  static_assert(!DS || (MODE == 1 && 4 * BN <= 512), "DS: TMA im2col, two double-buffered accumulators");
+  using L = ConvSmem<BN, STAGES, DS>;
+  constexpr int NACC_COLS = (DS ? 2 : 1) * BN;   // TMEM columns per accumulator buffer
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // Resident-B mode (sh.bres, im2col modes, one N tile): the whole BN x Kpad
@@ -117,7 +127,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     fence_mbar_init();
     tma_prefetch(&map_w);
   }
-  if (warp == kConvProdWarps) tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == kConvProdWarps) tmem_alloc(tmem_slot, 2 * NACC_COLS);
   if (b_loaded && threadIdx.x == 0) {   // weights: independent of the predecessor
     mbar_expect_tx(b_full, num_kb * L::B_BYTES);
     for (int kb = 0; kb < num_kb; ++kb) tma_load_2d(bres + kb * L::B_BYTES, &map_w, b_full, kb * 64, 0);
@@ -150,7 +160,12 @@ __global__ void __launch_bounds__(kConvThreads, 1)
           const int s = it % nst;
           mbar_wait_sleep(&empty[s], ((it / nst) & 1) ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
-          mbar_expect_tx(&full[s], sh.bres ? L::A_BYTES : L::STAGE_BYTES);
+          {
+            uint32_t bytes = sh.bres ? L::A_BYTES : L::A_BYTES + L::B_BYTES;
+            if constexpr (DS)
+              if (kb / cblocks == (sh.R * sh.S) / 2) bytes += L::B_BYTES;
+            mbar_expect_tx(&full[s], bytes);
+          }
           constexpr int kLoads = MODE == 1 ? 1 : 4;
 #pragma unroll
           for (int q = 0; q < kLoads; ++q) {
@@ -171,6 +186,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                 : "memory");
           }
           if (!sh.bres) tma_load_2d(sa + L::A_BYTES, &map_w, &full[s], kb * 64, tn * BN);
+          if constexpr (DS) {   // centre tap: the downsample's weights for this channel block
+            const int tap = kb / cblocks;
+            if (tap == (sh.R * sh.S) / 2)
+              tma_load_2d(sa + L::A_BYTES + L::B_BYTES, &map_wds, &full[s], (kb - tap * cblocks) * 64, tn * BN);
+          }
         }
       }
     }
@@ -237,7 +257,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const uint32_t use = t >> 1;
         mbar_wait(&acc_empty[acc], (use & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * NACC_COLS;
         for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
           const int s = it % nst;
           mbar_wait(&full[s], (it / nst) & 1);
@@ -250,6 +270,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
               umma_bf16(d_tmem, MODE == 2 ? sdesc_k_sw32(sa + kk * 4096) : sdesc_k_sw128(sa + kk * 32),
                         sdesc_k_sw128(sb + kk * 32), idesc,
                         (kb != w.kb0 || kk != 0));
+            if constexpr (DS) {
+              const int cbl = sh.C / 64, tap = kb / cbl;
+              if (tap == (sh.R * sh.S) / 2) {   // downsample accumulator: K = Cin (centre tap only)
+                const uint32_t sd = sa + L::A_BYTES + L::B_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  umma_bf16(d_tmem + BN, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sd + kk * 32), idesc,
+                            (kb - tap * cbl) != 0 || kk != 0);
+              }
+            }
             umma_commit(&empty[s]);
           }
           __syncwarp();
@@ -269,7 +299,8 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       const int acc = t & 1;
       mbar_wait_sleep(&acc_full[acc], (t >> 1) & 1);
       tc_fence_after();
-      const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      const uint32_t tacc0 = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NACC_COLS;
+      const uint32_t tacc = tacc0;
       const bool partial = w.kb0 != 0 || w.kb1 != num_kb;
       SkFix fx;
       if (partial) {   // stream-K: the last arriving segment reduces and stores the tile
@@ -296,9 +327,14 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         oidx = ((int64_t)n * (sh.Ho + 2) + ho + 1) * (sh.Wo + 2) + wo + 1;
       }
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int cc = 0; cc < (DS ? 2 : 1) * BN; cc += 32) {
+        // DS: columns [BN, 2 BN) of the buffer are the downsample accumulator
+        const bool dsp = DS && cc >= BN;
+        const int c = dsp ? cc - BN : cc;
+        __nv_bfloat16* yout = dsp ? ep.y_ds : ep.y;
+        const float* bvec = dsp ? ep.bias_ds : ep.bias;
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tacc + c, r);
+        tmem_ld_32x32b_x32(tacc + cc, r);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
@@ -308,13 +344,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int col0 = tn * BN + c;
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
-          const float4 b = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + i));
+          const float4 b = __ldg(reinterpret_cast<const float4*>(bvec + col0 + i));
           v[i] += b.x;
           v[i + 1] += b.y;
           v[i + 2] += b.z;
           v[i + 3] += b.w;
         }
-        if (ep.residual) {
+        if (ep.residual && !dsp) {
           const uint4* rp = reinterpret_cast<const uint4*>(ep.residual + oidx * sh.Cout + col0);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -328,11 +364,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
             }
           }
         }
-        if (ep.relu) {
+        if (ep.relu && !dsp) {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
         }
-        uint4* dp = reinterpret_cast<uint4*>(ep.y + oidx * sh.Cout + col0);
+        uint4* dp = reinterpret_cast<uint4*>(yout + oidx * sh.Cout + col0);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint4 u;
@@ -351,15 +387,16 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   __syncthreads();
   if (warp == kConvProdWarps) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * BN);
+    tmem_dealloc(tmem_base, 2 * NACC_COLS);
   }
 }
 
-template <int BN, int STAGES, int MODE>
+template <int BN, int STAGES, int MODE, bool DS = false>
 static int launch_conv(const __nv_bfloat16* x, const CUtensorMap& mw, const CUtensorMap& mx,
-                       const ConvShape& sh, const ConvEpi& ep, cudaStream_t s) {
-  using L = ConvSmem<BN, STAGES>;
-  auto kern = conv_bf16_tcgen05<BN, STAGES, MODE>;
+                       const ConvShape& sh, const ConvEpi& ep, cudaStream_t s,
+                       const CUtensorMap* mwds = nullptr) {
+  using L = ConvSmem<BN, STAGES, DS>;
+  auto kern = conv_bf16_tcgen05<BN, STAGES, MODE, DS>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
@@ -370,7 +407,8 @@ static int launch_conv(const __nv_bfloat16* x, const CUtensorMap& mw, const CUte
   const int grid = ep.sk.enabled ? num_sms() : (tiles < num_sms() ? tiles : num_sms());
   const int smem = sh.bres ? sh.bres_stages * L::STAGE_BYTES + (sh.Kpad / 64) * L::B_BYTES + 256 + 1024
                            : L::TOTAL;
-  if (launch_pdl(kern, dim3(grid), dim3(kConvThreads), smem, s, x, mw, mx, sh, ep) != cudaSuccess)
+  if (launch_pdl(kern, dim3(grid), dim3(kConvThreads), smem, s, x, mw, mx, mwds ? *mwds : mw, sh, ep) !=
+      cudaSuccess)
     return GG_ERR_CUDA;
   return GG_OK;
 }
@@ -600,7 +638,7 @@ extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t
   sh.M = (int)M;
   ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
              reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, out_pad,
-             StreamK{nullptr, nullptr, 0}};
+             StreamK{nullptr, nullptr, 0}, nullptr, nullptr};
   // N tile: minimize the larger of (tensor time of the busiest SM) and (operand
   // bytes streamed from L2: every tile re-reads its A rows and its B columns per
   // k-block).  Measured on B200: ~8 TB/s of TMA operand traffic, MMA 128xBN x K16
@@ -666,6 +704,37 @@ extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t
     case 128: return launch_conv<128, 6, 0>(xb, mw, mx, sh, ep, s);
     default: return launch_conv<64, 8, 0>(xb, mw, mx, sh, ep, s);
   }
+}
+
+extern "C" int gg_conv2d_ds(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
+                            int32_t Cout, const float* bias, void* y, const void* w_ds,
+                            const float* bias_ds, void* y_ds, const int32_t* count_dev, void* stream) {
+  // 3x3 / stride 2 (+ folded BN + ReLU) on a zero-bordered [N, H, W, C] input (pad 0)
+  // fused with the block's 1x1 / stride 2 downsample (+ folded BN, no ReLU) of the
+  // same input: both outputs zero-bordered [N, Ho+2, Wo+2, Cout]
+  if (!x || !w || !y || !bias || !w_ds || !bias_ds || !y_ds || N <= 0 || H < 3 || W < 3)
+    return GG_ERR_INVALID_ARGUMENT;
+  if (C % 64 || Cout % 128) return GG_ERR_UNSUPPORTED;
+  ConvShape sh;
+  sh.N = N; sh.H = H; sh.W = W; sh.C = C; sh.Cout = Cout;
+  sh.R = 3; sh.S = 3; sh.stride = 2; sh.pad = 0; sh.pad_hi = 0; sh.Kpad = 9 * C;
+  sh.bres = 0;
+  sh.bres_stages = 0;
+  sh.Ho = (H - 3) / 2 + 1;
+  sh.Wo = (W - 3) / 2 + 1;
+  const int64_t M = (int64_t)N * sh.Ho * sh.Wo;
+  if (M > 0x7fffffff) return GG_ERR_UNSUPPORTED;
+  sh.M = (int)M;
+  ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, 1, count_dev, 1,
+             StreamK{nullptr, nullptr, 0}, reinterpret_cast<__nv_bfloat16*>(y_ds), bias_ds};
+  constexpr int BN = 128;
+  CUtensorMap mw, mwds, mx;
+  int rc = make_map_2d(&mw, w, Cout, sh.Kpad, sh.Kpad, BN);
+  if (!rc) rc = make_map_2d(&mwds, w_ds, Cout, C, C, BN);
+  if (!rc) rc = make_map_im2col(&mx, x, sh, 64);
+  if (rc) return rc;
+  return launch_conv<BN, 4, 1, true>(reinterpret_cast<const __nv_bfloat16*>(x), mw, mx, sh, ep,
+                                     gg_stream(stream), &mwds);
 }
 
 extern "C" int gg_nchw_to_nhwc(const float* x, int32_t N, int32_t C, int32_t H, int32_t W,

@@ -223,6 +223,13 @@ class ResNet18B200:
     # nine taps); GG_RESNET_IM2COL_STAGES="2,3" selects the alternative.
     IM2COL_STAGES = ()
 
+    # stride-2 conv1 + 1x1 downsample of a stage's first block as one kernel
+    # (gg_conv2d_ds); GG_RESNET_SPLIT_DS=1 runs them as two
+    @property
+    def fused_ds(self) -> bool:
+        import os
+        return os.environ.get("GG_RESNET_SPLIT_DS") != "1"
+
     def _stride1(self, conv, bn, dev, stage):
         import os
         env = os.environ.get("GG_RESNET_IM2COL_STAGES")
@@ -270,8 +277,15 @@ class ResNet18B200:
             if li != stage:   # first block of a new stage: strided conv + downsample
                 sp = self.sizes[stage] + 2                       # previous padded extent
                 t1, t2, out = bufs[li]
-                c1(lib, cur, B, sp, sp, t1, st, relu=True, count=count)
-                ds(lib, cur, B, sp, sp, t2, st, relu=False, count=count)
+                if self.fused_ds:
+                    # one kernel: the downsample rides on the 3x3/2's centre-tap tiles
+                    _native.check("gg_conv2d_ds", lib.gg_conv2d_ds(
+                        C.c_void_p(cur), B, sp, sp, c1.cin, _native.ptr(c1.w), c1.cout,
+                        _native.ptr(c1.b), C.c_void_p(t1), _native.ptr(ds.w), _native.ptr(ds.b),
+                        C.c_void_p(t2), cnt, st))
+                else:
+                    c1(lib, cur, B, sp, sp, t1, st, relu=True, count=count)
+                    ds(lib, cur, B, sp, sp, t2, st, relu=False, count=count)
                 c2(lib, t1, B, s, s, out, st, residual=t2, relu=True, count=count)
                 cur, free = out, [t1, t2]
                 stage = li

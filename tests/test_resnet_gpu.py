@@ -151,6 +151,41 @@ def test_pools(env):
     assert (zp.float() - ref.mean(dim=(2, 3))).abs().max().item() < 1e-2
 
 
+@pytest.mark.parametrize("n,h,cin,cout", [(64, 58, 64, 128), (64, 30, 128, 256), (64, 16, 256, 512),
+                                         (3, 16, 256, 512)])
+def test_conv2d_ds_fused(env, n, h, cin, cout):
+    """3x3/2 conv + 1x1/2 downsample in one kernel (gg_conv2d_ds) == the two
+    separate gg_conv2d launches, bit for bit (same K order per accumulator), on a
+    zero-bordered input of padded extent h; both outputs zero-bordered."""
+    torch, nat, lib = env
+    g = torch.Generator(device="cuda").manual_seed(h + cin)
+    x = torch.zeros((n, h, h, cin), dtype=torch.bfloat16, device="cuda")
+    x[:, 1:-1, 1:-1] = torch.randn((n, h - 2, h - 2, cin), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((cout, 9 * cin), device="cuda", generator=g) / (9 * cin) ** 0.5).to(torch.bfloat16)
+    wd = (torch.randn((cout, cin), device="cuda", generator=g) / cin ** 0.5).to(torch.bfloat16)
+    b = torch.randn(cout, device="cuda", generator=g)
+    bd = torch.randn(cout, device="cuda", generator=g)
+    ho = (h - 3) // 2 + 1
+    shape = (n, ho + 2, ho + 2, cout)
+    y1, yd1, y2, yd2 = (torch.zeros(shape, dtype=torch.bfloat16, device="cuda") for _ in range(4))
+    nat.check("gg_conv2d", lib.gg_conv2d(nat.ptr(x), n, h, h, cin, nat.ptr(w), cout, 3, 3, 2, 0, 9 * cin,
+                                         nat.ptr(b), None, 1, nat.ptr(y1), 0, 1, None, nat.stream_ptr()))
+    nat.check("gg_conv2d", lib.gg_conv2d(nat.ptr(x), n, h, h, cin, nat.ptr(wd), cout, 1, 1, 2, -1, cin,
+                                         nat.ptr(bd), None, 0, nat.ptr(yd1), -1, 1, None, nat.stream_ptr()))
+    nat.check("gg_conv2d_ds", lib.gg_conv2d_ds(nat.ptr(x), n, h, h, cin, nat.ptr(w), cout, nat.ptr(b),
+                                               nat.ptr(y2), nat.ptr(wd), nat.ptr(bd), nat.ptr(yd2), None,
+                                               nat.stream_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert torch.equal(yd1, yd2)
+    # and against torch on the interior
+    xi = x.float().permute(0, 3, 1, 2)
+    ref = torch.relu(torch.nn.functional.conv2d(xi, w.float().reshape(cout, 3, 3, cin).permute(0, 3, 1, 2),
+                                                b, stride=2))
+    got = y2[:, 1:-1, 1:-1].float().permute(0, 3, 1, 2)
+    assert (got - ref).abs().max().item() <= 2e-2 * max(1.0, ref.abs().max().item())
+
+
 @pytest.mark.parametrize("n,c,h,w", [(3, 64, 29, 31), (1, 128, 9, 10), (2, 8, 7, 5)])
 def test_maxpool_ragged_shapes(env, n, c, h, w):
     """Blocked max pool (4 x 2 outputs per thread) at sizes that leave partial blocks: exact."""
