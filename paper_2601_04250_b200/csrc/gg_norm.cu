@@ -68,28 +68,79 @@ __device__ __forceinline__ void load_row(const __nv_bfloat16* src, float (&x)[PE
   }
 }
 
-// One row per warp (kLnRowsPerWarp; 2 measured slower), launched
-// with programmatic dependent launch: the CTAs start while the producing GEMM
-// drains and wait for it in griddepcontrol.wait.
-constexpr int kLnRowsPerWarp = 1;
+// A warp normalizes kLnRowsPerWarp rows in turn with its lanes' gamma / beta held
+// in registers (loaded once, not once per row: per-row reloads made this kernel
+// L1-throughput-bound, ncu l1tex 73 %), the next row's load issued before the
+// current row's reductions.  Launched with programmatic dependent launch.
+constexpr int kLnRowsPerWarp = 4;
+constexpr int kLnWarps = 4;
 template <int PER_LANE>
-__global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* x, int64_t ldx,
-                                                        __nv_bfloat16* y, int64_t ldy,
-                                                        const float* gamma, const float* beta,
-                                                        int64_t rows, int width, float eps,
-                                                        const int32_t* count, int rows_per_item) {
+__global__ void __launch_bounds__(32 * kLnWarps) layernorm_kernel(const __nv_bfloat16* x, int64_t ldx,
+                                                                 __nv_bfloat16* y, int64_t ldy,
+                                                                 const float* gamma, const float* beta,
+                                                                 int64_t rows, int width, float eps,
+                                                                 const int32_t* count, int rows_per_item) {
+  const int lane = threadIdx.x & 31;
+  float g[PER_LANE], bt[PER_LANE];
+#pragma unroll
+  for (int c = 0; c < PER_LANE / 8; ++c) {
+    const int col = (c * 32 + lane) * 8;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const float4 gg4 = __ldg(reinterpret_cast<const float4*>(gamma + col) + h);
+      const float4 bb4 = __ldg(reinterpret_cast<const float4*>(beta + col) + h);
+      g[c * 8 + 4 * h + 0] = gg4.x; g[c * 8 + 4 * h + 1] = gg4.y;
+      g[c * 8 + 4 * h + 2] = gg4.z; g[c * 8 + 4 * h + 3] = gg4.w;
+      bt[c * 8 + 4 * h + 0] = bb4.x; bt[c * 8 + 4 * h + 1] = bb4.y;
+      bt[c * 8 + 4 * h + 2] = bb4.z; bt[c * 8 + 4 * h + 3] = bb4.w;
+    }
+  }
   griddep_wait();
   griddep_launch();
-  const int64_t r0 = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * kLnRowsPerWarp;
   if (count) rows = min(rows, (int64_t)__ldg(count) * rows_per_item);
+  const int64_t r0 = ((int64_t)blockIdx.x * kLnWarps + (threadIdx.x >> 5)) * kLnRowsPerWarp;
   if (r0 >= rows) return;
-  float v[kLnRowsPerWarp][PER_LANE];
+  float v[PER_LANE], nx[PER_LANE];
+  load_row<PER_LANE>(x + r0 * ldx, v, false);
+#pragma unroll 1
+  for (int j = 0; j < kLnRowsPerWarp; ++j) {
+    const int64_t r = r0 + j;
+    if (r >= rows) break;
+    if (j + 1 < kLnRowsPerWarp && r + 1 < rows) load_row<PER_LANE>(x + (r + 1) * ldx, nx, false);
+    float sum = 0.f;
 #pragma unroll
-  for (int j = 0; j < kLnRowsPerWarp; ++j)
-    if (r0 + j < rows) load_row<PER_LANE>(x + (r0 + j) * ldx, v[j], false);
+    for (int i = 0; i < PER_LANE; ++i) sum += v[i];
 #pragma unroll
-  for (int j = 0; j < kLnRowsPerWarp; ++j)
-    if (r0 + j < rows) ln_row<PER_LANE>(v[j], width, gamma, beta, eps, y + (r0 + j) * ldy);
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const float mean = sum / width;
+    float var = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER_LANE; ++i) {
+      const float d = v[i] - mean;
+      var += d * d;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+    const float rstd = rsqrtf(var / width + eps);
+    __nv_bfloat16* yr = y + r * ldy;
+#pragma unroll
+    for (int c = 0; c < PER_LANE / 8; ++c) {
+      const int col = (c * 32 + lane) * 8;
+      float o8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o8[e] = (v[c * 8 + e] - mean) * rstd * g[c * 8 + e] + bt[c * 8 + e];
+      uint4 u;
+      __nv_bfloat162 t0 = __floats2bfloat162_rn(o8[0], o8[1]), t1 = __floats2bfloat162_rn(o8[2], o8[3]);
+      __nv_bfloat162 t2 = __floats2bfloat162_rn(o8[4], o8[5]), t3 = __floats2bfloat162_rn(o8[6], o8[7]);
+      u.x = *reinterpret_cast<uint32_t*>(&t0);
+      u.y = *reinterpret_cast<uint32_t*>(&t1);
+      u.z = *reinterpret_cast<uint32_t*>(&t2);
+      u.w = *reinterpret_cast<uint32_t*>(&t3);
+      *reinterpret_cast<uint4*>(yr + col) = u;
+    }
+#pragma unroll
+    for (int i = 0; i < PER_LANE; ++i) v[i] = nx[i];
+  }
 }
 
 template <int PER_LANE>
@@ -119,8 +170,8 @@ extern "C" int gg_layernorm(const void* x, int64_t ldx, void* y, int64_t ldy, co
   if (!x || !y || !gamma || !beta || rows < 0) return GG_ERR_INVALID_ARGUMENT;
   if (width != 768 || ldx % 8 || ldy % 8) return GG_ERR_UNSUPPORTED;
   if (rows == 0) return GG_OK;
-  const int64_t per_block = 8 * kLnRowsPerWarp;
-  if (launch_pdl(layernorm_kernel<24>, dim3((unsigned)((rows + per_block - 1) / per_block)), dim3(256), 0,
+  const int64_t per_block = kLnWarps * kLnRowsPerWarp;
+  if (launch_pdl(layernorm_kernel<24>, dim3((unsigned)((rows + per_block - 1) / per_block)), dim3(32 * kLnWarps), 0,
                  gg_stream(stream), reinterpret_cast<const __nv_bfloat16*>(x), ldx,
                  reinterpret_cast<__nv_bfloat16*>(y), ldy, gamma, beta, rows, width, eps, count_dev,
                  rows_per_item) != cudaSuccess)

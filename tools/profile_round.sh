@@ -19,6 +19,10 @@ timeout 300 $NCU --set full --import-source on -k regex:conv_span_tcgen05 -s 1 -
   -o "$OUT/resnet18_layer1_span" python tools/forward_once.py resnet18 1 > /dev/null 2>&1
 timeout 300 $NCU --set full --import-source on -k regex:gemm_bf16_pair -s 2 -c 1 \
   -o "$OUT/distilbert_ffn_up_gemm_pair" python tools/forward_once.py distilbert 1 > /dev/null 2>&1
+timeout 300 $NCU --set full --import-source on -k regex:layernorm_kernel -s 1 -c 1 \
+  -o "$OUT/distilbert_layernorm" python tools/forward_once.py distilbert 1 > /dev/null 2>&1
+timeout 300 $NCU --set full --import-source on -k regex:attention_tcgen05 -s 1 -c 1 \
+  -o "$OUT/distilbert_attention" python tools/forward_once.py distilbert 1 > /dev/null 2>&1
 GG_PROBE_EAGER=1 timeout 300 $NCU --set full --import-source on -k regex:admit_small_kernel -s 1 -c 1 \
   -o "$OUT/k1_admit_2p26" python tools/kernel_probe.py k1 1 > /dev/null 2>&1
 for f in "$OUT"/*.ncu-rep; do
