@@ -117,7 +117,17 @@ int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const v
  * y_ds zero-bordered [N, Ho+2, Wo+2, Cout].  C % 64 == 0, Cout % 128 == 0. */
 int gg_conv2d_ds(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
                  int32_t Cout, const float* bias, void* y, const void* w_ds, const float* bias_ds,
-                 void* y_ds, const int32_t* count_dev, void* stream);
+                 void* y_ds, int32_t in_shared, int32_t out_shared, const int32_t* count_dev,
+                 void* stream);
+
+/* 3x3 / 1 span conv (as gg_conv3x3_padded) on the shared-border layout: per image
+ * [H+1, W+1] with one zero row and column (the left / top neighbours of an image's
+ * first column / row are the previous row's / image's zeros), after a zero margin of
+ * W+2 rows; x, residual and y point at the margin.  ~15-30 % fewer positions than
+ * [H+2, W+2] at the 28 / 14 / 7 maps of ResNet layers 2-4. */
+int gg_conv3x3_shared(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
+                      int32_t Cout, const float* bias, const void* residual, int32_t relu, void* y,
+                      const int32_t* count_dev, void* stream);
 
 int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
                       int32_t Cout, const float* bias, const void* residual, int32_t relu,

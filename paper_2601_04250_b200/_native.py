@@ -49,7 +49,9 @@ SIGNATURES: dict[str, tuple] = {
     "gg_token_gather": (C.c_int, [_P, _P, _I64, _P, _P, _I32, _I32, _P, _P, _P]),
     "gg_conv2d": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32,
                             _P, _P, _I32, _P, _I32, _I32, _P, _P]),
-    "gg_conv2d_ds": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P, _P]),
+    "gg_conv2d_ds": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _I32, _I32,
+                               _P, _P]),
+    "gg_conv3x3_shared": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _I32, _P, _P, _P]),
     "gg_conv3x3_padded": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _I32, _P, _P,
                                     _P]),
     "gg_nchw_to_nhwc": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _P, _P]),

@@ -320,11 +320,13 @@ __global__ void __launch_bounds__(kConvThreads, 1)
       }
       const int m = tm * 128 + quarter * 32 + lane;
       const bool ok = m < M;
-      int64_t oidx = m;   // output row: dense, or inside a zero-bordered [Ho+2, Wo+2] layout
+      int64_t oidx = m;   // output row: dense, zero-bordered [Ho+2, Wo+2], or shared-border
       if (ep.out_pad) {
         const int n = m / (sh.Ho * sh.Wo), rem = m - (m / (sh.Ho * sh.Wo)) * sh.Ho * sh.Wo;
         const int ho = rem / sh.Wo, wo = rem - (rem / sh.Wo) * sh.Wo;
-        oidx = ((int64_t)n * (sh.Ho + 2) + ho + 1) * (sh.Wo + 2) + wo + 1;
+        oidx = ep.out_pad == 2
+                   ? (int64_t)(sh.Wo + 2) + ((int64_t)n * (sh.Ho + 1) + ho) * (sh.Wo + 1) + wo   // [Wo+2 margin][N, Ho+1, Wo+1]
+                   : ((int64_t)n * (sh.Ho + 2) + ho + 1) * (sh.Wo + 2) + wo + 1;
       }
 #pragma unroll 1
       for (int cc = 0; cc < (DS ? 2 : 1) * BN; cc += 32) {
@@ -708,24 +710,28 @@ extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t
 
 extern "C" int gg_conv2d_ds(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
                             int32_t Cout, const float* bias, void* y, const void* w_ds,
-                            const float* bias_ds, void* y_ds, const int32_t* count_dev, void* stream) {
-  // 3x3 / stride 2 (+ folded BN + ReLU) on a zero-bordered [N, H, W, C] input (pad 0)
-  // fused with the block's 1x1 / stride 2 downsample (+ folded BN, no ReLU) of the
-  // same input: both outputs zero-bordered [N, Ho+2, Wo+2, Cout]
+                            const float* bias_ds, void* y_ds, int32_t in_shared, int32_t out_shared,
+                            const int32_t* count_dev, void* stream) {
+  // 3x3 / stride 2 (+ folded BN + ReLU) fused with the block's 1x1 / stride 2
+  // downsample (+ folded BN, no ReLU) of the same input.  Input: zero-bordered
+  // [N, H, W, C] (H, W padded extents, pad 0) or, in_shared, the shared-border
+  // layout ([W+1 margin][N, H, W, C] with the image in [H-1, W-1]: pad 1 before, the
+  // zero row / column after).  Outputs zero-bordered or (out_shared) shared-border.
   if (!x || !w || !y || !bias || !w_ds || !bias_ds || !y_ds || N <= 0 || H < 3 || W < 3)
     return GG_ERR_INVALID_ARGUMENT;
   if (C % 64 || Cout % 128) return GG_ERR_UNSUPPORTED;
   ConvShape sh;
   sh.N = N; sh.H = H; sh.W = W; sh.C = C; sh.Cout = Cout;
-  sh.R = 3; sh.S = 3; sh.stride = 2; sh.pad = 0; sh.pad_hi = 0; sh.Kpad = 9 * C;
+  sh.R = 3; sh.S = 3; sh.stride = 2; sh.pad = in_shared ? 1 : 0; sh.pad_hi = 0; sh.Kpad = 9 * C;
   sh.bres = 0;
   sh.bres_stages = 0;
-  sh.Ho = (H - 3) / 2 + 1;
-  sh.Wo = (W - 3) / 2 + 1;
+  sh.Ho = (H + sh.pad - 3) / 2 + 1;
+  sh.Wo = (W + sh.pad - 3) / 2 + 1;
+  if (in_shared) x = reinterpret_cast<const __nv_bfloat16*>(x) + (int64_t)(W + 1) * C;   // past the margin
   const int64_t M = (int64_t)N * sh.Ho * sh.Wo;
   if (M > 0x7fffffff) return GG_ERR_UNSUPPORTED;
   sh.M = (int)M;
-  ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, 1, count_dev, 1,
+  ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, 1, count_dev, out_shared ? 2 : 1,
              StreamK{nullptr, nullptr, 0}, reinterpret_cast<__nv_bfloat16*>(y_ds), bias_ds};
   constexpr int BN = 128;
   CUtensorMap mw, mwds, mx;

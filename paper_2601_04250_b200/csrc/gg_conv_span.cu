@@ -1180,15 +1180,18 @@ static bool plan_span(SpanShape& sh, int bn, int rb, int taps, bool single_ntile
 
 using namespace gg;
 
-extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W, int32_t C,
-                                 const void* w, int32_t Cout, const float* bias,
-                                 const void* residual, int32_t relu, void* y,
-                                 const int32_t* count_dev, void* stream) {
+// border 2: zero-bordered [N, H+2, W+2, C]; border 1: shared-border layout (one zero
+// row / column per image, [N, H+1, W+1, C] after a W+2-row zero margin) — the left
+// and top neighbours of an image's first column / row are the previous column's /
+// image's zero row, so 3x3 taps stay uniform row shifts with Wp = W + 1.
+static int conv3x3_span(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
+                        int32_t Cout, const float* bias, const void* residual, int32_t relu, void* y,
+                        const int32_t* count_dev, void* stream, int border) {
   if (!x || !w || !y || !bias || N <= 0 || H <= 0 || W <= 0) return GG_ERR_INVALID_ARGUMENT;
   if (C % 64 || Cout % 64) return GG_ERR_UNSUPPORTED;
   SpanShape sh;
   sh.N = N; sh.H = H; sh.W = W; sh.C = C; sh.Cout = Cout;
-  sh.Hp = H + 2; sh.Wp = W + 2;
+  sh.Hp = H + border; sh.Wp = W + border;
   sh.Ho = H; sh.Wo = W;
   const int64_t Mtot = (int64_t)N * sh.Hp * sh.Wp;
   // Tile shape (BN x 128*MT) by a per-SM time model: MMA cycles per tile
@@ -1203,7 +1206,12 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
   // N = 64 pairs (layer 1) measured slower than single-CTA tiles (GG_SPAN_PAIR64=1 opts in)
   static const bool pair64 = getenv("GG_SPAN_PAIR64") && atoi(getenv("GG_SPAN_PAIR64")) == 1;
   if (!no_pair && (Cout % 128 == 0 || (Cout == 64 && pair64)) && !getenv("GG_SPAN_TILE")) {
-    const int bn = Cout % 256 == 0 ? 256 : Cout % 128 == 0 ? 128 : 64;
+    int bn = Cout % 256 == 0 ? 256 : Cout % 128 == 0 ? 128 : 64;
+    if (bn == 256) {   // N = 128 pair tiles when they finish in fewer rounds x width (layer 4)
+      const int64_t mt = (Mtot + 255) / 256, P = num_sms() / 2;
+      const int64_t r256 = (mt * (Cout / 256) + P - 1) / P, r128 = (mt * (Cout / 128) + P - 1) / P;
+      if (r128 * 128 < r256 * 256) bn = 128;
+    }
     sh.span_rows = 128 + 2 * sh.Wp + 2;
     // coalesced TMA-box epilogue (GG_NO_TMA_EPI=1 keeps row-per-thread stores)
     static const bool no_tma_epi = getenv("GG_NO_TMA_EPI") != nullptr;
@@ -1300,6 +1308,20 @@ extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W,
     case 64 * 4 + 2: return launch_span<64, 64, 3, false, 2>(mx, mw, sh, ep, s, po, pr);
     default: return launch_span<64, 64, 3, false, 1>(mx, mw, sh, ep, s, po, pr);
   }
+}
+
+extern "C" int gg_conv3x3_padded(const void* x, int32_t N, int32_t H, int32_t W, int32_t C,
+                                 const void* w, int32_t Cout, const float* bias,
+                                 const void* residual, int32_t relu, void* y,
+                                 const int32_t* count_dev, void* stream) {
+  return conv3x3_span(x, N, H, W, C, w, Cout, bias, residual, relu, y, count_dev, stream, 2);
+}
+
+extern "C" int gg_conv3x3_shared(const void* x, int32_t N, int32_t H, int32_t W, int32_t C,
+                                 const void* w, int32_t Cout, const float* bias,
+                                 const void* residual, int32_t relu, void* y,
+                                 const int32_t* count_dev, void* stream) {
+  return conv3x3_span(x, N, H, W, C, w, Cout, bias, residual, relu, y, count_dev, stream, 1);
 }
 
 extern "C" int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws, const void* w,

@@ -1,24 +1,27 @@
 """ResNet-18 (torchvision architecture, 224x224) forward on sm_100a, NHWC bf16.
 
-Layout: from layer1 on every activation lives in a zero-bordered buffer
-[N, H+2, W+2, C], one set of three buffers per stage geometry (58², 30², 16²,
-9²), zeroed once.  Then:
+Layout: layer 1's activations live in zero-bordered buffers [N, 58, 58, 64];
+layers 2-4 in the shared-border layout ([s+2 zero rows][N, s+1, s+1, C]: one
+zero row and column per image, which are also the next row's / image's left /
+top border), 7-31 % fewer positions for the span convs at 28² / 14² / 7².
+Three buffers per stage, zeroed once.  Then:
 
-  stem       conv1 7x7/2 + bn1 + ReLU as a 4x4/1 conv over the space-to-depth(2)
-             input (gg_conv2d, TMA im2col 16-channel mode), dense output
-  maxpool    gg_maxpool3x3s2 into the interior of the layer1 buffer
-  3x3 / 1    gg_conv3x3_padded: one TMA span load per 64-channel block feeds all
-             nine taps (shifted UMMA descriptors); borders written as zeros
-  3x3 / 2    gg_conv2d (TMA im2col) reading the padded input with pad 0,
-             writing the next stage's padded buffer
-  1x1 / 2    gg_conv2d with pad -1 (interior of the padded input)
-  head       gg_avgpool over the padded 9x9 map (divides by 49) + fc on gg_gemm
-             with fp32 logits for the K3 epilogue
+  stem       conv1 7x7/2 + bn1 + ReLU as a 4x4/1 span conv over the
+             space-to-depth(2) input, dense output
+  maxpool    gg_maxpool3x3s2 into the interior of the layer-1 buffer
+  3x3 / 1    gg_conv3x3_padded (layer 1) / gg_conv3x3_shared (layers 2-4): one
+             TMA span load per 64-channel block feeds all nine taps (shifted UMMA
+             descriptors); CTA pairs for Cout >= 128; border positions written as
+             zeros
+  3x3 / 2    gg_conv2d_ds: TMA im2col of the previous stage's buffer, fused with
+  + 1x1 / 2  the block's downsample (the 1x1/2 reads the 3x3's centre-tap tiles;
+             second TMEM accumulator), both outputs in the shared-border layout
+  head       gg_avgpool over the shared-border 8x8 map (divides by 49) + fc on
+             gg_gemm with fp32 logits for the K3 epilogue
 
 Eval-mode BatchNorm is folded into every conv's weights/bias; residual add and
 ReLU are fused into the conv epilogues.
 """
-
 from __future__ import annotations
 
 import ctypes as C
@@ -144,8 +147,9 @@ class _SpanConv:
     """3x3 / 1 conv on padded activations (gg_conv3x3_padded); weights in
     (channel block, tap, channel) K order."""
 
-    def __init__(self, conv, bn, device):
+    def __init__(self, conv, bn, device, shared: bool = False):
         import torch
+        self.shared = shared                 # shared-border layout (layers 2-4)
         w, b = _fold(conv, bn)               # [Cout, 3, 3, Cin]
         cout, _, _, cin = w.shape
         wk = w.reshape(cout, 9, cin // 64, 64).permute(0, 2, 1, 3).reshape(cout, 9 * cin)
@@ -155,7 +159,8 @@ class _SpanConv:
         self.algo_macs_per_pixel = 9 * cin * cout
 
     def __call__(self, lib, x, n, h, w, y, st, residual=None, relu=True, count=None):
-        _native.check("gg_conv3x3_padded", lib.gg_conv3x3_padded(
+        fn = lib.gg_conv3x3_shared if self.shared else lib.gg_conv3x3_padded
+        _native.check("gg_conv3x3", fn(
             C.c_void_p(x), n, h, w, self.cin, _native.ptr(self.w), self.cout, _native.ptr(self.b),
             None if residual is None else C.c_void_p(residual), int(relu), C.c_void_p(y),
             _native.ptr(count), st))
@@ -212,29 +217,35 @@ class ResNet18B200:
         self.sizes = [H // 4, H // 8, H // 16, H // 32]             # 56, 28, 14, 7
         chans = [64, 128, 256, 512]
         # three zero-bordered buffers per stage (zeroed once; interiors rewritten every forward)
-        self.stage_bufs = [[torch.zeros(B * (s + 2) * (s + 2) * c, **z) for _ in range(3)]
-                           for s, c in zip(self.sizes, chans)]
+        # layer 1: zero-bordered [B, 58, 58, 64]; layers 2-4: shared-border layout
+        # ([s+2 zero rows][B, s+1, s+1, C]: one zero row / column per image, 7-31 %
+        # fewer positions for the span convs than [s+2, s+2])
+        self.stage_bufs = [[torch.zeros(self._stage_rows(i, s, B) * c, **z) for _ in range(3)]
+                           for i, (s, c) in enumerate(zip(self.sizes, chans))]
         self.pooled = torch.empty((B, 512), **z)
         self.logits = torch.empty((B, npad), dtype=torch.float32, device=dev)
 
     # stages whose 3x3/1 convs run as TMA-im2col instead of span convs (no border
     # rows: 31 % / 65 % of layers 3 / 4's 16^2 / 9^2 padded maps).  Empty: the
     # span convs measured faster at every stage on B200 (one operand load feeds
-    # nine taps); GG_RESNET_IM2COL_STAGES="2,3" selects the alternative.
+    # nine taps); GG_RESNET_IM2COL_STAGES="0" selects the alternative for layer 1
+    # (layers 2-4 use the shared-border layout, span convs only).
     IM2COL_STAGES = ()
 
-    # stride-2 conv1 + 1x1 downsample of a stage's first block as one kernel
-    # (gg_conv2d_ds); GG_RESNET_SPLIT_DS=1 runs them as two
-    @property
-    def fused_ds(self) -> bool:
-        import os
-        return os.environ.get("GG_RESNET_SPLIT_DS") != "1"
+    @staticmethod
+    def _stage_rows(stage: int, s: int, batch: int) -> int:
+        """Rows (pixels) of a stage buffer: bordered for layer 1, shared-border after."""
+        if stage == 0:
+            return batch * (s + 2) * (s + 2)
+        return (s + 2) + batch * (s + 1) * (s + 1)
 
     def _stride1(self, conv, bn, dev, stage):
         import os
         env = os.environ.get("GG_RESNET_IM2COL_STAGES")
         stages = self.IM2COL_STAGES if env is None else tuple(int(v) for v in env.split(",") if v)
-        return _PaddedIm2col(conv, bn, dev) if stage in stages else _SpanConv(conv, bn, dev)
+        if stage in stages and stage == 0:
+            return _PaddedIm2col(conv, bn, dev)
+        return _SpanConv(conv, bn, dev, shared=stage > 0)
 
     def flops(self, batch: int) -> float:
         """Algorithmic FLOPs (3.628 GF/img at 224x224)."""
@@ -275,17 +286,15 @@ class ResNet18B200:
         for li, c1, c2, ds in self.blocks:
             s = self.sizes[li]
             if li != stage:   # first block of a new stage: strided conv + downsample
-                sp = self.sizes[stage] + 2                       # previous padded extent
+                # one kernel (gg_conv2d_ds): the 1x1/2 downsample rides on the 3x3/2's
+                # centre-tap tiles; input bordered (layer 1) or shared-border, output shared
+                in_shared = 1 if stage > 0 else 0
+                sp = self.sizes[stage] + (1 if in_shared else 2)   # previous per-image extent
                 t1, t2, out = bufs[li]
-                if self.fused_ds:
-                    # one kernel: the downsample rides on the 3x3/2's centre-tap tiles
-                    _native.check("gg_conv2d_ds", lib.gg_conv2d_ds(
-                        C.c_void_p(cur), B, sp, sp, c1.cin, _native.ptr(c1.w), c1.cout,
-                        _native.ptr(c1.b), C.c_void_p(t1), _native.ptr(ds.w), _native.ptr(ds.b),
-                        C.c_void_p(t2), cnt, st))
-                else:
-                    c1(lib, cur, B, sp, sp, t1, st, relu=True, count=count)
-                    ds(lib, cur, B, sp, sp, t2, st, relu=False, count=count)
+                _native.check("gg_conv2d_ds", lib.gg_conv2d_ds(
+                    C.c_void_p(cur), B, sp, sp, c1.cin, _native.ptr(c1.w), c1.cout,
+                    _native.ptr(c1.b), C.c_void_p(t1), _native.ptr(ds.w), _native.ptr(ds.b),
+                    C.c_void_p(t2), in_shared, 1, cnt, st))
                 c2(lib, t1, B, s, s, out, st, residual=t2, relu=True, count=count)
                 cur, free = out, [t1, t2]
                 stage = li
@@ -296,8 +305,10 @@ class ResNet18B200:
                 free = [cur, t1]
                 cur = out
         s = self.sizes[-1]
-        _native.check("gg_avgpool", lib.gg_avgpool(C.c_void_p(cur), B, (s + 2) * (s + 2), 512,
-                                                   _native.ptr(self.pooled), s * s, cnt, st))
+        # shared-border map: per image (s+1)^2 positions after an (s+2)-row margin, zeros
+        # outside the s x s interior (divide by s^2)
+        _native.check("gg_avgpool", lib.gg_avgpool(C.c_void_p(cur + (s + 2) * 512 * 2), B, (s + 1) * (s + 1),
+                                                   512, _native.ptr(self.pooled), s * s, cnt, st))
         gemm(lib, self.pooled.data_ptr(), 512, self.w_fc, self.logits.data_ptr(),
              self.logits.stride(0), B, self.w_fc.shape[0], 512, st, bias=self.b_fc,
              out_mode=OUT_F32, tile_n=64, count=count, rows_per_item=1)

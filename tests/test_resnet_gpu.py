@@ -173,8 +173,8 @@ def test_conv2d_ds_fused(env, n, h, cin, cout):
     nat.check("gg_conv2d", lib.gg_conv2d(nat.ptr(x), n, h, h, cin, nat.ptr(wd), cout, 1, 1, 2, -1, cin,
                                          nat.ptr(bd), None, 0, nat.ptr(yd1), -1, 1, None, nat.stream_ptr()))
     nat.check("gg_conv2d_ds", lib.gg_conv2d_ds(nat.ptr(x), n, h, h, cin, nat.ptr(w), cout, nat.ptr(b),
-                                               nat.ptr(y2), nat.ptr(wd), nat.ptr(bd), nat.ptr(yd2), None,
-                                               nat.stream_ptr()))
+                                               nat.ptr(y2), nat.ptr(wd), nat.ptr(bd), nat.ptr(yd2), 0, 0,
+                                               None, nat.stream_ptr()))
     torch.cuda.synchronize()
     assert torch.equal(y1, y2)
     assert torch.equal(yd1, yd2)
@@ -184,6 +184,81 @@ def test_conv2d_ds_fused(env, n, h, cin, cout):
                                                 b, stride=2))
     got = y2[:, 1:-1, 1:-1].float().permute(0, 3, 1, 2)
     assert (got - ref).abs().max().item() <= 2e-2 * max(1.0, ref.abs().max().item())
+
+
+def _to_shared(t, s):
+    """[n, s, s, c] interior -> shared-border buffer [(s+2) margin][n, s+1, s+1, c] (flat rows)."""
+    import torch
+    n, _, _, c = t.shape
+    img = torch.zeros((n, s + 1, s + 1, c), dtype=t.dtype, device=t.device)
+    img[:, :s, :s] = t
+    return torch.cat([torch.zeros((s + 2, c), dtype=t.dtype, device=t.device), img.reshape(-1, c)])
+
+
+def _from_shared(buf, n, s, c):
+    return buf[s + 2:].reshape(n, s + 1, s + 1, c)
+
+
+@pytest.mark.parametrize("n,s,c,cout", [(64, 28, 128, 128), (64, 14, 256, 256), (64, 7, 512, 512),
+                                        (3, 7, 512, 512)])
+def test_conv3x3_shared_border(env, n, s, c, cout):
+    """Span conv on the shared-border layout (layers 2-4) vs torch's padded conv, with
+    residual; the zero row / column of every image stays zero."""
+    torch, nat, lib = env
+    from tests.test_conv_span_gpu import pack_span_weights
+    g = torch.Generator(device="cuda").manual_seed(s + c)
+    x = torch.randn((n, s, s, c), device="cuda", generator=g).to(torch.bfloat16)
+    r = torch.randn((n, s, s, cout), device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn((cout, c, 3, 3), device="cuda", generator=g) / (9 * c) ** 0.5).to(torch.bfloat16)
+    b = torch.randn(cout, device="cuda", generator=g)
+    xs, rs = _to_shared(x, s), _to_shared(r, s)
+    ys = torch.full_like(_to_shared(torch.zeros((n, s, s, cout), dtype=torch.bfloat16, device="cuda"), s), 0)
+    nat.check("gg_conv3x3_shared", lib.gg_conv3x3_shared(
+        nat.ptr(xs), n, s, s, c, nat.ptr(pack_span_weights(w)), cout, nat.ptr(b), nat.ptr(rs), 1,
+        nat.ptr(ys), None, nat.stream_ptr()))
+    torch.cuda.synchronize()
+    ref = torch.relu(torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), w.float(), b, padding=1) +
+                     r.float().permute(0, 3, 1, 2))
+    got = _from_shared(ys, n, s, cout)
+    err = (got[:, :s, :s].float().permute(0, 3, 1, 2) - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+    assert (got[:, s] == 0).all() and (got[:, :, s] == 0).all() and (ys[: s + 2] == 0).all()
+
+
+@pytest.mark.parametrize("n,s,cin,cout,in_shared", [(64, 56, 64, 128, 0), (64, 28, 128, 256, 1),
+                                                    (64, 14, 256, 512, 1), (2, 14, 256, 512, 1)])
+def test_conv2d_ds_shared_border(env, n, s, cin, cout, in_shared):
+    """Fused stride-2 conv + downsample reading a bordered (layer 1) or shared-border
+    input and writing shared-border outputs, vs torch."""
+    torch, nat, lib = env
+    g = torch.Generator(device="cuda").manual_seed(s + cin)
+    x = torch.randn((n, s, s, cin), device="cuda", generator=g).to(torch.bfloat16)
+    if in_shared:
+        xb, ext = _to_shared(x, s), s + 1
+    else:
+        xb = torch.zeros((n, s + 2, s + 2, cin), dtype=torch.bfloat16, device="cuda")
+        xb[:, 1:-1, 1:-1] = x
+        ext = s + 2
+    w = (torch.randn((cout, 9 * cin), device="cuda", generator=g) / (9 * cin) ** 0.5).to(torch.bfloat16)
+    wd = (torch.randn((cout, cin), device="cuda", generator=g) / cin ** 0.5).to(torch.bfloat16)
+    b = torch.randn(cout, device="cuda", generator=g)
+    bd = torch.randn(cout, device="cuda", generator=g)
+    so = s // 2
+    y = _to_shared(torch.zeros((n, so, so, cout), dtype=torch.bfloat16, device="cuda"), so)
+    yd = y.clone()
+    nat.check("gg_conv2d_ds", lib.gg_conv2d_ds(nat.ptr(xb), n, ext, ext, cin, nat.ptr(w), cout, nat.ptr(b),
+                                               nat.ptr(y), nat.ptr(wd), nat.ptr(bd), nat.ptr(yd), in_shared, 1,
+                                               None, nat.stream_ptr()))
+    torch.cuda.synchronize()
+    xi = x.float().permute(0, 3, 1, 2)
+    ref = torch.relu(torch.nn.functional.conv2d(xi, w.float().reshape(cout, 3, 3, cin).permute(0, 3, 1, 2),
+                                                b, stride=2, padding=1))
+    refd = torch.nn.functional.conv2d(xi, wd.float().reshape(cout, cin, 1, 1), bd, stride=2)
+    got = _from_shared(y, n, so, cout)[:, :so, :so].float().permute(0, 3, 1, 2)
+    gotd = _from_shared(yd, n, so, cout)[:, :so, :so].float().permute(0, 3, 1, 2)
+    for a, rr in ((got, ref), (gotd, refd)):
+        assert (a - rr).abs().max().item() <= 2e-2 * max(1.0, rr.abs().max().item())
+    assert (_from_shared(y, n, so, cout)[:, so] == 0).all()
 
 
 @pytest.mark.parametrize("n,c,h,w", [(3, 64, 29, 31), (1, 128, 9, 10), (2, 8, 7, 5)])
