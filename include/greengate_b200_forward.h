@@ -162,7 +162,8 @@ int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_
                    const int32_t* count_dev, int32_t B, int32_t H, int32_t W,
                    const float* mean3, const float* std3, int32_t padded, void* y, void* stream);
 /* 3x3 / stride 2 / pad 1 max pool (NHWC, C % 8 == 0); out_pad = 1 writes the
- * interior of a zero-bordered [N, Ho+2, Wo+2, C] buffer. */
+ * interior of a zero-bordered [N, Ho+2, Wo+2, C] buffer, out_pad = 2 the interior of
+ * a shared-border buffer ([Wo+2 zero rows][N, Ho+1, Wo+1, C], see gg_conv3x3_shared). */
 int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, void* y,
                     int32_t out_pad, const int32_t* count_dev, void* stream);
 /* Global average pool NHWC [N, HW, C] -> [N, C], dividing by denom (0 = HW;

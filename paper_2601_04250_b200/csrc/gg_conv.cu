@@ -566,7 +566,9 @@ __global__ void __launch_bounds__(256) maxpool3x3s2_blocked(const __nv_bfloat16*
     for (int j = 0; j < kPoolCols; ++j) {
       const int wo = wo0 + j;
       if (wo >= Wo) break;
-      const int64_t o = out_pad ? ((int64_t)n * (Ho + 2) + ho + 1) * (Wo + 2) + wo + 1
+      const int64_t o = out_pad == 2   // shared-border layout: (Wo+2)-row margin, [Ho+1, Wo+1] images
+                            ? (int64_t)(Wo + 2) + ((int64_t)n * (Ho + 1) + ho) * (Wo + 1) + wo
+                        : out_pad ? ((int64_t)n * (Ho + 2) + ho + 1) * (Wo + 2) + wo + 1
                                 : ((int64_t)n * Ho + ho) * Wo + wo;
       *reinterpret_cast<uint4*>(out + o * C + c0) = *reinterpret_cast<const uint4*>(m[i][j]);
     }

@@ -1,15 +1,15 @@
 """ResNet-18 (torchvision architecture, 224x224) forward on sm_100a, NHWC bf16.
 
-Layout: layer 1's activations live in zero-bordered buffers [N, 58, 58, 64];
-layers 2-4 in the shared-border layout ([s+2 zero rows][N, s+1, s+1, C]: one
-zero row and column per image, which are also the next row's / image's left /
-top border), 7-31 % fewer positions for the span convs at 28² / 14² / 7².
+Layout: every stage's activations live in the shared-border layout ([s+2 zero
+rows][N, s+1, s+1, C]: one zero row and column per image, which are also the next
+row's / image's left / top border), 3-31 % fewer positions for the span convs
+than [s+2, s+2] at 56² / 28² / 14² / 7².
 Three buffers per stage, zeroed once.  Then:
 
   stem       conv1 7x7/2 + bn1 + ReLU as a 4x4/1 span conv over the
              space-to-depth(2) input, dense output
   maxpool    gg_maxpool3x3s2 into the interior of the layer-1 buffer
-  3x3 / 1    gg_conv3x3_padded (layer 1) / gg_conv3x3_shared (layers 2-4): one
+  3x3 / 1    gg_conv3x3_shared: one
              TMA span load per 64-channel block feeds all nine taps (shifted UMMA
              descriptors); CTA pairs for Cout >= 128; border positions written as
              zeros
@@ -128,21 +128,6 @@ class _StemConv(_Conv):
         return _Conv.__call__(self, lib, x, n, h, w, y, st, relu=relu, count=count)
 
 
-class _PaddedIm2col(_Conv):
-    """3x3 / 1 conv on a zero-bordered [N, s+2, s+2, C] buffer through gg_conv2d's
-    TMA-im2col mode (pad 0 on the padded input, interior of the padded output):
-    no work on border positions, and stream-K when the tile count leaves a
-    partly empty wave (layers 3-4: 14x14 / 7x7 maps, K = 2304 / 4608)."""
-
-    def __init__(self, conv, bn, device):
-        super().__init__(conv, bn, device, pad=0, pad_hi=0, out_pad=1)
-
-    def __call__(self, lib, x, n, h, w, y, st, residual=None, relu=True, count=None):
-        _Conv.__call__(self, lib, x, n, h + 2, w + 2, y, st, residual=residual, relu=relu,
-                       count=count)
-        return h, w
-
-
 class _SpanConv:
     """3x3 / 1 conv on padded activations (gg_conv3x3_padded); weights in
     (channel block, tap, channel) K order."""
@@ -225,27 +210,13 @@ class ResNet18B200:
         self.pooled = torch.empty((B, 512), **z)
         self.logits = torch.empty((B, npad), dtype=torch.float32, device=dev)
 
-    # stages whose 3x3/1 convs run as TMA-im2col instead of span convs (no border
-    # rows: 31 % / 65 % of layers 3 / 4's 16^2 / 9^2 padded maps).  Empty: the
-    # span convs measured faster at every stage on B200 (one operand load feeds
-    # nine taps); GG_RESNET_IM2COL_STAGES="0" selects the alternative for layer 1
-    # (layers 2-4 use the shared-border layout, span convs only).
-    IM2COL_STAGES = ()
-
     @staticmethod
     def _stage_rows(stage: int, s: int, batch: int) -> int:
-        """Rows (pixels) of a stage buffer: bordered for layer 1, shared-border after."""
-        if stage == 0:
-            return batch * (s + 2) * (s + 2)
+        """Rows (pixels) of a shared-border stage buffer: (s+2) margin + batch x (s+1)^2."""
         return (s + 2) + batch * (s + 1) * (s + 1)
 
     def _stride1(self, conv, bn, dev, stage):
-        import os
-        env = os.environ.get("GG_RESNET_IM2COL_STAGES")
-        stages = self.IM2COL_STAGES if env is None else tuple(int(v) for v in env.split(",") if v)
-        if stage in stages and stage == 0:
-            return _PaddedIm2col(conv, bn, dev)
-        return _SpanConv(conv, bn, dev, shared=stage > 0)
+        return _SpanConv(conv, bn, dev, shared=True)
 
     def flops(self, batch: int) -> float:
         """Algorithmic FLOPs (3.628 GF/img at 224x224)."""
@@ -280,21 +251,20 @@ class ResNet18B200:
                          st, count=count)                                     # 112x112x64 dense
         bufs = [[t.data_ptr() for t in stage] for stage in self.stage_bufs]
         _native.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(
-            _native.ptr(self.stem_out), B, h, w, 64, C.c_void_p(bufs[0][0]), 1, cnt, st))
+            _native.ptr(self.stem_out), B, h, w, 64, C.c_void_p(bufs[0][0]), 2, cnt, st))
         cur, free = bufs[0][0], [bufs[0][1], bufs[0][2]]
         stage = 0
         for li, c1, c2, ds in self.blocks:
             s = self.sizes[li]
             if li != stage:   # first block of a new stage: strided conv + downsample
                 # one kernel (gg_conv2d_ds): the 1x1/2 downsample rides on the 3x3/2's
-                # centre-tap tiles; input bordered (layer 1) or shared-border, output shared
-                in_shared = 1 if stage > 0 else 0
-                sp = self.sizes[stage] + (1 if in_shared else 2)   # previous per-image extent
+                # centre-tap tiles; shared-border input and outputs
+                sp = self.sizes[stage] + 1                       # previous per-image extent
                 t1, t2, out = bufs[li]
                 _native.check("gg_conv2d_ds", lib.gg_conv2d_ds(
                     C.c_void_p(cur), B, sp, sp, c1.cin, _native.ptr(c1.w), c1.cout,
                     _native.ptr(c1.b), C.c_void_p(t1), _native.ptr(ds.w), _native.ptr(ds.b),
-                    C.c_void_p(t2), in_shared, 1, cnt, st))
+                    C.c_void_p(t2), 1, 1, cnt, st))
                 c2(lib, t1, B, s, s, out, st, residual=t2, relu=True, count=count)
                 cur, free = out, [t1, t2]
                 stage = li
