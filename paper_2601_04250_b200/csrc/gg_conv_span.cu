@@ -1210,7 +1210,10 @@ static int conv3x3_span(const void* x, int32_t N, int32_t H, int32_t W, int32_t 
     if (bn == 256) {   // N = 128 pair tiles when they finish in fewer rounds x width (layer 4)
       const int64_t mt = (Mtot + 255) / 256, P = num_sms() / 2;
       const int64_t r256 = (mt * (Cout / 256) + P - 1) / P, r128 = (mt * (Cout / 128) + P - 1) / P;
-      if (r128 * 128 < r256 * 256) bn = 128;
+      // (a tie — layer 3: 114 N=128 tiles in 2 rounds vs 57 in 1 — measured even or
+      // slightly worse with N = 128; GG_SPAN_PAIR_BN=128/256 forces a width)
+      static const int pair_bn = getenv("GG_SPAN_PAIR_BN") ? atoi(getenv("GG_SPAN_PAIR_BN")) : 0;
+      if (pair_bn == 128 || (pair_bn != 256 && r128 * 128 < r256 * 256)) bn = 128;
     }
     sh.span_rows = 128 + 2 * sh.Wp + 2;
     // coalesced TMA-box epilogue (GG_NO_TMA_EPI=1 keeps row-per-thread stores)
