@@ -195,11 +195,12 @@ __device__ __forceinline__ void store_s2d_cell(__nv_bfloat16* y, int64_t q, cons
   dst[1] = swap ? lo : hi;
 }
 
-// One block per (image, s2d row): the two source image rows (2 x W x 3 bytes)
-// are staged in shared memory with 16-byte loads when aligned, then each thread
-// builds s2d pixels from shared memory and writes 32 contiguous bytes
-// (consecutive threads -> consecutive pixels: coalesced).
+// One block per (image, kGatherRows s2d rows): the 2 * kGatherRows source image
+// rows are staged in shared memory with 16-byte loads (all issued before the
+// first use) when aligned, then each thread builds s2d pixels from shared memory
+// and writes 32 contiguous bytes (consecutive threads -> consecutive pixels).
 constexpr int kGatherThreads = 128;
+constexpr int kGatherRows = 4;
 
 __global__ void __launch_bounds__(kGatherThreads) stem_gather_kernel(
     const uint8_t* __restrict__ pool, int64_t pool_size, const int32_t* ids, const int32_t* count,
@@ -207,37 +208,49 @@ __global__ void __launch_bounds__(kGatherThreads) stem_gather_kernel(
     __nv_bfloat16* __restrict__ y) {
   griddep_wait();   // PDL: the predecessor has completed and flushed
   griddep_launch();
-  extern __shared__ __align__(16) uint8_t rows[];   // [2][W * 3]
+  extern __shared__ __align__(16) uint8_t rows[];   // [2 * kGatherRows][W * 3]
+  // the normalization of a uint8 value is one of 3 x 256 bf16 results: built once
+  // per block with the exact arithmetic, then looked up (12 fp32 divisions per
+  // cell made this kernel issue-bound)
+  __shared__ __nv_bfloat16 lut[3][256];
   const int n_valid = count ? min(B, __ldg(count)) : B;
-  const int n = blockIdx.y, yy = blockIdx.x;
+  const int n = blockIdx.y, yy0 = blockIdx.x * kGatherRows;
   if (n >= n_valid) return;
   const int Ho = H / 2, Wo = W / 2;
+  const int nrows = min(kGatherRows, Ho - yy0);
   const int64_t img = ids ? (int64_t)__ldg(ids + n) % pool_size : n;
   const int rb = W * 3;
-  const uint8_t* src = pool + (img * H + 2 * yy) * (int64_t)rb;   // two consecutive rows
+  const uint8_t* src = pool + (img * H + 2 * yy0) * (int64_t)rb;   // 2 * nrows consecutive rows
+  const int bytes = 2 * nrows * rb;
   if (((reinterpret_cast<uintptr_t>(src) | (uintptr_t)rb) & 15) == 0) {
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
-    for (int i = threadIdx.x; i < 2 * rb / 16; i += kGatherThreads)
-      reinterpret_cast<uint4*>(rows)[i] = __ldg(s4 + i);
+    for (int i = threadIdx.x; i < bytes / 16; i += kGatherThreads) reinterpret_cast<uint4*>(rows)[i] = __ldg(s4 + i);
   } else {
-    for (int i = threadIdx.x; i < 2 * rb; i += kGatherThreads) rows[i] = __ldg(src + i);
+    for (int i = threadIdx.x; i < bytes; i += kGatherThreads) rows[i] = __ldg(src + i);
+  }
+  {
+    const float mean[3] = {m0, m1, m2}, sd[3] = {s0, s1, s2};
+    for (int i = threadIdx.x; i < 3 * 256; i += kGatherThreads) {
+      const int c = i >> 8, xv = i & 255;
+      lut[c][xv] = __float2bfloat16_rn(((float)xv * (1.0f / 255.0f) - mean[c]) / sd[c]);
+    }
   }
   __syncthreads();
-  const float mean[3] = {m0, m1, m2}, sd[3] = {s0, s1, s2};
-  for (int xx = threadIdx.x; xx < Wo; xx += kGatherThreads) {
+  for (int cell = threadIdx.x; cell < nrows * Wo; cell += kGatherThreads) {
+    const int r = cell / Wo, xx = cell - r * Wo;
     __align__(16) __nv_bfloat16 v[16];
 #pragma unroll
     for (int dy = 0; dy < 2; ++dy) {
-      const uint8_t* row = rows + dy * rb + 2 * xx * 3;
+      const uint8_t* row = rows + (2 * r + dy) * rb + 2 * xx * 3;
 #pragma unroll
       for (int i = 0; i < 6; ++i) {  // (dx, c) pairs of this input row
         const int c = i % 3, dx = i / 3;
-        v[(dy * 2 + dx) * 3 + c] = __float2bfloat16_rn((row[i] * (1.0f / 255.0f) - mean[c]) / sd[c]);
+        v[(dy * 2 + dx) * 3 + c] = lut[c][row[i]];
       }
     }
 #pragma unroll
     for (int e = 12; e < 16; ++e) v[e] = __float2bfloat16_rn(0.0f);
-    store_s2d_cell(y, s2d_index(n, yy, xx, Ho, Wo, padded), reinterpret_cast<uint4*>(v)[0],
+    store_s2d_cell(y, s2d_index(n, yy0 + r, xx, Ho, Wo, padded), reinterpret_cast<uint4*>(v)[0],
                    reinterpret_cast<uint4*>(v)[1], padded);
   }
 }
@@ -328,8 +341,9 @@ int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_
                    const float* std3, int32_t padded, void* y, void* stream) {
   if (!pool || pool_size < 1 || !mean3 || !std3 || !y || B < 1 || H % 2 || W % 2)
     return GG_ERR_INVALID_ARGUMENT;
-  if (2 * W * 3 > 48 * 1024 || B > 65535) return GG_ERR_UNSUPPORTED;
-  GG_PDL_LAUNCH((stem_gather_kernel), dim3((unsigned)(H / 2), (unsigned)B), kGatherThreads, 2 * W * 3, gg_stream(stream), 
+  if (2 * kGatherRows * W * 3 > 48 * 1024 || B > 65535) return GG_ERR_UNSUPPORTED;
+  GG_PDL_LAUNCH((stem_gather_kernel), dim3((unsigned)((H / 2 + kGatherRows - 1) / kGatherRows), (unsigned)B),
+                kGatherThreads, 2 * kGatherRows * W * 3, gg_stream(stream),
       pool, pool_size, batch_ids, count_dev, B, H, W, mean3[0], mean3[1], mean3[2], std3[0],
       std3[1], std3[2], padded, reinterpret_cast<__nv_bfloat16*>(y));
   GG_LAUNCH_OK();
