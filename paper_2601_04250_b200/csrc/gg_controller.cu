@@ -1304,6 +1304,15 @@ constexpr int kOutThreads = 512;
 constexpr int kOutChunk = 512;
 constexpr int kOutMaxSlots = 64;
 
+// Order-preserving uint64 key of a non-NaN double (NaNs take the sequential
+// kernel), with -0.0 mapped onto +0.0 so the zeros compare equal as in Python;
+// key 0 is below every real value (the "removed" sentinel).
+__device__ __forceinline__ unsigned long long order_ukey(double x) {
+  long long b = __double_as_longlong(x);
+  if ((b << 1) == 0) b = 0;
+  return b < 0 ? (unsigned long long)(~b) : ((unsigned long long)b | 0x8000000000000000ULL);
+}
+
 template <int S>
 __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
     gg_params p, gg_state* st, const double* lat, const double* jou, const int32_t* qd, int64_t n,
@@ -1315,7 +1324,6 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
   __shared__ int32_t sq[kOutChunk];
   __shared__ double sp[kOutChunk];
   __shared__ double sew[kOutChunk];   // EWMA after each outcome (energy channel observes)
-  __shared__ int16_t spos[GG_P95_WINDOW_MAX];   // arrival position: stable sort key
   __shared__ int64_t slot_off[kOutMaxSlots + 1];
   __shared__ int s_flag, s_first;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1435,44 +1443,46 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
       const int cnt = min(cap, h + c + 1);
       const int start = h + c + 1 - cnt;
       double v[S];
+      unsigned long long kv[S];
 #pragma unroll
       for (int q = 0; q < S; ++q) {
         const int j = q * 32 + lane;
-        v[q] = j < cnt ? seq[start + j] : -INFINITY;
+        v[q] = j < cnt ? seq[start + j] : 0.0;
+        kv[q] = j < cnt ? order_ukey(v[q]) : 0ULL;
       }
       const int k = (int)ceil(f64_mul(0.95, (double)cnt));   // ceil(95.0/100.0 * n)
       const int r = cnt - k + 1;                             // k-th smallest = r-th largest
+      // r rounds of "remove the largest": warp max of the order keys with two
+      // redux.sync (high, then low word), ties to the later arrival (CPython's
+      // sorted() is stable, so from the top of the ascending window equal values
+      // — e.g. -0.0 / +0.0 — come latest-arrival first) by a third redux over the
+      // candidates' window positions
       double got = 0.0;
       #pragma unroll 1
       for (int it = 0; it < r; ++it) {
-        double bv = v[0];
+        unsigned long long bk = kv[0];
         int bq = 0;
 #pragma unroll
         for (int q = 1; q < S; ++q)
-          if (v[q] >= bv) {   // ties: the later position (q * 32 + lane grows with q)
-            bv = v[q];
+          if (kv[q] >= bk) {   // ties: the later position (q * 32 + lane grows with q)
+            bk = kv[q];
             bq = q;
           }
-        int bl = lane;
+        const unsigned hi = (unsigned)(bk >> 32), lo = (unsigned)bk;
+        const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+        const bool cand = hi == mh && lo == ml;
+        const unsigned pos = __reduce_max_sync(0xffffffffu, cand ? (unsigned)(bq * 32 + lane + 1) : 0u) - 1u;
+        const int wl = (int)(pos & 31u), wq = (int)(pos >> 5);
+        double wv = 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-          const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
-          // ties: the later arrival first — CPython's sorted() is stable, so counting
-          // down from the top of the ascending window, equal values (e.g. -0.0 and
-          // +0.0) come latest-arrival first
-          if (ov > bv || (ov == bv && (oq * 32 + ol) > (bq * 32 + bl))) {
-            bv = ov;
-            bl = ol;
-            bq = oq;
-          }
-        }
-        got = bv;
-        if (lane == bl) {
+        for (int q = 0; q < S; ++q)
+          if (q == wq) wv = v[q];
+        got = __shfl_sync(0xffffffffu, wv, wl);
+        if (lane == wl) {
 #pragma unroll
           for (int q = 0; q < S; ++q)
-            if (q == bq) v[q] = -INFINITY;
+            if (q == wq) kv[q] = 0ULL;
         }
       }
       if (lane == 0) sp[c] = got;
@@ -1571,42 +1581,20 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
   const int head_f = (count0 + m_total <= cap) ? head0 : (int)((head0 + (count0 + m_total - cap)) % cap);
   #pragma unroll 1
   for (int j = tid; j < h; j += kOutThreads) st->win[(head_f + j) % cap] = seq[j];
-  // sorted window: bitonic sort of seq[0, h) padded with +inf to the next power of
-  // two (in place)
-  int P2 = 1;
-  while (P2 < h) P2 <<= 1;
+  // sorted window = CPython's stable sorted(): each element lands at its stable rank
+  // (smaller values, then equal values earlier in arrival order): h^2 / 512 compares
+  // against the smem window instead of a bitonic network's syncs
   #pragma unroll 1
-  for (int j = h + tid; j < P2; j += kOutThreads) seq[j] = INFINITY;
-  #pragma unroll 1
-  for (int j = tid; j < P2; j += kOutThreads) spos[j] = (int16_t)j;
-  __syncthreads();
-  #pragma unroll 1
-  for (int size = 2; size <= P2; size <<= 1) {
-    #pragma unroll 1
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      #pragma unroll 1
-      for (int i = tid; i < P2; i += kOutThreads) {
-        const int jx = i ^ stride;
-        if (jx > i) {
-          // keys (value, arrival position): the result is CPython's stable sorted()
-          // (equal values such as -0.0 / +0.0 keep their arrival order)
-          const bool up = (i & size) == 0;
-          const double a = seq[i], b = seq[jx];
-          const int16_t pa = spos[i], pb = spos[jx];
-          const bool a_gt_b = a > b || (a == b && pa > pb);
-          if (a_gt_b == up) {
-            seq[i] = b;
-            seq[jx] = a;
-            spos[i] = pb;
-            spos[jx] = pa;
-          }
-        }
-      }
-      __syncthreads();
+  for (int j = tid; j < h; j += kOutThreads) {
+    const double vj = seq[j];
+    int rk = 0;
+    #pragma unroll 4
+    for (int i = 0; i < h; ++i) {
+      const double vi = seq[i];
+      rk += (vi < vj || (vi == vj && i < j)) ? 1 : 0;
     }
+    st->win_sorted[rk] = vj;
   }
-  #pragma unroll 1
-  for (int j = tid; j < h; j += kOutThreads) st->win_sorted[j] = seq[j];
   if (tid == 0) {
     if (slots && fifo) {   // global queue depth seen by this rank's next snapshot
       int64_t extra = 0;
