@@ -385,7 +385,8 @@ def roofline_forward(srv, net, B):
     pk = peaks()
     achieved = flops / (ms * 1e-3) / 1e12
     kern = ("ResNet-18 forward: stem span conv + max pool + 4 span convs (layer 1) + 9 CTA-pair "
-            "span convs (layers 2-4) + 6 TMA-im2col convs + avg pool + fc, all tcgen05"
+            "span convs (layers 2-4) + 3 fused stride-2 conv/downsample (TMA im2col) + avg pool + "
+            "fc, all tcgen05, shared-border NHWC layout"
             if srv.kind == "resnet18"
             else "DistilBERT forward: 24 CTA-pair tcgen05 GEMMs + 2 single-CTA GEMMs + 6 tcgen05 "
                  "attention + 12 LayerNorm + embedding-LN")
