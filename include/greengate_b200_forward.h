@@ -155,6 +155,16 @@ int gg_nchw_to_s2d16(const float* x, int32_t N, int32_t H, int32_t W, int32_t pa
 int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws, const void* w, int32_t Cout,
                      const float* bias, int32_t relu, void* y, const int32_t* count_dev,
                      void* stream);
+/* ResNet-18 stem + max pool in one kernel: conv1 + bn1 + relu as gg_stem_s2d_span, then
+ * 3x3 / 2 / pad 1 max pool, without writing the stem output.  Hs, Ws even, Ws <= 128;
+ * y = pooled [N, Hs/2, Ws/2, 64]: dense (out_pad 0) or the interior of the shared-border
+ * layer-1 layout (out_pad 2, as gg_maxpool3x3s2).  Identical values to
+ * gg_stem_s2d_span + gg_maxpool3x3s2 (max is order-free, bf16 rounding monotonic).
+ * Replaces model.conv1/bn1/relu/maxpool of torchvision resnet18, which the reference
+ * runs through torch (kernel K8). */
+int gg_stem_pool_span(const void* x, int32_t N, int32_t Hs, int32_t Ws, const void* w, int32_t Cout,
+                      const float* bias, void* y, int32_t out_pad, const int32_t* count_dev,
+                      void* stream);
 /* Served-batch stem input: image i of the batch = uint8 HWC image
  * pool[batch_ids[i] % pool_size], normalized ((x/255 - mean[c]) / std[c]) into
  * the space-to-depth(2) 16-channel layout of gg_nchw_to_s2d16. */

@@ -57,6 +57,7 @@ SIGNATURES: dict[str, tuple] = {
     "gg_nchw_to_nhwc": (C.c_int, [_P, _I32, _I32, _I32, _I32, _I32, _P, _P]),
     "gg_nchw_to_s2d16": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P]),
     "gg_stem_s2d_span": (C.c_int, [_P, _I32, _I32, _I32, _P, _I32, _P, _I32, _P, _P, _P]),
+    "gg_stem_pool_span": (C.c_int, [_P, _I32, _I32, _I32, _P, _I32, _P, _P, _I32, _P, _P]),
     "gg_stem_gather": (C.c_int, [_P, _I64, _P, _P, _I32, _I32, _I32, _P, _P, _I32, _P, _P]),
     "gg_maxpool3x3s2": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P]),
     "gg_avgpool": (C.c_int, [_P, _I32, _I32, _I32, _P, _I32, _P, _P]),

@@ -1176,6 +1176,229 @@ static bool plan_span(SpanShape& sh, int bn, int rb, int taps, bool single_ntile
   return sh.a_stages >= 2 && sh.b_stages >= 1;
 }
 
+// ---------------------------------------------------------------------------
+// Stem conv + 3x3/2 max pool in one kernel (ResNet-18 conv1 / bn1 / relu / maxpool).
+//
+// The stem's 112 x 112 x 64 output (103 MB at batch 64) only feeds the max pool,
+// so writing it and reading it back is pure HBM/L2 traffic.  Here a tile is ONE
+// stem output row (n, h): the 128 accumulator lanes are w = 0..127 (w >= Ws
+// discarded), the A span starts at the row's first padded pixel (rounded down to
+// an 8-row swizzle atom; the descriptor carries the remainder), 16 taps x one
+// K = 16 MMA each, B (64 x 256) resident.  Each CTA owns a contiguous band of
+// pool rows g = n * Ho + ho and computes the stem rows they need in order
+// (2ho - 1 once at the band start, then 2ho, 2ho + 1 per pool row), so:
+//   epilogue phase 1: bias + ReLU + bf16 of the row into a swizzled smem row
+//                     (double buffered), one named barrier;
+//   epilogue phase 2: horizontal 3-max at stride 2 from smem, then the vertical
+//                     3-max against a running partial held in registers (thread
+//                     -> (wo, 8-channel group) fixed across tiles); odd rows emit
+//                     pool row (h - 1) / 2.
+// Max is order-independent and bf16 rounding is monotonic, so the pooled values
+// are identical to stem -> bf16 -> gg_maxpool3x3s2.  Rows computed per CTA:
+// 2 x band + 1 (+1 per image boundary) — ~2 % more MMA rows than the stem alone,
+// plus 128 / Ws lanes per row (14 % at Ws = 112).
+struct StemPoolShape {
+  int N, Hs, Ws, Hp, Wp, Ho, Wo;
+  int span_rows;      // 128 + 3 * (Wp + 1) + 7: one row's span, atom-aligned start
+  int a_stage_bytes;
+  int a_stages;
+  int out_pad;        // 0: dense [N, Ho, Wo, 64]; 2: shared-border layer-1 layout
+};
+
+constexpr int kStemPoolRowBytes = 128 * 128;   // one bf16 stem row: 128 px x 64 ch
+
+struct StemTile { int n, h; bool emit; };
+
+// Tile i of the CTA owning pool rows [g0, g1): (image, stem row, emits a pool row)
+__device__ __forceinline__ StemTile stem_tile(int i, int g0, int pre, int Ho) {
+  StemTile t;
+  if (pre && i == 0) {
+    t.n = g0 / Ho;
+    t.h = 2 * (g0 - t.n * Ho) - 1;
+    t.emit = false;
+  } else {
+    const int k = i - pre, g = g0 + (k >> 1);
+    t.n = g / Ho;
+    t.h = 2 * (g - t.n * Ho) + (k & 1);
+    t.emit = (k & 1) != 0;
+  }
+  return t;
+}
+
+__global__ void __launch_bounds__(kSpanThreads, 1)
+    stem_pool_span(const __grid_constant__ CUtensorMap map_w, StemPoolShape sh,
+                   const __nv_bfloat16* __restrict__ x16, const float* __restrict__ bias,
+                   __nv_bfloat16* __restrict__ y, const int32_t* count) {
+  constexpr int BN = 64, RB = 32, TAPS = 16, B_BYTES = BN * RB, NACC = 4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int AST = sh.a_stages;
+  uint8_t* a_base = smem;
+  uint8_t* b_base = smem + AST * sh.a_stage_bytes;
+  uint8_t* rowbuf = b_base + TAPS * B_BYTES;   // [2][128 px][128 B], 16-B chunks XOR (px & 7)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rowbuf + 2 * kStemPoolRowBytes);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + kSpanMaxStages;
+  uint64_t* acc_full = a_empty + kSpanMaxStages;
+  uint64_t* acc_empty = acc_full + NACC;
+  uint64_t* b_full = acc_empty + NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  griddep_launch();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < AST; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < NACC; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kSpanEpiWarps);
+    }
+    mbar_init(b_full, 1);
+    fence_mbar_init();
+    tma_prefetch(&map_w);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, NACC * BN);
+  // weights do not depend on the predecessor: load them before the wait
+  if (warp == 0 && lane == 0) {
+    mbar_expect_tx(b_full, TAPS * B_BYTES);
+    for (int kb = 0; kb < TAPS; ++kb) tma_load_2d(b_base + kb * B_BYTES, &map_w, b_full, kb * 16, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+  const int n_eff = count ? min(sh.N, __ldg(count)) : sh.N;
+  const int total = n_eff * sh.Ho;   // pool rows
+  const int g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
+  const int g1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
+  const int pre = (g1 > g0 && g0 % sh.Ho != 0) ? 1 : 0;
+  const int ntiles = g1 > g0 ? pre + 2 * (g1 - g0) : 0;
+  const int64_t rows_all = (int64_t)sh.N * sh.Hp * sh.Wp;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < ntiles; ++i) {
+        const StemTile t = stem_tile(i, g0, pre, sh.Ho);
+        const int as = i % AST;
+        mbar_wait_sleep(&a_empty[as], ((i / AST) & 1) ^ 1);
+        // output (h, w) reads padded input (h + r, w + s): the span of row h starts at
+        // padded pixel (n, h, 0); the 16-channel input is stored pre-swizzled (SW32),
+        // so a linear copy from an 8-row-aligned start reproduces the swizzled image
+        const int64_t m0 = ((int64_t)t.n * sh.Hp + t.h) * sh.Wp;
+        const int64_t m0a = m0 & ~int64_t(7);
+        const int64_t left = rows_all - m0a;
+        const int rows = left < sh.span_rows ? (int)left : sh.span_rows;
+        mbar_expect_tx(&a_full[as], rows * RB);
+        bulk_load(a_base + as * sh.a_stage_bytes, x16 + m0a * 16, rows * RB, &a_full[as]);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+    uint64_t tap_off[TAPS];
+#pragma unroll
+    for (int tap = 0; tap < TAPS; ++tap) tap_off[tap] = (uint64_t)(((tap >> 2) * sh.Wp + (tap & 3)) * (RB / 16));
+    mbar_wait(b_full, 0);
+    const uint64_t bdesc = sdesc_k_sw32(smem_u32(b_base));
+    for (int i = 0; i < ntiles; ++i) {
+      const StemTile t = stem_tile(i, g0, pre, sh.Ho);
+      const int acc = i % NACC, as = i % AST;
+      mbar_wait(&acc_empty[acc], ((i / NACC) & 1) ^ 1);
+      mbar_wait(&a_full[as], (i / AST) & 1);
+      tc_fence_after();
+      const int64_t m0 = ((int64_t)t.n * sh.Hp + t.h) * sh.Wp;
+      const uint64_t ad = sdesc_k_sw32(smem_u32(a_base + as * sh.a_stage_bytes)) + (uint64_t)((m0 & 7) * (RB / 16));
+      if (elect_one_sync()) {
+#pragma unroll
+        for (int tap = 0; tap < TAPS; ++tap)
+          umma_bf16(tmem_base + acc * BN, ad + tap_off[tap], bdesc + (uint64_t)(tap * (B_BYTES >> 4)), idesc,
+                    tap != 0);
+        umma_commit(&a_empty[as]);
+        umma_commit(&acc_full[acc]);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int etid = threadIdx.x - 64;   // 0..255
+    const int w = quarter * 32 + lane;   // this lane's stem column
+    float bz[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) bz[i] = __ldg(bias + half * 32 + i);
+    const int items = sh.Wo * 8;   // (pool column, 8-channel group)
+    const __nv_bfloat162 ninf = __float2bfloat162_rn(-INFINITY);
+    uint4 part[2];
+    for (int i = 0; i < ntiles; ++i) {
+      const StemTile t = stem_tile(i, g0, pre, sh.Ho);
+      const int acc = i % NACC;
+      mbar_wait_sleep(&acc_full[acc], (i / NACC) & 1);
+      tc_fence_after();
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * 32, r);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      uint8_t* rb = rowbuf + (i & 1) * kStemPoolRowBytes;
+      if (w < sh.Ws) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = fmaxf(__uint_as_float(r[q * 8 + e]) + bz[q * 8 + e], 0.0f);
+          uint4 u;
+          u.x = pack_bf16(v[0], v[1]);
+          u.y = pack_bf16(v[2], v[3]);
+          u.z = pack_bf16(v[4], v[5]);
+          u.w = pack_bf16(v[6], v[7]);
+          *reinterpret_cast<uint4*>(rb + w * 128 + (((half * 4 + q) ^ (w & 7)) << 4)) = u;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kSpanEpiWarps) : "memory");
+      const bool first = i == 0 || t.h == 0;
+      const int ho = (t.h - 1) >> 1;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int it = etid + j * 256;
+        if (it >= items) continue;
+        const int wo = it >> 3, c = it & 7;
+        __nv_bfloat162 hm[4] = {ninf, ninf, ninf, ninf};
+#pragma unroll
+        for (int dw = -1; dw <= 1; ++dw) {
+          const int ww = 2 * wo + dw;
+          if (ww < 0 || ww >= sh.Ws) continue;
+          const uint4 u = *reinterpret_cast<const uint4*>(rb + ww * 128 + ((c ^ (ww & 7)) << 4));
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) hm[e] = __hmax2(hm[e], h2[e]);
+        }
+        uint4 hv = *reinterpret_cast<const uint4*>(hm);
+        if (first) {
+          part[j] = hv;
+        } else {
+          __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&part[j]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) p2[e] = __hmax2(p2[e], hm[e]);
+        }
+        if (t.emit) {
+          const int64_t o = sh.out_pad == 2
+                                ? (int64_t)(sh.Wo + 2) + ((int64_t)t.n * (sh.Ho + 1) + ho) * (sh.Wo + 1) + wo
+                                : ((int64_t)t.n * sh.Ho + ho) * sh.Wo + wo;
+          *reinterpret_cast<uint4*>(y + o * 64 + c * 8) = part[j];
+          part[j] = hv;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, NACC * BN);
+  }
+}
+
 }  // namespace gg
 
 using namespace gg;
@@ -1363,4 +1586,41 @@ extern "C" int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws
     return launch_span_pair<64, 16, 4, true>(mxp, mwp, sp, ep, gg_stream(stream));
   }
   return launch_span<64, 16, 4, true, 1>(mx, mw, sh, ep, gg_stream(stream));
+}
+
+extern "C" int gg_stem_pool_span(const void* x, int32_t N, int32_t Hs, int32_t Ws, const void* w,
+                                 int32_t Cout, const float* bias, void* y, int32_t out_pad,
+                                 const int32_t* count_dev, void* stream) {
+  if (!x || !w || !y || !bias || N <= 0 || Hs <= 0 || Ws <= 0) return GG_ERR_INVALID_ARGUMENT;
+  if (reinterpret_cast<uintptr_t>(x) & 15) return GG_ERR_INVALID_ARGUMENT;
+  if (Cout != 64 || (Hs & 1) || (Ws & 1) || Ws > 128 || (out_pad != 0 && out_pad != 2))
+    return GG_ERR_UNSUPPORTED;
+  StemPoolShape sh;
+  sh.N = N; sh.Hs = Hs; sh.Ws = Ws;
+  sh.Hp = Hs + 3; sh.Wp = Ws + 3;   // space-to-depth input padded 2 before, 1 after
+  sh.Ho = Hs / 2; sh.Wo = Ws / 2;   // 3x3 / 2 / pad 1 over an even extent
+  sh.out_pad = out_pad;
+  sh.span_rows = 128 + 3 * sh.Wp + 3 + 7;
+  sh.a_stage_bytes = (sh.span_rows * 32 + 1023) / 1024 * 1024;
+  const int fixed = 1024 + 16 * 64 * 32 + 2 * kStemPoolRowBytes + 1024;
+  sh.a_stages = (kSpanSmemMax - fixed) / sh.a_stage_bytes;
+  if (sh.a_stages > 8) sh.a_stages = 8;
+  if (sh.a_stages < 2) return GG_ERR_UNSUPPORTED;
+  CUtensorMap mw;
+  if (int rc = make_map_span(&mw, w, Cout, 256, 16, 64)) return rc;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(stem_pool_span, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpanSmemMax) !=
+        cudaSuccess)
+      return GG_ERR_CUDA;
+    attr = true;
+  }
+  const int smem = fixed + sh.a_stages * sh.a_stage_bytes;
+  const int64_t rows = (int64_t)N * sh.Ho;
+  const int grid = rows < num_sms() ? (int)rows : num_sms();
+  if (launch_pdl(stem_pool_span, dim3(grid), dim3(kSpanThreads), smem, gg_stream(stream), mw, sh,
+                 reinterpret_cast<const __nv_bfloat16*>(x), bias, reinterpret_cast<__nv_bfloat16*>(y),
+                 count_dev) != cudaSuccess)
+    return GG_ERR_CUDA;
+  return GG_OK;
 }

@@ -6,9 +6,12 @@ row's / image's left / top border), 3-31 % fewer positions for the span convs
 than [s+2, s+2] at 56² / 28² / 14² / 7².
 Three buffers per stage, zeroed once.  Then:
 
-  stem       conv1 7x7/2 + bn1 + ReLU as a 4x4/1 span conv over the
-             space-to-depth(2) input, dense output
-  maxpool    gg_maxpool3x3s2 into the interior of the layer-1 buffer
+  stem+pool  gg_stem_pool_span: conv1 7x7/2 + bn1 + ReLU as a 4x4/1 span conv
+             over the space-to-depth(2) input, one stem row per tile, with the
+             3x3/2 max pool in the epilogue (smem row + register partials),
+             written into the interior of the layer-1 buffer; the stem output
+             never reaches memory (GG_STEM_UNFUSED=1: gg_stem_s2d_span +
+             gg_maxpool3x3s2)
   3x3 / 1    gg_conv3x3_shared: one
              TMA span load per 64-channel block feeds all nine taps (shifted UMMA
              descriptors); CTA pairs for Cout >= 128; border positions written as
@@ -25,6 +28,7 @@ ReLU are fused into the conv epilogues.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 from . import _native
 from .distilbert import OUT_F32, gemm
@@ -198,7 +202,9 @@ class ResNet18B200:
         z = dict(dtype=torch.bfloat16, device=dev)
         # zero-bordered space-to-depth stem input [B, H/2+3, H/2+3, 16] (interior rewritten)
         self.x16 = torch.zeros(B * (H // 2 + 3) * (H // 2 + 3) * 16, **z)
-        self.stem_out = torch.empty(B * (H // 2) * (H // 2) * 64, **z)
+        # GG_STEM_UNFUSED=1: separate stem conv + max pool kernels (A/B and cross-check)
+        self.fuse_stem_pool = os.environ.get("GG_STEM_UNFUSED", "0") != "1"
+        self.stem_out = torch.empty(B * (H // 2) * (H // 2) * 64 if not self.fuse_stem_pool else 0, **z)
         self.sizes = [H // 4, H // 8, H // 16, H // 32]             # 56, 28, 14, 7
         chans = [64, 128, 256, 512]
         # three zero-bordered buffers per stage (zeroed once; interiors rewritten every forward)
@@ -247,11 +253,17 @@ class ResNet18B200:
         H = self.image
         st = _native.stream_ptr(stream)
         cnt = _native.ptr(count)
-        h, w = self.stem(lib, self.x16.data_ptr(), B, H // 2, H // 2, self.stem_out.data_ptr(),
-                         st, count=count)                                     # 112x112x64 dense
         bufs = [[t.data_ptr() for t in stage] for stage in self.stage_bufs]
-        _native.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(
-            _native.ptr(self.stem_out), B, h, w, 64, C.c_void_p(bufs[0][0]), 2, cnt, st))
+        if self.fuse_stem_pool:
+            # stem conv + max pool in one kernel: the 112x112x64 stem output never leaves the SM
+            _native.check("gg_stem_pool_span", lib.gg_stem_pool_span(
+                C.c_void_p(self.x16.data_ptr()), B, H // 2, H // 2, _native.ptr(self.stem.w), 64,
+                _native.ptr(self.stem.b), C.c_void_p(bufs[0][0]), 2, cnt, st))
+        else:
+            h, w = self.stem(lib, self.x16.data_ptr(), B, H // 2, H // 2, self.stem_out.data_ptr(),
+                             st, count=count)                                     # 112x112x64 dense
+            _native.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(
+                _native.ptr(self.stem_out), B, h, w, 64, C.c_void_p(bufs[0][0]), 2, cnt, st))
         cur, free = bufs[0][0], [bufs[0][1], bufs[0][2]]
         stage = 0
         for li, c1, c2, ds in self.blocks:

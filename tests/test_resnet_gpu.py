@@ -127,6 +127,53 @@ def test_space_to_depth_stem_vs_torch(env):
     assert err2 <= 2e-2 * max(1.0, ref.abs().max().item()), err2
 
 
+@pytest.mark.parametrize("n,hs,count,out_pad", [(3, 112, None, 0), (64, 112, None, 2), (64, 112, 37, 2),
+                                                 (5, 32, None, 0), (7, 20, 6, 2), (1, 128, None, 0)])
+def test_stem_pool_fused(env, n, hs, count, out_pad):
+    """gg_stem_pool_span == gg_stem_s2d_span -> gg_maxpool3x3s2, bit for bit (max is
+    order-free and bf16 rounding monotonic); pool-row bands that cross images, a
+    device count below the batch, and the shared-border output's zero border."""
+    torch, nat, lib = env
+    from paper_2601_04250_b200.resnet18 import _StemConv
+    g = torch.Generator().manual_seed(hs + n)
+    conv = torch.nn.Conv2d(3, 64, 7, 2, 3, bias=False)
+    bn = torch.nn.BatchNorm2d(64).eval()
+    with torch.no_grad():
+        conv.weight.copy_(torch.randn(conv.weight.shape, generator=g) * 0.1)
+        bn.running_mean.copy_(torch.randn(64, generator=g) * 0.1)
+        bn.running_var.copy_(torch.rand(64, generator=g) + 0.5)
+        bn.weight.copy_(torch.rand(64, generator=g) + 0.5)
+        bn.bias.copy_(torch.randn(64, generator=g) * 0.1)
+    stem = _StemConv(conv, bn, "cuda")
+    x = torch.randn((n, 3, 2 * hs, 2 * hs), generator=g).cuda()
+    x16p = torch.zeros((n, hs + 3, hs + 3, 16), dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_nchw_to_s2d16", lib.gg_nchw_to_s2d16(nat.ptr(x), n, 2 * hs, 2 * hs, 1, nat.ptr(x16p),
+                                                       nat.stream_ptr()))
+    cnt = torch.tensor([count], dtype=torch.int32, device="cuda") if count is not None else None
+    y = torch.empty((n, hs, hs, 64), dtype=torch.bfloat16, device="cuda")
+    stem(lib, x16p.data_ptr(), n, hs, hs, y.data_ptr(), nat.stream_ptr(), relu=True)
+    ho = hs // 2
+    ref = torch.empty((n, ho, ho, 64), dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(nat.ptr(y), n, hs, hs, 64, nat.ptr(ref), 0, None,
+                                                     nat.stream_ptr()))
+    if out_pad == 2:
+        out = torch.zeros(((ho + 2) + n * (ho + 1) * (ho + 1), 64), dtype=torch.bfloat16, device="cuda")
+    else:
+        out = torch.full((n, ho, ho, 64), -7.0, dtype=torch.bfloat16, device="cuda")
+    nat.check("gg_stem_pool_span", lib.gg_stem_pool_span(
+        nat.ptr(x16p), n, hs, hs, nat.ptr(stem.w), 64, nat.ptr(stem.b), nat.ptr(out), out_pad,
+        nat.ptr(cnt), nat.stream_ptr()))
+    torch.cuda.synchronize()
+    got = _from_shared(out, n, ho, 64) if out_pad == 2 else out
+    k = n if count is None else count
+    assert torch.equal(got[:k, :ho, :ho], ref[:k])
+    if out_pad == 2:
+        assert (got[:, ho] == 0).all() and (got[:, :, ho] == 0).all() and (out[: ho + 2] == 0).all()
+        assert (got[k:] == 0).all()
+    else:
+        assert (got[k:] == -7.0).all()
+
+
 def test_pools(env):
     torch, nat, lib = env
     x = torch.randn((2, 64, 112, 112), device="cuda").to(torch.bfloat16)
