@@ -1180,48 +1180,48 @@ static bool plan_span(SpanShape& sh, int bn, int rb, int taps, bool single_ntile
 // Stem conv + 3x3/2 max pool in one kernel (ResNet-18 conv1 / bn1 / relu / maxpool).
 //
 // The stem's 112 x 112 x 64 output (103 MB at batch 64) only feeds the max pool,
-// so writing it and reading it back is pure HBM/L2 traffic.  Here a tile is ONE
-// stem output row (n, h): the 128 accumulator lanes are w = 0..127 (w >= Ws
-// discarded), the A span starts at the row's first padded pixel (rounded down to
-// an 8-row swizzle atom; the descriptor carries the remainder), 16 taps x one
-// K = 16 MMA each, B (64 x 256) resident.  Each CTA owns a contiguous band of
-// pool rows g = n * Ho + ho and computes the stem rows they need in order
-// (2ho - 1 once at the band start, then 2ho, 2ho + 1 per pool row), so:
-//   epilogue phase 1: bias + ReLU + bf16 of the row into a swizzled smem row
+// so writing it and reading it back is pure HBM/L2 traffic.  Here a tile is TWO
+// stem output rows (n, h) and (n, h + 1), h even: the 128 accumulator lanes are
+// w = 0..127 (w >= Ws discarded) and the 128 accumulator columns are
+// [row h: 64 channels | row h + 1: 64 channels].  Output row h + 1's tap (r, s)
+// reads the same padded pixels as row h's tap (r + 1, s), so each of the 5 x 4
+// row/column shifts (r', s) of the A span is ONE N = 128 MMA whose B slab is
+// [W(r', s) ; W(r' - 1, s)] (zero halves at r' = 4 / r' = 0): 20 MMAs per two
+// rows instead of 32 N = 64 ones — an M = 128, K = 16 MMA takes ~64 tensor cycles
+// at N = 64 and N = 128 alike (tools/mma_bench.cu), so N = 64 wastes half the
+// pipe.  The two B halves are TMA boxes of the [64, 256] weight matrix; the A
+// span starts at the row's first padded pixel, rounded down to an 8-row swizzle
+// atom (the descriptor carries the remainder).  Each CTA owns a contiguous band
+// of pool rows g = n * Ho + ho; tile (2ho, 2ho + 1) completes pool row ho with
+// the previous tile's row 2ho - 1 (a register partial), plus one extra tile
+// (2ho0 - 2, 2ho0 - 1) at a band start inside an image:
+//   epilogue phase 1: bias + ReLU + bf16 of both rows into swizzled smem rows
 //                     (double buffered), one named barrier;
-//   epilogue phase 2: horizontal 3-max at stride 2 from smem, then the vertical
-//                     3-max against a running partial held in registers (thread
-//                     -> (wo, 8-channel group) fixed across tiles); odd rows emit
-//                     pool row (h - 1) / 2.
-// Max is order-independent and bf16 rounding is monotonic, so the pooled values
-// are identical to stem -> bf16 -> gg_maxpool3x3s2.  Rows computed per CTA:
-// 2 x band + 1 (+1 per image boundary) — ~2 % more MMA rows than the stem alone,
-// plus 128 / Ws lanes per row (14 % at Ws = 112).
+//   epilogue phase 2: horizontal 3-max at stride 2 from smem, vertical 3-max with
+//                     the partial (thread -> (wo, 8-channel group) fixed), store.
+// Max is order-independent and bf16 rounding monotonic, so the pooled values are
+// identical to stem -> bf16 -> gg_maxpool3x3s2 (tests/test_resnet_gpu.py).
 struct StemPoolShape {
   int N, Hs, Ws, Hp, Wp, Ho, Wo;
-  int span_rows;      // 128 + 3 * (Wp + 1) + 7: one row's span, atom-aligned start
+  int span_rows;      // 128 + 4 * Wp + 3 + 7: a row pair's span, atom-aligned start
   int a_stage_bytes;
   int a_stages;
-  int out_pad;        // 0: dense [N, Ho, Wo, 64]; 2: shared-border layer-1 layout
+  int out_pad;        // 0: dense [N, Ho, Wo, 64]; 2: shared-border layout
 };
 
 constexpr int kStemPoolRowBytes = 128 * 128;   // one bf16 stem row: 128 px x 64 ch
+constexpr int kStemShifts = 20;                // (r', s): r' = 0..4, s = 0..3
+constexpr int kStemBSlab = 128 * 32;           // one shift's B: 128 rows x 16 ch
 
-struct StemTile { int n, h; bool emit; };
+struct StemTile { int n, h; bool pre; };
 
-// Tile i of the CTA owning pool rows [g0, g1): (image, stem row, emits a pool row)
+// Tile i of the CTA owning pool rows [g0, g1): image, first (even) stem row
 __device__ __forceinline__ StemTile stem_tile(int i, int g0, int pre, int Ho) {
   StemTile t;
-  if (pre && i == 0) {
-    t.n = g0 / Ho;
-    t.h = 2 * (g0 - t.n * Ho) - 1;
-    t.emit = false;
-  } else {
-    const int k = i - pre, g = g0 + (k >> 1);
-    t.n = g / Ho;
-    t.h = 2 * (g - t.n * Ho) + (k & 1);
-    t.emit = (k & 1) != 0;
-  }
+  t.pre = pre && i == 0;
+  const int g = t.pre ? g0 : g0 + i - pre;
+  t.n = g / Ho;
+  t.h = 2 * (g - t.n * Ho) - (t.pre ? 2 : 0);
   return t;
 }
 
@@ -1229,14 +1229,14 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     stem_pool_span(const __grid_constant__ CUtensorMap map_w, StemPoolShape sh,
                    const __nv_bfloat16* __restrict__ x16, const float* __restrict__ bias,
                    __nv_bfloat16* __restrict__ y, const int32_t* count) {
-  constexpr int BN = 64, RB = 32, TAPS = 16, B_BYTES = BN * RB, NACC = 4;
+  constexpr int RB = 32, NACC = 4, ACC_COLS = 128;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int AST = sh.a_stages;
   uint8_t* a_base = smem;
   uint8_t* b_base = smem + AST * sh.a_stage_bytes;
-  uint8_t* rowbuf = b_base + TAPS * B_BYTES;   // [2][128 px][128 B], 16-B chunks XOR (px & 7)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rowbuf + 2 * kStemPoolRowBytes);
+  uint8_t* rowbuf = b_base + kStemShifts * kStemBSlab;   // [2 bufs][2 rows][128 px][128 B], chunks XOR (px & 7)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rowbuf + 4 * kStemPoolRowBytes);
   uint64_t* a_full = bars;
   uint64_t* a_empty = a_full + kSpanMaxStages;
   uint64_t* acc_full = a_empty + kSpanMaxStages;
@@ -1259,11 +1259,25 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     fence_mbar_init();
     tma_prefetch(&map_w);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, NACC * BN);
-  // weights do not depend on the predecessor: load them before the wait
+  if (warp == 1) tmem_alloc(tmem_slot, NACC * ACC_COLS);
+  __syncthreads();
+  // weights do not depend on the predecessor: load them before the wait.  Shift
+  // (r', s): rows 0-63 = tap (r', s) for row h, rows 64-127 = tap (r' - 1, s) for h + 1
   if (warp == 0 && lane == 0) {
-    mbar_expect_tx(b_full, TAPS * B_BYTES);
-    for (int kb = 0; kb < TAPS; ++kb) tma_load_2d(b_base + kb * B_BYTES, &map_w, b_full, kb * 16, 0);
+    mbar_expect_tx(b_full, 32 * 64 * RB);
+    for (int j = 0; j < kStemShifts; ++j) {
+      const int rr = j >> 2, s = j & 3;
+      if (rr <= 3) tma_load_2d(b_base + j * kStemBSlab, &map_w, b_full, (rr * 4 + s) * 16, 0);
+      if (rr >= 1) tma_load_2d(b_base + j * kStemBSlab + 64 * RB, &map_w, b_full, ((rr - 1) * 4 + s) * 16, 0);
+    }
+  } else if (warp >= 2) {   // the zero halves: top of r' = 4, bottom of r' = 0
+    const int e = threadIdx.x - 64;   // 256 threads x 16 B x 4 = 16 KB
+    for (int k = e; k < 1024; k += 256) {
+      const int j = k >> 7, off = (k & 127) * 16;   // 8 half-slabs of 2 KB
+      uint8_t* p = j < 4 ? b_base + (16 + j) * kStemBSlab + off : b_base + (j - 4) * kStemBSlab + 64 * RB + off;
+      *reinterpret_cast<uint4*>(p) = make_uint4(0, 0, 0, 0);
+    }
+    fence_proxy_async_smem();
   }
   tc_fence_before();
   __syncthreads();
@@ -1275,7 +1289,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   const int g0 = (int)((int64_t)blockIdx.x * total / gridDim.x);
   const int g1 = (int)((int64_t)(blockIdx.x + 1) * total / gridDim.x);
   const int pre = (g1 > g0 && g0 % sh.Ho != 0) ? 1 : 0;
-  const int ntiles = g1 > g0 ? pre + 2 * (g1 - g0) : 0;
+  const int ntiles = g1 > g0 ? pre + (g1 - g0) : 0;
   const int64_t rows_all = (int64_t)sh.N * sh.Hp * sh.Wp;
 
   if (warp == 0) {
@@ -1284,9 +1298,9 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
         const StemTile t = stem_tile(i, g0, pre, sh.Ho);
         const int as = i % AST;
         mbar_wait_sleep(&a_empty[as], ((i / AST) & 1) ^ 1);
-        // output (h, w) reads padded input (h + r, w + s): the span of row h starts at
-        // padded pixel (n, h, 0); the 16-channel input is stored pre-swizzled (SW32),
-        // so a linear copy from an 8-row-aligned start reproduces the swizzled image
+        // output (h, w) reads padded input (h + r, w + s): the span of the pair starts at
+        // padded pixel (n, h, 0); the 16-channel input is stored pre-swizzled (SW32), so
+        // a linear copy from an 8-row-aligned start reproduces the swizzled image
         const int64_t m0 = ((int64_t)t.n * sh.Hp + t.h) * sh.Wp;
         const int64_t m0a = m0 & ~int64_t(7);
         const int64_t left = rows_all - m0a;
@@ -1296,10 +1310,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
-    uint64_t tap_off[TAPS];
+    constexpr uint32_t idesc = idesc_bf16_f32(128, ACC_COLS);
+    uint64_t sh_off[kStemShifts];
 #pragma unroll
-    for (int tap = 0; tap < TAPS; ++tap) tap_off[tap] = (uint64_t)(((tap >> 2) * sh.Wp + (tap & 3)) * (RB / 16));
+    for (int j = 0; j < kStemShifts; ++j) sh_off[j] = (uint64_t)(((j >> 2) * sh.Wp + (j & 3)) * (RB / 16));
     mbar_wait(b_full, 0);
     const uint64_t bdesc = sdesc_k_sw32(smem_u32(b_base));
     for (int i = 0; i < ntiles; ++i) {
@@ -1312,90 +1326,96 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       const uint64_t ad = sdesc_k_sw32(smem_u32(a_base + as * sh.a_stage_bytes)) + (uint64_t)((m0 & 7) * (RB / 16));
       if (elect_one_sync()) {
 #pragma unroll
-        for (int tap = 0; tap < TAPS; ++tap)
-          umma_bf16(tmem_base + acc * BN, ad + tap_off[tap], bdesc + (uint64_t)(tap * (B_BYTES >> 4)), idesc,
-                    tap != 0);
+        for (int j = 0; j < kStemShifts; ++j)
+          umma_bf16(tmem_base + acc * ACC_COLS, ad + sh_off[j], bdesc + (uint64_t)(j * (kStemBSlab >> 4)), idesc,
+                    j != 0);
         umma_commit(&a_empty[as]);
         umma_commit(&acc_full[acc]);
       }
       __syncwarp();
     }
   } else {
-    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int quarter = warp & 3, row = (warp - 2) >> 2;   // row 0: h, row 1: h + 1
     const int etid = threadIdx.x - 64;   // 0..255
     const int w = quarter * 32 + lane;   // this lane's stem column
-    float bz[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) bz[i] = __ldg(bias + half * 32 + i);
-    const int items = sh.Wo * 8;   // (pool column, 8-channel group)
+    const int items = sh.Wo * 8;         // (pool column, 8-channel group)
     const __nv_bfloat162 ninf = __float2bfloat162_rn(-INFINITY);
-    uint4 part[2];
+    uint4 part[2];                       // max over stem row 2ho - 1 (the previous tile's second row)
     for (int i = 0; i < ntiles; ++i) {
       const StemTile t = stem_tile(i, g0, pre, sh.Ho);
       const int acc = i % NACC;
       mbar_wait_sleep(&acc_full[acc], (i / NACC) & 1);
       tc_fence_after();
-      uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + half * 32, r);
+      uint32_t r[2][32];
+      const uint32_t ta = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ACC_COLS + row * 64;
+      tmem_ld_32x32b_x32(ta, r[0]);
+      tmem_ld_32x32b_x32(ta + 32, r[1]);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
-      uint8_t* rb = rowbuf + (i & 1) * kStemPoolRowBytes;
+      uint8_t* rb = rowbuf + ((i & 1) * 2) * kStemPoolRowBytes;
       if (w < sh.Ws) {
+        uint8_t* myrow = rb + row * kStemPoolRowBytes + w * 128;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 8; ++q) {
+          const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + q * 8));
+          const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + q * 8 + 4));
+          const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
           float v[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = fmaxf(__uint_as_float(r[q * 8 + e]) + bz[q * 8 + e], 0.0f);
+          for (int e = 0; e < 8; ++e) v[e] = fmaxf(__uint_as_float(r[q >> 2][(q & 3) * 8 + e]) + bb[e], 0.0f);
           uint4 u;
           u.x = pack_bf16(v[0], v[1]);
           u.y = pack_bf16(v[2], v[3]);
           u.z = pack_bf16(v[4], v[5]);
           u.w = pack_bf16(v[6], v[7]);
-          *reinterpret_cast<uint4*>(rb + w * 128 + (((half * 4 + q) ^ (w & 7)) << 4)) = u;
+          *reinterpret_cast<uint4*>(myrow + ((q ^ (w & 7)) << 4)) = u;
         }
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kSpanEpiWarps) : "memory");
-      const bool first = i == 0 || t.h == 0;
-      const int ho = (t.h - 1) >> 1;
+      const int ho = t.h >> 1;
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int it = etid + j * 256;
         if (it >= items) continue;
         const int wo = it >> 3, c = it & 7;
-        __nv_bfloat162 hm[4] = {ninf, ninf, ninf, ninf};
+        __nv_bfloat162 hm[2][4];
 #pragma unroll
-        for (int dw = -1; dw <= 1; ++dw) {
-          const int ww = 2 * wo + dw;
-          if (ww < 0 || ww >= sh.Ws) continue;
-          const uint4 u = *reinterpret_cast<const uint4*>(rb + ww * 128 + ((c ^ (ww & 7)) << 4));
-          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        for (int rr = 0; rr < 2; ++rr) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) hm[e] = __hmax2(hm[e], h2[e]);
-        }
-        uint4 hv = *reinterpret_cast<const uint4*>(hm);
-        if (first) {
-          part[j] = hv;
-        } else {
-          __nv_bfloat162* p2 = reinterpret_cast<__nv_bfloat162*>(&part[j]);
+          for (int e = 0; e < 4; ++e) hm[rr][e] = ninf;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) p2[e] = __hmax2(p2[e], hm[e]);
+          for (int dw = -1; dw <= 1; ++dw) {
+            const int ww = 2 * wo + dw;
+            if (ww < 0 || ww >= sh.Ws) continue;
+            const uint4 u = *reinterpret_cast<const uint4*>(rb + rr * kStemPoolRowBytes + ww * 128 + ((c ^ (ww & 7)) << 4));
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) hm[rr][e] = __hmax2(hm[rr][e], h2[e]);
+          }
         }
-        if (t.emit) {
-          const int64_t o = sh.out_pad == 2
-                                ? (int64_t)(sh.Wo + 2) + ((int64_t)t.n * (sh.Ho + 1) + ho) * (sh.Wo + 1) + wo
-                                : ((int64_t)t.n * sh.Ho + ho) * sh.Wo + wo;
-          *reinterpret_cast<uint4*>(y + o * 64 + c * 8) = part[j];
-          part[j] = hv;
+        if (!t.pre) {
+          __nv_bfloat162 o[4];
+          const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&part[j]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            o[e] = __hmax2(hm[0][e], hm[1][e]);
+            if (t.h != 0) o[e] = __hmax2(o[e], p2[e]);   // stem row 2ho - 1 (none above row 0)
+          }
+          const int64_t oi = sh.out_pad == 2
+                                 ? (int64_t)(sh.Wo + 2) + ((int64_t)t.n * (sh.Ho + 1) + ho) * (sh.Wo + 1) + wo
+                                 : ((int64_t)t.n * sh.Ho + ho) * sh.Wo + wo;
+          *reinterpret_cast<uint4*>(y + oi * 64 + c * 8) = *reinterpret_cast<const uint4*>(o);
         }
+        part[j] = *reinterpret_cast<const uint4*>(hm[1]);
       }
     }
   }
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, NACC * BN);
+    tmem_dealloc(tmem_base, NACC * ACC_COLS);
   }
 }
 
@@ -1600,9 +1620,9 @@ extern "C" int gg_stem_pool_span(const void* x, int32_t N, int32_t Hs, int32_t W
   sh.Hp = Hs + 3; sh.Wp = Ws + 3;   // space-to-depth input padded 2 before, 1 after
   sh.Ho = Hs / 2; sh.Wo = Ws / 2;   // 3x3 / 2 / pad 1 over an even extent
   sh.out_pad = out_pad;
-  sh.span_rows = 128 + 3 * sh.Wp + 3 + 7;
+  sh.span_rows = 128 + 4 * sh.Wp + 3 + 7;
   sh.a_stage_bytes = (sh.span_rows * 32 + 1023) / 1024 * 1024;
-  const int fixed = 1024 + 16 * 64 * 32 + 2 * kStemPoolRowBytes + 1024;
+  const int fixed = 1024 + kStemShifts * kStemBSlab + 4 * kStemPoolRowBytes + 1024;
   sh.a_stages = (kSpanSmemMax - fixed) / sh.a_stage_bytes;
   if (sh.a_stages > 8) sh.a_stages = 8;
   if (sh.a_stages < 2) return GG_ERR_UNSUPPORTED;
