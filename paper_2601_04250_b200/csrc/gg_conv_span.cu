@@ -1209,11 +1209,15 @@ struct StemPoolShape {
   int out_pad;        // 0: dense [N, Ho, Wo, 64]; 2: shared-border layout
 };
 
-constexpr int kStemPoolRowBytes = 128 * 128;   // one bf16 stem row: 128 px x 64 ch
 constexpr int kStemShifts = 20;                // (r', s): r' = 0..4, s = 0..3
 constexpr int kStemBSlab = 128 * 32;           // one shift's B: 128 rows x 16 ch
 
 struct StemTile { int n, h; bool pre; };
+
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {   // packed bf16x2 max (exact)
+  __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
 
 // Tile i of the CTA owning pool rows [g0, g1): image, first (even) stem row
 __device__ __forceinline__ StemTile stem_tile(int i, int g0, int pre, int Ho) {
@@ -1235,8 +1239,8 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   const int AST = sh.a_stages;
   uint8_t* a_base = smem;
   uint8_t* b_base = smem + AST * sh.a_stage_bytes;
-  uint8_t* rowbuf = b_base + kStemShifts * kStemBSlab;   // [2 bufs][2 rows][128 px][128 B], chunks XOR (px & 7)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rowbuf + 4 * kStemPoolRowBytes);
+  uint8_t* rowbuf = b_base + kStemShifts * kStemBSlab;   // epilogue column-exchange slots (1 KB)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rowbuf + 1024);
   uint64_t* a_full = bars;
   uint64_t* a_empty = a_full + kSpanMaxStages;
   uint64_t* acc_full = a_empty + kSpanMaxStages;
@@ -1335,80 +1339,69 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       __syncwarp();
     }
   } else {
-    const int quarter = warp & 3, row = (warp - 2) >> 2;   // row 0: h, row 1: h + 1
-    const int etid = threadIdx.x - 64;   // 0..255
+    // warp (quarter q, channel half c): lanes w = 32q + lane, channels 32c..32c+31 of
+    // both rows.  Pool vertically in registers first (rows 2ho - 1 | 2ho | 2ho + 1:
+    // the previous tile's second row is the register partial), then horizontally
+    // across lanes by shuffles; lane 0 takes column w - 1 from the previous quarter's
+    // lane 31 through a 64-byte smem slot.  No staging of the rows in shared memory
+    // (whose bandwidth the N = 128 MMAs nearly saturate).
+    const int quarter = warp & 3, c = (warp - 2) >> 2;
     const int w = quarter * 32 + lane;   // this lane's stem column
-    const int items = sh.Wo * 8;         // (pool column, 8-channel group)
-    const __nv_bfloat162 ninf = __float2bfloat162_rn(-INFINITY);
-    uint4 part[2];                       // max over stem row 2ho - 1 (the previous tile's second row)
+    uint32_t* xch = reinterpret_cast<uint32_t*>(rowbuf);   // [2 bufs][2 halves][4 quarters][16 words]
+    float bz[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) bz[i] = __ldg(bias + c * 32 + i);
+    uint32_t part[16];   // stem row 2ho - 1 at (w, this half's channels), bf16x2
     for (int i = 0; i < ntiles; ++i) {
       const StemTile t = stem_tile(i, g0, pre, sh.Ho);
       const int acc = i % NACC;
       mbar_wait_sleep(&acc_full[acc], (i / NACC) & 1);
       tc_fence_after();
-      uint32_t r[2][32];
-      const uint32_t ta = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ACC_COLS + row * 64;
-      tmem_ld_32x32b_x32(ta, r[0]);
-      tmem_ld_32x32b_x32(ta + 32, r[1]);
+      uint32_t r0[32], r1[32];
+      const uint32_t ta = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ACC_COLS + c * 32;
+      tmem_ld_32x32b_x32(ta, r0);        // row h
+      tmem_ld_32x32b_x32(ta + 64, r1);   // row h + 1
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[acc]);
-      uint8_t* rb = rowbuf + ((i & 1) * 2) * kStemPoolRowBytes;
-      if (w < sh.Ws) {
-        uint8_t* myrow = rb + row * kStemPoolRowBytes + w * 128;
+      uint32_t vm[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + q * 8));
-          const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + q * 8 + 4));
-          const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-          float v[8];
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t a0 = pack_bf16(fmaxf(__uint_as_float(r0[2 * e]) + bz[2 * e], 0.0f),
+                                      fmaxf(__uint_as_float(r0[2 * e + 1]) + bz[2 * e + 1], 0.0f));
+        const uint32_t a1 = pack_bf16(fmaxf(__uint_as_float(r1[2 * e]) + bz[2 * e], 0.0f),
+                                      fmaxf(__uint_as_float(r1[2 * e + 1]) + bz[2 * e + 1], 0.0f));
+        uint32_t v = bmax2(a0, a1);
+        if (t.h != 0) v = bmax2(v, part[e]);   // no stem row above row 0
+        vm[e] = v;
+        part[e] = a1;
+      }
+      if (t.pre) continue;   // band-start tile: only the partial (row 2ho0 - 1)
+      uint32_t* slot = xch + (((i & 1) * 2 + c) * 4) * 16;
+      if (lane == 31 && quarter < 3) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) v[e] = fmaxf(__uint_as_float(r[q >> 2][(q & 3) * 8 + e]) + bb[e], 0.0f);
-          uint4 u;
-          u.x = pack_bf16(v[0], v[1]);
-          u.y = pack_bf16(v[2], v[3]);
-          u.z = pack_bf16(v[4], v[5]);
-          u.w = pack_bf16(v[6], v[7]);
-          *reinterpret_cast<uint4*>(myrow + ((q ^ (w & 7)) << 4)) = u;
-        }
+        for (int e = 0; e < 16; e += 4)
+          *reinterpret_cast<uint4*>(slot + quarter * 16 + e) = make_uint4(vm[e], vm[e + 1], vm[e + 2], vm[e + 3]);
       }
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kSpanEpiWarps) : "memory");
-      const int ho = t.h >> 1;
+      uint32_t o[16];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int it = etid + j * 256;
-        if (it >= items) continue;
-        const int wo = it >> 3, c = it & 7;
-        __nv_bfloat162 hm[2][4];
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t right = __shfl_down_sync(0xffffffffu, vm[e], 1);
+        uint32_t left = __shfl_up_sync(0xffffffffu, vm[e], 1);
+        if (lane == 0) left = quarter > 0 ? slot[(quarter - 1) * 16 + e] : vm[e];   // w = 0: no column -1
+        o[e] = bmax2(bmax2(left, vm[e]), right);
+      }
+      const int wo = w >> 1;
+      if (!(lane & 1) && wo < sh.Wo) {
+        const int ho = t.h >> 1;
+        const int64_t oi = sh.out_pad == 2
+                               ? (int64_t)(sh.Wo + 2) + ((int64_t)t.n * (sh.Ho + 1) + ho) * (sh.Wo + 1) + wo
+                               : ((int64_t)t.n * sh.Ho + ho) * sh.Wo + wo;
+        uint4* dst = reinterpret_cast<uint4*>(y + oi * 64 + c * 32);
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) hm[rr][e] = ninf;
-#pragma unroll
-          for (int dw = -1; dw <= 1; ++dw) {
-            const int ww = 2 * wo + dw;
-            if (ww < 0 || ww >= sh.Ws) continue;
-            const uint4 u = *reinterpret_cast<const uint4*>(rb + rr * kStemPoolRowBytes + ww * 128 + ((c ^ (ww & 7)) << 4));
-            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) hm[rr][e] = __hmax2(hm[rr][e], h2[e]);
-          }
-        }
-        if (!t.pre) {
-          __nv_bfloat162 o[4];
-          const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&part[j]);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            o[e] = __hmax2(hm[0][e], hm[1][e]);
-            if (t.h != 0) o[e] = __hmax2(o[e], p2[e]);   // stem row 2ho - 1 (none above row 0)
-          }
-          const int64_t oi = sh.out_pad == 2
-                                 ? (int64_t)(sh.Wo + 2) + ((int64_t)t.n * (sh.Ho + 1) + ho) * (sh.Wo + 1) + wo
-                                 : ((int64_t)t.n * sh.Ho + ho) * sh.Wo + wo;
-          *reinterpret_cast<uint4*>(y + oi * 64 + c * 8) = *reinterpret_cast<const uint4*>(o);
-        }
-        part[j] = *reinterpret_cast<const uint4*>(hm[1]);
+        for (int e = 0; e < 16; e += 4) dst[e / 4] = make_uint4(o[e], o[e + 1], o[e + 2], o[e + 3]);
       }
     }
   }
@@ -1622,7 +1615,7 @@ extern "C" int gg_stem_pool_span(const void* x, int32_t N, int32_t Hs, int32_t W
   sh.out_pad = out_pad;
   sh.span_rows = 128 + 4 * sh.Wp + 3 + 7;
   sh.a_stage_bytes = (sh.span_rows * 32 + 1023) / 1024 * 1024;
-  const int fixed = 1024 + kStemShifts * kStemBSlab + 4 * kStemPoolRowBytes + 1024;
+  const int fixed = 1024 + kStemShifts * kStemBSlab + 1024 + 1024;
   sh.a_stages = (kSpanSmemMax - fixed) / sh.a_stage_bytes;
   if (sh.a_stages > 8) sh.a_stages = 8;
   if (sh.a_stages < 2) return GG_ERR_UNSUPPORTED;

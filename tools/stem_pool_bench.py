@@ -13,7 +13,7 @@ import torch  # noqa: E402
 def main():
     from paper_2601_04250_b200 import _native as nat
     lib = nat.load()
-    n, hs = 64, 112
+    n, hs = int(os.environ.get("N", "64")), 112
     x16 = torch.randn(((n * (hs + 3) * (hs + 3)), 16), device="cuda").to(torch.bfloat16)
     w = (torch.randn((64, 256), device="cuda") * 0.05).to(torch.bfloat16)
     b = torch.randn(64, device="cuda")
