@@ -23,7 +23,7 @@ timeout 300 $NCU --set full --import-source on -k regex:layernorm_kernel -s 1 -c
   -o "$OUT/distilbert_layernorm" python tools/forward_once.py distilbert 1 > /dev/null 2>&1
 timeout 300 $NCU --set full --import-source on -k regex:attention_tcgen05 -s 1 -c 1 \
   -o "$OUT/distilbert_attention" python tools/forward_once.py distilbert 1 > /dev/null 2>&1
-timeout 300 $NCU --set full --import-source on -k regex:stem_pool_span -s 1 -c 1 \
+timeout 300 $NCU --set full --import-source on -k regex:stem_pool_span -s 0 -c 1 \
   -o "$OUT/resnet18_stem_pool" python tools/forward_once.py resnet18 1 > /dev/null 2>&1
 GG_PROBE_EAGER=1 timeout 300 $NCU --set full --import-source on -k regex:admit_small_kernel -s 1 -c 1 \
   -o "$OUT/k1_admit_2p26" python tools/kernel_probe.py k1 1 > /dev/null 2>&1
