@@ -209,6 +209,7 @@ def run_ours(args, wl, rank, world, local_rank, pg):
 
     # ---- roofline of the forward (full batch, CUDA events on the launch stream)
     ro = roofline_forward(srv, net, B)
+    energy = forward_energy(srv, net, B, local_rank)
     k1 = admission_kernel_roofline(dev) if rank == 0 else None
 
     tot = torch.tensor([ms, float(served), float(decided), float(admitted), e2e["ms"],
@@ -225,6 +226,7 @@ def run_ours(args, wl, rank, world, local_rank, pg):
     res = srv.results()
     return dict(ms=ms_max, served=served_all, decided=decided_all, admitted=admitted_all,
                 e2e_ms=e2e_ms_max, e2e_served=e2e_served_all, e2e=e2e, roofline=ro, clocks=clk, k1=k1,
+                energy=energy,
                 launches_per_step=launches_per_step, overflow=res["overflow"],
                 queue_depth=res["queue_depth"])
 
@@ -384,7 +386,7 @@ def roofline_forward(srv, net, B):
     flops = net.flops(B)
     pk = peaks()
     achieved = flops / (ms * 1e-3) / 1e12
-    kern = ("ResNet-18 forward: stem span conv + max pool + 4 span convs (layer 1) + 9 CTA-pair "
+    kern = ("ResNet-18 forward: fused stem conv + max pool + 4 span convs (layer 1) + 9 CTA-pair "
             "span convs (layers 2-4) + 3 fused stride-2 conv/downsample (TMA im2col) + avg pool + "
             "fc, all tcgen05, shared-border NHWC layout"
             if srv.kind == "resnet18"
@@ -402,6 +404,54 @@ def roofline_forward(srv, net, B):
             "traffic": traffic, "traffic_unit": "bytes per forward (DRAM read + write)",
             "traffic_source": traffic_src, "kernel": kern, "flops_per_launch": flops,
             "ms_per_launch": round(ms, 4), "peak_source": pk["source"] + " bf16_tflops_sustained"}
+
+
+def forward_energy(srv, net, B, local_rank, seconds: float = 0.5):
+    """Measured energy (NVML total-energy counter, this GPU) of full-batch forwards
+    replayed back to back for >= `seconds` — joules per inference of the dominant
+    kernel family (telemetry).  None without NVML."""
+    import time
+    import torch
+    from paper_2601_04250_b200.nvml_energy import NvmlEnergyMeter, NvmlUnavailable, energy_report
+    try:
+        meter = NvmlEnergyMeter(torch.cuda.current_device() if local_rank is None else local_rank)
+    except NvmlUnavailable:
+        return None
+    full = torch.full((1,), B, dtype=torch.int32, device=srv.dev)
+    s = srv.stream
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        if srv.kind == "resnet18":
+            net.forward_s2d(B, stream=s, count=full)
+        else:
+            net.forward(srv.tok_ids, srv.tok_mask, batch=B, stream=s, count=full)
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        for _ in range(10):
+            if srv.kind == "resnet18":
+                net.forward_s2d(B, stream=s, count=full)
+            else:
+                net.forward(srv.tok_ids, srv.tok_mask, batch=B, stream=s, count=full)
+    n = 0
+    torch.cuda.synchronize()
+    meter.start()
+    t0 = time.perf_counter()
+    with torch.cuda.stream(s):
+        while time.perf_counter() - t0 < seconds:
+            for _ in range(20):
+                g.replay()
+            n += 200
+            torch.cuda.synchronize()
+    joules = meter.stop()
+    secs = time.perf_counter() - t0
+    r = energy_report(joules, float(n * B))
+    r.update({"seconds": round(secs, 3), "mean_watts": round(joules / secs, 1) if secs > 0 else None,
+              "scope": f"{n} full-batch forwards (B={B}) replayed back to back, NVML "
+                       "nvmlDeviceGetTotalEnergyConsumption delta on this GPU; telemetry, not "
+                       "fed to the controller"})
+    for k in ("joules", "joules_per_inference", "kwh_per_million", "kg_co2_per_million"):
+        r[k] = round(r[k], 6) if r[k] == r[k] else None
+    return r
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -541,7 +591,8 @@ def main():
                     "h2d_bytes_per_step": r["e2e"]["h2d_bytes_per_step"],
                     "d2h_bytes_per_step": r["e2e"]["d2h_bytes_per_step"]},
             "gpu_launches": r["launches_per_step"] * args.steps,
-            "clocks": r["clocks"]}
+            "clocks": r["clocks"],
+            "energy": r["energy"]}
     print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist
