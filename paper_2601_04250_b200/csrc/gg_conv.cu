@@ -145,8 +145,11 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     // ===== TMA producer (im2col A + tiled B) =====
     if (threadIdx.x == 0) {
       tma_prefetch(&map_x);
+      // lean like the issuer: stage / phase and (tap, channel block) advance incrementally
       const int cblocks = sh.C / 64;
-      int it = 0;
+      const int ctap = (sh.R * sh.S) / 2;
+      int s = 0;
+      uint32_t ph = 0;
       SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
       SkWork w;
       while (sc.next(w)) {
@@ -156,40 +159,52 @@ __global__ void __launch_bounds__(kConvThreads, 1)
         const int rem = m0 - n0 * sh.Ho * sh.Wo;
         const int ho0 = rem / sh.Wo, wo0 = rem - (rem / sh.Wo) * sh.Wo;
         const int wc = wo0 * sh.stride - sh.pad, hc = ho0 * sh.stride - sh.pad;
-        for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
-          const int s = it % nst;
-          mbar_wait_sleep(&empty[s], ((it / nst) & 1) ^ 1);
+        // MODE 1: k-block kb = (tap, channel block cb); MODE 2: taps 4 kb .. 4 kb + 3
+        int tap = MODE == 1 ? w.kb0 / cblocks : w.kb0 * 4;
+        int cb = MODE == 1 ? w.kb0 - tap * cblocks : 0;
+        int rr = tap / sh.S, ss = tap - rr * sh.S;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          mbar_wait_sleep(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
           {
             uint32_t bytes = sh.bres ? L::A_BYTES : L::A_BYTES + L::B_BYTES;
             if constexpr (DS)
-              if (kb / cblocks == (sh.R * sh.S) / 2) bytes += L::B_BYTES;
+              if (tap == ctap) bytes += L::B_BYTES;
             mbar_expect_tx(&full[s], bytes);
           }
           constexpr int kLoads = MODE == 1 ? 1 : 4;
 #pragma unroll
           for (int q = 0; q < kLoads; ++q) {
-            int tap, c0;
-            if (MODE == 1) {
-              tap = kb / cblocks;
-              c0 = (kb - tap * cblocks) * 64;
-            } else {
-              tap = kb * 4 + q;
-              c0 = 0;
-            }
-            const int rr = tap / sh.S, ss = tap - rr * sh.S;
             asm volatile(
                 "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
                 " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(sa + q * 4096)),
-                "l"(&map_x), "r"(smem_u32(&full[s])), "r"(c0), "r"(wc), "r"(hc), "r"(n0),
+                "l"(&map_x), "r"(smem_u32(&full[s])), "r"(cb * 64), "r"(wc), "r"(hc), "r"(n0),
                 "h"((uint16_t)ss), "h"((uint16_t)rr)
                 : "memory");
+            if (MODE == 2) {   // next tap
+              if (++ss == sh.S) {
+                ss = 0;
+                ++rr;
+              }
+            }
           }
           if (!sh.bres) tma_load_2d(sa + L::A_BYTES, &map_w, &full[s], kb * 64, tn * BN);
           if constexpr (DS) {   // centre tap: the downsample's weights for this channel block
-            const int tap = kb / cblocks;
-            if (tap == (sh.R * sh.S) / 2)
-              tma_load_2d(sa + L::A_BYTES + L::B_BYTES, &map_wds, &full[s], (kb - tap * cblocks) * 64, tn * BN);
+            if (tap == ctap)
+              tma_load_2d(sa + L::A_BYTES + L::B_BYTES, &map_wds, &full[s], cb * 64, tn * BN);
+          }
+          if (MODE == 1 && ++cb == cblocks) {   // next (tap, channel block)
+            cb = 0;
+            ++tap;
+            if (++ss == sh.S) {
+              ss = 0;
+              ++rr;
+            }
+          }
+          if (MODE == 2) tap += 4;
+          if (++s == nst) {
+            s = 0;
+            ph ^= 1;
           }
         }
       }
@@ -247,42 +262,54 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   } else if (warp == kConvProdWarps) {
     // ===== MMA issuer: the warp runs the loop, one elected lane issues =====
     {
+      // The issuer is one dependent instruction stream: at ~64 tensor cycles per MMA
+      // a k-block's 4 MMAs last ~256 cycles, so its bookkeeping must stay well below
+      // that.  Stage index / phase advance incrementally (no runtime % and /), the
+      // operand descriptors are base + constant offsets (the 14-bit start-address
+      // field never carries: smem < 256 KB), the centre-tap range is precomputed.
       constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
-      int it = 0, t = 0;
+      int t = 0, s = 0;
+      uint32_t ph = 0;
       if (b_loaded) mbar_wait(b_full, 0);   // also when the count leaves no tile: drain
       SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
       SkWork w;
+      const uint64_t a_desc0 = MODE == 2 ? sdesc_k_sw32(smem_u32(smem)) : sdesc_k_sw128(smem_u32(smem));
+      const uint64_t b_desc0 = sdesc_k_sw128(smem_u32(sh.bres ? bres : smem + L::A_BYTES));
+      constexpr uint64_t kStageD = (uint64_t)(L::STAGE_BYTES >> 4), kBD = (uint64_t)(L::B_BYTES >> 4);
+      const int cbl = sh.C / 64;
+      const int kb_c0 = ((sh.R * sh.S) / 2) * cbl, kb_c1 = kb_c0 + cbl;   // DS: centre-tap k-blocks
       for (; sc.next(w); ++t) {
         const int acc = t & 1;
         const uint32_t use = t >> 1;
         mbar_wait(&acc_empty[acc], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * NACC_COLS;
-        for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
-          const int s = it % nst;
-          mbar_wait(&full[s], (it / nst) & 1);
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
-          const uint32_t sb = sh.bres ? smem_u32(bres + kb * L::B_BYTES) : sa + L::A_BYTES;
+          const uint64_t ad = a_desc0 + (uint64_t)s * kStageD;
+          const uint64_t bd = sh.bres ? b_desc0 + (uint64_t)kb * kBD : b_desc0 + (uint64_t)s * kStageD;
           if (elect_one_sync()) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              umma_bf16(d_tmem, MODE == 2 ? sdesc_k_sw32(sa + kk * 4096) : sdesc_k_sw128(sa + kk * 32),
-                        sdesc_k_sw128(sb + kk * 32), idesc,
+              umma_bf16(d_tmem, ad + (uint64_t)(MODE == 2 ? kk * 256 : kk * 2), bd + (uint64_t)(kk * 2), idesc,
                         (kb != w.kb0 || kk != 0));
             if constexpr (DS) {
-              const int cbl = sh.C / 64, tap = kb / cbl;
-              if (tap == (sh.R * sh.S) / 2) {   // downsample accumulator: K = Cin (centre tap only)
-                const uint32_t sd = sa + L::A_BYTES + L::B_BYTES;
+              if (kb >= kb_c0 && kb < kb_c1) {   // downsample accumulator: K = Cin (centre tap only)
+                const uint64_t dd = b_desc0 + (uint64_t)s * kStageD + kBD;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                  umma_bf16(d_tmem + BN, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sd + kk * 32), idesc,
-                            (kb - tap * cbl) != 0 || kk != 0);
+                  umma_bf16(d_tmem + BN, ad + (uint64_t)(kk * 2), dd + (uint64_t)(kk * 2), idesc,
+                            kb != kb_c0 || kk != 0);
               }
             }
             umma_commit(&empty[s]);
           }
           __syncwarp();
+          if (++s == nst) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         if (elect_one_sync()) umma_commit(&acc_full[acc]);
         __syncwarp();
