@@ -750,29 +750,37 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int ait = 0, bit = 0;
+      // ring positions advance incrementally (no runtime % and / per load)
+      int as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
       SkSched sc(ep.sk.enabled, num_tiles, cblocks, pair, npairs);
       SkWork wk;
       while (sc.next(wk)) {
         const int tile = wk.tile;
         const int tm = tile % tiles_m, tn = tile / tiles_m;
         const int m0 = tm * 256 + rank * 128;
-        for (int cb = wk.kb0; cb < wk.kb1; ++cb, ++ait) {
-          const int as = ait % AST;
-          mbar_wait_sleep(&a_empty[as], ((ait / AST) & 1) ^ 1);
+        for (int cb = wk.kb0; cb < wk.kb1; ++cb) {
+          mbar_wait_sleep(&a_empty[as], aph ^ 1);
           uint8_t* sa = a_base + as * sh.a_stage_bytes;
           const uint32_t fa = mapa_shared(smem_u32(&a_full[as]), 0);
           if (rank == 0) mbar_expect_tx(&a_full[as], 2 * sh.boxes * sh.box_rows * RB);
           for (int bx = 0; bx < sh.boxes; ++bx)
             tma_load_2d_pair(sa + bx * sh.box_rows * RB, &map_x, fa, cb * CH, m0 + bx * sh.box_rows);
+          if (++as == AST) {
+            as = 0;
+            aph ^= 1;
+          }
           if (!sh.bres) {
-            for (int tap = 0; tap < TAPS; ++tap, ++bit) {
-              const int bs = bit % BST;
-              mbar_wait_sleep(&b_empty[bs], ((bit / BST) & 1) ^ 1);
+            for (int tap = 0; tap < TAPS; ++tap) {
+              mbar_wait_sleep(&b_empty[bs], bph ^ 1);
               const uint32_t fb = mapa_shared(smem_u32(&b_full[bs]), 0);
               if (rank == 0) mbar_expect_tx(&b_full[bs], 2 * B_BYTES);
               tma_load_2d_pair(b_base + bs * B_BYTES, &map_w, fb, (cb * TAPS + tap) * CH,
                                tn * BN + rank * BH);
+              if (++bs == BST) {
+                bs = 0;
+                bph ^= 1;
+              }
             }
           }
         }
@@ -786,7 +794,12 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       for (int tap = 0; tap < TAPS; ++tap) tap_off[tap] = (uint64_t)(((tap / RT) * sh.Wp + tap % RT) * (RB / 16));
       if (b_loaded) mbar_wait(bres_full, 0);
       const uint64_t bres_desc = sdesc_sw(smem_u32(b_base), RB);
-      int ait = 0, bit = 0, t = 0;
+      const uint64_t a_desc0 = sdesc_sw(smem_u32(a_base), RB);
+      const uint64_t a_stage_d = (uint64_t)(sh.a_stage_bytes >> 4);
+      // one dependent instruction stream feeds the tensor pipe: ring positions and
+      // descriptors advance incrementally (no runtime % and / per tap)
+      int as = 0, bs = 0, t = 0;
+      uint32_t aph = 0, bph = 0;
       SkSched sc(ep.sk.enabled, num_tiles, cblocks, pair, npairs);
       SkWork wk;
       for (; sc.next(wk); ++t) {
@@ -794,11 +807,15 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
         mbar_wait(&acc_empty[acc], ((t / NACC) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int cb = wk.kb0; cb < wk.kb1; ++cb, ++ait) {
-          const int as = ait % AST;
-          mbar_wait(&a_full[as], (ait / AST) & 1);
+        for (int cb = wk.kb0; cb < wk.kb1; ++cb) {
+          mbar_wait(&a_full[as], aph);
           tc_fence_after();
-          const uint64_t ad = sdesc_sw(smem_u32(a_base + as * sh.a_stage_bytes), RB);
+          const uint64_t ad = a_desc0 + (uint64_t)as * a_stage_d;
+          const int as_now = as;
+          if (++as == AST) {
+            as = 0;
+            aph ^= 1;
+          }
           if (sh.bres) {
             const uint64_t bd = bres_desc + (uint64_t)(cb * TAPS * (B_BYTES >> 4));
             if (elect_one_sync()) {
@@ -811,26 +828,29 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
                   umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
                                  (cb != wk.kb0 || tap != 0 || kk != 0));
               }
-              umma_commit_pair(&a_empty[as], 3);
+              umma_commit_pair(&a_empty[as_now], 3);
             }
             __syncwarp();
           } else {
 #pragma unroll
-            for (int tap = 0; tap < TAPS; ++tap, ++bit) {
-              const int bs = bit % BST;
-              mbar_wait(&b_full[bs], (bit / BST) & 1);
+            for (int tap = 0; tap < TAPS; ++tap) {
+              mbar_wait(&b_full[bs], bph);
               tc_fence_after();
               const uint64_t ao = ad + tap_off[tap];
-              const uint64_t bo = bres_desc + (uint64_t)(bs * (B_BYTES >> 4));
+              const uint64_t bo = bres_desc + (uint64_t)bs * (uint64_t)(B_BYTES >> 4);
               if (elect_one_sync()) {
 #pragma unroll
                 for (int kk = 0; kk < KSTEPS; ++kk)
                   umma_bf16_pair(d_tmem, ao + (uint64_t)(kk * 2), bo + (uint64_t)(kk * 2), idesc,
                                  (cb != wk.kb0 || tap != 0 || kk != 0));
                 umma_commit_pair(&b_empty[bs], 3);
-                if (tap == TAPS - 1) umma_commit_pair(&a_empty[as], 3);
+                if (tap == TAPS - 1) umma_commit_pair(&a_empty[as_now], 3);
               }
               __syncwarp();
+              if (++bs == BST) {
+                bs = 0;
+                bph ^= 1;
+              }
             }
           }
         }
