@@ -179,7 +179,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ===== TMA producer =====
     if (lane == 0) {
-      int it = 0;
+      int s = 0;
+      uint32_t ph = 0;
       SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
       SkWork w;
       while (sc.next(w)) {
@@ -188,15 +189,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         // once share A row blocks (read from HBM once, reused across the N tiles)
         const int tm = ep.raster_n ? w.tile / tiles_n : w.tile % tiles_m;
         const int tn = ep.raster_n ? w.tile % tiles_n : w.tile / tiles_m;
-        for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
-          const int s = it % STAGES;
-          const uint32_t round = it / STAGES;
-          mbar_wait_sleep(&empty[s], (round & 1) ^ 1);
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          mbar_wait_sleep(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
           uint8_t* sb = sa + L::A_BYTES;
           mbar_expect_tx(&full[s], L::STAGE_BYTES);
           tma_load_2d(sa, &map_a, &full[s], kb * kBK, tm * BM);
           tma_load_2d(sb, &map_b, &full[s], kb * kBK, tn * BN);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
     }
@@ -204,7 +207,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===== MMA issuer: the warp runs the loop, one elected lane issues =====
     {
       constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
-      int it = 0, t = 0;
+      int s = 0, t = 0;
+      uint32_t ph = 0;
+      const uint64_t a_desc0 = sdesc_k_sw128(smem_u32(smem));
       SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
       SkWork w;
       for (; sc.next(w); ++t) {
@@ -213,22 +218,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&acc_empty[acc], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = w.kb0; kb < w.kb1; ++kb, ++it) {
-          const int s = it % STAGES;
-          const uint32_t round = it / STAGES;
-          mbar_wait(&full[s], round & 1);
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {   // lean chain: incremental ring / descriptors
+          mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
-          const uint32_t sb = sa + L::A_BYTES;
+          const uint64_t ad = a_desc0 + (uint64_t)s * (uint64_t)(L::STAGE_BYTES >> 4);
+          const uint64_t bd = ad + (uint64_t)(L::A_BYTES >> 4);
           if (elect_one_sync()) {
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk) {
-              umma_bf16(d_tmem, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sb + kk * 32), idesc,
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              umma_bf16(d_tmem, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
                         (kb != w.kb0 || kk != 0));
-            }
             umma_commit(&empty[s]);
           }
           __syncwarp();
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         if (elect_one_sync()) umma_commit(&acc_full[acc]);
         __syncwarp();
@@ -513,26 +519,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int it = 0;
+      int s = 0;
+      uint32_t ph = 0;
       for (int tile = pair; tile < num_tiles; tile += npairs) {
         const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;   // raster: see above
         const int tn = ep.raster_n ? tile % tiles_n : tile / tiles_m;
         const int m0 = tm * 256 + rank * 128, n0 = tn * kPairBN + rank * 128;
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
-          const int s = it % STAGES;
-          mbar_wait_sleep(&empty[s], ((it / STAGES) & 1) ^ 1);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait_sleep(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * STAGE_BYTES;
           if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
           const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
           tma_load_2d_pair(sa, &map_a, fb, kb * kBK, m0);
           tma_load_2d_pair(sa + A_BYTES, &map_b, fb, kb * kBK, n0);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (rank == 0) {   // leader: the warp runs the loop, one elected lane issues
       constexpr uint32_t idesc = idesc_bf16_f32(256, kPairBN);
-      int it = 0, t = 0;
+      int s = 0, t = 0;
+      uint32_t ph = 0;
+      const uint64_t a_desc0 = sdesc_k_sw128(smem_u32(smem));
       long long w_acc = 0, w_full = 0;            // GG_GEMM_PROF: issuer wait cycles
       const long long t0 = ep.prof ? clock64() : 0;
       for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
@@ -546,26 +558,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kPairBN;
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
-          const int s = it % STAGES;
+        // lean per-k-block chain: ring position and descriptors advance incrementally
+        for (int kb = 0; kb < num_kb; ++kb) {
           if (ep.prof) {
             const long long a = clock64();
-            mbar_wait(&full[s], (it / STAGES) & 1);
+            mbar_wait(&full[s], ph);
             w_full += clock64() - a;
           } else {
-            mbar_wait(&full[s], (it / STAGES) & 1);
+            mbar_wait(&full[s], ph);
           }
           tc_fence_after();
-          const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+          const uint64_t ad = a_desc0 + (uint64_t)s * (uint64_t)(STAGE_BYTES >> 4);
+          const uint64_t bd = ad + (uint64_t)(A_BYTES >> 4);
           if (elect_one_sync()) {
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk)
-              umma_bf16_pair(d_tmem, sdesc_k_sw128(sa + kk * 32), sdesc_k_sw128(sb + kk * 32), idesc,
-                             (kb | kk) != 0);
+              umma_bf16_pair(d_tmem, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
             umma_commit_pair(&empty[s], 3);
           }
           __syncwarp();
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         if (elect_one_sync()) umma_commit_pair(&acc_full[acc], 3);
         __syncwarp();
