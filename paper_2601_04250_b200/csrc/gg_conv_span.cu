@@ -173,13 +173,13 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int ait = 0, bit = 0;
+      int ait = 0, as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int tm = tile % tiles_m, tn = tile / tiles_m;
         const int m0 = tm * BM;
         for (int cb = 0; cb < cblocks; ++cb, ++ait) {
-          const int as = ait % AST;
-          mbar_wait_sleep(&a_empty[as], ((ait / AST) & 1) ^ 1);
+          mbar_wait_sleep(&a_empty[as], aph ^ 1);
           if (ep.prof && blockIdx.x == 0 && cb == 0 && ait / cblocks < 16)
             ep.prof[4096 + (ait / cblocks) * 8 + 0] = clock64();
           uint8_t* sa = a_base + as * sh.a_stage_bytes;
@@ -196,12 +196,19 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
             for (int bx = 0; bx < sh.boxes; ++bx)   // boxes of <= 256 rows (TMA limit)
               tma_load_2d(sa + bx * sh.box_rows * RB, &map_x, &a_full[as], cb * CH, m0 + bx * sh.box_rows);
           }
+          if (++as == AST) {
+            as = 0;
+            aph ^= 1;
+          }
           if (!sh.bres) {
-            for (int tap = 0; tap < TAPS; ++tap, ++bit) {
-              const int bs = bit % BST;
-              mbar_wait_sleep(&b_empty[bs], ((bit / BST) & 1) ^ 1);
+            for (int tap = 0; tap < TAPS; ++tap) {
+              mbar_wait_sleep(&b_empty[bs], bph ^ 1);
               mbar_expect_tx(&b_full[bs], B_BYTES);
               tma_load_2d(b_base + bs * B_BYTES, &map_w, &b_full[bs], (cb * TAPS + tap) * CH, tn * BN);
+              if (++bs == BST) {
+                bs = 0;
+                bph ^= 1;
+              }
             }
           }
         }
@@ -228,18 +235,25 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   } while (0)
       if (b_loaded) mbar_wait(bres_full, 0);   // also when the count leaves no tile: drain the TMA
       const uint64_t bres_desc = sdesc_sw(smem_u32(b_base), RB);
-      int ait = 0, bit = 0, t = 0;
+      const uint64_t a_desc0 = sdesc_sw(smem_u32(a_base), RB);
+      const uint64_t a_stage_d = (uint64_t)(sh.a_stage_bytes >> 4);
+      int as = 0, bs = 0, t = 0;   // ring positions advance incrementally (lean issue chain)
+      uint32_t aph = 0, bph = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
         const int acc = t % NACC;
         SPAN_WAIT(&acc_empty[acc], ((t / NACC) & 1) ^ 1, 0);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * ACC_COLS;
-        for (int cb = 0; cb < cblocks; ++cb, ++ait) {
-          const int as = ait % AST;
-          SPAN_WAIT(&a_full[as], (ait / AST) & 1, 1);
+        for (int cb = 0; cb < cblocks; ++cb) {
+          SPAN_WAIT(&a_full[as], aph, 1);
           if (ep.prof && blockIdx.x == 0 && cb == 0 && t < 16 && lane == 0) ep.prof[4096 + t * 8 + 1] = clock64();
           tc_fence_after();
-          const uint64_t ad = sdesc_sw(smem_u32(a_base + as * sh.a_stage_bytes), RB);
+          const uint64_t ad = a_desc0 + (uint64_t)as * a_stage_d;
+          const int as_now = as;
+          if (++as == AST) {
+            as = 0;
+            aph ^= 1;
+          }
           if (sh.bres) {
             const uint64_t bd = bres_desc + (uint64_t)(cb * TAPS * (B_BYTES >> 4));
             if (elect_one_sync()) {
@@ -254,17 +268,16 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
                     umma_bf16(d_tmem + mt * BN, ao + (uint64_t)(mt * 128 * RB / 16 + kk * 2),
                               bo + (uint64_t)(kk * 2), idesc, (cb | tap | kk) != 0);
               }
-              umma_commit(&a_empty[as]);
+              umma_commit(&a_empty[as_now]);
             }
             __syncwarp();
           } else {
 #pragma unroll
-            for (int tap = 0; tap < TAPS; ++tap, ++bit) {
-              const int bs = bit % BST;
-              SPAN_WAIT(&b_full[bs], (bit / BST) & 1, 2);
+            for (int tap = 0; tap < TAPS; ++tap) {
+              SPAN_WAIT(&b_full[bs], bph, 2);
               tc_fence_after();
               const uint64_t ao = ad + tap_off[tap];
-              const uint64_t bo = bres_desc + (uint64_t)(bs * (B_BYTES >> 4));
+              const uint64_t bo = bres_desc + (uint64_t)bs * (uint64_t)(B_BYTES >> 4);
               if (elect_one_sync()) {
 #pragma unroll
                 for (int kk = 0; kk < KSTEPS; ++kk)
@@ -273,9 +286,13 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
                     umma_bf16(d_tmem + mt * BN, ao + (uint64_t)(mt * 128 * RB / 16 + kk * 2),
                               bo + (uint64_t)(kk * 2), idesc, (cb | tap | kk) != 0);
                 umma_commit(&b_empty[bs]);
-                if (tap == TAPS - 1) umma_commit(&a_empty[as]);
+                if (tap == TAPS - 1) umma_commit(&a_empty[as_now]);
               }
               __syncwarp();
+              if (++bs == BST) {
+                bs = 0;
+                bph ^= 1;
+              }
             }
           }
         }
@@ -1340,20 +1357,29 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     for (int j = 0; j < kStemShifts; ++j) sh_off[j] = (uint64_t)(((j >> 2) * sh.Wp + (j & 3)) * (RB / 16));
     mbar_wait(b_full, 0);
     const uint64_t bdesc = sdesc_k_sw32(smem_u32(b_base));
+    const uint64_t a_desc0 = sdesc_k_sw32(smem_u32(a_base));
+    const uint64_t a_stage_d = (uint64_t)(sh.a_stage_bytes >> 4);
+    int as = 0;
+    uint32_t aph = 0;
     for (int i = 0; i < ntiles; ++i) {
       const StemTile t = stem_tile(i, g0, pre, sh.Ho);
-      const int acc = i % NACC, as = i % AST;
+      const int acc = i % NACC;
       mbar_wait(&acc_empty[acc], ((i / NACC) & 1) ^ 1);
-      mbar_wait(&a_full[as], (i / AST) & 1);
+      mbar_wait(&a_full[as], aph);
       tc_fence_after();
       const int64_t m0 = ((int64_t)t.n * sh.Hp + t.h) * sh.Wp;
-      const uint64_t ad = sdesc_k_sw32(smem_u32(a_base + as * sh.a_stage_bytes)) + (uint64_t)((m0 & 7) * (RB / 16));
+      const uint64_t ad = a_desc0 + (uint64_t)as * a_stage_d + (uint64_t)((m0 & 7) * (RB / 16));
+      const int as_now = as;
+      if (++as == AST) {
+        as = 0;
+        aph ^= 1;
+      }
       if (elect_one_sync()) {
 #pragma unroll
         for (int j = 0; j < kStemShifts; ++j)
           umma_bf16(tmem_base + acc * ACC_COLS, ad + sh_off[j], bdesc + (uint64_t)(j * (kStemBSlab >> 4)), idesc,
                     j != 0);
-        umma_commit(&a_empty[as]);
+        umma_commit(&a_empty[as_now]);
         umma_commit(&acc_full[acc]);
       }
       __syncwarp();
