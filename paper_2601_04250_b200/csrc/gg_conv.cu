@@ -47,7 +47,10 @@ struct ConvEpi {
 };
 
 constexpr int kConvProdWarps = 4;
-constexpr int kConvThreads = 32 * (kConvProdWarps + 1 + 4);
+// epilogue warps: 4 (one per TMEM lane quarter); the fused conv + downsample has
+// twice the accumulator columns per tile and uses 8 (two column halves)
+constexpr int kConvThreadsMax = 32 * (kConvProdWarps + 1 + 8);
+__host__ __device__ constexpr int conv_epi_warps(bool ds) { return ds ? 8 : 4; }
 constexpr int kLag = 2;  // cp.async groups in flight per producer thread
 
 template <int BN, int STAGES, bool DS = false>
@@ -84,7 +87,7 @@ __device__ __forceinline__ void cp_async_wait() {
 //   second weight slab per centre-tap stage and a second TMEM accumulator — instead
 //   of a separate kernel re-loading the input.
 template <int BN, int STAGES, int MODE, bool DS = false>
-__global__ void __launch_bounds__(kConvThreads, 1)
+__global__ void __launch_bounds__(kConvThreadsMax, 1)
     conv_bf16_tcgen05(const __nv_bfloat16* __restrict__ x, const __grid_constant__ CUtensorMap map_w,
                       const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_wds,
                       ConvShape sh, ConvEpi ep) {
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
-      mbar_init(&acc_empty[a], 4);
+      mbar_init(&acc_empty[a], conv_epi_warps(DS));
     }
     fence_mbar_init();
     tma_prefetch(&map_w);
@@ -318,6 +321,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
   } else {
     // ===== epilogue =====
     const int quarter = warp & 3;
+    const int chalf = (warp - kConvProdWarps - 1) >> 2;   // DS: column half of this warp
     int t = 0;
     SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
     SkWork w;
@@ -356,7 +360,7 @@ __global__ void __launch_bounds__(kConvThreads, 1)
                    : ((int64_t)n * (sh.Ho + 2) + ho + 1) * (sh.Wo + 2) + wo + 1;
       }
 #pragma unroll 1
-      for (int cc = 0; cc < (DS ? 2 : 1) * BN; cc += 32) {
+      for (int cc = DS ? chalf * BN : 0; cc < (DS ? (chalf + 1) * BN : BN); cc += 32) {
         // DS: columns [BN, 2 BN) of the buffer are the downsample accumulator
         const bool dsp = DS && cc >= BN;
         const int c = dsp ? cc - BN : cc;
@@ -436,7 +440,8 @@ static int launch_conv(const __nv_bfloat16* x, const CUtensorMap& mw, const CUte
   const int grid = ep.sk.enabled ? num_sms() : (tiles < num_sms() ? tiles : num_sms());
   const int smem = sh.bres ? sh.bres_stages * L::STAGE_BYTES + (sh.Kpad / 64) * L::B_BYTES + 256 + 1024
                            : L::TOTAL;
-  if (launch_pdl(kern, dim3(grid), dim3(kConvThreads), smem, s, x, mw, mx, mwds ? *mwds : mw, sh, ep) !=
+  if (launch_pdl(kern, dim3(grid), dim3(32 * (kConvProdWarps + 1 + conv_epi_warps(DS))), smem, s, x, mw, mx,
+                 mwds ? *mwds : mw, sh, ep) !=
       cudaSuccess)
     return GG_ERR_CUDA;
   return GG_OK;
