@@ -1430,7 +1430,8 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
         for (int e = 0; e < 16; e += 4)
           *reinterpret_cast<uint4*>(slot + quarter * 16 + e) = make_uint4(vm[e], vm[e + 1], vm[e + 2], vm[e + 3]);
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * kSpanEpiWarps) : "memory");
+      // the exchange stays within a channel half: one named barrier per half (4 warps)
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + c) : "memory");
       uint32_t o[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
