@@ -1490,13 +1490,14 @@ static int conv3x3_span(const void* x, int32_t N, int32_t H, int32_t W, int32_t 
   static const bool pair64 = getenv("GG_SPAN_PAIR64") && atoi(getenv("GG_SPAN_PAIR64")) == 1;
   if (!no_pair && (Cout % 128 == 0 || (Cout == 64 && pair64)) && !getenv("GG_SPAN_TILE")) {
     int bn = Cout % 256 == 0 ? 256 : Cout % 128 == 0 ? 128 : 64;
-    if (bn == 256) {   // N = 128 pair tiles when they finish in fewer rounds x width (layer 4)
+    if (bn == 256) {   // N = 128 pair tiles unless N = 256 finishes in strictly fewer rounds x width
       const int64_t mt = (Mtot + 255) / 256, P = num_sms() / 2;
       const int64_t r256 = (mt * (Cout / 256) + P - 1) / P, r128 = (mt * (Cout / 128) + P - 1) / P;
-      // (a tie — layer 3: 114 N=128 tiles in 2 rounds vs 57 in 1 — measured even or
-      // slightly worse with N = 128; GG_SPAN_PAIR_BN=128/256 forces a width)
+      // ties go to N = 128 (layer 3: 114 tiles in 2 rounds beat 57 in 1 once the issue
+      // loop was lean — 17.5 vs 19.5 us — the second tile's MMAs overlap the first's
+      // epilogue); GG_SPAN_PAIR_BN=128/256 forces a width
       static const int pair_bn = getenv("GG_SPAN_PAIR_BN") ? atoi(getenv("GG_SPAN_PAIR_BN")) : 0;
-      if (pair_bn == 128 || (pair_bn != 256 && r128 * 128 < r256 * 256)) bn = 128;
+      if (pair_bn == 128 || (pair_bn != 256 && r128 * 128 <= r256 * 256)) bn = 128;
     }
     sh.span_rows = 128 + 2 * sh.Wp + 2;
     // coalesced TMA-box epilogue (GG_NO_TMA_EPI=1 keeps row-per-thread stores)
