@@ -206,13 +206,21 @@ __global__ void __launch_bounds__(kGatherThreads) stem_gather_kernel(
     const uint8_t* __restrict__ pool, int64_t pool_size, const int32_t* ids, const int32_t* count,
     int B, int H, int W, float m0, float m1, float m2, float s0, float s1, float s2, int padded,
     __nv_bfloat16* __restrict__ y) {
-  griddep_wait();   // PDL: the predecessor has completed and flushed
-  griddep_launch();
   extern __shared__ __align__(16) uint8_t rows[];   // [2 * kGatherRows][W * 3]
   // the normalization of a uint8 value is one of 3 x 256 bf16 results: built once
   // per block with the exact arithmetic, then looked up (12 fp32 divisions per
-  // cell made this kernel issue-bound)
+  // cell made this kernel issue-bound).  It depends on nothing the predecessor
+  // writes, so it is built before the PDL wait, overlapping the predecessor's tail.
   __shared__ __nv_bfloat16 lut[3][256];
+  {
+    const float mean[3] = {m0, m1, m2}, sd[3] = {s0, s1, s2};
+    for (int i = threadIdx.x; i < 3 * 256; i += kGatherThreads) {
+      const int c = i >> 8, xv = i & 255;
+      lut[c][xv] = __float2bfloat16_rn(((float)xv * (1.0f / 255.0f) - mean[c]) / sd[c]);
+    }
+  }
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
   const int n_valid = count ? min(B, __ldg(count)) : B;
   const int n = blockIdx.y, yy0 = blockIdx.x * kGatherRows;
   if (n >= n_valid) return;
@@ -227,13 +235,6 @@ __global__ void __launch_bounds__(kGatherThreads) stem_gather_kernel(
     for (int i = threadIdx.x; i < bytes / 16; i += kGatherThreads) reinterpret_cast<uint4*>(rows)[i] = __ldg(s4 + i);
   } else {
     for (int i = threadIdx.x; i < bytes; i += kGatherThreads) rows[i] = __ldg(src + i);
-  }
-  {
-    const float mean[3] = {m0, m1, m2}, sd[3] = {s0, s1, s2};
-    for (int i = threadIdx.x; i < 3 * 256; i += kGatherThreads) {
-      const int c = i >> 8, xv = i & 255;
-      lut[c][xv] = __float2bfloat16_rn(((float)xv * (1.0f / 255.0f) - mean[c]) / sd[c]);
-    }
   }
   __syncthreads();
   for (int cell = threadIdx.x; cell < nrows * Wo; cell += kGatherThreads) {
