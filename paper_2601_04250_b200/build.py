@@ -23,7 +23,8 @@ OUT = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT, "libgreengate_b200.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-lineinfo", *(["-DGG_GELU_TANH"] if os.environ.get("GG_GELU_TANH") else []), "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+COMMON = ["-O3", "-lineinfo", *(["-DGG_GELU_TANH"] if os.environ.get("GG_GELU_TANH") else []),
+          *os.environ.get("GG_EXTRA_NVCC", "").split(), "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 # per-translation-unit extra flags
 UNITS = {
@@ -51,6 +52,12 @@ def _stale(target: str, deps: list[str]) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(os.path.join(OUT, "obj"), exist_ok=True)
+    # objects built with other flags (e.g. GG_EXTRA_NVCC debug builds) are stale
+    stamp = os.path.join(OUT, "obj", ".flags")
+    flags = " ".join([*ARCH, *COMMON])
+    prev = open(stamp).read() if os.path.exists(stamp) else None
+    if prev != flags:
+        force = True
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "greengate_b200.h"))
     objs = []
@@ -68,6 +75,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-ldl", "-lrt",
                "-lpthread"]
         subprocess.run(cmd, check=True)
+    with open(stamp, "w") as f:
+        f.write(flags)
     return LIB
 
 

@@ -987,8 +987,14 @@ __device__ __forceinline__ bool finite_nonneg(double x) {
 
 template <bool REG>
 __global__ void __launch_bounds__(kFastThreads) admit_large_fast_kernel(AdmitArgs a) {
+#ifdef GG_K1_PROF
+  const unsigned long long tp0 = globaltimer_ns();
+#endif
   griddep_wait();   // PDL: the predecessor has completed and flushed
   griddep_launch();
+#ifdef GG_K1_PROF
+  const unsigned long long tp1 = globaltimer_ns();
+#endif
   __shared__ AdmitShared<kFastThreads, 1> sm;
   __shared__ FastBlock fb_s;
   __shared__ uint8_t codes[kFastRows];
@@ -1008,11 +1014,16 @@ __global__ void __launch_bounds__(kFastThreads) admit_large_fast_kernel(AdmitArg
       xr[i] = (have && c < k) ? __ldg(row + c) : 0.0;
     }
   }
+  // the row's arrival time too (the decision needs it right after the reductions)
+  const double now_g = have ? __ldg(a.now + row0 + r) : 0.0;
   if (tid == 0) {
     block_setup(a, sm);
     fb_s = fast_block(a, sm.bc);
   }
   __syncthreads();
+#ifdef GG_K1_PROF
+  const unsigned long long tp2 = globaltimer_ns();
+#endif
   const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
   if (have) {
     const int64_t g = row0 + r;
@@ -1056,14 +1067,14 @@ __global__ void __launch_bounds__(kFastThreads) admit_large_fast_kernel(AdmitArg
       const FastBlock f = fb_s;
       const float u = entropy ? fminf(fmaxf(-(float)hd * f.inv_log2k, 0.0f), 1.0f)
                               : (float)(1.0 - mx);
-      const float el = (float)fmax(a.now[g] - f.t_origin, 0.0);
+      const float el = (float)fmax(now_g - f.t_origin, 0.0);
       const float tau = f.tau_inf + f.dtau * ex2_approx(f.negk_log2e * el);
       const float d = (f.alpha * u + f.jc) - tau;
       if (!(fabsf(d) > f.margin)) exact = true;
       else code = (f.geq ? d > 0.0f : d < 0.0f) ? f.adm_code : GG_DECISION_SKIP;
     }
     if (exact)   // warp-uniform; rare: the reference's own evaluation order
-      code = exact_row_warp(a, sm.bc, row, k, a.now[g], entropy, mx);
+      code = exact_row_warp(a, sm.bc, row, k, now_g, entropy, mx);
     if (lane == 0) {
       codes[warp] = (uint8_t)code;
       a.decision[g] = (uint8_t)code;
@@ -1078,7 +1089,15 @@ __global__ void __launch_bounds__(kFastThreads) admit_large_fast_kernel(AdmitArg
   const unsigned long long my_bad =
       (in && code == GG_DECISION_INVALID) ? (unsigned long long)(nw - rr) : 0ull;
   uint32_t ballots[1] = {__ballot_sync(0xffffffffu, in && (code == GG_DECISION_DIRECT || code == GG_DECISION_BATCHED))};
+#ifdef GG_K1_PROF
+  const unsigned long long tp3 = globaltimer_ns();
+#endif
   finish_tile<kFastThreads, 1>(a, sm, tile0, ballots, my_skip, my_bad);
+#ifdef GG_K1_PROF
+  if (tid == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+    printf("K1 block %d/%d: wait %llu, setup+loads %llu, rows %llu, finish %llu ns (start %llu)\n", blockIdx.x,
+           gridDim.x, tp1 - tp0, tp2 - tp1, tp3 - tp2, globaltimer_ns() - tp3, tp0 % 1000000ull);
+#endif
 }
 
 // ---------------------------------------------------------------------------
