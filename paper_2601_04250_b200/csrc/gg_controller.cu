@@ -1343,6 +1343,8 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
   __shared__ int32_t sq[kOutChunk];
   __shared__ double sp[kOutChunk];
   __shared__ double sew[kOutChunk];   // EWMA after each outcome (energy channel observes)
+  __shared__ double s_ewma, s_total;  // the EWMA chain's results (last warp -> thread 0)
+  __shared__ int64_t s_seen;
   __shared__ int64_t slot_off[kOutMaxSlots + 1];
   __shared__ int s_flag, s_first;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1456,9 +1458,25 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
         bad = e;
       }
     }
-    // p95 after each outcome: one warp per outcome
+    // the order-dependent chains, one thread in CPython order — the EWMA recurrence
+    // (energy.py:24-36, 75-87) and the running total — on the last warp, which
+    // takes no p95 work, so the chain overlaps the p95 selection below
+    if (tid == kOutThreads - 32) {
+      #pragma unroll 1
+      for (int c = 0; c < nc; ++c) {
+        const double J = sj[c];
+        ewma = (seen > 0) ? f64_add(f64_mul(lam, ewma), f64_mul(one_minus_lam, J)) : J;
+        seen += 1;
+        total = f64_add(total, J);
+        sew[c] = ewma;
+      }
+      s_ewma = ewma;
+      s_total = total;
+      s_seen = seen;
+    }
+    // p95 after each outcome: one warp per outcome (all warps but the chain's)
     #pragma unroll 1
-    for (int c = warp; c < nc; c += kOutThreads / 32) {
+    for (int c = warp; c < nc && warp < kOutThreads / 32 - 1; c += kOutThreads / 32 - 1) {
       const int cnt = min(cap, h + c + 1);
       const int start = h + c + 1 - cnt;
       double v[S];
@@ -1508,16 +1526,9 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
     }
     __syncthreads();
     if (tid == 0) {
-      // the order-dependent chains, one thread in CPython order: the EWMA recurrence
-      // (energy.py:24-36, 75-87) and the running total
-      #pragma unroll 1
-      for (int c = 0; c < nc; ++c) {
-        const double J = sj[c];
-        ewma = (seen > 0) ? f64_add(f64_mul(lam, ewma), f64_mul(one_minus_lam, J)) : J;
-        seen += 1;
-        total = f64_add(total, J);
-        sew[c] = ewma;
-      }
+      ewma = s_ewma;
+      total = s_total;
+      seen = s_seen;
       outc += nc;
       if (nc > 0) {
         p95 = sp[nc - 1];
