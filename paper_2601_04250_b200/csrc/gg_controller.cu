@@ -1371,24 +1371,32 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
   bool nan_here = false;
   #pragma unroll 1
   for (int j = tid; j < count0; j += kOutThreads) nan_here |= isnan(seq[j]);
+  // one pass over the outcomes: NaN check, and the first chunk's (latency, joules,
+  // depth) staged in smem for the chunk loop (one global round trip instead of two)
   #pragma unroll 1
   for (int64_t e = tid; e < n_tot; e += kOutThreads) {
-    double L;
+    double L, J;
+    int32_t Q;
     if (slots) {
       int gi = 0;
       while (e >= slot_off[gi + 1]) ++gi;
-      L = slots[(int64_t)gi * (3 * B + 8) + (e - slot_off[gi])];
+      const double* sl = slots + (int64_t)gi * (3 * B + 8);
+      const int64_t i = e - slot_off[gi];
+      L = sl[i];
+      J = sl[B + i];
+      Q = (int32_t)sl[2 * B + i];
     } else {
       L = lat[e];
+      J = jou[e];
+      Q = qd[e];
     }
-    nan_here |= isnan(L);
     // a NaN joule makes the EWMA NaN, whose min/max observes are order-dependent in a
     // way the parallel ordered reduction below does not model: sequential kernel
-    nan_here |= isnan(slots ? 0.0 : jou[e]);
-    if (slots) {
-      int gi = 0;
-      while (e >= slot_off[gi + 1]) ++gi;
-      nan_here |= isnan(slots[(int64_t)gi * (3 * B + 8) + B + (e - slot_off[gi])]);
+    nan_here |= isnan(L) || isnan(J);
+    if (e < kOutChunk) {
+      seq[count0 + e] = L;
+      sj[e] = J;
+      sq[e] = Q;
     }
   }
   if (__syncthreads_or(nan_here)) {
@@ -1428,7 +1436,11 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
       const int64_t e = e0 + c;
       double L, J;
       int32_t Q;
-      if (slots) {
+      if (e0 == 0) {   // staged by the NaN pass (h == count0 here)
+        L = seq[h + c];
+        J = sj[c];
+        Q = sq[c];
+      } else if (slots) {
         int gi = 0;
         while (e >= slot_off[gi + 1]) ++gi;
         const double* sl = slots + (int64_t)gi * (3 * B + 8);
