@@ -105,7 +105,16 @@ def jsonl_bytes(request_id, admitted, path, enqueue_t, start_t, finish_t, latenc
     k = min(w * 4, max(1, n // 32768))
     bounds = [n * i // k for i in range(k + 1)]
     chunks = [[c[bounds[i]:bounds[i + 1]] for c in cols] for i in range(k)]
-    with ProcessPoolExecutor(max_workers=w, mp_context=mp.get_context("fork")) as ex:
+    # fork is cheap, but not after this process created a CUDA context (the children
+    # only format text, yet a forked copy of a CUDA process is unsafe): spawn then
+    ctx = "fork"
+    try:
+        import torch
+        if torch.cuda.is_initialized():
+            ctx = "spawn"
+    except ImportError:
+        pass
+    with ProcessPoolExecutor(max_workers=w, mp_context=mp.get_context(ctx)) as ex:
         return "".join(ex.map(_chunk_text, chunks))
 
 
