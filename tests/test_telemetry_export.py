@@ -8,6 +8,7 @@ import os
 from collections import namedtuple
 
 import numpy as np
+import pytest
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
@@ -65,3 +66,16 @@ def test_parallel_chunks_equal_single_process():
     assert par == one
     first = json.dumps(dict(zip(JSONL_FIELDS, [a[1].item() if hasattr(a[1], "item") else a[1] for a in args])))
     assert par.splitlines()[1] == first
+
+
+@pytest.mark.gpu
+def test_parallel_export_after_cuda_init():
+    """In a process that holds a CUDA context the pool spawns instead of forking."""
+    import torch
+    from paper_2601_04250_b200.telemetry import JSONL_FIELDS, jsonl_bytes
+    torch.zeros(1, device="cuda")
+    assert torch.cuda.is_initialized()
+    c = _cols()
+    reps = (140_000 + len(c["path"]) - 1) // len(c["path"])
+    args = [np.concatenate([c[f]] * reps) for f in JSONL_FIELDS]
+    assert jsonl_bytes(*args, workers=2) == jsonl_bytes(*args, workers=1)
