@@ -86,12 +86,15 @@ __global__ void __launch_bounds__(kAttnThreads, 4)
   tc_fence_after();
   float mx = -INFINITY;
 #pragma unroll
-  for (int c = 0; c < kAttnS; c += 32) {
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(trow + c, r);
+  for (int c = 0; c < kAttnS; c += 64) {   // two TMEM loads per wait
+    uint32_t r[2][32];
+    tmem_ld_32x32b_x32(trow + c, r[0]);
+    tmem_ld_32x32b_x32(trow + c + 32, r[1]);
     tmem_ld_wait();
 #pragma unroll
-    for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]) + key_bias[c + i]);
+    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[hh][i]) + key_bias[c + 32 * hh + i]);
   }
   const float mref = (mx == -INFINITY) ? 0.0f : mx;
   const float l2e = 1.4426950408889634f;
