@@ -414,7 +414,7 @@ def forward_energy(srv, net, B, local_rank, seconds: float = 0.5):
     import torch
     from paper_2601_04250_b200.nvml_energy import NvmlEnergyMeter, NvmlUnavailable, energy_report
     try:
-        meter = NvmlEnergyMeter(torch.cuda.current_device() if local_rank is None else local_rank)
+        meter = NvmlEnergyMeter.for_cuda_device(torch.cuda.current_device())
     except NvmlUnavailable:
         return None
     full = torch.full((1,), B, dtype=torch.int32, device=srv.dev)

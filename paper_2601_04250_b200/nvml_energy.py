@@ -33,6 +33,25 @@ class NvmlEnergyMeter:
             raise NvmlUnavailable(f"NVML energy counter unavailable: {exc}") from None
         self._t0: int | None = None
 
+    @classmethod
+    def for_cuda_device(cls, device: int) -> "NvmlEnergyMeter":
+        """The meter of CUDA device `device`, matched by PCI address (CUDA's device
+        order need not be NVML's); falls back to the same index."""
+        m = cls.__new__(cls)
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(device)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            m._nvml = pynvml
+            m._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            pynvml.nvmlDeviceGetTotalEnergyConsumption(m._h)
+            m._t0 = None
+            return m
+        except Exception:
+            return cls(device)
+
     def read_mj(self) -> int:
         return int(self._nvml.nvmlDeviceGetTotalEnergyConsumption(self._h))
 
