@@ -87,8 +87,11 @@ class GatewayBatcher:
 
     def __init__(self, config: ControllerConfig | None, *, ewma_lambda: float = DEFAULT_EWMA_LAMBDA,
                  clock=time.monotonic, max_batch: int = 1024, max_wait_s: float = 200e-6,
-                 device=None, controller=None) -> None:
+                 device=None, controller=None, record_order: bool = False) -> None:
         self.clock = clock
+        # record_order: keep (kind, body) in enqueue order — the total order the
+        # answers are defined by (tests replay it through the sequential gateway)
+        self.order: list | None = [] if record_order else None
         self.queue_depth = 0
         self.max_batch = int(max_batch)
         self.max_wait_s = float(max_wait_s)
@@ -127,6 +130,8 @@ class GatewayBatcher:
                 raise ApiError(503, "gateway closed")
             now = float(ts) if ts is not None else self.clock()
             self._q.append(_Item("decide", fut, tuple(float(s) for s in scores), now, depth))
+            if self.order is not None:
+                self.order.append(("decide", body))
             self._cv.notify()
         return fut
 
@@ -142,6 +147,8 @@ class GatewayBatcher:
             if self._closed:
                 raise ApiError(503, "gateway closed")
             self._q.append(_Item("outcome", fut, depth=depth, latency_ms=latency, joules=joules))
+            if self.order is not None:
+                self.order.append(("outcome", body))
             self._cv.notify()
         return fut
 

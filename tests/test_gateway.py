@@ -223,3 +223,36 @@ def test_batcher_device_controller_vs_sequential_oracle():
             assert g[key] == w[key]
         for key in ("j", "tau", "l", "e", "c"):
             assert _ulp(g[key], w[key]) <= 4 or (math.isnan(g[key]) and math.isnan(w[key])), key
+
+
+def test_batcher_concurrent_clients_cpu():
+    """8 client threads hammer decide/outcome concurrently: every answer equals the
+    sequential gateway's answer for the enqueue order the batcher recorded, and the
+    final controller state matches."""
+    import threading
+    from paper_2601_04250_b200.gateway import GatewayBatcher
+    reqs = _requests(seed=23, n=800)
+    per = [reqs[i::8] for i in range(8)]
+    fake = OracleBackedController()
+    answers = {}
+    with GatewayBatcher(None, controller=fake, max_wait_s=50e-6, clock=lambda: 0.0,
+                        record_order=True) as gw:
+        def client(part):
+            for kind, b in part:
+                try:
+                    r = gw.decide(b) if kind == "decide" else gw.outcome(b)
+                except Exception as exc:
+                    r = getattr(exc, "status", exc)
+                answers[b["id"]] = r
+        ts = [threading.Thread(target=client, args=(p,)) for p in per]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        order = list(gw.order)
+    assert len(order) == len(reqs)
+    want, octl = sequential_gateway(order)
+    for (kind, b), w in zip(order, want):
+        assert answers[b["id"]] == w, (kind, b["id"])
+    assert fake.o.state_tuple() == octl.state_tuple()
+    assert len(fake.calls) < len(reqs)   # requests were coalesced
