@@ -187,6 +187,16 @@ class GatewayBatcher:
     def __exit__(self, *exc):
         self.close()
 
+    def _pinned(self, name: str, nbytes: int):
+        """A reused pinned host buffer of >= nbytes (grown by doubling)."""
+        import torch
+        bufs = self.__dict__.setdefault("_pin", {})
+        b = bufs.get(name)
+        if b is None or b.numel() < nbytes:
+            b = bufs[name] = torch.empty(max(nbytes, 2 * (b.numel() if b is not None else 0), 4096),
+                                         dtype=torch.uint8).pin_memory()
+        return b
+
     # ----------------------------------------------------------------- worker
     def _run(self) -> None:
         while True:
@@ -241,14 +251,35 @@ class GatewayBatcher:
             for it in run:
                 it.fut.set_exception(ApiError(400, f"need at least 2 class scores, got {k}"))
             return
-        scores = _to_device(torch.tensor([it.scores for it in run], dtype=torch.float64), ctl.device)
-        now = _to_device(torch.tensor([it.now for it in run], dtype=torch.float64), ctl.device)
+        n = len(run)
+        dev = torch.device(ctl.device)
+        if dev.type == "cuda":
+            # reused pinned staging: [scores n x k | now n] up, [codes | breakdown | info] down
+            hin = self._pinned("in", n * (k + 1) * 8).view(torch.float64)
+            hin[: n * k].view(n, k).copy_(torch.tensor([it.scores for it in run], dtype=torch.float64))
+            hin[n * k: n * (k + 1)].copy_(torch.tensor([it.now for it in run], dtype=torch.float64))
+            din = hin[: n * (k + 1)].to(dev, non_blocking=True)
+            scores, now = din[: n * k].view(n, k), din[n * k:]
+        else:
+            scores = torch.tensor([it.scores for it in run], dtype=torch.float64)
+            now = torch.tensor([it.now for it in run], dtype=torch.float64)
         snap = CongestionSnapshot(queue_depth=depth, p95_latency_ms=ctl.p95_ms(), batch_fill=0.0)
         out = ctl.decide_batch(scores, now, snap, breakdown=True)
         self.launches["decide"] += 1
-        codes = out.decision.cpu().tolist()
-        bd = out.breakdown.cpu().tolist()
-        info = _abi.gg_batch_info.from_buffer_copy(bytes(out.info.cpu().numpy().tobytes()))
+        if dev.type == "cuda":
+            hb = self._pinned("bd", n * 24).view(torch.float64)[: n * 3].view(n, 3)
+            hc = self._pinned("dec", n)[:n]
+            hi = self._pinned("info", _abi.BATCH_INFO_BYTES)[: _abi.BATCH_INFO_BYTES]
+            hb.copy_(out.breakdown, non_blocking=True)
+            hc.copy_(out.decision, non_blocking=True)
+            hi.copy_(out.info, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            codes, bd = hc.tolist(), hb.tolist()
+            info = _abi.gg_batch_info.from_buffer_copy(bytes(hi.numpy().tobytes()))
+        else:
+            codes = out.decision.tolist()
+            bd = out.breakdown.tolist()
+            info = _abi.gg_batch_info.from_buffer_copy(bytes(out.info.numpy().tobytes()))
         geq = ctl.direction is Direction.GEQ
         for it, code, (u, jv, tau) in zip(run, codes, bd):
             if code == _abi.GG_DECISION_INVALID:
