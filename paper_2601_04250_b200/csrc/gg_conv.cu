@@ -58,8 +58,11 @@ struct ConvSmem {
   static constexpr int A_BYTES = 128 * 128;
   static constexpr int B_BYTES = BN * 128;
   // DS: a second weight slab per stage (the downsample's, used at the centre tap)
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES * (DS ? 2 : 1);
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  // DS: the downsample's weight slabs (used by the centre-tap k-blocks only) have
+  // their own 2-slot ring after the stages, so every stage stays A + B
+  static constexpr int DS_SLOTS = DS ? 2 : 0;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES + DS_SLOTS * B_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
@@ -102,13 +105,16 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
   const int num_kb = sh.Kpad / 64;
   const int nst = sh.bres ? sh.bres_stages : STAGES;
   uint8_t* bres = smem + nst * L::STAGE_BYTES;
-  const int bar_off = nst * L::STAGE_BYTES + (sh.bres ? num_kb * L::B_BYTES : 0);
+  uint8_t* ds_ring = smem + STAGES * L::STAGE_BYTES;   // DS weight slots (never with bres)
+  const int bar_off = sh.bres ? nst * L::STAGE_BYTES + num_kb * L::B_BYTES : L::BAR_OFF;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + bar_off);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* b_full = acc_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + 1);
+  uint64_t* ds_full = b_full + 1;
+  uint64_t* ds_empty = ds_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ds_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   griddep_launch();   // the successor may begin its prologue as SMs free up
@@ -126,6 +132,8 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], conv_epi_warps(DS));
+      mbar_init(&ds_full[a], 1);
+      mbar_init(&ds_empty[a], 1);
     }
     fence_mbar_init();
     tma_prefetch(&map_w);
@@ -151,8 +159,8 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
       // lean like the issuer: stage / phase and (tap, channel block) advance incrementally
       const int cblocks = sh.C / 64;
       const int ctap = (sh.R * sh.S) / 2;
-      int s = 0;
-      uint32_t ph = 0;
+      int s = 0, dsl = 0;
+      uint32_t ph = 0, dph = 0;
       SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
       SkWork w;
       while (sc.next(w)) {
@@ -170,9 +178,7 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
           mbar_wait_sleep(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
           {
-            uint32_t bytes = sh.bres ? L::A_BYTES : L::A_BYTES + L::B_BYTES;
-            if constexpr (DS)
-              if (tap == ctap) bytes += L::B_BYTES;
+            const uint32_t bytes = sh.bres ? L::A_BYTES : L::A_BYTES + L::B_BYTES;
             mbar_expect_tx(&full[s], bytes);
           }
           constexpr int kLoads = MODE == 1 ? 1 : 4;
@@ -193,8 +199,15 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
           }
           if (!sh.bres) tma_load_2d(sa + L::A_BYTES, &map_w, &full[s], kb * 64, tn * BN);
           if constexpr (DS) {   // centre tap: the downsample's weights for this channel block
-            if (tap == ctap)
-              tma_load_2d(sa + L::A_BYTES + L::B_BYTES, &map_wds, &full[s], cb * 64, tn * BN);
+            if (tap == ctap) {
+              mbar_wait_sleep(&ds_empty[dsl], dph ^ 1);
+              mbar_expect_tx(&ds_full[dsl], L::B_BYTES);
+              tma_load_2d(ds_ring + dsl * L::B_BYTES, &map_wds, &ds_full[dsl], cb * 64, tn * BN);
+              if (++dsl == 2) {
+                dsl = 0;
+                dph ^= 1;
+              }
+            }
           }
           if (MODE == 1 && ++cb == cblocks) {   // next (tap, channel block)
             cb = 0;
@@ -271,13 +284,14 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
       // operand descriptors are base + constant offsets (the 14-bit start-address
       // field never carries: smem < 256 KB), the centre-tap range is precomputed.
       constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
-      int t = 0, s = 0;
-      uint32_t ph = 0;
+      int t = 0, s = 0, dsl = 0;
+      uint32_t ph = 0, dph = 0;
       if (b_loaded) mbar_wait(b_full, 0);   // also when the count leaves no tile: drain
       SkSched sc(ep.sk.enabled, num_tiles, num_kb, blockIdx.x, gridDim.x);
       SkWork w;
       const uint64_t a_desc0 = MODE == 2 ? sdesc_k_sw32(smem_u32(smem)) : sdesc_k_sw128(smem_u32(smem));
       const uint64_t b_desc0 = sdesc_k_sw128(smem_u32(sh.bres ? bres : smem + L::A_BYTES));
+      const uint64_t ds_desc0 = sdesc_k_sw128(smem_u32(ds_ring));
       constexpr uint64_t kStageD = (uint64_t)(L::STAGE_BYTES >> 4), kBD = (uint64_t)(L::B_BYTES >> 4);
       const int cbl = sh.C / 64;
       const int kb_c0 = ((sh.R * sh.S) / 2) * cbl, kb_c1 = kb_c0 + cbl;   // DS: centre-tap k-blocks
@@ -292,23 +306,33 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
           tc_fence_after();
           const uint64_t ad = a_desc0 + (uint64_t)s * kStageD;
           const uint64_t bd = sh.bres ? b_desc0 + (uint64_t)kb * kBD : b_desc0 + (uint64_t)s * kStageD;
+          const bool ctr = DS && kb >= kb_c0 && kb < kb_c1;   // centre tap: downsample MMAs too
+          if (ctr) {
+            mbar_wait(&ds_full[dsl], dph);
+            tc_fence_after();
+          }
           if (elect_one_sync()) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
               umma_bf16(d_tmem, ad + (uint64_t)(MODE == 2 ? kk * 256 : kk * 2), bd + (uint64_t)(kk * 2), idesc,
                         (kb != w.kb0 || kk != 0));
             if constexpr (DS) {
-              if (kb >= kb_c0 && kb < kb_c1) {   // downsample accumulator: K = Cin (centre tap only)
-                const uint64_t dd = b_desc0 + (uint64_t)s * kStageD + kBD;
+              if (ctr) {   // downsample accumulator: K = Cin (centre tap only)
+                const uint64_t dd = ds_desc0 + (uint64_t)dsl * kBD;
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
                   umma_bf16(d_tmem + BN, ad + (uint64_t)(kk * 2), dd + (uint64_t)(kk * 2), idesc,
                             kb != kb_c0 || kk != 0);
+                umma_commit(&ds_empty[dsl]);
               }
             }
             umma_commit(&empty[s]);
           }
           __syncwarp();
+          if (ctr && ++dsl == 2) {
+            dsl = 0;
+            dph ^= 1;
+          }
           if (++s == nst) {
             s = 0;
             ph ^= 1;
@@ -773,7 +797,7 @@ extern "C" int gg_conv2d_ds(const void* x, int32_t N, int32_t H, int32_t W, int3
   if (!rc) rc = make_map_2d(&mwds, w_ds, Cout, C, C, BN);
   if (!rc) rc = make_map_im2col(&mx, x, sh, 64);
   if (rc) return rc;
-  return launch_conv<BN, 4, 1, true>(reinterpret_cast<const __nv_bfloat16*>(x), mw, mx, sh, ep,
+  return launch_conv<BN, 6, 1, true>(reinterpret_cast<const __nv_bfloat16*>(x), mw, mx, sh, ep,
                                      gg_stream(stream), &mwds);
 }
 
