@@ -22,7 +22,7 @@ exchange for N > 1), K2 feedback.  Captured once as a CUDA graph and replayed.
           algorithmic FLOPs / CUDA-event time of a full batch, vs the measured
           sustained bf16 peak (MEASURED_PEAKS.json); traffic = the DRAM bytes of
           one full-batch forward from the committed ncu launch list
-          (profiles/r1f_forward_traffic.json).
+          (profiles/r1g_forward_traffic.json).
   cpu_baseline / --impl reference
           the reference's CPU path: the controller port (oracle/, the
           reference's algorithm in CPython) deciding the same windows, plus a
@@ -394,7 +394,7 @@ def roofline_forward(srv, net, B):
                  "attention + 12 LayerNorm + embedding-LN")
     traffic, traffic_src = None, None
     try:   # committed ncu evidence: DRAM bytes of one full-batch forward (tools/profile_round.sh)
-        with open(os.path.join(ROOT, "profiles", "r1f_forward_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1g_forward_traffic.json")) as f:
             t = json.load(f)[srv.kind]
         traffic, traffic_src = int(t["dram_bytes_per_forward"]), t["source"]
     except Exception:
