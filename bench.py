@@ -1,33 +1,52 @@
 #!/usr/bin/env python
-"""Benchmark of the gated-inference hot path (driver contract; see DESIGN.md §Measurement).
+"""Benchmark of the gated-inference hot path (driver contract; see DESIGN.md §6).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload resnet18|distilbert]
+                    [--workload distilbert|resnet18] [--no-extras]
 
 Metric (BASELINE.json): admitted inferences/sec — requests that passed the
-admission controller AND completed a forward pass, per second, whole job.
+admission controller AND completed a forward pass, per second, whole job; and
+the trace wall time of the bio-controller vs the open-loop arm (`ablation`).
 
-One step = one closed-loop serving step (serving.GatedServer): K1 admission
-of `window` new arrivals against the device FIFO's congestion snapshot, pop
-up to B admitted requests, gather their payloads, forward (ResNet-18 224x224,
-B = 64 | DistilBERT seq 128, B = 128), K3 epilogue, outcome record, (K9
-exchange for N > 1), K2 feedback.  Captured once as a CUDA graph and replayed.
+Headline workload (default, BASELINE configs[2] driven by configs[4]'s
+K = 2 ablation request model): DistilBERT seq 128, forward batch B = 128,
+224 Poisson arrivals per step with ablation-style scores (confidence
+U(0.85, 0.97), presets.py:88-95); tau(t) decays 0.4 -> 0.2 (k = 5 /s) inside
+the timed region, and the congestion term (gamma = -0.3 on queue depth, p95 of
+trace-time latencies, batch fill) regulates admission to the forward's
+capacity: a closed loop, not static thresholding.  `resnet18` key: the same
+loop for ResNet-18 224x224, B = 64, K = 1000 (configs[1]).
 
-  value   device-resident trace + payload pool, graph replays, CUDA events,
-          max over ranks.
-  e2e     same loop through the public API with host buffers: every step
-          copies the window's scores/now and payload images from pinned host
-          memory and reads back the served batch's predictions.
-  roofline  the forward pass (the dominant kernel family: ~90 % of a step),
-          algorithmic FLOPs / CUDA-event time of a full batch, vs the measured
-          sustained bf16 peak (MEASURED_PEAKS.json); traffic = the DRAM bytes of
-          one full-batch forward from the committed ncu launch list
-          (profiles/r1g_forward_traffic.json).
+One step = one closed-loop serving step (serving.GatedServer): K1 admission of
+the window against the device FIFO's congestion snapshot, fallback answers for
+the skipped rows, Path-B pop (full batch or 10 ms window, servesim.py:148-162),
+payload gather, forward, K3 epilogue, outcome record (trace-time latency),
+(K9 exchange for N > 1), K2 feedback.  Captured once as a CUDA graph.
+
+  value     device-resident trace + payload pool, graph replays, CUDA events on
+            the serving stream, max over ranks; inputs (> 126 MB L2 working set
+            per forward) are not re-flushed.
+  e2e       same loop through the public API with host buffers: every step
+            copies the window's scores/now and payloads from pinned host memory
+            and reads back the served batch's predictions and the decisions.
+  roofline  the forward pass (the dominant kernel family), algorithmic FLOPs /
+            CUDA-event time of a full batch, vs the measured bf16 peak
+            (MEASURED_PEAKS.json; burst: the forward is timed alone, 20 reps);
+            traffic = DRAM bytes of one full-batch forward from the committed
+            ncu launch list.
+  ablation  C4: ONOFF 800/50 rps, 25 s, 10,147 arrivals,
+            each tagged DistilBERT or ResNet-18 by a seeded coin; open-loop arm
+            (admit all, servesim.py:231-240) vs bio-controller on the identical
+            trace; device wall time to serve the trace, plus the reference's
+            SummaryRow / compare_ablation figures (trace makespan, latency,
+            accuracy with fallback answers, admission rate).
   cpu_baseline / --impl reference
-          the reference's CPU path: the controller port (oracle/, the
-          reference's algorithm in CPython) deciding the same windows, plus a
-          torch-eager fp32 CPU forward of the admitted requests as the stand-in
-          for the inference the reference only simulates, on all host cores.
+            the reference's CPU path: the UNMODIFIED reference AdmissionController
+            (baseline/_ref, tools/install_reference.sh) deciding the same windows
+            and recording the outcomes, plus a torch-eager fp32 CPU forward of the
+            admitted requests (stand-in for the inference the reference only
+            simulates), all host cores.  Falls back to the oracle port when the
+            reference is not installed (kind "port").
 """
 
 from __future__ import annotations
@@ -35,6 +54,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -45,18 +65,23 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # BASELINE.json configs[1]: ResNet-18 224x224 gated inference, batch 64
-    "resnet18": dict(batch=64, window=112, k=1000, conf_lo=0.3, conf_hi=0.9, pool=2048,
-                     ctl=dict(alpha=1.0, beta=-0.1, gamma=-0.3, tau0=0.35, tau_inf=0.35, k=1.0),
-                     outcome=dict(batch_base_ms=4.0, per_item_ms=0.05, batch_base_energy_j=6.0,
-                                  per_item_energy_j=1.5)),
-    # BASELINE.json configs[2]: DistilBERT seq 128 gated inference, batch 128, bf16
-    "distilbert": dict(batch=128, window=224, k=2, conf_lo=0.85, conf_hi=0.97, pool=4096,
-                       ctl=dict(alpha=1.0, beta=-0.1, gamma=-0.3, tau0=0.39796077431433013,
-                                tau_inf=0.39796077431433013, k=1.0),
+    # BASELINE.json configs[2]: DistilBERT seq 128 gated inference, batch 128, bf16;
+    # request model of configs[4] / ablation_reference (K = 2, confidence U(0.85, 0.97))
+    "distilbert": dict(batch=128, window=224, k=2, conf_lo=0.85, conf_hi=0.97, rate=20000.0,
+                       pool=4096,
+                       ctl=dict(alpha=1.0, beta=-0.1, gamma=-0.3, tau0=0.4, tau_inf=0.2, k=5.0),
                        outcome=dict(batch_base_ms=4.0, per_item_ms=0.02, batch_base_energy_j=6.0,
-                                    per_item_energy_j=1.0)),
+                                    per_item_energy_j=1.0),
+                       batching_window_ms=10.0, fallback_degradation=0.013),
+    # BASELINE.json configs[1]: ResNet-18 224x224 gated inference, batch 64
+    "resnet18": dict(batch=64, window=112, k=1000, conf_lo=0.3, conf_hi=0.9, rate=10000.0,
+                     pool=2048,
+                     ctl=dict(alpha=1.0, beta=-0.1, gamma=-0.3, tau0=0.35, tau_inf=0.2, k=5.0),
+                     outcome=dict(batch_base_ms=4.0, per_item_ms=0.05, batch_base_energy_j=6.0,
+                                  per_item_energy_j=1.5),
+                     batching_window_ms=10.0, fallback_degradation=0.05),
 }
+METRIC = "admitted inferences/sec"
 
 
 def peaks() -> dict:
@@ -130,14 +155,18 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- setup
 def make_trace(wl: dict, n: int, seed: int):
+    """Poisson arrivals at wl['rate'] with the workload's score model, in the
+    reference's draw order (workload.py).  Returns scores, arrival times, labels."""
     import numpy as np
     import paper_2601_04250_b200 as gg
-    cfg = gg.WorkloadConfig(mode=gg.ArrivalMode.POISSON, rate_rps=20000.0, num_classes=wl["k"],
-                            confidence_low=wl["conf_lo"], confidence_high=wl["conf_hi"])
-    horizon = 1.5 * n / 20000.0 + 1.0
+    cfg = gg.WorkloadConfig(mode=gg.ArrivalMode.POISSON, rate_rps=wl["rate"], num_classes=wl["k"],
+                            confidence_low=wl["conf_lo"], confidence_high=wl["conf_hi"],
+                            fallback_degradation=wl["fallback_degradation"])
+    horizon = 1.3 * n / wl["rate"] + 1.0
     tr = gg.generate_trace(cfg, horizon, np.random.default_rng(seed))
     assert len(tr) >= n, (len(tr), n)
-    return tr.scores[:n].copy(), tr.arrival_t[:n].copy()
+    return (tr.scores[:n].copy(), tr.arrival_t[:n].copy(),
+            tr.true_label[:n].astype(np.int32).copy())
 
 
 def build_net(name: str, B: int):
@@ -148,31 +177,47 @@ def build_net(name: str, B: int):
     return DistilBertB200(random_model(0), max_batch=B)
 
 
-# ----------------------------------------------------------------------------- our arm
-def run_ours(args, wl, rank, world, local_rank, pg):
-    import numpy as np
+def make_server(wl, kind, net, scores, now, labels, payloads, dev, *, rank=0, world=1, pg=None,
+                open_loop=False, coin_seed=0):
     import torch
     import paper_2601_04250_b200 as gg
-    from paper_2601_04250_b200 import _native, serving
+    from paper_2601_04250_b200 import serving
+    ctl = gg.ControllerConfig(**wl["ctl"], routing=gg.RoutePolicy.ALL_BATCHED).build(
+        gg.EnergyLedger(), device=dev)
+    T = int(scores.shape[0])
+    coins = torch.from_numpy(serving.fallback_coins(coin_seed, T)).to(dev)
+    return serving.GatedServer(
+        ctl, net, scores, now, payloads, window=wl["window"],
+        outcome=serving.OutcomeModel(**wl["outcome"], latency="trace"), rank=rank, world=world,
+        process_group=pg, open_loop=open_loop, batching_window_ms=wl["batching_window_ms"],
+        labels=labels, coins=coins, fallback_degradation=wl["fallback_degradation"])
 
+
+def payload_pool(kind, n, seed, dev):
+    from paper_2601_04250_b200 import serving
+    if kind == "resnet18":
+        return serving.synthetic_images(n, seed=seed, device=dev)
+    return serving.synthetic_tokens(n, seed=seed, device=dev)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, kind, rank, world, local_rank, pg, with_clocks=True):
+    import torch
+    from paper_2601_04250_b200 import _native
+    wl = WORKLOADS[kind]
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     B, W = wl["batch"], wl["window"]
     e2e_steps = args.steps
     n_rows = (args.warmup + 2 + args.steps + args.warmup + e2e_steps + 4) * W
-    scores_np, now_np = make_trace(wl, n_rows, seed=1000 + rank)
-    net = build_net(args.workload, B)
-    ctl = gg.ControllerConfig(**wl["ctl"], routing=gg.RoutePolicy.ALL_BATCHED).build(
-        gg.EnergyLedger(), device=dev)
-    if args.workload == "resnet18":
-        payloads = serving.synthetic_images(wl["pool"], seed=rank, device=dev)
-    else:
-        payloads = serving.synthetic_tokens(wl["pool"], seed=rank, device=dev)
+    scores_np, now_np, labels_np = make_trace(wl, n_rows, seed=1000 + rank)
+    net = build_net(kind, B)
+    payloads = payload_pool(kind, wl["pool"], rank, dev)
     scores = torch.from_numpy(scores_np).to(dev)
     now = torch.from_numpy(now_np).to(dev)
-    srv = serving.GatedServer(ctl, net, scores, now, payloads, window=W,
-                              outcome=serving.OutcomeModel(**wl["outcome"]), rank=rank,
-                              world=world, process_group=pg)
+    labels = torch.from_numpy(labels_np).to(dev)
+    srv = make_server(wl, kind, net, scores, now, labels, payloads, dev, rank=rank, world=world,
+                      pg=pg, coin_seed=1000 + rank)
     # warm-up: one eager step (allocations, tensor-map encodes), capture, W graph steps
     srv.run(1)
     torch.cuda.synchronize()
@@ -187,8 +232,10 @@ def run_ours(args, wl, rank, world, local_rank, pg):
             torch.distributed.barrier()
 
     f0 = srv.fifo_state()
+    st0 = srv.ctl.state_struct()
     clocks = ClockSampler(local_rank)
-    clocks.start()
+    if with_clocks:
+        clocks.start()
     barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -197,20 +244,27 @@ def run_ours(args, wl, rank, world, local_rank, pg):
     end.record(srv.stream)
     torch.cuda.synchronize()
     barrier()
-    clk = clocks.stop()
+    clk = clocks.stop() if with_clocks else None
     ms = start.elapsed_time(end)
     f1 = srv.fifo_state()
+    st1 = srv.ctl.state_struct()
     served = f1.head - f0.head
     decided = f1.cursor - f0.cursor
     admitted = f1.tail - f0.tail
+    tau = _tau_range(wl["ctl"], now_np, f0.cursor, f1.cursor, st0.t_origin)
+    loop = {"admission_rate": round(admitted / max(1, decided), 4),
+            "mean_forward_batch": round(served / args.steps, 2),
+            "queue_depth_end": int(f1.tail - f1.head), "fifo_overflow": int(f1.overflow),
+            "tau_timed_region": tau,
+            "p95_ms": [round(st0.p95_current, 3), round(st1.p95_current, 3)],
+            "trace_clock_s": [round(f0.clock, 4), round(f1.clock, 4)]}
 
     # ---- e2e through the public API with host buffers -----------------------
-    e2e = run_e2e(srv, scores_np, now_np, payloads, wl, e2e_steps, args.warmup)
+    e2e = run_e2e(srv, scores_np, now_np, payloads, e2e_steps, args.warmup)
 
     # ---- roofline of the forward (full batch, CUDA events on the launch stream)
     ro = roofline_forward(srv, net, B)
-    energy = forward_energy(srv, net, B, local_rank)
-    k1 = admission_kernel_roofline(dev) if rank == 0 else None
+    energy = forward_energy(srv, net, B) if not args.no_extras else None
 
     tot = torch.tensor([ms, float(served), float(decided), float(admitted), e2e["ms"],
                         float(e2e["served"])], dtype=torch.float64, device=dev)
@@ -221,20 +275,27 @@ def run_ours(args, wl, rank, world, local_rank, pg):
         ms_max, e2e_ms_max = mx[0].item(), mx[4].item()
     else:
         ms_max, e2e_ms_max = ms, e2e["ms"]
-    served_all, decided_all, admitted_all = tot[1].item(), tot[2].item(), tot[3].item()
-    e2e_served_all = tot[5].item()
-    res = srv.results()
-    return dict(ms=ms_max, served=served_all, decided=decided_all, admitted=admitted_all,
-                e2e_ms=e2e_ms_max, e2e_served=e2e_served_all, e2e=e2e, roofline=ro, clocks=clk, k1=k1,
-                energy=energy,
-                launches_per_step=launches_per_step, overflow=res["overflow"],
-                queue_depth=res["queue_depth"])
+    res = dict(ms=ms_max, served=tot[1].item(), decided=tot[2].item(), admitted=tot[3].item(),
+               e2e_ms=e2e_ms_max, e2e_served=tot[5].item(), e2e=e2e, roofline=ro, clocks=clk,
+               energy=energy, launches_per_step=launches_per_step, loop=loop)
+    del srv, net, payloads
+    torch.cuda.empty_cache()
+    return res
 
 
-def run_e2e(srv, scores_np, now_np, payloads, wl, steps, warmup):
+def _tau_range(ctl, now_np, c0, c1, t_origin):
+    import math
+    t0, t1 = float(now_np[c0]), float(now_np[max(c0, c1 - 1)])
+
+    def tau(t):
+        return ctl["tau_inf"] + (ctl["tau0"] - ctl["tau_inf"]) * math.exp(-ctl["k"] * max(0.0, t - t_origin))
+    return [round(tau(t0), 4), round(tau(t1), 4)]
+
+
+def run_e2e(srv, scores_np, now_np, payloads, steps, warmup):
     """Public-API loop with host buffers, pipelined like a serving front end: the
-    window of step i+1 (scores, arrival times, payload images: pinned host ->
-    device on a copy stream) uploads while step i computes; every step's served
+    window of step i+1 (scores, arrival times, payloads: pinned host -> device on
+    a copy stream) uploads while step i computes; every step's served
     predictions/confidences and the window's decisions come back device -> host
     and the host waits for them one step behind.  All copies are inside the
     timed region (CUDA events)."""
@@ -349,7 +410,7 @@ def admission_kernel_roofline(dev, n_rows: int = 1 << 26, k: int = 2, reps: int 
     nbytes = n_rows * (8 * k + 8 + 1) + 4 * n_adm
     gbs = nbytes / (ms * 1e-3) / 1e9
     pk = peaks()
-    res = {"kernel": "admit_small_kernel<2> (K1: validate + entropy + J/tau + ballot compaction)",
+    res = {"kernel": "K1 gg_admit (validate + entropy + J/tau + ballot compaction), K=2",
            "rows": n_rows, "k": k, "ms_per_launch": round(ms, 4),
            "decisions_per_s": round(n_rows / (ms * 1e-3), 1), "bound": "hbm",
            "achieved": round(gbs, 1), "peak": pk["hbm"], "unit": "GB/s",
@@ -357,6 +418,55 @@ def admission_kernel_roofline(dev, n_rows: int = 1 << 26, k: int = 2, reps: int 
     del scores, now, out
     torch.cuda.empty_cache()
     return res
+
+
+def exchange_cost(dev, B: int = 128, reps: int = 50) -> dict:
+    """K2 of a G-rank step emulated on one GPU: gg_outcome_slots
+    replays G*B outcomes (every rank's full batch, rank order) through the
+    sequential EWMA / p95 chain that keeps the replicas identical.  µs per step
+    for G = 1, 2, 4, 8 (the all_reduce itself is NCCL's and not timed here)."""
+    import ctypes as C
+    import torch
+    import paper_2601_04250_b200 as gg
+    from paper_2601_04250_b200 import _abi, _native
+    lib = _native.load()
+    out = {}
+    for G in (1, 2, 4, 8):
+        ctl = gg.ControllerConfig(alpha=1.0, beta=-0.1, gamma=-0.3, tau0=0.4, tau_inf=0.2,
+                                  k=5.0).build(gg.EnergyLedger(), device=dev)
+        L = 3 * B + 8
+        slots = torch.zeros(G * L, dtype=torch.float64, device=dev)
+        g = torch.Generator(device=dev).manual_seed(G)
+        for r in range(G):
+            sl = slots[r * L:(r + 1) * L]
+            sl[:B] = 5.0 + 20.0 * torch.rand(B, generator=g, device=dev, dtype=torch.float64)
+            sl[B:2 * B] = 1.0 + torch.rand(B, generator=g, device=dev, dtype=torch.float64)
+            sl[2 * B:3 * B] = float(r + 3)
+            sl[3 * B] = float(B)
+            sl[3 * B + 1] = 4.0
+            sl[3 * B + 2:3 * B + 8] = torch.tensor([224.0, 0.0, 128.0, 96.0, 4.0, 12.0],
+                                                   dtype=torch.float64)
+        fifo = torch.zeros(C.sizeof(_abi.gg_fifo), dtype=torch.uint8, device=dev)
+        err = torch.empty(1, dtype=torch.int64, device=dev)
+        s = torch.cuda.current_stream(dev)
+        st = _native.stream_ptr(s)
+
+        def call():
+            _native.check("gg_outcome_slots", lib.gg_outcome_slots(
+                C.byref(ctl.params), _native.ptr(ctl.state), _native.ptr(slots), G, B,
+                0, _native.ptr(fifo), _native.ptr(err), st))
+        for _ in range(5):
+            call()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(reps):
+            call()
+        b.record(s)
+        torch.cuda.synchronize()
+        out[f"G{G}"] = round(1e3 * a.elapsed_time(b) / reps, 2)
+    return {"kernel": "gg_outcome_slots (K2 over G x B outcomes in rank order)", "B": B,
+            "us_per_step": out}
 
 
 def roofline_forward(srv, net, B):
@@ -387,30 +497,35 @@ def roofline_forward(srv, net, B):
     pk = peaks()
     achieved = flops / (ms * 1e-3) / 1e12
     kern = ("ResNet-18 forward: fused stem conv + max pool + 4 span convs (layer 1) + 9 CTA-pair "
-            "span convs (layers 2-4) + 3 fused stride-2 conv/downsample (TMA im2col) + avg pool + "
-            "fc, all tcgen05, shared-border NHWC layout"
+            "span convs (layers 2-4) + 3 fused stride-2 conv/downsample (TMA im2col) + fused "
+            "avg pool/fc (fp32), all convs tcgen05, shared-border NHWC layout"
             if srv.kind == "resnet18"
-            else "DistilBERT forward: 24 CTA-pair tcgen05 GEMMs + 2 single-CTA GEMMs + 6 tcgen05 "
-                 "attention + 12 LayerNorm + embedding-LN")
+            else "DistilBERT forward: CTA-pair tcgen05 GEMMs (QKV, out-proj, FFN) with fused "
+                 "bias/GELU/residual epilogues, tcgen05 attention, LayerNorm, embedding-LN, "
+                 "classifier head")
     traffic, traffic_src = None, None
-    try:   # committed ncu evidence: DRAM bytes of one full-batch forward (tools/profile_round.sh)
-        with open(os.path.join(ROOT, "profiles", "r1g_forward_traffic.json")) as f:
-            t = json.load(f)[srv.kind]
-        traffic, traffic_src = int(t["dram_bytes_per_forward"]), t["source"]
-    except Exception:
-        pass
-    return {"bound": "tensor", "achieved": round(achieved, 2), "peak": pk["bf16_sustained"],
-            "unit": "TFLOP/s", "frac": round(achieved / pk["bf16_sustained"], 4),
+    for name in ("r2_forward_traffic.json", "r1g_forward_traffic.json"):
+        try:   # committed ncu evidence: DRAM bytes of one full-batch forward
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                t = json.load(f)[srv.kind]
+            traffic, traffic_src = int(t["dram_bytes_per_forward"]), t["source"]
+            break
+        except Exception:
+            continue
+    return {"bound": "tensor", "achieved": round(achieved, 2), "peak": pk["bf16"],
+            "unit": "TFLOP/s", "frac": round(achieved / pk["bf16"], 4),
+            "frac_of_sustained": round(achieved / pk["bf16_sustained"], 4),
             "traffic": traffic, "traffic_unit": "bytes per forward (DRAM read + write)",
             "traffic_source": traffic_src, "kernel": kern, "flops_per_launch": flops,
-            "ms_per_launch": round(ms, 4), "peak_source": pk["source"] + " bf16_tflops_sustained"}
+            "ms_per_launch": round(ms, 4),
+            "peak_source": pk["source"] + " bf16_tflops (burst: the forward is timed alone, "
+                                          f"{reps} back-to-back reps)"}
 
 
-def forward_energy(srv, net, B, local_rank, seconds: float = 0.5):
+def forward_energy(srv, net, B, seconds: float = 0.5):
     """Measured energy (NVML total-energy counter, this GPU) of full-batch forwards
     replayed back to back for >= `seconds` — joules per inference of the dominant
     kernel family (telemetry).  None without NVML."""
-    import time
     import torch
     from paper_2601_04250_b200.nvml_energy import NvmlEnergyMeter, NvmlUnavailable, energy_report
     try:
@@ -419,19 +534,19 @@ def forward_energy(srv, net, B, local_rank, seconds: float = 0.5):
         return None
     full = torch.full((1,), B, dtype=torch.int32, device=srv.dev)
     s = srv.stream
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(s):
+
+    def fwd():
         if srv.kind == "resnet18":
             net.forward_s2d(B, stream=s, count=full)
         else:
             net.forward(srv.tok_ids, srv.tok_mask, batch=B, stream=s, count=full)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        fwd()
     torch.cuda.synchronize()
     with torch.cuda.graph(g, stream=s):
         for _ in range(10):
-            if srv.kind == "resnet18":
-                net.forward_s2d(B, stream=s, count=full)
-            else:
-                net.forward(srv.tok_ids, srv.tok_mask, batch=B, stream=s, count=full)
+            fwd()
     n = 0
     torch.cuda.synchronize()
     meter.start()
@@ -454,20 +569,139 @@ def forward_energy(srv, net, B, local_rank, seconds: float = 0.5):
     return r
 
 
-# ----------------------------------------------------------------------------- reference arm
-def cpu_reference(wl: dict, workload: str, steps: int, warmup: int, sample_steps: int | None = None):
-    """Reference CPU path: the controller port in CPython (oracle/controller_oracle.py,
-    the reference's algorithm) deciding each window + a torch-eager fp32 CPU forward
-    of the admitted requests (stand-in: the reference only simulates inference)."""
+# ----------------------------------------------------------------------------- ablation (C4)
+def c4_trace():
+    """ONOFF on = 800 / off = 50 rps, phase 0.5 s, 25 s horizon
+    through the simulator's workload stream (SimConfig(seed=11): SeedSequence(11)
+    child 0) -> 10,147 arrivals with K = 2 ablation-style scores; a seeded coin
+    tags each request DistilBERT or ResNet-18; the ResNet requests get K = 1000
+    scores (confidence U(0.3, 0.9)) from their own stream."""
     import numpy as np
+    import paper_2601_04250_b200 as gg
+    cfg = gg.WorkloadConfig(mode=gg.ArrivalMode.ONOFF, on_rate_rps=800.0, off_rate_rps=50.0,
+                            phase_mean_s=0.5, num_classes=2, confidence_low=0.85,
+                            confidence_high=0.97, fallback_degradation=0.013)
+    tr = gg.generate_trace(cfg, 25.0, np.random.default_rng(np.random.SeedSequence(11).spawn(3)[0]))
+    tag = np.random.default_rng(1011).random(len(tr)) < 0.5          # True -> DistilBERT
+    d_idx, r_idx = np.nonzero(tag)[0], np.nonzero(~tag)[0]
+    rcfg = gg.WorkloadConfig(mode=gg.ArrivalMode.CLOSED, num_requests=len(r_idx), num_classes=1000,
+                             confidence_low=0.3, confidence_high=0.9, fallback_degradation=0.05)
+    rtr = gg.generate_trace(rcfg, 1.0, np.random.default_rng(2022))
+    parts = {
+        "distilbert": (tr.scores[d_idx].copy(), tr.arrival_t[d_idx].copy(),
+                       tr.true_label[d_idx].astype(np.int32)),
+        "resnet18": (rtr.scores.copy(), tr.arrival_t[r_idx].copy(),
+                     rtr.true_label.astype(np.int32)),
+    }
+    return len(tr), parts
+
+
+def run_ablation(dev, nets) -> dict:
+    """Both arms on the identical C4 trace; per arm the device wall time (CUDA
+    events) to serve every request of both sub-traces, and the reference's
+    summary figures (telemetry.py:87-145 semantics) over all 10,147 requests."""
     import torch
+    total, parts = c4_trace()
+    res = {}
+    for arm, open_loop in (("open_loop", True), ("bio", False)):
+        srvs = []
+        for kind, (sc, nw, lb) in parts.items():
+            wl = WORKLOADS[kind]
+            srv = make_server(wl, kind, nets[kind], torch.from_numpy(sc).to(dev),
+                              torch.from_numpy(nw).to(dev), torch.from_numpy(lb).to(dev),
+                              payload_pool(kind, 256, 7, dev), dev, open_loop=open_loop,
+                              coin_seed=11 if kind == "distilbert" else 12)
+            srv.run(1)          # eager warm step (allocations), then one graph per server
+            srv.capture()
+            srvs.append(srv)
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream(device=dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        while True:
+            torch.cuda.synchronize()
+            live = [v for v in srvs if not v.done()]
+            if not live:
+                break
+            for v in live:                 # the two models' loops run concurrently
+                v.stream.wait_stream(s)
+            for v in live:
+                v.run(4)
+            for v in live:
+                s.wait_stream(v.stream)
+        b.record(s)
+        torch.cuda.synchronize()
+        rows = [v.summary(label=f"{arm}:{v.kind}") for v in srvs]
+        n = sum(r["admitted_count"] + r["skipped_count"] for r in rows)
+        assert n == total, (n, total)
+        lat = sum(r["avg_latency_ms"] * (r["admitted_count"] + r["skipped_count"]) for r in rows) / n
+        acc = sum(r["accuracy"] * (r["admitted_count"] + r["skipped_count"]) for r in rows) / n
+        adm = sum(r["admitted_count"] for r in rows)
+        res[arm] = {"device_wall_ms": round(a.elapsed_time(b), 3),
+                    "served": sum(r["served_count"] for r in rows), "admitted": adm,
+                    "admission_rate_pct": round(100.0 * adm / n, 3),
+                    "trace_makespan_s": round(max(r["total_time_s"] for r in rows), 4),
+                    "avg_latency_ms": round(lat, 4), "accuracy": round(acc, 5),
+                    "energy_kwh_modeled": sum(r["energy_kwh"] for r in rows),
+                    "per_model": {r["label"].split(":")[1]: {
+                        k: (round(v, 5) if isinstance(v, float) else v) for k, v in r.items()
+                        if k != "label"} for r in rows}}
+        del srvs
+    o, c = res["open_loop"], res["bio"]
+
+    def pct(x, y):
+        return round((x - y) / y * 100.0, 3) if y else None
+    return {"trace": f"C4: ONOFF 800/50 rps, phase 0.5 s, 25 s, {total} arrivals, DistilBERT/ResNet-18 "
+                     "by a seeded coin, Path-B 10 ms window, trace-time latency",
+            "arms": res,
+            "device_wall_time_delta_pct": pct(c["device_wall_ms"], o["device_wall_ms"]),
+            "trace_makespan_delta_pct": pct(c["trace_makespan_s"], o["trace_makespan_s"]),
+            "latency_delta_pct": pct(c["avg_latency_ms"], o["avg_latency_ms"]),
+            "accuracy_delta_pp": round((c["accuracy"] - o["accuracy"]) * 100.0, 3),
+            "admission_rate_pct": c["admission_rate_pct"]}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def _reference_controller(c: dict, B: int):
+    """The UNMODIFIED reference controller (baseline/_ref) when installed, else the
+    oracle port.  Returns (kind, decide(scores, now, snapshot) -> admit,
+    record(lat, joules, depth), p95())."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "greengate")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import greengate as G
+        box = {}
+        ctl = G.ControllerConfig(alpha=c["alpha"], beta=c["beta"], gamma=c["gamma"],
+                                 tau0=c["tau0"], tau_inf=c["tau_inf"], k=c["k"],
+                                 routing=G.RoutePolicy.ALL_BATCHED).build(
+            G.EnergyLedger(), lambda: box["snap"])
+
+        def decide(row, now, snap):
+            box["snap"] = G.CongestionSnapshot(*snap)
+            return ctl.decide(G.RequestFeatures(0, now, tuple(float(v) for v in row), None),
+                              now).admit
+        return "reference", decide, ctl.record_outcome, ctl.p95_ms
     from oracle import controller_oracle as O
+    ctl = O.OracleController(O.OracleParams(alpha=c["alpha"], beta=c["beta"], gamma=c["gamma"],
+                                            tau0=c["tau0"], tau_inf=c["tau_inf"], k=c["k"],
+                                            routing=O.ALL_BATCHED))
+    return ("port", lambda row, now, snap: ctl.decide([float(v) for v in row], now, snap).admit,
+            ctl.record_outcome, ctl.p95_ms)
+
+
+def cpu_reference(wl: dict, workload: str, steps: int, warmup: int):
+    """Reference CPU path: the reference AdmissionController deciding each window
+    (frozen snapshot per window through its congestion_source hook) and recording
+    the served outcomes, + a torch-eager fp32 CPU forward of the served batch
+    (stand-in: the reference only simulates inference), all host cores."""
+    import torch
 
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
     B, W = wl["batch"], wl["window"]
     n_steps = warmup + steps
-    scores, now = make_trace(wl, (n_steps + 2) * W, seed=1000)
+    scores, now, _labels = make_trace(wl, (n_steps + 2) * W, seed=1000)
     if workload == "resnet18":
         from paper_2601_04250_b200.resnet18 import random_model
         model = random_model(0).eval()
@@ -476,10 +710,7 @@ def cpu_reference(wl: dict, workload: str, steps: int, warmup: int, sample_steps
         from paper_2601_04250_b200.distilbert import random_model
         model = random_model(0).eval()
         x_pool = torch.randint(0, 30522, (8, 128))
-    c = wl["ctl"]
-    ctl = O.OracleController(O.OracleParams(alpha=c["alpha"], beta=c["beta"], gamma=c["gamma"],
-                                            tau0=c["tau0"], tau_inf=c["tau_inf"], k=c["k"],
-                                            routing=O.ALL_BATCHED))
+    kind, decide, record, p95 = _reference_controller(wl["ctl"], B)
     fifo: list[int] = []
     m = wl["outcome"]
     served = 0
@@ -487,11 +718,10 @@ def cpu_reference(wl: dict, workload: str, steps: int, warmup: int, sample_steps
     for s in range(n_steps):
         t0 = time.perf_counter()
         depth = len(fifo)
-        snap = (depth, ctl.p95_ms(), min(1.0, depth / B))
+        snap = (depth, p95(), min(1.0, depth / B))
         rows = scores[s * W:(s + 1) * W]
         for i in range(rows.shape[0]):
-            d = ctl.decide([float(v) for v in rows[i]], float(now[s * W + i]), snap)
-            if d.admit:
+            if decide(rows[i], float(now[s * W + i]), snap):
                 fifo.append(s * W + i)
         batch, fifo = fifo[:B], fifo[B:]
         n = len(batch)
@@ -499,57 +729,98 @@ def cpu_reference(wl: dict, workload: str, steps: int, warmup: int, sample_steps
             with torch.no_grad():
                 xb = x_pool[torch.arange(n) % x_pool.shape[0]]
                 model(xb) if workload == "resnet18" else model(input_ids=xb)
-            lat = m["batch_base_ms"] + m["per_item_ms"] * n
+            clock = float(now[min(len(now), (s + 1) * W) - 1])
+            service = (m["batch_base_ms"] + m["per_item_ms"] * n) / 1000.0
             jo = (m["batch_base_energy_j"] + m["per_item_energy_j"] * n) / n
-            for _ in range(n):
-                ctl.record_outcome(lat, jo, len(fifo))
+            for r in batch:
+                record((clock + service - float(now[r])) * 1000.0, jo, len(fifo))
         dt = time.perf_counter() - t0
         if s >= warmup:
             t_total += dt
             served += n
     return {"value": served / t_total, "served": served, "seconds": t_total, "cores": threads,
-            "steps": steps}
+            "steps": steps, "kind": kind}
 
 
 # ----------------------------------------------------------------------------- main
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _config(kind: str, world: int) -> dict:
+    wl = WORKLOADS[kind]
+    return {"workload": (f"{kind} gated inference, forward batch {wl['batch']}, {wl['window']} "
+                         f"Poisson arrivals/step at {wl['rate']:.0f} rps, K={wl['k']} gating "
+                         f"scores (confidence U({wl['conf_lo']}, {wl['conf_hi']})), tau(t) "
+                         f"{wl['ctl']['tau0']} -> {wl['ctl']['tau_inf']} (k={wl['ctl']['k']}/s) "
+                         f"with congestion feedback, Path-B {wl['batching_window_ms']} ms window"),
+            "model": kind, "global_batch": wl["batch"] * world,
+            "seq_len": 128 if kind == "distilbert" else None,
+            "image": 224 if kind == "resnet18" else None, "window": wl["window"],
+            "controller": wl["ctl"], "parallelism": f"dp{world}" if world > 1 else "single",
+            "l2": "activation working set > 126 MB L2 (no flush needed)"}
+
+
+def _line(r: dict, args, world: int, kind: str) -> dict:
+    value = r["served"] / (r["ms"] * 1e-3)
+    e2e_value = r["e2e_served"] / (r["e2e_ms"] * 1e-3) if r["e2e_ms"] > 0 else None
+    return {"metric": METRIC, "value": round(value, 2), "unit": "inferences/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(r["ms"] / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference-order numpy traces, random-init weights)",
+            "config": _config(kind, world), **r["loop"],
+            "roofline": r["roofline"],
+            "e2e": {"value": round(e2e_value, 2) if e2e_value else None, "unit": "inferences/s",
+                    "h2d_bytes_per_step": r["e2e"]["h2d_bytes_per_step"],
+                    "d2h_bytes_per_step": r["e2e"]["d2h_bytes_per_step"]},
+            "gpu_launches": r["launches_per_step"] * args.steps, "clocks": r["clocks"],
+            "energy": r["energy"]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=list(WORKLOADS), default="resnet18")
+    ap.add_argument("--workload", choices=list(WORKLOADS), default="distilbert")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the second workload, ablation, K1/K2 micro-rooflines, energy")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    wl = WORKLOADS[args.workload]
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    metric = "admitted inferences/sec"
-    config = {"workload": f"{args.workload} gated inference, forward batch {wl['batch']}, "
-                          f"{wl['window']} arrivals/step, K={wl['k']} gating scores",
-              "model": args.workload, "global_batch": wl["batch"] * world,
-              "seq_len": 128 if args.workload == "distilbert" else None,
-              "image": 224 if args.workload == "resnet18" else None,
-              "window": wl["window"], "controller": wl["ctl"],
-              "parallelism": f"dp{world}" if world > 1 else "single",
-              "l2": "activation working set > 126 MB L2 (no flush needed)"}
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+
+    kind = args.workload
+    wl = WORKLOADS[kind]
     if args.impl == "reference":
         if rank != 0:
             return
-        steps = min(args.steps, 10)
-        r = cpu_reference(wl, args.workload, steps, min(args.warmup, 3))
-        line = {"impl": "reference", "metric": metric, "value": round(r["value"], 3),
-                "unit": "inferences/s", "n_gpus": args.gpus, "steps": steps,
-                "warmup": min(args.warmup, 3), "ms_per_step": round(1e3 * r["seconds"] / steps, 3),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "fp64 controller / fp32 forward", "data": "synthetic", "config": config,
+        steps, warm = min(args.steps, 10), min(args.warmup, 3)
+        r = cpu_reference(wl, kind, steps, warm)
+        who = ("the unmodified reference AdmissionController (baseline/_ref)" if r["kind"] ==
+               "reference" else "the CPython controller port (oracle/, reference not installed)")
+        line = {"impl": "reference", "metric": METRIC, "value": round(r["value"], 3),
+                "unit": "inferences/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+                "ms_per_step": round(1e3 * r["seconds"] / steps, 3), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "fp64 controller / fp32 forward",
+                "data": "synthetic", "config": _config(kind, 1),
                 "cpu_baseline": {"value": round(r["value"], 3), "unit": "inferences/s",
-                                 "cores": r["cores"], "kind": "port",
-                                 "sample": f"{steps} steps x {wl['window']} arrivals: CPython "
-                                           "controller port + torch-eager fp32 CPU forward "
+                                 "cores": r["cores"], "kind": r["kind"],
+                                 "sample": f"{steps} steps x {wl['window']} arrivals: {who} + "
+                                           "torch-eager fp32 CPU forward of each served batch "
                                            "(stand-in; the reference simulates inference)"},
                 "e2e": {"value": round(r["value"], 3), "unit": "inferences/s",
                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -563,36 +834,38 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         pg = dist.group.WORLD
-    r = run_ours(args, wl, rank, world, local_rank, pg)
+    r = run_ours(args, kind, rank, world, local_rank, pg)
+    other = None
+    if not args.no_extras:
+        okind = "resnet18" if kind == "distilbert" else "distilbert"
+        other = run_ours(args, okind, rank, world, local_rank, pg, with_clocks=False)
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
         return
-    value = r["served"] / (r["ms"] * 1e-3)
-    e2e_value = r["e2e_served"] / (r["e2e_ms"] * 1e-3) if r["e2e_ms"] > 0 else None
+    import torch
+    dev = torch.device("cuda", local_rank)
+    line = _line(r, args, world, kind)
+    if other is not None:
+        ol = _line(other, args, world, okind)
+        line[okind] = {k: ol[k] for k in ("value", "ms_per_step", "config", "admission_rate",
+                                           "mean_forward_batch", "tau_timed_region", "roofline",
+                                           "e2e", "gpu_launches", "energy")}
+    if not args.no_extras:
+        line["admission_roofline"] = admission_kernel_roofline(dev)
+        line["exchange"] = exchange_cost(dev)
+        nets = {k: build_net(k, WORKLOADS[k]["batch"]) for k in WORKLOADS}
+        line["ablation"] = run_ablation(dev, nets)
+        del nets
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        c = cpu_reference(wl, args.workload, steps=2, warmup=1)
+        c = cpu_reference(wl, kind, steps=2, warmup=1)
         cpu = {"value": round(c["value"], 3), "unit": "inferences/s", "cores": c["cores"],
-               "kind": "port",
-               "sample": f"2 steps x {wl['window']} arrivals: CPython controller port + "
-                         "torch-eager fp32 CPU forward (stand-in)"}
-    line = {"metric": metric, "value": round(value, 2), "unit": "inferences/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(r["ms"] / args.steps, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (reference-order numpy traces, random-init weights)",
-            "config": config,
-            "admission_rate": round(r["admitted"] / max(1, r["decided"]), 4),
-            "mean_forward_batch": round(r["served"] / (args.steps * world), 2),
-            "queue_depth_end": r["queue_depth"], "fifo_overflow": r["overflow"],
-            "roofline": r["roofline"], "admission_roofline": r["k1"], "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_value, 2) if e2e_value else None, "unit": "inferences/s",
-                    "h2d_bytes_per_step": r["e2e"]["h2d_bytes_per_step"],
-                    "d2h_bytes_per_step": r["e2e"]["d2h_bytes_per_step"]},
-            "gpu_launches": r["launches_per_step"] * args.steps,
-            "clocks": r["clocks"],
-            "energy": r["energy"]}
+               "kind": c["kind"],
+               "sample": f"2 steps x {wl['window']} arrivals: reference AdmissionController "
+                         "+ torch-eager fp32 CPU forward of each served batch (stand-in)"}
+    line["cpu_baseline"] = cpu
     print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

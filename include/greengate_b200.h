@@ -213,6 +213,7 @@ typedef struct {
   int64_t trace_len;    /* rows of the resident trace */
   int64_t extra_depth;  /* queue depth of the other ranks (multi-GPU exchange) */
   int64_t overflow;     /* admissions lost to a full ring (must stay 0) */
+  double clock;         /* trace time of the last pop (gg_fifo_pop_windowed), monotone */
 } gg_fifo;
 
 /* Stream form of gg_admit: decides rows [fifo.cursor, fifo.cursor + window)
@@ -227,17 +228,57 @@ int gg_admit_stream(const gg_params* params, gg_state* state_dev, gg_fifo* fifo_
                     const gg_snapshot* snapshot_dev, uint8_t* decision_dev,
                     gg_batch_info* info_dev, void* workspace_dev, size_t workspace_bytes,
                     void* stream);
+/* Open-loop arm of Simulation._decide (servesim.py:231-240, controller
+ * disabled): every row of the window [fifo.cursor, +window) is admitted with
+ * the static route (ALL_DIRECT -> DIRECT, ALL_BATCHED -> BATCHED,
+ * THRESHOLD_ON_QUEUE -> BATCHED iff depth + extra_depth > queue_threshold) and
+ * appended to the ring; no score is read or validated.  The state gets the
+ * counters and snapshot observes of an always-admitting decide(). */
+int gg_admit_open_stream(const gg_params* params, gg_state* state_dev, gg_fifo* fifo_dev,
+                         int32_t* ring_ids_dev, uint64_t* ring_ns_dev, int64_t window,
+                         uint8_t* decision_dev, gg_batch_info* info_dev, void* stream);
 /* Pops n = min(B, depth) requests: batch_ids[0..n) (trace rows), batch_ns,
  * *count_dev = n. */
 int gg_fifo_pop(gg_fifo* fifo_dev, const int32_t* ring_ids_dev, const uint64_t* ring_ns_dev,
                 int32_t* batch_ids_dev, uint64_t* batch_ns_dev, int32_t* count_dev, int32_t B,
                 void* stream);
+/* Path-B pop with the reference's flush policy (batch_flush_policy,
+ * servesim.py:148-162): with batching_window_s > 0 the batch flushes when B
+ * requests are pending (n = B) or the oldest has waited >= window - 1e-12 s of
+ * trace time (n = depth), else n = 0.  The trace clock is now_dev[cursor - 1]
+ * (the last decided arrival); once the trace is exhausted the batch timer
+ * fires (clock = oldest arrival + window).  fifo.clock records it.
+ * batching_window_s == 0: size trigger only (n = min(B, depth)). */
+int gg_fifo_pop_windowed(gg_fifo* fifo_dev, const int32_t* ring_ids_dev,
+                         const uint64_t* ring_ns_dev, const double* now_dev,
+                         double batching_window_s, int32_t* batch_ids_dev,
+                         uint64_t* batch_ns_dev, int32_t* count_dev, int32_t B, void* stream);
+/* Fallback answers and accounting (Simulation._complete, servesim.py:246-256)
+ * for the rows a window decided (fifo_dev/info_dev: the rows gg_admit_stream
+ * just decided; else [row0, row0 + n)): answer[row] = top_class(scores)
+ * (first max, workload.py:42-43) for every decided row; correct[row] =
+ * (top == label) for admitted rows, and (top == label AND coin >= degradation)
+ * for skipped rows, where coins_dev is the host-drawn `_fb_rng` stream consumed
+ * in trace order by the skipped rows with top == label (*coin_cursor_dev
+ * advances).  Invalid rows (255) are left untouched. */
+int gg_fallback_answers(const double* probs_dev, int32_t k, int64_t row_stride,
+                        const int32_t* labels_dev, const uint8_t* decision_dev,
+                        const gg_fifo* fifo_dev, const gg_batch_info* info_dev, int64_t row0,
+                        int64_t n, const double* coins_dev, int64_t* coin_cursor_dev,
+                        double fallback_degradation, int32_t* answer_dev, uint8_t* correct_dev,
+                        void* stream);
 /* Outcome model of a served batch (servesim.py:137-139, 303-305 for the
  * modeled path; %globaltimer latency for the measured path). */
+enum {
+  GG_LATENCY_MODEL = 0,     /* latency = base + per_item * n (service time only) */
+  GG_LATENCY_MEASURED = 1,  /* device %globaltimer: completion - admission */
+  GG_LATENCY_TRACE = 2      /* trace time: (fifo.clock + service_s - arrival) * 1000,
+                               the reference's finish_t - enqueue_t (servesim.py:258-266) */
+};
 typedef struct {
   double batch_base_ms, per_item_ms;        /* modeled latency = base + per_item * n */
   double batch_base_energy_j, per_item_energy_j;  /* joules each = (base + per_item*n)/n */
-  int32_t measured_latency;                 /* 1: latency = now - admission time */
+  int32_t measured_latency;                 /* GG_LATENCY_* */
   int32_t reserved;
 } gg_outcome_model;
 /* Writes one rank's step into its exchange slot (fp64, GG_SLOT_LEN(B) values):
@@ -251,6 +292,14 @@ typedef struct {
 int gg_served_outcomes(const gg_fifo* fifo_dev, const int32_t* count_dev,
                        const uint64_t* batch_ns_dev, const gg_outcome_model* model,
                        const gg_batch_info* info_dev, double* slot_dev, int32_t B, void* stream);
+/* Same, with the served batch's trace rows and arrival times (needed by
+ * GG_LATENCY_TRACE); latency_row_dev (NULL or fp64 [trace_len]) receives each
+ * served request's latency_ms at its trace row (CompletionRecord.latency_ms). */
+int gg_served_outcomes_trace(const gg_fifo* fifo_dev, const int32_t* count_dev,
+                             const uint64_t* batch_ns_dev, const int32_t* batch_ids_dev,
+                             const double* now_dev, const gg_outcome_model* model,
+                             const gg_batch_info* info_dev, double* slot_dev, int32_t B,
+                             double* latency_row_dev, void* stream);
 /* Applies G exchange slots (all-reduced) to this rank's replica: first the
  * other ranks' admission effects (normalizer observes of their snapshots,
  * counters), then every rank's outcomes in rank order (K2, record_outcome

@@ -24,6 +24,7 @@ GG_ERR_UNSUPPORTED = 7
 GG_DIR_GEQ, GG_DIR_LT = 0, 1
 GG_UTIL_ENTROPY, GG_UTIL_ONE_MINUS_CONFIDENCE = 0, 1
 GG_ROUTE_ALL_DIRECT, GG_ROUTE_ALL_BATCHED, GG_ROUTE_THRESHOLD_ON_QUEUE = 0, 1, 2
+GG_LATENCY_MODEL, GG_LATENCY_MEASURED, GG_LATENCY_TRACE = 0, 1, 2
 GG_DECISION_SKIP, GG_DECISION_DIRECT, GG_DECISION_BATCHED, GG_DECISION_INVALID = 0, 1, 2, 255
 
 
@@ -71,7 +72,7 @@ class gg_batch_info(C.Structure):
 class gg_fifo(C.Structure):
     _fields_ = [("head", C.c_int64), ("tail", C.c_int64), ("capacity", C.c_int64),
                 ("batch_cap", C.c_int64), ("cursor", C.c_int64), ("trace_len", C.c_int64),
-                ("extra_depth", C.c_int64), ("overflow", C.c_int64)]
+                ("extra_depth", C.c_int64), ("overflow", C.c_int64), ("clock", C.c_double)]
 
 
 class gg_outcome_model(C.Structure):

@@ -64,8 +64,13 @@ SIGNATURES: dict[str, tuple] = {
     # serving loop (include/greengate_b200.h)
     "gg_admit_stream": (C.c_int, [_P, _P, _P, _P, _P, _P, _I32, _I64, _P, _I64, _P, _P, _P, _P,
                                   C.c_size_t, _P]),
+    "gg_admit_open_stream": (C.c_int, [_P, _P, _P, _P, _P, _I64, _P, _P, _P]),
     "gg_fifo_pop": (C.c_int, [_P, _P, _P, _P, _P, _P, _I32, _P]),
+    "gg_fifo_pop_windowed": (C.c_int, [_P, _P, _P, _P, _D, _P, _P, _P, _I32, _P]),
+    "gg_fallback_answers": (C.c_int, [_P, _I32, _I64, _P, _P, _P, _P, _I64, _I64, _P, _P, _D, _P,
+                                      _P, _P]),
     "gg_served_outcomes": (C.c_int, [_P, _P, _P, _P, _P, _P, _I32, _P]),
+    "gg_served_outcomes_trace": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P]),
     "gg_outcome_slots": (C.c_int, [_P, _P, _P, _I32, _I32, _I32, _P, _P, _P]),
     "gg_epilogue_served": (C.c_int, [_P, _P, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P, _P]),
 }

@@ -59,7 +59,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if prev != flags:
         force = True
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
-    headers.append(os.path.join(ROOT, "include", "greengate_b200.h"))
+    headers += [os.path.join(ROOT, "include", h) for h in os.listdir(os.path.join(ROOT, "include"))
+                if h.endswith(".h")]
     objs = []
     for src in _sources():
         path = os.path.join(CSRC, src)

@@ -19,6 +19,7 @@ fallback: without the library or a CUDA device, construction raises
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import math
 import struct
@@ -30,6 +31,7 @@ from typing import Callable, Sequence
 
 from . import _abi, _native
 from .energy import EnergyLedger
+from . import errors as _errors
 from .errors import InvalidDistribution, InvalidSchedule, NegativeMeasurement, from_status
 
 
@@ -175,25 +177,35 @@ class CongestionSnapshot:
 # --------------------------------------------------------------- device helpers
 
 class _Device:
-    """Per-process scratch buffers for the stateless helpers (one per device)."""
+    """Per-process scratch buffers for the stateless helpers (one per device).
 
-    _lock = threading.Lock()
+    `use()` holds the lock across the whole copy -> launch -> read-back
+    sequence, so concurrent callers (threads, or different current streams)
+    never see each other's inputs; the reference functions are pure and
+    thread-safe, and so are these."""
+
+    _lock = threading.RLock()
     _scratch: dict = {}
 
     @classmethod
-    def tensors(cls, device, n: int, k: int):
+    def _tensors(cls, device, n: int, k: int):
         torch = _native.require_cuda()
         key = (str(device),)
+        buf = cls._scratch.get(key)
+        if buf is None or buf["cap"] < n * max(k, 3):
+            cap = max(64, n * max(k, 3))
+            buf = {"cap": cap,
+                   "in": torch.empty(cap, dtype=torch.float64, device=device),
+                   "out": torch.empty(cap, dtype=torch.float64, device=device),
+                   "valid": torch.empty(cap, dtype=torch.uint8, device=device)}
+            cls._scratch[key] = buf
+        return buf
+
+    @classmethod
+    @contextlib.contextmanager
+    def use(cls, device, n: int, k: int):
         with cls._lock:
-            buf = cls._scratch.get(key)
-            if buf is None or buf["cap"] < n * max(k, 3):
-                cap = max(64, n * max(k, 3))
-                buf = {"cap": cap,
-                       "in": torch.empty(cap, dtype=torch.float64, device=device),
-                       "out": torch.empty(cap, dtype=torch.float64, device=device),
-                       "valid": torch.empty(cap, dtype=torch.uint8, device=device)}
-                cls._scratch[key] = buf
-            return buf
+            yield cls._tensors(device, n, k)
 
 
 def _default_device():
@@ -208,14 +220,15 @@ def _utility_device(scores: Sequence[float], proxy: UtilityProxy) -> float:
     if len(xs) < 2:
         raise InvalidDistribution(f"need at least 2 class scores, got {len(xs)}")
     dev = _default_device()
-    buf = _Device.tensors(dev, 1, len(xs))
     host = torch.tensor(xs, dtype=torch.float64)
-    buf["in"][: len(xs)].copy_(host)
-    _native.check("gg_utility", lib.gg_utility(_native.ptr(buf["in"]), 1, len(xs), len(xs),
-                                               _UTIL[proxy], _native.ptr(buf["out"]),
-                                               _native.ptr(buf["valid"]), _native.stream_ptr()))
-    u = float(buf["out"][0].item())
-    if not int(buf["valid"][0].item()):
+    with _Device.use(dev, 1, len(xs)) as buf:
+        buf["in"][: len(xs)].copy_(host)
+        _native.check("gg_utility", lib.gg_utility(_native.ptr(buf["in"]), 1, len(xs), len(xs),
+                                                   _UTIL[proxy], _native.ptr(buf["out"]),
+                                                   _native.ptr(buf["valid"]), _native.stream_ptr()))
+        u = float(buf["out"][0].item())
+        valid = int(buf["valid"][0].item())
+    if not valid:
         total = sum(xs)
         if any(not math.isfinite(x) or x < 0.0 for x in xs):
             raise InvalidDistribution(f"scores must be finite and >= 0: {xs}")
@@ -237,28 +250,27 @@ def threshold_at(schedule: ThresholdSchedule, t: float) -> float:
     """controller.py:114-123, evaluated by the device (gg_threshold)."""
     if not (math.isfinite(schedule.k) and schedule.k > 0.0):
         raise InvalidSchedule(f"decay rate k must be > 0, got {schedule.k!r}")
-    torch = _native.require_cuda()
     lib = _native.load()
-    buf = _Device.tensors(_default_device(), 1, 1)
-    buf["in"][:1].fill_(float(t))
-    _native.check("gg_threshold", lib.gg_threshold(schedule.tau0, schedule.tau_inf, schedule.k,
-                                                   schedule.t_origin, _native.ptr(buf["in"]),
-                                                   _native.ptr(buf["out"]), 1,
-                                                   _native.stream_ptr()))
-    del torch
-    return float(buf["out"][0].item())
+    with _Device.use(_default_device(), 1, 1) as buf:
+        buf["in"][:1].fill_(float(t))
+        _native.check("gg_threshold", lib.gg_threshold(schedule.tau0, schedule.tau_inf, schedule.k,
+                                                       schedule.t_origin, _native.ptr(buf["in"]),
+                                                       _native.ptr(buf["out"]), 1,
+                                                       _native.stream_ptr()))
+        return float(buf["out"][0].item())
 
 
 def cost(weights: CostWeights, utility: float, energy: float, congestion: float) -> float:
     """controller.py:214-216, evaluated by the device (gg_cost)."""
     lib = _native.load()
-    buf = _Device.tensors(_default_device(), 1, 3)
-    buf["in"][:3].copy_(_native.require_cuda().tensor([utility, energy, congestion],
-                                                      dtype=_native.require_cuda().float64))
-    _native.check("gg_cost", lib.gg_cost(weights.alpha, weights.beta, weights.gamma,
-                                         _native.ptr(buf["in"]), _native.ptr(buf["out"]), 1,
-                                         _native.stream_ptr()))
-    return float(buf["out"][0].item())
+    torch = _native.require_cuda()
+    host = torch.tensor([utility, energy, congestion], dtype=torch.float64)
+    with _Device.use(_default_device(), 1, 3) as buf:
+        buf["in"][:3].copy_(host)
+        _native.check("gg_cost", lib.gg_cost(weights.alpha, weights.beta, weights.gamma,
+                                             _native.ptr(buf["in"]), _native.ptr(buf["out"]), 1,
+                                             _native.stream_ptr()))
+        return float(buf["out"][0].item())
 
 
 _UTILITY_FN = {UtilityProxy.ENTROPY: entropy_utility,
@@ -343,14 +355,6 @@ class AdmissionController:
                  p95_window: int = 100, device=None) -> None:
         torch = _native.require_cuda()
         self._lib = _native.load()
-        self.weights = weights
-        self._schedule = schedule
-        self.congestion_source = congestion_source
-        self.direction = _enum(Direction, direction)
-        self.utility_proxy = _enum(UtilityProxy, utility_proxy)
-        self.routing = _enum(RoutePolicy, routing)
-        self.queue_threshold = int(queue_threshold)
-        self.p95_window = int(p95_window)
         self.device = torch.device(device) if device is not None else _default_device()
         # Ledgers of the reference package (or any foreign object) are mirrored:
         # the device owns the EWMA, the foreign object's fields are refreshed
@@ -364,13 +368,20 @@ class AdmissionController:
                                        ewma_joules_per_request=ledger.ewma_joules_per_request,
                                        samples_seen=ledger.samples_seen)
             self._mirror = ledger
-        self.params = _abi.gg_params(
-            weights.alpha, weights.beta, weights.gamma, schedule.tau0, schedule.tau_inf,
-            schedule.k, self.ledger.ewma_lambda, _DIR[self.direction], _UTIL[self.utility_proxy],
-            _ROUTE[self.routing], self.queue_threshold, self.p95_window, 0)
-        rc = self._lib.gg_validate_params(C.byref(self.params))
-        if rc != _abi.GG_OK:
-            raise from_status(rc, f"invalid controller parameters (gg_status {rc})")
+        # exception classes raised by decide()/record_outcome(): ours, or (when
+        # patched into a host package, integration.py) classes deriving from
+        # both the host's and ours, so either side's `except` clauses match
+        self.errors = _errors
+        # policy attributes: assigning any of them (like the reference, whose
+        # decide() reads them on every call) rebuilds the device parameter block
+        self._policy = dict(weights=weights, schedule=schedule,
+                            direction=_enum(Direction, direction),
+                            utility_proxy=_enum(UtilityProxy, utility_proxy),
+                            routing=_enum(RoutePolicy, routing),
+                            queue_threshold=int(queue_threshold))
+        self.congestion_source = congestion_source
+        self.p95_window = int(p95_window)
+        self.params = self._build_params(self._policy)
         with torch.cuda.device(self.device):
             self.state = torch.zeros(_abi.STATE_BYTES, dtype=torch.uint8, device=self.device)
             self._ws = torch.zeros(self._lib.gg_admit_workspace_bytes(1), dtype=torch.uint8,
@@ -389,6 +400,25 @@ class AdmissionController:
         self.result_types = sys.modules[__name__]
 
     # ------------------------------------------------------------------ plumbing
+    def _build_params(self, pol: dict) -> _abi.gg_params:
+        w, sc = pol["weights"], pol["schedule"]
+        p = _abi.gg_params(
+            w.alpha, w.beta, w.gamma, sc.tau0, sc.tau_inf, sc.k, self.ledger.ewma_lambda,
+            _DIR[_enum(Direction, pol["direction"])],
+            _UTIL[_enum(UtilityProxy, pol["utility_proxy"])],
+            _ROUTE[_enum(RoutePolicy, pol["routing"])], int(pol["queue_threshold"]),
+            self.p95_window, 0)
+        rc = self._lib.gg_validate_params(C.byref(p))
+        if rc != _abi.GG_OK:
+            raise from_status(rc, f"invalid controller parameters (gg_status {rc})")
+        return p
+
+    def _set_policy(self, name: str, value) -> None:
+        pol = dict(self._policy)
+        pol[name] = value
+        self.params = self._build_params(pol)   # validates before committing
+        self._policy = pol
+
     def _stream(self):
         torch = _native.require_cuda()
         return _native.stream_ptr(torch.cuda.current_stream(self.device))
@@ -405,7 +435,7 @@ class AdmissionController:
         s.ewma_joules_per_request = led._ewma
         s.samples_seen = led._seen
         s.total_joules = led._total
-        s.t_origin = self._schedule.t_origin
+        s.t_origin = self.schedule.t_origin
         self.state.copy_(torch.frombuffer(bytearray(bytes(s)), dtype=torch.uint8))
 
     def _state_scalar(self, name: str):
@@ -437,13 +467,55 @@ class AdmissionController:
     # ------------------------------------------------------------------ reference API
     @property
     def schedule(self) -> ThresholdSchedule:
-        return self._schedule
+        return self._policy["schedule"]
 
     @schedule.setter
     def schedule(self, value: ThresholdSchedule) -> None:
-        self._schedule = value
+        """A replacement schedule takes effect on the next decide(): tau0 /
+        tau_inf / k go into the parameter block, t_origin into the device state."""
+        self._set_policy("schedule", value)
         _native.check("gg_reset_clock", self._lib.gg_reset_clock(
             _native.ptr(self.state), value.t_origin, self._stream()))
+
+    @property
+    def weights(self) -> CostWeights:
+        return self._policy["weights"]
+
+    @weights.setter
+    def weights(self, value: CostWeights) -> None:
+        self._set_policy("weights", value)
+
+    @property
+    def direction(self) -> Direction:
+        return self._policy["direction"]
+
+    @direction.setter
+    def direction(self, value) -> None:
+        self._set_policy("direction", _enum(Direction, value))
+
+    @property
+    def utility_proxy(self) -> UtilityProxy:
+        return self._policy["utility_proxy"]
+
+    @utility_proxy.setter
+    def utility_proxy(self, value) -> None:
+        self._set_policy("utility_proxy", _enum(UtilityProxy, value))
+
+    @property
+    def routing(self) -> RoutePolicy:
+        return self._policy["routing"]
+
+    @routing.setter
+    def routing(self, value) -> None:
+        self._set_policy("routing", _enum(RoutePolicy, value))
+
+    @property
+    def queue_threshold(self) -> int:
+        return self._policy["queue_threshold"]
+
+    @queue_threshold.setter
+    def queue_threshold(self, value: int) -> None:
+        self._set_policy("queue_threshold", int(value))
 
     @property
     def admitted_total(self) -> int:
@@ -487,8 +559,9 @@ class AdmissionController:
         torch = _native.require_cuda()
         xs = [float(s) for s in features.scores]
         k = len(xs)
+        E = self.errors
         if k < 2:
-            raise InvalidDistribution(f"need at least 2 class scores, got {k}")
+            raise E.InvalidDistribution(f"need at least 2 class scores, got {k}")
         snap = self._snapshot_struct()
         io = self._io_buffer(k)
         o_snap = 8 * (k + 1)
@@ -508,8 +581,8 @@ class AdmissionController:
         code = raw[24 + _abi.BATCH_INFO_BYTES]
         if code == _abi.GG_DECISION_INVALID:
             if any(not math.isfinite(x) or x < 0.0 for x in xs):
-                raise InvalidDistribution(f"scores must be finite and >= 0: {xs}")
-            raise InvalidDistribution(f"scores must sum to 1 (got {sum(xs)!r})")
+                raise E.InvalidDistribution(f"scores must be finite and >= 0: {xs}")
+            raise E.InvalidDistribution(f"scores must sum to 1 (got {sum(xs)!r})")
         admit = code in (_abi.GG_DECISION_DIRECT, _abi.GG_DECISION_BATCHED)
         # result types: ours, or the host package's when patched into it (integration.py)
         T = self.result_types
@@ -526,7 +599,7 @@ class AdmissionController:
     def record_outcome(self, latency_ms: float, joules: float, queue_depth: int) -> None:
         """controller.py:345-358: one K2 launch (stream-ordered, no host sync)."""
         if latency_ms < 0.0 or joules < 0.0 or queue_depth < 0:
-            raise NegativeMeasurement(
+            raise self.errors.NegativeMeasurement(
                 f"outcome measurements must be >= 0, got "
                 f"latency={latency_ms!r} joules={joules!r} depth={queue_depth!r}")
         torch = _native.require_cuda()
@@ -543,7 +616,7 @@ class AdmissionController:
 
     def reset_clock(self, t_origin: float) -> None:
         """controller.py:360-362."""
-        self.schedule = replace(self._schedule, t_origin=t_origin)
+        self.schedule = replace(self.schedule, t_origin=t_origin)
 
     # ------------------------------------------------------------------ batch API
     def decide_batch(self, scores, now, snapshot=None, *, breakdown: bool = True,
@@ -558,11 +631,17 @@ class AdmissionController:
         snapshot; invalid rows get code 255 and change no state.
         """
         torch = _native.require_cuda()
+        if scores.dim() != 2:
+            raise ValueError(f"scores must be [n, k], got shape {tuple(scores.shape)}")
         n, k = int(scores.shape[0]), int(scores.shape[1])
         if scores.dtype != torch.float64 or now.dtype != torch.float64:
             raise TypeError("scores and now must be float64 CUDA tensors")
+        self._check_device(scores=scores, now=now)
         if n > 0 and k > 1 and scores.stride(1) != 1:
             raise ValueError("scores rows must be contiguous")
+        if now.dim() != 1 or now.numel() < n or (n > 0 and now.stride(0) != 1):
+            raise ValueError(f"now must be a contiguous [n] tensor with n >= {n}, "
+                             f"got shape {tuple(now.shape)}")
         self._ensure_ws(n)
         if out is None:
             out = BatchDecision(
@@ -596,7 +675,20 @@ class AdmissionController:
         check=True the call syncs and raises NegativeMeasurement like a Python
         loop over record_outcome would (outcomes before the bad one stay applied).
         """
+        torch = _native.require_cuda()
+        for name, t, dt in (("latency_ms", latency_ms, torch.float64),
+                            ("joules", joules, torch.float64),
+                            ("queue_depth", queue_depth, torch.int32)):
+            if not hasattr(t, "data_ptr") or t.dtype != dt:
+                raise TypeError(f"{name} must be a {dt} CUDA tensor, got "
+                                f"{getattr(t, 'dtype', type(t).__name__)}")
+            if t.dim() != 1 or (t.numel() > 1 and t.stride(0) != 1):
+                raise ValueError(f"{name} must be a contiguous 1-D tensor")
+        self._check_device(latency_ms=latency_ms, joules=joules, queue_depth=queue_depth)
         n = int(latency_ms.shape[0])
+        if int(joules.shape[0]) != n or int(queue_depth.shape[0]) != n:
+            raise ValueError(f"latency_ms, joules and queue_depth must have equal lengths, got "
+                             f"{n}, {int(joules.shape[0])}, {int(queue_depth.shape[0])}")
         _native.check("gg_outcome", self._lib.gg_outcome(
             C.byref(self.params), _native.ptr(self.state), _native.ptr(latency_ms),
             _native.ptr(joules), _native.ptr(queue_depth), n, int(set_queue_depth),
@@ -604,12 +696,17 @@ class AdmissionController:
         if check:
             bad = int(self._err.item())
             if bad >= 0:
-                raise NegativeMeasurement(
+                raise self.errors.NegativeMeasurement(
                     f"outcome measurements must be >= 0, got latency={float(latency_ms[bad])!r} "
                     f"joules={float(joules[bad])!r} depth={int(queue_depth[bad])!r}")
             if self._mirror is not None:
                 self._sync_mirror()
         return self._err
+
+    def _check_device(self, **tensors) -> None:
+        for name, t in tensors.items():
+            if t.device != self.device:
+                raise ValueError(f"{name} is on {t.device}, the controller on {self.device}")
 
     def set_queue_depth(self, depth: int) -> None:
         """The gateway's reported depth (gateway.py:191-192, 230) for the default snapshot."""

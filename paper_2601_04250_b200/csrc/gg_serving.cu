@@ -14,16 +14,41 @@ __device__ __forceinline__ uint64_t now_ns() {
   return t;
 }
 
-// One block: n = min(B, depth); copy the ring slots [head, head+n) out.
+// One block: pops n requests and copies the ring slots [head, head+n) out.
+// Without a batching window n = min(B, depth).  With one (Path B,
+// batch_flush_policy servesim.py:148-162) the batch flushes when it is full
+// (n = B) or when the oldest pending request has waited the window in trace
+// time (n = depth); otherwise nothing is popped this step.  The trace clock is
+// the arrival time of the last decided row (after the trace is exhausted the
+// batching timer fires: clock = oldest enqueue + window); it is kept in
+// f->clock (monotone) for the served outcomes' latency.
 __global__ void fifo_pop_kernel(gg_fifo* f, const int32_t* ring, const uint64_t* ring_ns,
-                                int32_t* ids, uint64_t* ns, int32_t* count, int B) {
+                                int32_t* ids, uint64_t* ns, int32_t* count, int B,
+                                const double* now_trace, double window_s) {
   griddep_wait();   // PDL: the predecessor has completed and flushed
   griddep_launch();
   __shared__ int64_t head_s, n_s;
   if (threadIdx.x == 0) {
     const int64_t depth = f->tail - f->head;
+    const int64_t mask = f->capacity - 1;
     head_s = f->head;
-    n_s = depth < B ? depth : B;
+    int64_t n = depth < B ? depth : B;
+    if (now_trace) {
+      const int64_t cur = f->cursor < f->trace_len ? f->cursor : f->trace_len;
+      double clock = cur > 0 ? now_trace[cur - 1] : 0.0;
+      if (window_s > 0.0 && depth > 0 && depth < B) {
+        const double oldest = now_trace[ring[head_s & mask]];
+        const double deadline = f64_sub(window_s, 1e-12);   // servesim.py:_TIME_EPS
+        if (f->cursor >= f->trace_len) {
+          const double fire = f64_add(oldest, window_s);       // the batch timer
+          clock = fire > clock ? fire : clock;
+        } else if (!(f64_sub(clock, oldest) >= deadline)) {
+          n = 0;
+        }
+      }
+      f->clock = clock > f->clock ? clock : f->clock;
+    }
+    n_s = n;
   }
   __syncthreads();
   const int64_t n = n_s, mask = f->capacity - 1;
@@ -46,7 +71,8 @@ __global__ void fifo_pop_kernel(gg_fifo* f, const int32_t* ring, const uint64_t*
 // Exchange slot of one rank's step (layout: GG_SLOT_LEN in greengate_b200.h).
 __global__ void served_outcomes_kernel(const gg_fifo* f, const int32_t* count, const uint64_t* ns,
                                        gg_outcome_model m, const gg_batch_info* info, double* slot,
-                                       int B) {
+                                       int B, const int32_t* ids, const double* now_trace,
+                                       double* latency_row) {
   griddep_wait();   // PDL: the predecessor has completed and flushed
   griddep_launch();
   const int n = *count;
@@ -57,12 +83,22 @@ __global__ void served_outcomes_kernel(const gg_fifo* f, const int32_t* count, c
   const double lat_model = f64_add(m.batch_base_ms, f64_mul(m.per_item_ms, dn));
   const double joules = f64_div(f64_add(m.batch_base_energy_j, f64_mul(m.per_item_energy_j, dn)), dn);
   const uint64_t t = now_ns();
+  // GG_LATENCY_TRACE: finish - enqueue in trace time (servesim.py:_maybe_flush /
+  // _complete): service_s = (base + per_item * n) / 1000, finish = clock + service_s,
+  // latency_ms = (finish - enqueue) * 1000 — the same fp64 operations
+  const double finish = f64_add(f->clock, f64_div(lat_model, 1000.0));
   for (int i = threadIdx.x; i < B; i += blockDim.x) {
     double lat = 0.0, jo = 0.0, q = 0.0;
     if (i < n) {
-      lat = (m.measured_latency && ns) ? (double)(t - ns[i]) * 1e-6 : lat_model;
+      if (m.measured_latency == GG_LATENCY_TRACE && ids && now_trace)
+        lat = f64_mul(f64_sub(finish, now_trace[ids[i]]), 1000.0);
+      else if (m.measured_latency == GG_LATENCY_MEASURED && ns)
+        lat = (double)(t - ns[i]) * 1e-6;
+      else
+        lat = lat_model;
       jo = joules;
       q = qd;
+      if (latency_row && ids) latency_row[ids[i]] = lat;
     }
     slot[i] = lat;
     slot[B + i] = jo;
@@ -294,6 +330,167 @@ __global__ void token_gather_kernel(const int32_t* pool_ids, const int32_t* pool
   if (out_mask) out_mask[t] = pool_mask ? pool_mask[src] : 1;
 }
 
+// ---- open-loop arm (servesim.py:231-240) ----------------------------------
+// With the controller disabled the reference admits every arrival and routes
+// it statically: ALL_BATCHED -> BATCHED; THRESHOLD_ON_QUEUE -> BATCHED iff the
+// queue depth exceeds the threshold, else DIRECT; ALL_DIRECT -> DIRECT.  No
+// score is read or validated.  The controller state sees what decide() of an
+// always-admitting controller leaves (counters, the snapshot's normalizer
+// observes), exactly like the other ranks' slots are applied by K2, so
+// multi-GPU replicas stay identical; the ledger is fed by K2 as
+// servesim.py:272-273 feeds it.
+__global__ void admit_open_kernel(gg_params p, gg_state* st, gg_fifo* f, int32_t* ring,
+                                  uint64_t* ring_ns, int64_t window, uint8_t* decision,
+                                  gg_batch_info* info) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ int64_t row0_s, n_s, tail_s, depth_s;
+  __shared__ uint8_t code_s;
+  if (threadIdx.x == 0) {
+    const int64_t row0 = f->cursor;
+    const int64_t left = f->trace_len - row0;
+    const int64_t n = left < window ? (left > 0 ? left : 0) : window;
+    const int64_t depth = f->tail - f->head;
+    const int64_t qd = depth + f->extra_depth;
+    uint8_t code = GG_DECISION_DIRECT;
+    if (p.routing == GG_ROUTE_ALL_BATCHED) code = GG_DECISION_BATCHED;
+    else if (p.routing == GG_ROUTE_THRESHOLD_ON_QUEUE && qd > (int64_t)p.queue_threshold)
+      code = GG_DECISION_BATCHED;
+    row0_s = row0; n_s = n; tail_s = f->tail; depth_s = depth; code_s = code;
+    double e = 0.0, c = 0.0;
+    const double p95 = st->p95_current;
+    const double fill0 = f64_div((double)depth, (double)f->batch_cap);
+    const double fill = fill0 < 1.0 ? fill0 : 1.0;
+    if (n > 0) {   // decide()'s normalize() observes (controller.py:316-325) + counters
+      gg_channel ce = st->n_energy, cq = st->n_queue_depth, cp = st->n_p95_ms;
+      e = st->samples_seen > 0 ? ch_normalize(ce, st->ewma_joules_per_request) : 0.0;
+      const double qn = ch_normalize(cq, (double)qd), pn = ch_normalize(cp, p95);
+      c = f64_div(f64_add(f64_add(qn, pn), fill), 3.0);
+      st->n_energy = ce; st->n_queue_depth = cq; st->n_p95_ms = cp;
+      st->admitted_total += n;
+    }
+    if (info) {
+      info->n_admitted = n; info->n_skipped = 0; info->n_invalid = 0; info->first_invalid = -1;
+      info->energy = e; info->congestion = c; info->n_decided = n;
+      info->snap_queue_depth = qd; info->snap_p95_ms = p95; info->snap_batch_fill = fill;
+    }
+  }
+  __syncthreads();
+  const int64_t n = n_s, row0 = row0_s, tail = tail_s, depth = depth_s;
+  const int64_t cap = f->capacity, mask = cap - 1;
+  const uint8_t code = code_s;
+  const uint64_t t = now_ns();
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    decision[row0 + i] = code;
+    if (depth + i < cap) {
+      const int64_t slot = (tail + i) & mask;
+      ring[slot] = (int32_t)(row0 + i);
+      if (ring_ns) ring_ns[slot] = t;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int64_t room = cap - depth;
+    const int64_t stored = n < room ? n : room;
+    f->tail = tail + stored;
+    if (n > stored) f->overflow += n - stored;
+    f->cursor = row0 + n;
+  }
+}
+
+// ---- fallback answers (servesim.py:246-256) ---------------------------------
+// Every decided row gets the reference's answer: top_class() of its scores
+// (first max, workload.py:42-43).  Accounting as in Simulation._complete:
+// admitted rows are correct iff top == label; a skipped row is correct iff
+// top == label AND its fallback coin >= fallback_degradation, where the coins
+// are the `_fb_rng` stream (drawn on the host, never on the device) consumed in
+// trace order by exactly the skipped rows with top == label (the `and`
+// short-circuits).  One block, rows in chunks of 256: top classes (a thread or
+// a warp per row), then a block scan of the coin flags.
+constexpr int kFbThreads = 256;
+
+__global__ void __launch_bounds__(kFbThreads) fallback_kernel(
+    const double* __restrict__ scores, int k, int64_t stride, const int32_t* __restrict__ labels,
+    const uint8_t* __restrict__ decision, const gg_fifo* f, const gg_batch_info* info,
+    int64_t row0_arg, int64_t n_arg, const double* __restrict__ coins, int64_t* coin_cursor,
+    double degradation, int32_t* answer, uint8_t* correct) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ int32_t top_s[kFbThreads];
+  __shared__ int32_t warp_tot[kFbThreads / 32];
+  __shared__ int64_t base_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int64_t row0 = row0_arg, n = n_arg;
+  if (f && info) {            // the window the admission kernel just decided
+    n = info->n_decided;
+    row0 = f->cursor - n;
+  }
+  if (tid == 0) base_s = *coin_cursor;
+  for (int64_t c0 = 0; c0 < n; c0 += kFbThreads) {
+    const int cn = (int)min((int64_t)kFbThreads, n - c0);
+    if (k <= 32) {
+      if (tid < cn) {
+        const double* x = scores + (row0 + c0 + tid) * stride;
+        double best = x[0];
+        int bi = 0;
+        for (int j = 1; j < k; ++j) {
+          const double v = x[j];
+          if (v > best) { best = v; bi = j; }
+        }
+        top_s[tid] = bi;
+      }
+    } else {
+      for (int r = warp; r < cn; r += kFbThreads / 32) {
+        const double* x = scores + (row0 + c0 + r) * stride;
+        double best = -INFINITY;
+        int bi = 0x7fffffff;
+        for (int j = lane; j < k; j += 32) {
+          const double v = __ldg(x + j);
+          if (v > best) { best = v; bi = j; }    // lanes see ascending j: first max per lane
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) top_s[r] = bi;
+      }
+    }
+    __syncthreads();
+    int flag = 0, top = -1, lab = -1;
+    uint8_t dec = GG_DECISION_INVALID;
+    const int64_t row = row0 + c0 + tid;
+    if (tid < cn) {
+      dec = decision[row];
+      top = top_s[tid];
+      lab = labels ? labels[row] : -1;
+      flag = (dec == GG_DECISION_SKIP) && (top == lab);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    if (lane == 0) warp_tot[warp] = __popc(bal);
+    __syncthreads();
+    int pre = __popc(bal & ((1u << lane) - 1u)), tot = 0;
+#pragma unroll
+    for (int w = 0; w < kFbThreads / 32; ++w) {
+      if (w < warp) pre += warp_tot[w];
+      tot += warp_tot[w];
+    }
+    if (tid < cn && dec != GG_DECISION_INVALID) {
+      if (answer) answer[row] = top;
+      if (correct) {
+        bool ok = (top == lab);
+        if (dec == GG_DECISION_SKIP) ok = flag && coins[base_s + pre] >= degradation;
+        correct[row] = ok ? 1 : 0;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) base_s += tot;
+    __syncthreads();
+  }
+  if (tid == 0) *coin_cursor = base_s;
+}
+
 }  // namespace gg
 
 using namespace gg;
@@ -303,9 +500,50 @@ extern "C" {
 int gg_fifo_pop(gg_fifo* fifo_dev, const int32_t* ring_ids_dev, const uint64_t* ring_ns_dev,
                 int32_t* batch_ids_dev, uint64_t* batch_ns_dev, int32_t* count_dev, int32_t B,
                 void* stream) {
+  return gg_fifo_pop_windowed(fifo_dev, ring_ids_dev, ring_ns_dev, nullptr, 0.0, batch_ids_dev,
+                              batch_ns_dev, count_dev, B, stream);
+}
+
+int gg_fifo_pop_windowed(gg_fifo* fifo_dev, const int32_t* ring_ids_dev,
+                         const uint64_t* ring_ns_dev, const double* now_dev,
+                         double batching_window_s, int32_t* batch_ids_dev,
+                         uint64_t* batch_ns_dev, int32_t* count_dev, int32_t B, void* stream) {
   if (!fifo_dev || !ring_ids_dev || !batch_ids_dev || !count_dev || B < 1) return GG_ERR_INVALID_ARGUMENT;
+  if (!(batching_window_s >= 0.0) || (batching_window_s > 0.0 && !now_dev)) return GG_ERR_INVALID_ARGUMENT;
   GG_PDL_LAUNCH((fifo_pop_kernel), 1, 256, 0, gg_stream(stream), fifo_dev, ring_ids_dev, ring_ns_dev,
-                                                    batch_ids_dev, batch_ns_dev, count_dev, B);
+                batch_ids_dev, batch_ns_dev, count_dev, B, now_dev, batching_window_s);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_admit_open_stream(const gg_params* params, gg_state* state_dev, gg_fifo* fifo_dev,
+                         int32_t* ring_ids_dev, uint64_t* ring_ns_dev, int64_t window,
+                         uint8_t* decision_dev, gg_batch_info* info_dev, void* stream) {
+  int rc = gg_validate_params(params);
+  if (rc != GG_OK) return rc;
+  if (!state_dev || !fifo_dev || !ring_ids_dev || !decision_dev || window < 1)
+    return GG_ERR_INVALID_ARGUMENT;
+  GG_PDL_LAUNCH((admit_open_kernel), 1, 256, 0, gg_stream(stream), *params, state_dev, fifo_dev,
+                ring_ids_dev, ring_ns_dev, window, decision_dev, info_dev);
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
+
+int gg_fallback_answers(const double* probs_dev, int32_t k, int64_t row_stride,
+                        const int32_t* labels_dev, const uint8_t* decision_dev,
+                        const gg_fifo* fifo_dev, const gg_batch_info* info_dev, int64_t row0,
+                        int64_t n, const double* coins_dev, int64_t* coin_cursor_dev,
+                        double fallback_degradation, int32_t* answer_dev, uint8_t* correct_dev,
+                        void* stream) {
+  if (!probs_dev || !decision_dev || !coin_cursor_dev || k < 1 || row_stride < k)
+    return GG_ERR_INVALID_ARGUMENT;
+  if ((fifo_dev == nullptr) != (info_dev == nullptr)) return GG_ERR_INVALID_ARGUMENT;
+  if (!fifo_dev && (row0 < 0 || n < 0)) return GG_ERR_INVALID_ARGUMENT;
+  if (correct_dev && (!coins_dev || !labels_dev)) return GG_ERR_INVALID_ARGUMENT;
+  if (!(fallback_degradation >= 0.0 && fallback_degradation <= 1.0)) return GG_ERR_INVALID_ARGUMENT;
+  GG_PDL_LAUNCH((fallback_kernel), 1, kFbThreads, 0, gg_stream(stream), probs_dev, k, row_stride,
+                labels_dev, decision_dev, fifo_dev, info_dev, row0, n, coins_dev, coin_cursor_dev,
+                fallback_degradation, answer_dev, correct_dev);
   GG_LAUNCH_OK();
   return GG_OK;
 }
@@ -313,12 +551,24 @@ int gg_fifo_pop(gg_fifo* fifo_dev, const int32_t* ring_ids_dev, const uint64_t* 
 int gg_served_outcomes(const gg_fifo* fifo_dev, const int32_t* count_dev,
                        const uint64_t* batch_ns_dev, const gg_outcome_model* model,
                        const gg_batch_info* info_dev, double* slot_dev, int32_t B, void* stream) {
+  return gg_served_outcomes_trace(fifo_dev, count_dev, batch_ns_dev, nullptr, nullptr, model,
+                                  info_dev, slot_dev, B, nullptr, stream);
+}
+
+int gg_served_outcomes_trace(const gg_fifo* fifo_dev, const int32_t* count_dev,
+                             const uint64_t* batch_ns_dev, const int32_t* batch_ids_dev,
+                             const double* now_dev, const gg_outcome_model* model,
+                             const gg_batch_info* info_dev, double* slot_dev, int32_t B,
+                             double* latency_row_dev, void* stream) {
   if (!fifo_dev || !count_dev || !model || !slot_dev || B < 1) return GG_ERR_INVALID_ARGUMENT;
+  if ((model->measured_latency == GG_LATENCY_TRACE && !now_dev) ||
+      ((model->measured_latency == GG_LATENCY_TRACE || latency_row_dev) && !batch_ids_dev))
+    return GG_ERR_INVALID_ARGUMENT;
   if (model->batch_base_ms < 0 || model->per_item_ms < 0 || model->batch_base_energy_j < 0 ||
       model->per_item_energy_j < 0)
     return GG_ERR_NEGATIVE_MEASUREMENT;
   GG_PDL_LAUNCH((served_outcomes_kernel), 1, 256, 0, gg_stream(stream), fifo_dev, count_dev, batch_ns_dev,
-                                                           *model, info_dev, slot_dev, B);
+                *model, info_dev, slot_dev, B, batch_ids_dev, now_dev, latency_row_dev);
   GG_LAUNCH_OK();
   return GG_OK;
 }

@@ -71,7 +71,7 @@ def _to_device(t, dev):
 
 @dataclass
 class _Item:
-    kind: str                 # "decide" | "outcome" | "barrier"
+    kind: str                 # "decide" | "outcome" | "reset" | "barrier"
     fut: Future
     scores: tuple = ()
     now: float = 0.0
@@ -160,17 +160,33 @@ class GatewayBatcher:
         """POST /v1/outcome (gateway.py:216-230)."""
         return self.submit_outcome(body).result()
 
-    def reset(self) -> None:
-        """POST /v1/reset: re-arm the threshold clock after everything queued so far."""
+    def submit_reset(self) -> Future:
+        """POST /v1/reset (gateway.py:232-237): queued like any request, so the
+        worker applies it in enqueue order (after every earlier request, before
+        every later one) on its own stream; `now` is sampled at enqueue."""
         if self.controller is None:
             raise ApiError(503, "controller not configured")
-        self.flush()
-        self.controller.reset_clock(self.clock())
+        fut: Future = Future()
+        with self._cv:
+            if self._closed:
+                raise ApiError(503, "gateway closed")
+            now = self.clock()
+            self._q.append(_Item("reset", fut, now=now))
+            if self.order is not None:
+                self.order.append(("reset", {"t_origin": now}))
+            self._cv.notify()
+        return fut
+
+    def reset(self) -> None:
+        """POST /v1/reset: re-arm the threshold clock (in request order)."""
+        return self.submit_reset().result()
 
     def flush(self) -> None:
         """Block until every request queued before this call has been applied."""
         fut: Future = Future()
         with self._cv:
+            if self._closed:
+                raise ApiError(503, "gateway closed")
             self._q.append(_Item("barrier", fut))
             self._cv.notify()
         fut.result()
@@ -224,6 +240,10 @@ class GatewayBatcher:
         while i < n:
             it = items[i]
             if it.kind == "barrier":
+                it.fut.set_result(None)
+                i += 1
+            elif it.kind == "reset":
+                self.controller.reset_clock(it.now)
                 it.fut.set_result(None)
                 i += 1
             elif it.kind == "decide":

@@ -18,6 +18,7 @@ RunTrace.ledger and /v1/state keep reporting the loop state.
 from __future__ import annotations
 
 from . import controller as _dev
+from . import errors as _errors
 
 
 def _device_build(self, ledger=None, congestion_source=None, *, p95_window: int = 100,
@@ -35,8 +36,37 @@ def _device_build(self, ledger=None, congestion_source=None, *, p95_window: int 
     # decide() returns the host package's own AdmissionDecision/ServicePath/Reason
     # members, so identity checks like `path is ServicePath.DIRECT` keep working
     import sys
-    ctl.result_types = sys.modules[type(self).__module__]
+    host_mod = sys.modules[type(self).__module__]
+    ctl.result_types = host_mod
+    # ... and raises exceptions the host's handlers catch: gateway.py:199/228
+    # (`except InvalidDistribution` / `except NegativeMeasurement` -> HTTP 400),
+    # cli.py:202 (`except GreengateError`)
+    host_pkg = host_mod.__name__.rpartition(".")[0]
+    host_errors = sys.modules.get(host_pkg + ".errors") if host_pkg else None
+    if host_errors is not None:
+        ctl.errors = _bridged_errors(host_errors)
     return ctl
+
+
+_BRIDGED: dict = {}
+
+
+def _bridged_errors(host_errors):
+    """Namespace of exception classes that derive from both the host package's
+    class and ours of the same name (cached per host module)."""
+    key = id(host_errors)
+    ns = _BRIDGED.get(key)
+    if ns is None:
+        import types
+        ns = types.SimpleNamespace()
+        for name in ("InvalidDistribution", "NegativeMeasurement", "InvalidSchedule",
+                     "InvalidLambda"):
+            ours, theirs = getattr(_errors, name), getattr(host_errors, name, None)
+            cls = ours if theirs is None else type(name, (theirs, ours), {
+                "__module__": host_errors.__name__, "__doc__": theirs.__doc__})
+            setattr(ns, name, cls)
+        _BRIDGED[key] = ns
+    return ns
 
 
 def patch_greengate(greengate_module) -> None:

@@ -33,19 +33,32 @@ IMAGENET_STD = (0.229, 0.224, 0.225)
 
 @dataclass
 class OutcomeModel:
-    """Latency/energy of a served batch (servesim.py:303-304 affine model by
-    default; measured_latency=True uses %globaltimer from admission to completion)."""
+    """Latency/energy of a served batch (PathBConfig, servesim.py:62-71, 303-304).
+
+    latency: "model"    base + per_item * n (service time only),
+             "trace"    the reference's finish_t - enqueue_t in trace time:
+                        queueing from arrival to the flush + the service time
+                        (servesim.py:_maybe_flush, _complete),
+             "measured" device %globaltimer from admission to completion.
+    measured_latency=True is the older spelling of latency="measured"."""
 
     batch_base_ms: float = 4.0
     per_item_ms: float = 0.05
     batch_base_energy_j: float = 6.0
     per_item_energy_j: float = 1.5
     measured_latency: bool = False
+    latency: str = "model"
+
+    def mode(self) -> int:
+        if self.measured_latency:
+            return _abi.GG_LATENCY_MEASURED
+        return {"model": _abi.GG_LATENCY_MODEL, "trace": _abi.GG_LATENCY_TRACE,
+                "measured": _abi.GG_LATENCY_MEASURED}[self.latency]
 
     def abi(self) -> _abi.gg_outcome_model:
         return _abi.gg_outcome_model(self.batch_base_ms, self.per_item_ms,
                                      self.batch_base_energy_j, self.per_item_energy_j,
-                                     int(self.measured_latency), 0)
+                                     self.mode(), 0)
 
 
 class GatedServer:
@@ -55,11 +68,22 @@ class GatedServer:
     net:        ResNet18B200 or DistilBertB200 (its max_batch is B)
     scores/now: CUDA fp64 [T, K] / [T] resident trace (this rank's shard)
     payloads:   ResNet: CUDA uint8 [P, H, W, 3]; DistilBERT: (ids int32 [P, S], mask int32 [P, S])
+    open_loop:  the reference's controller-disabled arm (servesim.py:231-240):
+                admit every arrival, static route (gg_admit_open_stream)
+    batching_window_ms: Path-B flush policy (servesim.py:148-162): a batch is
+                popped when B requests are pending or the oldest waited the
+                window in trace time; None pops min(B, depth) every step
+    labels / coins / fallback_degradation: fallback answers and accuracy
+                accounting of every decided request (servesim.py:246-256);
+                labels CUDA int32 [T], coins CUDA fp64 [>= T] (the `_fb_rng`
+                stream, drawn on the host, see fallback_coins)
     """
 
     def __init__(self, controller, net, scores, now, payloads, *, window: int,
                  outcome: OutcomeModel | None = None, fifo_capacity: int = 1 << 20,
-                 rank: int = 0, world: int = 1, process_group=None):
+                 rank: int = 0, world: int = 1, process_group=None, open_loop: bool = False,
+                 batching_window_ms: float | None = None, labels=None, coins=None,
+                 fallback_degradation: float = 0.05):
         torch = _native.require_cuda()
         self.torch = torch
         self.lib = _native.load()
@@ -71,8 +95,24 @@ class GatedServer:
         self.scores, self.now = scores, now
         self.kind = "resnet18" if hasattr(net, "blocks") else "distilbert"
         self.payloads = payloads
-        self.outcome = (outcome or OutcomeModel()).abi()
+        self.outcome_model = outcome or OutcomeModel()
+        self.outcome = self.outcome_model.abi()
         self.rank, self.world, self.pg = rank, world, process_group
+        self.open_loop = bool(open_loop)
+        self.window_s = 0.0 if batching_window_ms is None else float(batching_window_ms) / 1000.0
+        if self.window_s < 0.0:
+            raise ValueError("batching_window_ms must be >= 0")
+        self.trace_clock = batching_window_ms is not None or \
+            self.outcome.measured_latency == _abi.GG_LATENCY_TRACE
+        if (labels is None) != (coins is None):
+            raise ValueError("labels and coins go together (fallback accounting)")
+        if labels is not None:
+            if labels.dtype != torch.int32 or coins.dtype != torch.float64:
+                raise TypeError("labels must be int32 and coins float64 CUDA tensors")
+            if labels.numel() < self.T or coins.numel() < self.T:
+                raise ValueError("labels and coins need one entry per trace row")
+        self.labels, self.coins = labels, coins
+        self.fallback_degradation = float(fallback_degradation)
         assert fifo_capacity & (fifo_capacity - 1) == 0
         z = dict(device=self.dev)
         fifo = _abi.gg_fifo(0, 0, fifo_capacity, self.B, 0, self.T, 0, 0)
@@ -89,6 +129,11 @@ class GatedServer:
         self.decision = torch.full((self.T,), 254, dtype=torch.uint8, **z)
         self.predicted = torch.full((self.T,), -1, dtype=torch.int32, **z)
         self.confidence = torch.full((self.T,), float("nan"), dtype=torch.float64, **z)
+        # reference-semantics record columns (CompletionRecord, servesim.py:99-110)
+        self.answer = torch.full((self.T,), -1, dtype=torch.int32, **z)       # predicted_label
+        self.correct = torch.zeros(self.T, dtype=torch.uint8, **z)
+        self.latency = torch.zeros(self.T, dtype=torch.float64, **z)        # latency_ms
+        self.coin_cursor = torch.zeros(1, dtype=torch.int64, **z)
         self.info = torch.empty(_abi.BATCH_INFO_BYTES, dtype=torch.uint8, **z)
         self.ws = torch.zeros(self.lib.gg_admit_workspace_bytes(self.W), dtype=torch.uint8, **z)
         self.err = torch.empty(1, dtype=torch.int64, **z)
@@ -138,16 +183,35 @@ class GatedServer:
         self._cur_stream = torch.cuda.current_stream(self.dev)
         st = _native.stream_ptr(self._cur_stream)
         ctl = self.ctl
-        _native.check("gg_admit_stream", lib.gg_admit_stream(
-            C.byref(ctl.params), _native.ptr(ctl.state), _native.ptr(self.fifo),
-            _native.ptr(self.ring), _native.ptr(self.ring_ns), _native.ptr(self.scores), self.K,
-            int(self.scores.stride(0)), _native.ptr(self.now), self.W, None,
-            _native.ptr(self.decision), _native.ptr(self.info), _native.ptr(self.ws),
-            self.ws.numel(), st))
-        _native.check("gg_fifo_pop", lib.gg_fifo_pop(
-            _native.ptr(self.fifo), _native.ptr(self.ring), _native.ptr(self.ring_ns),
-            _native.ptr(self.batch_ids), _native.ptr(self.batch_ns), _native.ptr(self.count),
-            self.B, st))
+        if self.open_loop:
+            _native.check("gg_admit_open_stream", lib.gg_admit_open_stream(
+                C.byref(ctl.params), _native.ptr(ctl.state), _native.ptr(self.fifo),
+                _native.ptr(self.ring), _native.ptr(self.ring_ns), self.W,
+                _native.ptr(self.decision), _native.ptr(self.info), st))
+        else:
+            _native.check("gg_admit_stream", lib.gg_admit_stream(
+                C.byref(ctl.params), _native.ptr(ctl.state), _native.ptr(self.fifo),
+                _native.ptr(self.ring), _native.ptr(self.ring_ns), _native.ptr(self.scores), self.K,
+                int(self.scores.stride(0)), _native.ptr(self.now), self.W, None,
+                _native.ptr(self.decision), _native.ptr(self.info), _native.ptr(self.ws),
+                self.ws.numel(), st))
+        if self.labels is not None:
+            _native.check("gg_fallback_answers", lib.gg_fallback_answers(
+                _native.ptr(self.scores), self.K, int(self.scores.stride(0)),
+                _native.ptr(self.labels), _native.ptr(self.decision), _native.ptr(self.fifo),
+                _native.ptr(self.info), 0, 0, _native.ptr(self.coins),
+                _native.ptr(self.coin_cursor), self.fallback_degradation,
+                _native.ptr(self.answer), _native.ptr(self.correct), st))
+        if self.trace_clock:
+            _native.check("gg_fifo_pop_windowed", lib.gg_fifo_pop_windowed(
+                _native.ptr(self.fifo), _native.ptr(self.ring), _native.ptr(self.ring_ns),
+                _native.ptr(self.now), self.window_s, _native.ptr(self.batch_ids),
+                _native.ptr(self.batch_ns), _native.ptr(self.count), self.B, st))
+        else:
+            _native.check("gg_fifo_pop", lib.gg_fifo_pop(
+                _native.ptr(self.fifo), _native.ptr(self.ring), _native.ptr(self.ring_ns),
+                _native.ptr(self.batch_ids), _native.ptr(self.batch_ns), _native.ptr(self.count),
+                self.B, st))
         logits = self._forward(st)
         _native.check("gg_epilogue_served", lib.gg_epilogue_served(
             C.c_void_p(logits.data_ptr()), _native.ptr(self.count), self.B, int(logits.shape[1]),
@@ -157,9 +221,10 @@ class GatedServer:
         if self.world > 1:
             self.slots.zero_()
         my_slot = self.slots[self.rank * self.slot_len:]
-        _native.check("gg_served_outcomes", lib.gg_served_outcomes(
+        _native.check("gg_served_outcomes_trace", lib.gg_served_outcomes_trace(
             _native.ptr(self.fifo), _native.ptr(self.count), _native.ptr(self.batch_ns),
-            C.byref(self.outcome), _native.ptr(self.info), _native.ptr(my_slot), self.B, st))
+            _native.ptr(self.batch_ids), _native.ptr(self.now), C.byref(self.outcome),
+            _native.ptr(self.info), _native.ptr(my_slot), self.B, _native.ptr(self.latency), st))
 
     def step_feedback(self):
         """K2 over every rank's slot (after the exchange)."""
@@ -228,9 +293,52 @@ class GatedServer:
         st = self.ctl.state_struct()
         return {"decided": int(f.cursor), "admitted": int(f.tail), "served": int(f.head),
                 "queue_depth": int(f.tail - f.head), "overflow": int(f.overflow),
+                "clock": f.clock,
                 "admitted_total": int(st.admitted_total), "skipped_total": int(st.skipped_total),
                 "outcomes_total": int(st.outcomes_total), "ewma_joules": st.ewma_joules_per_request,
                 "p95_ms": st.p95_current}
+
+
+    def summary(self, label: str = "run", grid_intensity: float = 0.5) -> dict:
+        """The reference's SummaryRow (telemetry.py:87-128) over the decided rows:
+        skipped requests complete at arrival through the fallback (latency 0,
+        zero joules); admitted ones carry their served latency; accuracy from the
+        fallback accounting (needs labels/coins); makespan in trace time.  Energy
+        is the modeled ledger total (EnergyLedger.total_joules)."""
+        import math
+        import numpy as np
+        f = self.fifo_state()
+        n = int(f.cursor)
+        if n == 0:
+            raise ValueError("empty trace")
+        dec = self.decision[:n].cpu().numpy()
+        lat = self.latency[:n].cpu().numpy()
+        arr = self.now[:n].cpu().numpy()
+        adm = (dec == _abi.GG_DECISION_DIRECT) | (dec == _abi.GG_DECISION_BATCHED)
+        served = self.predicted[:n].cpu().numpy() >= 0
+        lat = np.where(adm, lat, 0.0)
+        finish = arr + lat / 1000.0
+        mean = float(sum(lat.tolist()) / n)
+        var = float(sum((x - mean) ** 2 for x in lat.tolist()) / n)
+        makespan = float(finish.max() - arr.min())
+        st = self.ctl.state_struct()
+        joules = float(st.total_joules)
+        kwh = joules / 3.6e6
+        correct = int(self.correct[:n].sum().item()) if self.labels is not None else None
+        return {"label": label, "avg_latency_ms": mean, "std_latency_ms": math.sqrt(var),
+                "throughput_rps": n / makespan if makespan > 0 else math.inf,
+                "total_time_s": makespan, "energy_kwh": kwh, "co2_kg": kwh * grid_intensity,
+                "admitted_count": int(adm.sum()), "skipped_count": int(n - adm.sum()),
+                "served_count": int(served.sum()),
+                "accuracy": None if correct is None else correct / n}
+
+
+def fallback_coins(seed: int, n: int):
+    """The simulator's fallback coin stream (servesim.py:177-180, 254): the third
+    child of SeedSequence(seed), one U[0, 1) draw per coin, host-side numpy."""
+    import numpy as np
+    rng = np.random.default_rng(np.random.SeedSequence(seed).spawn(3)[2])
+    return rng.random(n)
 
 
 def synthetic_images(n: int, image: int = 224, seed: int = 0, device="cuda"):

@@ -60,6 +60,10 @@ def sequential_gateway(reqs):
     depth = 0
     out = []
     for kind, b in reqs:
+        if kind == "reset":
+            ctl.reset_clock(b["t_origin"])
+            out.append(None)
+            continue
         if kind == "decide":
             if "queue_depth" in b:
                 depth = b["queue_depth"]
@@ -122,7 +126,9 @@ class OracleBackedController:
 
 
 def _run_batched(gw, reqs):
-    futs = [gw.submit_decide(b) if kind == "decide" else gw.submit_outcome(b) for kind, b in reqs]
+    sub = {"decide": gw.submit_decide, "outcome": gw.submit_outcome,
+           "reset": lambda b: gw.submit_reset()}
+    futs = [sub[kind](b) for kind, b in reqs]
     out = []
     for f in futs:
         try:
@@ -256,3 +262,29 @@ def test_batcher_concurrent_clients_cpu():
         assert answers[b["id"]] == w, (kind, b["id"])
     assert fake.o.state_tuple() == octl.state_tuple()
     assert len(fake.calls) < len(reqs)   # requests were coalesced
+
+
+def test_batcher_reset_in_request_order_cpu():
+    """POST /v1/reset is applied by the worker in enqueue order: decides queued
+    before it see the old clock origin, decides after it the new one; the
+    recorded order replays through the sequential gateway; a closed gateway
+    answers 503 instead of blocking."""
+    import itertools
+    from paper_2601_04250_b200.gateway import ApiError, GatewayBatcher
+    reqs = _requests(seed=5, n=200)
+    reqs = reqs[:60] + [("reset", {})] + reqs[60:140] + [("reset", {})] + reqs[140:]
+    ticks = itertools.count(1)
+    fake = OracleBackedController()
+    with GatewayBatcher(None, controller=fake, max_batch=len(reqs), max_wait_s=30.0,
+                        clock=lambda: 0.5 * next(ticks), record_order=True) as gw:
+        got = _run_batched(gw, reqs)
+        order = list(gw.order)
+    want, octl = sequential_gateway(order)
+    assert [k for k, _ in order].count("reset") == 2
+    assert got == want
+    assert fake.o.state_tuple() == octl.state_tuple()
+    for call in (gw.flush, gw.reset, lambda: gw.decide({"id": "a", "scores": [0.5, 0.5]}),
+                 lambda: gw.outcome({"id": "a", "latency_ms": 1.0, "joules": 1.0, "queue_depth": 0})):
+        with pytest.raises(ApiError) as e:
+            call()
+        assert e.value.status == 503

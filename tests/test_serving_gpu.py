@@ -82,3 +82,84 @@ def test_serving_loop_vs_oracle(kind, k, B, window, graph):
     assert got == want
     conf = srv.confidence.cpu().numpy()[pred >= 0]
     assert ((conf > 0) & (conf <= 1)).all()
+
+
+def _labels(n, k, seed):
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, k, size=n).astype(np.int32)
+
+
+@pytest.mark.parametrize("kind,k,B,window,open_loop,win_ms,latency,routing", [
+    ("distilbert", 2, 16, 40, False, 6.0, "trace", 1),     # Path-B flush + queueing latency
+    ("distilbert", 2, 16, 40, True, 6.0, "trace", 2),      # open-loop arm, THRESHOLD_ON_QUEUE
+    ("distilbert", 2, 16, 24, True, None, "model", 0),     # open-loop, size trigger only
+    ("resnet18", 1000, 8, 12, False, 4.0, "trace", 2),
+    ("resnet18", 1000, 8, 12, True, 4.0, "model", 1),
+])
+def test_serving_policies_vs_oracle(kind, k, B, window, open_loop, win_ms, latency, routing):
+    """Open-loop arm (servesim.py:231-240), Path-B flush policy (148-162), trace-time
+    latency (finish - enqueue) and the fallback answers / accuracy accounting
+    (246-256) on the device loop == the host replay, row for row, and the final
+    controller state byte-equal."""
+    import torch
+    import paper_2601_04250_b200 as gg
+    from paper_2601_04250_b200 import serving
+    n = 500 if kind == "distilbert" else 200
+    scores, now = make_trace(n, k, seed=k + 3)
+    labels = _labels(n, k, seed=9)
+    coins = serving.fallback_coins(123, n)
+    deg = 0.2
+    cfg_kw = dict(alpha=1.0, beta=-0.2, gamma=-0.4, tau0=0.8, tau_inf=0.35, k=1.5,
+                  routing=[gg.RoutePolicy.ALL_DIRECT, gg.RoutePolicy.ALL_BATCHED,
+                           gg.RoutePolicy.THRESHOLD_ON_QUEUE][routing], queue_threshold=6)
+    ctl = gg.ControllerConfig(**cfg_kw).build(gg.EnergyLedger())
+    if kind == "resnet18":
+        from paper_2601_04250_b200.resnet18 import ResNet18B200, random_model
+        net = ResNet18B200(random_model(0), max_batch=B)
+        payloads = serving.synthetic_images(32)
+    else:
+        from paper_2601_04250_b200.distilbert import DistilBertB200, random_model
+        net = DistilBertB200(random_model(0), max_batch=B)
+        payloads = serving.synthetic_tokens(32)
+    srv = serving.GatedServer(
+        ctl, net, torch.from_numpy(scores).cuda(), torch.from_numpy(now).cuda(), payloads,
+        window=window, outcome=serving.OutcomeModel(**MODEL, latency=latency), fifo_capacity=4096,
+        open_loop=open_loop, batching_window_ms=win_ms, labels=torch.from_numpy(labels).cuda(),
+        coins=torch.from_numpy(coins).cuda(), fallback_degradation=deg)
+    srv.run(1)
+    srv.capture()
+    steps = 1
+    while not srv.done():
+        srv.run(1)
+        steps += 1
+        assert steps < 10_000
+    torch.cuda.synchronize()
+    p = G.abi_params(dict(alpha=1.0, beta=-0.2, gamma=-0.4, tau0=0.8, tau_inf=0.35, k=1.5,
+                          ewma_lambda=0.9, direction=0, utility_proxy=0, routing=routing,
+                          queue_threshold=6, p95_window=100))
+    rec = {}
+    dec_o, served_o, st_o = serving_oracle.replay(
+        p, [(scores, now)], window, B, MODEL, steps, open_loop=open_loop,
+        window_s=None if win_ms is None else win_ms / 1000.0, latency=latency, labels=[labels],
+        coins=[coins], degradation=deg, records=rec)
+    dec = srv.decision.cpu().numpy()
+    assert np.array_equal(dec, dec_o[0])
+    if open_loop:
+        assert (dec != 0).all()                       # admit everything
+    cols = rec["columns"][0]
+    assert np.array_equal(srv.answer.cpu().numpy(), cols["answer"])
+    assert np.array_equal(srv.correct.cpu().numpy(), cols["correct"])
+    assert int(srv.coin_cursor.item()) == rec["coin_cursor"][0]
+    assert np.array_equal(srv.latency.cpu().numpy(), cols["latency"])   # bit-exact fp64
+    pred = srv.predicted.cpu().numpy()
+    assert set(np.nonzero(pred >= 0)[0]) == set(served_o[0])
+    r = srv.results()
+    assert r["overflow"] == 0 and r["served"] == len(served_o[0]) and r["clock"] == rec["clock"][0]
+    st = srv.ctl.state_struct()
+    assert G.state_dict_of_abi(st) == G.state_dict_of_abi(st_o)
+    assert (st.outcomes_total, st.win_count, st.queue_depth) == \
+        (st_o.outcomes_total, st_o.win_count, st_o.queue_depth)
+    if open_loop:
+        assert r["served"] == n
+    s = srv.summary()
+    assert s["admitted_count"] + s["skipped_count"] == n and 0.0 <= s["accuracy"] <= 1.0
