@@ -178,7 +178,7 @@ def build_net(name: str, B: int):
 
 
 def make_server(wl, kind, net, scores, now, labels, payloads, dev, *, rank=0, world=1, pg=None,
-                open_loop=False, coin_seed=0):
+                open_loop=False, coin_seed=0, window=None):
     import torch
     import paper_2601_04250_b200 as gg
     from paper_2601_04250_b200 import serving
@@ -187,7 +187,7 @@ def make_server(wl, kind, net, scores, now, labels, payloads, dev, *, rank=0, wo
     T = int(scores.shape[0])
     coins = torch.from_numpy(serving.fallback_coins(coin_seed, T)).to(dev)
     return serving.GatedServer(
-        ctl, net, scores, now, payloads, window=wl["window"],
+        ctl, net, scores, now, payloads, window=window or wl["window"],
         outcome=serving.OutcomeModel(**wl["outcome"], latency="trace"), rank=rank, world=world,
         process_group=pg, open_loop=open_loop, batching_window_ms=wl["batching_window_ms"],
         labels=labels, coins=coins, fallback_degradation=wl["fallback_degradation"])
@@ -599,7 +599,10 @@ def c4_trace():
 def run_ablation(dev, nets) -> dict:
     """Both arms on the identical C4 trace; per arm the device wall time (CUDA
     events) to serve every request of both sub-traces, and the reference's
-    summary figures (telemetry.py:87-145 semantics) over all 10,147 requests."""
+    summary figures (telemetry.py:87-145 semantics) over all 10,147 requests.
+    Each step decides B arrivals (window = forward batch), so the open-loop arm
+    never queues beyond one batch: the arms differ only by what the controller
+    keeps off the GPU.  The two models' loops run on two streams."""
     import torch
     total, parts = c4_trace()
     res = {}
@@ -610,7 +613,7 @@ def run_ablation(dev, nets) -> dict:
             srv = make_server(wl, kind, nets[kind], torch.from_numpy(sc).to(dev),
                               torch.from_numpy(nw).to(dev), torch.from_numpy(lb).to(dev),
                               payload_pool(kind, 256, 7, dev), dev, open_loop=open_loop,
-                              coin_seed=11 if kind == "distilbert" else 12)
+                              coin_seed=11 if kind == "distilbert" else 12, window=wl["batch"])
             srv.run(1)          # eager warm step (allocations), then one graph per server
             srv.capture()
             srvs.append(srv)
@@ -652,7 +655,8 @@ def run_ablation(dev, nets) -> dict:
     def pct(x, y):
         return round((x - y) / y * 100.0, 3) if y else None
     return {"trace": f"C4: ONOFF 800/50 rps, phase 0.5 s, 25 s, {total} arrivals, DistilBERT/ResNet-18 "
-                     "by a seeded coin, Path-B 10 ms window, trace-time latency",
+                     "by a seeded coin, B arrivals decided per step, Path-B 10 ms window, "
+                     "trace-time latency",
             "arms": res,
             "device_wall_time_delta_pct": pct(c["device_wall_ms"], o["device_wall_ms"]),
             "trace_makespan_delta_pct": pct(c["trace_makespan_s"], o["trace_makespan_s"]),
