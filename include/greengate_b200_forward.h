@@ -180,6 +180,14 @@ int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, v
  * a zero-bordered input passes its interior pixel count); C % 64 == 0. */
 int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y, int32_t denom,
                const int32_t* count_dev, void* stream);
+/* ResNet head in fp32: global average pool of the bf16 NHWC map into
+ * pooled [N, C] fp32 (no bf16 rounding), then logits [N, ld_logits] fp32 =
+ * pooled . w_fc^T + b_fc with fp32 weights [ncls, C] (torchvision's avgpool +
+ * fc, fp32 end to end).  Rows past *count_dev are untouched.  C % 64 == 0,
+ * C <= 1536. */
+int gg_avgpool_fc(const void* x, int32_t N, int32_t HW, int32_t C, int32_t denom,
+                  const float* w_fc, const float* b_fc, int32_t ncls, float* pooled,
+                  float* logits, int64_t ld_logits, const int32_t* count_dev, void* stream);
 
 #ifdef __cplusplus
 }

@@ -61,6 +61,7 @@ SIGNATURES: dict[str, tuple] = {
     "gg_stem_gather": (C.c_int, [_P, _I64, _P, _P, _I32, _I32, _I32, _P, _P, _I32, _P, _P]),
     "gg_maxpool3x3s2": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P]),
     "gg_avgpool": (C.c_int, [_P, _I32, _I32, _I32, _P, _I32, _P, _P]),
+    "gg_avgpool_fc": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _I32, _P, _P, _I64, _P, _P]),
     # serving loop (include/greengate_b200.h)
     "gg_admit_stream": (C.c_int, [_P, _P, _P, _P, _P, _P, _I32, _I64, _P, _I64, _P, _P, _P, _P,
                                   C.c_size_t, _P]),

@@ -19,6 +19,7 @@
 #include "gg_kernels.h"
 #include "gg_streamk.cuh"
 #include "gg_tc.cuh"
+#include "gg_act.cuh"
 
 namespace gg {
 using namespace tc;
@@ -35,14 +36,14 @@ struct ConvShape {
 };
 
 struct ConvEpi {
-  __nv_bfloat16* y;               // [M, Cout]
+  act_t* y;               // [M, Cout]
   const float* bias;              // [Cout]
-  const __nv_bfloat16* residual;  // [M, Cout] or null
+  const act_t* residual;  // [M, Cout] or null
   int relu;
   const int32_t* count;           // device image count (dynamic batch) or null
   int out_pad;                    // 1: y (and residual) are [N, Ho+2, Wo+2, Cout] zero-bordered
   StreamK sk;                     // stream-K split (TMA im2col mode only), or disabled
-  __nv_bfloat16* y_ds;            // DS: the fused 1x1 / stride-2 downsample output (no ReLU)
+  act_t* y_ds;            // DS: the fused 1x1 / stride-2 downsample output (no ReLU)
   const float* bias_ds;           // DS: its folded-BN bias
 };
 
@@ -91,7 +92,7 @@ __device__ __forceinline__ void cp_async_wait() {
 //   of a separate kernel re-loading the input.
 template <int BN, int STAGES, int MODE, bool DS = false>
 __global__ void __launch_bounds__(kConvThreadsMax, 1)
-    conv_bf16_tcgen05(const __nv_bfloat16* __restrict__ x, const __grid_constant__ CUtensorMap map_w,
+    conv_bf16_tcgen05(const act_t* __restrict__ x, const __grid_constant__ CUtensorMap map_w,
                       const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_wds,
                       ConvShape sh, ConvEpi ep) {
   static_assert(!DS || (MODE == 1 && 4 * BN <= 512), "DS: TMA im2col, two double-buffered accumulators");
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
         wo = rem - ho * sh.Wo;
       }
       const int hi0 = ho * sh.stride - sh.pad, wi0 = wo * sh.stride - sh.pad;
-      const __nv_bfloat16* xn = x + (int64_t)n * sh.H * sh.W * sh.C;
+      const act_t* xn = x + (int64_t)n * sh.H * sh.W * sh.C;
       for (int kb = 0; kb < num_kb; ++kb, ++it) {
         const int s = it % STAGES;
         const uint32_t round = it / STAGES;
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
           const int rr = tap / sh.S, ss = tap - rr * sh.S;
           const int hi = hi0 + rr, wi = wi0 + ss;
           const bool ok = m_ok && tap < sh.R * sh.S && hi >= 0 && hi < sh.H && wi >= 0 && wi < sh.W;
-          const __nv_bfloat16* src = ok ? xn + ((int64_t)hi * sh.W + wi) * sh.C + c0 : x;
+          const act_t* src = ok ? xn + ((int64_t)hi * sh.W + wi) * sh.C + c0 : x;
           cp_async_16(sa + ((j ^ sw) << 4), src, ok);
         }
         cp_async_commit();
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
       // that.  Stage index / phase advance incrementally (no runtime % and /), the
       // operand descriptors are base + constant offsets (the 14-bit start-address
       // field never carries: smem < 256 KB), the centre-tap range is precomputed.
-      constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+      constexpr uint32_t idesc = idesc_act_f32(128, BN);
       int t = 0, s = 0, dsl = 0;
       uint32_t ph = 0, dph = 0;
       if (b_loaded) mbar_wait(b_full, 0);   // also when the count leaves no tile: drain
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
         // DS: columns [BN, 2 BN) of the buffer are the downsample accumulator
         const bool dsp = DS && cc >= BN;
         const int c = dsp ? cc - BN : cc;
-        __nv_bfloat16* yout = dsp ? ep.y_ds : ep.y;
+        act_t* yout = dsp ? ep.y_ds : ep.y;
         const float* bvec = dsp ? ep.bias_ds : ep.bias;
         uint32_t r[32];
         tmem_ld_32x32b_x32(tacc + cc, r);
@@ -412,10 +413,10 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const uint4 u = __ldg(rp + q);
-            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+            const act2_t* h2 = reinterpret_cast<const act2_t*>(&u);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(h2[e]);
+              const float2 f = act2_to_float2(h2[e]);
               v[q * 8 + 2 * e] += f.x;
               v[q * 8 + 2 * e + 1] += f.y;
             }
@@ -429,10 +430,10 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint4 u;
-          u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-          u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-          u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-          u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+          u.x = pack_act(v[q * 8 + 0], v[q * 8 + 1]);
+          u.y = pack_act(v[q * 8 + 2], v[q * 8 + 3]);
+          u.z = pack_act(v[q * 8 + 4], v[q * 8 + 5]);
+          u.w = pack_act(v[q * 8 + 6], v[q * 8 + 7]);
           dp[q] = u;
         }
       }
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
 }
 
 template <int BN, int STAGES, int MODE, bool DS = false>
-static int launch_conv(const __nv_bfloat16* x, const CUtensorMap& mw, const CUtensorMap& mx,
+static int launch_conv(const act_t* x, const CUtensorMap& mw, const CUtensorMap& mx,
                        const ConvShape& sh, const ConvEpi& ep, cudaStream_t s,
                        const CUtensorMap* mwds = nullptr) {
   using L = ConvSmem<BN, STAGES, DS>;
@@ -489,7 +490,7 @@ static int make_map_im2col(CUtensorMap* map, const void* x, const ConvShape& sh,
   int lower[2] = {-sh.pad, -sh.pad};
   int upper[2] = {sh.pad_hi - (sh.S - 1), sh.pad_hi - (sh.R - 1)};
   cuuint32_t estr[4] = {1, (cuuint32_t)sh.stride, (cuuint32_t)sh.stride, 1};
-  CUresult r = g_encode_im2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims,
+  CUresult r = g_encode_im2col(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(x), dims,
                                strides, lower, upper, (cuuint32_t)cpb, 128, estr,
                                CU_TENSOR_MAP_INTERLEAVE_NONE,
                                cpb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
@@ -499,25 +500,25 @@ static int make_map_im2col(CUtensorMap* map, const void* x, const ConvShape& sh,
 
 // ---- pooling / layout kernels (HBM-bound) -----------------------------------
 // NCHW fp32 image -> NHWC bf16 with channels zero-padded to cpad.
-__global__ void nchw_to_nhwc_pad(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+__global__ void nchw_to_nhwc_pad(const float* __restrict__ in, act_t* __restrict__ out,
                                  int N, int C, int H, int W, int cpad) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // pixel
   if (p >= (int64_t)N * H * W) return;
   const int n = p / (H * W);
   const int hw = p - (int64_t)n * H * W;
-  __align__(16) __nv_bfloat16 v[8];
+  __align__(16) act_t v[8];
   for (int c0 = 0; c0 < cpad; c0 += 8) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int c = c0 + e;
-      v[e] = __float2bfloat16_rn(c < C ? __ldg(in + ((int64_t)n * C + c) * H * W + hw) : 0.0f);
+      v[e] = float2act(c < C ? __ldg(in + ((int64_t)n * C + c) * H * W + hw) : 0.0f);
     }
     *reinterpret_cast<uint4*>(out + p * cpad + c0) = *reinterpret_cast<uint4*>(v);
   }
 }
 
 // 3x3 stride-2 pad-1 max pool, NHWC, 8 channels per thread.
-__global__ void maxpool3x3s2(const __nv_bfloat16* __restrict__ in, __nv_bfloat16* __restrict__ out,
+__global__ void maxpool3x3s2(const act_t* __restrict__ in, act_t* __restrict__ out,
                              int N, int H, int W, int C, int Ho, int Wo, const int32_t* count,
                              int out_pad) {
   griddep_wait();
@@ -539,20 +540,20 @@ __global__ void maxpool3x3s2(const __nv_bfloat16* __restrict__ in, __nv_bfloat16
       const int wi = wo * 2 - 1 + s;
       if (wi < 0 || wi >= W) continue;
       const uint4 u = __ldg(reinterpret_cast<const uint4*>(in + (((int64_t)n * H + hi) * W + wi) * C + c0));
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+      const act2_t* h2 = reinterpret_cast<const act2_t*>(&u);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h2[e]);
+        const float2 f = act2_to_float2(h2[e]);
         m[2 * e] = fmaxf(m[2 * e], f.x);
         m[2 * e + 1] = fmaxf(m[2 * e + 1], f.y);
       }
     }
   }
   uint4 u;
-  u.x = pack_bf16(m[0], m[1]);
-  u.y = pack_bf16(m[2], m[3]);
-  u.z = pack_bf16(m[4], m[5]);
-  u.w = pack_bf16(m[6], m[7]);
+  u.x = pack_act(m[0], m[1]);
+  u.y = pack_act(m[2], m[3]);
+  u.z = pack_act(m[4], m[5]);
+  u.w = pack_act(m[6], m[7]);
   const int64_t o = out_pad ? ((int64_t)n * (Ho + 2) + ho + 1) * (Wo + 2) + wo + 1 : p;
   *reinterpret_cast<uint4*>(out + o * C + c0) = u;
 }
@@ -563,8 +564,8 @@ __global__ void maxpool3x3s2(const __nv_bfloat16* __restrict__ in, __nv_bfloat16
 // a warp: 8 channel groups x 4 column pairs, so every load instruction touches
 // four 128-byte pixel rows.
 constexpr int kPoolRows = 4, kPoolCols = 2;
-__global__ void __launch_bounds__(256) maxpool3x3s2_blocked(const __nv_bfloat16* __restrict__ in,
-                                                            __nv_bfloat16* __restrict__ out, int N,
+__global__ void __launch_bounds__(256) maxpool3x3s2_blocked(const act_t* __restrict__ in,
+                                                            act_t* __restrict__ out, int N,
                                                             int H, int W, int C, int Ho, int Wo,
                                                             const int32_t* count, int out_pad) {
   griddep_wait();
@@ -581,15 +582,15 @@ __global__ void __launch_bounds__(256) maxpool3x3s2_blocked(const __nv_bfloat16*
   const int bh = (int)(idx % hb);
   const int n = (int)(idx / hb);
   const int ho0 = bh * kPoolRows, wo0 = bw * kPoolCols;
-  const __nv_bfloat162 ninf = __float2bfloat162_rn(-INFINITY);
-  __nv_bfloat162 m[kPoolRows][kPoolCols][4];
+  const act2_t ninf = float2act2(-INFINITY);
+  act2_t m[kPoolRows][kPoolCols][4];
 #pragma unroll
   for (int i = 0; i < kPoolRows; ++i)
 #pragma unroll
     for (int j = 0; j < kPoolCols; ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) m[i][j][e] = ninf;
-  const __nv_bfloat16* img = in + (int64_t)n * H * W * C + c0;
+  const act_t* img = in + (int64_t)n * H * W * C + c0;
   const uint64_t pol = l2_policy_evict_first();   // single-use input (kept in L2 by the stem)
 #pragma unroll
   for (int r = 0; r < 2 * kPoolRows + 1; ++r) {
@@ -600,7 +601,7 @@ __global__ void __launch_bounds__(256) maxpool3x3s2_blocked(const __nv_bfloat16*
       const int wi = 2 * wo0 - 1 + q;
       if (wi < 0 || wi >= W) continue;
       const uint4 u = ld_global_nc_v4_hint(img + ((int64_t)hi * W + wi) * C, pol);
-      const __nv_bfloat162* v = reinterpret_cast<const __nv_bfloat162*>(&u);
+      const act2_t* v = reinterpret_cast<const act2_t*>(&u);
       // input row r feeds output rows i with 2i <= r <= 2i + 2; column q feeds j with 2j <= q <= 2j + 2
 #pragma unroll
       for (int i = 0; i < kPoolRows; ++i) {
@@ -634,8 +635,8 @@ __global__ void __launch_bounds__(256) maxpool3x3s2_blocked(const __nv_bfloat16*
 // Global average pool NHWC [N, HW, C] -> [N, C] bf16 (fp32 sum).  Block =
 // (image, 64 channels): warp w owns channels 8w..8w+7 (one 16-byte load per
 // pixel), its lanes stride over the pixels, then a warp reduction.
-__global__ void __launch_bounds__(256) avgpool_global(const __nv_bfloat16* __restrict__ in,
-                                                      __nv_bfloat16* __restrict__ out, int N,
+__global__ void __launch_bounds__(256) avgpool_global(const act_t* __restrict__ in,
+                                                      act_t* __restrict__ out, int N,
                                                       int HW, int C, const int32_t* count,
                                                       int denom) {
   griddep_wait();
@@ -646,13 +647,13 @@ __global__ void __launch_bounds__(256) avgpool_global(const __nv_bfloat16* __res
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = blockIdx.x * 64 + warp * 8;
   float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const __nv_bfloat16* base = in + (int64_t)n * HW * C + c0;
+  const act_t* base = in + (int64_t)n * HW * C + c0;
   for (int p = lane; p < HW; p += 32) {
     const uint4 u = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)p * C));
-    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+    const act2_t* h2 = reinterpret_cast<const act2_t*>(&u);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const float2 f = __bfloat1622float2(h2[e]);
+      const float2 f = act2_to_float2(h2[e]);
       s[2 * e] += f.x;
       s[2 * e + 1] += f.y;
     }
@@ -664,17 +665,129 @@ __global__ void __launch_bounds__(256) avgpool_global(const __nv_bfloat16* __res
   if (lane == 0) {
     const float inv = 1.0f / (denom > 0 ? denom : HW);   // padded input: borders are zeros
     uint4 u;
-    u.x = pack_bf16(s[0] * inv, s[1] * inv);
-    u.y = pack_bf16(s[2] * inv, s[3] * inv);
-    u.z = pack_bf16(s[4] * inv, s[5] * inv);
-    u.w = pack_bf16(s[6] * inv, s[7] * inv);
+    u.x = pack_act(s[0] * inv, s[1] * inv);
+    u.y = pack_act(s[2] * inv, s[3] * inv);
+    u.z = pack_act(s[4] * inv, s[5] * inv);
+    u.w = pack_act(s[6] * inv, s[7] * inv);
     *reinterpret_cast<uint4*>(out + (int64_t)n * C + c0) = u;
+  }
+}
+
+// Global average pool to fp32 [N, C] (same traversal as avgpool_global, no
+// bf16 rounding of the pooled vector: the head stays in fp32).
+__global__ void __launch_bounds__(256) avgpool_global_f32(const act_t* __restrict__ in,
+                                                          float* __restrict__ out, int N, int HW,
+                                                          int C, const int32_t* count, int denom) {
+  griddep_wait();
+  griddep_launch();
+  if (count) N = min(N, __ldg(count));
+  const int n = blockIdx.y;
+  if (n >= N) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * 64 + warp * 8;
+  float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const act_t* base = in + (int64_t)n * HW * C + c0;
+  for (int p = lane; p < HW; p += 32) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)p * C));
+    const act2_t* h2 = reinterpret_cast<const act2_t*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = act2_to_float2(h2[e]);
+      s[2 * e] += f.x;
+      s[2 * e + 1] += f.y;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s[e] += __shfl_xor_sync(0xffffffffu, s[e], o);
+  if (lane == 0) {
+    const float inv = 1.0f / (denom > 0 ? denom : HW);
+    float4* o4 = reinterpret_cast<float4*>(out + (int64_t)n * C + c0);
+    o4[0] = make_float4(s[0] * inv, s[1] * inv, s[2] * inv, s[3] * inv);
+    o4[1] = make_float4(s[4] * inv, s[5] * inv, s[6] * inv, s[7] * inv);
+  }
+}
+
+// fp32 classifier head: logits[n, j] = pooled[n, :] . w[j, :] + b[j] for the
+// first *count images.  Block = 8 classes (their weight rows staged in smem);
+// 4 threads per image split the reduction in interleaved float4 chunks (the
+// four lanes of an image read consecutive 16-byte words: conflict-free), then
+// a 2-step shuffle reduction; each lane stores 2 of the 8 logits.
+constexpr int kFcCls = 8;
+__global__ void __launch_bounds__(256) fc_f32_kernel(const float* __restrict__ pooled,
+                                                     const float* __restrict__ w,
+                                                     const float* __restrict__ b, int N, int C,
+                                                     int ncls, float* __restrict__ logits,
+                                                     int64_t ldl, const int32_t* count) {
+  extern __shared__ __align__(16) float ws[];   // [kFcCls][C]
+  const int j0 = blockIdx.x * kFcCls;
+  const int nc = min(kFcCls, ncls - j0);
+  for (int e = threadIdx.x * 4; e < kFcCls * C; e += blockDim.x * 4) {
+    const int c = e / C;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < nc) v = __ldg(reinterpret_cast<const float4*>(w + (int64_t)(j0 + c) * C + (e - c * C)));
+    *reinterpret_cast<float4*>(ws + e) = v;
+  }
+  griddep_wait();
+  griddep_launch();
+  if (count) N = min(N, __ldg(count));
+  __syncthreads();
+  const int q = threadIdx.x & 3;
+  const int nf = C / 16;   // float4 chunks per lane
+  for (int i = threadIdx.x >> 2; i < N; i += blockDim.x >> 2) {
+    float acc[kFcCls];
+#pragma unroll
+    for (int c = 0; c < kFcCls; ++c) acc[c] = 0.f;
+    const float4* x4 = reinterpret_cast<const float4*>(pooled + (int64_t)i * C);
+    for (int jj = 0; jj < nf; ++jj) {
+      const int f = 4 * jj + q;
+      const float4 x = __ldg(x4 + f);
+#pragma unroll
+      for (int c = 0; c < kFcCls; ++c) {
+        const float4 wv = *reinterpret_cast<const float4*>(ws + c * C + 4 * f);
+        acc[c] = fmaf(x.x, wv.x, acc[c]);
+        acc[c] = fmaf(x.y, wv.y, acc[c]);
+        acc[c] = fmaf(x.z, wv.z, acc[c]);
+        acc[c] = fmaf(x.w, wv.w, acc[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kFcCls; ++c) {
+      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
+      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 2);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = 2 * q + h;
+      if (c < nc) logits[(int64_t)i * ldl + j0 + c] = acc[c] + __ldg(b + j0 + c);
+    }
   }
 }
 
 }  // namespace gg
 
 using namespace gg;
+
+extern "C" int gg_avgpool_fc(const void* x, int32_t N, int32_t HW, int32_t C, int32_t denom,
+                             const float* w_fc, const float* b_fc, int32_t ncls, float* pooled,
+                             float* logits, int64_t ld_logits, const int32_t* count_dev,
+                             void* stream) {
+  if (!x || !w_fc || !b_fc || !pooled || !logits || N < 1 || ncls < 1 || denom < 0 ||
+      ld_logits < ncls)
+    return GG_ERR_INVALID_ARGUMENT;
+  if (C % 64 || N > 65535 || kFcCls * C * 4 > 48 * 1024) return GG_ERR_UNSUPPORTED;
+  if (launch_pdl(avgpool_global_f32, dim3((unsigned)(C / 64), (unsigned)N), dim3(256), 0,
+                 gg_stream(stream), reinterpret_cast<const act_t*>(x), pooled, N, HW, C,
+                 count_dev, denom) != cudaSuccess)
+    return GG_ERR_CUDA;
+  if (launch_pdl(fc_f32_kernel, dim3((unsigned)((ncls + kFcCls - 1) / kFcCls)), dim3(256),
+                 (size_t)kFcCls * C * 4, gg_stream(stream), (const float*)pooled, w_fc, b_fc, N, C,
+                 ncls, logits, ld_logits, count_dev) != cudaSuccess)
+    return GG_ERR_CUDA;
+  GG_LAUNCH_OK();
+  return GG_OK;
+}
 
 extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t C, const void* w,
                          int32_t Cout, int32_t R, int32_t S, int32_t stride, int32_t pad,
@@ -696,8 +809,8 @@ extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t
   const int64_t M = (int64_t)N * sh.Ho * sh.Wo;
   if (M > 0x7fffffff) return GG_ERR_UNSUPPORTED;
   sh.M = (int)M;
-  ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
-             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, out_pad,
+  ConvEpi ep{reinterpret_cast<act_t*>(y), bias,
+             reinterpret_cast<const act_t*>(residual), relu, count_dev, out_pad,
              StreamK{nullptr, nullptr, 0}, nullptr, nullptr};
   // N tile: minimize the larger of (tensor time of the busiest SM) and (operand
   // bytes streamed from L2: every tile re-reads its A rows and its B columns per
@@ -738,7 +851,7 @@ extern "C" int gg_conv2d(const void* x, int32_t N, int32_t H, int32_t W, int32_t
     mx = mw;  // unused by the gather path
   }
   cudaStream_t s = gg_stream(stream);
-  const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(x);
+  const act_t* xb = reinterpret_cast<const act_t*>(x);
   if (mode == 1 && streamk_wanted(tiles_m * (Cout / bn), nkb, num_sms())) {
     bool ok = false;
     StreamK sk = streamk_workspace(s, (int64_t)num_sms() * 2 * 128 * bn,
@@ -785,19 +898,19 @@ extern "C" int gg_conv2d_ds(const void* x, int32_t N, int32_t H, int32_t W, int3
   sh.bres_stages = 0;
   sh.Ho = (H + sh.pad - 3) / 2 + 1;
   sh.Wo = (W + sh.pad - 3) / 2 + 1;
-  if (in_shared) x = reinterpret_cast<const __nv_bfloat16*>(x) + (int64_t)(W + 1) * C;   // past the margin
+  if (in_shared) x = reinterpret_cast<const act_t*>(x) + (int64_t)(W + 1) * C;   // past the margin
   const int64_t M = (int64_t)N * sh.Ho * sh.Wo;
   if (M > 0x7fffffff) return GG_ERR_UNSUPPORTED;
   sh.M = (int)M;
-  ConvEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, 1, count_dev, out_shared ? 2 : 1,
-             StreamK{nullptr, nullptr, 0}, reinterpret_cast<__nv_bfloat16*>(y_ds), bias_ds};
+  ConvEpi ep{reinterpret_cast<act_t*>(y), bias, nullptr, 1, count_dev, out_shared ? 2 : 1,
+             StreamK{nullptr, nullptr, 0}, reinterpret_cast<act_t*>(y_ds), bias_ds};
   constexpr int BN = 128;
   CUtensorMap mw, mwds, mx;
   int rc = make_map_2d(&mw, w, Cout, sh.Kpad, sh.Kpad, BN);
   if (!rc) rc = make_map_2d(&mwds, w_ds, Cout, C, C, BN);
   if (!rc) rc = make_map_im2col(&mx, x, sh, 64);
   if (rc) return rc;
-  return launch_conv<BN, 6, 1, true>(reinterpret_cast<const __nv_bfloat16*>(x), mw, mx, sh, ep,
+  return launch_conv<BN, 6, 1, true>(reinterpret_cast<const act_t*>(x), mw, mx, sh, ep,
                                      gg_stream(stream), &mwds);
 }
 
@@ -806,7 +919,7 @@ extern "C" int gg_nchw_to_nhwc(const float* x, int32_t N, int32_t C, int32_t H, 
   if (!x || !y || cpad % 8 || cpad < C) return GG_ERR_INVALID_ARGUMENT;
   const int64_t pixels = (int64_t)N * H * W;
   nchw_to_nhwc_pad<<<(unsigned)((pixels + 255) / 256), 256, 0, gg_stream(stream)>>>(
-      x, reinterpret_cast<__nv_bfloat16*>(y), N, C, H, W, cpad);
+      x, reinterpret_cast<act_t*>(y), N, C, H, W, cpad);
   GG_LAUNCH_OK();
   return GG_OK;
 }
@@ -818,7 +931,7 @@ extern "C" int gg_maxpool3x3s2(const void* x, int32_t N, int32_t H, int32_t W, i
   const int64_t work = (int64_t)N * ((Ho + kPoolRows - 1) / kPoolRows) *
                        ((Wo + kPoolCols - 1) / kPoolCols) * (C / 8);
   if (launch_pdl(maxpool3x3s2_blocked, dim3((unsigned)((work + 255) / 256)), dim3(256), 0, gg_stream(stream),
-      reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, H, W, C,
+      reinterpret_cast<const act_t*>(x), reinterpret_cast<act_t*>(y), N, H, W, C,
       Ho, Wo, count_dev, out_pad) != cudaSuccess)
     return GG_ERR_CUDA;
   GG_LAUNCH_OK();
@@ -830,7 +943,7 @@ extern "C" int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void*
   if (!x || !y || C % 8 || denom < 0 || N < 1) return GG_ERR_INVALID_ARGUMENT;
   if (C % 64 || N > 65535) return GG_ERR_UNSUPPORTED;
   if (launch_pdl(avgpool_global, dim3((unsigned)(C / 64), (unsigned)N), dim3(256), 0, gg_stream(stream),
-      reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<__nv_bfloat16*>(y), N, HW, C,
+      reinterpret_cast<const act_t*>(x), reinterpret_cast<act_t*>(y), N, HW, C,
       count_dev, denom) != cudaSuccess)
     return GG_ERR_CUDA;
   GG_LAUNCH_OK();

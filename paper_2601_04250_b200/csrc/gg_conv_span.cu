@@ -41,6 +41,7 @@
 #include "gg_kernels.h"
 #include "gg_streamk.cuh"
 #include "gg_tc.cuh"
+#include "gg_act.cuh"
 
 namespace gg {
 using namespace tc;
@@ -64,13 +65,13 @@ struct SpanShape {
 };
 
 struct SpanEpi {
-  __nv_bfloat16* y;
+  act_t* y;
   const float* bias;
-  const __nv_bfloat16* residual;  // padded, same geometry as y (padded mode), or null
+  const act_t* residual;  // padded, same geometry as y (padded mode), or null
   int relu;
   const int32_t* count;
   unsigned long long* prof;   // debug (GG_SPAN_PROF): per-CTA globaltimer start / end
-  const __nv_bfloat16* x16;   // CH == 16: the pre-swizzled input (bulk-copied)
+  const act_t* x16;   // CH == 16: the pre-swizzled input (bulk-copied)
   int nostore;                // debug (GG_SPAN_NOSTORE): skip the output stores
   int tma_out;                // pair kernel, padded mode: outputs / residuals via smem + TMA
   StreamK sk;                 // pair kernel: stream-K over (pair tile, channel block), or disabled
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     }
   } else if (warp == 1) {
     {   // the whole warp runs the loop; MMA batches / commits go out from one elected lane
-      constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+      constexpr uint32_t idesc = idesc_act_f32(128, BN);
       uint64_t tap_off[TAPS];   // row shift of tap (r, s) in 16-B descriptor units
 #pragma unroll
       for (int tap = 0; tap < TAPS; ++tap)
@@ -380,10 +381,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                   const uint4 u = myrow[q ^ sw];
-                  const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+                  const act2_t* h2 = reinterpret_cast<const act2_t*>(&u);
 #pragma unroll
                   for (int e = 0; e < 4; ++e) {
-                    const float2 f = __bfloat1622float2(h2[e]);
+                    const float2 f = act2_to_float2(h2[e]);
                     v[q * 8 + 2 * e] += f.x;
                     v[q * 8 + 2 * e + 1] += f.y;
                   }
@@ -400,10 +401,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               uint4 u;
-              u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-              u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-              u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-              u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+              u.x = pack_act(v[q * 8 + 0], v[q * 8 + 1]);
+              u.y = pack_act(v[q * 8 + 2], v[q * 8 + 3]);
+              u.z = pack_act(v[q * 8 + 4], v[q * 8 + 5]);
+              u.w = pack_act(v[q * 8 + 6], v[q * 8 + 7]);
               myrow[q ^ sw] = u;
             }
             fence_proxy_async_smem();
@@ -476,10 +477,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
             uint4 outr[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              outr[q].x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-              outr[q].y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-              outr[q].z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-              outr[q].w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+              outr[q].x = pack_act(v[q * 8 + 0], v[q * 8 + 1]);
+              outr[q].y = pack_act(v[q * 8 + 2], v[q * 8 + 3]);
+              outr[q].z = pack_act(v[q * 8 + 4], v[q * 8 + 5]);
+              outr[q].w = pack_act(v[q * 8 + 6], v[q * 8 + 7]);
             }
             // the stem output (103 MB at batch 64) is read once by the max pool right
             // after: keep it in L2 (evict_last); the pool reads it evict_first
@@ -500,10 +501,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
             if (use_res) {
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&res[q]);
+                const act2_t* h2 = reinterpret_cast<const act2_t*>(&res[q]);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  const float2 f = __bfloat1622float2(h2[e]);
+                  const float2 f = act2_to_float2(h2[e]);
                   v[q * 8 + 2 * e] += f.x;
                   v[q * 8 + 2 * e + 1] += f.y;
                 }
@@ -522,10 +523,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint4 u;
-            u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-            u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-            u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-            u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+            u.x = pack_act(v[q * 8 + 0], v[q * 8 + 1]);
+            u.y = pack_act(v[q * 8 + 2], v[q * 8 + 3]);
+            u.z = pack_act(v[q * 8 + 4], v[q * 8 + 5]);
+            u.w = pack_act(v[q * 8 + 6], v[q * 8 + 7]);
             dp[q] = u;
           }
         }
@@ -563,7 +564,7 @@ static int make_map_span(CUtensorMap* map, const void* ptr, int64_t rows, int64_
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
   cuuint32_t box[2] = {(cuuint32_t)ch, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    preswizzled ? CU_TENSOR_MAP_SWIZZLE_NONE
                    : ch == 64  ? CU_TENSOR_MAP_SWIZZLE_128B
@@ -588,7 +589,7 @@ static int make_map_box32(CUtensorMap* map, const void* ptr, int64_t rows, int64
   cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
   cuuint32_t box[2] = {32, 32};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? GG_OK : GG_ERR_INVALID_ARGUMENT;
@@ -805,7 +806,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
     }
   } else if (warp == 1) {
     if (rank == 0) {   // leader: the warp runs the loop, one elected lane issues
-      constexpr uint32_t idesc = idesc_bf16_f32(256, BN);
+      constexpr uint32_t idesc = idesc_act_f32(256, BN);
       uint64_t tap_off[TAPS];
 #pragma unroll
       for (int tap = 0; tap < TAPS; ++tap) tap_off[tap] = (uint64_t)(((tap / RT) * sh.Wp + tap % RT) * (RB / 16));
@@ -1022,10 +1023,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const uint4 u = myrow[q ^ sw];
-                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+                const act2_t* h2 = reinterpret_cast<const act2_t*>(&u);
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  const float2 f = __bfloat1622float2(h2[e]);
+                  const float2 f = act2_to_float2(h2[e]);
                   v[q * 8 + 2 * e] += f.x;
                   v[q * 8 + 2 * e + 1] += f.y;
                 }
@@ -1042,10 +1043,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint4 u;
-            u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-            u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-            u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-            u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+            u.x = pack_act(v[q * 8 + 0], v[q * 8 + 1]);
+            u.y = pack_act(v[q * 8 + 2], v[q * 8 + 3]);
+            u.z = pack_act(v[q * 8 + 4], v[q * 8 + 5]);
+            u.w = pack_act(v[q * 8 + 6], v[q * 8 + 7]);
             myrow[q ^ sw] = u;
           }
           fence_proxy_async_smem();
@@ -1104,10 +1105,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
           if (use_res) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&res[q]);
+              const act2_t* h2 = reinterpret_cast<const act2_t*>(&res[q]);
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h2[e]);
+                const float2 f = act2_to_float2(h2[e]);
                 v[q * 8 + 2 * e] += f.x;
                 v[q * 8 + 2 * e + 1] += f.y;
               }
@@ -1125,10 +1126,10 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint4 u;
-          u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-          u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-          u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-          u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+          u.x = pack_act(v[q * 8 + 0], v[q * 8 + 1]);
+          u.y = pack_act(v[q * 8 + 2], v[q * 8 + 3]);
+          u.z = pack_act(v[q * 8 + 4], v[q * 8 + 5]);
+          u.w = pack_act(v[q * 8 + 6], v[q * 8 + 7]);
           dp[q] = u;
         }
       }
@@ -1252,7 +1253,7 @@ constexpr int kStemBSlab = 128 * 32;           // one shift's B: 128 rows x 16 c
 struct StemTile { int n, h; bool pre; };
 
 __device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {   // packed bf16x2 max (exact)
-  __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+  act2_t r = __hmax2(*reinterpret_cast<act2_t*>(&a), *reinterpret_cast<act2_t*>(&b));
   return *reinterpret_cast<uint32_t*>(&r);
 }
 
@@ -1268,8 +1269,8 @@ __device__ __forceinline__ StemTile stem_tile(int i, int g0, int pre, int Ho) {
 
 __global__ void __launch_bounds__(kSpanThreads, 1)
     stem_pool_span(const __grid_constant__ CUtensorMap map_w, StemPoolShape sh,
-                   const __nv_bfloat16* __restrict__ x16, const float* __restrict__ bias,
-                   __nv_bfloat16* __restrict__ y, const int32_t* count) {
+                   const act_t* __restrict__ x16, const float* __restrict__ bias,
+                   act_t* __restrict__ y, const int32_t* count) {
   constexpr int RB = 32, NACC = 4, ACC_COLS = 128;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1351,7 +1352,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16_f32(128, ACC_COLS);
+    constexpr uint32_t idesc = idesc_act_f32(128, ACC_COLS);
     uint64_t sh_off[kStemShifts];
 #pragma unroll
     for (int j = 0; j < kStemShifts; ++j) sh_off[j] = (uint64_t)(((j >> 2) * sh.Wp + (j & 3)) * (RB / 16));
@@ -1414,9 +1415,9 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       uint32_t vm[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const uint32_t a0 = pack_bf16(fmaxf(__uint_as_float(r0[2 * e]) + bz[2 * e], 0.0f),
+        const uint32_t a0 = pack_act(fmaxf(__uint_as_float(r0[2 * e]) + bz[2 * e], 0.0f),
                                       fmaxf(__uint_as_float(r0[2 * e + 1]) + bz[2 * e + 1], 0.0f));
-        const uint32_t a1 = pack_bf16(fmaxf(__uint_as_float(r1[2 * e]) + bz[2 * e], 0.0f),
+        const uint32_t a1 = pack_act(fmaxf(__uint_as_float(r1[2 * e]) + bz[2 * e], 0.0f),
                                       fmaxf(__uint_as_float(r1[2 * e + 1]) + bz[2 * e + 1], 0.0f));
         uint32_t v = bmax2(a0, a1);
         if (t.h != 0) v = bmax2(v, part[e]);   // no stem row above row 0
@@ -1510,8 +1511,8 @@ static int conv3x3_span(const void* x, int32_t N, int32_t H, int32_t W, int32_t 
       if (!rc && tma_epi) rc = make_map_box32(&mo, y, Mtot, Cout);
       if (!rc && tma_epi && residual) rc = make_map_box32(&mr, residual, Mtot, Cout);
       if (rc) return rc;
-      SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
-                 reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0,
+      SpanEpi ep{reinterpret_cast<act_t*>(y), bias,
+                 reinterpret_cast<const act_t*>(residual), relu, count_dev, nullptr, nullptr, 0,
                  tma_epi ? 1 : 0, StreamK{nullptr, nullptr, 0}};
       cudaStream_t s = gg_stream(stream);
       // stream-K over (pair tile, channel block) for pair tiles that leave the last
@@ -1582,8 +1583,8 @@ static int conv3x3_span(const void* x, int32_t N, int32_t H, int32_t W, int32_t 
   if (!rc && tma1) rc = make_map_box32(&mo, y, Mtot, Cout);
   if (!rc && tma1 && residual) rc = make_map_box32(&mr, residual, Mtot, Cout);
   if (rc) return rc;
-  SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias,
-             reinterpret_cast<const __nv_bfloat16*>(residual), relu, count_dev, nullptr, nullptr, 0,
+  SpanEpi ep{reinterpret_cast<act_t*>(y), bias,
+             reinterpret_cast<const act_t*>(residual), relu, count_dev, nullptr, nullptr, 0,
              tma1 ? 1 : 0, StreamK{nullptr, nullptr, 0}};
   cudaStream_t s = gg_stream(stream);
   const CUtensorMap* po = tma1 ? &mo : nullptr;
@@ -1628,8 +1629,8 @@ extern "C" int gg_stem_s2d_span(const void* x, int32_t N, int32_t Hs, int32_t Ws
   int rc = make_map_span(&mx, x, Mtot, 16, 16, sh.box_rows);
   if (!rc) rc = make_map_span(&mw, w, Cout, 256, 16, 64);
   if (rc) return rc;
-  SpanEpi ep{reinterpret_cast<__nv_bfloat16*>(y), bias, nullptr, relu, count_dev, nullptr,
-             reinterpret_cast<const __nv_bfloat16*>(x), 0, 0, StreamK{nullptr, nullptr, 0}};
+  SpanEpi ep{reinterpret_cast<act_t*>(y), bias, nullptr, relu, count_dev, nullptr,
+             reinterpret_cast<const act_t*>(x), 0, 0, StreamK{nullptr, nullptr, 0}};
   if (reinterpret_cast<uintptr_t>(x) & 15) return GG_ERR_INVALID_ARGUMENT;
   // CTA-pair stem: correct but measured 94 us vs 59 us for single-CTA tiles
   // (N = 64 pair MMAs); GG_SPAN_PAIR64=1 opts in
@@ -1680,7 +1681,7 @@ extern "C" int gg_stem_pool_span(const void* x, int32_t N, int32_t Hs, int32_t W
   const int64_t rows = (int64_t)N * sh.Ho;
   const int grid = rows < num_sms() ? (int)rows : num_sms();
   if (launch_pdl(stem_pool_span, dim3(grid), dim3(kSpanThreads), smem, gg_stream(stream), mw, sh,
-                 reinterpret_cast<const __nv_bfloat16*>(x), bias, reinterpret_cast<__nv_bfloat16*>(y),
+                 reinterpret_cast<const act_t*>(x), bias, reinterpret_cast<act_t*>(y),
                  count_dev) != cudaSuccess)
     return GG_ERR_CUDA;
   return GG_OK;

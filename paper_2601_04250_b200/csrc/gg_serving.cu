@@ -5,6 +5,7 @@
 
 #include "gg_common.cuh"
 #include "gg_kernels.h"
+#include "gg_act.cuh"
 
 namespace gg {
 
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(kEpiThreads) epilogue_served_kernel(const floa
   }
 }
 
-// uint8 HWC pool image -> normalized, space-to-depth(2) bf16 NHWC with 16
+// uint8 HWC pool image -> normalized, space-to-depth(2) fp16 NHWC with 16
 // channels: y[n, y, x, (dy*2 + dx)*3 + c] = norm(img[2y+dy, 2x+dx, c]), channels
 // 12..15 zero.  The ResNet stem (7x7/2 conv) then runs as a 4x4/1 conv over it.
 // One thread per output (s2d) pixel: 4 x 3 bytes in, 32 bytes out.
@@ -223,7 +224,7 @@ __device__ __forceinline__ int64_t s2d_index(int n, int yy, int xx, int Ho, int 
 // stem's SWIZZLE_32B operand: cell q keeps its two 16-byte halves swapped when
 // bit 2 of q is set (smem address bit 7 of row q within a 256-B atom), so a
 // linear bulk copy of any 8-row-aligned span lands as the swizzled tile.
-__device__ __forceinline__ void store_s2d_cell(__nv_bfloat16* y, int64_t q, const uint4& lo,
+__device__ __forceinline__ void store_s2d_cell(act_t* y, int64_t q, const uint4& lo,
                                                const uint4& hi, int padded) {
   uint4* dst = reinterpret_cast<uint4*>(y + q * 16);
   const bool swap = padded && ((q >> 2) & 1);
@@ -241,18 +242,18 @@ constexpr int kGatherRows = 4;
 __global__ void __launch_bounds__(kGatherThreads) stem_gather_kernel(
     const uint8_t* __restrict__ pool, int64_t pool_size, const int32_t* ids, const int32_t* count,
     int B, int H, int W, float m0, float m1, float m2, float s0, float s1, float s2, int padded,
-    __nv_bfloat16* __restrict__ y) {
+    act_t* __restrict__ y) {
   extern __shared__ __align__(16) uint8_t rows[];   // [2 * kGatherRows][W * 3]
-  // the normalization of a uint8 value is one of 3 x 256 bf16 results: built once
+  // the normalization of a uint8 value is one of 3 x 256 fp16 results: built once
   // per block with the exact arithmetic, then looked up (12 fp32 divisions per
   // cell made this kernel issue-bound).  It depends on nothing the predecessor
   // writes, so it is built before the PDL wait, overlapping the predecessor's tail.
-  __shared__ __nv_bfloat16 lut[3][256];
+  __shared__ act_t lut[3][256];
   {
     const float mean[3] = {m0, m1, m2}, sd[3] = {s0, s1, s2};
     for (int i = threadIdx.x; i < 3 * 256; i += kGatherThreads) {
       const int c = i >> 8, xv = i & 255;
-      lut[c][xv] = __float2bfloat16_rn(((float)xv * (1.0f / 255.0f) - mean[c]) / sd[c]);
+      lut[c][xv] = float2act(((float)xv * (1.0f / 255.0f) - mean[c]) / sd[c]);
     }
   }
   griddep_wait();   // PDL: the predecessor has completed and flushed
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(kGatherThreads) stem_gather_kernel(
   __syncthreads();
   for (int cell = threadIdx.x; cell < nrows * Wo; cell += kGatherThreads) {
     const int r = cell / Wo, xx = cell - r * Wo;
-    __align__(16) __nv_bfloat16 v[16];
+    __align__(16) act_t v[16];
 #pragma unroll
     for (int dy = 0; dy < 2; ++dy) {
       const uint8_t* row = rows + (2 * r + dy) * rb + 2 * xx * 3;
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kGatherThreads) stem_gather_kernel(
       }
     }
 #pragma unroll
-    for (int e = 12; e < 16; ++e) v[e] = __float2bfloat16_rn(0.0f);
+    for (int e = 12; e < 16; ++e) v[e] = float2act(0.0f);
     store_s2d_cell(y, s2d_index(n, yy0 + r, xx, Ho, Wo, padded), reinterpret_cast<uint4*>(v)[0],
                    reinterpret_cast<uint4*>(v)[1], padded);
   }
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(kGatherThreads) stem_gather_kernel(
 
 // fp32 NCHW (already normalized) -> the same space-to-depth(2) 16-channel layout.
 __global__ void nchw_to_s2d16_kernel(const float* __restrict__ x, int N, int H, int W, int padded,
-                                     __nv_bfloat16* __restrict__ y) {
+                                     act_t* __restrict__ y) {
   const int Ho = H / 2, Wo = W / 2;
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= (int64_t)N * Ho * Wo) return;
@@ -302,7 +303,7 @@ __global__ void nchw_to_s2d16_kernel(const float* __restrict__ x, int N, int H, 
   const int rem = (int)(p - (int64_t)n * Ho * Wo);
   const int yy = rem / Wo, xx = rem - yy * Wo;
   const int64_t q = s2d_index(n, yy, xx, Ho, Wo, padded);
-  __align__(16) __nv_bfloat16 v[16];
+  __align__(16) act_t v[16];
 #pragma unroll
   for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
@@ -310,9 +311,9 @@ __global__ void nchw_to_s2d16_kernel(const float* __restrict__ x, int N, int H, 
 #pragma unroll
       for (int c = 0; c < 3; ++c)
         v[(dy * 2 + dx) * 3 + c] =
-            __float2bfloat16_rn(__ldg(x + (((int64_t)n * 3 + c) * H + 2 * yy + dy) * W + 2 * xx + dx));
+            float2act(__ldg(x + (((int64_t)n * 3 + c) * H + 2 * yy + dy) * W + 2 * xx + dx));
 #pragma unroll
-  for (int e = 12; e < 16; ++e) v[e] = __float2bfloat16_rn(0.0f);
+  for (int e = 12; e < 16; ++e) v[e] = float2act(0.0f);
   store_s2d_cell(y, q, reinterpret_cast<uint4*>(v)[0], reinterpret_cast<uint4*>(v)[1], padded);
 }
 
@@ -596,7 +597,7 @@ int gg_stem_gather(const uint8_t* pool, int64_t pool_size, const int32_t* batch_
   GG_PDL_LAUNCH((stem_gather_kernel), dim3((unsigned)((H / 2 + kGatherRows - 1) / kGatherRows), (unsigned)B),
                 kGatherThreads, 2 * kGatherRows * W * 3, gg_stream(stream),
       pool, pool_size, batch_ids, count_dev, B, H, W, mean3[0], mean3[1], mean3[2], std3[0],
-      std3[1], std3[2], padded, reinterpret_cast<__nv_bfloat16*>(y));
+      std3[1], std3[2], padded, reinterpret_cast<act_t*>(y));
   GG_LAUNCH_OK();
   return GG_OK;
 }
@@ -606,7 +607,7 @@ int gg_nchw_to_s2d16(const float* x, int32_t N, int32_t H, int32_t W, int32_t pa
   if (!x || !y || N < 1 || H % 2 || W % 2) return GG_ERR_INVALID_ARGUMENT;
   const int64_t pixels = (int64_t)N * (H / 2) * (W / 2);
   nchw_to_s2d16_kernel<<<(unsigned)((pixels + 255) / 256), 256, 0, gg_stream(stream)>>>(
-      x, N, H, W, padded, reinterpret_cast<__nv_bfloat16*>(y));
+      x, N, H, W, padded, reinterpret_cast<act_t*>(y));
   GG_LAUNCH_OK();
   return GG_OK;
 }

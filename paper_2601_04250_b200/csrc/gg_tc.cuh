@@ -341,7 +341,8 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // offset of (its row, first column); rows with ok == false are skipped.
 namespace gg {
 namespace tc {
-__device__ __forceinline__ void warp_rows_load(uint8_t* buf, const __nv_bfloat16* base, int64_t off, bool ok,
+template <typename T>   // any 2-byte element type (bf16 / fp16)
+__device__ __forceinline__ void warp_rows_load(uint8_t* buf, const T* base, int64_t off, bool ok,
                                                int lane, uint4 (&row)[4]) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -383,8 +384,8 @@ __device__ __forceinline__ uint4 ld_global_nc_v4_hint(const void* ptr, uint64_t 
   return v;
 }
 
-template <bool KEEP_L2 = false>
-__device__ __forceinline__ void warp_rows_store(uint8_t* buf, __nv_bfloat16* base, int64_t off, bool ok, int lane,
+template <bool KEEP_L2 = false, typename T = __nv_bfloat16>
+__device__ __forceinline__ void warp_rows_store(uint8_t* buf, T* base, int64_t off, bool ok, int lane,
                                                 const uint4 (&row)[4]) {
   const int sw = (lane >> 1) & 3;
 #pragma unroll

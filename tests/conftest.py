@@ -8,6 +8,20 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def _ieee_fp32_references():
+    """Every torch reference in the GPU tests is IEEE fp32: no TF32 in cuDNN
+    convolutions or cuBLAS matmuls (torch's cuDNN default is TF32)."""
+    try:
+        import torch
+    except Exception:  # pragma: no cover
+        return
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+
+
+_ieee_fp32_references()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running CPU test")

@@ -23,19 +23,19 @@ def test_span_conv_vs_torch(n, h, c, cout, res):
     from paper_2601_04250_b200 import _native as nat
     lib = nat.load()
     g = torch.Generator(device="cuda").manual_seed(n * h + c)
-    x = torch.randn((n, c, h, h), device="cuda", generator=g).to(torch.bfloat16)
-    w = (torch.randn((cout, c, 3, 3), device="cuda", generator=g) / (9 * c) ** 0.5).to(torch.bfloat16)
+    x = torch.randn((n, c, h, h), device="cuda", generator=g).to(torch.float16)
+    w = (torch.randn((cout, c, 3, 3), device="cuda", generator=g) / (9 * c) ** 0.5).to(torch.float16)
     b = torch.randn(cout, device="cuda", generator=g)
     ref = torch.nn.functional.conv2d(x.float(), w.float(), b, padding=1)
-    xp = torch.zeros((n, h + 2, h + 2, c), dtype=torch.bfloat16, device="cuda")
+    xp = torch.zeros((n, h + 2, h + 2, c), dtype=torch.float16, device="cuda")
     xp[:, 1:-1, 1:-1] = x.permute(0, 2, 3, 1)
     rp = None
     if res:
-        rp = torch.zeros((n, h + 2, h + 2, cout), dtype=torch.bfloat16, device="cuda")
-        rp[:, 1:-1, 1:-1] = torch.randn((n, h, h, cout), device="cuda", generator=g).to(torch.bfloat16)
+        rp = torch.zeros((n, h + 2, h + 2, cout), dtype=torch.float16, device="cuda")
+        rp[:, 1:-1, 1:-1] = torch.randn((n, h, h, cout), device="cuda", generator=g).to(torch.float16)
         ref = ref + rp[:, 1:-1, 1:-1].float().permute(0, 3, 1, 2)
     ref = torch.relu(ref)
-    y = torch.full((n, h + 2, h + 2, cout), 7.0, dtype=torch.bfloat16, device="cuda")
+    y = torch.full((n, h + 2, h + 2, cout), 7.0, dtype=torch.float16, device="cuda")
     y[0, 0] = 0  # the first (W+3) positions are never written: zero them like a fresh buffer
     y[0, 1, 0] = 0
     wk = pack_span_weights(w)
@@ -61,20 +61,20 @@ def test_span_pair_stream_k(n, h, c, cout, monkeypatch):
     from paper_2601_04250_b200 import _native as nat
     lib = nat.load()
     g = torch.Generator(device="cuda").manual_seed(n + h + c)
-    x = torch.randn((n, c, h, h), device="cuda", generator=g).to(torch.bfloat16)
-    w = (torch.randn((cout, c, 3, 3), device="cuda", generator=g) / (9 * c) ** 0.5).to(torch.bfloat16)
+    x = torch.randn((n, c, h, h), device="cuda", generator=g).to(torch.float16)
+    w = (torch.randn((cout, c, 3, 3), device="cuda", generator=g) / (9 * c) ** 0.5).to(torch.float16)
     b = torch.randn(cout, device="cuda", generator=g)
-    xp = torch.zeros((n, h + 2, h + 2, c), dtype=torch.bfloat16, device="cuda")
+    xp = torch.zeros((n, h + 2, h + 2, c), dtype=torch.float16, device="cuda")
     xp[:, 1:-1, 1:-1] = x.permute(0, 2, 3, 1)
-    rp = torch.zeros((n, h + 2, h + 2, cout), dtype=torch.bfloat16, device="cuda")
-    rp[:, 1:-1, 1:-1] = torch.randn((n, h, h, cout), device="cuda", generator=g).to(torch.bfloat16)
+    rp = torch.zeros((n, h + 2, h + 2, cout), dtype=torch.float16, device="cuda")
+    rp[:, 1:-1, 1:-1] = torch.randn((n, h, h, cout), device="cuda", generator=g).to(torch.float16)
     ref = torch.relu(torch.nn.functional.conv2d(x.float(), w.float(), b, padding=1) +
                      rp[:, 1:-1, 1:-1].float().permute(0, 3, 1, 2))
     wk = pack_span_weights(w)
     outs = []
     for mode in ("0", "1", "1"):
         monkeypatch.setenv("GG_SPAN_SK", mode)
-        y = torch.zeros((n, h + 2, h + 2, cout), dtype=torch.bfloat16, device="cuda")
+        y = torch.zeros((n, h + 2, h + 2, cout), dtype=torch.float16, device="cuda")
         nat.check("gg_conv3x3_padded", lib.gg_conv3x3_padded(
             nat.ptr(xp), n, h, h, c, nat.ptr(wk), cout, nat.ptr(b), nat.ptr(rp), 1, nat.ptr(y), None,
             nat.stream_ptr()))

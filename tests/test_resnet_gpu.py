@@ -1,9 +1,10 @@
-"""ResNet-18 forward (implicit-GEMM tcgen05 convs) vs torchvision eager fp32.
+"""ResNet-18 forward (implicit-GEMM tcgen05 convs, fp16 storage) vs torchvision eager fp32.
 
-Tolerance: the north star's bf16 2e-2, applied to the logits relative to their
-scale (random-init ResNet-18 logits are O(1..10); bf16 activations through 20
-convs carry ~1e-2 relative error).  Single convolutions are checked against
-torch's fp32 conv2d on the same bf16 inputs.
+Oracle: torchvision eager in IEEE fp32 (cuDNN / cuBLAS TF32 disabled by
+tests/conftest.py).  Logits: the north star's 2e-2 ABSOLUTE bound on every
+logit (b = 2 and b = 64).  Single convolutions are checked against torch's
+fp32 conv2d on the same 16-bit inputs, within 2e-2 relative to the output
+scale (one rounding of the output).
 """
 
 from __future__ import annotations
@@ -29,21 +30,21 @@ def env():
 def test_conv_vs_torch(env, n, h, cin, cout, r, stride, pad, res):
     torch, nat, lib = env
     g = torch.Generator(device="cuda").manual_seed(n * h + cin)
-    x = torch.randn((n, cin, h, h), device="cuda", generator=g).to(torch.bfloat16)
-    w = (torch.randn((cout, cin, r, r), device="cuda", generator=g) / (cin * r * r) ** 0.5).to(torch.bfloat16)
+    x = torch.randn((n, cin, h, h), device="cuda", generator=g).to(torch.float16)
+    w = (torch.randn((cout, cin, r, r), device="cuda", generator=g) / (cin * r * r) ** 0.5).to(torch.float16)
     b = torch.randn(cout, device="cuda", generator=g)
     ref = torch.nn.functional.conv2d(x.float(), w.float(), b, stride=stride, padding=pad)
     ho = ref.shape[2]
-    resid = torch.randn((n, ho, ho, cout), device="cuda", generator=g).to(torch.bfloat16) if res else None
+    resid = torch.randn((n, ho, ho, cout), device="cuda", generator=g).to(torch.float16) if res else None
     if res:
         ref = ref + resid.float().permute(0, 3, 1, 2)
     ref = torch.relu(ref)
     k = r * r * cin
     kpad = (k + 63) // 64 * 64
-    wk = torch.zeros((cout, kpad), dtype=torch.bfloat16, device="cuda")
+    wk = torch.zeros((cout, kpad), dtype=torch.float16, device="cuda")
     wk[:, :k] = w.permute(0, 2, 3, 1).reshape(cout, k)
     xn = x.permute(0, 2, 3, 1).contiguous()
-    y = torch.empty((n, ho, ho, cout), dtype=torch.bfloat16, device="cuda")
+    y = torch.empty((n, ho, ho, cout), dtype=torch.float16, device="cuda")
     nat.check("gg_conv2d", lib.gg_conv2d(nat.ptr(xn), n, h, h, cin, nat.ptr(wk), cout, r, r, stride,
                                          pad, kpad, nat.ptr(b), nat.ptr(resid), 1, nat.ptr(y),
                                          -1, 0, None, nat.stream_ptr()))
@@ -60,18 +61,18 @@ def test_conv_stream_k(env, n, h, cin, cout, r, stride, pad, res):
     bit-identical across runs."""
     torch, nat, lib = env
     g = torch.Generator(device="cuda").manual_seed(n * h + cin + cout)
-    x = torch.randn((n, h, h, cin), device="cuda", generator=g).to(torch.bfloat16)
-    w = (torch.randn((cout, r * r * cin), device="cuda", generator=g) / (cin * r * r) ** 0.5).to(torch.bfloat16)
+    x = torch.randn((n, h, h, cin), device="cuda", generator=g).to(torch.float16)
+    w = (torch.randn((cout, r * r * cin), device="cuda", generator=g) / (cin * r * r) ** 0.5).to(torch.float16)
     b = torch.randn(cout, device="cuda", generator=g)
     ho = (h + 2 * pad - r) // stride + 1
-    resid = torch.randn((n, ho, ho, cout), device="cuda", generator=g).to(torch.bfloat16) if res else None
+    resid = torch.randn((n, ho, ho, cout), device="cuda", generator=g).to(torch.float16) if res else None
     outs = []
     assert lib.gg_streamk_reserve() == 0
     prev = lib.gg_streamk_mode(0)
     try:
         for mode in (0, 1, 1):
             lib.gg_streamk_mode(mode)
-            y = torch.empty((n, ho, ho, cout), dtype=torch.bfloat16, device="cuda")
+            y = torch.empty((n, ho, ho, cout), dtype=torch.float16, device="cuda")
             nat.check("gg_conv2d", lib.gg_conv2d(nat.ptr(x), n, h, h, cin, nat.ptr(w), cout, r, r,
                                                  stride, pad, r * r * cin, nat.ptr(b), nat.ptr(resid),
                                                  1, nat.ptr(y), -1, 0, None, nat.stream_ptr()))
@@ -107,18 +108,18 @@ def test_space_to_depth_stem_vs_torch(env):
     stem = _StemConv(conv, bn, "cuda")
     x = torch.randn((3, 3, 224, 224), generator=g).cuda()
     with torch.no_grad():
-        ref = torch.relu(bn.cuda()(conv.cuda()(x.to(torch.bfloat16).float())))
+        ref = torch.relu(bn.cuda()(conv.cuda()(x.to(torch.float16).float())))
     # span path: zero-bordered s2d input
-    x16p = torch.zeros((3, 115, 115, 16), dtype=torch.bfloat16, device="cuda")
+    x16p = torch.zeros((3, 115, 115, 16), dtype=torch.float16, device="cuda")
     nat.check("gg_nchw_to_s2d16", lib.gg_nchw_to_s2d16(nat.ptr(x), 3, 224, 224, 1, nat.ptr(x16p),
                                                        nat.stream_ptr()))
-    y = torch.empty((3, 112, 112, 64), dtype=torch.bfloat16, device="cuda")
+    y = torch.empty((3, 112, 112, 64), dtype=torch.float16, device="cuda")
     stem(lib, x16p.data_ptr(), 3, 112, 112, y.data_ptr(), nat.stream_ptr(), relu=True)
     got = y.float().permute(0, 3, 1, 2)
     err = (got - ref).abs().max().item()
     assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
     # im2col cross-check path: dense s2d input
-    x16 = torch.empty((3, 112, 112, 16), dtype=torch.bfloat16, device="cuda")
+    x16 = torch.empty((3, 112, 112, 16), dtype=torch.float16, device="cuda")
     nat.check("gg_nchw_to_s2d16", lib.gg_nchw_to_s2d16(nat.ptr(x), 3, 224, 224, 0, nat.ptr(x16),
                                                        nat.stream_ptr()))
     y2 = torch.empty_like(y)
@@ -146,20 +147,20 @@ def test_stem_pool_fused(env, n, hs, count, out_pad):
         bn.bias.copy_(torch.randn(64, generator=g) * 0.1)
     stem = _StemConv(conv, bn, "cuda")
     x = torch.randn((n, 3, 2 * hs, 2 * hs), generator=g).cuda()
-    x16p = torch.zeros((n, hs + 3, hs + 3, 16), dtype=torch.bfloat16, device="cuda")
+    x16p = torch.zeros((n, hs + 3, hs + 3, 16), dtype=torch.float16, device="cuda")
     nat.check("gg_nchw_to_s2d16", lib.gg_nchw_to_s2d16(nat.ptr(x), n, 2 * hs, 2 * hs, 1, nat.ptr(x16p),
                                                        nat.stream_ptr()))
     cnt = torch.tensor([count], dtype=torch.int32, device="cuda") if count is not None else None
-    y = torch.empty((n, hs, hs, 64), dtype=torch.bfloat16, device="cuda")
+    y = torch.empty((n, hs, hs, 64), dtype=torch.float16, device="cuda")
     stem(lib, x16p.data_ptr(), n, hs, hs, y.data_ptr(), nat.stream_ptr(), relu=True)
     ho = hs // 2
-    ref = torch.empty((n, ho, ho, 64), dtype=torch.bfloat16, device="cuda")
+    ref = torch.empty((n, ho, ho, 64), dtype=torch.float16, device="cuda")
     nat.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(nat.ptr(y), n, hs, hs, 64, nat.ptr(ref), 0, None,
                                                      nat.stream_ptr()))
     if out_pad == 2:
-        out = torch.zeros(((ho + 2) + n * (ho + 1) * (ho + 1), 64), dtype=torch.bfloat16, device="cuda")
+        out = torch.zeros(((ho + 2) + n * (ho + 1) * (ho + 1), 64), dtype=torch.float16, device="cuda")
     else:
-        out = torch.full((n, ho, ho, 64), -7.0, dtype=torch.bfloat16, device="cuda")
+        out = torch.full((n, ho, ho, 64), -7.0, dtype=torch.float16, device="cuda")
     nat.check("gg_stem_pool_span", lib.gg_stem_pool_span(
         nat.ptr(x16p), n, hs, hs, nat.ptr(stem.w), 64, nat.ptr(stem.b), nat.ptr(out), out_pad,
         nat.ptr(cnt), nat.stream_ptr()))
@@ -176,23 +177,23 @@ def test_stem_pool_fused(env, n, hs, count, out_pad):
 
 def test_pools(env):
     torch, nat, lib = env
-    x = torch.randn((2, 64, 112, 112), device="cuda").to(torch.bfloat16)
+    x = torch.randn((2, 64, 112, 112), device="cuda").to(torch.float16)
     xn = x.permute(0, 2, 3, 1).contiguous()
-    y = torch.empty((2, 56, 56, 64), dtype=torch.bfloat16, device="cuda")
+    y = torch.empty((2, 56, 56, 64), dtype=torch.float16, device="cuda")
     nat.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(nat.ptr(xn), 2, 112, 112, 64, nat.ptr(y),
                                                      0, None, nat.stream_ptr()))
     ref = torch.nn.functional.max_pool2d(x.float(), 3, 2, 1)
     assert torch.equal(y.float().permute(0, 3, 1, 2), ref)
-    z = torch.empty((2, 64), dtype=torch.bfloat16, device="cuda")
+    z = torch.empty((2, 64), dtype=torch.float16, device="cuda")
     nat.check("gg_avgpool", lib.gg_avgpool(nat.ptr(y), 2, 56 * 56, 64, nat.ptr(z), 0, None,
                                            nat.stream_ptr()))
     assert (z.float() - ref.mean(dim=(2, 3))).abs().max().item() < 1e-2
     # padded variants: maxpool into a zero-bordered buffer, avgpool over it with the interior count
-    yp = torch.zeros((2, 58, 58, 64), dtype=torch.bfloat16, device="cuda")
+    yp = torch.zeros((2, 58, 58, 64), dtype=torch.float16, device="cuda")
     nat.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(nat.ptr(xn), 2, 112, 112, 64, nat.ptr(yp),
                                                      1, None, nat.stream_ptr()))
     assert torch.equal(yp[:, 1:-1, 1:-1], y) and (yp[:, 0] == 0).all() and (yp[:, :, -1] == 0).all()
-    zp = torch.empty((2, 64), dtype=torch.bfloat16, device="cuda")
+    zp = torch.empty((2, 64), dtype=torch.float16, device="cuda")
     nat.check("gg_avgpool", lib.gg_avgpool(nat.ptr(yp), 2, 58 * 58, 64, nat.ptr(zp), 56 * 56, None,
                                            nat.stream_ptr()))
     assert (zp.float() - ref.mean(dim=(2, 3))).abs().max().item() < 1e-2
@@ -206,15 +207,15 @@ def test_conv2d_ds_fused(env, n, h, cin, cout):
     zero-bordered input of padded extent h; both outputs zero-bordered."""
     torch, nat, lib = env
     g = torch.Generator(device="cuda").manual_seed(h + cin)
-    x = torch.zeros((n, h, h, cin), dtype=torch.bfloat16, device="cuda")
-    x[:, 1:-1, 1:-1] = torch.randn((n, h - 2, h - 2, cin), device="cuda", generator=g).to(torch.bfloat16)
-    w = (torch.randn((cout, 9 * cin), device="cuda", generator=g) / (9 * cin) ** 0.5).to(torch.bfloat16)
-    wd = (torch.randn((cout, cin), device="cuda", generator=g) / cin ** 0.5).to(torch.bfloat16)
+    x = torch.zeros((n, h, h, cin), dtype=torch.float16, device="cuda")
+    x[:, 1:-1, 1:-1] = torch.randn((n, h - 2, h - 2, cin), device="cuda", generator=g).to(torch.float16)
+    w = (torch.randn((cout, 9 * cin), device="cuda", generator=g) / (9 * cin) ** 0.5).to(torch.float16)
+    wd = (torch.randn((cout, cin), device="cuda", generator=g) / cin ** 0.5).to(torch.float16)
     b = torch.randn(cout, device="cuda", generator=g)
     bd = torch.randn(cout, device="cuda", generator=g)
     ho = (h - 3) // 2 + 1
     shape = (n, ho + 2, ho + 2, cout)
-    y1, yd1, y2, yd2 = (torch.zeros(shape, dtype=torch.bfloat16, device="cuda") for _ in range(4))
+    y1, yd1, y2, yd2 = (torch.zeros(shape, dtype=torch.float16, device="cuda") for _ in range(4))
     nat.check("gg_conv2d", lib.gg_conv2d(nat.ptr(x), n, h, h, cin, nat.ptr(w), cout, 3, 3, 2, 0, 9 * cin,
                                          nat.ptr(b), None, 1, nat.ptr(y1), 0, 1, None, nat.stream_ptr()))
     nat.check("gg_conv2d", lib.gg_conv2d(nat.ptr(x), n, h, h, cin, nat.ptr(wd), cout, 1, 1, 2, -1, cin,
@@ -254,12 +255,12 @@ def test_conv3x3_shared_border(env, n, s, c, cout):
     torch, nat, lib = env
     from tests.test_conv_span_gpu import pack_span_weights
     g = torch.Generator(device="cuda").manual_seed(s + c)
-    x = torch.randn((n, s, s, c), device="cuda", generator=g).to(torch.bfloat16)
-    r = torch.randn((n, s, s, cout), device="cuda", generator=g).to(torch.bfloat16)
-    w = (torch.randn((cout, c, 3, 3), device="cuda", generator=g) / (9 * c) ** 0.5).to(torch.bfloat16)
+    x = torch.randn((n, s, s, c), device="cuda", generator=g).to(torch.float16)
+    r = torch.randn((n, s, s, cout), device="cuda", generator=g).to(torch.float16)
+    w = (torch.randn((cout, c, 3, 3), device="cuda", generator=g) / (9 * c) ** 0.5).to(torch.float16)
     b = torch.randn(cout, device="cuda", generator=g)
     xs, rs = _to_shared(x, s), _to_shared(r, s)
-    ys = torch.full_like(_to_shared(torch.zeros((n, s, s, cout), dtype=torch.bfloat16, device="cuda"), s), 0)
+    ys = torch.full_like(_to_shared(torch.zeros((n, s, s, cout), dtype=torch.float16, device="cuda"), s), 0)
     nat.check("gg_conv3x3_shared", lib.gg_conv3x3_shared(
         nat.ptr(xs), n, s, s, c, nat.ptr(pack_span_weights(w)), cout, nat.ptr(b), nat.ptr(rs), 1,
         nat.ptr(ys), None, nat.stream_ptr()))
@@ -279,19 +280,19 @@ def test_conv2d_ds_shared_border(env, n, s, cin, cout, in_shared):
     input and writing shared-border outputs, vs torch."""
     torch, nat, lib = env
     g = torch.Generator(device="cuda").manual_seed(s + cin)
-    x = torch.randn((n, s, s, cin), device="cuda", generator=g).to(torch.bfloat16)
+    x = torch.randn((n, s, s, cin), device="cuda", generator=g).to(torch.float16)
     if in_shared:
         xb, ext = _to_shared(x, s), s + 1
     else:
-        xb = torch.zeros((n, s + 2, s + 2, cin), dtype=torch.bfloat16, device="cuda")
+        xb = torch.zeros((n, s + 2, s + 2, cin), dtype=torch.float16, device="cuda")
         xb[:, 1:-1, 1:-1] = x
         ext = s + 2
-    w = (torch.randn((cout, 9 * cin), device="cuda", generator=g) / (9 * cin) ** 0.5).to(torch.bfloat16)
-    wd = (torch.randn((cout, cin), device="cuda", generator=g) / cin ** 0.5).to(torch.bfloat16)
+    w = (torch.randn((cout, 9 * cin), device="cuda", generator=g) / (9 * cin) ** 0.5).to(torch.float16)
+    wd = (torch.randn((cout, cin), device="cuda", generator=g) / cin ** 0.5).to(torch.float16)
     b = torch.randn(cout, device="cuda", generator=g)
     bd = torch.randn(cout, device="cuda", generator=g)
     so = s // 2
-    y = _to_shared(torch.zeros((n, so, so, cout), dtype=torch.bfloat16, device="cuda"), so)
+    y = _to_shared(torch.zeros((n, so, so, cout), dtype=torch.float16, device="cuda"), so)
     yd = y.clone()
     nat.check("gg_conv2d_ds", lib.gg_conv2d_ds(nat.ptr(xb), n, ext, ext, cin, nat.ptr(w), cout, nat.ptr(b),
                                                nat.ptr(y), nat.ptr(wd), nat.ptr(bd), nat.ptr(yd), in_shared, 1,
@@ -312,11 +313,11 @@ def test_conv2d_ds_shared_border(env, n, s, cin, cout, in_shared):
 def test_maxpool_ragged_shapes(env, n, c, h, w):
     """Blocked max pool (4 x 2 outputs per thread) at sizes that leave partial blocks: exact."""
     torch, nat, lib = env
-    x = torch.randn((n, c, h, w), device="cuda").to(torch.bfloat16)
+    x = torch.randn((n, c, h, w), device="cuda").to(torch.float16)
     xn = x.permute(0, 2, 3, 1).contiguous()
     ref = torch.nn.functional.max_pool2d(x.float(), 3, 2, 1)
     ho, wo = ref.shape[2], ref.shape[3]
-    y = torch.full((n, ho, wo, c), 7.0, dtype=torch.bfloat16, device="cuda")
+    y = torch.full((n, ho, wo, c), 7.0, dtype=torch.float16, device="cuda")
     nat.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(nat.ptr(xn), n, h, w, c, nat.ptr(y), 0, None,
                                                      nat.stream_ptr()))
     assert torch.equal(y.float().permute(0, 3, 1, 2), ref)
@@ -328,6 +329,7 @@ def test_resnet18_logits_vs_eager(env, batch):
     from paper_2601_04250_b200.resnet18 import ResNet18B200, random_model
     model = random_model(0)
     x = torch.randn((batch, 3, 224, 224), generator=torch.Generator().manual_seed(1))
+    assert not torch.backends.cudnn.allow_tf32       # IEEE fp32 oracle (conftest.py)
     with torch.no_grad():
         ref = model.cuda()(x.cuda()).float()
     net = ResNet18B200(model, max_batch=batch)
@@ -337,7 +339,7 @@ def test_resnet18_logits_vs_eager(env, batch):
     err = (out - ref).abs().max().item()
     print(f"resnet18 b={batch}: max |logit err| = {err:.3e}, logit scale {scale:.3f}, "
           f"argmax agree {(out.argmax(1) == ref.argmax(1)).float().mean().item():.3f}")
-    assert err <= 2e-2 * max(1.0, scale), err
+    assert err <= 2e-2, err                           # absolute (north star)
 
 
 @pytest.mark.parametrize("padded", [0, 1])
@@ -352,7 +354,7 @@ def test_stem_gather(env, padded):
     mean = torch.tensor([0.485, 0.456, 0.406], dtype=torch.float32)
     std = torch.tensor([0.229, 0.224, 0.225], dtype=torch.float32)
     shape = (4, 115, 115, 16) if padded else (4, 112, 112, 16)
-    y = torch.full(shape, 9.0, dtype=torch.bfloat16, device="cuda")
+    y = torch.full(shape, 9.0, dtype=torch.float16, device="cuda")
     nat.check("gg_stem_gather", lib.gg_stem_gather(
         nat.ptr(pool), 5, nat.ptr(ids), nat.ptr(count), 4, 224, 224,
         mean.numpy().ctypes.data_as(C.c_void_p), std.numpy().ctypes.data_as(C.c_void_p), padded,
@@ -367,7 +369,7 @@ def test_stem_gather(env, padded):
         sw = ((q >> 2) & 1).bool()
         y = torch.where(sw[..., None], torch.cat([y[..., 8:], y[..., :8]], dim=-1), y)
     got = y[:3, 2:-1, 2:-1] if padded else y[:3]
-    assert torch.equal(got[..., :12].float(), s2d.to(torch.bfloat16).float())
+    assert torch.equal(got[..., :12].float(), s2d.to(torch.float16).float())
     assert (got[..., 12:].float() == 0).all()
     assert (y[3].float() == 9.0).all()                            # beyond the count
     if padded:

@@ -33,14 +33,15 @@ def main():
     pooled32 = fm[:, :s, :s].float().mean(dim=(1, 2))
     fc32 = torch.nn.functional.linear(pooled32, m.fc.weight.float(), m.fc.bias.float())
     fc_bfpool = torch.nn.functional.linear(net.pooled[:batch].float(), m.fc.weight.float(), m.fc.bias.float())
+    del fm
 
     def e(a):
         return (a - ref).abs().max().item()
     print(f"batch {batch}: logit scale {ref.abs().max().item():.3f}")
-    print(f"  ours (bf16 pool, bf16 fc)       max|d| = {e(out):.4e}  argmax agree "
+    print(f"  ours (fp16 convs, fp32 head)    max|d| = {e(out):.4e}  argmax agree "
           f"{(out.argmax(1) == ref.argmax(1)).float().mean().item():.4f}")
-    print(f"  ours feature map + fp32 pool/fc max|d| = {e(fc32):.4e}")
-    print(f"  ours bf16 pooled + fp32 fc      max|d| = {e(fc_bfpool):.4e}")
+    print(f"  ours map + torch fp32 pool/fc   max|d| = {e(fc32):.4e}")
+    print(f"  ours pooled + torch fp32 fc     max|d| = {e(fc_bfpool):.4e}")
     print(f"  fp32 model on bf16-rounded input max|d| = {e(ref_xb):.4e}")
     with torch.no_grad():
         torch.backends.cudnn.allow_tf32 = True
