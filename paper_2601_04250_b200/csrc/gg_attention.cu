@@ -10,6 +10,9 @@
 //   MMA 2: O = P V (M=128, N=64, K=128) into TMEM columns [128, 192);
 //   epilogue: O / rowsum -> bf16 ctx[b*S + s, h*64 + d].
 #include <cudaTypedefs.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "gg_common.cuh"
 #include "gg_kernels.h"
@@ -167,6 +170,261 @@ __global__ void __launch_bounds__(kAttnThreads, 4)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Persistent, warp-specialized attention: one CTA per SM walks the (batch,
+// head) items c, c + grid, ... with every phase of consecutive items
+// overlapped (the per-item kernel above serializes load -> QK^T -> softmax ->
+// PV -> store inside one CTA and ran latency-bound at ~19 % occupancy):
+//   warp 0     TMA producer: Q, K, V^T (+ the item's key-mask row) into one of
+//              two 48 KB stages
+//   warp 1     MMA issuer: S(t+1) = Q K^T is issued before O(t) = P(t) V, so the
+//              tensor core works on the next item while the softmax runs
+//   warps 2-5, 6-9  two compute groups, items alternating between them;
+//              thread = query row.  softmax: the 128 scores of its row from
+//              TMEM into registers, max, ex2, sum, unnormalized P row (bf16,
+//              <= 1) into the group's swizzled A-operand buffer; epilogue
+//              after O = P V: O row / sum -> bf16 -> SW128 staging tile -> one
+//              TMA store of the [128 x 64] ctx box per item.  While one group
+//              waits for its O, the other group's softmax runs.
+// TMEM: S buffers [0, 256) and O buffers [256, 384), one of each per group.
+constexpr int kApThreads = 320;
+constexpr int kApStages = 3;                        // loads in flight per SM (HBM latency)
+constexpr int kApStageBytes = 50176;                 // Q 16K | K 16K | V^T 16K | mask 512 (1 KB pad)
+constexpr int kApOffStage = 0;
+constexpr int kApOffP = kApStages * kApStageBytes;   // 2 x 32 KB (P, then the ctx staging tile)
+constexpr int kApOffBar = kApOffP + 2 * 32768;
+constexpr int kApSmem = kApOffBar + 256 + 1024;
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(kApThreads, 1)
+    attention_persist(const __grid_constant__ CUtensorMap map_q,
+                      const __grid_constant__ CUtensorMap map_k,
+                      const __grid_constant__ CUtensorMap map_vt,
+                      const __grid_constant__ CUtensorMap map_o, const int32_t* mask, int batch,
+                      int heads, const int32_t* count, int dbg) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kApOffBar);
+  uint64_t* full = bars;         // [3] stage loaded (tx bytes)
+  uint64_t* empty = bars + 3;    // [3] stage free (MMA commit after O)
+  uint64_t* s_full = bars + 6;   // [2] S in TMEM (MMA commit), per group
+  uint64_t* s_empty = bars + 8;  // [2] S read by the group's 128 threads
+  uint64_t* p_full = bars + 10;  // [2] P written by the group's 128 threads
+  uint64_t* o_full = bars + 12;  // [2] O in TMEM (MMA commit)
+  uint64_t* o_empty = bars + 14; // [2] O read by the group's 128 threads
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  griddep_launch();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kApStages; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(s_empty + i, 128);
+      mbar_init(p_full + i, 128);
+      mbar_init(o_full + i, 1);
+      mbar_init(o_empty + i, 128);
+    }
+    fence_mbar_init();
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_vt);
+    tma_prefetch(&map_o);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();     // Q/K/V, the mask and the count follow the predecessor
+  const int nb = count ? min(batch, __ldg(count)) : batch;
+  const int n_items = nb * heads;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (elect_one_sync()) {
+      int t = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++t) {
+        const int st = t % kApStages;
+        const uint32_t ph = (t / kApStages) & 1;
+        mbar_wait(empty + st, ph ^ 1);
+        uint8_t* sb = smem + kApOffStage + st * kApStageBytes;
+        mbar_expect_tx(full + st, 49152 + (mask ? 512 : 0));
+        const int li = (dbg & 1) ? (int)blockIdx.x : it;
+        tma_load_2d(sb, &map_q, full + st, 0, li * kAttnS);
+        tma_load_2d(sb + 16384, &map_k, full + st, 0, li * kAttnS);
+        tma_load_2d(sb + 32768, &map_vt, full + st, 0, li * kAttnD);
+        tma_load_2d(sb + 40960, &map_vt, full + st, 64, li * kAttnD);
+        if (mask) bulk_load(sb + 49152, mask + (int64_t)(it / heads) * kAttnS, 512, full + st);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    // Non-blocking scheduler: S(t) = Q K^T is issued as soon as item t's stage
+    // has landed and its group's S buffer is free; O(t) = P V as soon as P(t)
+    // is written and the O buffer is free.  Neither waits behind the other, so
+    // a late load never holds back the PV of an item already in softmax.
+    constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(128, 64);
+    const int my_items = blockIdx.x < n_items ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    int ns = 0, no = 0;   // next item to issue S for / O for
+    while (no < my_items) {
+      bool done_any = false;
+      if (ns < my_items) {
+        const int st = ns % kApStages, gb = ns & 1;
+        if (mbar_test(full + st, (ns / kApStages) & 1) && mbar_test(s_empty + gb, ((ns >> 1) & 1) ^ 1)) {
+          tc_fence_after();
+          if (elect_one_sync()) {
+            const uint32_t sq = smem_u32(smem + kApOffStage + st * kApStageBytes);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              umma_bf16(tmem + gb * 128, sdesc_k_sw128(sq + kk * 32), sdesc_k_sw128(sq + 16384 + kk * 32),
+                        idesc_s, kk != 0);
+            umma_commit(s_full + gb);
+          }
+          __syncwarp();
+          ++ns;
+          done_any = true;
+        }
+      }
+      if (no < ns) {
+        const int ub = no & 1;
+        const uint32_t uph = (no >> 1) & 1;
+        if (mbar_test(p_full + ub, uph) && mbar_test(o_empty + ub, uph ^ 1)) {
+          tc_fence_after();
+          if (elect_one_sync()) {
+            const uint32_t sp = smem_u32(smem + kApOffP + ub * 32768);
+            const uint32_t sv = smem_u32(smem + kApOffStage + (no % kApStages) * kApStageBytes + 32768);
+#pragma unroll
+            for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                umma_bf16(tmem + 256 + ub * 64, sdesc_k_sw128(sp + kb * 16384 + kk * 32),
+                          sdesc_k_sw128(sv + kb * 8192 + kk * 32), idesc_o, (kb | kk) != 0);
+            umma_commit(o_full + ub);
+            umma_commit(empty + no % kApStages);
+          }
+          __syncwarp();
+          ++no;
+          done_any = true;
+        }
+      }
+      if (!done_any) __nanosleep(32);
+    }
+  } else {
+    // ------- compute groups: softmax + epilogue, thread = query row -------
+    // group g = (warp - 2) / 4 owns the items t = g, g + 2, ... of this CTA:
+    // softmax(t) -> [MMA: O(t)] -> epilogue(t) -> softmax(t + 2) ...; the other
+    // group's softmax runs while this one waits for O(t).
+    const int g = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const bool leader = (threadIdx.x & 127) == 0 && warp == 2 + 4 * g;
+    const float l2e = 1.4426950408889634f;
+    uint8_t* prow = smem + kApOffP + g * 32768 + (row >> 3) * 1024 + (row & 7) * 128;
+    uint8_t* orow = smem + kApOffP + g * 32768 + row * 128;   // staging tile reuses P
+    int t = g;
+    for (int it = blockIdx.x + g * gridDim.x; it < n_items; it += 2 * gridDim.x, t += 2) {
+      const uint32_t ph = (t >> 1) & 1;
+      if (t >= 2) {                        // the previous ctx store has read the P buffer
+        if (leader) bulk_wait_read<0>();
+        named_bar_sync(1 + g, 128);
+      }
+      // ---- softmax(t): the row's 128 scores in registers
+      mbar_wait(s_full + g, ph);
+      tc_fence_after();
+      uint32_t r[4][32];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(lane_base + g * 128 + c * 32, r[c]);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(s_empty + g);
+      float mx = -INFINITY;
+      if (mask) {
+        const int32_t* mrow = reinterpret_cast<const int32_t*>(smem + kApOffStage + (t % kApStages) * kApStageBytes + 49152);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (mrow[c * 32 + i] == 0) r[c][i] = __float_as_uint(-INFINITY);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[c][i]));
+      const float mref = (mx == -INFINITY) ? 0.0f : mx * l2e;
+      float sum = 0.0f;
+      // unnormalized P row (every value <= 1) -> A operand (K-major, SW128)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float e[8];
+          if (dbg & 2) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) e[j] = __uint_as_float(r[c][8 * q + j]);
+          } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            e[j] = ex2_approx(fmaf(__uint_as_float(r[c][8 * q + j]), l2e, -mref));
+            sum += e[j];
+          }
+          }
+          uint4 u;
+          u.x = pack_bf16(e[0], e[1]);
+          u.y = pack_bf16(e[2], e[3]);
+          u.z = pack_bf16(e[4], e[5]);
+          u.w = pack_bf16(e[6], e[7]);
+          const int chunk = (c & 1) * 4 + q;
+          *reinterpret_cast<uint4*>(prow + (c >> 1) * 16384 + ((chunk ^ (row & 7)) << 4)) = u;
+        }
+      const float inv = sum > 0.0f ? 1.0f / sum : 0.0f;
+      fence_proxy_async_smem();
+      mbar_arrive(p_full + g);
+      // ---- epilogue(t): O row / sum -> bf16 -> SW128 staging -> TMA store
+      mbar_wait(o_full + g, ph);
+      tc_fence_after();
+      uint32_t o[2][32];
+      tmem_ld_32x32b_x32(lane_base + 256 + g * 64, o[0]);
+      tmem_ld_32x32b_x32(lane_base + 256 + g * 64 + 32, o[1]);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(o_empty + g);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t* v = &o[c >> 2][(c & 3) * 8];
+        uint4 u;
+        u.x = pack_bf16(__uint_as_float(v[0]) * inv, __uint_as_float(v[1]) * inv);
+        u.y = pack_bf16(__uint_as_float(v[2]) * inv, __uint_as_float(v[3]) * inv);
+        u.z = pack_bf16(__uint_as_float(v[4]) * inv, __uint_as_float(v[5]) * inv);
+        u.w = pack_bf16(__uint_as_float(v[6]) * inv, __uint_as_float(v[7]) * inv);
+        *reinterpret_cast<uint4*>(orow + ((c ^ (row & 7)) << 4)) = u;
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1 + g, 128);
+      if (leader && !(dbg & 4)) {
+        tma_store_2d(&map_o, smem + kApOffP + g * 32768, (it % heads) * kAttnD, (it / heads) * kAttnS);
+        bulk_commit();
+      }
+    }
+    if (leader) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace gg
 
 using namespace gg;
@@ -184,6 +442,29 @@ extern "C" int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int
   if (!rc) rc = make_map_2d(&mk, base + plane, rows, kAttnD, kAttnD, 128);
   if (!rc) rc = make_map_2d(&mv, base + 2 * plane, (int64_t)batch * heads * kAttnD, seq_len, seq_len, 64);
   if (rc) return rc;
+  static const bool simple = getenv("GG_ATTN_SIMPLE") != nullptr;
+  // GG_ATTN_DBG (probe switches, tools/attn_probe.py; never set in production):
+  // 1 = every CTA reloads its first item (L2-resident loads), 2 = no exp in the
+  // softmax, 4 = no ctx stores
+  static const int dbg = getenv("GG_ATTN_DBG") ? atoi(getenv("GG_ATTN_DBG")) : 0;
+  if (!simple) {
+    CUtensorMap mo;
+    if (int rc2 = make_map_2d(&mo, ctx, (int64_t)batch * seq_len, (int64_t)heads * kAttnD, ldc, 128))
+      return rc2;
+    static bool pattr = false;
+    if (!pattr) {
+      if (cudaFuncSetAttribute(attention_persist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kApSmem) != cudaSuccess)
+        return GG_ERR_CUDA;
+      pattr = true;
+    }
+    const int grid = (int)std::min<int64_t>((int64_t)batch * heads, num_sms());
+    if (launch_pdl(attention_persist, dim3(grid), dim3(kApThreads), kApSmem, gg_stream(stream), mq, mk,
+                   mv, mo, mask, batch, heads, count_dev, dbg) != cudaSuccess)
+      return GG_ERR_CUDA;
+    GG_LAUNCH_OK();
+    return GG_OK;
+  }
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(attention_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
