@@ -57,6 +57,33 @@ typedef struct {
 int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
             int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* epilogue, void* stream);
 
+/* LayerNorm folded into the GEMMs around it (no LayerNorm kernel, no
+ * normalized activation in HBM).  Row statistics travel as partials: one
+ * float2 (mean_i, M2_i) per 128 output columns of a row, plane-major
+ * [ln_width / 128][M].
+ *   out_stats  this GEMM's output rows (bf16-rounded values): written
+ *   a_stats    A holds RAW rows h; the GEMM computes LN(h) W^T + b as
+ *              rstd (h W'^T) - rstd mean s_j + c_j, with W' = W diag(gamma)
+ *              (the B operand), a_colsum = s_j = sum_k W'_jk and the bias
+ *              c_j = b_j + sum_k beta_k W_jk (transformers LayerNorm -> Linear)
+ *   r_stats    the residual holds RAW rows h; it is added as
+ *              (h - mean) rstd r_gamma + r_beta
+ * Only the CTA-pair TMA-epilogue path (N % 256 == 0, M >= 4096) supports it
+ * (GG_ERR_UNSUPPORTED otherwise). */
+typedef struct {
+  const float* a_stats;
+  const float* a_colsum;
+  const float* r_stats;
+  const float* r_gamma;
+  const float* r_beta;
+  float* out_stats;
+  int32_t ln_width;      /* LayerNorm width (768), a multiple of 128 */
+  float eps;             /* LayerNorm epsilon */
+} gg_gemm_ln_params;
+int gg_gemm_ln(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
+               int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* epilogue,
+               const gg_gemm_ln_params* ln, void* stream);
+
 /* Allocate this device's stream-K workspace (48 MB fp32 partial tiles + 2 MB
  * counters) now, outside any CUDA graph capture.  gg_gemm / gg_conv2d split
  * their (tile, k-block) space evenly over the SMs when the tile count leaves a

@@ -40,6 +40,7 @@ SIGNATURES: dict[str, tuple] = {
     "gg_gemm_bf16": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _I64, _I32,
                                _I32, _P]),
     "gg_gemm": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P]),
+    "gg_gemm_ln": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _P]),
     "gg_streamk_reserve": (C.c_int, []),
     "gg_streamk_mode": (C.c_int, [_I32]),
     "gg_attention": (C.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, _P, _P]),

@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kApThreads, 1)
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-    const bool leader = (threadIdx.x & 127) == 0 && warp == 2 + 4 * g;
+    const bool leader = threadIdx.x == 64 + 128 * g;   // lane 0 of the group's first warp
     const float l2e = 1.4426950408889634f;
     uint8_t* prow = smem + kApOffP + g * 32768 + (row >> 3) * 1024 + (row & 7) * 128;
     uint8_t* orow = smem + kApOffP + g * 32768 + row * 128;   // staging tile reuses P

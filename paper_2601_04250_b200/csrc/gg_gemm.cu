@@ -41,7 +41,48 @@ struct GemmEpilogue {
   int raster_n;                    // 1: N-fastest tile order (A larger than ~L2/2), else M-fastest
   long long* prof;                 // debug (GG_GEMM_PROF): per-pair issuer cycles / waits, or null
   int tma_out;                     // pair kernel: outputs (and residual) through smem + TMA
+  // LayerNorm folding (pair kernel, TMA epilogue; see gg_gemm_ln):
+  const float2* a_stats;           // row statistics partials of A (raw h rows), [a_parts][ln_ld]
+  const float* a_colsum;           // [N] s_j = sum_k W'_jk (W' = W diag(gamma))
+  const float2* r_stats;           // row statistics partials of the residual rows
+  const float* r_gamma;            // [ln_width] gamma / beta of the residual's LayerNorm
+  const float* r_beta;
+  float2* out_stats;               // this GEMM's output row partials, [N / 128][ln_ld]
+  int a_parts, r_parts, ln_width;
+  int64_t ln_ld;                   // rows per partial plane (the GEMM's M)
+  float eps;
 };
+
+// LayerNorm row statistics carried between kernels as partials: one (mean_i,
+// M2_i) per 128 columns of a row (one epilogue warp's slice), merged with
+// Chan's formula by the consumer: mean = avg(mean_i), M2 = sum M2_i +
+// 128 sum (mean_i - mean)^2, var = M2 / width (biased, like torch).
+__device__ __forceinline__ void ln_row_params(const float2* st, int parts, int64_t ld, int64_t row,
+                                              int width, float eps, float& scale, float& shift) {
+  float m[8], q[8];
+  float mean = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i < parts) {
+      const float2 v = __ldg(st + (int64_t)i * ld + row);
+      m[i] = v.x;
+      q[i] = v.y;
+      mean += v.x;
+    }
+  }
+  mean /= (float)parts;
+  float m2 = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i < parts) {
+      const float d = m[i] - mean;
+      m2 += q[i] + 128.0f * d * d;
+    }
+  }
+  const float rstd = rsqrtf(m2 / (float)width + eps);
+  scale = rstd;
+  shift = -mean * rstd;
+}
 
 constexpr int kBK = 64;            // 64 bf16 = 128 B = one swizzle row
 // 8 epilogue warps: two per TMEM lane quarter, each draining half of the tile's
@@ -462,6 +503,7 @@ static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int 
 //   warps 2-9  epilogue in both CTAs (their own 128 rows), release to the leader
 constexpr int kPairBN = 256;
 constexpr int kPairMaxN = 4096;   // bias staged in smem
+constexpr int kPairAuxFloats = 3072;   // LN folding: s_j (N <= 3072) or gamma | beta (width <= 1536)
 
 template <int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -482,6 +524,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // per epilogue warp: two 2 KB staging buffers = the SWIZZLE_64B image of a
   // 32 x 32 bf16 box (output for the TMA store, residual from a TMA load)
   uint8_t* stg_base = smem + ((STAGES * STAGE_BYTES + 512 + kPairMaxN * 4 + 1023) & ~1023);
+  // LayerNorm folding: column sums s_j [N] (A side) or gamma | beta (residual side)
+  float* aux_s = reinterpret_cast<float*>(stg_base + kEpiWarps * 4096);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -599,6 +643,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the bias vector once per CTA in smem (broadcast LDS instead of per-chunk LDG)
     if (ep.bias)
       for (int i = threadIdx.x - 64; i < N; i += 32 * kEpiWarps) bias_s[i] = __ldg(ep.bias + i);
+    if (ep.a_colsum)
+      for (int i = threadIdx.x - 64; i < N; i += 32 * kEpiWarps) aux_s[i] = __ldg(ep.a_colsum + i);
+    if (ep.r_stats)
+      for (int i = threadIdx.x - 64; i < ep.ln_width; i += 32 * kEpiWarps) {
+        aux_s[i] = __ldg(ep.r_gamma + i);
+        aux_s[ep.ln_width + i] = __ldg(ep.r_beta + i);
+      }
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
     int t = 0;
     if (ep.tma_out) {
@@ -624,6 +675,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(&rb[0], 2048);
           tma_load_2d(stg, &map_res, &rb[0], colw, row0);
         }
+        // LayerNorm folding: this lane's row (row0 + lane) affine parameters
+        float a_sc = 1.0f, a_sh = 0.0f, r_sc = 1.0f, r_sh = 0.0f;
+        if (rows_ok && ep.a_stats)
+          ln_row_params(ep.a_stats, ep.a_parts, ep.ln_ld, row0 + lane, ep.ln_width, ep.eps, a_sc, a_sh);
+        if (rows_ok && ep.r_stats)
+          ln_row_params(ep.r_stats, ep.r_parts, ep.ln_ld, row0 + lane, ep.ln_width, ep.eps, r_sc, r_sh);
+        float st_k = 0.0f, st_s1 = 0.0f, st_s2 = 0.0f;   // output row partial (shifted sums)
         mbar_wait_sleep(&acc_full[acc], (t >> 1) & 1);
         tc_fence_after();
         const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * kPairBN + half * (kPairBN / 2);
@@ -651,7 +709,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (ep.bias) {
+          if (ep.a_stats) {   // LN(h) W^T + b = rstd (h W'^T) + (c_j - rstd mean s_j)
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 sj = *reinterpret_cast<const float4*>(aux_s + col0 + i);
+              const float4 cj = *reinterpret_cast<const float4*>(bias_s + col0 + i);
+              v[i] = fmaf(a_sc, v[i], fmaf(a_sh, sj.x, cj.x));
+              v[i + 1] = fmaf(a_sc, v[i + 1], fmaf(a_sh, sj.y, cj.y));
+              v[i + 2] = fmaf(a_sc, v[i + 2], fmaf(a_sh, sj.z, cj.z));
+              v[i + 3] = fmaf(a_sc, v[i + 3], fmaf(a_sh, sj.w, cj.w));
+            }
+          } else if (ep.bias) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + i);
@@ -666,12 +734,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int q = 0; q < 4; ++q) {
               const uint4 u = myrow[q ^ sw];
               const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+              float rr[8];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
                 const float2 f = __bfloat1622float2(h2[e]);
-                v[q * 8 + 2 * e] += f.x;
-                v[q * 8 + 2 * e + 1] += f.y;
+                rr[2 * e] = f.x;
+                rr[2 * e + 1] = f.y;
               }
+              if (ep.r_stats) {   // residual = LayerNorm(raw h) on the fly
+                const int cc = col0 + q * 8;
+                const float4 g0 = *reinterpret_cast<const float4*>(aux_s + cc);
+                const float4 g1 = *reinterpret_cast<const float4*>(aux_s + cc + 4);
+                const float4 b0 = *reinterpret_cast<const float4*>(aux_s + ep.ln_width + cc);
+                const float4 b1 = *reinterpret_cast<const float4*>(aux_s + ep.ln_width + cc + 4);
+                const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+                const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) rr[e] = fmaf(fmaf(rr[e], r_sc, r_sh), gg[e], bb[e]);
+              }
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[q * 8 + e] += rr[e];
             }
           }
           if (ep.act == ACT_RELU) {
@@ -714,12 +796,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
             myrow[q ^ sw] = u;
           }
+          if (ep.out_stats) {   // row statistics of this chunk (shifted sums, fp32 values)
+            if (c == 0) st_k = v[0];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float d = v[i] - st_k;
+              st_s1 += d;
+              st_s2 = fmaf(d, d, st_s2);
+            }
+          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             tma_store_2d(&map_out, buf, gx, gy);
             bulk_commit();
           }
+        }
+        if (ep.out_stats && rows_ok) {
+          const float n = (float)(kPairBN / 2);
+          const float mi = st_k + st_s1 / n;
+          const float m2 = fmaxf(st_s2 - st_s1 * st_s1 / n, 0.0f);
+          ep.out_stats[(int64_t)(tn * 2 + half) * ep.ln_ld + row0 + lane] = make_float2(mi, m2);
         }
         tc_fence_before();
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
@@ -789,7 +886,8 @@ template <int STAGES>
 static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                             const CUtensorMap& mr, int M, int N, int K, const GemmEpilogue& ep,
                             cudaStream_t s) {
-  constexpr int SMEM = STAGES * 2 * 128 * kBK * 2 + 512 + kPairMaxN * 4 + 1024 + kEpiWarps * 4096 + 1024;
+  constexpr int SMEM = STAGES * 2 * 128 * kBK * 2 + 512 + kPairMaxN * 4 + 1024 + kEpiWarps * 4096 +
+                       kPairAuxFloats * 4 + 1024;
   auto kern = gemm_bf16_pair<STAGES>;
   static bool attr = false;
   if (!attr) {
@@ -846,9 +944,9 @@ static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, const 
 
 using namespace gg;
 
-extern "C" int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
-                       int64_t ldd, int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* e,
-                       void* stream) {
+static int gemm_impl(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
+                     int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* e,
+                     const gg_gemm_ln_params* ln, void* stream) {
   if (!A || !B || !D || !e || M <= 0 || N <= 0 || K <= 0) return GG_ERR_INVALID_ARGUMENT;
   if (K % 64 || N % 32 || lda % 8 || ldb % 8 || (e->residual && e->ldr % 8)) return GG_ERR_INVALID_ARGUMENT;
   if (e->act < 0 || e->act > 2 || e->out_mode < 0 || e->out_mode > 2) return GG_ERR_INVALID_ARGUMENT;
@@ -871,6 +969,24 @@ extern "C" int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, v
                   e->out_mode == OUT_QKV_HEADS ? M * 64 * (int64_t)e->heads : 0,
                   e->count_dev, e->rows_per_item, StreamK{nullptr, nullptr, 0},
                   M * K * 2 > (48LL << 20) ? 1 : 0, nullptr, 0};
+  if (ln) {
+    if (ln->ln_width <= 0 || ln->ln_width % 128 || ln->ln_width > kPairAuxFloats / 2)
+      return GG_ERR_INVALID_ARGUMENT;
+    if ((ln->a_stats && !ln->a_colsum) || (ln->r_stats && (!ln->r_gamma || !ln->r_beta || !e->residual)))
+      return GG_ERR_INVALID_ARGUMENT;
+    if (ln->a_stats && (ln->ln_width != K || N > kPairAuxFloats)) return GG_ERR_INVALID_ARGUMENT;
+    if ((ln->r_stats || ln->out_stats) && ln->ln_width != N) return GG_ERR_INVALID_ARGUMENT;
+    ep.a_stats = reinterpret_cast<const float2*>(ln->a_stats);
+    ep.a_colsum = ln->a_colsum;
+    ep.r_stats = reinterpret_cast<const float2*>(ln->r_stats);
+    ep.r_gamma = ln->r_gamma;
+    ep.r_beta = ln->r_beta;
+    ep.out_stats = reinterpret_cast<float2*>(ln->out_stats);
+    ep.a_parts = ep.r_parts = ln->ln_width / 128;
+    ep.ln_width = ln->ln_width;
+    ep.ln_ld = M;
+    ep.eps = ln->eps;
+  }
   cudaStream_t s = gg_stream(stream);
   // CTA pairs for wide GEMMs (tile_n auto, N % 256 == 0, enough 256-row tiles
   // to fill most pairs); GG_NO_PAIR=1 keeps single-CTA tiles
@@ -894,13 +1010,28 @@ extern "C" int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, v
       if (rc) return rc;
       ep.tma_out = 1;
     }
+    if (ln && !ep.tma_out) return GG_ERR_UNSUPPORTED;
     return launch_gemm_pair<5>(ma, mbp, mo, mr, (int)M, (int)N, (int)K, ep, s);
   }
+  if (ln) return GG_ERR_UNSUPPORTED;   // LayerNorm folding lives in the CTA-pair epilogue
   switch (bn) {
     case 256: return launch_gemm<128, 256, 4>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
     case 128: return launch_gemm<128, 128, 6>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
     default: return launch_gemm<128, 64, 8>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
   }
+}
+
+extern "C" int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
+                       int64_t ldd, int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* e,
+                       void* stream) {
+  return gemm_impl(A, lda, B, ldb, D, ldd, M, N, K, e, nullptr, stream);
+}
+
+extern "C" int gg_gemm_ln(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
+                          int64_t ldd, int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* e,
+                          const gg_gemm_ln_params* ln, void* stream) {
+  if (!ln) return GG_ERR_INVALID_ARGUMENT;
+  return gemm_impl(A, lda, B, ldb, D, ldd, M, N, K, e, ln, stream);
 }
 
 extern "C" int gg_streamk_reserve(void) {

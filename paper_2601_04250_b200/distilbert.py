@@ -17,11 +17,21 @@ kernels of csrc/ through the forward C ABI (include/greengate_b200_forward.h):
 
 Weights are packed once from a transformers module (bf16 matrices, fp32
 bias/LN vectors); PyTorch only owns the buffers.
+
+LayerNorm folding (default when max_batch * seq_len >= 4096, the CTA-pair GEMM
+path; GG_LN_UNFUSED=1 keeps the LayerNorm kernels): no LayerNorm kernel runs
+inside the encoder.  The residual GEMMs (out_lin, lin2) write the RAW sum h and
+per-row statistics partials of it; the next GEMM on the normalized rows
+(QKV, lin1) multiplies raw h by W' = W diag(gamma) and corrects per row in its
+epilogue, rstd (h W'^T) - rstd mean s_j + (b_j + beta W^T), and the residual
+GEMM downstream adds LN(h) = (h - mean) rstd gamma + beta on the fly (gg_gemm_ln).
+Only the 128 CLS rows before the head go through gg_layernorm.
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 from . import _native
 
@@ -36,15 +46,31 @@ class GemmEpilogue(C.Structure):
                 ("count_dev", C.c_void_p)]
 
 
+class GemmLn(C.Structure):
+    """gg_gemm_ln_params (include/greengate_b200_forward.h)."""
+    _fields_ = [("a_stats", C.c_void_p), ("a_colsum", C.c_void_p), ("r_stats", C.c_void_p),
+                ("r_gamma", C.c_void_p), ("r_beta", C.c_void_p), ("out_stats", C.c_void_p),
+                ("ln_width", C.c_int32), ("eps", C.c_float)]
+
+
 def gemm(lib, A, lda, W, D, ldd, M, N, K, stream, bias=None, residual=None, act=NONE,
-         out_mode=OUT_BF16, seq_len=0, heads=0, tile_n=0, count=None, rows_per_item=1):
-    ep = GemmEpilogue(None if bias is None else bias.data_ptr(),
-                      None if residual is None else residual.data_ptr(),
-                      0 if residual is None else residual.stride(0), act, out_mode, seq_len,
+         out_mode=OUT_BF16, seq_len=0, heads=0, tile_n=0, count=None, rows_per_item=1, ln=None,
+         ldr=None):
+    res_ptr = None if residual is None else (residual if isinstance(residual, int)
+                                             else residual.data_ptr())
+    if residual is not None and ldr is None:
+        ldr = residual.stride(0)
+    ep = GemmEpilogue(None if bias is None else bias.data_ptr(), res_ptr,
+                      0 if residual is None else ldr, act, out_mode, seq_len,
                       heads, tile_n, rows_per_item if count is not None else 0,
                       None if count is None else count.data_ptr())
-    _native.check("gg_gemm", lib.gg_gemm(C.c_void_p(A), lda, _native.ptr(W), W.stride(0),
-                                         C.c_void_p(D), ldd, M, N, K, C.byref(ep), stream))
+    if ln is None:
+        _native.check("gg_gemm", lib.gg_gemm(C.c_void_p(A), lda, _native.ptr(W), W.stride(0),
+                                             C.c_void_p(D), ldd, M, N, K, C.byref(ep), stream))
+    else:
+        _native.check("gg_gemm_ln", lib.gg_gemm_ln(C.c_void_p(A), lda, _native.ptr(W), W.stride(0),
+                                                   C.c_void_p(D), ldd, M, N, K, C.byref(ep),
+                                                   C.byref(ln), stream))
 
 
 class DistilBertB200:
@@ -89,6 +115,10 @@ class DistilBertB200:
                 w2=bf(sd[q + "ffn.lin2.weight"]), b2=f32(sd[q + "ffn.lin2.bias"]),
                 ln2_g=f32(sd[q + "output_layer_norm.weight"]), ln2_b=f32(sd[q + "output_layer_norm.bias"]),
             ))
+        M = max_batch * seq_len
+        self.fused_ln = M >= 4096 and os.environ.get("GG_LN_UNFUSED") != "1"
+        if self.fused_ln:
+            self._fold_layernorms(sd)
         self.w_pre = bf(sd["pre_classifier.weight"])
         self.b_pre = f32(sd["pre_classifier.bias"])
         ncls = 32  # classifier rows padded to the GEMM's N granularity with zeros
@@ -97,7 +127,6 @@ class DistilBertB200:
         b_cls = torch.zeros(ncls, dtype=torch.float32)
         b_cls[: self.num_labels] = sd["classifier.bias"].float().cpu()
         self.w_cls, self.b_cls = bf(w_cls), f32(b_cls)
-        M = max_batch * seq_len
         z = dict(dtype=torch.bfloat16, device=self.device)
         self.x = torch.empty((M, self.DIM), **z)
         self.x1 = torch.empty((M, self.DIM), **z)
@@ -106,7 +135,40 @@ class DistilBertB200:
         self.ctx = torch.empty((M, self.DIM), **z)
         self.ffn = torch.empty((M, self.FFN), **z)
         self.pooled = torch.empty((max_batch, self.DIM), **z)
+        self.cls = torch.empty((max_batch, self.DIM), **z)
         self.logits = torch.empty((max_batch, ncls), dtype=torch.float32, device=self.device)
+        # LayerNorm folding: per-row statistics partials of h1 / h2 ([768 / 128][M] float2)
+        parts = self.DIM // 128
+        self.st1 = torch.empty((parts, M, 2), dtype=torch.float32, device=self.device)
+        self.st2 = torch.empty((parts, M, 2), dtype=torch.float32, device=self.device)
+
+    def _fold_layernorms(self, sd) -> None:
+        """W' = W diag(gamma) (bf16), s_j = sum_k W'_jk and c_j = b_j + sum_k beta_k W_jk
+        for every GEMM that consumes a LayerNorm output as its A operand: QKV of
+        layer L >= 1 (output_layer_norm of L - 1), lin1 of every layer
+        (sa_layer_norm).  fp64 on the host, once."""
+        torch = _native.require_cuda()
+
+        def fold(w_fp32, b, gamma, beta):
+            w = w_fp32.double().cpu()
+            g, bt = gamma.double().cpu(), beta.double().cpu()
+            wp = (w * g[None, :]).to(torch.bfloat16)
+            colsum = wp.double().sum(dim=1)
+            c = b.double().cpu() + w @ bt
+            dev = self.device
+            return (wp.to(dev).contiguous(), colsum.float().to(dev).contiguous(),
+                    c.float().to(dev).contiguous())
+        p = "distilbert.transformer.layer."
+        for i, L in enumerate(self.layers):
+            a = f"{p}{i}.attention."
+            if i > 0:
+                P = self.layers[i - 1]
+                w_qkv = torch.cat([sd[a + "q_lin.weight"], sd[a + "k_lin.weight"],
+                                   sd[a + "v_lin.weight"]])
+                L["w_qkv_f"], L["s_qkv"], L["c_qkv"] = fold(w_qkv, L["b_qkv"], P["ln2_g"],
+                                                            P["ln2_b"])
+            L["w1_f"], L["s_1"], L["c_1"] = fold(sd[f"{p}{i}.ffn.lin1.weight"], L["b1"],
+                                                 L["ln1_g"], L["ln1_b"])
 
     def flops(self, batch: int) -> float:
         """Algorithmic FLOPs of one forward (11.17 GF/seq at S=128)."""
@@ -129,12 +191,15 @@ class DistilBertB200:
         M = B * S
         st = _native.stream_ptr(stream)
         cnt = _native.ptr(count)
+        self._mask = attention_mask
         _native.check("gg_embed_layernorm", lib.gg_embed_layernorm(
             _native.ptr(input_ids), _native.ptr(self.word), _native.ptr(self.pos),
             _native.ptr(self.x), _native.ptr(self.emb_g), _native.ptr(self.emb_b), M, S, D,
             C.c_float(self.EPS), cnt, st))
         x, x1, h = self.x.data_ptr(), self.x1.data_ptr(), self.h.data_ptr()
         dyn = dict(count=count, rows_per_item=S)
+        if self.fused_ln:
+            return self._forward_folded(B, S, D, M, st, cnt, count, dyn)
         for L in self.layers:
             gemm(lib, x, D, L["w_qkv"], self.qkv.data_ptr(), 3 * D, M, 3 * D, D, st,
                  bias=L["b_qkv"], out_mode=OUT_QKV, seq_len=S, heads=self.HEADS, **dyn)
@@ -156,6 +221,55 @@ class DistilBertB200:
         # CLS rows (stride S*D) -> pre_classifier + ReLU -> classifier (fp32 logits)
         gemm(lib, x, S * D, self.w_pre, self.pooled.data_ptr(), D, B, D, D, st, bias=self.b_pre,
              act=RELU, tile_n=64, count=count, rows_per_item=1)
+        gemm(lib, self.pooled.data_ptr(), D, self.w_cls, self.logits.data_ptr(),
+             self.logits.stride(0), B, self.w_cls.shape[0], D, st, bias=self.b_cls,
+             out_mode=OUT_F32, tile_n=64, count=count, rows_per_item=1)
+        return self.logits[:B, : self.num_labels]
+
+
+    def _forward_folded(self, B, S, D, M, st, cnt, count, dyn):
+        """Encoder with every LayerNorm folded into the GEMMs (class docstring)."""
+        lib, eps = self.lib, self.EPS
+        x0 = self.x.data_ptr()       # embeddings + LayerNorm (normalized)
+        hA = self.x1.data_ptr()      # h1 = ctx W_o^T + b_o + x   (raw, LN1 folded downstream)
+        hB = self.h.data_ptr()       # h2 = ffn W_2^T + b_2 + x1  (raw, LN2 folded downstream)
+        p1, p2 = self.st1.data_ptr(), self.st2.data_ptr()
+        f = C.c_float(eps)
+        for i, L in enumerate(self.layers):
+            P = self.layers[i - 1] if i > 0 else None
+            if i == 0:
+                gemm(lib, x0, D, L["w_qkv"], self.qkv.data_ptr(), 3 * D, M, 3 * D, D, st,
+                     bias=L["b_qkv"], out_mode=OUT_QKV, seq_len=S, heads=self.HEADS, **dyn)
+            else:
+                gemm(lib, hB, D, L["w_qkv_f"], self.qkv.data_ptr(), 3 * D, M, 3 * D, D, st,
+                     bias=L["c_qkv"], out_mode=OUT_QKV, seq_len=S, heads=self.HEADS,
+                     ln=GemmLn(p2, L["s_qkv"].data_ptr(), None, None, None, None, D, f), **dyn)
+            _native.check("gg_attention", lib.gg_attention(
+                _native.ptr(self.qkv), _native.ptr(self._mask), _native.ptr(self.ctx), D, B,
+                self.HEADS, S, cnt, st))
+            if i == 0:   # residual = x0 (already normalized)
+                gemm(lib, self.ctx.data_ptr(), D, L["w_o"], hA, D, M, D, D, st, bias=L["b_o"],
+                     residual=x0, ldr=D,
+                     ln=GemmLn(None, None, None, None, None, p1, D, f), **dyn)
+            else:        # residual = LN2_{i-1}(h2)
+                gemm(lib, self.ctx.data_ptr(), D, L["w_o"], hA, D, M, D, D, st, bias=L["b_o"],
+                     residual=hB, ldr=D,
+                     ln=GemmLn(None, None, p2, P["ln2_g"].data_ptr(), P["ln2_b"].data_ptr(), p1,
+                               D, f), **dyn)
+            gemm(lib, hA, D, L["w1_f"], self.ffn.data_ptr(), self.FFN, M, self.FFN, D, st,
+                 bias=L["c_1"], act=GELU,
+                 ln=GemmLn(p1, L["s_1"].data_ptr(), None, None, None, None, D, f), **dyn)
+            gemm(lib, self.ffn.data_ptr(), self.FFN, L["w2"], hB, D, M, D, self.FFN, st,
+                 bias=L["b2"], residual=hA, ldr=D,
+                 ln=GemmLn(None, None, p1, L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), p2, D, f),
+                 **dyn)
+        last = self.layers[-1]
+        # the head reads only the CLS rows: LayerNorm of those B rows (stride S*D)
+        _native.check("gg_layernorm", lib.gg_layernorm(
+            C.c_void_p(hB), S * D, _native.ptr(self.cls), D, _native.ptr(last["ln2_g"]),
+            _native.ptr(last["ln2_b"]), B, D, f, cnt, 1, st))
+        gemm(lib, self.cls.data_ptr(), D, self.w_pre, self.pooled.data_ptr(), D, B, D, D, st,
+             bias=self.b_pre, act=RELU, tile_n=64, count=count, rows_per_item=1)
         gemm(lib, self.pooled.data_ptr(), D, self.w_cls, self.logits.data_ptr(),
              self.logits.stride(0), B, self.w_cls.shape[0], D, st, bias=self.b_cls,
              out_mode=OUT_F32, tile_n=64, count=count, rows_per_item=1)

@@ -77,3 +77,27 @@ def test_distilbert_logits_vs_eager(env, batch):
     err = (out - ref).abs().max().item()
     print(f"distilbert b={batch}: max |logit err| = {err:.3e}, |ref| max {ref.abs().max().item():.3f}")
     assert err <= 2e-2, err
+
+
+@pytest.mark.parametrize("fold", [True, False])
+def test_distilbert_layernorm_folding(env, fold, monkeypatch):
+    """b = 32 (M = 4096, the CTA-pair path): the LayerNorm-folded encoder
+    (gg_gemm_ln: row statistics partials, W diag(gamma) + column-sum correction,
+    LayerNorm'd residual on the fly) and the LayerNorm-kernel encoder both match
+    transformers eager fp32 within the bf16 bound; with a key mask."""
+    torch = env[0]
+    from paper_2601_04250_b200.distilbert import DistilBertB200, random_model
+    monkeypatch.setenv("GG_LN_UNFUSED", "0" if fold else "1")
+    model = random_model(0)
+    ids = torch.randint(0, model.config.vocab_size, (32, 128), generator=torch.Generator().manual_seed(3))
+    mask = torch.ones((32, 128), dtype=torch.int64)
+    mask[5, 100:] = 0
+    with torch.no_grad():
+        ref = model.cuda()(input_ids=ids.cuda(), attention_mask=mask.cuda()).logits.float()
+    net = DistilBertB200(model, max_batch=32)
+    assert net.fused_ln == fold
+    out = net.forward(ids.to(torch.int32).cuda(), mask.to(torch.int32).cuda())
+    torch.cuda.synchronize()
+    err = (out - ref).abs().max().item()
+    print(f"distilbert b=32 fold={fold}: max |logit err| = {err:.3e}")
+    assert err <= 2e-2, err
