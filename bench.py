@@ -82,6 +82,15 @@ WORKLOADS = {
                      batching_window_ms=10.0, fallback_degradation=0.05),
 }
 METRIC = "admitted inferences/sec"
+# The ablation's bio arm (C4): the reference's frozen ablation controller
+# (presets.ablation_reference: alpha = 1, beta = gamma = 0, tau0 = tau_inf =
+# ABLATION_TAU, entropy utility) for the DistilBERT requests, the same form with
+# a K = 1000 threshold for the ResNet-18 requests.
+ABLATION_TAU = 0.39796077431433013
+ABLATION_CTL = {
+    "distilbert": dict(alpha=1.0, beta=0.0, gamma=0.0, tau0=ABLATION_TAU, tau_inf=ABLATION_TAU, k=1.0),
+    "resnet18": dict(alpha=1.0, beta=0.0, gamma=0.0, tau0=0.35, tau_inf=0.35, k=1.0),
+}
 
 
 def peaks() -> dict:
@@ -178,11 +187,11 @@ def build_net(name: str, B: int):
 
 
 def make_server(wl, kind, net, scores, now, labels, payloads, dev, *, rank=0, world=1, pg=None,
-                open_loop=False, coin_seed=0, window=None):
+                open_loop=False, coin_seed=0, window=None, ctl=None):
     import torch
     import paper_2601_04250_b200 as gg
     from paper_2601_04250_b200 import serving
-    ctl = gg.ControllerConfig(**wl["ctl"], routing=gg.RoutePolicy.ALL_BATCHED).build(
+    ctl = gg.ControllerConfig(**(ctl or wl["ctl"]), routing=gg.RoutePolicy.ALL_BATCHED).build(
         gg.EnergyLedger(), device=dev)
     T = int(scores.shape[0])
     coins = torch.from_numpy(serving.fallback_coins(coin_seed, T)).to(dev)
@@ -613,7 +622,8 @@ def run_ablation(dev, nets) -> dict:
             srv = make_server(wl, kind, nets[kind], torch.from_numpy(sc).to(dev),
                               torch.from_numpy(nw).to(dev), torch.from_numpy(lb).to(dev),
                               payload_pool(kind, 256, 7, dev), dev, open_loop=open_loop,
-                              coin_seed=11 if kind == "distilbert" else 12, window=wl["batch"])
+                              coin_seed=11 if kind == "distilbert" else 12, window=wl["batch"],
+                              ctl=ABLATION_CTL[kind])
             srv.run(1)          # eager warm step (allocations), then one graph per server
             srv.capture()
             srvs.append(srv)
@@ -656,7 +666,8 @@ def run_ablation(dev, nets) -> dict:
         return round((x - y) / y * 100.0, 3) if y else None
     return {"trace": f"C4: ONOFF 800/50 rps, phase 0.5 s, 25 s, {total} arrivals, DistilBERT/ResNet-18 "
                      "by a seeded coin, B arrivals decided per step, Path-B 10 ms window, "
-                     "trace-time latency",
+                     "trace-time latency; bio arm = the reference's ablation controller "
+                     "(tau = ABLATION_TAU for DistilBERT, 0.35 for ResNet-18)",
             "arms": res,
             "device_wall_time_delta_pct": pct(c["device_wall_ms"], o["device_wall_ms"]),
             "trace_makespan_delta_pct": pct(c["trace_makespan_s"], o["trace_makespan_s"]),
