@@ -349,34 +349,40 @@ __global__ void __launch_bounds__(kApThreads, 1)
       mbar_arrive(s_empty + g);
       float mx = -INFINITY;
       if (mask) {
-        const int32_t* mrow = reinterpret_cast<const int32_t*>(smem + kApOffStage + (t % kApStages) * kApStageBytes + 49152);
+        const int4* mrow = reinterpret_cast<const int4*>(smem + kApOffStage + (t % kApStages) * kApStageBytes + 49152);
 #pragma unroll
         for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (mrow[c * 32 + i] == 0) r[c][i] = __float_as_uint(-INFINITY);
+          for (int i = 0; i < 32; i += 4) {
+            const int4 m4 = mrow[(c * 32 + i) >> 2];   // same address in every lane: broadcast
+            if (m4.x == 0) r[c][i] = __float_as_uint(-INFINITY);
+            if (m4.y == 0) r[c][i + 1] = __float_as_uint(-INFINITY);
+            if (m4.z == 0) r[c][i + 2] = __float_as_uint(-INFINITY);
+            if (m4.w == 0) r[c][i + 3] = __float_as_uint(-INFINITY);
+          }
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[c][i]));
+        for (int i = 0; i < 32; i += 2) mx = fmax3(mx, __uint_as_float(r[c][i]), __uint_as_float(r[c][i + 1]));
       const float mref = (mx == -INFINITY) ? 0.0f : mx * l2e;
-      float sum = 0.0f;
-      // unnormalized P row (every value <= 1) -> A operand (K-major, SW128)
+      const uint64_t l2e2 = f2_pack(l2e, l2e), nm2 = f2_pack(-mref, -mref);
+      uint64_t sum2 = f2_pack(0.0f, 0.0f);
+      // unnormalized P row (every value <= 1) -> A operand (K-major, SW128); packed
+      // fp32x2 FMA / add around the scalar MUFU ex2
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           float e[8];
-          if (dbg & 2) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) e[j] = __uint_as_float(r[c][8 * q + j]);
-          } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            e[j] = ex2_approx(fmaf(__uint_as_float(r[c][8 * q + j]), l2e, -mref));
-            sum += e[j];
-          }
+          for (int j = 0; j < 8; j += 2) {
+            float y0, y1;
+            f2_unpack(f2_fma(f2_pack(__uint_as_float(r[c][8 * q + j]), __uint_as_float(r[c][8 * q + j + 1])),
+                             l2e2, nm2), y0, y1);
+            e[j] = ex2_approx(y0);
+            e[j + 1] = ex2_approx(y1);
+            sum2 = f2_add(sum2, f2_pack(e[j], e[j + 1]));
           }
           uint4 u;
           u.x = pack_bf16(e[0], e[1]);
@@ -386,6 +392,9 @@ __global__ void __launch_bounds__(kApThreads, 1)
           const int chunk = (c & 1) * 4 + q;
           *reinterpret_cast<uint4*>(prow + (c >> 1) * 16384 + ((chunk ^ (row & 7)) << 4)) = u;
         }
+      float s0, s1;
+      f2_unpack(sum2, s0, s1);
+      const float sum = s0 + s1;
       const float inv = sum > 0.0f ? 1.0f / sum : 0.0f;
       fence_proxy_async_smem();
       mbar_arrive(p_full + g);

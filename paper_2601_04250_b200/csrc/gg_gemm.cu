@@ -710,20 +710,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
           if (ep.a_stats) {   // LN(h) W^T + b = rstd (h W'^T) + (c_j - rstd mean s_j)
+            const uint64_t sc2 = f2_pack(a_sc, a_sc), sh2 = f2_pack(a_sh, a_sh);
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               const float4 sj = *reinterpret_cast<const float4*>(aux_s + col0 + i);
               const float4 cj = *reinterpret_cast<const float4*>(bias_s + col0 + i);
-              v[i] = fmaf(a_sc, v[i], fmaf(a_sh, sj.x, cj.x));
-              v[i + 1] = fmaf(a_sc, v[i + 1], fmaf(a_sh, sj.y, cj.y));
-              v[i + 2] = fmaf(a_sc, v[i + 2], fmaf(a_sh, sj.z, cj.z));
-              v[i + 3] = fmaf(a_sc, v[i + 3], fmaf(a_sh, sj.w, cj.w));
+              const uint64_t t0 = f2_fma(sh2, f2_pack(sj.x, sj.y), f2_pack(cj.x, cj.y));
+              const uint64_t t1 = f2_fma(sh2, f2_pack(sj.z, sj.w), f2_pack(cj.z, cj.w));
+              f2_unpack(f2_fma(sc2, f2_pack(v[i], v[i + 1]), t0), v[i], v[i + 1]);
+              f2_unpack(f2_fma(sc2, f2_pack(v[i + 2], v[i + 3]), t1), v[i + 2], v[i + 3]);
             }
           } else if (ep.bias) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + i);
-              v[i] += bb.x; v[i + 1] += bb.y; v[i + 2] += bb.z; v[i + 3] += bb.w;
+              f2_unpack(f2_add(f2_pack(v[i], v[i + 1]), f2_pack(bb.x, bb.y)), v[i], v[i + 1]);
+              f2_unpack(f2_add(f2_pack(v[i + 2], v[i + 3]), f2_pack(bb.z, bb.w)), v[i + 2], v[i + 3]);
             }
           }
           uint4* myrow = reinterpret_cast<uint4*>(buf + lane * 64);
@@ -749,11 +751,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float4 b1 = *reinterpret_cast<const float4*>(aux_s + ep.ln_width + cc + 4);
                 const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
                 const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                const uint64_t sc2 = f2_pack(r_sc, r_sc), sh2 = f2_pack(r_sh, r_sh);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) rr[e] = fmaf(fmaf(rr[e], r_sc, r_sh), gg[e], bb[e]);
+                for (int e = 0; e < 8; e += 2) {
+                  const uint64_t nrm = f2_fma(f2_pack(rr[e], rr[e + 1]), sc2, sh2);
+                  f2_unpack(f2_fma(nrm, f2_pack(gg[e], gg[e + 1]), f2_pack(bb[e], bb[e + 1])), rr[e],
+                            rr[e + 1]);
+                }
               }
 #pragma unroll
-              for (int e = 0; e < 8; ++e) v[q * 8 + e] += rr[e];
+              for (int e = 0; e < 8; e += 2)
+                f2_unpack(f2_add(f2_pack(v[q * 8 + e], v[q * 8 + e + 1]), f2_pack(rr[e], rr[e + 1])),
+                          v[q * 8 + e], v[q * 8 + e + 1]);
             }
           }
           if (ep.act == ACT_RELU) {
@@ -761,7 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
           } else if (ep.act == ACT_GELU) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
+            for (int i = 0; i < 32; i += 2) gelu_erf2(v[i], v[i + 1]);
           }
           int gx = col0, gy = row0;
           if (ep.out_mode == OUT_QKV_HEADS) {
@@ -798,12 +807,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (ep.out_stats) {   // row statistics of this chunk (shifted sums, fp32 values)
             if (c == 0) st_k = v[0];
+            const uint64_t nk = f2_pack(-st_k, -st_k);
+            uint64_t s1 = f2_pack(0.0f, 0.0f), s2 = f2_pack(0.0f, 0.0f);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float d = v[i] - st_k;
-              st_s1 += d;
-              st_s2 = fmaf(d, d, st_s2);
+            for (int i = 0; i < 32; i += 2) {
+              const uint64_t d = f2_add(f2_pack(v[i], v[i + 1]), nk);
+              s1 = f2_add(s1, d);
+              s2 = f2_fma(d, d, s2);
             }
+            float a0, a1, c0, c1;
+            f2_unpack(s1, a0, a1);
+            f2_unpack(s2, c0, c1);
+            st_s1 += a0 + a1;
+            st_s2 += c0 + c1;
           }
           fence_proxy_async_smem();
           __syncwarp();
