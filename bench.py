@@ -479,6 +479,10 @@ def exchange_cost(dev, B: int = 128, reps: int = 50) -> dict:
 
 
 def roofline_forward(srv, net, B):
+    """Device time of one full-batch forward: the forward's launches captured in
+    a CUDA graph (as in the serving step) and replayed `reps` times back to back
+    between CUDA events on the serving stream (eager launches would time the
+    host's ctypes / tensor-map encoding instead of the kernels)."""
     import torch
     torch.cuda.synchronize()
     full = torch.full((1,), B, dtype=torch.int32, device=srv.dev)
@@ -491,14 +495,20 @@ def roofline_forward(srv, net, B):
         else:
             net.forward(srv.tok_ids, srv.tok_mask, batch=B, stream=s, count=full)
     with torch.cuda.stream(s):
+        fwd()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fwd()
+    with torch.cuda.stream(s):
         for _ in range(3):
-            fwd()
+            g.replay()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(s)
     with torch.cuda.stream(s):
         for _ in range(reps):
-            fwd()
+            g.replay()
     b.record(s)
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
