@@ -210,7 +210,7 @@ int gg_avgpool(const void* x, int32_t N, int32_t HW, int32_t C, void* y, int32_t
 /* ResNet head in fp32: global average pool of the bf16 NHWC map into
  * pooled [N, C] fp32 (no bf16 rounding), then logits [N, ld_logits] fp32 =
  * pooled . w_fc^T + b_fc with fp32 weights [ncls, C] (torchvision's avgpool +
- * fc, fp32 end to end).  Rows past *count_dev are untouched.  C % 64 == 0,
+ * fc, fp32 end to end).  Rows past *count_dev are untouched.  C % 128 == 0,
  * C <= 1536. */
 int gg_avgpool_fc(const void* x, int32_t N, int32_t HW, int32_t C, int32_t denom,
                   const float* w_fc, const float* b_fc, int32_t ncls, float* pooled,

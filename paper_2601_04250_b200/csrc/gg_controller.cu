@@ -8,6 +8,7 @@
 // (pkg/src/greengate/controller.py, energy.py, telemetry.py).
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "gg_common.cuh"
 #include "gg_kernels.h"
@@ -1913,7 +1914,9 @@ static int launch_admit(const AdmitArgs& args, void* stream) {
     // large batches: decide / scan / compact (three launches, no cross-block
     // waiting); the serving window (FIFO mode, small n): single pass with a
     // decoupled look-back
-    const bool split = !a.fifo && nb >= 4 * num_sms_cached();
+    static const int split_env = getenv("GG_K1_SPLIT") ? atoi(getenv("GG_K1_SPLIT")) : -1;
+    const bool split = split_env >= 0 ? (split_env != 0 && !a.fifo)
+                                      : (!a.fifo && nb >= 4 * num_sms_cached());
     const unsigned g = (unsigned)nb;
     if (split) {   // counters after the look-back words (gg_admit_workspace_bytes)
       int sh = 2;

@@ -710,58 +710,66 @@ __global__ void __launch_bounds__(256) avgpool_global_f32(const act_t* __restric
 }
 
 // fp32 classifier head: logits[n, j] = pooled[n, :] . w[j, :] + b[j] for the
-// first *count images.  Block = 8 classes (their weight rows staged in smem);
-// 4 threads per image split the reduction in interleaved float4 chunks (the
-// four lanes of an image read consecutive 16-byte words: conflict-free), then
-// a 2-step shuffle reduction; each lane stores 2 of the 8 logits.
+// first *count images.  Block = (kFcCls classes, kFcImg images), one warp per
+// image: the classes' weight rows are staged in smem once per block (before the
+// PDL wait), each lane takes a C / 32 slice of the image row (coalesced float4
+// loads) against the kFcCls rows (conflict-free float4 LDS), then one
+// butterfly reduction per class.  ~1000 small blocks: the head is latency-
+// bound, so parallelism beats reuse here.
 constexpr int kFcCls = 8;
-__global__ void __launch_bounds__(256) fc_f32_kernel(const float* __restrict__ pooled,
-                                                     const float* __restrict__ w,
-                                                     const float* __restrict__ b, int N, int C,
-                                                     int ncls, float* __restrict__ logits,
-                                                     int64_t ldl, const int32_t* count) {
+constexpr int kFcImg = 8;
+__global__ void __launch_bounds__(32 * kFcImg) fc_f32_kernel(const float* __restrict__ pooled,
+                                                            const float* __restrict__ w,
+                                                            const float* __restrict__ b, int N, int C,
+                                                            int ncls, float* __restrict__ logits,
+                                                            int64_t ldl, const int32_t* count) {
   extern __shared__ __align__(16) float ws[];   // [kFcCls][C]
   const int j0 = blockIdx.x * kFcCls;
   const int nc = min(kFcCls, ncls - j0);
-  for (int e = threadIdx.x * 4; e < kFcCls * C; e += blockDim.x * 4) {
-    const int c = e / C;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (c < nc) v = __ldg(reinterpret_cast<const float4*>(w + (int64_t)(j0 + c) * C + (e - c * C)));
-    *reinterpret_cast<float4*>(ws + e) = v;
+  const int c4 = C / 4;
+  for (int e0 = threadIdx.x; e0 < kFcCls * c4; e0 += 4 * blockDim.x) {
+    float4 v[4];   // four loads in flight before the stores
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x, c = e / c4, k = e - c * c4;
+      v[u] = (e < kFcCls * c4 && c < nc)
+                 ? __ldg(reinterpret_cast<const float4*>(w + (int64_t)(j0 + c) * C) + k)
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < kFcCls * c4) reinterpret_cast<float4*>(ws)[e] = v[u];
+    }
   }
   griddep_wait();
   griddep_launch();
   if (count) N = min(N, __ldg(count));
   __syncthreads();
-  const int q = threadIdx.x & 3;
-  const int nf = C / 16;   // float4 chunks per lane
-  for (int i = threadIdx.x >> 2; i < N; i += blockDim.x >> 2) {
-    float acc[kFcCls];
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.y * kFcImg + (threadIdx.x >> 5);
+  if (i >= N) return;
+  const float4* x4 = reinterpret_cast<const float4*>(pooled + (int64_t)i * C);
+  float acc[kFcCls];
 #pragma unroll
-    for (int c = 0; c < kFcCls; ++c) acc[c] = 0.f;
-    const float4* x4 = reinterpret_cast<const float4*>(pooled + (int64_t)i * C);
-    for (int jj = 0; jj < nf; ++jj) {
-      const int f = 4 * jj + q;
-      const float4 x = __ldg(x4 + f);
-#pragma unroll
-      for (int c = 0; c < kFcCls; ++c) {
-        const float4 wv = *reinterpret_cast<const float4*>(ws + c * C + 4 * f);
-        acc[c] = fmaf(x.x, wv.x, acc[c]);
-        acc[c] = fmaf(x.y, wv.y, acc[c]);
-        acc[c] = fmaf(x.z, wv.z, acc[c]);
-        acc[c] = fmaf(x.w, wv.w, acc[c]);
-      }
-    }
+  for (int c = 0; c < kFcCls; ++c) acc[c] = 0.f;
+  for (int f = lane; f < c4; f += 32) {
+    const float4 x = __ldg(x4 + f);
 #pragma unroll
     for (int c = 0; c < kFcCls; ++c) {
-      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 1);
-      acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], 2);
+      const float4 v = reinterpret_cast<const float4*>(ws + c * C)[f];
+      acc[c] = fmaf(x.w, v.w, fmaf(x.z, v.z, fmaf(x.y, v.y, fmaf(x.x, v.x, acc[c]))));
     }
+  }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = 2 * q + h;
-      if (c < nc) logits[(int64_t)i * ldl + j0 + c] = acc[c] + __ldg(b + j0 + c);
-    }
+  for (int c = 0; c < kFcCls; ++c)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+  if (lane < nc) {
+    float r = acc[0];
+#pragma unroll
+    for (int c = 1; c < kFcCls; ++c) r = lane == c ? acc[c] : r;
+    logits[(int64_t)i * ldl + j0 + lane] = r + __ldg(b + j0 + lane);
   }
 }
 
@@ -776,14 +784,15 @@ extern "C" int gg_avgpool_fc(const void* x, int32_t N, int32_t HW, int32_t C, in
   if (!x || !w_fc || !b_fc || !pooled || !logits || N < 1 || ncls < 1 || denom < 0 ||
       ld_logits < ncls)
     return GG_ERR_INVALID_ARGUMENT;
-  if (C % 64 || N > 65535 || kFcCls * C * 4 > 48 * 1024) return GG_ERR_UNSUPPORTED;
+  if (C % 128 || C > 1536 || N > 65535 * kFcImg) return GG_ERR_UNSUPPORTED;
   if (launch_pdl(avgpool_global_f32, dim3((unsigned)(C / 64), (unsigned)N), dim3(256), 0,
                  gg_stream(stream), reinterpret_cast<const act_t*>(x), pooled, N, HW, C,
                  count_dev, denom) != cudaSuccess)
     return GG_ERR_CUDA;
-  if (launch_pdl(fc_f32_kernel, dim3((unsigned)((ncls + kFcCls - 1) / kFcCls)), dim3(256),
-                 (size_t)kFcCls * C * 4, gg_stream(stream), (const float*)pooled, w_fc, b_fc, N, C,
-                 ncls, logits, ld_logits, count_dev) != cudaSuccess)
+  if (launch_pdl(fc_f32_kernel,
+                 dim3((unsigned)((ncls + kFcCls - 1) / kFcCls), (unsigned)((N + kFcImg - 1) / kFcImg)),
+                 dim3(32 * kFcImg), (size_t)kFcCls * C * 4, gg_stream(stream),
+                 (const float*)pooled, w_fc, b_fc, N, C, ncls, logits, ld_logits, count_dev) != cudaSuccess)
     return GG_ERR_CUDA;
   GG_LAUNCH_OK();
   return GG_OK;

@@ -50,10 +50,14 @@ def k1(reps):
     now = torch.linspace(0.0, 10.0, n, device="cuda", dtype=torch.float64)
     ctl = gg.ControllerConfig(alpha=1.0, beta=-0.1, gamma=-0.3, tau0=0.9, tau_inf=0.4, k=0.5,
                               routing=gg.RoutePolicy.THRESHOLD_ON_QUEUE).build(gg.EnergyLedger())
-    snap = gg.CongestionSnapshot(3, 7.5, 0.25)
+    from paper_2601_04250_b200 import _abi
+    s = _abi.gg_snapshot(3, 7.5, 0.25)   # device-resident snapshot (graph-capturable)
+    snap = torch.frombuffer(bytearray(bytes(s)), dtype=torch.uint8).cuda()
     out = ctl.decide_batch(scores, now, snap, breakdown=False)
     ms = _time(lambda: ctl.decide_batch(scores, now, snap, breakdown=False, out=out), reps)
-    print(f"k1 n={n}: {ms:.4f} ms  {n * 25 / ms / 1e6:.1f} GB/s")
+    n_adm = out.n_admitted
+    nbytes = n * 25 + 4 * n_adm
+    print(f"k1 n={n}: {ms:.4f} ms  {nbytes / ms / 1e6:.1f} GB/s algorithmic (25 B/row + 4 B/admitted)")
 
 
 SPANS = {"span1": (64, 56, 64, 64), "span2": (64, 28, 128, 128), "span3": (64, 14, 256, 256),
