@@ -505,7 +505,7 @@ constexpr int kPairBN = 256;
 constexpr int kPairMaxN = 4096;   // bias staged in smem
 constexpr int kPairAuxFloats = 3072;   // LN folding: s_j (N <= 3072) or gamma | beta (width <= 1536)
 
-template <int STAGES>
+template <int STAGES, int NBUF>   // NBUF: 2 KB epilogue staging boxes per warp (2 or 4)
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_res,
@@ -518,14 +518,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;     // [2]
   uint64_t* acc_empty = acc_full + 2;      // [2] (the leader's counts both CTAs' epilogues)
-  uint64_t* res_full = acc_empty + 2;      // [8 warps][2 buffers]: residual boxes landed
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(res_full + 2 * kEpiWarps);
+  uint64_t* res_full = acc_empty + 2;      // [8 warps][NBUF buffers]: residual boxes landed
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(res_full + NBUF * kEpiWarps);
   float* bias_s = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 512);   // [N] (N <= kPairMaxN)
   // per epilogue warp: two 2 KB staging buffers = the SWIZZLE_64B image of a
   // 32 x 32 bf16 box (output for the TMA store, residual from a TMA load)
   uint8_t* stg_base = smem + ((STAGES * STAGE_BYTES + 512 + kPairMaxN * 4 + 1023) & ~1023);
   // LayerNorm folding: column sums s_j [N] (A side) or gamma | beta (residual side)
-  float* aux_s = reinterpret_cast<float*>(stg_base + kEpiWarps * 4096);
+  float* aux_s = reinterpret_cast<float*>(stg_base + kEpiWarps * NBUF * 2048);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 2);   // one elected arrive per CTA of the pair
     }
-    for (int i = 0; i < 2 * kEpiWarps; ++i) mbar_init(&res_full[i], 1);
+    for (int i = 0; i < NBUF * kEpiWarps; ++i) mbar_init(&res_full[i], 1);
     fence_mbar_init();
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
@@ -657,10 +657,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // stores / residual loads touch 32 rows (32 L1 wavefronts) per instruction.
       // Instead each warp stages its 32 x 32 chunk in smem (SW64 image, conflict-
       // free for row-per-lane 16-B accesses) and moves it with one TMA store; the
-      // residual box arrives by TMA one chunk ahead.
-      uint8_t* stg = stg_base + (warp - 2) * 4096;
-      uint64_t* rb = res_full + (warp - 2) * 2;
-      uint32_t rph0 = 0, rph1 = 0;
+      // residual boxes arrive by TMA: with NBUF = 4 all four chunks of the tile
+      // are requested before the accumulator wait (their latency hides under the
+      // MMAs), with NBUF = 2 one chunk ahead.
+      uint8_t* stg = stg_base + (warp - 2) * (NBUF * 2048);
+      uint64_t* rb = res_full + (warp - 2) * NBUF;
+      uint32_t rph = 0;   // parity bit per staging buffer
       const bool has_res = ep.residual != nullptr;
       const int sw = (lane >> 1) & 3;
       for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
@@ -670,10 +672,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row0 = tm * 256 + rank * 128 + quarter * 32;   // this warp's 32 rows
         const int colw = tn * kPairBN + half * (kPairBN / 2);   // this warp's 128 columns
         const bool rows_ok = row0 < M;
-        if (has_res && rows_ok && lane == 0) {   // residual of chunk 0
+        if (has_res && rows_ok && lane == 0) {   // residual of chunk 0 (NBUF = 4: all chunks)
           bulk_wait_read<0>();
-          mbar_expect_tx(&rb[0], 2048);
-          tma_load_2d(stg, &map_res, &rb[0], colw, row0);
+#pragma unroll
+          for (int c = 0; c < (NBUF >= 4 ? 4 : 1); ++c) {
+            mbar_expect_tx(&rb[c], 2048);
+            tma_load_2d(stg + c * 2048, &map_res, &rb[c], colw + 32 * c, row0);
+          }
         }
         // LayerNorm folding: this lane's row (row0 + lane) affine parameters
         float a_sc = 1.0f, a_sh = 0.0f, r_sc = 1.0f, r_sh = 0.0f;
@@ -687,20 +692,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * kPairBN + half * (kPairBN / 2);
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
-          const int b = c & 1;
+          const int b = c % NBUF;
           uint8_t* buf = stg + b * 2048;
           if (rows_ok && lane == 0) {
             if (has_res) {
-              if (c + 1 < 4) {   // next chunk's residual into the other buffer once its store has read it
+              if (NBUF == 2 && c + 1 < 4) {   // next chunk's residual into the other buffer once its store has read it
                 bulk_wait_read<0>();
                 mbar_expect_tx(&rb[b ^ 1], 2048);
                 tma_load_2d(stg + (b ^ 1) * 2048, &map_res, &rb[b ^ 1], colw + 32 * (c + 1), row0);
               }
             } else {
-              bulk_wait_read<1>();   // the store of chunk c - 2 (same buffer) has read it
+              bulk_wait_read<NBUF - 1>();   // the store of chunk c - NBUF (same buffer) has read it
             }
           }
           __syncwarp();
+          // (reading chunk c + 1 from TMEM ahead of this chunk's math, fully
+          // unrolled, measured 5 % slower: register spills and code size)
           uint32_t r[32];
           tmem_ld_32x32b_x32(tacc + 32 * c, r);
           tmem_ld_wait();
@@ -730,8 +737,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           uint4* myrow = reinterpret_cast<uint4*>(buf + lane * 64);
           if (has_res) {
-            if (b == 0) { mbar_wait(&rb[0], rph0); rph0 ^= 1; }
-            else { mbar_wait(&rb[1], rph1); rph1 ^= 1; }
+            mbar_wait(&rb[b], (rph >> b) & 1u);
+            rph ^= 1u << b;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const uint4 u = myrow[q ^ sw];
@@ -898,13 +905,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int STAGES>
+template <int STAGES, int NBUF>
 static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                             const CUtensorMap& mr, int M, int N, int K, const GemmEpilogue& ep,
                             cudaStream_t s) {
-  constexpr int SMEM = STAGES * 2 * 128 * kBK * 2 + 512 + kPairMaxN * 4 + 1024 + kEpiWarps * 4096 +
+  constexpr int SMEM = STAGES * 2 * 128 * kBK * 2 + 512 + kPairMaxN * 4 + 1024 + kEpiWarps * NBUF * 2048 +
                        kPairAuxFloats * 4 + 1024;
-  auto kern = gemm_bf16_pair<STAGES>;
+  static_assert(SMEM <= 232448, "pair GEMM shared memory");
+  auto kern = gemm_bf16_pair<STAGES, NBUF>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
@@ -1027,7 +1035,14 @@ static int gemm_impl(const void* A, int64_t lda, const void* B, int64_t ldb, voi
       ep.tma_out = 1;
     }
     if (ln && !ep.tma_out) return GG_ERR_UNSUPPORTED;
-    return launch_gemm_pair<5>(ma, mbp, mo, mr, (int)M, (int)N, (int)K, ep, s);
+    // GG_PAIR_RES4=1: residual GEMMs with 4 staging boxes per warp (every residual
+    // chunk of a tile in flight during its MMAs) at the cost of one operand
+    // stage -- measured slower (FFN-down 60 -> 68 us: K = 3072 needs the stage;
+    // out_lin unchanged), so off by default
+    static const int res_cfg = getenv("GG_PAIR_RES4") ? atoi(getenv("GG_PAIR_RES4")) : 0;
+    if (ep.residual && ep.tma_out && res_cfg)
+      return launch_gemm_pair<4, 4>(ma, mbp, mo, mr, (int)M, (int)N, (int)K, ep, s);
+    return launch_gemm_pair<5, 2>(ma, mbp, mo, mr, (int)M, (int)N, (int)K, ep, s);
   }
   if (ln) return GG_ERR_UNSUPPORTED;   // LayerNorm folding lives in the CTA-pair epilogue
   switch (bn) {
