@@ -10,6 +10,7 @@
 // The CTA is persistent over tiles (grid = #SMs); the accumulator is double
 // buffered in TMEM so the epilogue of tile i overlaps the MMAs of tile i+1.
 #include <cudaTypedefs.h>
+#include <limits.h>
 #include <stdio.h>
 
 #include "gg_common.cuh"
@@ -41,6 +42,7 @@ struct GemmEpilogue {
   int raster_n;                    // 1: N-fastest tile order (A larger than ~L2/2), else M-fastest
   long long* prof;                 // debug (GG_GEMM_PROF): per-pair issuer cycles / waits, or null
   int tma_out;                     // pair kernel: outputs (and residual) through smem + TMA
+  int dbg_skip_epi;                // GG_GEMM_SKIP_EPI (probe): release accumulators without the epilogue
   // LayerNorm folding (pair kernel, TMA epilogue; see gg_gemm_ln):
   const float2* a_stats;           // row statistics partials of A (raw h rows), [a_parts][ln_ld]
   const float* a_colsum;           // [N] s_j = sum_k W'_jk (W' = W diag(gamma))
@@ -85,6 +87,12 @@ __device__ __forceinline__ void ln_row_params(const float2* st, int parts, int64
 }
 
 constexpr int kBK = 64;            // 64 bf16 = 128 B = one swizzle row
+
+__device__ __forceinline__ long long gtimer_ns() {   // GG_GEMM_PROF timeline stamps
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 // 8 epilogue warps: two per TMEM lane quarter, each draining half of the tile's
 // columns, so bias/GELU/residual math keeps pace with the MMA of the next tile.
 constexpr int kEpiWarps = 8;
@@ -505,31 +513,64 @@ constexpr int kPairBN = 256;
 constexpr int kPairMaxN = 4096;   // bias staged in smem
 constexpr int kPairAuxFloats = 3072;   // LN folding: s_j (N <= 3072) or gamma | beta (width <= 1536)
 
-template <int STAGES, int NBUF>   // NBUF: 2 KB epilogue staging boxes per warp (2 or 4)
-__global__ void __launch_bounds__(kThreads, 1)
+// Compile-time epilogue kinds of the pair kernel: the flags that shape the
+// epilogue's instruction stream are template parameters (no per-chunk runtime
+// branches); bias, ReLU, the residual LayerNorm and output statistics stay
+// runtime flags (uniform branches, residual kernels only).
+enum : int { EK_ALN = 1, EK_GELU = 2, EK_RES = 4, EK_QKV = 8 };
+
+// EW epilogue warps (8 or 16): warp w drains TMEM lane quarter w % 4 and one of
+// EW / 4 column parts of the tile (128 or 64 columns = 4 or 2 chunks of 32).
+// NBUF 2 KB staging boxes per epilogue warp (residual kernels: 2, the next
+// chunk's residual lands while this one is computed; otherwise 1).
+template <int STAGES, int EW, int NBUF, int EK>
+struct PairCfg {
+  static constexpr int kThreads = 64 + 32 * EW;
+  static constexpr int A_BYTES = 128 * kBK * 2, B_BYTES = 128 * kBK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;                  // 512 B of barriers
+  static constexpr int BIAS_OFF = BAR_OFF + 512;                         // [kPairMaxN] fp32
+  static constexpr int STG_OFF = (BIAS_OFF + kPairMaxN * 4 + 1023) & ~1023;
+  static constexpr int AUX_OFF = STG_OFF + EW * NBUF * 2048;           // [kPairAuxFloats] fp32
+  static constexpr int SMEM = AUX_OFF + kPairAuxFloats * 4 + 1024;       // + alignment slack
+  static_assert(SMEM <= 232448, "pair GEMM shared memory");
+  static_assert(EW == 8 || EW == 16, "epilogue warps");
+};
+
+template <int STAGES, int EW, int NBUF, int EK>
+__global__ void __launch_bounds__(64 + 32 * EW, 1)
     gemm_bf16_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_res,
                    int M_max, int N, int K, GemmEpilogue ep) {
-  constexpr int A_BYTES = 128 * kBK * 2, B_BYTES = 128 * kBK * 2;
-  constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  using C = PairCfg<STAGES, EW, NBUF, EK>;
+  constexpr bool ALN = EK & EK_ALN, GELU = EK & EK_GELU, RES = EK & EK_RES, QKV = EK & EK_QKV;
+  constexpr int PARTS = EW / 4, CW = kPairBN / PARTS, NCH = CW / 32;
+  static_assert(!RES || NBUF >= 2, "residual boxes need a second staging buffer");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // stay in the shared window (LDS / STS, not generic LD / ST): offset the
+  // array itself instead of round-tripping the pointer through an integer
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_u32 + 1023u) & ~1023u) - raw_u32);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;     // [2]
   uint64_t* acc_empty = acc_full + 2;      // [2] (the leader's counts both CTAs' epilogues)
-  uint64_t* res_full = acc_empty + 2;      // [8 warps][NBUF buffers]: residual boxes landed
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(res_full + NBUF * kEpiWarps);
-  float* bias_s = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 512);   // [N] (N <= kPairMaxN)
-  // per epilogue warp: two 2 KB staging buffers = the SWIZZLE_64B image of a
+  uint64_t* res_full = acc_empty + 2;      // [EW warps][NBUF buffers]: residual boxes landed
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(res_full + NBUF * EW);
+  float* bias_s = reinterpret_cast<float*>(smem + C::BIAS_OFF);   // [N] (N <= kPairMaxN)
+  // per epilogue warp: NBUF 2 KB staging buffers = the SWIZZLE_64B image of a
   // 32 x 32 bf16 box (output for the TMA store, residual from a TMA load)
-  uint8_t* stg_base = smem + ((STAGES * STAGE_BYTES + 512 + kPairMaxN * 4 + 1023) & ~1023);
+  uint8_t* stg_base = smem + C::STG_OFF;
   // LayerNorm folding: column sums s_j [N] (A side) or gamma | beta (residual side)
-  float* aux_s = reinterpret_cast<float*>(stg_base + kEpiWarps * NBUF * 2048);
+  float* aux_s = reinterpret_cast<float*>(smem + C::AUX_OFF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  if (ep.prof && threadIdx.x == 0 && rank == 0) {
+    ep.prof[pair * 8 + 4] = gtimer_ns();
+    ep.prof[2048 + pair * 2] = clock64();
+  }
   griddep_launch();
   const int num_kb = K / kBK;
 
@@ -542,14 +583,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&acc_full[a], 1);
       mbar_init(&acc_empty[a], 2);   // one elected arrive per CTA of the pair
     }
-    for (int i = 0; i < NBUF * kEpiWarps; ++i) mbar_init(&res_full[i], 1);
+    for (int i = 0; i < NBUF * EW; ++i) mbar_init(&res_full[i], 1);
     fence_mbar_init();
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
-    if (ep.tma_out) {
-      tma_prefetch(&map_out);
-      if (ep.residual) tma_prefetch(&map_res);
-    }
+    tma_prefetch(&map_out);
+    if (RES) tma_prefetch(&map_res);
   }
   if (warp == 1) tmem_alloc_pair(tmem_base_smem, 2 * kPairBN);
   tc_fence_before();
@@ -557,6 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
   griddep_wait();
+  if (ep.prof && threadIdx.x == 0 && rank == 0) ep.prof[pair * 8 + 5] = gtimer_ns();
   const int M = ep.count ? min(M_max, __ldg(ep.count) * ep.rows_per_item) : M_max;
   const int tiles_m = (M + 255) / 256, tiles_n = N / kPairBN;
   const int num_tiles = tiles_m * tiles_n;
@@ -566,16 +606,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int tile = pair; tile < num_tiles; tile += npairs) {
-        const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;   // raster: see above
+        const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;   // raster: see gemm_impl
         const int tn = ep.raster_n ? tile % tiles_n : tile / tiles_m;
         const int m0 = tm * 256 + rank * 128, n0 = tn * kPairBN + rank * 128;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait_sleep(&empty[s], ph ^ 1);
-          uint8_t* sa = smem + s * STAGE_BYTES;
-          if (rank == 0) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+          uint8_t* sa = smem + s * C::STAGE_BYTES;
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * C::STAGE_BYTES);
           const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
           tma_load_2d_pair(sa, &map_a, fb, kb * kBK, m0);
-          tma_load_2d_pair(sa + A_BYTES, &map_b, fb, kb * kBK, n0);
+          tma_load_2d_pair(sa + C::A_BYTES, &map_b, fb, kb * kBK, n0);
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
@@ -612,8 +652,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&full[s], ph);
           }
           tc_fence_after();
-          const uint64_t ad = a_desc0 + (uint64_t)s * (uint64_t)(STAGE_BYTES >> 4);
-          const uint64_t bd = ad + (uint64_t)(A_BYTES >> 4);
+          const uint64_t ad = a_desc0 + (uint64_t)s * (uint64_t)(C::STAGE_BYTES >> 4);
+          const uint64_t bd = ad + (uint64_t)(C::A_BYTES >> 4);
           if (elect_one_sync()) {
 #pragma unroll
             for (int kk = 0; kk < kBK / 16; ++kk)
@@ -630,271 +670,222 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
       if (ep.prof && lane == 0) {
-        ep.prof[pair * 4 + 0] = clock64() - t0;
-        ep.prof[pair * 4 + 1] = w_acc;
-        ep.prof[pair * 4 + 2] = w_full;
-        ep.prof[pair * 4 + 3] = t;
+        ep.prof[pair * 8 + 0] = clock64() - t0;
+        ep.prof[pair * 8 + 1] = w_acc;
+        ep.prof[pair * 8 + 2] = w_full;
+        ep.prof[pair * 8 + 3] = t;
+        ep.prof[pair * 8 + 6] = gtimer_ns();
       }
     }
   } else {
+    // ===== epilogue warps: TMEM -> registers -> fused math -> SW64 smem box -> TMA store
+    // A thread owns one accumulator row, so direct global stores / residual loads
+    // would touch 32 rows (32 L1 wavefronts) per instruction; instead each warp
+    // stages its 32 x 32 chunk in smem (SW64 image, conflict-free for row-per-lane
+    // 16-B accesses) and moves it with one TMA store.  Residual boxes arrive by
+    // TMA one chunk ahead.
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int part = (warp - 2) >> 2;
+    const int ew = warp - 2;
     const uint32_t leader_empty0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
     // the bias vector once per CTA in smem (broadcast LDS instead of per-chunk LDG)
     if (ep.bias)
-      for (int i = threadIdx.x - 64; i < N; i += 32 * kEpiWarps) bias_s[i] = __ldg(ep.bias + i);
-    if (ep.a_colsum)
-      for (int i = threadIdx.x - 64; i < N; i += 32 * kEpiWarps) aux_s[i] = __ldg(ep.a_colsum + i);
-    if (ep.r_stats)
-      for (int i = threadIdx.x - 64; i < ep.ln_width; i += 32 * kEpiWarps) {
+      for (int i = threadIdx.x - 64; i < N; i += 32 * EW) bias_s[i] = __ldg(ep.bias + i);
+    if (ALN)
+      for (int i = threadIdx.x - 64; i < N; i += 32 * EW) aux_s[i] = __ldg(ep.a_colsum + i);
+    if (RES && ep.r_stats)
+      for (int i = threadIdx.x - 64; i < ep.ln_width; i += 32 * EW) {
         aux_s[i] = __ldg(ep.r_gamma + i);
         aux_s[ep.ln_width + i] = __ldg(ep.r_beta + i);
       }
-    asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+    uint8_t* stg = stg_base + ew * (NBUF * 2048);
+    uint64_t* rb = res_full + ew * NBUF;
+    uint32_t rph = 0;   // parity bit per staging buffer
+    const int sw = (lane >> 1) & 3;
+    const bool has_bias = ep.bias != nullptr;
     int t = 0;
-    if (ep.tma_out) {
-      // Coalesced epilogue: a thread owns one accumulator row, so direct global
-      // stores / residual loads touch 32 rows (32 L1 wavefronts) per instruction.
-      // Instead each warp stages its 32 x 32 chunk in smem (SW64 image, conflict-
-      // free for row-per-lane 16-B accesses) and moves it with one TMA store; the
-      // residual boxes arrive by TMA: with NBUF = 4 all four chunks of the tile
-      // are requested before the accumulator wait (their latency hides under the
-      // MMAs), with NBUF = 2 one chunk ahead.
-      uint8_t* stg = stg_base + (warp - 2) * (NBUF * 2048);
-      uint64_t* rb = res_full + (warp - 2) * NBUF;
-      uint32_t rph = 0;   // parity bit per staging buffer
-      const bool has_res = ep.residual != nullptr;
-      const int sw = (lane >> 1) & 3;
-      for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
-        const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;
-        const int tn = ep.raster_n ? tile % tiles_n : tile / tiles_m;
-        const int acc = t & 1;
-        const int row0 = tm * 256 + rank * 128 + quarter * 32;   // this warp's 32 rows
-        const int colw = tn * kPairBN + half * (kPairBN / 2);   // this warp's 128 columns
-        const bool rows_ok = row0 < M;
-        if (has_res && rows_ok && lane == 0) {   // residual of chunk 0 (NBUF = 4: all chunks)
-          bulk_wait_read<0>();
-#pragma unroll
-          for (int c = 0; c < (NBUF >= 4 ? 4 : 1); ++c) {
-            mbar_expect_tx(&rb[c], 2048);
-            tma_load_2d(stg + c * 2048, &map_res, &rb[c], colw + 32 * c, row0);
-          }
-        }
-        // LayerNorm folding: this lane's row (row0 + lane) affine parameters
-        float a_sc = 1.0f, a_sh = 0.0f, r_sc = 1.0f, r_sh = 0.0f;
-        if (rows_ok && ep.a_stats)
-          ln_row_params(ep.a_stats, ep.a_parts, ep.ln_ld, row0 + lane, ep.ln_width, ep.eps, a_sc, a_sh);
-        if (rows_ok && ep.r_stats)
-          ln_row_params(ep.r_stats, ep.r_parts, ep.ln_ld, row0 + lane, ep.ln_width, ep.eps, r_sc, r_sh);
-        float st_k = 0.0f, st_s1 = 0.0f, st_s2 = 0.0f;   // output row partial (shifted sums)
-        mbar_wait_sleep(&acc_full[acc], (t >> 1) & 1);
-        tc_fence_after();
-        const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * kPairBN + half * (kPairBN / 2);
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          const int b = c % NBUF;
-          uint8_t* buf = stg + b * 2048;
-          if (rows_ok && lane == 0) {
-            if (has_res) {
-              if (NBUF == 2 && c + 1 < 4) {   // next chunk's residual into the other buffer once its store has read it
-                bulk_wait_read<0>();
-                mbar_expect_tx(&rb[b ^ 1], 2048);
-                tma_load_2d(stg + (b ^ 1) * 2048, &map_res, &rb[b ^ 1], colw + 32 * (c + 1), row0);
-              }
-            } else {
-              bulk_wait_read<NBUF - 1>();   // the store of chunk c - NBUF (same buffer) has read it
-            }
-          }
-          __syncwarp();
-          // (reading chunk c + 1 from TMEM ahead of this chunk's math, fully
-          // unrolled, measured 5 % slower: register spills and code size)
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tacc + 32 * c, r);
-          tmem_ld_wait();
-          if (!rows_ok) continue;
-          const int col0 = colw + 32 * c;
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (ep.a_stats) {   // LN(h) W^T + b = rstd (h W'^T) + (c_j - rstd mean s_j)
-            const uint64_t sc2 = f2_pack(a_sc, a_sc), sh2 = f2_pack(a_sh, a_sh);
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              const float4 sj = *reinterpret_cast<const float4*>(aux_s + col0 + i);
-              const float4 cj = *reinterpret_cast<const float4*>(bias_s + col0 + i);
-              const uint64_t t0 = f2_fma(sh2, f2_pack(sj.x, sj.y), f2_pack(cj.x, cj.y));
-              const uint64_t t1 = f2_fma(sh2, f2_pack(sj.z, sj.w), f2_pack(cj.z, cj.w));
-              f2_unpack(f2_fma(sc2, f2_pack(v[i], v[i + 1]), t0), v[i], v[i + 1]);
-              f2_unpack(f2_fma(sc2, f2_pack(v[i + 2], v[i + 3]), t1), v[i + 2], v[i + 3]);
-            }
-          } else if (ep.bias) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + i);
-              f2_unpack(f2_add(f2_pack(v[i], v[i + 1]), f2_pack(bb.x, bb.y)), v[i], v[i + 1]);
-              f2_unpack(f2_add(f2_pack(v[i + 2], v[i + 3]), f2_pack(bb.z, bb.w)), v[i + 2], v[i + 3]);
-            }
-          }
-          uint4* myrow = reinterpret_cast<uint4*>(buf + lane * 64);
-          if (has_res) {
-            mbar_wait(&rb[b], (rph >> b) & 1u);
-            rph ^= 1u << b;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint4 u = myrow[q ^ sw];
-              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-              float rr[8];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h2[e]);
-                rr[2 * e] = f.x;
-                rr[2 * e + 1] = f.y;
-              }
-              if (ep.r_stats) {   // residual = LayerNorm(raw h) on the fly
-                const int cc = col0 + q * 8;
-                const float4 g0 = *reinterpret_cast<const float4*>(aux_s + cc);
-                const float4 g1 = *reinterpret_cast<const float4*>(aux_s + cc + 4);
-                const float4 b0 = *reinterpret_cast<const float4*>(aux_s + ep.ln_width + cc);
-                const float4 b1 = *reinterpret_cast<const float4*>(aux_s + ep.ln_width + cc + 4);
-                const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-                const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-                const uint64_t sc2 = f2_pack(r_sc, r_sc), sh2 = f2_pack(r_sh, r_sh);
-#pragma unroll
-                for (int e = 0; e < 8; e += 2) {
-                  const uint64_t nrm = f2_fma(f2_pack(rr[e], rr[e + 1]), sc2, sh2);
-                  f2_unpack(f2_fma(nrm, f2_pack(gg[e], gg[e + 1]), f2_pack(bb[e], bb[e + 1])), rr[e],
-                            rr[e + 1]);
-                }
-              }
-#pragma unroll
-              for (int e = 0; e < 8; e += 2)
-                f2_unpack(f2_add(f2_pack(v[q * 8 + e], v[q * 8 + e + 1]), f2_pack(rr[e], rr[e + 1])),
-                          v[q * 8 + e], v[q * 8 + e + 1]);
-            }
-          }
-          if (ep.act == ACT_RELU) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
-          } else if (ep.act == ACT_GELU) {
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) gelu_erf2(v[i], v[i + 1]);
-          }
-          int gx = col0, gy = row0;
-          if (ep.out_mode == OUT_QKV_HEADS) {
-            // Q (x 1/sqrt(64)) and K boxes into their [B, H, S, 64] planes (the V^T plane
-            // keeps the lane-coalesced transposed path below)
-            const int hd = ep.heads * 64;
-            const int which = col0 / hd, hh = (col0 % hd) / 64;
-            if (which == 2) {
-              const int bq = row0 / ep.seq_len;
-              __nv_bfloat16* plane = reinterpret_cast<__nv_bfloat16*>(ep.D) + 2 * ep.qkv_plane;
-              const int64_t bh = (int64_t)bq * ep.heads + hh;
-              const int s_ = row0 % ep.seq_len + lane, d0 = col0 % 64;
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                plane[(bh * 64 + d0 + i) * ep.seq_len + s_] = __float2bfloat16_rn(v[i]);
-              continue;
-            }
-            if (which == 0) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= 0.125f;
-            }
-            gx = col0 % 64;
-            gy = (int)((int64_t)which * (ep.qkv_plane / 64) +
-                       ((int64_t)(row0 / ep.seq_len) * ep.heads + hh) * ep.seq_len + row0 % ep.seq_len);
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 u;
-            u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-            u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-            u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-            u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
-            myrow[q ^ sw] = u;
-          }
-          if (ep.out_stats) {   // row statistics of this chunk (shifted sums, fp32 values)
-            if (c == 0) st_k = v[0];
-            const uint64_t nk = f2_pack(-st_k, -st_k);
-            uint64_t s1 = f2_pack(0.0f, 0.0f), s2 = f2_pack(0.0f, 0.0f);
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              const uint64_t d = f2_add(f2_pack(v[i], v[i + 1]), nk);
-              s1 = f2_add(s1, d);
-              s2 = f2_fma(d, d, s2);
-            }
-            float a0, a1, c0, c1;
-            f2_unpack(s1, a0, a1);
-            f2_unpack(s2, c0, c1);
-            st_s1 += a0 + a1;
-            st_s2 += c0 + c1;
-          }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_2d(&map_out, buf, gx, gy);
-            bulk_commit();
-          }
-        }
-        if (ep.out_stats && rows_ok) {
-          const float n = (float)(kPairBN / 2);
-          const float mi = st_k + st_s1 / n;
-          const float m2 = fmaxf(st_s2 - st_s1 * st_s1 / n, 0.0f);
-          ep.out_stats[(int64_t)(tn * 2 + half) * ep.ln_ld + row0 + lane] = make_float2(mi, m2);
-        }
-        tc_fence_before();
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-        if (threadIdx.x == 64) {
-          if (rank == 0) mbar_arrive(&acc_empty[acc]);
-          else mbar_arrive_cluster(leader_empty0 + acc * 8);
-        }
-      }
-      if (lane == 0) bulk_wait<0>();
-    }
-    if (!ep.tma_out)
     for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
       const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;
       const int tn = ep.raster_n ? tile % tiles_n : tile / tiles_m;
       const int acc = t & 1;
+      const int row0 = tm * 256 + rank * 128 + quarter * 32;   // this warp's 32 rows
+      const int colw = tn * kPairBN + part * CW;                 // this warp's CW columns
+      const bool rows_ok = row0 < M && !ep.dbg_skip_epi;
+      if (RES && rows_ok && lane == 0) {   // residual of chunk 0
+        bulk_wait_read<0>();
+        mbar_expect_tx(&rb[0], 2048);
+        tma_load_2d(stg, &map_res, &rb[0], colw, row0);
+      }
+      // LayerNorm folding: this lane's row (row0 + lane) affine parameters
+      float a_sc = 1.0f, a_sh = 0.0f, r_sc = 1.0f, r_sh = 0.0f;
+      if (ALN && rows_ok)
+        ln_row_params(ep.a_stats, ep.a_parts, ep.ln_ld, row0 + lane, ep.ln_width, ep.eps, a_sc, a_sh);
+      if (RES && rows_ok && ep.r_stats)
+        ln_row_params(ep.r_stats, ep.r_parts, ep.ln_ld, row0 + lane, ep.ln_width, ep.eps, r_sc, r_sh);
+      float st_k = 0.0f, st_s1 = 0.0f, st_s2 = 0.0f;   // output row partial (shifted sums)
       mbar_wait_sleep(&acc_full[acc], (t >> 1) & 1);
       tc_fence_after();
-      const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * kPairBN;
-      const int row = tm * 256 + rank * 128 + quarter * 32 + lane;
-      const bool row_ok = row < M;
-      // residual rows are prefetched one chunk ahead so their latency overlaps
-      // the TMEM read and the math of the previous chunk
-      const bool pre = ep.residual != nullptr && row_ok;
-      const __nv_bfloat16* rrow = ep.residual + (int64_t)row * ep.ldr + tn * kPairBN;
-      uint4 res[4];
-      if (pre) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) res[q] = __ldg(reinterpret_cast<const uint4*>(rrow + half * (kPairBN / 2)) + q);
-      }
+      const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * kPairBN + part * CW;
 #pragma unroll 1
-      for (int c = half * (kPairBN / 2); c < (half + 1) * (kPairBN / 2); c += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tacc + c, r);
-        uint4 cur[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) cur[q] = res[q];
-        if (pre && c + 32 < (half + 1) * (kPairBN / 2)) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) res[q] = __ldg(reinterpret_cast<const uint4*>(rrow + c + 32) + q);
+      for (int c = 0; c < NCH; ++c) {
+        const int b = NBUF == 1 ? 0 : (c & 1);
+        uint8_t* buf = stg + b * 2048;
+        if (RES && rows_ok && lane == 0 && c + 1 < NCH) {
+          // next chunk's residual into the other buffer once its last store has read it
+          bulk_wait_read<0>();
+          mbar_expect_tx(&rb[b ^ 1], 2048);
+          tma_load_2d(stg + (b ^ 1) * 2048, &map_res, &rb[b ^ 1], colw + 32 * (c + 1), row0);
         }
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tacc + 32 * c, r);
         tmem_ld_wait();
-        if (!row_ok) continue;
+        if (!rows_ok) continue;
+        const int col0 = colw + 32 * c;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        epi_chunk(ep, row, tn * kPairBN + c, v, pre ? cur : nullptr, bias_s);
+        if (ALN) {   // LN(h) W^T + b = rstd (h W'^T) + (c_j - rstd mean s_j)
+          const uint64_t sc2 = f2_pack(a_sc, a_sc), sh2 = f2_pack(a_sh, a_sh);
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 sj = *reinterpret_cast<const float4*>(aux_s + col0 + i);
+            const float4 cj = *reinterpret_cast<const float4*>(bias_s + col0 + i);
+            const uint64_t t0 = f2_fma(sh2, f2_pack(sj.x, sj.y), f2_pack(cj.x, cj.y));
+            const uint64_t t1 = f2_fma(sh2, f2_pack(sj.z, sj.w), f2_pack(cj.z, cj.w));
+            f2_unpack(f2_fma(sc2, f2_pack(v[i], v[i + 1]), t0), v[i], v[i + 1]);
+            f2_unpack(f2_fma(sc2, f2_pack(v[i + 2], v[i + 3]), t1), v[i + 2], v[i + 3]);
+          }
+        } else if (has_bias) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 bb = *reinterpret_cast<const float4*>(bias_s + col0 + i);
+            f2_unpack(f2_add(f2_pack(v[i], v[i + 1]), f2_pack(bb.x, bb.y)), v[i], v[i + 1]);
+            f2_unpack(f2_add(f2_pack(v[i + 2], v[i + 3]), f2_pack(bb.z, bb.w)), v[i + 2], v[i + 3]);
+          }
+        }
+        uint4* myrow = reinterpret_cast<uint4*>(buf + lane * 64);
+        if (RES) {
+          mbar_wait(&rb[b], (rph >> b) & 1u);
+          rph ^= 1u << b;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 u = myrow[q ^ sw];
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+            float rr[8];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h2[e]);
+              rr[2 * e] = f.x;
+              rr[2 * e + 1] = f.y;
+            }
+            if (ep.r_stats) {   // residual = LayerNorm(raw h) on the fly
+              const int cc = col0 + q * 8;
+              const float4 g0 = *reinterpret_cast<const float4*>(aux_s + cc);
+              const float4 g1 = *reinterpret_cast<const float4*>(aux_s + cc + 4);
+              const float4 b0 = *reinterpret_cast<const float4*>(aux_s + ep.ln_width + cc);
+              const float4 b1 = *reinterpret_cast<const float4*>(aux_s + ep.ln_width + cc + 4);
+              const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+              const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+              const uint64_t sc2 = f2_pack(r_sc, r_sc), sh2 = f2_pack(r_sh, r_sh);
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) {
+                const uint64_t nrm = f2_fma(f2_pack(rr[e], rr[e + 1]), sc2, sh2);
+                f2_unpack(f2_fma(nrm, f2_pack(gg[e], gg[e + 1]), f2_pack(bb[e], bb[e + 1])), rr[e],
+                          rr[e + 1]);
+              }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; e += 2)
+              f2_unpack(f2_add(f2_pack(v[q * 8 + e], v[q * 8 + e + 1]), f2_pack(rr[e], rr[e + 1])),
+                        v[q * 8 + e], v[q * 8 + e + 1]);
+          }
+        }
+        if (GELU) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) gelu_erf2(v[i], v[i + 1]);
+        } else if (ep.act == ACT_RELU) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+        }
+        int gx = col0, gy = row0;
+        if (QKV) {
+          // Q (x 1/sqrt(64)) and K boxes into their [B, H, S, 64] planes (the V^T plane
+          // keeps the lane-coalesced transposed path below)
+          const int hd = ep.heads * 64;
+          const int which = col0 / hd, hh = (col0 % hd) / 64;
+          if (which == 2) {
+            const int bq = row0 / ep.seq_len;
+            __nv_bfloat16* plane = reinterpret_cast<__nv_bfloat16*>(ep.D) + 2 * ep.qkv_plane;
+            const int64_t bh = (int64_t)bq * ep.heads + hh;
+            const int s_ = row0 % ep.seq_len + lane, d0 = col0 % 64;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              plane[(bh * 64 + d0 + i) * ep.seq_len + s_] = __float2bfloat16_rn(v[i]);
+            continue;
+          }
+          if (which == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= 0.125f;
+          }
+          gx = col0 % 64;
+          gy = (int)((int64_t)which * (ep.qkv_plane / 64) +
+                     ((int64_t)(row0 / ep.seq_len) * ep.heads + hh) * ep.seq_len + row0 % ep.seq_len);
+        }
+        uint4 u[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          u[q].x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+          u[q].y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+          u[q].z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+          u[q].w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+        }
+        if (!RES) {   // the store that last read this buffer (NBUF chunks ago) is done
+          if (lane == 0) bulk_wait_read<NBUF - 1>();
+          __syncwarp();
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) myrow[q ^ sw] = u[q];
+        if (RES && ep.out_stats) {   // row statistics of this chunk (shifted sums, fp32 values)
+          if (c == 0) st_k = v[0];
+          const uint64_t nk = f2_pack(-st_k, -st_k);
+          uint64_t s1 = f2_pack(0.0f, 0.0f), s2 = f2_pack(0.0f, 0.0f);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const uint64_t d = f2_add(f2_pack(v[i], v[i + 1]), nk);
+            s1 = f2_add(s1, d);
+            s2 = f2_fma(d, d, s2);
+          }
+          float a0, a1, c0, c1;
+          f2_unpack(s1, a0, a1);
+          f2_unpack(s2, c0, c1);
+          st_s1 += a0 + a1;
+          st_s2 += c0 + c1;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&map_out, buf, gx, gy);
+          bulk_commit();
+        }
       }
-      // release the accumulator: all epilogue warps of this CTA, then one arrive
-      // on the leader's barrier (local for the leader, remote for the peer)
+      if (RES && ep.out_stats && rows_ok) {
+        const float n = (float)CW;
+        const float mi = st_k + st_s1 / n;
+        const float m2 = fmaxf(st_s2 - st_s1 * st_s1 / n, 0.0f);
+        ep.out_stats[(int64_t)(tn * PARTS + part) * ep.ln_ld + row0 + lane] = make_float2(mi, m2);
+      }
       tc_fence_before();
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
       if (threadIdx.x == 64) {
         if (rank == 0) mbar_arrive(&acc_empty[acc]);
         else mbar_arrive_cluster(leader_empty0 + acc * 8);
       }
+    }
+    if (lane == 0) bulk_wait<0>();
+    if (ep.prof && threadIdx.x == 64 && rank == 0) {
+      ep.prof[pair * 8 + 7] = gtimer_ns();
+      ep.prof[2048 + pair * 2 + 1] = clock64();
     }
   }
   __syncthreads();
@@ -905,17 +896,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int STAGES, int NBUF>
+template <int STAGES, int EW, int NBUF, int EK>
 static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                             const CUtensorMap& mr, int M, int N, int K, const GemmEpilogue& ep,
                             cudaStream_t s) {
-  constexpr int SMEM = STAGES * 2 * 128 * kBK * 2 + 512 + kPairMaxN * 4 + 1024 + kEpiWarps * NBUF * 2048 +
-                       kPairAuxFloats * 4 + 1024;
-  static_assert(SMEM <= 232448, "pair GEMM shared memory");
-  auto kern = gemm_bf16_pair<STAGES, NBUF>;
+  using Cf = PairCfg<STAGES, EW, NBUF, EK>;
+  auto kern = gemm_bf16_pair<STAGES, EW, NBUF, EK>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM) != cudaSuccess)
       return GG_ERR_CUDA;
     attr = true;
   }
@@ -924,8 +913,8 @@ static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, const 
   const int grid = 2 * (tiles < pairs ? tiles : pairs);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = SMEM;
+  cfg.blockDim = dim3(Cf::kThreads);
+  cfg.dynamicSmemBytes = Cf::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -940,6 +929,7 @@ static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, const 
   GemmEpilogue e2 = ep;
   const bool do_prof = getenv("GG_GEMM_PROF") != nullptr;
   if (do_prof) {
+    e2.dbg_skip_epi = getenv("GG_GEMM_SKIP_EPI") != nullptr;
     if (!prof) cudaMalloc(&prof, 4096 * sizeof(long long));
     cudaMemsetAsync(prof, 0, 4096 * sizeof(long long), s);
     e2.prof = prof;
@@ -951,18 +941,67 @@ static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, const 
     cudaDeviceSynchronize();
     cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
     double tot = 0, wa = 0, wf = 0, nt = 0;
+    long long e0 = LLONG_MAX, e1 = 0, w1 = 0, i1 = 0, x1 = 0;
     const int np = grid / 2;
+    double ghz = 0;
+    for (int i = 0; i < np; ++i)
+      ghz += (double)(h[2048 + 2 * i + 1] - h[2048 + 2 * i]) / (double)(h[8 * i + 7] - h[8 * i + 4]) / np;
     for (int i = 0; i < np; ++i) {
-      tot += h[4 * i];
-      wa += h[4 * i + 1];
-      wf += h[4 * i + 2];
-      nt += h[4 * i + 3];
+      tot += h[8 * i];
+      wa += h[8 * i + 1];
+      wf += h[8 * i + 2];
+      nt += h[8 * i + 3];
+      e0 = h[8 * i + 4] < e0 ? h[8 * i + 4] : e0;
+      e1 = h[8 * i + 4] > e1 ? h[8 * i + 4] : e1;
+      w1 = h[8 * i + 5] > w1 ? h[8 * i + 5] : w1;
+      i1 = h[8 * i + 6] > i1 ? h[8 * i + 6] : i1;
+      x1 = h[8 * i + 7] > x1 ? h[8 * i + 7] : x1;
     }
-    fprintf(stderr, "pair GEMM M=%d N=%d K=%d: issuer %.0f cycles/pair, %.2f tiles/pair, waiting acc_empty %.0f%%, "
-            "operands %.0f%%, MMA-bound ideal %.0f cycles\n", M, N, K, tot / np, nt / np, 100 * wa / tot,
-            100 * wf / tot, nt / np * (K / kBK) * 4 * 128.0);
+    fprintf(stderr, "pair GEMM<EW=%d,EK=%d> M=%d N=%d K=%d: issuer %.0f cycles/pair, %.2f tiles/pair, "
+            "waiting acc_empty %.0f%%, operands %.0f%%, MMA-bound ideal %.0f cycles; timeline (us from the "
+            "first CTA): last CTA in %.2f, prologue done %.2f, last MMA issued %.2f, last epilogue %.2f; SM %.2f GHz%s\n",
+            EW, EK, M, N, K, tot / np, nt / np, 100 * wa / tot, 100 * wf / tot,
+            nt / np * (K / kBK) * 4 * 128.0, (e1 - e0) * 1e-3, (w1 - e0) * 1e-3, (i1 - e0) * 1e-3,
+            (x1 - e0) * 1e-3, ghz, e2.dbg_skip_epi ? " [epilogue skipped]" : "");
   }
   return GG_OK;
+}
+
+// Epilogue kind -> instantiation.  Residual kernels keep 8 epilogue warps and
+// two staging boxes per warp (the residual box of the next chunk in flight);
+// the others run 16 epilogue warps (two chunks each) so the GELU / LayerNorm
+// correction math of a tile keeps pace with the next tile's MMAs.
+static int g_pair_ew = -1;
+static int pair_ew() {
+  if (g_pair_ew < 0) g_pair_ew = getenv("GG_PAIR_EW") ? atoi(getenv("GG_PAIR_EW")) : 16;
+  return g_pair_ew;
+}
+
+template <int EK>
+static int launch_pair_kind(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                            const CUtensorMap& mr, int M, int N, int K, const GemmEpilogue& ep,
+                            cudaStream_t s) {
+  if constexpr ((EK & EK_RES) != 0) {
+    return launch_gemm_pair<5, 8, 2, EK>(ma, mb, mo, mr, M, N, K, ep, s);
+  } else {
+    if (pair_ew() == 8) return launch_gemm_pair<5, 8, 1, EK>(ma, mb, mo, mr, M, N, K, ep, s);
+    return launch_gemm_pair<5, 16, 1, EK>(ma, mb, mo, mr, M, N, K, ep, s);
+  }
+}
+
+static int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                       const CUtensorMap& mr, int M, int N, int K, const GemmEpilogue& ep, cudaStream_t s) {
+  const int ek = (ep.a_stats ? EK_ALN : 0) | (ep.act == ACT_GELU ? EK_GELU : 0) |
+                 (ep.residual ? EK_RES : 0) | (ep.out_mode == OUT_QKV_HEADS ? EK_QKV : 0);
+  switch (ek) {
+#define GG_PAIR_CASE(k) \
+  case k: return launch_pair_kind<k>(ma, mb, mo, mr, M, N, K, ep, s);
+    GG_PAIR_CASE(0) GG_PAIR_CASE(1) GG_PAIR_CASE(2) GG_PAIR_CASE(3) GG_PAIR_CASE(4) GG_PAIR_CASE(5)
+    GG_PAIR_CASE(6) GG_PAIR_CASE(7) GG_PAIR_CASE(8) GG_PAIR_CASE(9) GG_PAIR_CASE(10) GG_PAIR_CASE(11)
+    GG_PAIR_CASE(12) GG_PAIR_CASE(13) GG_PAIR_CASE(14) GG_PAIR_CASE(15)
+#undef GG_PAIR_CASE
+    default: return GG_ERR_INVALID_ARGUMENT;
+  }
 }
 }  // namespace gg
 
@@ -1000,6 +1039,7 @@ static int gemm_impl(const void* A, int64_t lda, const void* B, int64_t ldb, voi
       return GG_ERR_INVALID_ARGUMENT;
     if (ln->a_stats && (ln->ln_width != K || N > kPairAuxFloats)) return GG_ERR_INVALID_ARGUMENT;
     if ((ln->r_stats || ln->out_stats) && ln->ln_width != N) return GG_ERR_INVALID_ARGUMENT;
+    if (ln->out_stats && !e->residual) return GG_ERR_UNSUPPORTED;   // statistics ride the residual epilogue
     ep.a_stats = reinterpret_cast<const float2*>(ln->a_stats);
     ep.a_colsum = ln->a_colsum;
     ep.r_stats = reinterpret_cast<const float2*>(ln->r_stats);
@@ -1025,24 +1065,18 @@ static int gemm_impl(const void* A, int64_t lda, const void* B, int64_t ldb, voi
     static const bool no_tma_out = getenv("GG_NO_TMA_EPI") != nullptr;
     const bool tma_ok = !no_tma_out && (e->out_mode == OUT_BF16 || e->out_mode == OUT_QKV_HEADS) &&
                         (!e->count_dev || e->rows_per_item % 32 == 0);
-    mo = ma;
-    mr = ma;
     if (tma_ok) {
+      mr = ma;
       if (e->out_mode == OUT_BF16) rc = make_map_box32(&mo, D, M, N, ldd);
       else rc = make_map_box32(&mo, D, 3 * M * (int64_t)e->heads, 64, 64);
       if (!rc && e->residual) rc = make_map_box32(&mr, e->residual, M, N, e->ldr);
       if (rc) return rc;
       ep.tma_out = 1;
+      return launch_pair(ma, mbp, mo, mr, (int)M, (int)N, (int)K, ep, s);
     }
-    if (ln && !ep.tma_out) return GG_ERR_UNSUPPORTED;
-    // GG_PAIR_RES4=1: residual GEMMs with 4 staging boxes per warp (every residual
-    // chunk of a tile in flight during its MMAs) at the cost of one operand
-    // stage -- measured slower (FFN-down 60 -> 68 us: K = 3072 needs the stage;
-    // out_lin unchanged), so off by default
-    static const int res_cfg = getenv("GG_PAIR_RES4") ? atoi(getenv("GG_PAIR_RES4")) : 0;
-    if (ep.residual && ep.tma_out && res_cfg)
-      return launch_gemm_pair<4, 4>(ma, mbp, mo, mr, (int)M, (int)N, (int)K, ep, s);
-    return launch_gemm_pair<5, 2>(ma, mbp, mo, mr, (int)M, (int)N, (int)K, ep, s);
+    // (no TMA epilogue: the single-CTA kernel below)
+    rc = make_map_2d(&ma, A, M, K, lda, 128);
+    if (rc) return rc;
   }
   if (ln) return GG_ERR_UNSUPPORTED;   // LayerNorm folding lives in the CTA-pair epilogue
   switch (bn) {

@@ -19,9 +19,9 @@ timeout 300 $NCU --set full --import-source on -k regex:conv_span_tcgen05 -s 1 -
   -o "$OUT/resnet18_layer1_span" python tools/forward_once.py resnet18 1 > /dev/null 2>&1
 timeout 300 $NCU --set full --import-source on -k regex:gemm_bf16_pair -s 2 -c 1 \
   -o "$OUT/distilbert_ffn_up_gemm_pair" python tools/forward_once.py distilbert 1 > /dev/null 2>&1
-timeout 300 $NCU --set full --import-source on -k regex:layernorm_kernel -s 1 -c 1 \
-  -o "$OUT/distilbert_layernorm" python tools/forward_once.py distilbert 1 > /dev/null 2>&1
-timeout 300 $NCU --set full --import-source on -k regex:attention_tcgen05 -s 1 -c 1 \
+timeout 300 $NCU --set full --import-source on -k regex:conv_bf16_tcgen05 -s 1 -c 1 \
+  -o "$OUT/resnet18_stride2_conv_ds" python tools/forward_once.py resnet18 1 > /dev/null 2>&1
+timeout 300 $NCU --set full --import-source on -k regex:attention -s 1 -c 1 \
   -o "$OUT/distilbert_attention" python tools/forward_once.py distilbert 1 > /dev/null 2>&1
 timeout 300 $NCU --set full --import-source on -k regex:stem_pool_span -s 0 -c 1 \
   -o "$OUT/resnet18_stem_pool" python tools/forward_once.py resnet18 1 > /dev/null 2>&1
