@@ -84,6 +84,35 @@ int gg_gemm_ln(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, 
                int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* epilogue,
                const gg_gemm_ln_params* ln, void* stream);
 
+/* Tile-level dependencies between consecutive forward kernels, instead of the
+ * grid-wide wait of programmatic dependent launch.  Rows are grouped in units
+ * of 128 (one DistilBERT sequence); every kernel of the chain counts, per unit,
+ * the column tiles (GEMM) or heads (attention) it has finished and published.
+ *   wait    the producing kernel's counters [units], or NULL: grid-wide wait on
+ *           the stream predecessor (the first kernel of a chain)
+ *   need    unit u is ready when wait[u] >= need (the producer's tiles per unit)
+ *   signal  this kernel's counters [units] (+1 per finished tile / head), or NULL
+ *   go      chain flag: the first kernel sets it to 1 after its grid-wide wait;
+ *           the others wait for it before reading count_dev
+ *   tiles   this launch's tile counter (GEMM): tiles are claimed dynamically in
+ *           row-block order, so CTAs that start early take more; NULL = static
+ * The caller zeroes every counter and `go` before the chain (gg_zero_async).
+ * Consumers must run after their producers in the same stream; a kernel whose
+ * CTAs are all resident only waits on kernels launched before it, so the chain
+ * cannot deadlock.  Rows must be consumed in whole units (rows_per_item % 128). */
+typedef struct {
+  const int32_t* wait;
+  int32_t need;
+  int32_t* signal;
+  int32_t* go;
+  int32_t* tiles;
+} gg_dep;
+int gg_gemm_dep(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
+                int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* epilogue,
+                const gg_gemm_ln_params* ln /* or NULL */, const gg_dep* dep, void* stream);
+/* cudaMemsetAsync(ptr, 0, bytes) on the stream (counter reset, graph-capturable). */
+int gg_zero_async(void* ptr, int64_t bytes, void* stream);
+
 /* Allocate this device's stream-K workspace (48 MB fp32 partial tiles + 2 MB
  * counters) now, outside any CUDA graph capture.  gg_gemm / gg_conv2d split
  * their (tile, k-block) space evenly over the SMs when the tile count leaves a
@@ -103,6 +132,11 @@ int gg_streamk_mode(int32_t mode);
  * Requires S == 128. */
 int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int64_t ldc, int32_t batch,
                  int32_t heads, int32_t seq_len, const int32_t* count_dev, void* stream);
+/* gg_attention with tile-level dependencies (gg_dep; unit = sequence b: waits
+ * for wait[b] >= need before loading (b, h), adds 1 to signal[b] per head). */
+int gg_attention_dep(const void* qkv, const int32_t* mask, void* ctx, int64_t ldc, int32_t batch,
+                     int32_t heads, int32_t seq_len, const int32_t* count_dev, const gg_dep* dep,
+                     void* stream);
 
 /* y = LayerNorm(x) * gamma + beta over rows of width `width` (fp32 statistics),
  * bf16 in/out; eps as in the model config (DistilBERT 1e-12). */

@@ -44,6 +44,9 @@ SIGNATURES: dict[str, tuple] = {
     "gg_streamk_reserve": (C.c_int, []),
     "gg_streamk_mode": (C.c_int, [_I32]),
     "gg_attention": (C.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, _P, _P]),
+    "gg_attention_dep": (C.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P]),
+    "gg_gemm_dep": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
+    "gg_zero_async": (C.c_int, [_P, _I64, _P]),
     "gg_layernorm": (C.c_int, [_P, _I64, _P, _I64, _P, _P, _I64, _I32, C.c_float, _P, _I32, _P]),
     "gg_embed_layernorm": (C.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, C.c_float, _P,
                                      _P]),

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kApThreads, 1)
                       const __grid_constant__ CUtensorMap map_k,
                       const __grid_constant__ CUtensorMap map_vt,
                       const __grid_constant__ CUtensorMap map_o, const int32_t* mask, int batch,
-                      int heads, const int32_t* count, int dbg) {
+                      int heads, const int32_t* count, int dbg, gg_dep dep) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kApOffBar);
@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(kApThreads, 1)
   uint64_t* o_full = bars + 12;  // [2] O in TMEM (MMA commit)
   uint64_t* o_empty = bars + 14; // [2] O read by the group's 128 threads
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  int* cnt_slot = reinterpret_cast<int*>(bars + 17);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   griddep_launch();
@@ -243,8 +244,19 @@ __global__ void __launch_bounds__(kApThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  griddep_wait();     // Q/K/V, the mask and the count follow the predecessor
-  const int nb = count ? min(batch, __ldg(count)) : batch;
+  if (dep.wait) {
+    // tile-level dependencies (gg_dep): the count once the chain has started;
+    // each item waits for its sequence's QKV tiles below
+    if (threadIdx.x == 0) {
+      dep_wait_geq(dep.go, 1);
+      *cnt_slot = count ? ld_relaxed_gpu(count) : batch;
+    }
+  } else {
+    griddep_wait();     // Q/K/V, the mask and the count follow the predecessor
+    if (threadIdx.x == 0) *cnt_slot = count ? __ldg(count) : batch;
+  }
+  __syncthreads();
+  const int nb = min(batch, *cnt_slot);
   const int n_items = nb * heads;
 
   if (warp == 0) {
@@ -255,6 +267,10 @@ __global__ void __launch_bounds__(kApThreads, 1)
         const int st = t % kApStages;
         const uint32_t ph = (t / kApStages) & 1;
         mbar_wait(empty + st, ph ^ 1);
+        if (dep.wait) {   // Q, K, V^T of sequence it / heads published by the QKV GEMM
+          dep_wait_geq(dep.wait + it / heads, dep.need);
+          fence_proxy_async_global();
+        }
         uint8_t* sb = smem + kApOffStage + st * kApStageBytes;
         mbar_expect_tx(full + st, 49152 + (mask ? 512 : 0));
         const int li = (dbg & 1) ? (int)blockIdx.x : it;
@@ -332,6 +348,7 @@ __global__ void __launch_bounds__(kApThreads, 1)
     uint8_t* prow = smem + kApOffP + g * 32768 + (row >> 3) * 1024 + (row & 7) * 128;
     uint8_t* orow = smem + kApOffP + g * 32768 + row * 128;   // staging tile reuses P
     int t = g;
+    int prev_b = -1;   // sequence of this group's previous item, published one item late
     for (int it = blockIdx.x + g * gridDim.x; it < n_items; it += 2 * gridDim.x, t += 2) {
       const uint32_t ph = (t >> 1) & 1;
       if (t >= 2) {                        // the previous ctx store has read the P buffer
@@ -423,8 +440,22 @@ __global__ void __launch_bounds__(kApThreads, 1)
         tma_store_2d(&map_o, smem + kApOffP + g * 32768, (it % heads) * kAttnD, (it / heads) * kAttnS);
         bulk_commit();
       }
+      if (leader && dep.signal) {   // the previous item's ctx box has landed: publish it
+        bulk_wait<1>();
+        if (prev_b >= 0) {
+          fence_proxy_async_global();
+          dep_signal_add(dep.signal + prev_b, 1);
+        }
+        prev_b = it / heads;
+      }
     }
-    if (leader) bulk_wait<0>();
+    if (leader) {
+      bulk_wait<0>();
+      if (dep.signal && prev_b >= 0) {
+        fence_proxy_async_global();
+        dep_signal_add(dep.signal + prev_b, 1);
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -438,10 +469,15 @@ __global__ void __launch_bounds__(kApThreads, 1)
 
 using namespace gg;
 
-extern "C" int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int64_t ldc,
-                            int32_t batch, int32_t heads, int32_t seq_len,
-                            const int32_t* count_dev, void* stream) {
+static int attention_impl(const void* qkv, const int32_t* mask, void* ctx, int64_t ldc,
+                          int32_t batch, int32_t heads, int32_t seq_len, const int32_t* count_dev,
+                          const gg_dep* dep_in, void* stream) {
   if (!qkv || !ctx || batch <= 0 || heads <= 0) return GG_ERR_INVALID_ARGUMENT;
+  gg_dep dep{nullptr, 0, nullptr, nullptr, nullptr};
+  if (dep_in && (dep_in->wait || dep_in->signal)) {
+    if (!dep_in->go || (dep_in->wait && dep_in->need <= 0)) return GG_ERR_INVALID_ARGUMENT;
+    dep = *dep_in;
+  }
   if (seq_len != kAttnS || ldc % 8 || ldc < (int64_t)heads * kAttnD) return GG_ERR_UNSUPPORTED;
   const int64_t plane = (int64_t)batch * heads * seq_len * kAttnD;
   const __nv_bfloat16* base = reinterpret_cast<const __nv_bfloat16*>(qkv);
@@ -469,11 +505,12 @@ extern "C" int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int
     }
     const int grid = (int)std::min<int64_t>((int64_t)batch * heads, num_sms());
     if (launch_pdl(attention_persist, dim3(grid), dim3(kApThreads), kApSmem, gg_stream(stream), mq, mk,
-                   mv, mo, mask, batch, heads, count_dev, dbg) != cudaSuccess)
+                   mv, mo, mask, batch, heads, count_dev, dbg, dep) != cudaSuccess)
       return GG_ERR_CUDA;
     GG_LAUNCH_OK();
     return GG_OK;
   }
+  if (dep.wait || dep.signal) return GG_ERR_UNSUPPORTED;   // the per-item kernel has no deps
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(attention_tcgen05, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -486,4 +523,17 @@ extern "C" int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int
     return GG_ERR_CUDA;
   GG_LAUNCH_OK();
   return GG_OK;
+}
+
+extern "C" int gg_attention(const void* qkv, const int32_t* mask, void* ctx, int64_t ldc,
+                            int32_t batch, int32_t heads, int32_t seq_len,
+                            const int32_t* count_dev, void* stream) {
+  return attention_impl(qkv, mask, ctx, ldc, batch, heads, seq_len, count_dev, nullptr, stream);
+}
+
+extern "C" int gg_attention_dep(const void* qkv, const int32_t* mask, void* ctx, int64_t ldc,
+                                int32_t batch, int32_t heads, int32_t seq_len,
+                                const int32_t* count_dev, const gg_dep* dep, void* stream) {
+  if (!dep) return GG_ERR_INVALID_ARGUMENT;
+  return attention_impl(qkv, mask, ctx, ldc, batch, heads, seq_len, count_dev, dep, stream);
 }

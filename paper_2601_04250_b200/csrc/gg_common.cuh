@@ -25,6 +25,36 @@ static inline cudaStream_t gg_stream(void* s) { return reinterpret_cast<cudaStre
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
+// Tile-level dependencies between consecutive kernels (gg_dep): per-unit
+// counters in global memory, released by the producer after its outputs are
+// complete, acquired by the consumer before it reads them.
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void dep_wait_geq(const int* p, int need) {
+  while (ld_acquire_gpu(p) < need) __nanosleep(100);
+}
+__device__ __forceinline__ void dep_signal_add(int* p, int v) {
+  asm volatile("fence.acq_rel.gpu;\n\tred.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void dep_signal_add_nofence(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void dep_set(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// completed bulk (TMA) writes / generic acquires <-> async-proxy accesses of global memory
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // Every fp64 operation of the controller goes through these so the rounding is
 // exactly CPython's (one IEEE rounding per binary op, no FMA contraction).
 __device__ __forceinline__ double f64_add(double a, double b) { return __dadd_rn(a, b); }

@@ -43,6 +43,14 @@ struct GemmEpilogue {
   long long* prof;                 // debug (GG_GEMM_PROF): per-pair issuer cycles / waits, or null
   int tma_out;                     // pair kernel: outputs (and residual) through smem + TMA
   int dbg_skip_epi;                // GG_GEMM_SKIP_EPI (probe): release accumulators without the epilogue
+  // tile-level dependencies (gg_dep, pair kernel): 128-row unit counters
+  const int* dep_wait;
+  int dep_need;
+  int* dep_signal;
+  int* dep_go;
+  int* dep_tiles;                  // dynamic tile counter (zeroed per chain) or null: static schedule
+  int dep_dbg;                     // GG_DEP_DBG probe bits (1 no producer proxy fence, 2 relaxed poll,
+                                   // 4 no signal fences)
   // LayerNorm folding (pair kernel, TMA epilogue; see gg_gemm_ln):
   const float2* a_stats;           // row statistics partials of A (raw h rows), [a_parts][ln_ld]
   const float* a_colsum;           // [N] s_j = sum_k W'_jk (W' = W diag(gamma))
@@ -66,7 +74,7 @@ __device__ __forceinline__ void ln_row_params(const float2* st, int parts, int64
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     if (i < parts) {
-      const float2 v = __ldg(st + (int64_t)i * ld + row);
+      const float2 v = __ldcg(st + (int64_t)i * ld + row);   // L2: written by a live producer
       m[i] = v.x;
       q[i] = v.y;
       mean += v.x;
@@ -525,7 +533,7 @@ enum : int { EK_ALN = 1, EK_GELU = 2, EK_RES = 4, EK_QKV = 8 };
 // chunk's residual lands while this one is computed; otherwise 1).
 template <int STAGES, int EW, int NBUF, int EK>
 struct PairCfg {
-  static constexpr int kThreads = 64 + 32 * EW;
+  static constexpr int kThreads = 96 + 32 * EW;   // + the tile-scheduler warp
   static constexpr int A_BYTES = 128 * kBK * 2, B_BYTES = 128 * kBK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;                  // 512 B of barriers
@@ -538,7 +546,7 @@ struct PairCfg {
 };
 
 template <int STAGES, int EW, int NBUF, int EK>
-__global__ void __launch_bounds__(64 + 32 * EW, 1)
+__global__ void __launch_bounds__(96 + 32 * EW, 1)
     gemm_bf16_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_res,
                    int M_max, int N, int K, GemmEpilogue ep) {
@@ -556,7 +564,12 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   uint64_t* acc_full = empty + STAGES;     // [2]
   uint64_t* acc_empty = acc_full + 2;      // [2] (the leader's counts both CTAs' epilogues)
   uint64_t* res_full = acc_empty + 2;      // [EW warps][NBUF buffers]: residual boxes landed
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(res_full + NBUF * EW);
+  uint64_t* tile_full = res_full + NBUF * EW;   // [4] dynamic schedule: tile index published
+  uint64_t* tile_empty = tile_full + 4;         // [4] (leader) every reader of the slot is done
+  uint64_t* tile_took = tile_empty + 4;         // [4] (leader) its producer started this slot's tile
+  uint64_t* dep_ok = tile_took + 4;             // [8] the producer acquired this tile's unit
+  int* tile_ring = reinterpret_cast<int*>(dep_ok + 8);   // [4] tile indices
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tile_ring + 4);
   float* bias_s = reinterpret_cast<float*>(smem + C::BIAS_OFF);   // [N] (N <= kPairMaxN)
   // per epilogue warp: NBUF 2 KB staging buffers = the SWIZZLE_64B image of a
   // 32 x 32 bf16 box (output for the TMA store, residual from a TMA load)
@@ -584,6 +597,13 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
       mbar_init(&acc_empty[a], 2);   // one elected arrive per CTA of the pair
     }
     for (int i = 0; i < NBUF * EW; ++i) mbar_init(&res_full[i], 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&tile_full[i], 1);
+      // readers: both producers, the leader's MMA warp, both CTAs' epilogue warps
+      mbar_init(&tile_empty[i], 3 + 2 * EW);
+      mbar_init(&tile_took[i], 1);
+    }
+    for (int i = 0; i < 8; ++i) mbar_init(&dep_ok[i], 1);
     fence_mbar_init();
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
@@ -595,20 +615,78 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
   cluster_sync_all();   // barriers of both CTAs initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
-  griddep_wait();
+  int* cnt_slot = reinterpret_cast<int*>(tmem_base_smem + 1);
+  if (ep.dep_wait) {
+    // tile-level dependencies: no grid-wide wait; the batch count is read once
+    // the chain's first kernel has passed its grid-wide wait
+    if (threadIdx.x == 0) {
+      dep_wait_geq(ep.dep_go, 1);
+      *cnt_slot = ep.count ? ld_relaxed_gpu(ep.count) : 0;
+    }
+    __syncthreads();
+  } else {
+    griddep_wait();
+    if (ep.dep_go && blockIdx.x == 0 && threadIdx.x == 0) dep_set(ep.dep_go, 1);
+    if (threadIdx.x == 0) *cnt_slot = ep.count ? __ldg(ep.count) : 0;
+    __syncthreads();
+  }
   if (ep.prof && threadIdx.x == 0 && rank == 0) ep.prof[pair * 8 + 5] = gtimer_ns();
-  const int M = ep.count ? min(M_max, __ldg(ep.count) * ep.rows_per_item) : M_max;
+  const int M = ep.count ? min(M_max, *cnt_slot * ep.rows_per_item) : M_max;
   const int tiles_m = (M + 255) / 256, tiles_n = N / kPairBN;
   const int num_tiles = tiles_m * tiles_n;
+  // Tile schedule.  Static: tile = pair + i * npairs.  Dynamic (dep_tiles): the
+  // leader's scheduler warp claims tiles from a global counter (pairs that start
+  // early -- on SMs the previous kernel's last wave left idle -- take more tiles)
+  // and publishes each index through a 4-slot ring in both CTAs' smem.  A warp of
+  // its own: an mbarrier arrive releases, i.e. waits for the issuing thread's
+  // outstanding atomics, so claims in the producer would stall its TMA issue.
+  const bool dyn = ep.dep_tiles != nullptr;
+  const uint32_t leader_tile_empty0 = mapa_shared(smem_u32(&tile_empty[0]), 0);
+  // reader side: the i-th tile of this CTA (every role except the leader's producer)
+  auto read_tile = [&](int i, bool release) -> int {
+    if (!dyn) return pair + i * npairs;
+    const int slot = i & 3;
+    // the leader's own readers: CTA-scope acquire of the local producer's arrive;
+    // the peer's: cluster-scope acquire of the leader's remote store + arrive
+    if (rank == 0 || (ep.dep_dbg & 32)) mbar_wait(&tile_full[slot], (i >> 2) & 1);
+    else mbar_wait_cluster(&tile_full[slot], (i >> 2) & 1);
+    const int tile = tile_ring[slot];
+    if (release && tile < num_tiles) {   // (control-dependent on the value read)
+      if (rank == 0) mbar_arrive_relaxed(&tile_empty[slot]);
+      else mbar_arrive_cluster_relaxed(leader_tile_empty0 + slot * 8);
+    }
+    return tile;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = pair; tile < num_tiles; tile += npairs) {
+      const uint32_t peer_full0 = mapa_shared(smem_u32(&tile_full[0]), 1);
+      const uint32_t peer_ring0 = mapa_shared(smem_u32(&tile_ring[0]), 1);
+      (void)peer_full0;
+      (void)peer_ring0;
+      for (int i = 0;; ++i) {
+        const int tile = read_tile(i, true);
+        if (tile >= num_tiles) break;
+        if (dyn && rank == 0) mbar_arrive_relaxed(&tile_took[i & 3]);   // the scheduler may claim the next
         const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;   // raster: see gemm_impl
         const int tn = ep.raster_n ? tile % tiles_n : tile / tiles_m;
         const int m0 = tm * 256 + rank * 128, n0 = tn * kPairBN + rank * 128;
+        if (ep.dep_wait) {
+          // this CTA's 128 A rows (unit 2 tm + rank) published by the producer; the
+          // epilogue's residual / statistics reads follow through dep_ok (every
+          // earlier kernel of the chain published before this unit's producer)
+          if (m0 < M) {
+            if (ep.dep_dbg & 2) {
+              while (ld_relaxed_gpu(ep.dep_wait + tm * 2 + rank) < ep.dep_need) __nanosleep(100);
+            } else {
+              dep_wait_geq(ep.dep_wait + tm * 2 + rank, ep.dep_need);
+            }
+            if (!(ep.dep_dbg & 1)) fence_proxy_async_global();
+          }
+          mbar_arrive(&dep_ok[i & 7]);
+        }
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait_sleep(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * C::STAGE_BYTES;
@@ -631,7 +709,16 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
       const uint64_t a_desc0 = sdesc_k_sw128(smem_u32(smem));
       long long w_acc = 0, w_full = 0;            // GG_GEMM_PROF: issuer wait cycles
       const long long t0 = ep.prof ? clock64() : 0;
-      for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
+      for (;; ++t) {
+        int tile;
+        if (dyn) {
+          tile = 0;
+          if (lane == 0) tile = read_tile(t, true);
+          tile = __shfl_sync(0xffffffffu, tile, 0);
+        } else {
+          tile = read_tile(t, false);
+        }
+        if (tile >= num_tiles) break;
         const int acc = t & 1;
         if (ep.prof) {
           const long long a = clock64();
@@ -677,6 +764,25 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
         ep.prof[pair * 8 + 6] = gtimer_ns();
       }
     }
+  } else if (warp == 2 + EW) {
+    // ===== tile scheduler (leader, dynamic schedule): claim, publish to both CTAs
+    if (dyn && rank == 0 && lane == 0) {
+      const uint32_t peer_full0 = mapa_shared(smem_u32(&tile_full[0]), 1);
+      const uint32_t peer_ring0 = mapa_shared(smem_u32(&tile_ring[0]), 1);
+      for (int i = 0;; ++i) {
+        const int slot = i & 3;
+        // at most one claimed tile waits behind the one being loaded: claim tile i
+        // once the producer has started tile i - 1 (pairs finish within ~a tile)
+        if (i > 0) mbar_wait(&tile_took[(i - 1) & 3], ((i - 1) >> 2) & 1);
+        mbar_wait(&tile_empty[slot], ((i >> 2) & 1) ^ 1);
+        const int tile = atomicAdd(ep.dep_tiles, 1);
+        tile_ring[slot] = tile;
+        st_shared_cluster_s32(peer_ring0 + slot * 4, tile);
+        mbar_arrive(&tile_full[slot]);
+        mbar_arrive_cluster(peer_full0 + slot * 8);
+        if (tile >= num_tiles) break;
+      }
+    }
   } else {
     // ===== epilogue warps: TMEM -> registers -> fused math -> SW64 smem box -> TMA store
     // A thread owns one accumulator row, so direct global stores / residual loads
@@ -704,14 +810,32 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
     uint32_t rph = 0;   // parity bit per staging buffer
     const int sw = (lane >> 1) & 3;
     const bool has_bias = ep.bias != nullptr;
+    int prev_unit = -1;   // unit of the previous tile, published one tile late
     int t = 0;
-    for (int tile = pair; tile < num_tiles; tile += npairs, ++t) {
+    for (;; ++t) {
+      int tile;
+      if (dyn) {
+        tile = 0;
+        if (lane == 0) tile = read_tile(t, true);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+      } else {
+        tile = read_tile(t, false);
+      }
+      if (tile >= num_tiles) break;
       const int tm = ep.raster_n ? tile / tiles_n : tile % tiles_m;
       const int tn = ep.raster_n ? tile % tiles_n : tile / tiles_m;
       const int acc = t & 1;
       const int row0 = tm * 256 + rank * 128 + quarter * 32;   // this warp's 32 rows
       const int colw = tn * kPairBN + part * CW;                 // this warp's CW columns
       const bool rows_ok = row0 < M && !ep.dbg_skip_epi;
+      const int unit = tm * 2 + (int)rank;
+      if ((ALN || RES) && ep.dep_wait) {
+        // the residual / statistics rows come from the producer or earlier kernels
+        // of the chain: the local producer acquired this unit (its arrive releases
+        // at CTA scope; the producer is < 8 tiles ahead: 2 TMEM buffers + its ring)
+        mbar_wait(&dep_ok[t & 7], (t >> 3) & 1);
+        if (RES && lane == 0) fence_proxy_async_global();
+      }
       if (RES && rows_ok && lane == 0) {   // residual of chunk 0
         bulk_wait_read<0>();
         mbar_expect_tx(&rb[0], 2048);
@@ -724,6 +848,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
       if (RES && rows_ok && ep.r_stats)
         ln_row_params(ep.r_stats, ep.r_parts, ep.ln_ld, row0 + lane, ep.ln_width, ep.eps, r_sc, r_sh);
       float st_k = 0.0f, st_s1 = 0.0f, st_s2 = 0.0f;   // output row partial (shifted sums)
+      int ngroups = 0;                                   // bulk store groups committed for this tile
       mbar_wait_sleep(&acc_full[acc], (t >> 1) & 1);
       tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * kPairBN + part * CW;
@@ -868,6 +993,7 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
           tma_store_2d(&map_out, buf, gx, gy);
           bulk_commit();
         }
+        ++ngroups;
       }
       if (RES && ep.out_stats && rows_ok) {
         const float n = (float)CW;
@@ -875,14 +1001,38 @@ __global__ void __launch_bounds__(64 + 32 * EW, 1)
         const float m2 = fmaxf(st_s2 - st_s1 * st_s1 / n, 0.0f);
         ep.out_stats[(int64_t)(tn * PARTS + part) * ep.ln_ld + row0 + lane] = make_float2(mi, m2);
       }
+      if (ep.dep_signal && lane == 0) {
+        // the previous tile's stores (older groups than this tile's) are complete
+        if (ngroups == 0) bulk_wait<0>();
+        else if (ngroups == 1) bulk_wait<1>();
+        else if (ngroups == 2) bulk_wait<2>();
+        else if (ngroups == 3) bulk_wait<3>();
+        else bulk_wait<4>();
+        if (!(ep.dep_dbg & 4)) fence_proxy_async_global();
+      }
       tc_fence_before();
       asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
       if (threadIdx.x == 64) {
         if (rank == 0) mbar_arrive(&acc_empty[acc]);
         else mbar_arrive_cluster(leader_empty0 + acc * 8);
+        // publish the previous tile (one tile late: its stores had this tile to land)
+        if (ep.dep_signal && prev_unit >= 0) {
+          // red.release: orders this thread's prior accesses and, cumulatively, the
+          // CTA's output writes it observed through the barrier above
+          if (ep.dep_dbg & 16) dep_signal_add(ep.dep_signal + prev_unit, 1);
+          else dep_signal_add_nofence(ep.dep_signal + prev_unit, 1);
+        }
       }
+      prev_unit = tm * 256 + (int)rank * 128 < M ? unit : -1;
     }
-    if (lane == 0) bulk_wait<0>();
+    if (lane == 0) {
+      bulk_wait<0>();
+      fence_proxy_async_global();
+    }
+    if (ep.dep_signal) {
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+      if (threadIdx.x == 64 && prev_unit >= 0) dep_signal_add_nofence(ep.dep_signal + prev_unit, 1);
+    }
     if (ep.prof && threadIdx.x == 64 && rank == 0) {
       ep.prof[pair * 8 + 7] = gtimer_ns();
       ep.prof[2048 + pair * 2 + 1] = clock64();
@@ -1009,7 +1159,7 @@ using namespace gg;
 
 static int gemm_impl(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
                      int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* e,
-                     const gg_gemm_ln_params* ln, void* stream) {
+                     const gg_gemm_ln_params* ln, const gg_dep* dep, void* stream) {
   if (!A || !B || !D || !e || M <= 0 || N <= 0 || K <= 0) return GG_ERR_INVALID_ARGUMENT;
   if (K % 64 || N % 32 || lda % 8 || ldb % 8 || (e->residual && e->ldr % 8)) return GG_ERR_INVALID_ARGUMENT;
   if (e->act < 0 || e->act > 2 || e->out_mode < 0 || e->out_mode > 2) return GG_ERR_INVALID_ARGUMENT;
@@ -1051,6 +1201,22 @@ static int gemm_impl(const void* A, int64_t lda, const void* B, int64_t ldb, voi
     ep.ln_ld = M;
     ep.eps = ln->eps;
   }
+  if (dep && (dep->wait || dep->signal)) {
+    // tile-level dependencies live in the CTA-pair kernel; units of 128 rows
+    if (M % 128 || (e->count_dev && e->rows_per_item % 128) || (dep->wait && dep->need <= 0) || !dep->go)
+      return GG_ERR_INVALID_ARGUMENT;
+    ep.dep_wait = dep->wait;
+    ep.dep_need = dep->need;
+    ep.dep_signal = dep->signal;
+    ep.dep_go = dep->go;
+    ep.dep_tiles = dep->tiles;
+    static const int dbg = getenv("GG_DEP_DBG") ? atoi(getenv("GG_DEP_DBG")) : 0;
+    ep.dep_dbg = dbg;
+    ep.raster_n = 1;   // row blocks in order: the consumer's readiness follows the producer's
+  }
+  const bool want_dep = ep.dep_wait || ep.dep_signal;
+  static const int raster_env = getenv("GG_RASTER_N") ? atoi(getenv("GG_RASTER_N")) : -1;
+  if (raster_env >= 0) ep.raster_n = raster_env;
   cudaStream_t s = gg_stream(stream);
   // CTA pairs for wide GEMMs (tile_n auto, N % 256 == 0, enough 256-row tiles
   // to fill most pairs); GG_NO_PAIR=1 keeps single-CTA tiles
@@ -1074,11 +1240,12 @@ static int gemm_impl(const void* A, int64_t lda, const void* B, int64_t ldb, voi
       ep.tma_out = 1;
       return launch_pair(ma, mbp, mo, mr, (int)M, (int)N, (int)K, ep, s);
     }
+    if (want_dep) return GG_ERR_UNSUPPORTED;
     // (no TMA epilogue: the single-CTA kernel below)
     rc = make_map_2d(&ma, A, M, K, lda, 128);
     if (rc) return rc;
   }
-  if (ln) return GG_ERR_UNSUPPORTED;   // LayerNorm folding lives in the CTA-pair epilogue
+  if (ln || want_dep) return GG_ERR_UNSUPPORTED;   // LayerNorm folding / deps live in the CTA-pair kernel
   switch (bn) {
     case 256: return launch_gemm<128, 256, 4>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
     case 128: return launch_gemm<128, 128, 6>(ma, mb, (int)M, (int)N, (int)K, ep, s, 0);
@@ -1089,14 +1256,26 @@ static int gemm_impl(const void* A, int64_t lda, const void* B, int64_t ldb, voi
 extern "C" int gg_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
                        int64_t ldd, int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* e,
                        void* stream) {
-  return gemm_impl(A, lda, B, ldb, D, ldd, M, N, K, e, nullptr, stream);
+  return gemm_impl(A, lda, B, ldb, D, ldd, M, N, K, e, nullptr, nullptr, stream);
 }
 
 extern "C" int gg_gemm_ln(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
                           int64_t ldd, int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* e,
                           const gg_gemm_ln_params* ln, void* stream) {
   if (!ln) return GG_ERR_INVALID_ARGUMENT;
-  return gemm_impl(A, lda, B, ldb, D, ldd, M, N, K, e, ln, stream);
+  return gemm_impl(A, lda, B, ldb, D, ldd, M, N, K, e, ln, nullptr, stream);
+}
+
+extern "C" int gg_gemm_dep(const void* A, int64_t lda, const void* B, int64_t ldb, void* D,
+                           int64_t ldd, int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* e,
+                           const gg_gemm_ln_params* ln, const gg_dep* dep, void* stream) {
+  if (!dep) return GG_ERR_INVALID_ARGUMENT;
+  return gemm_impl(A, lda, B, ldb, D, ldd, M, N, K, e, ln, dep, stream);
+}
+
+extern "C" int gg_zero_async(void* ptr, int64_t bytes, void* stream) {
+  if (!ptr || bytes < 0) return GG_ERR_INVALID_ARGUMENT;
+  return cudaMemsetAsync(ptr, 0, (size_t)bytes, gg_stream(stream)) == cudaSuccess ? GG_OK : GG_ERR_CUDA;
 }
 
 extern "C" int gg_streamk_reserve(void) {

@@ -46,6 +46,12 @@ class GemmEpilogue(C.Structure):
                 ("count_dev", C.c_void_p)]
 
 
+class GgDep(C.Structure):
+    """gg_dep (include/greengate_b200_forward.h): tile-level dependencies."""
+    _fields_ = [("wait", C.c_void_p), ("need", C.c_int32), ("signal", C.c_void_p), ("go", C.c_void_p),
+                ("tiles", C.c_void_p)]
+
+
 class GemmLn(C.Structure):
     """gg_gemm_ln_params (include/greengate_b200_forward.h)."""
     _fields_ = [("a_stats", C.c_void_p), ("a_colsum", C.c_void_p), ("r_stats", C.c_void_p),
@@ -55,7 +61,7 @@ class GemmLn(C.Structure):
 
 def gemm(lib, A, lda, W, D, ldd, M, N, K, stream, bias=None, residual=None, act=NONE,
          out_mode=OUT_BF16, seq_len=0, heads=0, tile_n=0, count=None, rows_per_item=1, ln=None,
-         ldr=None):
+         ldr=None, dep=None):
     res_ptr = None if residual is None else (residual if isinstance(residual, int)
                                              else residual.data_ptr())
     if residual is not None and ldr is None:
@@ -64,7 +70,11 @@ def gemm(lib, A, lda, W, D, ldd, M, N, K, stream, bias=None, residual=None, act=
                       0 if residual is None else ldr, act, out_mode, seq_len,
                       heads, tile_n, rows_per_item if count is not None else 0,
                       None if count is None else count.data_ptr())
-    if ln is None:
+    if dep is not None:
+        _native.check("gg_gemm_dep", lib.gg_gemm_dep(
+            C.c_void_p(A), lda, _native.ptr(W), W.stride(0), C.c_void_p(D), ldd, M, N, K,
+            C.byref(ep), None if ln is None else C.byref(ln), C.byref(dep), stream))
+    elif ln is None:
         _native.check("gg_gemm", lib.gg_gemm(C.c_void_p(A), lda, _native.ptr(W), W.stride(0),
                                              C.c_void_p(D), ldd, M, N, K, C.byref(ep), stream))
     else:
@@ -141,6 +151,17 @@ class DistilBertB200:
         parts = self.DIM // 128
         self.st1 = torch.empty((parts, M, 2), dtype=torch.float32, device=self.device)
         self.st2 = torch.empty((parts, M, 2), dtype=torch.float32, device=self.device)
+        # tile-level dependencies between the encoder's kernels (gg_dep; folded path):
+        # [go | per layer: QKV, attention, out_lin, lin1, lin2 counters per sequence |
+        #  per layer and kernel: dynamic tile counter]
+        # Opt-in (GG_DEP=1): measured no faster than grid-wide PDL waits on B200 --
+        # the row-block raster and per-tile signalling cost the QKV / lin1 epilogues
+        # about what the overlap of kernel tails recovers.
+        self.use_deps = self.fused_ln and os.environ.get("GG_DEP") == "1"
+        self.dyn_tiles = os.environ.get("GG_STATIC_TILES") != "1"
+        nl = len(self.layers)
+        self.deps = torch.zeros(1 + nl * 5 * max_batch + nl * 5, dtype=torch.int32,
+                                device=self.device)
 
     def _fold_layernorms(self, sd) -> None:
         """W' = W diag(gamma) (bf16), s_j = sum_k W'_jk and c_j = b_j + sum_k beta_k W_jk
@@ -230,6 +251,26 @@ class DistilBertB200:
     def _forward_folded(self, B, S, D, M, st, cnt, count, dyn):
         """Encoder with every LayerNorm folded into the GEMMs (class docstring)."""
         lib, eps = self.lib, self.EPS
+        # Tile-level dependencies: each kernel of the encoder waits per sequence for
+        # the tiles it reads instead of the whole previous grid, so a kernel's first
+        # tiles start on the SMs its predecessor's last wave leaves idle.
+        dp = self.deps.data_ptr()
+        nl, mb = len(self.layers), self.max_batch
+        go = C.c_void_p(dp)
+
+        def ctr(i, k):   # k: 0 QKV, 1 attention, 2 out_lin, 3 lin1, 4 lin2
+            return C.c_void_p(dp + 4 * (1 + (i * 5 + k) * mb))
+
+        def dep(i, k, wait, need):
+            if not self.use_deps:
+                return None
+            sig = ctr(i, k) if not (i == nl - 1 and k == 4) else None
+            tiles = C.c_void_p(dp + 4 * (1 + nl * 5 * mb + i * 5 + k)) if self.dyn_tiles else None
+            return GgDep(wait, need, sig, go, tiles)
+        if self.use_deps:
+            _native.check("gg_zero_async", lib.gg_zero_async(_native.ptr(self.deps),
+                                                             self.deps.numel() * 4, st))
+        H = self.HEADS
         x0 = self.x.data_ptr()       # embeddings + LayerNorm (normalized)
         hA = self.x1.data_ptr()      # h1 = ctx W_o^T + b_o + x   (raw, LN1 folded downstream)
         hB = self.h.data_ptr()       # h2 = ffn W_2^T + b_2 + x1  (raw, LN2 folded downstream)
@@ -237,32 +278,43 @@ class DistilBertB200:
         f = C.c_float(eps)
         for i, L in enumerate(self.layers):
             P = self.layers[i - 1] if i > 0 else None
+            # QKV waits for the previous layer's lin2 (3 column tiles per sequence)
+            d_qkv = dep(i, 0, None if i == 0 else ctr(i - 1, 4), 3)
             if i == 0:
                 gemm(lib, x0, D, L["w_qkv"], self.qkv.data_ptr(), 3 * D, M, 3 * D, D, st,
-                     bias=L["b_qkv"], out_mode=OUT_QKV, seq_len=S, heads=self.HEADS, **dyn)
+                     bias=L["b_qkv"], out_mode=OUT_QKV, seq_len=S, heads=H, dep=d_qkv, **dyn)
             else:
                 gemm(lib, hB, D, L["w_qkv_f"], self.qkv.data_ptr(), 3 * D, M, 3 * D, D, st,
-                     bias=L["c_qkv"], out_mode=OUT_QKV, seq_len=S, heads=self.HEADS,
-                     ln=GemmLn(p2, L["s_qkv"].data_ptr(), None, None, None, None, D, f), **dyn)
-            _native.check("gg_attention", lib.gg_attention(
-                _native.ptr(self.qkv), _native.ptr(self._mask), _native.ptr(self.ctx), D, B,
-                self.HEADS, S, cnt, st))
+                     bias=L["c_qkv"], out_mode=OUT_QKV, seq_len=S, heads=H,
+                     ln=GemmLn(p2, L["s_qkv"].data_ptr(), None, None, None, None, D, f),
+                     dep=d_qkv, **dyn)
+            d_att = dep(i, 1, ctr(i, 0), 3 * D // 256)
+            if d_att is None:
+                _native.check("gg_attention", lib.gg_attention(
+                    _native.ptr(self.qkv), _native.ptr(self._mask), _native.ptr(self.ctx), D, B,
+                    H, S, cnt, st))
+            else:
+                _native.check("gg_attention_dep", lib.gg_attention_dep(
+                    _native.ptr(self.qkv), _native.ptr(self._mask), _native.ptr(self.ctx), D, B,
+                    H, S, cnt, C.byref(d_att), st))
+            d_out = dep(i, 2, ctr(i, 1), H)
             if i == 0:   # residual = x0 (already normalized)
                 gemm(lib, self.ctx.data_ptr(), D, L["w_o"], hA, D, M, D, D, st, bias=L["b_o"],
                      residual=x0, ldr=D,
-                     ln=GemmLn(None, None, None, None, None, p1, D, f), **dyn)
+                     ln=GemmLn(None, None, None, None, None, p1, D, f), dep=d_out, **dyn)
             else:        # residual = LN2_{i-1}(h2)
                 gemm(lib, self.ctx.data_ptr(), D, L["w_o"], hA, D, M, D, D, st, bias=L["b_o"],
                      residual=hB, ldr=D,
                      ln=GemmLn(None, None, p2, P["ln2_g"].data_ptr(), P["ln2_b"].data_ptr(), p1,
-                               D, f), **dyn)
+                               D, f), dep=d_out, **dyn)
             gemm(lib, hA, D, L["w1_f"], self.ffn.data_ptr(), self.FFN, M, self.FFN, D, st,
                  bias=L["c_1"], act=GELU,
-                 ln=GemmLn(p1, L["s_1"].data_ptr(), None, None, None, None, D, f), **dyn)
+                 ln=GemmLn(p1, L["s_1"].data_ptr(), None, None, None, None, D, f),
+                 dep=dep(i, 3, ctr(i, 2), D // 256), **dyn)
             gemm(lib, self.ffn.data_ptr(), self.FFN, L["w2"], hB, D, M, D, self.FFN, st,
                  bias=L["b2"], residual=hA, ldr=D,
                  ln=GemmLn(None, None, p1, L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), p2, D, f),
-                 **dyn)
+                 dep=dep(i, 4, ctr(i, 3), self.FFN // 256), **dyn)
         last = self.layers[-1]
         # the head reads only the CLS rows: LayerNorm of those B rows (stride S*D)
         _native.check("gg_layernorm", lib.gg_layernorm(

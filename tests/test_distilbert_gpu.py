@@ -101,3 +101,43 @@ def test_distilbert_layernorm_folding(env, fold, monkeypatch):
     err = (out - ref).abs().max().item()
     print(f"distilbert b=32 fold={fold}: max |logit err| = {err:.3e}")
     assert err <= 2e-2, err
+
+
+def test_distilbert_dependency_chain(env):
+    """Tile-level dependencies (gg_dep) between the encoder's kernels produce the
+    same logits bit for bit as grid-wide waits, at the full batch and at a
+    dynamic count (the counters of units beyond the count are never awaited),
+    over repeated forwards (counters re-zeroed per forward), inside a CUDA graph."""
+    torch = env[0]
+    from paper_2601_04250_b200.distilbert import DistilBertB200, random_model
+    model = random_model(0)
+    ids = torch.randint(0, model.config.vocab_size, (128, 128),
+                        generator=torch.Generator().manual_seed(5)).to(torch.int32).cuda()
+    mask = torch.ones((128, 128), dtype=torch.int32, device="cuda")
+    mask[7, 90:] = 0
+    net = DistilBertB200(model, max_batch=128)
+    assert net.fused_ln
+    outs = {}
+    for use in (False, True):
+        net.use_deps = use
+        for cnt in (128, 45):
+            count = torch.tensor([cnt], dtype=torch.int32, device="cuda")
+            for _ in range(3):
+                out = net.forward(ids, mask, count=count).clone()
+            outs[(use, cnt)] = out
+    torch.cuda.synchronize()
+    for cnt in (128, 45):
+        assert torch.equal(outs[(True, cnt)][:cnt], outs[(False, cnt)][:cnt])
+    # the captured graph replays the chain (memset node + kernels) identically
+    net.use_deps = True
+    count = torch.tensor([128], dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        net.forward(ids, mask, count=count, stream=s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            gout = net.forward(ids, mask, count=count, stream=s)
+    for _ in range(5):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(gout, outs[(True, 128)])
