@@ -465,6 +465,280 @@ __global__ void __launch_bounds__(kApThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// attention_tp: attention_persist with the probabilities kept in tensor memory.
+// The softmax writes its unnormalized bf16 P row back into the first 64 TMEM
+// columns of its own S buffer (tcgen05.st) and O = P V reads A from TMEM (the
+// "ts" MMA form), so P never touches shared memory: no P stores, no async-proxy
+// fence, and the 64 KB of P buffers become a fourth load stage (HBM / L2
+// latency: loads in flight per SM).  S(t + 2) of a group is issued only after
+// O(t) (same TMEM columns; MMAs execute in issue order).
+//   smem: 4 stages x (Q 16K | K 16K | V^T 16K), 2 x 16 KB ctx staging tiles,
+//         4 x 512 B key-mask rows, barriers
+//   TMEM: S / P buffers [0, 256) (128 columns per group), O buffers [256, 384)
+constexpr int kTpStageBytes = 49152;
+constexpr int kTpOffStg = 4 * kTpStageBytes;              // 2 x 16 KB
+constexpr int kTpOffMask = kTpOffStg + 2 * 16384;         // 4 x 512 B
+constexpr int kTpOffBar = kTpOffMask + 4 * 512;
+constexpr int kTpSmemNeed = kTpOffBar + 256;              // from a 1 KB-aligned base
+constexpr int kTpSmem = 232448;                           // the per-CTA maximum
+
+__global__ void __launch_bounds__(kApThreads, 1)
+    attention_tp(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                 const __grid_constant__ CUtensorMap map_vt, const __grid_constant__ CUtensorMap map_o,
+                 const int32_t* mask, int batch, int heads, const int32_t* count, gg_dep dep) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t raw_u32 = smem_u32(smem_raw);
+  const uint32_t pad = ((raw_u32 + 1023u) & ~1023u) - raw_u32;
+  uint8_t* smem = smem_raw + pad;
+  // four stages when the window's alignment leaves room, else three
+  const int nst = (int)pad + kTpSmemNeed <= kTpSmem ? 4 : 3;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (nst == 4 ? kTpOffBar : kTpOffBar - kTpStageBytes));
+  uint8_t* stg0 = smem + (nst == 4 ? kTpOffStg : kTpOffStg - kTpStageBytes);
+  uint8_t* mask0 = smem + (nst == 4 ? kTpOffMask : kTpOffMask - kTpStageBytes);
+  uint64_t* full = bars;          // [4] stage loaded (tx bytes)
+  uint64_t* empty = bars + 4;     // [4] stage free (MMA commit after O)
+  uint64_t* s_full = bars + 8;    // [2] S in TMEM, per group
+  uint64_t* p_full = bars + 10;   // [2] P written to TMEM by the group's 128 threads
+  uint64_t* o_full = bars + 12;   // [2] O in TMEM
+  uint64_t* o_empty = bars + 14;  // [2] O read by the group's 128 threads
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  int* cnt_slot = reinterpret_cast<int*>(bars + 17);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  griddep_launch();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(p_full + i, 128);
+      mbar_init(o_full + i, 1);
+      mbar_init(o_empty + i, 128);
+    }
+    fence_mbar_init();
+    tma_prefetch(&map_q);
+    tma_prefetch(&map_k);
+    tma_prefetch(&map_vt);
+    tma_prefetch(&map_o);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (dep.wait) {
+    if (threadIdx.x == 0) {
+      dep_wait_geq(dep.go, 1);
+      *cnt_slot = count ? ld_relaxed_gpu(count) : batch;
+    }
+  } else {
+    griddep_wait();     // Q/K/V, the mask and the count follow the predecessor
+    if (threadIdx.x == 0) *cnt_slot = count ? __ldg(count) : batch;
+  }
+  __syncthreads();
+  const int nb = min(batch, *cnt_slot);
+  const int n_items = nb * heads;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (elect_one_sync()) {
+      int t = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++t) {
+        const int st = t % nst;
+        const uint32_t ph = (t / nst) & 1;
+        mbar_wait(empty + st, ph ^ 1);
+        if (dep.wait) {
+          dep_wait_geq(dep.wait + it / heads, dep.need);
+          fence_proxy_async_global();
+        }
+        uint8_t* sb = smem + st * kTpStageBytes;
+        mbar_expect_tx(full + st, 49152 + (mask ? 512 : 0));
+        tma_load_2d(sb, &map_q, full + st, 0, it * kAttnS);
+        tma_load_2d(sb + 16384, &map_k, full + st, 0, it * kAttnS);
+        tma_load_2d(sb + 32768, &map_vt, full + st, 0, it * kAttnD);
+        tma_load_2d(sb + 40960, &map_vt, full + st, 64, it * kAttnD);
+        if (mask) bulk_load(mask0 + st * 512, mask + (int64_t)(it / heads) * kAttnS, 512, full + st);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (non-blocking scheduler) ----------------
+    constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128);
+    constexpr uint32_t idesc_o = idesc_bf16_f32(128, 64);
+    const int my_items = blockIdx.x < n_items ? (n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    int ns = 0, no = 0;   // next item to issue S for / O for
+    while (no < my_items) {
+      bool done_any = false;
+      // S(ns) once its stage landed and O(ns - 2) (same group, same TMEM columns) is issued
+      if (ns < my_items && ns < no + 2) {
+        const int st = ns % nst, gb = ns & 1;
+        if (mbar_test(full + st, (ns / nst) & 1)) {
+          tc_fence_after();
+          if (elect_one_sync()) {
+            const uint32_t sq = smem_u32(smem + st * kTpStageBytes);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              umma_bf16(tmem + gb * 128, sdesc_k_sw128(sq + kk * 32), sdesc_k_sw128(sq + 16384 + kk * 32),
+                        idesc_s, kk != 0);
+            umma_commit(s_full + gb);
+          }
+          __syncwarp();
+          ++ns;
+          done_any = true;
+        }
+      }
+      if (no < ns) {
+        const int ub = no & 1;
+        const uint32_t uph = (no >> 1) & 1;
+        if (mbar_test(p_full + ub, uph) && mbar_test(o_empty + ub, uph ^ 1)) {
+          tc_fence_after();
+          if (elect_one_sync()) {
+            const uint32_t sv = smem_u32(smem + (no % nst) * kTpStageBytes + 32768);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)   // K = 128 keys: P columns 8 kk.., V^T key block kk / 4
+              umma_bf16_ts(tmem + 256 + ub * 64, tmem + ub * 128 + kk * 8,
+                           sdesc_k_sw128(sv + (kk >> 2) * 8192 + (kk & 3) * 32), idesc_o, kk != 0);
+            umma_commit(o_full + ub);
+            umma_commit(empty + no % nst);
+          }
+          __syncwarp();
+          ++no;
+          done_any = true;
+        }
+      }
+      if (!done_any) __nanosleep(32);
+    }
+  } else {
+    // ------- compute groups: softmax + epilogue, thread = query row -------
+    const int g = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const bool leader = threadIdx.x == 64 + 128 * g;
+    const float l2e = 1.4426950408889634f;
+    uint8_t* stg = stg0 + g * 16384;
+    uint8_t* orow = stg + row * 128;
+    int t = g;
+    int prev_b = -1;
+    for (int it = blockIdx.x + g * gridDim.x; it < n_items; it += 2 * gridDim.x, t += 2) {
+      const uint32_t ph = (t >> 1) & 1;
+      // ---- softmax(t): two passes over the row's 128 scores straight from TMEM
+      // (max, then exp -> bf16 P back into TMEM), 64 / 32 scores in registers
+      mbar_wait(s_full + g, ph);
+      tc_fence_after();
+      const int4* mrow = reinterpret_cast<const int4*>(mask0 + (t % nst) * 512);
+      auto apply_mask = [&](uint32_t (&r)[32], int c) {
+        if (!mask) return;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const int4 m4 = mrow[(c * 32 + i) >> 2];   // same address in every lane: broadcast
+          if (m4.x == 0) r[i] = __float_as_uint(-INFINITY);
+          if (m4.y == 0) r[i + 1] = __float_as_uint(-INFINITY);
+          if (m4.z == 0) r[i + 2] = __float_as_uint(-INFINITY);
+          if (m4.w == 0) r[i + 3] = __float_as_uint(-INFINITY);
+        }
+      };
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; c += 2) {
+        uint32_t r0[32], r1[32];
+        tmem_ld_32x32b_x32(lane_base + g * 128 + c * 32, r0);
+        tmem_ld_32x32b_x32(lane_base + g * 128 + c * 32 + 32, r1);
+        tmem_ld_wait();
+        apply_mask(r0, c);
+        apply_mask(r1, c + 1);
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          mx = fmax3(mx, __uint_as_float(r0[i]), __uint_as_float(r0[i + 1]));
+          mx = fmax3(mx, __uint_as_float(r1[i]), __uint_as_float(r1[i + 1]));
+        }
+      }
+      const float mref = (mx == -INFINITY) ? 0.0f : mx * l2e;
+      const uint64_t l2e2 = f2_pack(l2e, l2e), nm2 = f2_pack(-mref, -mref);
+      uint64_t sum2 = f2_pack(0.0f, 0.0f);
+      // unnormalized P row (every value <= 1), bf16 pairs -> TMEM columns [g*128, g*128 + 64):
+      // chunk c's 16 packed columns overwrite scores this thread has already read
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(lane_base + g * 128 + c * 32, r);
+        tmem_ld_wait();
+        apply_mask(r, c);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float y0, y1;
+          f2_unpack(f2_fma(f2_pack(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), l2e2, nm2), y0, y1);
+          const float e0 = ex2_approx(y0), e1 = ex2_approx(y1);
+          sum2 = f2_add(sum2, f2_pack(e0, e1));
+          pk[i >> 1] = pack_bf16(e0, e1);
+        }
+        tmem_st_32x32b_x16(lane_base + g * 128 + c * 16, pk);
+      }
+      float s0, s1;
+      f2_unpack(sum2, s0, s1);
+      const float sum = s0 + s1;
+      const float inv = sum > 0.0f ? 1.0f / sum : 0.0f;
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(p_full + g);
+      // ---- epilogue(t): O row / sum -> bf16 -> SW128 staging -> TMA store
+      mbar_wait(o_full + g, ph);
+      tc_fence_after();
+      uint32_t o[2][32];
+      tmem_ld_32x32b_x32(lane_base + 256 + g * 64, o[0]);
+      tmem_ld_32x32b_x32(lane_base + 256 + g * 64 + 32, o[1]);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(o_empty + g);
+      if (t >= 2) {                        // the previous ctx store has read the staging tile
+        if (leader) bulk_wait_read<0>();
+        named_bar_sync(1 + g, 128);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint32_t* v = &o[c >> 2][(c & 3) * 8];
+        uint4 u;
+        u.x = pack_bf16(__uint_as_float(v[0]) * inv, __uint_as_float(v[1]) * inv);
+        u.y = pack_bf16(__uint_as_float(v[2]) * inv, __uint_as_float(v[3]) * inv);
+        u.z = pack_bf16(__uint_as_float(v[4]) * inv, __uint_as_float(v[5]) * inv);
+        u.w = pack_bf16(__uint_as_float(v[6]) * inv, __uint_as_float(v[7]) * inv);
+        *reinterpret_cast<uint4*>(orow + ((c ^ (row & 7)) << 4)) = u;
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1 + g, 128);
+      if (leader) {
+        tma_store_2d(&map_o, stg, (it % heads) * kAttnD, (it / heads) * kAttnS);
+        bulk_commit();
+        if (dep.signal) {   // the previous item's ctx box has landed: publish it
+          bulk_wait<1>();
+          if (prev_b >= 0) {
+            fence_proxy_async_global();
+            dep_signal_add(dep.signal + prev_b, 1);
+          }
+          prev_b = it / heads;
+        }
+      }
+    }
+    if (leader) {
+      bulk_wait<0>();
+      if (dep.signal && prev_b >= 0) {
+        fence_proxy_async_global();
+        dep_signal_add(dep.signal + prev_b, 1);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace gg
 
 using namespace gg;
@@ -492,6 +766,25 @@ static int attention_impl(const void* qkv, const int32_t* mask, void* ctx, int64
   // 1 = every CTA reloads its first item (L2-resident loads), 2 = no exp in the
   // softmax, 4 = no ctx stores
   static const int dbg = getenv("GG_ATTN_DBG") ? atoi(getenv("GG_ATTN_DBG")) : 0;
+  static const bool smem_p = getenv("GG_ATTN_SMEM_P") != nullptr;   // A/B: P through shared memory
+  if (!simple && !smem_p && !dbg) {
+    CUtensorMap mo;
+    if (int rc2 = make_map_2d(&mo, ctx, (int64_t)batch * seq_len, (int64_t)heads * kAttnD, ldc, 128))
+      return rc2;
+    static bool tattr = false;
+    if (!tattr) {
+      if (cudaFuncSetAttribute(attention_tp, cudaFuncAttributeMaxDynamicSharedMemorySize, kTpSmem) !=
+          cudaSuccess)
+        return GG_ERR_CUDA;
+      tattr = true;
+    }
+    const int grid = (int)std::min<int64_t>((int64_t)batch * heads, num_sms());
+    if (launch_pdl(attention_tp, dim3(grid), dim3(kApThreads), kTpSmem, gg_stream(stream), mq, mk, mv, mo,
+                   mask, batch, heads, count_dev, dep) != cudaSuccess)
+      return GG_ERR_CUDA;
+    GG_LAUNCH_OK();
+    return GG_OK;
+  }
   if (!simple) {
     CUtensorMap mo;
     if (int rc2 = make_map_2d(&mo, ctx, (int64_t)batch * seq_len, (int64_t)heads * kAttnD, ldc, 128))
