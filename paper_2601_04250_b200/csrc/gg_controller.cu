@@ -491,7 +491,9 @@ __device__ __forceinline__ int fast_row(const double* x, int k, double now, cons
   for (int c = 0; c < (KC > 0 ? KC : 16); ++c) {
     if (KC == 0 && c >= k) break;
     const double xc = x[c];
-    ok = ok && (xc >= 0.0) && (xc <= 1.7976931348623157e308);   // finite and >= 0
+    // finite and >= 0.  K = 2: x >= 0 alone suffices -- NaN fails it, and an
+    // infinite value (the other one >= 0) makes the total inf, failing the sum check
+    ok = ok && (xc >= 0.0) && (KC == 2 || xc <= 1.7976931348623157e308);
     if (KC != 2) ns.add(xc);
     if (entropy) {   // p log2 p; u = -sum / log2 K (the ln 2 factors cancel)
       const float pf = (float)xc;
