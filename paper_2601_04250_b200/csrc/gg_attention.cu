@@ -10,6 +10,7 @@
 //   MMA 2: O = P V (M=128, N=64, K=128) into TMEM columns [128, 192);
 //   epilogue: O / rowsum -> bf16 ctx[b*S + s, h*64 + d].
 #include <cudaTypedefs.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -487,13 +488,14 @@ constexpr int kTpSmem = 232448;                           // the per-CTA maximum
 __global__ void __launch_bounds__(kApThreads, 1)
     attention_tp(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                  const __grid_constant__ CUtensorMap map_vt, const __grid_constant__ CUtensorMap map_o,
-                 const int32_t* mask, int batch, int heads, const int32_t* count, gg_dep dep) {
+                 const int32_t* mask, int batch, int heads, const int32_t* count, gg_dep dep, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t raw_u32 = smem_u32(smem_raw);
   const uint32_t pad = ((raw_u32 + 1023u) & ~1023u) - raw_u32;
   uint8_t* smem = smem_raw + pad;
   // four stages when the window's alignment leaves room, else three
   const int nst = (int)pad + kTpSmemNeed <= kTpSmem ? 4 : 3;
+  if ((dbg & 8) && blockIdx.x == 0 && threadIdx.x == 0) printf("attention_tp: smem pad %u, %d stages\n", pad, nst);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (nst == 4 ? kTpOffBar : kTpOffBar - kTpStageBytes));
   uint8_t* stg0 = smem + (nst == 4 ? kTpOffStg : kTpOffStg - kTpStageBytes);
   uint8_t* mask0 = smem + (nst == 4 ? kTpOffMask : kTpOffMask - kTpStageBytes);
@@ -642,41 +644,43 @@ __global__ void __launch_bounds__(kApThreads, 1)
         }
       };
       float mx = -INFINITY;
+      {   // pass 1: all four 32-column loads in flight, one wait
+        uint32_t r[4][32];
 #pragma unroll
-      for (int c = 0; c < 4; c += 2) {
-        uint32_t r0[32], r1[32];
-        tmem_ld_32x32b_x32(lane_base + g * 128 + c * 32, r0);
-        tmem_ld_32x32b_x32(lane_base + g * 128 + c * 32 + 32, r1);
+        for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(lane_base + g * 128 + c * 32, r[c]);
         tmem_ld_wait();
-        apply_mask(r0, c);
-        apply_mask(r1, c + 1);
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          mx = fmax3(mx, __uint_as_float(r0[i]), __uint_as_float(r0[i + 1]));
-          mx = fmax3(mx, __uint_as_float(r1[i]), __uint_as_float(r1[i + 1]));
+        for (int c = 0; c < 4; ++c) {
+          apply_mask(r[c], c);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) mx = fmax3(mx, __uint_as_float(r[c][i]), __uint_as_float(r[c][i + 1]));
         }
       }
       const float mref = (mx == -INFINITY) ? 0.0f : mx * l2e;
       const uint64_t l2e2 = f2_pack(l2e, l2e), nm2 = f2_pack(-mref, -mref);
       uint64_t sum2 = f2_pack(0.0f, 0.0f);
-      // unnormalized P row (every value <= 1), bf16 pairs -> TMEM columns [g*128, g*128 + 64):
-      // chunk c's 16 packed columns overwrite scores this thread has already read
+      // pass 2: unnormalized P row (every value <= 1), bf16 pairs -> TMEM columns
+      // [g*128, g*128 + 64); chunk c + 1's load is in flight while chunk c is
+      // computed, and chunk c's 16 packed columns overwrite scores already read
+      uint32_t r[2][32];
+      tmem_ld_32x32b_x32(lane_base + g * 128, r[0]);
+      tmem_ld_wait();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(lane_base + g * 128 + c * 32, r);
-        tmem_ld_wait();
-        apply_mask(r, c);
+        if (c + 1 < 4) tmem_ld_32x32b_x32(lane_base + g * 128 + (c + 1) * 32, r[(c + 1) & 1]);
+        uint32_t (&rc)[32] = r[c & 1];
+        apply_mask(rc, c);
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
           float y0, y1;
-          f2_unpack(f2_fma(f2_pack(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), l2e2, nm2), y0, y1);
+          f2_unpack(f2_fma(f2_pack(__uint_as_float(rc[i]), __uint_as_float(rc[i + 1])), l2e2, nm2), y0, y1);
           const float e0 = ex2_approx(y0), e1 = ex2_approx(y1);
           sum2 = f2_add(sum2, f2_pack(e0, e1));
           pk[i >> 1] = pack_bf16(e0, e1);
         }
         tmem_st_32x32b_x16(lane_base + g * 128 + c * 16, pk);
+        if (c + 1 < 4) tmem_ld_wait();
       }
       float s0, s1;
       f2_unpack(sum2, s0, s1);
@@ -767,7 +771,7 @@ static int attention_impl(const void* qkv, const int32_t* mask, void* ctx, int64
   // softmax, 4 = no ctx stores
   static const int dbg = getenv("GG_ATTN_DBG") ? atoi(getenv("GG_ATTN_DBG")) : 0;
   static const bool smem_p = getenv("GG_ATTN_SMEM_P") != nullptr;   // A/B: P through shared memory
-  if (!simple && !smem_p && !dbg) {
+  if (!simple && !smem_p && !(dbg & 7)) {
     CUtensorMap mo;
     if (int rc2 = make_map_2d(&mo, ctx, (int64_t)batch * seq_len, (int64_t)heads * kAttnD, ldc, 128))
       return rc2;
@@ -780,7 +784,7 @@ static int attention_impl(const void* qkv, const int32_t* mask, void* ctx, int64
     }
     const int grid = (int)std::min<int64_t>((int64_t)batch * heads, num_sms());
     if (launch_pdl(attention_tp, dim3(grid), dim3(kApThreads), kTpSmem, gg_stream(stream), mq, mk, mv, mo,
-                   mask, batch, heads, count_dev, dep) != cudaSuccess)
+                   mask, batch, heads, count_dev, dep, dbg) != cudaSuccess)
       return GG_ERR_CUDA;
     GG_LAUNCH_OK();
     return GG_OK;
