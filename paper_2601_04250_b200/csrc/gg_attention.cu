@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(kApThreads, 1)
 //   smem: 4 stages x (Q 16K | K 16K | V^T 16K), 2 x 16 KB ctx staging tiles,
 //         4 x 512 B key-mask rows, barriers
 //   TMEM: S / P buffers [0, 256) (128 columns per group), O buffers [256, 384)
+__device__ unsigned long long g_attn_tl[64 * 8];   // GG_ATTN_DBG & 16 probe timeline
 constexpr int kTpStageBytes = 49152;
 constexpr int kTpOffStg = 4 * kTpStageBytes;              // 2 x 16 KB
 constexpr int kTpOffMask = kTpOffStg + 2 * 16384;         // 4 x 512 B
@@ -508,6 +509,13 @@ __global__ void __launch_bounds__(kApThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   int* cnt_slot = reinterpret_cast<int*>(bars + 17);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // GG_ATTN_DBG & 16: per-item timeline of CTA 0 (probe; tools/attn_probe.py)
+  unsigned long long* tl = (dbg & 16) && blockIdx.x == 0 ? g_attn_tl : nullptr;
+  auto now_ns = []() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+  };
 
   griddep_launch();
   if (threadIdx.x == 0) {
@@ -558,6 +566,7 @@ __global__ void __launch_bounds__(kApThreads, 1)
           fence_proxy_async_global();
         }
         uint8_t* sb = smem + st * kTpStageBytes;
+        if (tl) tl[t * 8 + 0] = now_ns();
         mbar_expect_tx(full + st, 49152 + (mask ? 512 : 0));
         tma_load_2d(sb, &map_q, full + st, 0, it * kAttnS);
         tma_load_2d(sb + 16384, &map_k, full + st, 0, it * kAttnS);
@@ -629,7 +638,9 @@ __global__ void __launch_bounds__(kApThreads, 1)
       const uint32_t ph = (t >> 1) & 1;
       // ---- softmax(t): two passes over the row's 128 scores straight from TMEM
       // (max, then exp -> bf16 P back into TMEM), 64 / 32 scores in registers
+      if (tl && (threadIdx.x & 127) == 64) tl[t * 8 + 1] = now_ns();
       mbar_wait(s_full + g, ph);
+      if (tl && (threadIdx.x & 127) == 64) tl[t * 8 + 2] = now_ns();
       tc_fence_after();
       const int4* mrow = reinterpret_cast<const int4*>(mask0 + (t % nst) * 512);
       auto apply_mask = [&](uint32_t (&r)[32], int c) {
@@ -689,8 +700,10 @@ __global__ void __launch_bounds__(kApThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(p_full + g);
+      if (tl && (threadIdx.x & 127) == 64) tl[t * 8 + 3] = now_ns();
       // ---- epilogue(t): O row / sum -> bf16 -> SW128 staging -> TMA store
       mbar_wait(o_full + g, ph);
+      if (tl && (threadIdx.x & 127) == 64) tl[t * 8 + 4] = now_ns();
       tc_fence_after();
       uint32_t o[2][32];
       tmem_ld_32x32b_x32(lane_base + 256 + g * 64, o[0]);
@@ -715,6 +728,7 @@ __global__ void __launch_bounds__(kApThreads, 1)
       fence_proxy_async_smem();
       named_bar_sync(1 + g, 128);
       if (leader) {
+        if (tl) tl[t * 8 + 5] = now_ns();
         tma_store_2d(&map_o, stg, (it % heads) * kAttnD, (it / heads) * kAttnS);
         bulk_commit();
         if (dep.signal) {   // the previous item's ctx box has landed: publish it
@@ -787,6 +801,17 @@ static int attention_impl(const void* qkv, const int32_t* mask, void* ctx, int64
                    mask, batch, heads, count_dev, dep, dbg) != cudaSuccess)
       return GG_ERR_CUDA;
     GG_LAUNCH_OK();
+    if (dbg & 16) {
+      unsigned long long h[64 * 8];
+      cudaDeviceSynchronize();
+      cudaMemcpyFromSymbol(h, g_attn_tl, sizeof(h));
+      const unsigned long long t0 = h[0];
+      for (int t = 0; t < 12; ++t)
+        fprintf(stderr, "attn item %2d: load issued %7.2f  S wait %7.2f -> %7.2f  P done %7.2f  O ready %7.2f  "
+                "store %7.2f us\n", t, (h[t * 8] - t0) * 1e-3, (h[t * 8 + 1] - t0) * 1e-3,
+                (h[t * 8 + 2] - t0) * 1e-3, (h[t * 8 + 3] - t0) * 1e-3, (h[t * 8 + 4] - t0) * 1e-3,
+                (h[t * 8 + 5] - t0) * 1e-3);
+    }
     return GG_OK;
   }
   if (!simple) {
