@@ -1322,7 +1322,13 @@ __global__ void __launch_bounds__(32) outcome_kernel(gg_params p, gg_state* st, 
 // buffer and the sorted window are rebuilt at the end (positions as the
 // deque's appends would leave them).  NaN latencies (whose sorted() order the
 // sequential kernel models) fall back to outcome_seq.
-constexpr int kOutThreads = 512;
+constexpr int kOutThreads = 512;   // the largest windows (S >= 16); smaller ones run 1024
+template <int S>
+struct OutCfg {
+  // p95 selection is one warp per outcome: more warps, more outcomes at once
+  // (registers: v[S] / kv[S] per lane, so the widest windows keep 512 threads)
+  static constexpr int kThreads = S <= 8 ? 1024 : 512;
+};
 constexpr int kOutChunk = 512;
 constexpr int kOutMaxSlots = 64;
 
@@ -1336,9 +1342,10 @@ __device__ __forceinline__ unsigned long long order_ukey(double x) {
 }
 
 template <int S>
-__global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
+__global__ void __launch_bounds__(OutCfg<S>::kThreads) outcome_par_kernel(
     gg_params p, gg_state* st, const double* lat, const double* jou, const int32_t* qd, int64_t n,
     int set_qd, int64_t* err, const double* slots, int G, int B, int rank, gg_fifo* fifo) {
+  constexpr int kOutThreadsS = OutCfg<S>::kThreads;
   griddep_wait();   // PDL: the predecessor has completed and flushed
   griddep_launch();
   __shared__ double seq[GG_P95_WINDOW_MAX + kOutChunk];   // window history ++ chunk latencies
@@ -1367,17 +1374,17 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
     }
   }
   #pragma unroll 1
-  for (int j = tid; j < count0; j += kOutThreads) seq[j] = st->win[(head0 + j) % cap];
+  for (int j = tid; j < count0; j += kOutThreadsS) seq[j] = st->win[(head0 + j) % cap];
   __syncthreads();
   const int64_t n_tot = slots ? slot_off[G] : n;
   // NaN latencies anywhere -> the sequential kernel's semantics
   bool nan_here = false;
   #pragma unroll 1
-  for (int j = tid; j < count0; j += kOutThreads) nan_here |= isnan(seq[j]);
+  for (int j = tid; j < count0; j += kOutThreadsS) nan_here |= isnan(seq[j]);
   // one pass over the outcomes: NaN check, and the first chunk's (latency, joules,
   // depth) staged in smem for the chunk loop (one global round trip instead of two)
   #pragma unroll 1
-  for (int64_t e = tid; e < n_tot; e += kOutThreads) {
+  for (int64_t e = tid; e < n_tot; e += kOutThreadsS) {
     double L, J;
     int32_t Q;
     if (slots) {
@@ -1435,7 +1442,7 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
     if (tid == 0) s_first = cn;
     __syncthreads();
     #pragma unroll 1
-    for (int c = tid; c < cn; c += kOutThreads) {
+    for (int c = tid; c < cn; c += kOutThreadsS) {
       const int64_t e = e0 + c;
       double L, J;
       int32_t Q;
@@ -1475,23 +1482,56 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
     }
     // the order-dependent chains, one thread in CPython order — the EWMA recurrence
     // (energy.py:24-36, 75-87) and the running total — on the last warp, which
-    // takes no p95 work, so the chain overlaps the p95 selection below
-    if (tid == kOutThreads - 32) {
+    // takes no p95 work, so the chain overlaps the p95 selection below.  The
+    // products (1 - lam) * J are order-independent: the warp forms them first
+    // (into sew), and the chain e = fl(fl(lam e) + t) runs on registers, eight
+    // outcomes' terms loaded ahead of their step.
+    if (warp == kOutThreadsS / 32 - 1) {
       #pragma unroll 1
-      for (int c = 0; c < nc; ++c) {
-        const double J = sj[c];
-        ewma = (seen > 0) ? f64_add(f64_mul(lam, ewma), f64_mul(one_minus_lam, J)) : J;
-        seen += 1;
-        total = f64_add(total, J);
-        sew[c] = ewma;
+      for (int c = lane; c < nc; c += 32) sew[c] = f64_mul(one_minus_lam, sj[c]);
+      __syncwarp();
+      if (lane == 0) {
+        const int64_t seen0 = seen;
+        int c = 0;
+        if (seen == 0 && nc > 0) {   // the first sample seeds the average
+          ewma = sj[0];
+          total = f64_add(total, sj[0]);
+          sew[0] = ewma;
+          seen = 1;
+          c = 1;
+        }
+        #pragma unroll 1
+        for (; c + 8 <= nc; c += 8) {
+          double t[8], jv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            t[q] = sew[c + q];
+            jv[q] = sj[c + q];
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            ewma = f64_add(f64_mul(lam, ewma), t[q]);
+            total = f64_add(total, jv[q]);
+            t[q] = ewma;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) sew[c + q] = t[q];
+        }
+        #pragma unroll 1
+        for (; c < nc; ++c) {
+          ewma = f64_add(f64_mul(lam, ewma), sew[c]);
+          total = f64_add(total, sj[c]);
+          sew[c] = ewma;
+        }
+        seen = seen0 + nc;
+        s_ewma = ewma;
+        s_total = total;
+        s_seen = seen;
       }
-      s_ewma = ewma;
-      s_total = total;
-      s_seen = seen;
     }
     // p95 after each outcome: one warp per outcome (all warps but the chain's)
     #pragma unroll 1
-    for (int c = warp; c < nc && warp < kOutThreads / 32 - 1; c += kOutThreads / 32 - 1) {
+    for (int c = warp; c < nc && warp < kOutThreadsS / 32 - 1; c += kOutThreadsS / 32 - 1) {
       const int cnt = min(cap, h + c + 1);
       const int start = h + c + 1 - cnt;
       double v[S];
@@ -1609,13 +1649,13 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
     double tmp[2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const int j = tid + q * kOutThreads;
+      const int j = tid + q * kOutThreadsS;
       tmp[q] = j < hn ? seq[src + j] : 0.0;
     }
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const int j = tid + q * kOutThreads;
+      const int j = tid + q * kOutThreadsS;
       if (j < hn) seq[j] = tmp[q];
     }
     h = hn;
@@ -1625,12 +1665,12 @@ __global__ void __launch_bounds__(kOutThreads) outcome_par_kernel(
   // ring buffer: window element j sits at (head_f + j) % cap
   const int head_f = (count0 + m_total <= cap) ? head0 : (int)((head0 + (count0 + m_total - cap)) % cap);
   #pragma unroll 1
-  for (int j = tid; j < h; j += kOutThreads) st->win[(head_f + j) % cap] = seq[j];
+  for (int j = tid; j < h; j += kOutThreadsS) st->win[(head_f + j) % cap] = seq[j];
   // sorted window = CPython's stable sorted(): each element lands at its stable rank
   // (smaller values, then equal values earlier in arrival order): h^2 / 512 compares
   // against the smem window instead of a bitonic network's syncs
   #pragma unroll 1
-  for (int j = tid; j < h; j += kOutThreads) {
+  for (int j = tid; j < h; j += kOutThreadsS) {
     const double vj = seq[j];
     int rk = 0;
     #pragma unroll 4
@@ -1855,7 +1895,7 @@ static int launch_outcome(const gg_params& p, gg_state* st, const double* lat, c
 #define GG_OUTCOME(SLOTS)                                                                        \
   do {                                                                                           \
     if (par)                                                                                     \
-      GG_PDL_LAUNCH((outcome_par_kernel<SLOTS>), 1, kOutThreads, 0, s, p, st, lat, jou, qd, n, set_qd, err, slots, \
+      GG_PDL_LAUNCH((outcome_par_kernel<SLOTS>), 1, OutCfg<SLOTS>::kThreads, 0, s, p, st, lat, jou, qd, n, set_qd, err, slots, \
                                                           G, B, rank, fifo);                     \
     else                                                                                         \
       GG_PDL_LAUNCH((outcome_kernel<SLOTS>), 1, 32, 0, s, p, st, lat, jou, qd, n, set_qd, err, slots, G, B,   \
