@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(96 + 32 * EW, 1)
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
     tma_prefetch(&map_out);
-    if (RES) tma_prefetch(&map_res);
+    if (RES || QKV) tma_prefetch(&map_res);
   }
   if (warp == 1) tmem_alloc_pair(tmem_base_smem, 2 * kPairBN);
   tc_fence_before();
@@ -934,28 +934,26 @@ __global__ void __launch_bounds__(96 + 32 * EW, 1)
           for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
         }
         int gx = col0, gy = row0;
+        bool vt = false;   // QKV: this chunk is V, stored transposed
         if (QKV) {
-          // Q (x 1/sqrt(64)) and K boxes into their [B, H, S, 64] planes (the V^T plane
-          // keeps the lane-coalesced transposed path below)
+          // Q (x 1/sqrt(64)) and K boxes into their [B, H, S, 64] planes; V^T boxes
+          // (32 d x 32 s, transposed in the staging tile) into the [B, H, 64, S] plane
           const int hd = ep.heads * 64;
           const int which = col0 / hd, hh = (col0 % hd) / 64;
           if (which == 2) {
-            const int bq = row0 / ep.seq_len;
-            __nv_bfloat16* plane = reinterpret_cast<__nv_bfloat16*>(ep.D) + 2 * ep.qkv_plane;
-            const int64_t bh = (int64_t)bq * ep.heads + hh;
-            const int s_ = row0 % ep.seq_len + lane, d0 = col0 % 64;
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              plane[(bh * 64 + d0 + i) * ep.seq_len + s_] = __float2bfloat16_rn(v[i]);
-            continue;
+            vt = true;
+            gx = row0 % ep.seq_len;
+            gy = (int)(((int64_t)(row0 / ep.seq_len) * ep.heads + hh) * 64 + col0 % 64);
           }
           if (which == 0) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] *= 0.125f;
           }
-          gx = col0 % 64;
-          gy = (int)((int64_t)which * (ep.qkv_plane / 64) +
-                     ((int64_t)(row0 / ep.seq_len) * ep.heads + hh) * ep.seq_len + row0 % ep.seq_len);
+          if (!vt) {
+            gx = col0 % 64;
+            gy = (int)((int64_t)which * (ep.qkv_plane / 64) +
+                       ((int64_t)(row0 / ep.seq_len) * ep.heads + hh) * ep.seq_len + row0 % ep.seq_len);
+          }
         }
         uint4 u[4];
 #pragma unroll
@@ -969,8 +967,18 @@ __global__ void __launch_bounds__(96 + 32 * EW, 1)
           if (lane == 0) bulk_wait_read<NBUF - 1>();
           __syncwarp();
         }
+        if (QKV && vt) {
+          // staging row i = head dim d0 + i (64 B, SW64: 16-B chunk c at c ^ ((i >> 1) & 3)),
+          // column = sequence position (this lane): 32 conflict-free 2-B stores per lane
 #pragma unroll
-        for (int q = 0; q < 4; ++q) myrow[q ^ sw] = u[q];
+          for (int i = 0; i < 32; ++i) {
+            const int off = i * 64 + ((((lane >> 3) ^ (i >> 1)) & 3) << 4) + ((lane & 7) << 1);
+            *reinterpret_cast<__nv_bfloat16*>(buf + off) = __float2bfloat16_rn(v[i]);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) myrow[q ^ sw] = u[q];
+        }
         if (RES && ep.out_stats) {   // row statistics of this chunk (shifted sums, fp32 values)
           if (c == 0) st_k = v[0];
           const uint64_t nk = f2_pack(-st_k, -st_k);
@@ -990,7 +998,7 @@ __global__ void __launch_bounds__(96 + 32 * EW, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&map_out, buf, gx, gy);
+          tma_store_2d(QKV && vt ? &map_res : &map_out, buf, gx, gy);   // (QKV: map_res = the V^T plane)
           bulk_commit();
         }
         ++ngroups;
@@ -1234,7 +1242,12 @@ static int gemm_impl(const void* A, int64_t lda, const void* B, int64_t ldb, voi
     if (tma_ok) {
       mr = ma;
       if (e->out_mode == OUT_BF16) rc = make_map_box32(&mo, D, M, N, ldd);
-      else rc = make_map_box32(&mo, D, 3 * M * (int64_t)e->heads, 64, 64);
+      else {   // Q / K planes as [3 B H S, 64]; the V^T plane [B H 64, S] in the residual slot
+        rc = make_map_box32(&mo, D, 3 * M * (int64_t)e->heads, 64, 64);
+        if (!rc)
+          rc = make_map_box32(&mr, reinterpret_cast<__nv_bfloat16*>(D) + 2 * M * 64 * (int64_t)e->heads,
+                              M / e->seq_len * e->heads * 64, e->seq_len, e->seq_len);
+      }
       if (!rc && e->residual) rc = make_map_box32(&mr, e->residual, M, N, e->ldr);
       if (rc) return rc;
       ep.tma_out = 1;
