@@ -513,7 +513,7 @@ __device__ __forceinline__ int fast_row(const double* x, int k, double now, cons
   float u;
   if (entropy) u = fminf(fmaxf(-(KC > 0 ? hf : (float)hd) * f.inv_log2k, 0.0f), 1.0f);
   else u = (float)(1.0 - mx);
-  const float el = (float)fmax(now - f.t_origin, 0.0);
+  const float el = fmaxf((float)(now - f.t_origin), 0.0f);   // == (float)fmax(now - t0, 0.0)
   const float tau = f.tau_inf + f.dtau * ex2_approx(f.negk_log2e * el);
   const float d = (f.alpha * u + f.jc) - tau;
   if (!(fabsf(d) > f.margin)) return kNeedExact;
@@ -557,7 +557,10 @@ struct SplitConsts {
 };
 static_assert(sizeof(SplitConsts) <= sizeof(((AdmitWorkspace*)0)->consts), "workspace consts");
 
-template <int KC, int RPT, bool BD, bool SPLIT>
+// UP: the utility proxy as a compile-time constant on the fast path (1 entropy,
+// 2 one-minus-confidence; 0 = read at run time) -- the per-row proxy branch was a
+// quarter of the decide kernel's instructions.
+template <int KC, int RPT, bool BD, bool SPLIT, int UP = 0>
 __global__ void __launch_bounds__(kSmallThreads) admit_small_kernel(AdmitArgs a) {
   griddep_wait();   // PDL: the predecessor has completed and flushed
   griddep_launch();
@@ -601,7 +604,7 @@ __global__ void __launch_bounds__(kSmallThreads) admit_small_kernel(AdmitArgs a)
     }
     __syncthreads();
   }
-  const bool entropy = a.p.utility_proxy == GG_UTIL_ENTROPY;
+  const bool entropy = UP == 0 ? a.p.utility_proxy == GG_UTIL_ENTROPY : UP == 1;
   const int k = KC > 0 ? KC : a.k;
   int code[RPT];
   bool any_exact = false;
@@ -1971,12 +1974,15 @@ static int launch_admit(const AdmitArgs& args, void* stream) {
       GG_PDL_LAUNCH((admit_prologue_kernel), 1, 32, 0, s, a);
       GG_LAUNCH_OK();
     }
+    const bool ent = a.p.utility_proxy == GG_UTIL_ENTROPY;
 #define GG_SMALL(KC)                                                                        \
   do {                                                                                      \
     if (bd && split) GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, true, true>), g, kSmallThreads, 0, s, a);    \
     else if (bd) GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, true, false>), g, kSmallThreads, 0, s, a);      \
-    else if (split) GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, false, true>), g, kSmallThreads, 0, s, a);   \
-    else GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, false, false>), g, kSmallThreads, 0, s, a);             \
+    else if (split && ent) GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, false, true, 1>), g, kSmallThreads, 0, s, a); \
+    else if (split) GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, false, true, 2>), g, kSmallThreads, 0, s, a);        \
+    else if (ent) GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, false, false, 1>), g, kSmallThreads, 0, s, a);         \
+    else GG_PDL_LAUNCH((admit_small_kernel<KC, kSmallRpt, false, false, 2>), g, kSmallThreads, 0, s, a);                  \
   } while (0)
     if (k == 2 && aligned16) GG_SMALL(2);
     else if (k == 4 && aligned16) GG_SMALL(4);
