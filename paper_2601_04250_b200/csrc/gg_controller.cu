@@ -7,6 +7,9 @@
 // rounds exactly like CPython's float op in the reference
 // (pkg/src/greengate/controller.py, energy.py, telemetry.py).
 #include <math.h>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
 #include <stdio.h>
 #include <stdlib.h>
 
@@ -1344,10 +1347,163 @@ __device__ __forceinline__ unsigned long long order_ukey(double x) {
   return b < 0 ? (unsigned long long)(~b) : ((unsigned long long)b | 0x8000000000000000ULL);
 }
 
+// Nearest-rank p95 (telemetry.py:35-46) of seq[start, start + cnt) for one warp:
+// the (cnt - k + 1)-th largest, k = ceil(0.95 cnt), extracted in CPython's
+// stable-sort order (equal values -- e.g. -0.0 / +0.0 -- latest arrival first).
+template <int S>
+__device__ __forceinline__ double p95_select(const double* seq, int start, int cnt, int lane) {
+  double v[S];
+  unsigned long long kv[S];
+#pragma unroll
+  for (int q = 0; q < S; ++q) {
+    const int j = q * 32 + lane;
+    v[q] = j < cnt ? seq[start + j] : 0.0;
+    kv[q] = j < cnt ? order_ukey(v[q]) : 0ULL;
+  }
+  const int k = (int)ceil(f64_mul(0.95, (double)cnt));   // ceil(95.0/100.0 * n)
+  const int r = cnt - k + 1;                             // k-th smallest = r-th largest
+  double got = 0.0;
+  if constexpr (S <= 8) {
+    // Same extraction order, cheaper rounds: each lane sorts its S (key,
+    // position) pairs once (key descending, later position first), so a
+    // round only reduces the lanes' heads and the winning lane shifts its
+    // list (the general loop below re-scans all S keys every round).
+    unsigned ps[S];
+#pragma unroll
+    for (int q = 0; q < S; ++q) ps[q] = (unsigned)(q * 32 + lane + 1);
+#pragma unroll
+    for (int x = 0; x < S; ++x)
+#pragma unroll
+      for (int y = S - 1; y > x; --y) {
+        const bool sw = kv[y] > kv[y - 1] || (kv[y] == kv[y - 1] && ps[y] > ps[y - 1]);
+        if (sw) {
+          const unsigned long long tk = kv[y];
+          kv[y] = kv[y - 1];
+          kv[y - 1] = tk;
+          const double tv = v[y];
+          v[y] = v[y - 1];
+          v[y - 1] = tv;
+          const unsigned tp = ps[y];
+          ps[y] = ps[y - 1];
+          ps[y - 1] = tp;
+        }
+      }
+    #pragma unroll 1
+    for (int it = 0; it < r; ++it) {
+      const unsigned hi = (unsigned)(kv[0] >> 32), lo = (unsigned)kv[0];
+      const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+      const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+      const bool cand = hi == mh && lo == ml;
+      const unsigned pos = __reduce_max_sync(0xffffffffu, cand ? ps[0] : 0u);
+      const int wl = (int)((pos - 1u) & 31u);
+      got = __shfl_sync(0xffffffffu, v[0], wl);
+      if (lane == wl) {
+#pragma unroll
+        for (int q = 0; q + 1 < S; ++q) {
+          kv[q] = kv[q + 1];
+          v[q] = v[q + 1];
+          ps[q] = ps[q + 1];
+        }
+        kv[S - 1] = 0ULL;
+        ps[S - 1] = 0u;
+      }
+    }
+  } else {
+  #pragma unroll 1
+  for (int it = 0; it < r; ++it) {
+    unsigned long long bk = kv[0];
+    int bq = 0;
+#pragma unroll
+    for (int q = 1; q < S; ++q)
+      if (kv[q] >= bk) {   // ties: the later position (q * 32 + lane grows with q)
+        bk = kv[q];
+        bq = q;
+      }
+    const unsigned hi = (unsigned)(bk >> 32), lo = (unsigned)bk;
+    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+    const bool cand = hi == mh && lo == ml;
+    const unsigned pos = __reduce_max_sync(0xffffffffu, cand ? (unsigned)(bq * 32 + lane + 1) : 0u) - 1u;
+    const int wl = (int)(pos & 31u), wq = (int)(pos >> 5);
+    double wv = 0.0;
+#pragma unroll
+    for (int q = 0; q < S; ++q)
+      if (q == wq) wv = v[q];
+    got = __shfl_sync(0xffffffffu, wv, wl);
+    if (lane == wl) {
+#pragma unroll
+      for (int q = 0; q < S; ++q)
+        if (q == wq) kv[q] = 0ULL;
+    }
+  }
+  }
+  return got;
+}
+
+// The p95 after every outcome is independent across outcomes: spread over CTAs
+// (kP95PerCta outcomes each, one warp per outcome) ahead of the one-CTA chain
+// kernel, which then reads them (outcome_par_kernel's p95_pre).  The window of
+// outcome e is the last min(W, h0 + e + 1) latencies of (history ++ batch).
+constexpr int kP95PerCta = 64;
+constexpr int kP95Threads = 256;
+template <int S>
+__global__ void __launch_bounds__(kP95Threads) outcome_p95_kernel(gg_params p, const gg_state* st,
+                                                                  const double* lat, int64_t n,
+                                                                  const double* slots, int G, int B,
+                                                                  double* out) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
+  __shared__ double seq[GG_P95_WINDOW_MAX + kP95PerCta];
+  __shared__ int64_t slot_off[kOutMaxSlots + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cap = p.p95_window;
+  const int count0 = st->win_count, head0 = st->win_head;
+  if (tid == 0 && slots) {
+    int64_t off = 0;
+    #pragma unroll 1
+    for (int gi = 0; gi < G; ++gi) {
+      slot_off[gi] = off;
+      off += (int64_t)slots[(int64_t)gi * (3 * B + 8) + 3 * B];
+    }
+    slot_off[G] = off;
+  }
+  __syncthreads();
+  const int64_t n_tot = slots ? slot_off[G] : n;
+  const int64_t e_lo = (int64_t)blockIdx.x * kP95PerCta;
+  if (e_lo >= n_tot) return;
+  const int64_t e_hi = min(n_tot, e_lo + kP95PerCta);
+  const int64_t lo_pos = max((int64_t)0, (int64_t)count0 + e_lo + 1 - cap), hi_pos = count0 + e_hi;
+  #pragma unroll 1
+  for (int64_t j = tid; j < hi_pos - lo_pos; j += kP95Threads) {
+    const int64_t pos = lo_pos + j;
+    double L;
+    if (pos < count0) {
+      L = st->win[(head0 + pos) % cap];
+    } else if (slots) {
+      const int64_t e = pos - count0;
+      int gi = 0;
+      while (e >= slot_off[gi + 1]) ++gi;
+      L = slots[(int64_t)gi * (3 * B + 8) + (e - slot_off[gi])];
+    } else {
+      L = lat[pos - count0];
+    }
+    seq[j] = L;
+  }
+  __syncthreads();
+  #pragma unroll 1
+  for (int64_t e = e_lo + warp; e < e_hi; e += kP95Threads / 32) {
+    const int cnt = (int)min((int64_t)cap, count0 + e + 1);
+    const int start = (int)(count0 + e + 1 - cnt - lo_pos);
+    const double got = p95_select<S>(seq, start, cnt, lane);
+    if (lane == 0) out[e] = got;
+  }
+}
+
 template <int S>
 __global__ void __launch_bounds__(OutCfg<S>::kThreads) outcome_par_kernel(
     gg_params p, gg_state* st, const double* lat, const double* jou, const int32_t* qd, int64_t n,
-    int set_qd, int64_t* err, const double* slots, int G, int B, int rank, gg_fifo* fifo) {
+    int set_qd, int64_t* err, const double* slots, int G, int B, int rank, gg_fifo* fifo,
+    const double* p95_pre) {
   constexpr int kOutThreadsS = OutCfg<S>::kThreads;
   griddep_wait();   // PDL: the predecessor has completed and flushed
   griddep_launch();
@@ -1532,54 +1688,17 @@ __global__ void __launch_bounds__(OutCfg<S>::kThreads) outcome_par_kernel(
         s_seen = seen;
       }
     }
-    // p95 after each outcome: one warp per outcome (all warps but the chain's)
+    // p95 after each outcome: precomputed by outcome_p95_kernel, or here with one
+    // warp per outcome (all warps but the chain's)
+    if (p95_pre) {
+      #pragma unroll 1
+      for (int c = tid; c < nc; c += kOutThreadsS) sp[c] = p95_pre[e0 + c];
+    }
     #pragma unroll 1
-    for (int c = warp; c < nc && warp < kOutThreadsS / 32 - 1; c += kOutThreadsS / 32 - 1) {
+    for (int c = warp; !p95_pre && c < nc && warp < kOutThreadsS / 32 - 1; c += kOutThreadsS / 32 - 1) {
       const int cnt = min(cap, h + c + 1);
       const int start = h + c + 1 - cnt;
-      double v[S];
-      unsigned long long kv[S];
-#pragma unroll
-      for (int q = 0; q < S; ++q) {
-        const int j = q * 32 + lane;
-        v[q] = j < cnt ? seq[start + j] : 0.0;
-        kv[q] = j < cnt ? order_ukey(v[q]) : 0ULL;
-      }
-      const int k = (int)ceil(f64_mul(0.95, (double)cnt));   // ceil(95.0/100.0 * n)
-      const int r = cnt - k + 1;                             // k-th smallest = r-th largest
-      // r rounds of "remove the largest": warp max of the order keys with two
-      // redux.sync (high, then low word), ties to the later arrival (CPython's
-      // sorted() is stable, so from the top of the ascending window equal values
-      // — e.g. -0.0 / +0.0 — come latest-arrival first) by a third redux over the
-      // candidates' window positions
-      double got = 0.0;
-      #pragma unroll 1
-      for (int it = 0; it < r; ++it) {
-        unsigned long long bk = kv[0];
-        int bq = 0;
-#pragma unroll
-        for (int q = 1; q < S; ++q)
-          if (kv[q] >= bk) {   // ties: the later position (q * 32 + lane grows with q)
-            bk = kv[q];
-            bq = q;
-          }
-        const unsigned hi = (unsigned)(bk >> 32), lo = (unsigned)bk;
-        const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
-        const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
-        const bool cand = hi == mh && lo == ml;
-        const unsigned pos = __reduce_max_sync(0xffffffffu, cand ? (unsigned)(bq * 32 + lane + 1) : 0u) - 1u;
-        const int wl = (int)(pos & 31u), wq = (int)(pos >> 5);
-        double wv = 0.0;
-#pragma unroll
-        for (int q = 0; q < S; ++q)
-          if (q == wq) wv = v[q];
-        got = __shfl_sync(0xffffffffu, wv, wl);
-        if (lane == wl) {
-#pragma unroll
-          for (int q = 0; q < S; ++q)
-            if (q == wq) kv[q] = 0ULL;
-        }
-      }
+      const double got = p95_select<S>(seq, start, cnt, lane);
       if (lane == 0) sp[c] = got;
     }
     __syncthreads();
@@ -1888,6 +2007,28 @@ size_t gg_admit_workspace_bytes(int64_t n) {
 static int launch_admit(const AdmitArgs& a, void* stream);
 
 // K2 instantiation by window capacity (register slots per lane = ceil(W / 32)).
+// Per-controller scratch for the p95 pre-pass (one double per outcome), keyed by
+// the state's device address; grown outside stream capture only (inside a
+// capture without room, the chain kernel computes the p95s itself).
+static std::mutex g_p95_mu;
+static std::unordered_map<const gg_state*, std::pair<double*, int64_t>> g_p95_scratch;
+static double* p95_scratch(const gg_state* st, int64_t need, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_p95_mu);
+  auto& e = g_p95_scratch[st];
+  if (e.second >= need) return e.first;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  const int64_t cap = need < 4096 ? 4096 : need;
+  double* ptr = nullptr;
+  if (cudaMalloc(&ptr, cap * sizeof(double)) != cudaSuccess) return nullptr;
+  if (e.first) {
+    cudaStreamSynchronize(s);   // the old scratch may still be read by queued work
+    cudaFree(e.first);
+  }
+  e = {ptr, cap};
+  return ptr;
+}
+
 static int launch_outcome(const gg_params& p, gg_state* st, const double* lat, const double* jou,
                           const int32_t* qd, int64_t n, int set_qd, int64_t* err,
                           const double* slots, int G, int B, int rank, gg_fifo* fifo,
@@ -1895,11 +2036,18 @@ static int launch_outcome(const gg_params& p, gg_state* st, const double* lat, c
   cudaStream_t s = gg_stream(stream);
   const int w = p.p95_window;
   const bool par = !getenv("GG_OUTCOME_SEQ") && (!slots || G <= kOutMaxSlots);
+  // p95 pre-pass over several CTAs once there are enough outcomes to spread
+  static const bool no_pre = getenv("GG_OUTCOME_NO_PRE") != nullptr;
+  const int64_t n_max = slots ? (int64_t)G * B : n;
+  double* pre = (par && !no_pre && n_max >= 2 * kP95PerCta) ? p95_scratch(st, n_max, s) : nullptr;
+  const unsigned pre_grid = (unsigned)((n_max + kP95PerCta - 1) / kP95PerCta);
 #define GG_OUTCOME(SLOTS)                                                                        \
   do {                                                                                           \
+    if (par && pre)                                                                              \
+      GG_PDL_LAUNCH((outcome_p95_kernel<SLOTS>), pre_grid, kP95Threads, 0, s, p, st, lat, n, slots, G, B, pre); \
     if (par)                                                                                     \
       GG_PDL_LAUNCH((outcome_par_kernel<SLOTS>), 1, OutCfg<SLOTS>::kThreads, 0, s, p, st, lat, jou, qd, n, set_qd, err, slots, \
-                                                          G, B, rank, fifo);                     \
+                                                          G, B, rank, fifo, (const double*)pre); \
     else                                                                                         \
       GG_PDL_LAUNCH((outcome_kernel<SLOTS>), 1, 32, 0, s, p, st, lat, jou, qd, n, set_qd, err, slots, G, B,   \
                                              rank, fifo);                                        \
