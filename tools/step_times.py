@@ -22,12 +22,12 @@ def main():
     which = sys.argv[1] if len(sys.argv) > 1 else "resnet18"
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
     wl = bench.WORKLOADS[which]
-    scores, now = bench.make_trace(wl, (steps + 16) * wl["window"], seed=1000)
+    dev = torch.device("cuda", 0)
+    scores, now, labels = bench.make_trace(wl, (steps + 16) * wl["window"], seed=1000)
     net = bench.build_net(which, wl["batch"])
-    ctl = gg.ControllerConfig(**wl["ctl"], routing=gg.RoutePolicy.ALL_BATCHED).build(gg.EnergyLedger())
-    pay = serving.synthetic_images(wl["pool"]) if which == "resnet18" else serving.synthetic_tokens(wl["pool"])
-    srv = serving.GatedServer(ctl, net, torch.from_numpy(scores).cuda(), torch.from_numpy(now).cuda(),
-                              pay, window=wl["window"], outcome=serving.OutcomeModel(**wl["outcome"]))
+    pay = bench.payload_pool(which, wl["pool"], 0, dev)
+    srv = bench.make_server(wl, which, net, torch.from_numpy(scores).to(dev), torch.from_numpy(now).to(dev),
+                            torch.from_numpy(labels).to(dev), pay, dev)
     srv.run(1)
     srv.capture()
     srv.run(4)
