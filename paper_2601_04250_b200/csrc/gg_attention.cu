@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kAttnThreads, 4)
                       const __grid_constant__ CUtensorMap map_vt, const int32_t* mask,
                       __nv_bfloat16* ctx, int64_t ldc, int heads, const int32_t* count) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1k(smem_raw);
   uint64_t* bar_load = reinterpret_cast<uint64_t*>(smem + 49152);
   uint64_t* bar_s = bar_load + 1;
   uint64_t* bar_o = bar_load + 2;
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kApThreads, 1)
                       const __grid_constant__ CUtensorMap map_o, const int32_t* mask, int batch,
                       int heads, const int32_t* count, int dbg, gg_dep dep) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kApOffBar);
   uint64_t* full = bars;         // [3] stage loaded (tx bytes)
   uint64_t* empty = bars + 3;    // [3] stage free (MMA commit after O)

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kConvThreadsMax, 1)
   using L = ConvSmem<BN, STAGES, DS>;
   constexpr int NACC_COLS = (DS ? 2 : 1) * BN;   // TMEM columns per accumulator buffer
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1k(smem_raw);
   // Resident-B mode (sh.bres, im2col modes, one N tile): the whole BN x Kpad
   // weight slab is loaded once per CTA after a shorter A ring and never re-read
   // from L2; the ring then carries only A tiles.

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   // taps x 4 MMAs — so two buffers let one slow epilogue stall the tensor pipe)
   constexpr int NACC = 512 / ACC_COLS >= 4 ? 4 : 2;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1k(smem_raw);
   const int cblocks = sh.C / CH;
   const int nkb = cblocks * TAPS;
   const int AST = sh.a_stages, BST = sh.b_stages;
@@ -119,8 +119,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   uint64_t* bres_full = acc_empty + NACC;
   uint64_t* res_full = bres_full + 1;      // [8 warps][2]: residual boxes landed (TMA epilogue)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 2 * kSpanEpiWarps);
-  uint8_t* stg_base = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(bars) + 1024 + 1023) & ~uintptr_t(1023));
+  uint8_t* stg_base = smem_align1k(reinterpret_cast<uint8_t*>(bars) + 1024);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (ep.prof && threadIdx.x == 0) {
@@ -697,7 +696,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   constexpr int B_BYTES = BH * RB;           // one tap slab of this CTA's B half
   constexpr int NACC = 512 / BN >= 4 ? 4 : 2;   // TMEM accumulator buffers
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1k(smem_raw);
   const int cblocks = sh.C / CH;
   const int nkb = cblocks * TAPS;
   const int AST = sh.a_stages, BST = sh.b_stages;
@@ -715,8 +714,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   uint64_t* res_full = bres_full + 1;      // [8 warps][2]: residual boxes landed (TMA epilogue)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 2 * kSpanEpiWarps);
   // TMA epilogue staging: per epilogue warp two 2 KB SW64 images of 32 x 32 bf16 boxes
-  uint8_t* stg_base = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(bars) + 1024 + 1023) & ~uintptr_t(1023));
+  uint8_t* stg_base = smem_align1k(reinterpret_cast<uint8_t*>(bars) + 1024);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -1273,7 +1271,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
                    act_t* __restrict__ y, const int32_t* count) {
   constexpr int RB = 32, NACC = 4, ACC_COLS = 128;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1k(smem_raw);
   const int AST = sh.a_stages;
   uint8_t* a_base = smem;
   uint8_t* b_base = smem + AST * sh.a_stage_bytes;

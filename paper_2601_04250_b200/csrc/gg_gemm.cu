@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   static_assert(BM == 128, "cta_group::1 tiles use all 128 TMEM lanes");
   static_assert(2 * BN <= 512, "two accumulators must fit TMEM");
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_align1k(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;     // [2]

@@ -15,6 +15,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 // ---- mbarrier ---------------------------------------------------------------
+// Round a dynamic-smem pointer up to 1 KB (SWIZZLE_128B atoms) while staying in
+// the shared address space: offsetting the array itself keeps LDS / STS; a round
+// trip through an integer address makes every access through the result generic.
+__device__ __forceinline__ uint8_t* smem_align1k(uint8_t* base) {
+  const uint32_t a = smem_u32(base);
+  return base + (((a + 1023u) & ~1023u) - a);
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
