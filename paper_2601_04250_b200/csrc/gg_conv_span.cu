@@ -816,15 +816,27 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
       // descriptors advance incrementally (no runtime % and / per tap)
       int as = 0, bs = 0, t = 0;
       uint32_t aph = 0, bph = 0;
+      long long wt_acc = 0, wt_a = 0, wt_b = 0;   // GG_SPAN_PROF: issuer wait cycles
+      const long long t_mma0 = clock64();
+#define GG_PAIR_WAIT(bar, par, acc_)                    \
+  do {                                                  \
+    if (ep.prof) {                                      \
+      const long long t_ = clock64();                   \
+      mbar_wait(bar, par);                              \
+      acc_ += clock64() - t_;                           \
+    } else {                                            \
+      mbar_wait(bar, par);                              \
+    }                                                   \
+  } while (0)
       SkSched sc(ep.sk.enabled, num_tiles, cblocks, pair, npairs);
       SkWork wk;
       for (; sc.next(wk); ++t) {
         const int acc = t % NACC;
-        mbar_wait(&acc_empty[acc], ((t / NACC) & 1) ^ 1);
+        GG_PAIR_WAIT(&acc_empty[acc], ((t / NACC) & 1) ^ 1, wt_acc);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int cb = wk.kb0; cb < wk.kb1; ++cb) {
-          mbar_wait(&a_full[as], aph);
+          GG_PAIR_WAIT(&a_full[as], aph, wt_a);
           tc_fence_after();
           const uint64_t ad = a_desc0 + (uint64_t)as * a_stage_d;
           const int as_now = as;
@@ -850,7 +862,7 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
           } else {
 #pragma unroll
             for (int tap = 0; tap < TAPS; ++tap) {
-              mbar_wait(&b_full[bs], bph);
+              GG_PAIR_WAIT(&b_full[bs], bph, wt_b);
               tc_fence_after();
               const uint64_t ao = ad + tap_off[tap];
               const uint64_t bo = bres_desc + (uint64_t)bs * (uint64_t)(B_BYTES >> 4);
@@ -872,6 +884,14 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
         }
         if (elect_one_sync()) umma_commit_pair(&acc_full[acc], 3);
         __syncwarp();
+      }
+#undef GG_PAIR_WAIT
+      if (ep.prof && lane == 0) {
+        ep.prof[6144 + pair * 4 + 0] = wt_acc;
+        ep.prof[6144 + pair * 4 + 1] = wt_a;
+        ep.prof[6144 + pair * 4 + 2] = wt_b;
+        ep.prof[6144 + pair * 4 + 3] = clock64() - t_mma0;
+        ep.prof[4096 + pair] = t;
       }
     }
   } else {
@@ -1173,8 +1193,36 @@ static int launch_span_pair(const CUtensorMap& mx, const CUtensorMap& mw, const 
   at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  if (cudaLaunchKernelEx(&cfg, kern, mx, mw, mo ? *mo : mx, mr ? *mr : mx, sh, ep) != cudaSuccess)
+  static unsigned long long* prof = nullptr;
+  SpanEpi e2 = ep;
+  const bool do_prof = getenv("GG_SPAN_PROF") != nullptr;
+  if (do_prof) {
+    if (!prof) cudaMalloc(&prof, 8 * 1024 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof, 0, 8 * 1024 * sizeof(unsigned long long), s);
+    e2.prof = prof;
+  }
+  if (cudaLaunchKernelEx(&cfg, kern, mx, mw, mo ? *mo : mx, mr ? *mr : mx, sh, e2) != cudaSuccess)
     return GG_ERR_CUDA;
+  if (do_prof) {
+    static unsigned long long h[8 * 1024];
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
+    const int np = grid / 2;
+    double w0 = 0, w1 = 0, w2 = 0, wt = 0, tl = 0, tmax = 0;
+    for (int i = 0; i < np; ++i) {
+      w0 += (double)h[6144 + 4 * i];
+      w1 += (double)h[6144 + 4 * i + 1];
+      w2 += (double)h[6144 + 4 * i + 2];
+      wt += (double)h[6144 + 4 * i + 3];
+      tl += (double)h[4096 + i];
+      tmax = (double)h[4096 + i] > tmax ? (double)h[4096 + i] : tmax;
+    }
+    const double mma_cyc = (double)(sh.C / CH) * RT * RT * (CH / 16) * (BN >= 128 ? 64.0 * BN / 128 : 48.0);
+    fprintf(stderr, "span pair BN=%d C=%d Cout=%d H=%d Wp=%d: %d pairs, tiles %.2f/pair (max %.0f), issuer %.0f cycles/pair, "
+            "waiting acc %.0f%% A %.0f%% B %.0f%%, MMA-bound %.0f cycles/tile, stages A%d B%d%s\n",
+            BN, sh.C, sh.Cout, sh.H, sh.Wp, np, tl / np, tmax, wt / np, 100 * w0 / wt, 100 * w1 / wt, 100 * w2 / wt,
+            mma_cyc, sh.a_stages, sh.b_stages, sh.bres ? " (B resident)" : "");
+  }
   return GG_OK;
 }
 
