@@ -529,8 +529,9 @@ def roofline_forward(srv, net, B):
             "avg pool/fc (fp32), all convs tcgen05, shared-border NHWC layout"
             if srv.kind == "resnet18"
             else "DistilBERT forward: CTA-pair tcgen05 GEMMs (QKV, out-proj, FFN) with fused "
-                 "bias/GELU/residual epilogues, tcgen05 attention, LayerNorm, embedding-LN, "
-                 "classifier head")
+                 "bias/GELU/residual/LayerNorm-folding epilogues (no LayerNorm kernel in the "
+                 "encoder), persistent tcgen05 attention with P in TMEM, embedding-LN, CLS "
+                 "LayerNorm + classifier head")
     traffic, traffic_src = None, None
     for name in ("r2_forward_traffic.json", "r1g_forward_traffic.json"):
         try:   # committed ncu evidence: DRAM bytes of one full-batch forward
