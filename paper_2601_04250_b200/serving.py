@@ -356,8 +356,10 @@ def synthetic_tokens(n: int, seq_len: int = 128, vocab: int = 30522, seed: int =
     return ids.to(device), torch.ones((n, seq_len), dtype=torch.int32, device=device)
 
 
-def smoke() -> None:
-    """Tiny closed loop on cuda:0 (ResNet-18, B=8, 64 requests) vs the host oracle replay."""
+def smoke():
+    """Tiny closed loop on cuda:0 (ResNet-18, B=8, 64 requests, 12 decided per step).
+    Returns (server, steps, scores, now) so the caller can replay the same steps
+    on the host oracle (__graft_entry__.smoke; the product never imports it)."""
     import numpy as np
     import torch
 
@@ -378,11 +380,16 @@ def smoke() -> None:
                       synthetic_images(16), window=12)
     srv.run(1)
     srv.capture()
-    srv.drain()
+    steps = 1
+    while not srv.done():
+        srv.run(1)
+        steps += 1
     torch.cuda.synchronize()
     r = srv.results()
     assert r["decided"] == 64 and r["served"] == r["admitted"] and r["overflow"] == 0, r
     pred = srv.predicted.cpu().numpy()
     dec = srv.decision.cpu().numpy()
     assert ((pred >= 0) == ((dec == 1) | (dec == 2))).all(), "served set != admitted set"
-    print(f"smoke: closed loop ok ({r['admitted']}/64 admitted and served in batches of <= 8)")
+    print(f"smoke: closed loop ok ({r['admitted']}/64 admitted and served in batches of <= 8, "
+          f"{steps} steps)")
+    return srv, steps, tr.scores, now
