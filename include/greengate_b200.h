@@ -295,6 +295,26 @@ int gg_served_outcomes(const gg_fifo* fifo_dev, const int32_t* count_dev,
 /* Same, with the served batch's trace rows and arrival times (needed by
  * GG_LATENCY_TRACE); latency_row_dev (NULL or fp64 [trace_len]) receives each
  * served request's latency_ms at its trace row (CompletionRecord.latency_ms). */
+/* Step record written straight into pinned (host-mapped) memory by the serving
+ * step's last kernel, in place of device -> host copies: the served batch's
+ * predictions / confidences and the window's decisions.  Two slots alternate
+ * by the device step counter *seq_dev (slot = seq & 1, then seq + 1), so the
+ * host reads step i's record while step i + 1 runs.  Layout of one slot
+ * (gg_step_record_bytes(B, W) bytes): the header, int32 pred[B], double
+ * conf[B] (8-byte aligned), uint8 decision[W]. */
+typedef struct {
+  int32_t count;         /* requests served by the step */
+  int32_t n_decided;     /* window rows decided by the step */
+  int64_t window_start;  /* trace row of the window's first decision */
+  int64_t step;          /* the device step counter before this step */
+  int64_t reserved;
+} gg_step_record;
+size_t gg_step_record_bytes(int32_t B, int32_t W);
+int gg_publish_step(const int32_t* count_dev, const int32_t* batch_pred_dev,
+                    const double* batch_conf_dev, const uint8_t* decision_dev,
+                    const gg_batch_info* info_dev, const gg_fifo* fifo_dev, int32_t B, int32_t W,
+                    void* host_records, int64_t* seq_dev, void* stream);
+
 int gg_served_outcomes_trace(const gg_fifo* fifo_dev, const int32_t* count_dev,
                              const uint64_t* batch_ns_dev, const int32_t* batch_ids_dev,
                              const double* now_dev, const gg_outcome_model* model,

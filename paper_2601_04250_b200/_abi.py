@@ -87,3 +87,9 @@ STATE_OFFSETS = {name: getattr(gg_state, name).offset for name, _ in gg_state._f
 STATE_BYTES = C.sizeof(gg_state)
 BATCH_INFO_BYTES = C.sizeof(gg_batch_info)
 SNAPSHOT_BYTES = C.sizeof(gg_snapshot)
+
+
+class gg_step_record(C.Structure):
+    """gg_step_record (include/greengate_b200.h): header of a published step record."""
+    _fields_ = [("count", C.c_int32), ("n_decided", C.c_int32), ("window_start", C.c_int64),
+                ("step", C.c_int64), ("reserved", C.c_int64)]

@@ -496,6 +496,47 @@ __global__ void __launch_bounds__(kFbThreads) fallback_kernel(
 
 using namespace gg;
 
+
+// ---- step record into host-mapped memory (gg_publish_step) -------------------
+static __host__ __device__ inline size_t step_rec_conf_off(int B) {
+  return (sizeof(gg_step_record) + 4 * (size_t)B + 7) & ~(size_t)7;
+}
+static __host__ __device__ inline size_t step_rec_bytes(int B, int W) {
+  return (step_rec_conf_off(B) + 8 * (size_t)B + (size_t)W + 63) & ~(size_t)63;
+}
+
+__global__ void publish_step_kernel(const int32_t* count, const int32_t* pred, const double* conf,
+                                    const uint8_t* decision, const gg_batch_info* info,
+                                    const gg_fifo* fifo, int B, int W, uint8_t* host, int64_t* seq) {
+  griddep_wait();   // PDL: the predecessor has completed and flushed
+  griddep_launch();
+  const int64_t s = *seq;
+  uint8_t* rec = host + (s & 1) * step_rec_bytes(B, W);
+  const int n = *count;
+  const int64_t nd = info ? info->n_decided : 0;
+  const int64_t w0 = fifo->cursor - nd;
+  int32_t* rp = reinterpret_cast<int32_t*>(rec + sizeof(gg_step_record));
+  double* rc = reinterpret_cast<double*>(rec + step_rec_conf_off(B));
+  uint8_t* rd = rec + step_rec_conf_off(B) + 8 * (size_t)B;
+  for (int i = threadIdx.x; i < B; i += blockDim.x) {
+    rp[i] = i < n ? pred[i] : -1;
+    rc[i] = i < n ? conf[i] : 0.0;
+  }
+  for (int i = threadIdx.x; i < W; i += blockDim.x) rd[i] = i < nd ? decision[w0 + i] : (uint8_t)254;
+  if (threadIdx.x == 0) {
+    gg_step_record h;
+    h.count = n;
+    h.n_decided = (int32_t)nd;
+    h.window_start = w0;
+    h.step = s;
+    h.reserved = 0;
+    *reinterpret_cast<gg_step_record*>(rec) = h;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) *seq = s + 1;
+}
+
 extern "C" {
 
 int gg_fifo_pop(gg_fifo* fifo_dev, const int32_t* ring_ids_dev, const uint64_t* ring_ns_dev,
@@ -554,6 +595,25 @@ int gg_served_outcomes(const gg_fifo* fifo_dev, const int32_t* count_dev,
                        const gg_batch_info* info_dev, double* slot_dev, int32_t B, void* stream) {
   return gg_served_outcomes_trace(fifo_dev, count_dev, batch_ns_dev, nullptr, nullptr, model,
                                   info_dev, slot_dev, B, nullptr, stream);
+}
+
+
+size_t gg_step_record_bytes(int32_t B, int32_t W) {
+  return (B < 1 || W < 1) ? 0 : step_rec_bytes(B, W);
+}
+
+int gg_publish_step(const int32_t* count_dev, const int32_t* batch_pred_dev,
+                    const double* batch_conf_dev, const uint8_t* decision_dev,
+                    const gg_batch_info* info_dev, const gg_fifo* fifo_dev, int32_t B, int32_t W,
+                    void* host_records, int64_t* seq_dev, void* stream) {
+  if (!count_dev || !batch_pred_dev || !batch_conf_dev || !decision_dev || !info_dev || !fifo_dev ||
+      !host_records || !seq_dev || B < 1 || W < 1)
+    return GG_ERR_INVALID_ARGUMENT;
+  GG_PDL_LAUNCH((publish_step_kernel), 1, 256, 0, gg_stream(stream), count_dev, batch_pred_dev,
+                batch_conf_dev, decision_dev, info_dev, fifo_dev, B, W,
+                reinterpret_cast<uint8_t*>(host_records), seq_dev);
+  GG_LAUNCH_OK();
+  return GG_OK;
 }
 
 int gg_served_outcomes_trace(const gg_fifo* fifo_dev, const int32_t* count_dev,

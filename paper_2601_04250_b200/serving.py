@@ -83,7 +83,7 @@ class GatedServer:
                  outcome: OutcomeModel | None = None, fifo_capacity: int = 1 << 20,
                  rank: int = 0, world: int = 1, process_group=None, open_loop: bool = False,
                  batching_window_ms: float | None = None, labels=None, coins=None,
-                 fallback_degradation: float = 0.05):
+                 fallback_degradation: float = 0.05, publish: bool = False):
         torch = _native.require_cuda()
         self.torch = torch
         self.lib = _native.load()
@@ -143,6 +143,14 @@ class GatedServer:
         else:
             self.tok_ids = torch.empty((self.B, net.seq_len), dtype=torch.int32, **z)
             self.tok_mask = torch.empty((self.B, net.seq_len), dtype=torch.int32, **z)
+        # publish: every step ends by writing its record (served predictions and
+        # confidences, the window's decisions) into pinned host memory
+        # (gg_publish_step), two slots alternating -- no device -> host copies
+        self.publish = bool(publish)
+        if self.publish:
+            self.rec_bytes = int(self.lib.gg_step_record_bytes(self.B, self.W))
+            self.host_records = torch.zeros(2 * self.rec_bytes, dtype=torch.uint8).pin_memory()
+            self.rec_seq = torch.zeros(1, dtype=torch.int64, **z)
         self.graph = None
         self.stream = torch.cuda.Stream(device=self.dev)
         self.steps_run = 0
@@ -225,6 +233,11 @@ class GatedServer:
             _native.ptr(self.fifo), _native.ptr(self.count), _native.ptr(self.batch_ns),
             _native.ptr(self.batch_ids), _native.ptr(self.now), C.byref(self.outcome),
             _native.ptr(self.info), _native.ptr(my_slot), self.B, _native.ptr(self.latency), st))
+        if self.publish:
+            _native.check("gg_publish_step", lib.gg_publish_step(
+                _native.ptr(self.count), _native.ptr(self.batch_pred), _native.ptr(self.batch_conf),
+                _native.ptr(self.decision), _native.ptr(self.info), _native.ptr(self.fifo), self.B,
+                self.W, C.c_void_p(self.host_records.data_ptr()), _native.ptr(self.rec_seq), st))
 
     def step_feedback(self):
         """K2 over every rank's slot (after the exchange)."""
@@ -271,6 +284,25 @@ class GatedServer:
         self.steps_run += steps
 
     # ------------------------------------------------------------------ host views
+    def record(self, step: int) -> dict:
+        """The published record of device step `step` (publish=True), read from pinned
+        host memory -- valid once the step has completed (e.g. after an event on
+        the serving stream recorded behind it) and before step + 2 runs."""
+        import numpy as np
+        if not self.publish:
+            raise RuntimeError("GatedServer(publish=True) writes step records")
+        raw = self.host_records.numpy()[(step & 1) * self.rec_bytes:((step & 1) + 1) * self.rec_bytes]
+        hdr = _abi.gg_step_record.from_buffer_copy(raw[:C.sizeof(_abi.gg_step_record)].tobytes())
+        if hdr.step != step:
+            raise RuntimeError(f"record slot holds step {hdr.step}, not {step}")
+        B, h = self.B, C.sizeof(_abi.gg_step_record)
+        co = (h + 4 * B + 7) & ~7
+        n = int(hdr.count)
+        return {"count": n, "window_start": int(hdr.window_start),
+                "pred": raw[h:h + 4 * B].view(np.int32)[:n].copy(),
+                "conf": raw[co:co + 8 * B].view(np.float64)[:n].copy(),
+                "decision": raw[co + 8 * B:co + 8 * B + int(hdr.n_decided)].copy()}
+
     def fifo_state(self) -> _abi.gg_fifo:
         return _abi.gg_fifo.from_buffer_copy(bytes(self.fifo.cpu().numpy().tobytes()))
 

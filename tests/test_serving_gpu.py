@@ -163,3 +163,38 @@ def test_serving_policies_vs_oracle(kind, k, B, window, open_loop, win_ms, laten
         assert r["served"] == n
     s = srv.summary()
     assert s["admitted_count"] + s["skipped_count"] == n and 0.0 <= s["accuracy"] <= 1.0
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_published_step_records(graph):
+    """GatedServer(publish=True): each step's last kernel writes the served batch's
+    predictions / confidences and the window's decisions into pinned host memory
+    (gg_publish_step); the record of step i equals the device arrays after step i."""
+    import torch
+    import paper_2601_04250_b200 as gg
+    from paper_2601_04250_b200 import serving
+    from paper_2601_04250_b200.distilbert import DistilBertB200, random_model
+    scores, now = make_trace(400, 2, seed=21)
+    ctl = gg.ControllerConfig(alpha=1.0, beta=-0.2, gamma=-0.3, tau0=0.8, tau_inf=0.35,
+                              k=1.5).build(gg.EnergyLedger())
+    net = DistilBertB200(random_model(0), max_batch=16)
+    srv = serving.GatedServer(ctl, net, torch.from_numpy(scores).cuda(),
+                              torch.from_numpy(now).cuda(), serving.synthetic_tokens(32),
+                              window=24, outcome=serving.OutcomeModel(**MODEL), publish=True)
+    srv.run(1)
+    if graph:
+        srv.capture()
+    c0 = 24
+    for _ in range(12):
+        srv.run(1)
+        torch.cuda.synchronize()
+        rec = srv.record(srv.steps_run - 1)
+        n = int(srv.count.item())
+        assert rec["count"] == n
+        assert np.array_equal(rec["pred"], srv.batch_pred[:n].cpu().numpy())
+        assert np.array_equal(rec["conf"], srv.batch_conf[:n].cpu().numpy())
+        assert rec["window_start"] == c0
+        assert np.array_equal(rec["decision"], srv.decision[c0:c0 + len(rec["decision"])].cpu().numpy())
+        c0 += len(rec["decision"])
+    with pytest.raises(RuntimeError):
+        srv.record(srv.steps_run - 3)   # the slot has been reused
