@@ -515,14 +515,27 @@ def roofline_forward(srv, net, B):
         for _ in range(3):
             g.replay()
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(s)
-    with torch.cuda.stream(s):
-        for _ in range(reps):
-            g.replay()
-    b.record(s)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / reps
+
+    def timed(n):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        with torch.cuda.stream(s):
+            for _ in range(n):
+                g.replay()
+        b.record(s)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+    # (1) "timed alone" (the burst peak's regime): after an idle gap that lets the
+    # board's power budget recover, 2 warm replays then 5 back to back (~7 ms at
+    # DistilBERT size, ~2 ms at ResNet size); the median of 3 such bursts.
+    # (2) 20 replays back to back: power-capped on B200, against the sustained peak.
+    bursts = []
+    for _ in range(3):
+        time.sleep(0.1)
+        timed(2)
+        bursts.append(timed(5))
+    ms = sorted(bursts)[1]
+    ms_sus = timed(reps)
     flops = net.flops(B)
     pk = peaks()
     achieved = flops / (ms * 1e-3) / 1e12
@@ -543,14 +556,19 @@ def roofline_forward(srv, net, B):
             break
         except Exception:
             continue
+    achieved_sus = flops / (ms_sus * 1e-3) / 1e12
     return {"bound": "tensor", "achieved": round(achieved, 2), "peak": pk["bf16"],
             "unit": "TFLOP/s", "frac": round(achieved / pk["bf16"], 4),
-            "frac_of_sustained": round(achieved / pk["bf16_sustained"], 4),
+            "ms_per_launch_back_to_back": round(ms_sus, 4),
+            "achieved_back_to_back": round(achieved_sus, 2),
+            "frac_of_sustained": round(achieved_sus / pk["bf16_sustained"], 4),
             "traffic": traffic, "traffic_unit": "bytes per forward (DRAM read + write)",
             "traffic_source": traffic_src, "kernel": kern, "flops_per_launch": flops,
             "ms_per_launch": round(ms, 4),
-            "peak_source": pk["source"] + " bf16_tflops (burst: the forward is timed alone, "
-                                          f"{reps} back-to-back reps)"}
+            "peak_source": pk["source"] + " bf16_tflops (burst: median of 3 bursts of 5 "
+                                          "back-to-back forwards after an idle gap; the "
+                                          f"{reps}-replay back-to-back figure is set against "
+                                          "bf16_tflops_sustained)"}
 
 
 def forward_energy(srv, net, B, seconds: float = 0.5):
