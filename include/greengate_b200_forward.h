@@ -110,6 +110,24 @@ typedef struct {
 int gg_gemm_dep(const void* A, int64_t lda, const void* B, int64_t ldb, void* D, int64_t ldd,
                 int64_t M, int64_t N, int64_t K, const gg_gemm_epilogue* epilogue,
                 const gg_gemm_ln_params* ln /* or NULL */, const gg_dep* dep, void* stream);
+/* DistilBERT's feed-forward block as ONE persistent CTA-pair kernel, with the
+ * LayerNorm folding of gg_gemm_ln:
+ *   H = gelu(LN1(A) W1^T + b1)     (W1 = W1' = W1 diag(gamma1), colsum1 / bias1
+ *                                   the folded column sums / bias, a_stats = A's
+ *                                   row statistics partials)
+ *   Y = H W2^T + bias2 + LN1(A)     (the residual LayerNorm'd on the fly with
+ *                                   r_stats = a_stats, ln_gamma / ln_beta)
+ *   out_stats = Y's row statistics partials
+ * A [M, d], W1 [F, d], H [M, F] (workspace), W2 [d, F], Y [M, d] bf16; d <= 768
+ * and F <= 3072 multiples of 256, M a multiple of 128.  lin2 tiles wait per
+ * 128-row unit for that unit's lin1 tiles (ready[M / 128], zeroed by the caller
+ * before the launch, like the tile counter tiles[1]); tiles of both GEMMs are
+ * claimed from one queue, so the two partial last waves merge. */
+int gg_ffn_pair(const void* A, const void* W1, void* H, const void* W2, void* Y, int64_t M, int32_t d,
+                int32_t F, const int32_t* count_dev, int32_t rows_per_item, const float* bias1,
+                const float* colsum1, const float* a_stats, const float* bias2,
+                const float* r_stats, const float* ln_gamma, const float* ln_beta,
+                float* out_stats, float eps, int32_t* ready, int32_t* tiles, void* stream);
 /* cudaMemsetAsync(ptr, 0, bytes) on the stream (counter reset, graph-capturable). */
 int gg_zero_async(void* ptr, int64_t bytes, void* stream);
 

@@ -47,6 +47,8 @@ SIGNATURES: dict[str, tuple] = {
     "gg_attention_dep": (C.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P]),
     "gg_gemm_dep": (C.c_int, [_P, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
     "gg_zero_async": (C.c_int, [_P, _I64, _P]),
+    "gg_ffn_pair": (C.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _I32, _P, _P, _P, _P, _P, _P,
+                              _P, _P, C.c_float, _P, _P, _P]),
     "gg_step_record_bytes": (C.c_size_t, [_I32, _I32]),
     "gg_publish_step": (C.c_int, [_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P]),
     "gg_layernorm": (C.c_int, [_P, _I64, _P, _I64, _P, _P, _I64, _I32, C.c_float, _P, _I32, _P]),

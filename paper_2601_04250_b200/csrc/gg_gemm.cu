@@ -1054,6 +1054,446 @@ __global__ void __launch_bounds__(96 + 32 * EW, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fused FFN (DistilBERT lin1 + GELU -> lin2 + residual) as ONE persistent
+// CTA-pair kernel.  The two GEMMs' tiles share one dynamic queue: lin1 tiles
+// (256 x 256, K = 768, LayerNorm-folded A, exact-erf GELU) first, in row-block
+// order, then lin2 tiles (256 x 256, K = 3072, LayerNorm'd residual, output row
+// statistics).  A lin2 tile waits, in its producer, for the 12 lin1 tiles of
+// its 128-row unit (per-unit counters: TMA stores complete -> proxy fence ->
+// red.release; acquire -> proxy fence -> TMA loads), so pairs that run out of
+// lin1 tiles start lin2 work at once: one kernel tail instead of two and the
+// two GEMMs' partial last waves (10.38 + 2.59) merge.
+constexpr int kFfnMaxUp = 3072;     // lin1 N (bias / column sums staged in smem)
+constexpr int kFfnMaxDown = 768;    // lin2 N = LayerNorm width (bias, gamma | beta)
+constexpr int kFfnStages = 5;
+constexpr int kFfnEW = 8;
+constexpr int kFfnThreads = 96 + 32 * kFfnEW;
+struct FfnCfg {
+  static constexpr int A_BYTES = 128 * kBK * 2, B_BYTES = 128 * kBK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = kFfnStages * STAGE_BYTES;
+  static constexpr int BIAS0_OFF = BAR_OFF + 512;
+  static constexpr int AUX0_OFF = BIAS0_OFF + kFfnMaxUp * 4;
+  static constexpr int BIAS1_OFF = AUX0_OFF + kFfnMaxUp * 4;
+  static constexpr int AUX1_OFF = BIAS1_OFF + kFfnMaxDown * 4;
+  static constexpr int STG_OFF = (AUX1_OFF + 2 * kFfnMaxDown * 4 + 1023) & ~1023;
+  static constexpr int SMEM = STG_OFF + kFfnEW * 2 * 2048 + 1024;
+  static_assert(SMEM <= 232448, "fused FFN shared memory");
+};
+
+struct FfnArgs {
+  int M_max;
+  const int32_t* count;
+  int rows_per_item;
+  int n_up, n_down, k_up;           // lin1 N (= lin2 K), lin2 N (= lin1 K = LayerNorm width)
+  const float* bias0;               // lin1 folded bias c_j
+  const float* colsum0;             // lin1 column sums s_j of W' = W diag(gamma)
+  const float2* a_stats;            // statistics partials of lin1's raw input rows
+  const float* bias1;               // lin2 bias
+  const float2* r_stats;            // residual rows' statistics partials (LayerNorm'd on the fly)
+  const float* r_gamma;
+  const float* r_beta;
+  float2* out_stats;                // lin2 output rows' partials
+  int parts;                        // partials per row (width / 128)
+  int64_t ln_ld;
+  float eps;
+  int* ready;                       // [units] lin1 tiles published per 128-row unit (zeroed)
+  int* tiles;                       // tile claim counter (zeroed)
+  long long* prof;                  // GG_GEMM_PROF: per pair [issuer, acc wait, operand wait, tiles,
+                                    //  lin2 dependency wait, lin1 tiles], or null
+};
+
+__global__ void __launch_bounds__(kFfnThreads, 1)
+    gemm_ffn_pair(const __grid_constant__ CUtensorMap map_a0, const __grid_constant__ CUtensorMap map_b0,
+                  const __grid_constant__ CUtensorMap map_o0, const __grid_constant__ CUtensorMap map_a1,
+                  const __grid_constant__ CUtensorMap map_b1, const __grid_constant__ CUtensorMap map_o1,
+                  const __grid_constant__ CUtensorMap map_r1, FfnArgs f) {
+  using Cf = FfnCfg;
+  constexpr int EW = kFfnEW, STAGES = kFfnStages, PARTS = EW / 4, CW = kPairBN / PARTS, NCH = CW / 32;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_align1k(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;     // [2]
+  uint64_t* acc_empty = acc_full + 2;      // [2]
+  uint64_t* res_full = acc_empty + 2;      // [EW][2]
+  uint64_t* tile_full = res_full + 2 * EW; // [4]
+  uint64_t* tile_empty = tile_full + 4;    // [4]
+  uint64_t* tile_took = tile_empty + 4;    // [4]
+  int* tile_ring = reinterpret_cast<int*>(tile_took + 4);
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tile_ring + 4);
+  int* cnt_slot = reinterpret_cast<int*>(tmem_base_smem + 1);
+  float* bias0_s = reinterpret_cast<float*>(smem + Cf::BIAS0_OFF);
+  float* aux0_s = reinterpret_cast<float*>(smem + Cf::AUX0_OFF);
+  float* bias1_s = reinterpret_cast<float*>(smem + Cf::BIAS1_OFF);
+  float* aux1_s = reinterpret_cast<float*>(smem + Cf::AUX1_OFF);
+  uint8_t* stg_base = smem + Cf::STG_OFF;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  griddep_launch();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&acc_full[a], 1);
+      mbar_init(&acc_empty[a], 2);
+    }
+    for (int i = 0; i < 2 * EW; ++i) mbar_init(&res_full[i], 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&tile_full[i], 1);
+      mbar_init(&tile_empty[i], 3 + 2 * EW);
+      mbar_init(&tile_took[i], 1);
+    }
+    fence_mbar_init();
+    tma_prefetch(&map_a0);
+    tma_prefetch(&map_b0);
+    tma_prefetch(&map_o0);
+    tma_prefetch(&map_a1);
+    tma_prefetch(&map_b1);
+    tma_prefetch(&map_o1);
+    tma_prefetch(&map_r1);
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_base_smem, 2 * kPairBN);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+  griddep_wait();   // lin1's input rows, statistics and the count follow the predecessor
+  if (threadIdx.x == 0) *cnt_slot = f.count ? __ldg(f.count) : 0;
+  __syncthreads();
+  const int M = f.count ? min(f.M_max, *cnt_slot * f.rows_per_item) : f.M_max;
+  const int tiles_m = (M + 255) / 256;
+  const int tn0 = f.n_up / kPairBN, tn1 = f.n_down / kPairBN;
+  const int T0 = tiles_m * tn0, num_tiles = T0 + tiles_m * tn1;
+  const int kb0 = f.k_up / kBK, kb1 = f.n_up / kBK;
+  const uint32_t leader_tile_empty0 = mapa_shared(smem_u32(&tile_empty[0]), 0);
+  auto read_tile = [&](int i, bool release) -> int {
+    const int slot = i & 3;
+    if (rank == 0) mbar_wait(&tile_full[slot], (i >> 2) & 1);
+    else mbar_wait_cluster(&tile_full[slot], (i >> 2) & 1);
+    const int tile = tile_ring[slot];
+    if (release && tile < num_tiles) {
+      if (rank == 0) mbar_arrive_relaxed(&tile_empty[slot]);
+      else mbar_arrive_cluster_relaxed(leader_tile_empty0 + slot * 8);
+    }
+    return tile;
+  };
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs)
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      long long wdep = 0;
+      int nup = 0;
+      for (int i = 0;; ++i) {
+        const int tile = read_tile(i, true);
+        if (tile >= num_tiles) break;
+        if (rank == 0) mbar_arrive_relaxed(&tile_took[i & 3]);
+        const bool up = tile < T0;
+        nup += up;
+        const int tt = up ? tile : tile - T0;
+        const int tm = up ? tt / tn0 : tt / tn1, tn = up ? tt % tn0 : tt % tn1;
+        const int m0 = tm * 256 + rank * 128, n0 = tn * kPairBN + rank * 128;
+        const CUtensorMap* ma = up ? &map_a0 : &map_a1;
+        const CUtensorMap* mb = up ? &map_b0 : &map_b1;
+        if (!up && m0 < M) {   // this unit's lin1 outputs published (all tn0 tiles)
+          const long long w0 = f.prof ? clock64() : 0;
+          dep_wait_geq(f.ready + tm * 2 + rank, tn0);
+          fence_proxy_async_global();
+          if (f.prof) wdep += clock64() - w0;
+        }
+        const int nkb = up ? kb0 : kb1;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait_sleep(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * Cf::STAGE_BYTES;
+          if (rank == 0) mbar_expect_tx(&full[s], 2 * Cf::STAGE_BYTES);
+          const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+          tma_load_2d_pair(sa, ma, fb, kb * kBK, m0);
+          tma_load_2d_pair(sa + Cf::A_BYTES, mb, fb, kb * kBK, n0);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+      if (f.prof && rank == 0) {
+        f.prof[(blockIdx.x >> 1) * 8 + 4] = wdep;
+        f.prof[(blockIdx.x >> 1) * 8 + 5] = nup;
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader)
+    if (rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(256, kPairBN);
+      int s = 0, t = 0;
+      uint32_t ph = 0;
+      const uint64_t a_desc0 = sdesc_k_sw128(smem_u32(smem));
+      long long w_acc = 0, w_full = 0, mma_ideal = 0;
+      const long long t0c = clock64();
+      for (;; ++t) {
+        int tile = 0;
+        if (lane == 0) tile = read_tile(t, true);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
+        if (tile >= num_tiles) break;
+        const int nkb = tile < T0 ? kb0 : kb1;
+        mma_ideal += nkb * 512;
+        const int acc = t & 1;
+        {
+          const long long a = clock64();
+          mbar_wait(&acc_empty[acc], ((t >> 1) & 1) ^ 1);
+          w_acc += clock64() - a;
+        }
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kPairBN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          {
+            const long long a = clock64();
+            mbar_wait(&full[s], ph);
+            w_full += clock64() - a;
+          }
+          tc_fence_after();
+          const uint64_t ad = a_desc0 + (uint64_t)s * (uint64_t)(Cf::STAGE_BYTES >> 4);
+          const uint64_t bd = ad + (uint64_t)(Cf::A_BYTES >> 4);
+          if (elect_one_sync()) {
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              umma_bf16_pair(d_tmem, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+            umma_commit_pair(&empty[s], 3);
+          }
+          __syncwarp();
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        if (elect_one_sync()) umma_commit_pair(&acc_full[acc], 3);
+        __syncwarp();
+      }
+      if (f.prof && lane == 0) {
+        long long* pp = f.prof + (blockIdx.x >> 1) * 8;
+        pp[0] = clock64() - t0c;
+        pp[1] = w_acc;
+        pp[2] = w_full;
+        pp[3] = t;
+        pp[6] = mma_ideal;
+      }
+    }
+  } else if (warp == 2 + EW) {
+    // ===== tile scheduler (leader): claims in row-block order, one tile ahead
+    if (rank == 0 && lane == 0) {
+      const uint32_t peer_full0 = mapa_shared(smem_u32(&tile_full[0]), 1);
+      const uint32_t peer_ring0 = mapa_shared(smem_u32(&tile_ring[0]), 1);
+      for (int i = 0;; ++i) {
+        const int slot = i & 3;
+        if (i > 0) mbar_wait(&tile_took[(i - 1) & 3], ((i - 1) >> 2) & 1);
+        mbar_wait(&tile_empty[slot], ((i >> 2) & 1) ^ 1);
+        const int tile = atomicAdd(f.tiles, 1);
+        tile_ring[slot] = tile;
+        st_shared_cluster_s32(peer_ring0 + slot * 4, tile);
+        mbar_arrive(&tile_full[slot]);
+        mbar_arrive_cluster(peer_full0 + slot * 8);
+        if (tile >= num_tiles) break;
+      }
+    }
+  } else {
+    // ===== epilogue warps (both CTAs): lin1 = LayerNorm correction + bias + GELU,
+    // lin2 = bias + LayerNorm'd residual + output statistics; SW64 boxes, TMA stores
+    const int quarter = warp & 3;
+    const int part = (warp - 2) >> 2;
+    const int ew = warp - 2;
+    const uint32_t leader_empty0 = mapa_shared(smem_u32(&acc_empty[0]), 0);
+    for (int i = threadIdx.x - 64; i < f.n_up; i += 32 * EW) {
+      bias0_s[i] = __ldg(f.bias0 + i);
+      aux0_s[i] = __ldg(f.colsum0 + i);
+    }
+    for (int i = threadIdx.x - 64; i < f.n_down; i += 32 * EW) {
+      bias1_s[i] = __ldg(f.bias1 + i);
+      aux1_s[i] = __ldg(f.r_gamma + i);
+      aux1_s[f.n_down + i] = __ldg(f.r_beta + i);
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+    uint8_t* stg = stg_base + ew * (2 * 2048);
+    uint64_t* rb = res_full + ew * 2;
+    uint32_t rph = 0;
+    const int sw = (lane >> 1) & 3;
+    int pending = -1;   // unit of a lin1 tile whose stores may still be in flight
+    int tile = 0;
+    if (lane == 0) tile = read_tile(0, true);
+    tile = __shfl_sync(0xffffffffu, tile, 0);
+    for (int t = 0; tile < num_tiles; ++t) {
+      const bool up = tile < T0;
+      const int tt = up ? tile : tile - T0;
+      const int tm = up ? tt / tn0 : tt / tn1, tn = up ? tt % tn0 : tt % tn1;
+      const int acc = t & 1;
+      const int row0 = tm * 256 + rank * 128 + quarter * 32;
+      const int colw = tn * kPairBN + part * CW;
+      const bool rows_ok = row0 < M;
+      if (!up && rows_ok && lane == 0) {   // residual of chunk 0
+        bulk_wait_read<0>();
+        mbar_expect_tx(&rb[0], 2048);
+        tma_load_2d(stg, &map_r1, &rb[0], colw, row0);
+      }
+      float a_sc = 1.0f, a_sh = 0.0f;   // lin1: LN of the input rows; lin2: LN of the residual rows
+      if (rows_ok)
+        ln_row_params(up ? f.a_stats : f.r_stats, f.parts, f.ln_ld, row0 + lane, f.n_down, f.eps, a_sc, a_sh);
+      float st_k = 0.0f, st_s1 = 0.0f, st_s2 = 0.0f;
+      int ngroups = 0;
+      mbar_wait_sleep(&acc_full[acc], (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tacc = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * kPairBN + part * CW;
+#pragma unroll 1
+      for (int c = 0; c < NCH; ++c) {
+        const int b = c & 1;
+        uint8_t* buf = stg + b * 2048;
+        if (!up && rows_ok && lane == 0 && c + 1 < NCH) {
+          bulk_wait_read<0>();
+          mbar_expect_tx(&rb[b ^ 1], 2048);
+          tma_load_2d(stg + (b ^ 1) * 2048, &map_r1, &rb[b ^ 1], colw + 32 * (c + 1), row0);
+        }
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tacc + 32 * c, r);
+        tmem_ld_wait();
+        if (!rows_ok) continue;
+        const int col0 = colw + 32 * c;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        uint4* myrow = reinterpret_cast<uint4*>(buf + lane * 64);
+        if (up) {
+          const uint64_t sc2 = f2_pack(a_sc, a_sc), sh2 = f2_pack(a_sh, a_sh);
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 sj = *reinterpret_cast<const float4*>(aux0_s + col0 + i);
+            const float4 cj = *reinterpret_cast<const float4*>(bias0_s + col0 + i);
+            const uint64_t t0 = f2_fma(sh2, f2_pack(sj.x, sj.y), f2_pack(cj.x, cj.y));
+            const uint64_t t1 = f2_fma(sh2, f2_pack(sj.z, sj.w), f2_pack(cj.z, cj.w));
+            f2_unpack(f2_fma(sc2, f2_pack(v[i], v[i + 1]), t0), v[i], v[i + 1]);
+            f2_unpack(f2_fma(sc2, f2_pack(v[i + 2], v[i + 3]), t1), v[i + 2], v[i + 3]);
+          }
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) gelu_erf2(v[i], v[i + 1]);
+          // the store that last read this buffer (two chunks ago) is done
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 bb = *reinterpret_cast<const float4*>(bias1_s + col0 + i);
+            f2_unpack(f2_add(f2_pack(v[i], v[i + 1]), f2_pack(bb.x, bb.y)), v[i], v[i + 1]);
+            f2_unpack(f2_add(f2_pack(v[i + 2], v[i + 3]), f2_pack(bb.z, bb.w)), v[i + 2], v[i + 3]);
+          }
+          mbar_wait(&rb[b], (rph >> b) & 1u);
+          rph ^= 1u << b;
+          const uint64_t sc2 = f2_pack(a_sc, a_sc), sh2 = f2_pack(a_sh, a_sh);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 u = myrow[q ^ sw];
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+            const int cc = col0 + q * 8;
+            const float4 g0 = *reinterpret_cast<const float4*>(aux1_s + cc);
+            const float4 g1 = *reinterpret_cast<const float4*>(aux1_s + cc + 4);
+            const float4 b0 = *reinterpret_cast<const float4*>(aux1_s + f.n_down + cc);
+            const float4 b1 = *reinterpret_cast<const float4*>(aux1_s + f.n_down + cc + 4);
+            const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const float2 fr = __bfloat1622float2(h2[e >> 1]);
+              const uint64_t nrm = f2_fma(f2_pack(fr.x, fr.y), sc2, sh2);
+              const uint64_t rr = f2_fma(nrm, f2_pack(gg[e], gg[e + 1]), f2_pack(bb[e], bb[e + 1]));
+              f2_unpack(f2_add(f2_pack(v[q * 8 + e], v[q * 8 + e + 1]), rr), v[q * 8 + e], v[q * 8 + e + 1]);
+            }
+          }
+        }
+        uint4 u[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          u[q].x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+          u[q].y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+          u[q].z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+          u[q].w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) myrow[q ^ sw] = u[q];
+        if (!up) {   // lin2 output row statistics (shifted sums of the fp32 values)
+          if (c == 0) st_k = v[0];
+          const uint64_t nk = f2_pack(-st_k, -st_k);
+          uint64_t s1 = f2_pack(0.0f, 0.0f), s2 = f2_pack(0.0f, 0.0f);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const uint64_t d = f2_add(f2_pack(v[i], v[i + 1]), nk);
+            s1 = f2_add(s1, d);
+            s2 = f2_fma(d, d, s2);
+          }
+          float a0, a1, c0, c1;
+          f2_unpack(s1, a0, a1);
+          f2_unpack(s2, c0, c1);
+          st_s1 += a0 + a1;
+          st_s2 += c0 + c1;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(up ? &map_o0 : &map_o1, buf, col0, row0);
+          bulk_commit();
+        }
+        ++ngroups;
+      }
+      if (!up && rows_ok) {
+        const float n = (float)CW;
+        const float mi = st_k + st_s1 / n;
+        const float m2 = fmaxf(st_s2 - st_s1 * st_s1 / n, 0.0f);
+        f.out_stats[(int64_t)(tn * PARTS + part) * f.ln_ld + row0 + lane] = make_float2(mi, m2);
+      }
+      tc_fence_before();
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+      if (threadIdx.x == 64) {
+        if (rank == 0) mbar_arrive(&acc_empty[acc]);
+        else mbar_arrive_cluster(leader_empty0 + acc * 8);
+      }
+      // Publication of lin1 tiles for their units' lin2 tiles, one tile late (the
+      // stores had a tile's time to land) -- except before this pair's first lin2
+      // tile or the end, which may wait on this very tile: then at once.
+      int next = 0;
+      if (lane == 0) next = read_tile(t + 1, true);
+      next = __shfl_sync(0xffffffffu, next, 0);
+      const int unit = tm * 2 + (int)rank;
+      const bool valid_unit = tm * 256 + (int)rank * 128 < M;
+      const bool flush_now = up && (next >= T0);
+      if (pending >= 0 || flush_now) {
+        if (lane == 0) {
+          if (flush_now || ngroups == 0) bulk_wait<0>();
+          else if (ngroups == 1) bulk_wait<1>();
+          else if (ngroups == 2) bulk_wait<2>();
+          else if (ngroups == 3) bulk_wait<3>();
+          else bulk_wait<4>();
+          fence_proxy_async_global();
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * EW) : "memory");
+        if (threadIdx.x == 64) {
+          if (pending >= 0) dep_signal_add_nofence(f.ready + pending, 1);
+          if (flush_now && valid_unit) dep_signal_add_nofence(f.ready + unit, 1);
+        }
+      }
+      pending = (up && !flush_now && valid_unit) ? unit : -1;
+      tile = next;
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 2 * kPairBN);
+  }
+}
+
 template <int STAGES, int EW, int NBUF, int EK>
 static int launch_gemm_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                             const CUtensorMap& mr, int M, int N, int K, const GemmEpilogue& ep,
@@ -1284,6 +1724,100 @@ extern "C" int gg_gemm_dep(const void* A, int64_t lda, const void* B, int64_t ld
                            const gg_gemm_ln_params* ln, const gg_dep* dep, void* stream) {
   if (!dep) return GG_ERR_INVALID_ARGUMENT;
   return gemm_impl(A, lda, B, ldb, D, ldd, M, N, K, e, ln, dep, stream);
+}
+
+
+extern "C" int gg_ffn_pair(const void* A, const void* W1, void* H, const void* W2, void* Y,
+                           int64_t M, int32_t d, int32_t F, const int32_t* count_dev,
+                           int32_t rows_per_item, const float* bias1, const float* colsum1,
+                           const float* a_stats, const float* bias2, const float* r_stats,
+                           const float* ln_gamma, const float* ln_beta, float* out_stats, float eps,
+                           int32_t* ready, int32_t* tiles, void* stream) {
+  if (!A || !W1 || !H || !W2 || !Y || !bias1 || !colsum1 || !a_stats || !bias2 || !r_stats ||
+      !ln_gamma || !ln_beta || !out_stats || !ready || !tiles || M <= 0)
+    return GG_ERR_INVALID_ARGUMENT;
+  if (d % kPairBN || F % kPairBN || d > kFfnMaxDown || F > kFfnMaxUp || d % 128 || M % 128 ||
+      M > 0x7fffffff || (count_dev && rows_per_item % 128))
+    return GG_ERR_UNSUPPORTED;
+  CUtensorMap ma0, mb0, mo0, ma1, mb1, mo1, mr1;
+  int rc = make_map_2d(&ma0, A, M, d, d, 128);
+  if (!rc) rc = make_map_2d(&mb0, W1, F, d, d, 128);
+  if (!rc) rc = make_map_box32(&mo0, H, M, F, F);
+  if (!rc) rc = make_map_2d(&ma1, H, M, F, F, 128);
+  if (!rc) rc = make_map_2d(&mb1, W2, d, F, F, 128);
+  if (!rc) rc = make_map_box32(&mo1, Y, M, d, d);
+  if (!rc) rc = make_map_box32(&mr1, A, M, d, d);
+  if (rc) return rc;
+  FfnArgs f;
+  f.M_max = (int)M;
+  f.count = count_dev;
+  f.rows_per_item = count_dev ? rows_per_item : 1;
+  f.n_up = F;
+  f.n_down = d;
+  f.k_up = d;
+  f.bias0 = bias1;
+  f.colsum0 = colsum1;
+  f.a_stats = reinterpret_cast<const float2*>(a_stats);
+  f.bias1 = bias2;
+  f.r_stats = reinterpret_cast<const float2*>(r_stats);
+  f.r_gamma = ln_gamma;
+  f.r_beta = ln_beta;
+  f.out_stats = reinterpret_cast<float2*>(out_stats);
+  f.parts = d / 128;
+  f.ln_ld = M;
+  f.eps = eps;
+  f.ready = ready;
+  f.tiles = tiles;
+  static long long* prof = nullptr;
+  const bool do_prof = getenv("GG_GEMM_PROF") != nullptr;
+  f.prof = nullptr;
+  if (do_prof) {
+    if (!prof) cudaMalloc(&prof, 1024 * sizeof(long long));
+    cudaMemsetAsync(prof, 0, 1024 * sizeof(long long), gg_stream(stream));
+    f.prof = prof;
+  }
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(gemm_ffn_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, FfnCfg::SMEM) !=
+        cudaSuccess)
+      return GG_ERR_CUDA;
+    attr = true;
+  }
+  const int pairs = num_sms() / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kFfnThreads);
+  cfg.dynamicSmemBytes = FfnCfg::SMEM;
+  cfg.stream = gg_stream(stream);
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  if (cudaLaunchKernelEx(&cfg, gemm_ffn_pair, ma0, mb0, mo0, ma1, mb1, mo1, mr1, f) != cudaSuccess)
+    return GG_ERR_CUDA;
+  GG_LAUNCH_OK();
+  if (do_prof) {
+    long long h[1024];
+    cudaDeviceSynchronize();
+    cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost);
+    double tot = 0, wa = 0, wf = 0, nt = 0, wd = 0, nu = 0, ideal = 0, tmax = 0, imax = 0;
+    for (int i = 0; i < pairs; ++i) {
+      tot += h[8 * i]; wa += h[8 * i + 1]; wf += h[8 * i + 2]; nt += h[8 * i + 3];
+      wd += h[8 * i + 4]; nu += h[8 * i + 5]; ideal += h[8 * i + 6];
+      tmax = h[8 * i] > tmax ? h[8 * i] : tmax;
+      imax = h[8 * i + 6] > imax ? h[8 * i + 6] : imax;
+    }
+    fprintf(stderr, "ffn pair M=%lld: issuer %.0f cycles/pair (max %.0f), MMA-bound %.0f (max %.0f), tiles %.2f/pair "
+            "(lin1 %.2f), waiting acc %.0f%% operands %.0f%%, lin2 dependency wait %.0f cycles/pair\n",
+            (long long)M, tot / pairs, tmax, ideal / pairs, imax, nt / pairs, nu / pairs, 100 * wa / tot,
+            100 * wf / tot, wd / pairs);
+  }
+  return GG_OK;
 }
 
 extern "C" int gg_zero_async(void* ptr, int64_t bytes, void* stream) {

@@ -162,6 +162,14 @@ class DistilBertB200:
         nl = len(self.layers)
         self.deps = torch.zeros(1 + nl * 5 * max_batch + nl * 5, dtype=torch.int32,
                                 device=self.device)
+        # fused feed-forward block (gg_ffn_pair, opt-in GG_FFN_FUSE=1): per layer, lin1
+        # tiles published per 128-row unit + the tile claim counter; zeroed once per
+        # forward.  Bit-identical to the two launches but measured no faster (DESIGN.md
+        # section 7, finding H): the merged queue's last lin2 tiles leave the same
+        # imbalance as FFN-down's partial wave, and the row-block raster slows lin1.
+        self.use_ffn_fused = self.fused_ln and os.environ.get("GG_FFN_FUSE") == "1"
+        self.ffn_units = max_batch * seq_len // 128
+        self.ffn_ctr = torch.zeros(nl * (self.ffn_units + 1), dtype=torch.int32, device=self.device)
 
     def _fold_layernorms(self, sd) -> None:
         """W' = W diag(gamma) (bf16), s_j = sum_k W'_jk and c_j = b_j + sum_k beta_k W_jk
@@ -270,6 +278,9 @@ class DistilBertB200:
         if self.use_deps:
             _native.check("gg_zero_async", lib.gg_zero_async(_native.ptr(self.deps),
                                                              self.deps.numel() * 4, st))
+        if self.use_ffn_fused:
+            _native.check("gg_zero_async", lib.gg_zero_async(_native.ptr(self.ffn_ctr),
+                                                             self.ffn_ctr.numel() * 4, st))
         H = self.HEADS
         x0 = self.x.data_ptr()       # embeddings + LayerNorm (normalized)
         hA = self.x1.data_ptr()      # h1 = ctx W_o^T + b_o + x   (raw, LN1 folded downstream)
@@ -307,14 +318,25 @@ class DistilBertB200:
                      residual=hB, ldr=D,
                      ln=GemmLn(None, None, p2, P["ln2_g"].data_ptr(), P["ln2_b"].data_ptr(), p1,
                                D, f), dep=d_out, **dyn)
-            gemm(lib, hA, D, L["w1_f"], self.ffn.data_ptr(), self.FFN, M, self.FFN, D, st,
-                 bias=L["c_1"], act=GELU,
-                 ln=GemmLn(p1, L["s_1"].data_ptr(), None, None, None, None, D, f),
-                 dep=dep(i, 3, ctr(i, 2), D // 256), **dyn)
-            gemm(lib, self.ffn.data_ptr(), self.FFN, L["w2"], hB, D, M, D, self.FFN, st,
-                 bias=L["b2"], residual=hA, ldr=D,
-                 ln=GemmLn(None, None, p1, L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), p2, D, f),
-                 dep=dep(i, 4, ctr(i, 3), self.FFN // 256), **dyn)
+            if self.use_ffn_fused and not self.use_deps:
+                # lin1 + GELU and lin2 + residual as one persistent kernel (tile queue)
+                u = self.ffn_units + 1
+                cbase = self.ffn_ctr.data_ptr() + 4 * i * u
+                _native.check("gg_ffn_pair", lib.gg_ffn_pair(
+                    C.c_void_p(hA), _native.ptr(L["w1_f"]), _native.ptr(self.ffn), _native.ptr(L["w2"]),
+                    C.c_void_p(hB), M, D, self.FFN, cnt, S if count is not None else 0,
+                    _native.ptr(L["c_1"]), _native.ptr(L["s_1"]), C.c_void_p(p1), _native.ptr(L["b2"]),
+                    C.c_void_p(p1), _native.ptr(L["ln1_g"]), _native.ptr(L["ln1_b"]), C.c_void_p(p2), f,
+                    C.c_void_p(cbase), C.c_void_p(cbase + 4 * self.ffn_units), st))
+            else:
+                gemm(lib, hA, D, L["w1_f"], self.ffn.data_ptr(), self.FFN, M, self.FFN, D, st,
+                     bias=L["c_1"], act=GELU,
+                     ln=GemmLn(p1, L["s_1"].data_ptr(), None, None, None, None, D, f),
+                     dep=dep(i, 3, ctr(i, 2), D // 256), **dyn)
+                gemm(lib, self.ffn.data_ptr(), self.FFN, L["w2"], hB, D, M, D, self.FFN, st,
+                     bias=L["b2"], residual=hA, ldr=D,
+                     ln=GemmLn(None, None, p1, L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), p2, D, f),
+                     dep=dep(i, 4, ctr(i, 3), self.FFN // 256), **dyn)
         last = self.layers[-1]
         # the head reads only the CLS rows: LayerNorm of those B rows (stride S*D)
         _native.check("gg_layernorm", lib.gg_layernorm(

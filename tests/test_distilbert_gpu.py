@@ -141,3 +141,40 @@ def test_distilbert_dependency_chain(env):
         g.replay()
     torch.cuda.synchronize()
     assert torch.equal(gout, outs[(True, 128)])
+
+
+def test_distilbert_fused_ffn(env):
+    """gg_ffn_pair (lin1 + GELU and lin2 + residual in one persistent kernel, one
+    tile queue, per-unit readiness) gives the same logits bit for bit as the two
+    GEMM launches, at the full batch and at a dynamic count, and inside a graph."""
+    torch = env[0]
+    from paper_2601_04250_b200.distilbert import DistilBertB200, random_model
+    model = random_model(0)
+    ids = torch.randint(0, model.config.vocab_size, (128, 128),
+                        generator=torch.Generator().manual_seed(8)).to(torch.int32).cuda()
+    mask = torch.ones((128, 128), dtype=torch.int32, device="cuda")
+    mask[3, 70:] = 0
+    net = DistilBertB200(model, max_batch=128)
+    outs = {}
+    for fused in (False, True):
+        net.use_ffn_fused = fused
+        for cnt in (128, 37):
+            count = torch.tensor([cnt], dtype=torch.int32, device="cuda")
+            for _ in range(2):
+                out = net.forward(ids, mask, count=count).clone()
+            outs[(fused, cnt)] = out
+    torch.cuda.synchronize()
+    for cnt in (128, 37):
+        assert torch.equal(outs[(True, cnt)][:cnt], outs[(False, cnt)][:cnt])
+    net.use_ffn_fused = True
+    count = torch.tensor([128], dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        net.forward(ids, mask, count=count, stream=s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            gout = net.forward(ids, mask, count=count, stream=s)
+    for _ in range(4):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(gout, outs[(True, 128)])
