@@ -162,6 +162,21 @@ int gg_layernorm(const void* x, int64_t ldx, void* y, int64_t ldy, const float* 
                  const float* beta, int64_t rows, int32_t width, float eps,
                  const int32_t* count_dev, int32_t rows_per_item, void* stream);
 
+/* DistilBERT classification head in one launch (replaces gg_layernorm of the CLS
+ * rows + the pre_classifier and classifier GEMMs): for each of `rows` CLS rows
+ * (row r at hidden + r * ld_rows, bf16 [768]): x = LayerNorm(row) (skipped when
+ * ln_gamma is NULL), pooled = bf16(ReLU(x W_pre^T + b_pre)), logits[r, :labels] =
+ * pooled W_cls^T + b_cls (fp32).  W_pre bf16 [768, 768], W_cls bf16 [labels, 768].
+ * scratch: gg_cls_head_scratch_bytes(max_rows) bytes; arrivals: int32
+ * [ceil(max_rows / 16)], zero before the first call (the kernel re-zeroes it).
+ * Deterministic. */
+int gg_cls_head(const void* hidden, int64_t ld_rows, const float* ln_gamma, const float* ln_beta,
+                float eps, const void* w_pre, const float* b_pre, const void* w_cls,
+                const float* b_cls, int32_t labels, float* logits, int64_t ld_logits, int32_t rows,
+                int32_t max_rows, const int32_t* count_dev, float* scratch, int32_t* arrivals,
+                void* stream);
+int64_t gg_cls_head_scratch_bytes(int32_t max_rows);
+
 /* DistilBERT embeddings: y[t] = LayerNorm(word[ids[t]] + pos[t % seq_len]) (bf16 tables). */
 int gg_embed_layernorm(const int32_t* ids, const void* word, const void* pos, void* y,
                        const float* gamma, const float* beta, int64_t tokens, int32_t seq_len,

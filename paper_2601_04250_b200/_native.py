@@ -52,6 +52,9 @@ SIGNATURES: dict[str, tuple] = {
     "gg_step_record_bytes": (C.c_size_t, [_I32, _I32]),
     "gg_publish_step": (C.c_int, [_P, _P, _P, _P, _P, _P, _I32, _I32, _P, _P, _P]),
     "gg_layernorm": (C.c_int, [_P, _I64, _P, _I64, _P, _P, _I64, _I32, C.c_float, _P, _I32, _P]),
+    "gg_cls_head": (C.c_int, [_P, _I64, _P, _P, C.c_float, _P, _P, _P, _P, _I32, _P, _I64, _I32,
+                              _I32, _P, _P, _P, _P]),
+    "gg_cls_head_scratch_bytes": (_I64, [_I32]),
     "gg_embed_layernorm": (C.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, C.c_float, _P,
                                      _P]),
     "gg_token_gather": (C.c_int, [_P, _P, _I64, _P, _P, _I32, _I32, _P, _P, _P]),

@@ -170,6 +170,12 @@ class DistilBertB200:
         self.use_ffn_fused = self.fused_ln and os.environ.get("GG_FFN_FUSE") == "1"
         self.ffn_units = max_batch * seq_len // 128
         self.ffn_ctr = torch.zeros(nl * (self.ffn_units + 1), dtype=torch.int32, device=self.device)
+        # classification head as one launch (gg_cls_head): column-block partials of the
+        # classifier + per-16-row arrival counters (re-zeroed by the kernel)
+        self.fused_head = os.environ.get("GG_HEAD_UNFUSED") != "1"
+        hb = int(self.lib.gg_cls_head_scratch_bytes(max_batch))
+        self.head_part = torch.empty(hb // 4, dtype=torch.float32, device=self.device)
+        self.head_arr = torch.zeros((max_batch + 15) // 16, dtype=torch.int32, device=self.device)
 
     def _fold_layernorms(self, sd) -> None:
         """W' = W diag(gamma) (bf16), s_j = sum_k W'_jk and c_j = b_j + sum_k beta_k W_jk
@@ -248,6 +254,8 @@ class DistilBertB200:
                 C.c_void_p(h), D, C.c_void_p(x), D, _native.ptr(L["ln2_g"]),
                 _native.ptr(L["ln2_b"]), M, D, C.c_float(self.EPS), cnt, S, st))
         # CLS rows (stride S*D) -> pre_classifier + ReLU -> classifier (fp32 logits)
+        if self.fused_head:
+            return self._head(x, S * D, None, B, st, cnt)
         gemm(lib, x, S * D, self.w_pre, self.pooled.data_ptr(), D, B, D, D, st, bias=self.b_pre,
              act=RELU, tile_n=64, count=count, rows_per_item=1)
         gemm(lib, self.pooled.data_ptr(), D, self.w_cls, self.logits.data_ptr(),
@@ -338,6 +346,8 @@ class DistilBertB200:
                      ln=GemmLn(None, None, p1, L["ln1_g"].data_ptr(), L["ln1_b"].data_ptr(), p2, D, f),
                      dep=dep(i, 4, ctr(i, 3), self.FFN // 256), **dyn)
         last = self.layers[-1]
+        if self.fused_head:
+            return self._head(hB, S * D, last, B, st, cnt)
         # the head reads only the CLS rows: LayerNorm of those B rows (stride S*D)
         _native.check("gg_layernorm", lib.gg_layernorm(
             C.c_void_p(hB), S * D, _native.ptr(self.cls), D, _native.ptr(last["ln2_g"]),
@@ -347,6 +357,18 @@ class DistilBertB200:
         gemm(lib, self.pooled.data_ptr(), D, self.w_cls, self.logits.data_ptr(),
              self.logits.stride(0), B, self.w_cls.shape[0], D, st, bias=self.b_cls,
              out_mode=OUT_F32, tile_n=64, count=count, rows_per_item=1)
+        return self.logits[:B, : self.num_labels]
+
+    def _head(self, rows_ptr, ld, ln, B, st, cnt):
+        """LayerNorm (ln = the last layer's output_layer_norm, or None when the rows are
+        already normalized) + pre_classifier + ReLU + classifier on the B CLS rows in
+        one launch (gg_cls_head)."""
+        _native.check("gg_cls_head", self.lib.gg_cls_head(
+            C.c_void_p(rows_ptr), ld, _native.ptr(ln["ln2_g"]) if ln else None,
+            _native.ptr(ln["ln2_b"]) if ln else None, C.c_float(self.EPS), _native.ptr(self.w_pre),
+            _native.ptr(self.b_pre), _native.ptr(self.w_cls), _native.ptr(self.b_cls),
+            self.num_labels, _native.ptr(self.logits), self.logits.stride(0), B, self.max_batch,
+            cnt, _native.ptr(self.head_part), _native.ptr(self.head_arr), st))
         return self.logits[:B, : self.num_labels]
 
 

@@ -178,3 +178,46 @@ def test_distilbert_fused_ffn(env):
         g.replay()
     torch.cuda.synchronize()
     assert torch.equal(gout, outs[(True, 128)])
+
+
+@pytest.mark.parametrize("batch", [4, 128])
+def test_distilbert_fused_head(env, batch):
+    """gg_cls_head (CLS LayerNorm + pre_classifier + ReLU + classifier in one launch)
+    agrees with the three-launch head (LayerNorm kernel + two tcgen05 GEMMs) within
+    the bf16 rounding of the pooled activation, is deterministic (fixed-order
+    column-block reduction), honours a dynamic count that ends inside a 16-row
+    block, and replays inside a CUDA graph (arrival counters re-zeroed)."""
+    torch = env[0]
+    from paper_2601_04250_b200.distilbert import DistilBertB200, random_model
+    model = random_model(0)
+    ids = torch.randint(0, model.config.vocab_size, (batch, 128),
+                        generator=torch.Generator().manual_seed(9)).to(torch.int32).cuda()
+    mask = torch.ones((batch, 128), dtype=torch.int32, device="cuda")
+    mask[1, 50:] = 0
+    net = DistilBertB200(model, max_batch=batch)
+    cnts = (batch, 37) if batch > 37 else (batch, 3)
+    outs = {}
+    for fused in (False, True):
+        net.fused_head = fused
+        for cnt in cnts:
+            count = torch.tensor([cnt], dtype=torch.int32, device="cuda")
+            outs[(fused, cnt)] = [net.forward(ids, mask, count=count).clone() for _ in range(2)]
+    torch.cuda.synchronize()
+    for cnt in cnts:
+        a, b = outs[(True, cnt)], outs[(False, cnt)]
+        assert torch.equal(a[0][:cnt], a[1][:cnt])
+        err = (a[0][:cnt] - b[0][:cnt]).abs().max().item()
+        print(f"fused head b={batch} count={cnt}: max |logit diff| vs 3-launch head = {err:.3e}")
+        assert err <= 1e-2, err
+    net.fused_head = True
+    count = torch.tensor([batch], dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        net.forward(ids, mask, count=count, stream=s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            gout = net.forward(ids, mask, count=count, stream=s)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(gout, outs[(True, batch)][0])
