@@ -6,6 +6,7 @@
 #include "gg_common.cuh"
 #include "gg_kernels.h"
 #include "gg_act.cuh"
+#include "gg_tc.cuh"
 
 namespace gg {
 
@@ -406,48 +407,63 @@ __global__ void admit_open_kernel(gg_params p, gg_state* st, gg_fifo* f, int32_t
 // top == label AND its fallback coin >= fallback_degradation, where the coins
 // are the `_fb_rng` stream (drawn on the host, never on the device) consumed in
 // trace order by exactly the skipped rows with top == label (the `and`
-// short-circuits).  One block, rows in chunks of 256: top classes (a thread or
-// a warp per row), then a block scan of the coin flags.
+// short-circuits).  One 8-CTA cluster: the top classes of up to kFbSuper rows
+// at a time are computed by all 64 warps (a thread per row for K <= 32, else a
+// warp per row) and stored into CTA 0's shared memory over DSMEM; after a
+// cluster barrier CTA 0 scans the coin flags in trace order, 256 rows per
+// block scan.  (As one block the K = 1000 ResNet window -- 112 rows x 8 KB --
+// took ~42 us of a 430 us serving step on a single SM's load bandwidth.)
 constexpr int kFbThreads = 256;
+constexpr int kFbCluster = 8;
+constexpr int kFbSuper = 4096;
 
-__global__ void __launch_bounds__(kFbThreads) fallback_kernel(
+__global__ void __cluster_dims__(kFbCluster, 1, 1) __launch_bounds__(kFbThreads) fallback_kernel(
     const double* __restrict__ scores, int k, int64_t stride, const int32_t* __restrict__ labels,
     const uint8_t* __restrict__ decision, const gg_fifo* f, const gg_batch_info* info,
     int64_t row0_arg, int64_t n_arg, const double* __restrict__ coins, int64_t* coin_cursor,
     double degradation, int32_t* answer, uint8_t* correct) {
   griddep_wait();
   griddep_launch();
-  __shared__ int32_t top_s[kFbThreads];
+  __shared__ int32_t top_s[kFbSuper];         // CTA 0's copy is the one written
   __shared__ int32_t warp_tot[kFbThreads / 32];
   __shared__ int64_t base_s;
+  const uint32_t crank = tc::cluster_ctarank();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gthread = (int)crank * kFbThreads + tid;
+  const int gwarp = gthread >> 5;
+  constexpr int kThreadsAll = kFbCluster * kFbThreads, kWarpsAll = kThreadsAll / 32;
+  const uint32_t top0 = tc::mapa_shared(tc::smem_u32(top_s), 0);
   int64_t row0 = row0_arg, n = n_arg;
   if (f && info) {            // the window the admission kernel just decided
     n = info->n_decided;
     row0 = f->cursor - n;
   }
-  if (tid == 0) base_s = *coin_cursor;
-  for (int64_t c0 = 0; c0 < n; c0 += kFbThreads) {
-    const int cn = (int)min((int64_t)kFbThreads, n - c0);
+  if (crank == 0 && tid == 0) base_s = *coin_cursor;
+  for (int64_t s0 = 0; s0 < n; s0 += kFbSuper) {   // uniform across the cluster
+    const int sn = (int)min((int64_t)kFbSuper, n - s0);
     if (k <= 32) {
-      if (tid < cn) {
-        const double* x = scores + (row0 + c0 + tid) * stride;
+      for (int i = gthread; i < sn; i += kThreadsAll) {
+        const double* x = scores + (row0 + s0 + i) * stride;
         double best = x[0];
         int bi = 0;
         for (int j = 1; j < k; ++j) {
           const double v = x[j];
           if (v > best) { best = v; bi = j; }
         }
-        top_s[tid] = bi;
+        tc::st_shared_cluster_s32(top0 + 4u * (uint32_t)i, bi);
       }
     } else {
-      for (int r = warp; r < cn; r += kFbThreads / 32) {
-        const double* x = scores + (row0 + c0 + r) * stride;
+      for (int i = gwarp; i < sn; i += kWarpsAll) {
+        const double* x = scores + (row0 + s0 + i) * stride;
         double best = -INFINITY;
         int bi = 0x7fffffff;
-        for (int j = lane; j < k; j += 32) {
-          const double v = __ldg(x + j);
-          if (v > best) { best = v; bi = j; }    // lanes see ascending j: first max per lane
+        for (int j0 = lane; j0 < k; j0 += 8 * 32) {   // 8 loads in flight per lane
+          double v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = j0 + 32 * e < k ? __ldg(x + j0 + 32 * e) : -INFINITY;
+#pragma unroll
+          for (int e = 0; e < 8; ++e)   // lanes see ascending j: first max per lane
+            if (v[e] > best) { best = v[e]; bi = j0 + 32 * e; }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -455,41 +471,47 @@ __global__ void __launch_bounds__(kFbThreads) fallback_kernel(
           const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
           if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
         }
-        if (lane == 0) top_s[r] = bi;
+        if (lane == 0) tc::st_shared_cluster_s32(top0 + 4u * (uint32_t)i, bi);
       }
     }
-    __syncthreads();
-    int flag = 0, top = -1, lab = -1;
-    uint8_t dec = GG_DECISION_INVALID;
-    const int64_t row = row0 + c0 + tid;
-    if (tid < cn) {
-      dec = decision[row];
-      top = top_s[tid];
-      lab = labels ? labels[row] : -1;
-      flag = (dec == GG_DECISION_SKIP) && (top == lab);
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, flag);
-    if (lane == 0) warp_tot[warp] = __popc(bal);
-    __syncthreads();
-    int pre = __popc(bal & ((1u << lane) - 1u)), tot = 0;
+    tc::cluster_sync_all();   // every top of the super-chunk is in CTA 0
+    if (crank == 0) {
+      for (int c0 = 0; c0 < sn; c0 += kFbThreads) {
+        const int cn = min(kFbThreads, sn - c0);
+        int flag = 0, top = -1, lab = -1;
+        uint8_t dec = GG_DECISION_INVALID;
+        const int64_t row = row0 + s0 + c0 + tid;
+        if (tid < cn) {
+          dec = decision[row];
+          top = top_s[c0 + tid];
+          lab = labels ? labels[row] : -1;
+          flag = (dec == GG_DECISION_SKIP) && (top == lab);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, flag);
+        if (lane == 0) warp_tot[warp] = __popc(bal);
+        __syncthreads();
+        int pre = __popc(bal & ((1u << lane) - 1u)), tot = 0;
 #pragma unroll
-    for (int w = 0; w < kFbThreads / 32; ++w) {
-      if (w < warp) pre += warp_tot[w];
-      tot += warp_tot[w];
-    }
-    if (tid < cn && dec != GG_DECISION_INVALID) {
-      if (answer) answer[row] = top;
-      if (correct) {
-        bool ok = (top == lab);
-        if (dec == GG_DECISION_SKIP) ok = flag && coins[base_s + pre] >= degradation;
-        correct[row] = ok ? 1 : 0;
+        for (int w = 0; w < kFbThreads / 32; ++w) {
+          if (w < warp) pre += warp_tot[w];
+          tot += warp_tot[w];
+        }
+        if (tid < cn && dec != GG_DECISION_INVALID) {
+          if (answer) answer[row] = top;
+          if (correct) {
+            bool ok = (top == lab);
+            if (dec == GG_DECISION_SKIP) ok = flag && coins[base_s + pre] >= degradation;
+            correct[row] = ok ? 1 : 0;
+          }
+        }
+        __syncthreads();
+        if (tid == 0) base_s += tot;
+        __syncthreads();
       }
     }
-    __syncthreads();
-    if (tid == 0) base_s += tot;
-    __syncthreads();
+    tc::cluster_sync_all();   // CTA 0 has read the tops before the next super-chunk
   }
-  if (tid == 0) *coin_cursor = base_s;
+  if (crank == 0 && tid == 0) *coin_cursor = base_s;
 }
 
 }  // namespace gg
@@ -583,7 +605,7 @@ int gg_fallback_answers(const double* probs_dev, int32_t k, int64_t row_stride,
   if (!fifo_dev && (row0 < 0 || n < 0)) return GG_ERR_INVALID_ARGUMENT;
   if (correct_dev && (!coins_dev || !labels_dev)) return GG_ERR_INVALID_ARGUMENT;
   if (!(fallback_degradation >= 0.0 && fallback_degradation <= 1.0)) return GG_ERR_INVALID_ARGUMENT;
-  GG_PDL_LAUNCH((fallback_kernel), 1, kFbThreads, 0, gg_stream(stream), probs_dev, k, row_stride,
+  GG_PDL_LAUNCH((fallback_kernel), kFbCluster, kFbThreads, 0, gg_stream(stream), probs_dev, k, row_stride,
                 labels_dev, decision_dev, fifo_dev, info_dev, row0, n, coins_dev, coin_cursor_dev,
                 fallback_degradation, answer_dev, correct_dev);
   GG_LAUNCH_OK();

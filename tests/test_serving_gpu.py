@@ -198,3 +198,59 @@ def test_published_step_records(graph):
         c0 += len(rec["decision"])
     with pytest.raises(RuntimeError):
         srv.record(srv.steps_run - 3)   # the slot has been reused
+
+
+@pytest.mark.parametrize("k", [2, 1000])
+def test_fallback_answers_large_window(k):
+    """gg_fallback_answers over an explicit row range longer than one cluster
+    super-chunk (4096 rows) and not starting at 0: answers = first-max top class
+    (rows with tied maxima included), correct flags and the coin cursor == the
+    reference accounting (servesim.py:246-256) replayed in numpy; invalid rows
+    are left untouched."""
+    import ctypes as C
+    import torch
+    from paper_2601_04250_b200 import _abi, _native
+    lib = _native.load()
+    rng = np.random.default_rng(k)
+    T, row0, n = 9000, 37, 8500
+    scores = rng.random((T, k))
+    scores /= scores.sum(axis=1, keepdims=True)
+    tie = rng.random(T) < 0.1                           # duplicated maxima: first max wins
+    for r in np.nonzero(tie)[0]:
+        m = int(np.argmax(scores[r]))
+        scores[r, (m + 1 + rng.integers(0, k - 1)) % k] = scores[r, m]
+    top = np.argmax(scores, axis=1)
+    labels = np.where(rng.random(T) < 0.6, top, rng.integers(0, k, T)).astype(np.int32)
+    codes = np.array([_abi.GG_DECISION_SKIP, _abi.GG_DECISION_DIRECT, _abi.GG_DECISION_BATCHED,
+                      _abi.GG_DECISION_INVALID], np.uint8)
+    dec = codes[rng.choice(4, T, p=[0.5, 0.2, 0.2, 0.1])]
+    coins = rng.random(T)
+    deg = 0.3
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    s_d, l_d, dec_d, c_d = d(scores), d(labels), d(dec), d(coins)
+    ans = torch.full((T,), -7, dtype=torch.int32, device="cuda")
+    cor = torch.full((T,), 9, dtype=torch.uint8, device="cuda")
+    cur = torch.tensor([5], dtype=torch.int64, device="cuda")
+    _native.check("gg_fallback_answers", lib.gg_fallback_answers(
+        _native.ptr(s_d), k, k, _native.ptr(l_d), _native.ptr(dec_d), None, None, row0, n,
+        _native.ptr(c_d), _native.ptr(cur), deg, _native.ptr(ans), _native.ptr(cor), None))
+    torch.cuda.synchronize()
+    want_a = np.full(T, -7, np.int32)
+    want_c = np.full(T, 9, np.uint8)
+    cc = 5
+    for r in range(row0, row0 + n):
+        if dec[r] == _abi.GG_DECISION_INVALID:
+            continue
+        want_a[r] = top[r]
+        hit = top[r] == labels[r]
+        if dec[r] == _abi.GG_DECISION_SKIP:
+            ok = False
+            if hit:
+                ok = coins[cc] >= deg
+                cc += 1
+        else:
+            ok = hit
+        want_c[r] = ok
+    assert np.array_equal(ans.cpu().numpy(), want_a)
+    assert np.array_equal(cor.cpu().numpy(), want_c)
+    assert int(cur.item()) == cc
