@@ -131,9 +131,11 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   const int tiles_n = sh.Cout / BN;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kSpanMaxStages; ++i) {
+    for (int i = 0; i < AST; ++i) {   // only the ring slots this launch uses
       mbar_init(&a_full[i], 1);
       mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < BST; ++i) {
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], 1);
     }
@@ -724,9 +726,11 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   const int tiles_n = sh.Cout / BN;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kSpanMaxStages; ++i) {
+    for (int i = 0; i < AST; ++i) {   // only the ring slots this launch uses
       mbar_init(&a_full[i], 1);
       mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < BST; ++i) {
       mbar_init(&b_full[i], 1);
       mbar_init(&b_empty[i], 1);
     }
