@@ -241,21 +241,23 @@ class ResNet18B200:
             _native.ptr(images), B, H, H, 1, _native.ptr(self.x16), st))
         return self.forward_s2d(B, stream=stream)
 
-    def forward_s2d(self, B: int, stream=None, count=None):
-        """Forward from self.x16 (fp16 space-to-depth(2) NHWC, 16 channels).
+    def forward_s2d(self, B: int, stream=None, count=None, x16=None):
+        """Forward from self.x16 (or `x16`: the same layout, e.g. a second input slot)
+        (fp16 space-to-depth(2) NHWC, 16 channels).
         count: optional CUDA int32 [1] = valid images (dynamic batch read on the device)."""
         lib = self.lib
         H = self.image
         st = _native.stream_ptr(stream)
         cnt = _native.ptr(count)
+        x16 = self.x16 if x16 is None else x16
         bufs = [[t.data_ptr() for t in stage] for stage in self.stage_bufs]
         if self.fuse_stem_pool:
             # stem conv + max pool in one kernel: the 112x112x64 stem output never leaves the SM
             _native.check("gg_stem_pool_span", lib.gg_stem_pool_span(
-                C.c_void_p(self.x16.data_ptr()), B, H // 2, H // 2, _native.ptr(self.stem.w), 64,
+                C.c_void_p(x16.data_ptr()), B, H // 2, H // 2, _native.ptr(self.stem.w), 64,
                 _native.ptr(self.stem.b), C.c_void_p(bufs[0][0]), 2, cnt, st))
         else:
-            h, w = self.stem(lib, self.x16.data_ptr(), B, H // 2, H // 2, self.stem_out.data_ptr(),
+            h, w = self.stem(lib, x16.data_ptr(), B, H // 2, H // 2, self.stem_out.data_ptr(),
                              st, count=count)                                     # 112x112x64 dense
             _native.check("gg_maxpool3x3s2", lib.gg_maxpool3x3s2(
                 _native.ptr(self.stem_out), B, h, w, 64, C.c_void_p(bufs[0][0]), 2, cnt, st))

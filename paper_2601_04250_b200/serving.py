@@ -77,13 +77,25 @@ class GatedServer:
                 accounting of every decided request (servesim.py:246-256);
                 labels CUDA int32 [T], coins CUDA fp64 [>= T] (the `_fb_rng`
                 stream, drawn on the host, see fallback_coins)
+    pipeline:   software-pipelined steps (single GPU; latency "model" or "trace"):
+                the control chain of step t+1 (K1, fallback, pop, gather, served
+                outcomes, K2) runs on the serving stream while step t's forward,
+                K3 and publish run on a second stream.  No kernel of the control
+                chain reads the forward's output, so every decision, answer,
+                prediction and the controller state are the sequential loop's;
+                the per-step buffers (batch ids / arrival stamps / count / batch
+                info / model inputs / FIFO snapshot) alternate between two sets.
+                run(n) completes n forwards with the control of the next step
+                already done; flush() (or done() once the trace is served)
+                completes the pending forward.
     """
 
     def __init__(self, controller, net, scores, now, payloads, *, window: int,
                  outcome: OutcomeModel | None = None, fifo_capacity: int = 1 << 20,
                  rank: int = 0, world: int = 1, process_group=None, open_loop: bool = False,
                  batching_window_ms: float | None = None, labels=None, coins=None,
-                 fallback_degradation: float = 0.05, publish: bool = False):
+                 fallback_degradation: float = 0.05, publish: bool = False,
+                 pipeline: bool = False):
         torch = _native.require_cuda()
         self.torch = torch
         self.lib = _native.load()
@@ -119,9 +131,10 @@ class GatedServer:
         self.fifo = torch.frombuffer(bytearray(bytes(fifo)), dtype=torch.uint8).to(self.dev)
         self.ring = torch.empty(fifo_capacity, dtype=torch.int32, **z)
         self.ring_ns = torch.empty(fifo_capacity, dtype=torch.int64, **z)
-        self.batch_ids = torch.full((self.B,), -1, dtype=torch.int32, **z)
-        self.batch_ns = torch.empty(self.B, dtype=torch.int64, **z)
-        self.count = torch.zeros(1, dtype=torch.int32, **z)
+        self.pipeline = bool(pipeline)
+        if self.pipeline and (world > 1 or self.outcome.measured_latency == _abi.GG_LATENCY_MEASURED):
+            raise ValueError("pipeline=True needs world == 1 and a latency model that does not "
+                             "time the forward (latency='model' or 'trace')")
         self.batch_pred = torch.full((self.B,), -1, dtype=torch.int32, **z)
         self.batch_conf = torch.zeros(self.B, dtype=torch.float64, **z)
         self.slot_len = 3 * self.B + 8   # GG_SLOT_LEN(B)
@@ -134,15 +147,29 @@ class GatedServer:
         self.correct = torch.zeros(self.T, dtype=torch.uint8, **z)
         self.latency = torch.zeros(self.T, dtype=torch.float64, **z)        # latency_ms
         self.coin_cursor = torch.zeros(1, dtype=torch.int64, **z)
-        self.info = torch.empty(_abi.BATCH_INFO_BYTES, dtype=torch.uint8, **z)
         self.ws = torch.zeros(self.lib.gg_admit_workspace_bytes(self.W), dtype=torch.uint8, **z)
         self.err = torch.empty(1, dtype=torch.int64, **z)
         if self.kind == "resnet18":
             self.mean = torch.tensor(IMAGENET_MEAN, dtype=torch.float32)
             self.std = torch.tensor(IMAGENET_STD, dtype=torch.float32)
-        else:
-            self.tok_ids = torch.empty((self.B, net.seq_len), dtype=torch.int32, **z)
-            self.tok_mask = torch.empty((self.B, net.seq_len), dtype=torch.int32, **z)
+        # per-step buffers: one set, or two alternating sets when pipelined
+        self._sets = []
+        for i in range(2 if self.pipeline else 1):
+            d = dict(batch_ids=torch.full((self.B,), -1, dtype=torch.int32, **z),
+                     batch_ns=torch.empty(self.B, dtype=torch.int64, **z),
+                     count=torch.zeros(1, dtype=torch.int32, **z),
+                     info=torch.empty(_abi.BATCH_INFO_BYTES, dtype=torch.uint8, **z),
+                     fsnap=torch.empty_like(self.fifo) if self.pipeline else None)
+            if self.kind == "resnet18":
+                d["x16"] = net.x16 if i == 0 else torch.zeros_like(net.x16)   # zero borders
+            else:
+                d["tok_ids"] = torch.empty((self.B, net.seq_len), dtype=torch.int32, **z)
+                d["tok_mask"] = torch.empty((self.B, net.seq_len), dtype=torch.int32, **z)
+            self._sets.append(d)
+        self._bind(0)
+        self._ahead = False     # pipelined: the control of a step ran, its forward pending
+        self._pset = 0          # pipelined: the set of that step
+        self.control_steps = 0
         # publish: every step ends by writing its record (served predictions and
         # confidences, the window's decisions) into pinned host memory
         # (gg_publish_step), two slots alternating -- no device -> host copies
@@ -153,10 +180,29 @@ class GatedServer:
             self.rec_seq = torch.zeros(1, dtype=torch.int64, **z)
         self.graph = None
         self.stream = torch.cuda.Stream(device=self.dev)
+        # the forward is the critical path: its stream has the higher priority, so the
+        # control chain fills SMs the forward leaves idle instead of delaying it
+        import os
+        prio = os.environ.get("GG_PIPE_PRIO", "f")
+        self.fstream = torch.cuda.Stream(device=self.dev, priority=-1 if prio == "f" else 0) \
+            if self.pipeline else None
+        if self.pipeline and prio == "c":
+            self.stream = torch.cuda.Stream(device=self.dev, priority=-1)
         self.steps_run = 0
 
+    def _bind(self, p: int) -> None:
+        """Point the per-step buffer attributes at set p."""
+        d = self._sets[p]
+        self.batch_ids, self.batch_ns, self.count = d["batch_ids"], d["batch_ns"], d["count"]
+        self.info, self._fsnap = d["info"], d["fsnap"]
+        if self.kind == "resnet18":
+            self._x16 = d["x16"]
+        else:
+            self.tok_ids, self.tok_mask = d["tok_ids"], d["tok_mask"]
+
     # ------------------------------------------------------------------ one step
-    def _forward(self, st):
+    def _gather(self, st):
+        """Payloads of the served batch -> this set's model inputs."""
         lib, B = self.lib, self.B
         if self.kind == "resnet18":
             pool = self.payloads
@@ -165,17 +211,20 @@ class GatedServer:
                 _native.ptr(pool), int(pool.shape[0]), _native.ptr(self.batch_ids),
                 _native.ptr(self.count), B, H, int(pool.shape[2]),
                 self.mean.numpy().ctypes.data_as(C.c_void_p),
-                self.std.numpy().ctypes.data_as(C.c_void_p), 1, _native.ptr(self.net.x16), st))
-            logits = self.net.forward_s2d(B, stream=self._cur_stream, count=self.count)
+                self.std.numpy().ctypes.data_as(C.c_void_p), 1, _native.ptr(self._x16), st))
         else:
             ids, mask = self.payloads
             _native.check("gg_token_gather", lib.gg_token_gather(
                 _native.ptr(ids), _native.ptr(mask), int(ids.shape[0]), _native.ptr(self.batch_ids),
                 _native.ptr(self.count), B, self.net.seq_len, _native.ptr(self.tok_ids),
                 _native.ptr(self.tok_mask), st))
-            logits = self.net.forward(self.tok_ids, self.tok_mask, batch=B,
-                                      stream=self._cur_stream, count=self.count)
-        return logits
+
+    def _forward(self, st):
+        B = self.B
+        if self.kind == "resnet18":
+            return self.net.forward_s2d(B, stream=self._cur_stream, count=self.count, x16=self._x16)
+        return self.net.forward(self.tok_ids, self.tok_mask, batch=B, stream=self._cur_stream,
+                                count=self.count)
 
     def step(self):
         """Enqueue one serving step on the current stream (graph-capturable)."""
@@ -187,10 +236,17 @@ class GatedServer:
 
     def step_local(self):
         """Admission, FIFO, forward, epilogue and this rank's exchange slot."""
-        torch, lib = self.torch, self.lib
+        torch = self.torch
         self._cur_stream = torch.cuda.current_stream(self.dev)
         st = _native.stream_ptr(self._cur_stream)
-        ctl = self.ctl
+        self._control_front(st)
+        self._forward_tail(st)
+        self._control_back(st)
+
+    def _control_front(self, st):
+        """K1 (decide the next window against the FIFO snapshot), fallback answers,
+        the Path-B pop and the gather of the served batch's payloads."""
+        lib, ctl = self.lib, self.ctl
         if self.open_loop:
             _native.check("gg_admit_open_stream", lib.gg_admit_open_stream(
                 C.byref(ctl.params), _native.ptr(ctl.state), _native.ptr(self.fifo),
@@ -220,12 +276,29 @@ class GatedServer:
                 _native.ptr(self.fifo), _native.ptr(self.ring), _native.ptr(self.ring_ns),
                 _native.ptr(self.batch_ids), _native.ptr(self.batch_ns), _native.ptr(self.count),
                 self.B, st))
+        if self._fsnap is not None:   # the window this step decided, for its publish
+            self._fsnap.copy_(self.fifo, non_blocking=True)
+        self._gather(st)
+
+    def _forward_tail(self, st):
+        """Forward on the gathered batch, K3 epilogue, publish of the step record."""
+        lib = self.lib
         logits = self._forward(st)
         _native.check("gg_epilogue_served", lib.gg_epilogue_served(
             C.c_void_p(logits.data_ptr()), _native.ptr(self.count), self.B, int(logits.shape[1]),
             int(logits.stride(0)), _native.ptr(self.batch_ids), _native.ptr(self.predicted),
             _native.ptr(self.confidence), None, _native.ptr(self.batch_pred),
             _native.ptr(self.batch_conf), st))
+        if self.publish:
+            fifo = self._fsnap if self._fsnap is not None else self.fifo
+            _native.check("gg_publish_step", lib.gg_publish_step(
+                _native.ptr(self.count), _native.ptr(self.batch_pred), _native.ptr(self.batch_conf),
+                _native.ptr(self.decision), _native.ptr(self.info), _native.ptr(fifo), self.B,
+                self.W, C.c_void_p(self.host_records.data_ptr()), _native.ptr(self.rec_seq), st))
+
+    def _control_back(self, st):
+        """Served outcomes of the popped batch into this rank's exchange slot."""
+        lib = self.lib
         if self.world > 1:
             self.slots.zero_()
         my_slot = self.slots[self.rank * self.slot_len:]
@@ -233,11 +306,48 @@ class GatedServer:
             _native.ptr(self.fifo), _native.ptr(self.count), _native.ptr(self.batch_ns),
             _native.ptr(self.batch_ids), _native.ptr(self.now), C.byref(self.outcome),
             _native.ptr(self.info), _native.ptr(my_slot), self.B, _native.ptr(self.latency), st))
-        if self.publish:
-            _native.check("gg_publish_step", lib.gg_publish_step(
-                _native.ptr(self.count), _native.ptr(self.batch_pred), _native.ptr(self.batch_conf),
-                _native.ptr(self.decision), _native.ptr(self.info), _native.ptr(self.fifo), self.B,
-                self.W, C.c_void_p(self.host_records.data_ptr()), _native.ptr(self.rec_seq), st))
+
+    # ------------------------------------------------------------------ pipelined steps
+    def _pipe_control(self, p):
+        """Control chain of one step into set p, on the current stream."""
+        torch = self.torch
+        self._bind(p)
+        self._cur_stream = torch.cuda.current_stream(self.dev)
+        st = _native.stream_ptr(self._cur_stream)
+        self._control_front(st)
+        self._control_back(st)
+        self.step_feedback()
+
+    def _pipe_body(self, p):
+        """Forward of the step whose control filled set p (second stream) || the
+        control of the next step into set 1 - p (current stream); joined."""
+        torch = self.torch
+        main = torch.cuda.current_stream(self.dev)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        self.fstream.wait_event(fork)
+        self._bind(p)
+        with torch.cuda.stream(self.fstream):
+            self._cur_stream = self.fstream
+            self._forward_tail(_native.stream_ptr(self.fstream))
+        self._pipe_control(1 - p)
+        join = torch.cuda.Event()
+        join.record(self.fstream)
+        main.wait_event(join)
+
+    def flush(self) -> None:
+        """Pipelined: complete the forward of the step whose control already ran."""
+        if not (self.pipeline and self._ahead):
+            return
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            self._bind(self._pset)
+            self._cur_stream = self.stream
+            self._forward_tail(_native.stream_ptr(self.stream))
+        self._ahead = False
+        self._pset ^= 1
+        self.steps_run += 1
+        self.stream.synchronize()
 
     def step_feedback(self):
         """K2 over every rank's slot (after the exchange)."""
@@ -256,6 +366,15 @@ class GatedServer:
         exchange buffer runs between them on the same stream (no collective
         inside a captured graph, so any NCCL/torch combination works)."""
         torch = self.torch
+        if self.pipeline:   # one graph per parity of the forward's buffer set
+            gs = []
+            for p in (0, 1):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._pipe_body(p)
+                gs.append(g)
+            self.graph = tuple(gs)
+            return
         if self.world == 1:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.stream):
@@ -271,6 +390,22 @@ class GatedServer:
 
     def run(self, steps: int) -> None:
         torch = self.torch
+        if self.pipeline:
+            with torch.cuda.stream(self.stream):
+                for _ in range(steps):
+                    if not self._ahead:   # prologue: the first step's control chain
+                        self._pipe_control(self._pset)
+                        self._ahead = True
+                        self.control_steps += 1
+                    if self.graph is None:
+                        self._pipe_body(self._pset)
+                    else:
+                        self.graph[self._pset].replay()
+                    self.control_steps += 1
+                    self._pset ^= 1
+            self.steps_run += steps
+            return
+        self.control_steps += steps
         with torch.cuda.stream(self.stream):   # replay() launches on the current stream
             for _ in range(steps):
                 if self.graph is None:
@@ -304,11 +439,16 @@ class GatedServer:
                 "decision": raw[co + 8 * B:co + 8 * B + int(hdr.n_decided)].copy()}
 
     def fifo_state(self) -> _abi.gg_fifo:
+        self.stream.synchronize()   # the FIFO is written by work queued on the serving stream
         return _abi.gg_fifo.from_buffer_copy(bytes(self.fifo.cpu().numpy().tobytes()))
 
     def done(self) -> bool:
+        """Trace decided and FIFO empty (pipelined: the pending forward is then flushed)."""
         f = self.fifo_state()
-        return f.cursor >= f.trace_len and f.tail == f.head
+        fin = f.cursor >= f.trace_len and f.tail == f.head
+        if fin:
+            self.flush()
+        return fin
 
     def drain(self, max_steps: int = 1 << 30) -> int:
         """Run steps until the trace is decided and the FIFO is empty."""

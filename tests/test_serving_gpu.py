@@ -254,3 +254,66 @@ def test_fallback_answers_large_window(k):
     assert np.array_equal(ans.cpu().numpy(), want_a)
     assert np.array_equal(cor.cpu().numpy(), want_c)
     assert int(cur.item()) == cc
+
+
+@pytest.mark.parametrize("kind,k,B,window,win_ms,latency", [
+    ("distilbert", 2, 16, 24, None, "model"),
+    ("distilbert", 2, 16, 24, 4.0, "trace"),
+    ("resnet18", 1000, 8, 12, 4.0, "trace"),
+])
+def test_pipelined_steps_match_sequential(kind, k, B, window, win_ms, latency):
+    """GatedServer(pipeline=True) -- the control chain of step t+1 on the serving
+    stream while step t's forward / K3 / publish run on a second stream, per-step
+    buffers in two alternating sets, two parity graphs -- ends in exactly the
+    sequential loop's state: decisions, fallback answers and accounting,
+    predictions and confidences, latencies, FIFO counters, controller state and
+    the last published record."""
+    import torch
+    import paper_2601_04250_b200 as gg
+    from paper_2601_04250_b200 import serving
+    n = 400 if kind == "distilbert" else 160
+    scores, now = make_trace(n, k, seed=k + 11)
+    labels = _labels(n, k, seed=4)
+    coins = serving.fallback_coins(77, n)
+    if kind == "resnet18":
+        from paper_2601_04250_b200.resnet18 import ResNet18B200, random_model
+        net_f = lambda: ResNet18B200(random_model(0), max_batch=B)   # noqa: E731
+        payloads = serving.synthetic_images(32)
+    else:
+        from paper_2601_04250_b200.distilbert import DistilBertB200, random_model
+        net_f = lambda: DistilBertB200(random_model(0), max_batch=B)   # noqa: E731
+        payloads = serving.synthetic_tokens(32)
+    out = {}
+    for pipe in (False, True):
+        ctl = gg.ControllerConfig(alpha=1.0, beta=-0.2, gamma=-0.4, tau0=0.8, tau_inf=0.35, k=1.5,
+                                  routing=gg.RoutePolicy.THRESHOLD_ON_QUEUE,
+                                  queue_threshold=6).build(gg.EnergyLedger())
+        srv = serving.GatedServer(
+            ctl, net_f(), torch.from_numpy(scores).cuda(), torch.from_numpy(now).cuda(), payloads,
+            window=window, outcome=serving.OutcomeModel(**MODEL, latency=latency),
+            fifo_capacity=4096, batching_window_ms=win_ms, labels=torch.from_numpy(labels).cuda(),
+            coins=torch.from_numpy(coins).cuda(), fallback_degradation=0.2, publish=True,
+            pipeline=pipe)
+        srv.run(1)
+        srv.capture()
+        steps = 1
+        while not srv.done():   # fifo_state() syncs the serving stream: exact step counts
+            srv.run(1)
+            steps += 1
+            assert steps < 10_000
+        torch.cuda.synchronize()
+        out[pipe] = dict(
+            arrays=[t.cpu().numpy() for t in (srv.decision, srv.answer, srv.correct, srv.predicted,
+                                              srv.confidence, srv.latency, srv.coin_cursor)],
+            results=srv.results(), state=G.state_dict_of_abi(srv.ctl.state_struct()),
+            steps=srv.steps_run, control=srv.control_steps,
+            last=srv.record(srv.steps_run - 1))
+    a, b = out[False], out[True]
+    for x, y in zip(a["arrays"], b["arrays"]):
+        assert np.array_equal(x, y, equal_nan=x.dtype.kind == "f")
+    assert a["results"] == b["results"] and a["state"] == b["state"]
+    assert a["steps"] == b["steps"] == a["control"] == b["control"]
+    for key in ("count", "window_start"):
+        assert a["last"][key] == b["last"][key]
+    for key in ("pred", "conf", "decision"):
+        assert np.array_equal(a["last"][key], b["last"][key])
