@@ -200,7 +200,7 @@ def make_server(wl, kind, net, scores, now, labels, payloads, dev, *, rank=0, wo
         outcome=serving.OutcomeModel(**wl["outcome"], latency="trace"), rank=rank, world=world,
         process_group=pg, open_loop=open_loop, batching_window_ms=wl["batching_window_ms"],
         labels=labels, coins=coins, fallback_degradation=wl["fallback_degradation"], publish=publish,
-        pipeline=world == 1 and os.environ.get("GG_PIPELINE", "1") != "0")
+        pipeline=os.environ.get("GG_PIPELINE", "1") != "0")
 
 
 def payload_pool(kind, n, seed, dev):
@@ -235,7 +235,7 @@ def run_ours(args, kind, rank, world, local_rank, pg, with_clocks=True):
     torch.cuda.synchronize()
     _native.LAUNCHES = 0
     srv.capture()
-    launches_per_step = _native.LAUNCHES // (2 if srv.pipeline else 1)   # pipelined: 2 parity graphs
+    launches_per_step = getattr(srv, "launches_per_step", _native.LAUNCHES)   # pipelined: per parity
     srv.run(args.warmup)
     torch.cuda.synchronize()
 

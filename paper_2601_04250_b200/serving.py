@@ -77,7 +77,7 @@ class GatedServer:
                 accounting of every decided request (servesim.py:246-256);
                 labels CUDA int32 [T], coins CUDA fp64 [>= T] (the `_fb_rng`
                 stream, drawn on the host, see fallback_coins)
-    pipeline:   software-pipelined steps (single GPU; latency "model" or "trace"):
+    pipeline:   software-pipelined steps (latency "model" or "trace"):
                 the control chain of step t+1 (K1, fallback, pop, gather, served
                 outcomes, K2) runs on the serving stream while step t's forward,
                 K3 and publish run on a second stream.  No kernel of the control
@@ -132,9 +132,9 @@ class GatedServer:
         self.ring = torch.empty(fifo_capacity, dtype=torch.int32, **z)
         self.ring_ns = torch.empty(fifo_capacity, dtype=torch.int64, **z)
         self.pipeline = bool(pipeline)
-        if self.pipeline and (world > 1 or self.outcome.measured_latency == _abi.GG_LATENCY_MEASURED):
-            raise ValueError("pipeline=True needs world == 1 and a latency model that does not "
-                             "time the forward (latency='model' or 'trace')")
+        if self.pipeline and self.outcome.measured_latency == _abi.GG_LATENCY_MEASURED:
+            raise ValueError("pipeline=True needs a latency model that does not time the "
+                             "forward (latency='model' or 'trace')")
         self.batch_pred = torch.full((self.B,), -1, dtype=torch.int32, **z)
         self.batch_conf = torch.zeros(self.B, dtype=torch.float64, **z)
         self.slot_len = 3 * self.B + 8   # GG_SLOT_LEN(B)
@@ -188,6 +188,8 @@ class GatedServer:
             if self.pipeline else None
         if self.pipeline and prio == "c":
             self.stream = torch.cuda.Stream(device=self.dev, priority=-1)
+        if self.pipeline:
+            self._fork, self._join = torch.cuda.Event(), torch.cuda.Event()
         self.steps_run = 0
 
     def _bind(self, p: int) -> None:
@@ -308,32 +310,49 @@ class GatedServer:
             _native.ptr(self.info), _native.ptr(my_slot), self.B, _native.ptr(self.latency), st))
 
     # ------------------------------------------------------------------ pipelined steps
-    def _pipe_control(self, p):
-        """Control chain of one step into set p, on the current stream."""
+    def _pipe_control(self, p, feedback: bool = True):
+        """Control chain of one step into set p, on the current stream (with the
+        exchange and K2 unless feedback=False)."""
         torch = self.torch
         self._bind(p)
         self._cur_stream = torch.cuda.current_stream(self.dev)
         st = _native.stream_ptr(self._cur_stream)
         self._control_front(st)
         self._control_back(st)
-        self.step_feedback()
+        if feedback:
+            if self.world > 1:
+                torch.distributed.all_reduce(self.slots, group=self.pg)
+            self.step_feedback()
 
-    def _pipe_body(self, p):
-        """Forward of the step whose control filled set p (second stream) || the
-        control of the next step into set 1 - p (current stream); joined."""
-        torch = self.torch
-        main = torch.cuda.current_stream(self.dev)
-        fork = torch.cuda.Event()
-        fork.record(main)
-        self.fstream.wait_event(fork)
+    def _pipe_forward(self, p):
+        """Forward tail of the step in set p, on the forward stream."""
         self._bind(p)
-        with torch.cuda.stream(self.fstream):
+        with self.torch.cuda.stream(self.fstream):
             self._cur_stream = self.fstream
             self._forward_tail(_native.stream_ptr(self.fstream))
-        self._pipe_control(1 - p)
-        join = torch.cuda.Event()
-        join.record(self.fstream)
-        main.wait_event(join)
+
+    def _pipe_body(self, p):
+        """Forward of the step whose control filled set p (forward stream) || the
+        control of the next step into set 1 - p (current stream); joined.  Captured:
+        graph(forward p) on the forward stream, graph(control 1 - p) [-> all_reduce
+        -> graph(K2) for world > 1] on the serving stream."""
+        torch = self.torch
+        main = torch.cuda.current_stream(self.dev)
+        self._fork.record(main)
+        self.fstream.wait_event(self._fork)
+        if self.graph is None:
+            self._pipe_forward(p)
+            self._pipe_control(1 - p)
+        else:
+            _, gf, gc, gk = self.graph
+            with torch.cuda.stream(self.fstream):
+                gf[p].replay()
+            gc[1 - p].replay()
+            if gk is not None:
+                torch.distributed.all_reduce(self.slots, group=self.pg)
+                gk.replay()
+        self._join.record(self.fstream)
+        main.wait_event(self._join)
 
     def flush(self) -> None:
         """Pipelined: complete the forward of the step whose control already ran."""
@@ -366,14 +385,29 @@ class GatedServer:
         exchange buffer runs between them on the same stream (no collective
         inside a captured graph, so any NCCL/torch combination works)."""
         torch = self.torch
-        if self.pipeline:   # one graph per parity of the forward's buffer set
-            gs = []
+        if self.pipeline:
+            # per buffer set: the forward tail (forward stream) and the control chain
+            # (serving stream; with K2 on one GPU, else K2 is its own graph after the
+            # exchange); _pipe_body forks / joins the two streams around the replays
+            gf, gc = [], []
+            l0 = _native.LAUNCHES
             for p in (0, 1):
                 g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.fstream):
+                    self._pipe_forward(p)
+                gf.append(g)
+                g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=self.stream):
-                    self._pipe_body(p)
-                gs.append(g)
-            self.graph = tuple(gs)
+                    self._pipe_control(p, feedback=self.world == 1)
+                gc.append(g)
+            n0 = _native.LAUNCHES
+            gk = None
+            if self.world > 1:
+                gk = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gk, stream=self.stream):
+                    self.step_feedback()
+            self.graph = ("pipe", tuple(gf), tuple(gc), gk)
+            self.launches_per_step = (n0 - l0) // 2 + (_native.LAUNCHES - n0)
             return
         if self.world == 1:
             g = torch.cuda.CUDAGraph()
@@ -397,10 +431,7 @@ class GatedServer:
                         self._pipe_control(self._pset)
                         self._ahead = True
                         self.control_steps += 1
-                    if self.graph is None:
-                        self._pipe_body(self._pset)
-                    else:
-                        self.graph[self._pset].replay()
+                    self._pipe_body(self._pset)
                     self.control_steps += 1
                     self._pset ^= 1
             self.steps_run += steps

@@ -11,6 +11,9 @@ buffer between them, exactly as bench.py --gpus N runs it.
   the device kernels is exercised on every GPU test run.
 * nccl backend, one GPU per rank: skipped unless >= 2 GPUs are visible.
 
+pipe=True: the software-pipelined serving loop (GatedServer(pipeline=True):
+graph(forward) on a second stream || graph(control) -> all_reduce -> graph(K2)).
+
 Checks: the two replicas' controller states are byte-identical after every
 step, and equal the host replay of the data-parallel semantics
 (oracle/serving_oracle.py) together with every rank's decisions and served set.
@@ -40,7 +43,7 @@ def _shard(rank):
     return tr.scores[:N].copy(), tr.arrival_t[:N].copy()
 
 
-def _worker(rank, world, port, backend, q):
+def _worker(rank, world, port, backend, q, pipe=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world))
     import torch
@@ -63,7 +66,8 @@ def _worker(rank, world, port, backend, q):
         srv = serving.GatedServer(ctl, net, torch.from_numpy(sc).to(dev), torch.from_numpy(nw).to(dev),
                                   serving.synthetic_tokens(32, device=dev), window=W,
                                   outcome=serving.OutcomeModel(**MODEL), fifo_capacity=1024,
-                                  rank=rank, world=world, process_group=dist.group.WORLD)
+                                  rank=rank, world=world, process_group=dist.group.WORLD,
+                                  pipeline=pipe)
         srv.run(1)                 # eager step (exchange through the process group)
         srv.capture()              # graph(local) -> all_reduce -> graph(feedback)
         steps, diverged = 1, -1
@@ -81,7 +85,7 @@ def _worker(rank, world, port, backend, q):
             dist.all_gather(other, st)
             if diverged < 0 and not all(torch.equal(other[0], o) for o in other):
                 diverged = steps
-        q.put((rank, steps, diverged, srv.decision.cpu().numpy(),
+        q.put((rank, srv.control_steps, diverged, srv.decision.cpu().numpy(),
                np.nonzero(srv.predicted.cpu().numpy() >= 0)[0], bytes(srv.ctl.state_struct()), None))
         dist.destroy_process_group()
     except Exception as exc:  # pragma: no cover - reported by the parent
@@ -96,12 +100,12 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _run(backend):
+def _run(backend, pipe=False):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, backend, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, backend, q, pipe)) for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in procs]
@@ -113,15 +117,16 @@ def _run(backend):
     return res
 
 
-@pytest.mark.parametrize("backend", ["gloo", "nccl"])
-def test_two_process_exchange(backend):
+@pytest.mark.parametrize("backend,pipe", [("gloo", False), ("gloo", True), ("nccl", False),
+                                          ("nccl", True)])
+def test_two_process_exchange(backend, pipe):
     import torch
     from oracle import serving_oracle
     from paper_2601_04250_b200 import _abi
     from tests import _golden as G
     if backend == "nccl" and torch.cuda.device_count() < 2:
         pytest.skip("NCCL exchange needs >= 2 GPUs (one rank per GPU)")
-    res = _run(backend)
+    res = _run(backend, pipe)
     steps = res[0][1]
     assert res[1][1] == steps
     assert res[0][2] < 0 and res[1][2] < 0, "replicas diverged"
