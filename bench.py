@@ -887,8 +887,14 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        import datetime
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # a rank that dies or hangs fails the job within the timeout instead of
+        # blocking the others forever (NCCL async error handling aborts the communicator)
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank),
+                                timeout=datetime.timedelta(
+                                    seconds=int(os.environ.get("GG_NCCL_TIMEOUT_S", "300"))))
         pg = dist.group.WORLD
     r = run_ours(args, kind, rank, world, local_rank, pg)
     other = None

@@ -378,6 +378,10 @@ class GatedServer:
 
     # ------------------------------------------------------------------ graphs
     def capture(self) -> None:
+        with self.torch.cuda.nvtx.range("gg.serve.capture"):
+            self._capture()
+
+    def _capture(self) -> None:
         """Capture one step as CUDA graph(s) (after one eager warm-up step).
 
         Single GPU: the whole step is one graph.  Multi-GPU: the local part and
@@ -423,6 +427,10 @@ class GatedServer:
             self.graph = (ga, gb)
 
     def run(self, steps: int) -> None:
+        with self.torch.cuda.nvtx.range(f"gg.serve.run[{steps}]"):   # host-side phase marker
+            self._run(steps)
+
+    def _run(self, steps: int) -> None:
         torch = self.torch
         if self.pipeline:
             with torch.cuda.stream(self.stream):
