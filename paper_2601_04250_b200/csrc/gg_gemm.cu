@@ -536,8 +536,9 @@ struct PairCfg {
   static constexpr int kThreads = 96 + 32 * EW;   // + the tile-scheduler warp
   static constexpr int A_BYTES = 128 * kBK * 2, B_BYTES = 128 * kBK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;                  // 512 B of barriers
-  static constexpr int BIAS_OFF = BAR_OFF + 512;                         // [kPairMaxN] fp32
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;                  // barriers, tile ring, TMEM slot
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4 + NBUF * EW + 12 + 8) + 4 * 4 + 4;
+  static constexpr int BIAS_OFF = BAR_OFF + ((BAR_BYTES + 127) & ~127);  // [kPairMaxN] fp32
   static constexpr int STG_OFF = (BIAS_OFF + kPairMaxN * 4 + 1023) & ~1023;
   static constexpr int AUX_OFF = STG_OFF + EW * NBUF * 2048;           // [kPairAuxFloats] fp32
   static constexpr int SMEM = AUX_OFF + kPairAuxFloats * 4 + 1024;       // + alignment slack
