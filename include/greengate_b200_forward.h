@@ -177,6 +177,12 @@ int gg_cls_head(const void* hidden, int64_t ld_rows, const float* ln_gamma, cons
                 void* stream);
 int64_t gg_cls_head_scratch_bytes(int32_t max_rows);
 
+/* Persistent kernels (GEMMs, attention, span convolutions) launched or captured
+ * after this call size their grids to (SM count - n) CTAs, n even: the pipelined
+ * serving loop keeps a TPC free for the control chain running beside the
+ * forward.  Returns the previous value, or -1 for an invalid n. */
+int gg_set_sm_reserve(int32_t n);
+
 /* DistilBERT embeddings: y[t] = LayerNorm(word[ids[t]] + pos[t % seq_len]) (bf16 tables). */
 int gg_embed_layernorm(const int32_t* ids, const void* word, const void* pos, void* y,
                        const float* gamma, const float* beta, int64_t tokens, int32_t seq_len,

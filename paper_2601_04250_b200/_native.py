@@ -55,6 +55,7 @@ SIGNATURES: dict[str, tuple] = {
     "gg_cls_head": (C.c_int, [_P, _I64, _P, _P, C.c_float, _P, _P, _P, _P, _I32, _P, _I64, _I32,
                               _I32, _P, _P, _P, _P]),
     "gg_cls_head_scratch_bytes": (_I64, [_I32]),
+    "gg_set_sm_reserve": (C.c_int, [_I32]),
     "gg_embed_layernorm": (C.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, C.c_float, _P,
                                      _P]),
     "gg_token_gather": (C.c_int, [_P, _P, _I64, _P, _P, _I32, _I32, _P, _P, _P]),

@@ -2039,8 +2039,10 @@ static int launch_outcome(const gg_params& p, gg_state* st, const double* lat, c
   // p95 pre-pass over several CTAs once there are enough outcomes to spread
   static const bool no_pre = getenv("GG_OUTCOME_NO_PRE") != nullptr;
   const int64_t n_max = slots ? (int64_t)G * B : n;
-  // (one serving batch, G = 1: the extra launch costs more than the single SM saves)
-  double* pre = (par && !no_pre && n_max >= 4 * kP95PerCta) ? p95_scratch(st, n_max, s) : nullptr;
+  // (>= 64 outcomes: one serving batch's p95s in parallel; the chain kernel's
+  // sequential p95 made K2 ~20 us at B = 128, on the pipelined step's critical tail)
+  static const int pre_min = getenv("GG_OUTCOME_PRE_MIN") ? atoi(getenv("GG_OUTCOME_PRE_MIN")) : kP95PerCta;
+  double* pre = (par && !no_pre && n_max >= pre_min) ? p95_scratch(st, n_max, s) : nullptr;
   const unsigned pre_grid = (unsigned)((n_max + kP95PerCta - 1) / kP95PerCta);
 #define GG_OUTCOME(SLOTS)                                                                        \
   do {                                                                                           \

@@ -465,7 +465,8 @@ static int make_map_box32(CUtensorMap* map, const void* ptr, int64_t rows, int64
 }
 
 static int g_num_sms = 0;
-int num_sms() {
+static int g_sm_reserve = 0;   // gg_set_sm_reserve: SMs persistent grids leave free
+static int device_sms() {
   if (!g_num_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -473,6 +474,7 @@ int num_sms() {
   }
   return g_num_sms;
 }
+int num_sms() { return device_sms() - g_sm_reserve; }
 
 template <int BM, int BN, int STAGES>
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, int M, int N, int K,
@@ -1844,4 +1846,15 @@ extern "C" int gg_gemm_bf16(const void* A, int64_t lda, const void* B, int64_t l
                             void* stream) {
   gg_gemm_epilogue e{bias, residual, ldr, act, OUT_BF16, 0, 0, tile_n, 0, nullptr};
   return gg_gemm(A, lda, B, ldb, D, ldd, M, N, K, &e, stream);
+}
+
+// Persistent grids (GEMMs, attention, span convolutions) size themselves to the
+// SM count minus `n` (even: CTA pairs) for launches issued -- or captured into a
+// graph -- after this call: the pipelined serving loop keeps a TPC free for the
+// control stream that runs beside the forward.  Returns the previous value.
+extern "C" int gg_set_sm_reserve(int32_t n) {
+  const int prev = g_sm_reserve;
+  if (n < 0 || (n & 1) || n >= device_sms()) return -1;
+  g_sm_reserve = n;
+  return prev;
 }

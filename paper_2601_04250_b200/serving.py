@@ -180,10 +180,16 @@ class GatedServer:
             self.rec_seq = torch.zeros(1, dtype=torch.int64, **z)
         self.graph = None
         self.stream = torch.cuda.Stream(device=self.dev)
-        # the forward is the critical path: its stream has the higher priority, so the
-        # control chain fills SMs the forward leaves idle instead of delaying it
+        # Pipelined: the forward's persistent grids leave one TPC (2 SMs) free for the
+        # control chain (gg_set_sm_reserve, applied to the captured graphs: it costs
+        # the forward nothing at these tile counts), and one stream has the higher
+        # priority -- the control stream for DistilBERT (its kernels are small and fit
+        # the free TPC), the forward's for ResNet-18 (the image gather is a
+        # 1792-block kernel that would take SMs from the forward).  Measured:
+        # DESIGN.md section 7, finding I.
         import os
-        prio = os.environ.get("GG_PIPE_PRIO", "f")
+        self.sm_reserve = int(os.environ.get("GG_PIPE_SM_RESERVE", "2")) if self.pipeline else 0
+        prio = os.environ.get("GG_PIPE_PRIO", "c" if self.kind == "distilbert" else "f")
         self.fstream = torch.cuda.Stream(device=self.dev, priority=-1 if prio == "f" else 0) \
             if self.pipeline else None
         if self.pipeline and prio == "c":
@@ -395,6 +401,9 @@ class GatedServer:
             # exchange); _pipe_body forks / joins the two streams around the replays
             gf, gc = [], []
             l0 = _native.LAUNCHES
+            prev = self.lib.gg_set_sm_reserve(self.sm_reserve)
+            if prev < 0:
+                raise ValueError(f"invalid SM reservation {self.sm_reserve}")
             for p in (0, 1):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=self.fstream):
@@ -404,6 +413,7 @@ class GatedServer:
                 with torch.cuda.graph(g, stream=self.stream):
                     self._pipe_control(p, feedback=self.world == 1)
                 gc.append(g)
+            self.lib.gg_set_sm_reserve(prev)
             n0 = _native.LAUNCHES
             gk = None
             if self.world > 1:

@@ -25,6 +25,10 @@ timeout 300 $NCU --set full --import-source on -k regex:attention -s 1 -c 1 \
   -o "$OUT/distilbert_attention" python tools/forward_once.py distilbert 1 > /dev/null 2>&1
 timeout 300 $NCU --set full --import-source on -k regex:stem_pool_span -s 0 -c 1 \
   -o "$OUT/resnet18_stem_pool" python tools/forward_once.py resnet18 1 > /dev/null 2>&1
+timeout 300 $NCU --set full --import-source on -k regex:cls_head_kernel -s 0 -c 1 \
+  -o "$OUT/distilbert_cls_head" python tools/forward_once.py distilbert 1 > /dev/null 2>&1
+timeout 300 $NCU --set full --import-source on -k regex:fallback_kernel -s 1 -c 1 \
+  -o "$OUT/resnet18_fallback_cluster" python tools/serve_once.py resnet18 3 > /dev/null 2>&1
 GG_PROBE_EAGER=1 timeout 300 $NCU --set full --import-source on -k regex:admit_small_kernel -s 1 -c 1 \
   -o "$OUT/k1_admit_2p26" python tools/kernel_probe.py k1 1 > /dev/null 2>&1
 for f in "$OUT"/*.ncu-rep; do
