@@ -167,9 +167,8 @@ int gg_layernorm(const void* x, int64_t ldx, void* y, int64_t ldy, const float* 
  * (row r at hidden + r * ld_rows, bf16 [768]): x = LayerNorm(row) (skipped when
  * ln_gamma is NULL), pooled = bf16(ReLU(x W_pre^T + b_pre)), logits[r, :labels] =
  * pooled W_cls^T + b_cls (fp32).  W_pre bf16 [768, 768], W_cls bf16 [labels, 768].
- * scratch: gg_cls_head_scratch_bytes(max_rows) bytes; arrivals: int32
- * [ceil(max_rows / 16)], zero before the first call (the kernel re-zeroes it).
- * Deterministic. */
+ * scratch / arrivals: reserved (may be NULL; the classifier partials are reduced
+ * inside a thread-block cluster).  Deterministic. */
 int gg_cls_head(const void* hidden, int64_t ld_rows, const float* ln_gamma, const float* ln_beta,
                 float eps, const void* w_pre, const float* b_pre, const void* w_cls,
                 const float* b_cls, int32_t labels, float* logits, int64_t ld_logits, int32_t rows,

@@ -10,9 +10,9 @@
 // normalises its 16 rows into shared memory exactly as gg_layernorm does (same bf16
 // operand), runs the 16 x 96 x 768 product on mma.sync (bf16, fp32 accumulate; the tile is
 // far too small for tcgen05 to pay), applies bias + ReLU + the bf16 rounding of the pooled
-// activation, and reduces its classifier partial dot products.  The last CTA of a row block
-// (per-row-block arrival counter) adds the 8 column-block partials in a fixed order — the
-// logits are deterministic.
+// activation, and reduces its classifier partial dot products; the 8 column-block CTAs of a
+// row block form a thread-block cluster and CTA 0 adds their partials from its shared
+// memory (written over DSMEM) in a fixed order — the logits are deterministic.
 #include "gg_common.cuh"
 #include "gg_kernels.h"
 #include "gg_tc.cuh"
@@ -28,7 +28,6 @@ constexpr int kHeadColBlocks = kHeadD / kHeadCols;
 constexpr int kHeadLd = kHeadD + 8;        // padded smem row (bf16): ldmatrix conflict-free
 constexpr int kHeadThreads = 256;
 constexpr int kHeadMaxLabels = 32;
-constexpr size_t kHeadSmem = (size_t)(kHeadCols + kHeadRows) * kHeadLd * 2;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
@@ -46,87 +45,119 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a
                : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-__global__ void __launch_bounds__(kHeadThreads, 1)
+// Shared memory: W_pre slice [96][kHeadLd] bf16 | CLS operand [16][kHeadLd] bf16 |
+// gamma, beta [768] fp32 | W_cls slice [labels][96] fp32 | classifier partials of
+// the cluster's 8 CTAs [8][16][kHeadMaxLabels] fp32 (written into CTA 0's copy).
+constexpr size_t kHeadOffA = (size_t)kHeadCols * kHeadLd * 2;
+constexpr size_t kHeadOffG = kHeadOffA + (size_t)kHeadRows * kHeadLd * 2;
+constexpr size_t kHeadOffWc = kHeadOffG + 2 * kHeadD * 4;
+constexpr size_t kHeadOffP = kHeadOffWc + (size_t)kHeadMaxLabels * kHeadCols * 4;
+constexpr size_t kHeadSmemAll = kHeadOffP + (size_t)kHeadColBlocks * kHeadRows * kHeadMaxLabels * 4;
+
+// One cluster per 16-row block: its 8 CTAs are the 96-column blocks of the
+// pre_classifier; their classifier partials meet in CTA 0's shared memory over
+// DSMEM (fixed summation order, no global round trip).
+__global__ void __cluster_dims__(kHeadColBlocks, 1, 1) __launch_bounds__(kHeadThreads, 1)
 cls_head_kernel(const __nv_bfloat16* __restrict__ hidden, int64_t ld_rows, const float* __restrict__ ln_g,
                 const float* __restrict__ ln_b, float eps, const __nv_bfloat16* __restrict__ w_pre,
                 const float* __restrict__ b_pre, const __nv_bfloat16* __restrict__ w_cls,
                 const float* __restrict__ b_cls, int labels, float* __restrict__ logits, int64_t ld_logits,
-                int rows, const int32_t* __restrict__ count, float* __restrict__ part,
-                int32_t* __restrict__ arrivals, int max_rows) {
+                int rows, const int32_t* __restrict__ count) {
   extern __shared__ __align__(128) uint8_t head_smem[];
-  __nv_bfloat16* sw = reinterpret_cast<__nv_bfloat16*>(head_smem);          // [96][kHeadLd]
-  __nv_bfloat16* sa = sw + kHeadCols * kHeadLd;                              // [16][kHeadLd]
+  __nv_bfloat16* sw = reinterpret_cast<__nv_bfloat16*>(head_smem);
+  __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(head_smem + kHeadOffA);
+  float* sg = reinterpret_cast<float*>(head_smem + kHeadOffG);       // gamma | beta
+  float* swc = reinterpret_cast<float*>(head_smem + kHeadOffWc);     // [labels][96]
+  float* spart = reinterpret_cast<float*>(head_smem + kHeadOffP);    // [8][16][kHeadMaxLabels]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int cb = blockIdx.x, rb = blockIdx.y;
   const int n0 = cb * kHeadCols;
-  // weight slice (independent of the encoder): issued before the dependency wait
+  // everything that does not depend on the encoder, before the dependency wait:
+  // the W_pre slice (cp.async), gamma / beta, the W_cls slice
   for (int i = tid; i < kHeadCols * (kHeadD / 8); i += kHeadThreads) {
     const int r = i / (kHeadD / 8), c = (i % (kHeadD / 8)) * 8;
     cp_async16(sw + r * kHeadLd + c, w_pre + (int64_t)(n0 + r) * kHeadD + c);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
+  if (ln_g)
+    for (int i = tid; i < kHeadD; i += kHeadThreads) {
+      sg[i] = __ldg(ln_g + i);
+      sg[kHeadD + i] = __ldg(ln_b + i);
+    }
+  for (int i = tid; i < labels * kHeadCols; i += kHeadThreads)
+    swc[i] = __bfloat162float(__ldg(w_cls + (int64_t)(i / kHeadCols) * kHeadD + n0 + i % kHeadCols));
   griddep_wait();
   griddep_launch();
   if (count) rows = min(rows, (int)__ldg(count));
   const int r0 = rb * kHeadRows;
-  if (r0 >= rows) {
+  if (r0 >= rows) {   // the whole cluster (one row block) leaves together
     asm volatile("cp.async.wait_all;" ::: "memory");
     return;
   }
-  // the CTA's CLS rows -> bf16 operand (LayerNorm as gg_layernorm computes it)
-  for (int j = warp; j < kHeadRows; j += kHeadThreads / 32) {
-    const int r = r0 + j;
-    __nv_bfloat16* dst = sa + j * kHeadLd;
-    if (r >= rows) {
-      for (int c = lane * 8; c < kHeadD; c += 256) *reinterpret_cast<uint4*>(dst + c) = make_uint4(0, 0, 0, 0);
-      continue;
-    }
-    const __nv_bfloat16* src = hidden + (int64_t)r * ld_rows;
-    if (!ln_g) {
-      for (int c = lane * 8; c < kHeadD; c += 256)
-        *reinterpret_cast<uint4*>(dst + c) = __ldg(reinterpret_cast<const uint4*>(src + c));
-      continue;
-    }
-    float v[24];
+  __syncthreads();   // gamma / beta visible
+  // the CTA's CLS rows -> bf16 operand (LayerNorm as gg_layernorm computes it);
+  // warp w takes rows w and w + 8, both rows' loads in flight before the reductions
+  {
+    float v[2][24];
+    bool have[2];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const uint4 u = __ldcg(reinterpret_cast<const uint4*>(src + (c * 32 + lane) * 8));
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    for (int h = 0; h < 2; ++h) {
+      const int r = r0 + warp + 8 * h;
+      have[h] = r < rows;
+      const __nv_bfloat16* src = hidden + (int64_t)(have[h] ? r : r0) * ld_rows;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h[e]);
-        v[c * 8 + 2 * e] = f.x;
-        v[c * 8 + 2 * e + 1] = f.y;
+      for (int c = 0; c < 3; ++c) {
+        const uint4 u = __ldcg(reinterpret_cast<const uint4*>(src + (c * 32 + lane) * 8));
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(h2[e]);
+          v[h][c * 8 + 2 * e] = f.x;
+          v[h][c * 8 + 2 * e + 1] = f.y;
+        }
       }
     }
-    float sum = 0.f;
 #pragma unroll
-    for (int i = 0; i < 24; ++i) sum += v[i];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    const float mean = sum / kHeadD;
-    float var = 0.f;
-#pragma unroll
-    for (int i = 0; i < 24; ++i) {
-      const float d = v[i] - mean;
-      var += d * d;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
-    const float rstd = rsqrtf(var / kHeadD + eps);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const int col = (c * 32 + lane) * 8;
-      uint32_t w[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float a = (v[c * 8 + 2 * e] - mean) * rstd * __ldg(ln_g + col + 2 * e) + __ldg(ln_b + col + 2 * e);
-        const float b =
-            (v[c * 8 + 2 * e + 1] - mean) * rstd * __ldg(ln_g + col + 2 * e + 1) + __ldg(ln_b + col + 2 * e + 1);
-        __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
-        w[e] = *reinterpret_cast<uint32_t*>(&t);
+    for (int h = 0; h < 2; ++h) {
+      __nv_bfloat16* dst = sa + (warp + 8 * h) * kHeadLd;
+      if (!have[h]) {
+        for (int c = lane * 8; c < kHeadD; c += 256) *reinterpret_cast<uint4*>(dst + c) = make_uint4(0, 0, 0, 0);
+        continue;
       }
-      *reinterpret_cast<uint4*>(dst + col) = make_uint4(w[0], w[1], w[2], w[3]);
+      float mean = 0.f, rstd = 1.f;
+      if (ln_g) {
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 24; ++i) sum += v[h][i];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        mean = sum / kHeadD;
+        float var = 0.f;
+#pragma unroll
+        for (int i = 0; i < 24; ++i) {
+          const float d = v[h][i] - mean;
+          var += d * d;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) var += __shfl_xor_sync(0xffffffffu, var, o);
+        rstd = rsqrtf(var / kHeadD + eps);
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int col = (c * 32 + lane) * 8;
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float x0 = v[h][c * 8 + 2 * e], x1 = v[h][c * 8 + 2 * e + 1];
+          if (ln_g) {
+            x0 = (x0 - mean) * rstd * sg[col + 2 * e] + sg[kHeadD + col + 2 * e];
+            x1 = (x1 - mean) * rstd * sg[col + 2 * e + 1] + sg[kHeadD + col + 2 * e + 1];
+          }
+          __nv_bfloat162 t = __floats2bfloat162_rn(x0, x1);
+          w[e] = *reinterpret_cast<uint32_t*>(&t);
+        }
+        *reinterpret_cast<uint4*>(dst + col) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
@@ -172,34 +203,26 @@ cls_head_kernel(const __nv_bfloat16* __restrict__ hidden, int64_t ld_rows, const
     pooled[i] = __bfloat162float(__float2bfloat16_rn(s));
   }
   __syncthreads();
-  // classifier partials over this CTA's 96 columns: part[cb][row][label]
+  // classifier partials over this CTA's 96 columns -> CTA 0's spart[cb] (DSMEM)
+  const uint32_t part0 = tc::mapa_shared(tc::smem_u32(spart), 0);
   for (int i = tid; i < kHeadRows * labels; i += kHeadThreads) {
     const int j = i / labels, l = i % labels;
-    if (r0 + j >= rows) continue;
-    const __nv_bfloat16* wl = w_cls + (int64_t)l * kHeadD + n0;
     float s = 0.f;
 #pragma unroll 8
-    for (int c = 0; c < kHeadCols; ++c) s += pooled[j * kHeadCols + c] * __bfloat162float(__ldg(wl + c));
-    part[((int64_t)cb * max_rows + r0 + j) * kHeadMaxLabels + l] = s;
+    for (int c = 0; c < kHeadCols; ++c) s += pooled[j * kHeadCols + c] * swc[l * kHeadCols + c];
+    tc::st_shared_cluster_s32(part0 + 4u * (uint32_t)((cb * kHeadRows + j) * kHeadMaxLabels + l),
+                              __float_as_int(s));
   }
-  __syncthreads();
-  __shared__ int last;
-  if (tid == 0) {
-    __threadfence();
-    last = atomicAdd(arrivals + rb, 1) == kHeadColBlocks - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
+  tc::cluster_sync_all();
+  if (tc::cluster_ctarank() != 0) return;
   for (int i = tid; i < kHeadRows * labels; i += kHeadThreads) {
     const int j = i / labels, l = i % labels;
     if (r0 + j >= rows) continue;
     float s = 0.f;
 #pragma unroll
-    for (int c = 0; c < kHeadColBlocks; ++c) s += __ldcg(part + ((int64_t)c * max_rows + r0 + j) * kHeadMaxLabels + l);
+    for (int c = 0; c < kHeadColBlocks; ++c) s += spart[(c * kHeadRows + j) * kHeadMaxLabels + l];
     logits[(int64_t)(r0 + j) * ld_logits + l] = s + __ldg(b_cls + l);
   }
-  if (tid == 0) arrivals[rb] = 0;  // ready for the next forward (graph replay)
 }
 
 }  // namespace gg
@@ -211,24 +234,26 @@ extern "C" int gg_cls_head(const void* hidden, int64_t ld_rows, const float* ln_
                            const float* b_cls, int32_t labels, float* logits, int64_t ld_logits, int32_t rows,
                            int32_t max_rows, const int32_t* count_dev, float* scratch, int32_t* arrivals,
                            void* stream) {
-  if (!hidden || !w_pre || !b_pre || !w_cls || !b_cls || !logits || !scratch || !arrivals || rows < 0 ||
+  (void)scratch;
+  (void)arrivals;
+  if (!hidden || !w_pre || !b_pre || !w_cls || !b_cls || !logits || rows < 0 ||
       rows > max_rows || (!ln_gamma) != (!ln_beta))
     return GG_ERR_INVALID_ARGUMENT;
   if (labels < 1 || labels > kHeadMaxLabels || ld_rows % 8 || ld_logits < labels) return GG_ERR_UNSUPPORTED;
   if (rows == 0) return GG_OK;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(cls_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHeadSmem) !=
+    if (cudaFuncSetAttribute(cls_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHeadSmemAll) !=
         cudaSuccess)
       return GG_ERR_CUDA;
     attr = true;
   }
+  (void)max_rows;   // scratch / arrivals: kept in the ABI, unused since the cluster reduction
   const dim3 grid(kHeadColBlocks, (unsigned)((rows + kHeadRows - 1) / kHeadRows));
-  if (launch_pdl(cls_head_kernel, grid, dim3(kHeadThreads), kHeadSmem, gg_stream(stream),
+  if (launch_pdl(cls_head_kernel, grid, dim3(kHeadThreads), kHeadSmemAll, gg_stream(stream),
                  reinterpret_cast<const __nv_bfloat16*>(hidden), ld_rows, ln_gamma, ln_beta, eps,
                  reinterpret_cast<const __nv_bfloat16*>(w_pre), b_pre, reinterpret_cast<const __nv_bfloat16*>(w_cls),
-                 b_cls, (int)labels, logits, ld_logits, (int)rows, count_dev, scratch, arrivals,
-                 (int)max_rows) != cudaSuccess)
+                 b_cls, (int)labels, logits, ld_logits, (int)rows, count_dev) != cudaSuccess)
     return GG_ERR_CUDA;
   GG_LAUNCH_OK();
   return GG_OK;
