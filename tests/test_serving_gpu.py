@@ -317,3 +317,45 @@ def test_pipelined_steps_match_sequential(kind, k, B, window, win_ms, latency):
         assert a["last"][key] == b["last"][key]
     for key in ("pred", "conf", "decision"):
         assert np.array_equal(a["last"][key], b["last"][key])
+
+
+def test_measured_latency_feedback():
+    """latency="measured": the served-outcome kernel stamps %globaltimer after the
+    forward and K3, so each served request's latency (admission -> completion of its
+    batch's epilogue) is the device's own and drives the controller on the device:
+    the state's p95 equals the nearest-rank p95 (telemetry.py:35-46) of the last
+    p95_window served latencies.  The pipelined loop refuses this mode (its control
+    chain does not wait for the forward)."""
+    import math
+    import torch
+    import paper_2601_04250_b200 as gg
+    from paper_2601_04250_b200 import serving
+    from paper_2601_04250_b200.distilbert import DistilBertB200, random_model
+    n, B, window = 240, 16, 24
+    scores, now = make_trace(n, 2, seed=21)
+    ctl = gg.ControllerConfig(alpha=1.0, beta=-0.2, gamma=-0.4, tau0=0.8, tau_inf=0.35, k=1.5,
+                              routing=gg.RoutePolicy.ALL_BATCHED).build(gg.EnergyLedger())
+    net = DistilBertB200(random_model(0), max_batch=B)
+    kw = dict(window=window, outcome=serving.OutcomeModel(**MODEL, latency="measured"),
+              fifo_capacity=1024)
+    with pytest.raises(ValueError):
+        serving.GatedServer(ctl, net, torch.from_numpy(scores).cuda(), torch.from_numpy(now).cuda(),
+                            serving.synthetic_tokens(32), pipeline=True, **kw)
+    srv = serving.GatedServer(ctl, net, torch.from_numpy(scores).cuda(), torch.from_numpy(now).cuda(),
+                              serving.synthetic_tokens(32), **kw)
+    srv.run(1)
+    srv.capture()
+    while not srv.done():
+        srv.run(1)
+    torch.cuda.synchronize()
+    pred = srv.predicted.cpu().numpy()
+    lat = srv.latency.cpu().numpy()
+    served = np.nonzero(pred >= 0)[0]                  # FIFO order == trace order
+    assert len(served) > 10
+    ls = lat[served]
+    assert np.all(np.isfinite(ls)) and np.all(ls > 0.0)
+    st = srv.ctl.state_struct()
+    assert st.outcomes_total == len(served)
+    last = np.sort(ls[-int(srv.ctl.params.p95_window):])
+    k = max(1, math.ceil(0.95 * len(last)))
+    assert st.p95_current == last[k - 1]
