@@ -256,12 +256,13 @@ def test_fallback_answers_large_window(k):
     assert int(cur.item()) == cc
 
 
-@pytest.mark.parametrize("kind,k,B,window,win_ms,latency", [
-    ("distilbert", 2, 16, 24, None, "model"),
-    ("distilbert", 2, 16, 24, 4.0, "trace"),
-    ("resnet18", 1000, 8, 12, 4.0, "trace"),
+@pytest.mark.parametrize("kind,k,B,window,win_ms,latency,open_loop", [
+    ("distilbert", 2, 16, 24, None, "model", False),
+    ("distilbert", 2, 16, 24, 4.0, "trace", False),
+    ("distilbert", 2, 16, 40, 6.0, "trace", True),
+    ("resnet18", 1000, 8, 12, 4.0, "trace", False),
 ])
-def test_pipelined_steps_match_sequential(kind, k, B, window, win_ms, latency):
+def test_pipelined_steps_match_sequential(kind, k, B, window, win_ms, latency, open_loop):
     """GatedServer(pipeline=True) -- the control chain of step t+1 on the serving
     stream while step t's forward / K3 / publish run on a second stream, per-step
     buffers in two alternating sets, two parity graphs -- ends in exactly the
@@ -293,7 +294,7 @@ def test_pipelined_steps_match_sequential(kind, k, B, window, win_ms, latency):
             window=window, outcome=serving.OutcomeModel(**MODEL, latency=latency),
             fifo_capacity=4096, batching_window_ms=win_ms, labels=torch.from_numpy(labels).cuda(),
             coins=torch.from_numpy(coins).cuda(), fallback_degradation=0.2, publish=True,
-            pipeline=pipe)
+            pipeline=pipe, open_loop=open_loop)
         srv.run(1)
         srv.capture()
         steps = 1
