@@ -115,3 +115,33 @@ def test_gemm_stream_k(env, M, N, K, act, res):
     assert torch.equal(d_sk, d_sk2)
     assert (d_sk.float() - ref).abs().max().item() <= 2e-2 * scale
     assert (d_sk.float() - d_dp.float()).abs().max().item() <= 1e-2 * scale
+
+
+def test_sm_reserve_grids_same_results(env):
+    """gg_set_sm_reserve: validation (even, >= 0, below the SM count; returns the
+    previous value) and persistent grids sized to the remaining SMs compute the same
+    bits: a DistilBERT forward captured with 2 SMs reserved (the pipelined serving
+    loop's setting) equals the full-grid forward exactly."""
+    torch, nat, lib = env
+    from paper_2601_04250_b200.distilbert import DistilBertB200, random_model
+    assert lib.gg_set_sm_reserve(3) == -1 and lib.gg_set_sm_reserve(-2) == -1
+    assert lib.gg_set_sm_reserve(100000) == -1
+    net = DistilBertB200(random_model(0), max_batch=64)
+    ids = torch.randint(0, 30522, (64, 128), generator=torch.Generator().manual_seed(4)).to(torch.int32).cuda()
+    full = net.forward(ids).clone()
+    outs = []
+    for reserve in (2, 4):
+        prev = lib.gg_set_sm_reserve(reserve)
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    out = net.forward(ids, stream=s)
+        finally:
+            assert lib.gg_set_sm_reserve(prev) == reserve
+        g.replay()
+        torch.cuda.synchronize()
+        outs.append(out.clone())
+    for o in outs:
+        assert torch.equal(o, full)
