@@ -549,7 +549,7 @@ def roofline_forward(srv, net, B):
                  "encoder), persistent tcgen05 attention with P in TMEM, embedding-LN, CLS "
                  "LayerNorm + classifier head")
     traffic, traffic_src = None, None
-    for name in ("r2c_forward_traffic.json", "r2_forward_traffic.json", "r1g_forward_traffic.json"):
+    for name in ("r2d_forward_traffic.json", "r2c_forward_traffic.json", "r2_forward_traffic.json", "r1g_forward_traffic.json"):
         try:   # committed ncu evidence: DRAM bytes of one full-batch forward
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 t = json.load(f)[srv.kind]
