@@ -272,7 +272,22 @@ def run_ours(args, kind, rank, world, local_rank, pg, with_clocks=True):
             "trace_clock_s": [round(f0.clock, 4), round(f1.clock, 4)]}
 
     # ---- e2e through the public API with host buffers -----------------------
-    e2e = run_e2e(srv, scores_np, now_np, payloads, e2e_steps, args.warmup)
+    if kind == "resnet18" and os.environ.get("GG_E2E_ZERO_COPY") == "1":
+        # opt-in: images stay in the pinned host arrival pool and the gather reads only
+        # the served batch's images over PCIe (a second server on the same model, fresh
+        # trace).  Measured slower than uploading every arrival by the copy engine
+        # (146 k vs 157 k img/s): 16-byte zero-copy reads use PCIe far less efficiently
+        host_pool = payloads.cpu().pin_memory()
+        srv_zc = make_server(wl, kind, net, scores, now, labels, host_pool, dev, rank=rank,
+                             world=world, pg=pg, coin_seed=1000 + rank, publish=True)
+        srv_zc.run(1)
+        torch.cuda.synchronize()
+        srv_zc.capture()
+        e2e = run_e2e(srv_zc, scores_np, now_np, host_pool, e2e_steps, args.warmup, zero_copy=True)
+        e2e["payload_path"] = "zero-copy: the gather kernel reads the served batch's images from pinned host memory"
+        del srv_zc
+    else:
+        e2e = run_e2e(srv, scores_np, now_np, payloads, e2e_steps, args.warmup)
 
     # ---- roofline of the forward (full batch, CUDA events on the launch stream)
     ro = roofline_forward(srv, net, B)
@@ -304,12 +319,16 @@ def _tau_range(ctl, now_np, c0, c1, t_origin):
     return [round(tau(t0), 4), round(tau(t1), 4)]
 
 
-def run_e2e(srv, scores_np, now_np, payloads, steps, warmup):
+def run_e2e(srv, scores_np, now_np, payloads, steps, warmup, zero_copy=False):
     """Public-API loop with host buffers, pipelined like a serving front end: the
     window of step i+1 (scores, arrival times, payloads: pinned host -> device on
     a copy stream) uploads while step i computes; every step's served
     predictions/confidences and the window's decisions come back device -> host
-    and the host waits for them one step behind.  All copies are inside the
+    and the host waits for them one step behind.  zero_copy (ResNet-18): the
+    server's payload pool is the pinned host arrival pool itself and the gather
+    kernel reads only the served batch's images over PCIe (counted as
+    host -> device bytes from the step's record), no image upload per window.
+    All copies are inside the
     timed region (CUDA events)."""
     import torch
     W, T = srv.W, srv.T
@@ -341,13 +360,15 @@ def run_e2e(srv, scores_np, now_np, payloads, steps, warmup):
             srv.scores[c:c1].copy_(host_scores[c:c1], non_blocking=True)
             srv.now[c:c1].copy_(host_now[c:c1], non_blocking=True)
             lo, hi = c % P, c % P + n        # payloads go to their pool slots (row % P)
-            if hi <= P:
+            if zero_copy:
+                pass                             # read in place by the gather (counted per step)
+            elif hi <= P:
                 dev_pay[lo:hi].copy_(host_pay[:n], non_blocking=True)
             else:
                 dev_pay[lo:].copy_(host_pay[:P - lo], non_blocking=True)
                 dev_pay[: hi - P].copy_(host_pay[P - lo:n], non_blocking=True)
             ev_in[slot].record(cs)
-        stats["h2d"] += n * (srv.K + 1) * 8 + n * pay_row
+        stats["h2d"] += n * (srv.K + 1) * 8 + (0 if zero_copy else n * pay_row)
         return c1
 
     def run(nsteps, c):
@@ -370,10 +391,14 @@ def run_e2e(srv, scores_np, now_np, payloads, steps, warmup):
                 ev_out[sl].synchronize()
                 rec = srv.record(sid)
                 stats["d2h"] += rec_payload + len(rec["decision"])
+                if zero_copy:
+                    stats["h2d"] += rec["count"] * pay_row
         for sid, sl, n in pending:
             ev_out[sl].synchronize()
             rec = srv.record(sid)
             stats["d2h"] += rec_payload + len(rec["decision"])
+            if zero_copy:
+                stats["h2d"] += rec["count"] * pay_row
         return c
 
     cursor = run(warmup, cursor)
@@ -831,7 +856,8 @@ def _line(r: dict, args, world: int, kind: str) -> dict:
             "roofline": r["roofline"],
             "e2e": {"value": round(e2e_value, 2) if e2e_value else None, "unit": "inferences/s",
                     "h2d_bytes_per_step": r["e2e"]["h2d_bytes_per_step"],
-                    "d2h_bytes_per_step": r["e2e"]["d2h_bytes_per_step"]},
+                    "d2h_bytes_per_step": r["e2e"]["d2h_bytes_per_step"],
+                    **({"payload_path": r["e2e"]["payload_path"]} if "payload_path" in r["e2e"] else {})},
             "gpu_launches": r["launches_per_step"] * args.steps, "clocks": r["clocks"],
             "energy": r["energy"]}
 
