@@ -297,7 +297,7 @@ class ControllerConfig:
 
     def build(self, ledger=None, congestion_source=None, *, p95_window: int = 100,
               t_origin: float = 0.0, device=None) -> "AdmissionController":
-        return AdmissionController(
+        ctl = AdmissionController(
             CostWeights(self.alpha, self.beta, self.gamma),
             ThresholdSchedule(self.tau0, self.tau_inf, self.k, t_origin),
             ledger if ledger is not None else EnergyLedger(),
@@ -309,6 +309,11 @@ class ControllerConfig:
             p95_window=p95_window,
             device=device,
         )
+        # `enabled` is read by the serving loop, as the reference's simulator reads it
+        # (servesim.py:231-240): GatedServer(open_loop=None) runs the open-loop arm
+        # for a controller built from a disabled config
+        ctl.enabled = bool(self.enabled)
+        return ctl
 
 
 @dataclass

@@ -69,7 +69,8 @@ class GatedServer:
     scores/now: CUDA fp64 [T, K] / [T] resident trace (this rank's shard)
     payloads:   ResNet: CUDA uint8 [P, H, W, 3]; DistilBERT: (ids int32 [P, S], mask int32 [P, S])
     open_loop:  the reference's controller-disabled arm (servesim.py:231-240):
-                admit every arrival, static route (gg_admit_open_stream)
+                admit every arrival, static route (gg_admit_open_stream); None
+                follows the controller's config (`ControllerConfig.enabled`)
     batching_window_ms: Path-B flush policy (servesim.py:148-162): a batch is
                 popped when B requests are pending or the oldest waited the
                 window in trace time; None pops min(B, depth) every step
@@ -92,7 +93,7 @@ class GatedServer:
 
     def __init__(self, controller, net, scores, now, payloads, *, window: int,
                  outcome: OutcomeModel | None = None, fifo_capacity: int = 1 << 20,
-                 rank: int = 0, world: int = 1, process_group=None, open_loop: bool = False,
+                 rank: int = 0, world: int = 1, process_group=None, open_loop: bool | None = None,
                  batching_window_ms: float | None = None, labels=None, coins=None,
                  fallback_degradation: float = 0.05, publish: bool = False,
                  pipeline: bool = False):
@@ -110,6 +111,8 @@ class GatedServer:
         self.outcome_model = outcome or OutcomeModel()
         self.outcome = self.outcome_model.abi()
         self.rank, self.world, self.pg = rank, world, process_group
+        if open_loop is None:
+            open_loop = not getattr(controller, "enabled", True)
         self.open_loop = bool(open_loop)
         self.window_s = 0.0 if batching_window_ms is None else float(batching_window_ms) / 1000.0
         if self.window_s < 0.0:

@@ -112,7 +112,8 @@ def test_serving_policies_vs_oracle(kind, k, B, window, open_loop, win_ms, laten
     cfg_kw = dict(alpha=1.0, beta=-0.2, gamma=-0.4, tau0=0.8, tau_inf=0.35, k=1.5,
                   routing=[gg.RoutePolicy.ALL_DIRECT, gg.RoutePolicy.ALL_BATCHED,
                            gg.RoutePolicy.THRESHOLD_ON_QUEUE][routing], queue_threshold=6)
-    ctl = gg.ControllerConfig(**cfg_kw).build(gg.EnergyLedger())
+    # the open-loop arm comes from the config's `enabled`, as in the reference simulator
+    ctl = gg.ControllerConfig(enabled=not open_loop, **cfg_kw).build(gg.EnergyLedger())
     if kind == "resnet18":
         from paper_2601_04250_b200.resnet18 import ResNet18B200, random_model
         net = ResNet18B200(random_model(0), max_batch=B)
@@ -124,8 +125,9 @@ def test_serving_policies_vs_oracle(kind, k, B, window, open_loop, win_ms, laten
     srv = serving.GatedServer(
         ctl, net, torch.from_numpy(scores).cuda(), torch.from_numpy(now).cuda(), payloads,
         window=window, outcome=serving.OutcomeModel(**MODEL, latency=latency), fifo_capacity=4096,
-        open_loop=open_loop, batching_window_ms=win_ms, labels=torch.from_numpy(labels).cuda(),
+        batching_window_ms=win_ms, labels=torch.from_numpy(labels).cuda(),
         coins=torch.from_numpy(coins).cuda(), fallback_degradation=deg)
+    assert srv.open_loop == open_loop
     srv.run(1)
     srv.capture()
     steps = 1
