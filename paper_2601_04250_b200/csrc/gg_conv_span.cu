@@ -1510,6 +1510,320 @@ __global__ void __launch_bounds__(kSpanThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Pixel-pair span convolution: 3x3 / 1 with C = Cout = 64 (ResNet-18 layer 1).
+//
+// An M = 128, K = 16 MMA costs the tensor pipe ~64 cycles at N = 64 and N = 128
+// alike (tools/mma_bench.cu), so the N = 64 span conv runs the pipe at half rate.
+// Here an accumulator row (TMEM lane) is a PAIR of consecutive padded pixels:
+// lane i of a tile owns window origins m = 2(q + i) + e, e in {0, 1}, and its 128
+// columns are [e = 0: 64 channels | e = 1: 64 channels] — exactly the 256 contiguous
+// output bytes of the pixel pair.  The activations are read as a [pixels / 2, 128]
+// matrix (two 64-channel K halves per pair row).  Tap (r, s) of slot e reads pixel
+// 2(q + i) + r*Wp + j with j = e + s in 0..3, i.e. pair row q + i + P and K half h
+// with P = (r*Wp + j) >> 1, h = (r*Wp + j) & 1 — the same for both slots.  So per
+// kernel row r there are four A operands (j = 0..3), each ONE row-shifted view of
+// the span, and j's B operand holds W(r, j - e) for the slots where 0 <= j - e <= 2:
+//   j = 0: [W(r,0) | -]      N = 64 into columns 0..63
+//   j = 1: [W(r,1) | W(r,0)] N = 128
+//   j = 2: [W(r,2) | W(r,1)] N = 128
+//   j = 3: [- | W(r,2)]      N = 64 into columns 64..127
+// With the row's three tap slabs stacked in shared memory as [W(r,2); W(r,1);
+// W(r,0)] (64 N-rows each, K-major SW128), every B operand is a contiguous run of
+// that stack (j = 2: rows 0..127, j = 1: rows 64..191, j = 0: rows 128..191, j = 3:
+// rows 0..63) — the weight slab is the unmodified [64, 9 * 64] matrix, loaded as
+// nine 64 x 64 TMA boxes.  48 MMAs per 256 outputs instead of 72 N = 64 ones.
+// Needs Wp odd (the shared-border layout) so the output offset Wp + 1 is a whole
+// number of pairs.  Epilogue as conv_span_tcgen05's TMA path, in pair rows.
+__global__ void __launch_bounds__(kSpanThreads, 1)
+    conv_span_px2(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+                  const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_res,
+                  SpanShape sh, SpanEpi ep) {
+  constexpr int ACC_COLS = 128, NACC = 4;
+  constexpr int TAP_BYTES = 64 * 128;           // one 64 x 64 weight box
+  constexpr int B_TOTAL = 9 * TAP_BYTES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_align1k(smem_raw);
+  const int AST = sh.a_stages;
+  const int half_bytes = sh.a_stage_bytes / 2;
+  uint8_t* a_base = smem;
+  uint8_t* b_base = smem + AST * sh.a_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + B_TOTAL);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + kSpanMaxStages;
+  uint64_t* acc_full = a_empty + kSpanMaxStages;
+  uint64_t* acc_empty = acc_full + NACC;
+  uint64_t* bres_full = acc_empty + NACC;
+  uint64_t* res_full = bres_full + 1;      // [8 warps][2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(res_full + 2 * kSpanEpiWarps);
+  uint8_t* stg_base = smem_align1k(reinterpret_cast<uint8_t*>(bars) + 1024);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  griddep_launch();
+  const int img = sh.Hp * sh.Wp;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < AST; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 1);
+    }
+    for (int i = 0; i < NACC; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], kSpanEpiWarps);
+    }
+    mbar_init(bres_full, 1);
+    for (int i = 0; i < 2 * kSpanEpiWarps; ++i) mbar_init(&res_full[i], 1);
+    fence_mbar_init();
+    tma_prefetch(&map_x);
+    tma_prefetch(&map_w);
+    tma_prefetch(&map_out);
+    if (ep.residual) tma_prefetch(&map_res);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, NACC * ACC_COLS);
+  const int tiles_max = (sh.N * img + 255) / 256;
+  const bool b_loaded = tiles_max > (int)blockIdx.x;
+  // the weights do not depend on the predecessor: row r's stack [W(r,2); W(r,1); W(r,0)]
+  if (warp == 0 && lane == 0 && b_loaded) {
+    mbar_expect_tx(bres_full, B_TOTAL);
+    for (int r = 0; r < 3; ++r)
+      for (int k = 0; k < 3; ++k)
+        tma_load_2d(b_base + (r * 3 + k) * TAP_BYTES, &map_w, bres_full, (r * 3 + 2 - k) * 64, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();
+  const int n_eff = ep.count ? min(sh.N, __ldg(ep.count)) : sh.N;
+  const int Mtot = n_eff * img;
+  const int num_tiles = (Mtot + 255) / 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int as = 0;
+      uint32_t aph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait_sleep(&a_empty[as], aph ^ 1);
+        uint8_t* sa = a_base + as * sh.a_stage_bytes;
+        mbar_expect_tx(&a_full[as], 2 * sh.box_rows * 128);
+        tma_load_2d(sa, &map_x, &a_full[as], 0, tile * 128);
+        tma_load_2d(sa + half_bytes, &map_x, &a_full[as], 64, tile * 128);
+        if (++as == AST) {
+          as = 0;
+          aph ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc128 = idesc_act_f32(128, 128);
+    constexpr uint32_t idesc64 = idesc_act_f32(128, 64);
+    // per (r, j): A offset (16-B units: K half + pair-row shift), B offset, N, column
+    uint32_t a_off[12];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int v = r * sh.Wp + j;
+        a_off[r * 4 + j] = (uint32_t)((v & 1) * (half_bytes >> 4) + (v >> 1) * 8);
+      }
+    if (b_loaded) mbar_wait(bres_full, 0);
+    const uint64_t b_desc0 = sdesc_k_sw128(smem_u32(b_base));
+    const uint64_t a_desc0 = sdesc_k_sw128(smem_u32(a_base));
+    const uint64_t a_stage_d = (uint64_t)(sh.a_stage_bytes >> 4);
+    int as = 0, t = 0;
+    uint32_t aph = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+      const int acc = t % NACC;
+      mbar_wait(&acc_empty[acc], ((t / NACC) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * ACC_COLS;
+      mbar_wait(&a_full[as], aph);
+      tc_fence_after();
+      const uint64_t ad = a_desc0 + (uint64_t)as * a_stage_d;
+      const int as_now = as;
+      if (++as == AST) {
+        as = 0;
+        aph ^= 1;
+      }
+      if (elect_one_sync()) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+          const uint64_t bs = b_desc0 + (uint64_t)(r * 3 * (TAP_BYTES >> 4));
+          // j = 1 first: on r = 0 its N = 128 MMA initialises all 128 columns
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_bf16(d, ad + a_off[r * 4 + 1] + kk * 2, bs + 64 * 8 + kk * 2, idesc128, (r | kk) != 0);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_bf16(d, ad + a_off[r * 4 + 0] + kk * 2, bs + 128 * 8 + kk * 2, idesc64, 1);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_bf16(d, ad + a_off[r * 4 + 2] + kk * 2, bs + kk * 2, idesc128, 1);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_bf16(d + 64, ad + a_off[r * 4 + 3] + kk * 2, bs + kk * 2, idesc64, 1);
+        }
+        umma_commit(&a_empty[as_now]);
+        umma_commit(&acc_full[acc]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // warp w: TMEM lane quarter w % 4, slot e = (w - 2) / 4 (columns e * 64 .. e * 64 + 63)
+    const int quarter = warp & 3;
+    const int e = (warp - 2) >> 2;
+    uint8_t* stg = stg_base + (warp - 2) * 4096;
+    uint64_t* rb = res_full + (warp - 2) * 2;
+    uint32_t rph[2] = {0, 0};
+    const bool has_res = ep.residual != nullptr;
+    const int sw = (lane >> 1) & 3;
+    const int out_shift = (sh.Wp + 1) >> 1;   // output position m + Wp + 1, in pairs
+    int t = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+      const int acc = t % NACC;
+      const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * ACC_COLS + e * 64;
+      const int pw = tile * 128 + quarter * 32;          // the warp's first pair row
+      const int orow0 = pw + out_shift;
+      const bool any = 2 * pw < Mtot;
+      const int m = 2 * (pw + lane) + e;                  // this lane's window origin
+      const int nimg = m / img;
+      const int within = m - nimg * img;
+      const int h = within / sh.Wp, w = within - h * sh.Wp;
+      const bool real = m < Mtot && h < sh.Ho && w < sh.Wo;
+      // staging buffer c for chunk c; with a residual both boxes are requested up
+      // front (their latency overlaps the accumulator wait and chunk 0's math)
+      if (has_res && any && lane == 0) {
+        bulk_wait_read<0>();   // the previous tile's stores have read both buffers
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          mbar_expect_tx(&rb[c], 2048);
+          tma_load_2d(stg + c * 2048, &map_res, &rb[c], e * 64 + 32 * c, orow0);
+        }
+      }
+      __syncwarp();
+      mbar_wait_sleep(&acc_full[acc], (t / NACC) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        const int bsel = c;
+        uint8_t* buf = stg + bsel * 2048;
+        const int pcol = e * 64 + 32 * c;                 // column in the pair row
+        if (!has_res && any && lane == 0) bulk_wait_read<1>();   // the store two chunks back
+        __syncwarp();
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tbase + 32 * c, r);
+        tmem_ld_wait();
+        if (!any) continue;
+        uint4* myrow = reinterpret_cast<uint4*>(buf + lane * 64);
+        float v[32];
+        if (has_res) {
+          mbar_wait(&rb[bsel], rph[bsel]);
+          rph[bsel] ^= 1;
+        }
+        if (real) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 bb = __ldg(reinterpret_cast<const float4*>(ep.bias + 32 * c + i));
+            v[i] = __uint_as_float(r[i]) + bb.x;
+            v[i + 1] = __uint_as_float(r[i + 1]) + bb.y;
+            v[i + 2] = __uint_as_float(r[i + 2]) + bb.z;
+            v[i + 3] = __uint_as_float(r[i + 3]) + bb.w;
+          }
+          if (has_res) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 u = myrow[q ^ sw];
+              const act2_t* h2 = reinterpret_cast<const act2_t*>(&u);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float2 f = act2_to_float2(h2[k]);
+                v[q * 8 + 2 * k] += f.x;
+                v[q * 8 + 2 * k + 1] += f.y;
+              }
+            }
+          }
+          if (ep.relu) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.0f);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.0f;      // padding positions stay zero
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_act(v[q * 8 + 0], v[q * 8 + 1]);
+          u.y = pack_act(v[q * 8 + 2], v[q * 8 + 3]);
+          u.z = pack_act(v[q * 8 + 4], v[q * 8 + 5]);
+          u.w = pack_act(v[q * 8 + 6], v[q * 8 + 7]);
+          myrow[q ^ sw] = u;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&map_out, buf, pcol, orow0);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, NACC * ACC_COLS);
+  }
+}
+
+// Launch conv_span_px2 for a shared-border 3x3 / 1 conv with C = Cout = 64 (Wp odd).
+// Returns GG_ERR_UNSUPPORTED when the shape does not qualify (the caller falls back).
+static int launch_span_px2(const void* x, const void* w, const float* bias, const void* residual,
+                           int relu, void* y, const int32_t* count_dev, SpanShape sh, cudaStream_t s) {
+  if (sh.C != 64 || sh.Cout != 64 || !(sh.Wp & 1)) return GG_ERR_UNSUPPORTED;
+  const int64_t Mtot = (int64_t)sh.N * sh.Hp * sh.Wp;
+  sh.span_rows = 128 + sh.Wp + 1;                    // pair rows: max shift (2 Wp + 3) >> 1
+  if (sh.span_rows > 256) return GG_ERR_UNSUPPORTED;
+  sh.boxes = 1;
+  sh.box_rows = sh.span_rows;
+  sh.a_stage_bytes = 2 * ((sh.span_rows * 128 + 1023) / 1024 * 1024);
+  sh.bres = 1;
+  sh.b_stages = 1;
+  const int fixed = 9 * 64 * 128 + 2048 + kSpanStgBytes;
+  sh.a_stages = (kSpanSmemMax - fixed) / sh.a_stage_bytes;
+  if (sh.a_stages > kSpanMaxStages) sh.a_stages = kSpanMaxStages;
+  if (sh.a_stages < 2) return GG_ERR_UNSUPPORTED;
+  // pair rows cover pixel Mtot when Mtot is odd: the buffers hold the W + 2-pixel
+  // margin beyond the N images (shared-border layout), and that pixel is a border
+  // column position (written as zero)
+  const int64_t prows = (Mtot + 1) / 2;
+  CUtensorMap mx, mw, mo, mr;
+  int rc = make_map_span(&mx, x, prows, 128, 64, sh.box_rows);
+  if (!rc) rc = make_map_span(&mw, w, 64, 9 * 64, 64, 64);
+  if (!rc) rc = make_map_box32(&mo, y, prows, 128);
+  if (!rc && residual) rc = make_map_box32(&mr, residual, prows, 128);
+  if (rc) return rc;
+  auto kern = conv_span_px2;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSpanSmemMax) != cudaSuccess)
+      return GG_ERR_CUDA;
+    attr = true;
+  }
+  SpanEpi ep{reinterpret_cast<act_t*>(y), bias, reinterpret_cast<const act_t*>(residual), relu, count_dev,
+             nullptr, nullptr, 0, 1, StreamK{nullptr, nullptr, 0}};
+  const int smem = sh.a_stages * sh.a_stage_bytes + fixed;
+  const int tiles = (int)((Mtot + 255) / 256);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  if (launch_pdl(kern, dim3(grid), dim3(kSpanThreads), smem, s, mx, mw, mo, residual ? mr : mo, sh, ep) !=
+      cudaSuccess)
+    return GG_ERR_CUDA;
+  return GG_OK;
+}
+
 }  // namespace gg
 
 using namespace gg;
@@ -1539,6 +1853,13 @@ static int conv3x3_span(const void* x, int32_t N, int32_t H, int32_t W, int32_t 
   static const bool no_pair = getenv("GG_SPAN_PAIR") && atoi(getenv("GG_SPAN_PAIR")) == 0;
   // N = 64 pairs (layer 1) measured slower than single-CTA tiles (GG_SPAN_PAIR64=1 opts in)
   static const bool pair64 = getenv("GG_SPAN_PAIR64") && atoi(getenv("GG_SPAN_PAIR64")) == 1;
+  // C = Cout = 64 on the shared-border layout: pixel-pair tiles (N = 128 MMAs, see
+  // conv_span_px2); GG_SPAN_PX2=0 keeps the N = 64 span conv
+  static const bool no_px2 = getenv("GG_SPAN_PX2") && atoi(getenv("GG_SPAN_PX2")) == 0;
+  if (!no_px2 && border == 1 && C == 64 && Cout == 64 && !pair64 && !getenv("GG_SPAN_TILE")) {
+    const int rc = launch_span_px2(x, w, bias, residual, relu, y, count_dev, sh, gg_stream(stream));
+    if (rc != GG_ERR_UNSUPPORTED) return rc;
+  }
   if (!no_pair && (Cout % 128 == 0 || (Cout == 64 && pair64)) && !getenv("GG_SPAN_TILE")) {
     int bn = Cout % 256 == 0 ? 256 : Cout % 128 == 0 ? 128 : 64;
     if (bn == 256) {   // N = 128 pair tiles unless N = 256 finishes in strictly fewer rounds x width

@@ -247,11 +247,13 @@ def _from_shared(buf, n, s, c):
     return buf[s + 2:].reshape(n, s + 1, s + 1, c)
 
 
-@pytest.mark.parametrize("n,s,c,cout", [(64, 28, 128, 128), (64, 14, 256, 256), (64, 7, 512, 512),
+@pytest.mark.parametrize("n,s,c,cout", [(64, 56, 64, 64), (3, 56, 64, 64), (1, 7, 64, 64), (5, 9, 64, 64),
+                                        (64, 28, 128, 128), (64, 14, 256, 256), (64, 7, 512, 512),
                                         (3, 7, 512, 512)])
 def test_conv3x3_shared_border(env, n, s, c, cout):
-    """Span conv on the shared-border layout (layers 2-4) vs torch's padded conv, with
-    residual; the zero row / column of every image stays zero."""
+    """Span conv on the shared-border layout (layers 1-4; C = Cout = 64 runs the
+    pixel-pair kernel conv_span_px2, odd pixel counts included) vs torch's padded
+    conv, with residual; the zero row / column of every image stays zero."""
     torch, nat, lib = env
     from tests.test_conv_span_gpu import pack_span_weights
     g = torch.Generator(device="cuda").manual_seed(s + c)

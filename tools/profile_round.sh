@@ -15,7 +15,7 @@ timeout 300 $NCU --metrics $M --csv --log-file "$OUT/distilbert_forward_launches
 # one full capture per dominant kernel (a forward's instance)
 timeout 300 $NCU --set full --import-source on -k regex:conv_span_pair -s 3 -c 1 \
   -o "$OUT/resnet18_layer3_span_pair" python tools/forward_once.py resnet18 1 > /dev/null 2>&1
-timeout 300 $NCU --set full --import-source on -k regex:conv_span_tcgen05 -s 1 -c 1 \
+timeout 300 $NCU --set full --import-source on -k regex:conv_span_px2 -s 1 -c 1 \
   -o "$OUT/resnet18_layer1_span" python tools/forward_once.py resnet18 1 > /dev/null 2>&1
 timeout 300 $NCU --set full --import-source on -k regex:gemm_bf16_pair -s 2 -c 1 \
   -o "$OUT/distilbert_ffn_up_gemm_pair" python tools/forward_once.py distilbert 1 > /dev/null 2>&1
