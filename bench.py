@@ -565,7 +565,7 @@ def roofline_forward(srv, net, B):
     flops = net.flops(B)
     pk = peaks()
     achieved = flops / (ms * 1e-3) / 1e12
-    kern = ("ResNet-18 forward: fused stem conv + max pool + 4 span convs (layer 1) + 9 CTA-pair "
+    kern = ("ResNet-18 forward: fused stem conv + max pool + 4 pixel-pair span convs (layer 1) + 9 CTA-pair "
             "span convs (layers 2-4) + 3 fused stride-2 conv/downsample (TMA im2col) + fused "
             "avg pool/fc (fp32), all convs tcgen05, shared-border NHWC layout"
             if srv.kind == "resnet18"
@@ -574,7 +574,7 @@ def roofline_forward(srv, net, B):
                  "encoder), persistent tcgen05 attention with P in TMEM, embedding-LN, CLS "
                  "LayerNorm + classifier head")
     traffic, traffic_src = None, None
-    for name in ("r2d_forward_traffic.json", "r2c_forward_traffic.json", "r2_forward_traffic.json", "r1g_forward_traffic.json"):
+    for name in ("r2e_forward_traffic.json", "r2d_forward_traffic.json", "r2c_forward_traffic.json", "r2_forward_traffic.json", "r1g_forward_traffic.json"):
         try:   # committed ncu evidence: DRAM bytes of one full-batch forward
             with open(os.path.join(ROOT, "profiles", name)) as f:
                 t = json.load(f)[srv.kind]
