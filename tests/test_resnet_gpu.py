@@ -263,10 +263,15 @@ def test_conv3x3_shared_border(env, n, s, c, cout):
     b = torch.randn(cout, device="cuda", generator=g)
     xs, rs = _to_shared(x, s), _to_shared(r, s)
     ys = torch.full_like(_to_shared(torch.zeros((n, s, s, cout), dtype=torch.float16, device="cuda"), s), 0)
+    # a canary region right after the output buffer must stay untouched
+    rows = ys.shape[0]
+    yc = torch.cat([ys, torch.full((64, cout), 7.0, dtype=torch.float16, device="cuda")])
     nat.check("gg_conv3x3_shared", lib.gg_conv3x3_shared(
         nat.ptr(xs), n, s, s, c, nat.ptr(pack_span_weights(w)), cout, nat.ptr(b), nat.ptr(rs), 1,
-        nat.ptr(ys), None, nat.stream_ptr()))
+        nat.ptr(yc), None, nat.stream_ptr()))
     torch.cuda.synchronize()
+    assert (yc[rows:] == 7.0).all()
+    ys = yc[:rows]
     ref = torch.relu(torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), w.float(), b, padding=1) +
                      r.float().permute(0, 3, 1, 2))
     got = _from_shared(ys, n, s, cout)
@@ -376,3 +381,27 @@ def test_stem_gather(env, padded):
     assert (y[3].float() == 9.0).all()                            # beyond the count
     if padded:
         assert (y[:3, :2].float() == 9.0).all()                   # borders not written
+
+
+def test_conv3x3_shared_border_px2_count(env):
+    """Pixel-pair layer-1 conv with a device image count below the batch (the serving
+    loop's dynamic batch): the counted images match torch."""
+    torch, nat, lib = env
+    from tests.test_conv_span_gpu import pack_span_weights
+    n, s, c, k = 6, 56, 64, 3
+    g = torch.Generator(device="cuda").manual_seed(77)
+    x = torch.randn((n, s, s, c), device="cuda", generator=g).to(torch.float16)
+    r = torch.randn((n, s, s, c), device="cuda", generator=g).to(torch.float16)
+    w = (torch.randn((c, c, 3, 3), device="cuda", generator=g) / (9 * c) ** 0.5).to(torch.float16)
+    b = torch.randn(c, device="cuda", generator=g)
+    xs, rs = _to_shared(x, s), _to_shared(r, s)
+    ys = torch.zeros_like(xs)
+    cnt = torch.tensor([k], dtype=torch.int32, device="cuda")
+    nat.check("gg_conv3x3_shared", lib.gg_conv3x3_shared(
+        nat.ptr(xs), n, s, s, c, nat.ptr(pack_span_weights(w)), c, nat.ptr(b), nat.ptr(rs), 1,
+        nat.ptr(ys), nat.ptr(cnt), nat.stream_ptr()))
+    torch.cuda.synchronize()
+    ref = torch.relu(torch.nn.functional.conv2d(x[:k].float().permute(0, 3, 1, 2), w.float(), b, padding=1) +
+                     r[:k].float().permute(0, 3, 1, 2))
+    got = _from_shared(ys, n, s, c)[:k, :s, :s].float().permute(0, 3, 1, 2)
+    assert (got - ref).abs().max().item() <= 2e-2 * max(1.0, ref.abs().max().item())
