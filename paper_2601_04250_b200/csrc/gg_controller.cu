@@ -723,6 +723,17 @@ __global__ void __launch_bounds__(kSmallThreads) admit_compact_kernel(AdmitArgs 
   __shared__ int last, tot_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t c0 = (int64_t)blockIdx.x * kCompactRows;
+  // ---- masks of admitted rows: lane owns rows r0 .. r0+31.  The decision loads
+  // are issued first so their latency overlaps the prefix loads below.
+  const int64_t r0 = c0 + (int64_t)(warp * 32 + lane) * 32;
+  uint32_t mask = 0;
+  const bool vec = ((reinterpret_cast<uintptr_t>(a.decision) & 15) == 0) && r0 + 32 <= a.n;
+  uint4 u0 = make_uint4(0, 0, 0, 0), u1 = u0;
+  if (vec) {
+    const uint4* p4 = reinterpret_cast<const uint4*>(a.decision + r0);
+    u0 = __ldcs(p4);
+    u1 = __ldcs(p4 + 1);
+  }
   // ---- global offset of this block: decide block i0 = first of its tiles
   const int i0 = (int)(c0 / kDecideRows);
   const int sup = i0 >> a.super_shift, sup0 = sup << a.super_shift;
@@ -732,13 +743,7 @@ __global__ void __launch_bounds__(kSmallThreads) admit_compact_kernel(AdmitArgs 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
   if (lane == 0) red[warp] = part;
-  // ---- masks of admitted rows: lane owns rows r0 .. r0+31
-  const int64_t r0 = c0 + (int64_t)(warp * 32 + lane) * 32;
-  uint32_t mask = 0;
-  const bool vec = ((reinterpret_cast<uintptr_t>(a.decision) & 15) == 0) && r0 + 32 <= a.n;
   if (vec) {
-    const uint4* p4 = reinterpret_cast<const uint4*>(a.decision + r0);
-    const uint4 u0 = p4[0], u1 = p4[1];
     const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -781,19 +786,18 @@ __global__ void __launch_bounds__(kSmallThreads) admit_compact_kernel(AdmitArgs 
   for (int q = 0; q < WARPS; ++q) base += red[q];
   int pos = warp_off[warp] + (v - cnt);
   for (uint32_t m = mask; m; m &= m - 1) out[pos++] = (int32_t)(r0 + __ffs(m) - 1);
-  __syncthreads();
-  if (a.admitted_idx) {
-    // block total = last warp's offset + its inclusive sum (broadcast via smem)
-    if (warp == WARPS - 1 && lane == 31) tot_s = warp_off[warp] + v;
-    __syncthreads();
-    int32_t* dst = a.admitted_idx + (base & kCnt31);
-    for (int i = tid; i < tot_s; i += THREADS) dst[i] = out[i];
-  }
-  // ---- completion: the last block finalizes and re-zeroes the split counters
-  __threadfence();
-  __syncthreads();
+  // block total = last warp's offset + its inclusive sum (broadcast via smem)
+  if (warp == WARPS - 1 && lane == 31) tot_s = warp_off[warp] + v;
+  // ---- completion count: every block has consumed its prefix words (split /
+  // super counts) before it counts itself done, and nothing the last block
+  // reads is written by this kernel, so no fence over the index stores below
+  // (a __threadfence there held each block until its stores were acknowledged)
   if (tid == 0) last = atomicAdd(&a.ws->done_counter, 1ull) == (unsigned long long)gridDim.x - 1ull;
   __syncthreads();
+  if (a.admitted_idx) {
+    int32_t* dst = a.admitted_idx + (base & kCnt31);
+    for (int i = tid; i < tot_s; i += THREADS) __stcs(dst + i, out[i]);
+  }
   if (!last) return;
   __threadfence();
   const int nsup = ((nb_decide - 1) >> a.super_shift) + 1;
